@@ -1,0 +1,409 @@
+#!/usr/bin/env python3
+"""SSQA replica-lattice benchmark (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3]
+                    [--impl ours|reference] [--engine auto|simt|tcgen05]
+
+A *step* is one full batched annealing run of the configured workload --
+init_lattice + run_lattice for every trial, sc sweeps each -- i.e. one pass of
+the hot path (annealer.cpp:313-361) over one batch, with the reference's
+fixed-budget bench semantics (stop_at_target = false, bench.cpp:336).
+Default workload is BASELINE config 3 (the metric's config): GI n=50 ->
+N=2500 spins, M=20 replicas, 1024 trials, 5000 sweeps, 99 % TTS.
+
+value : replica-spin updates/s = N*M*T*sc / step time, device-timed with CUDA
+        events on the engine's stream, inputs resident in HBM, max over ranks.
+e2e   : same metric through the public C-ABI call ssqa_run_batch with HOST
+        buffers (quantize + upload of the model, seeds and schedule, the run,
+        download of per-trial results and best states) inside the timed region.
+--impl reference : the reference's own C++ run_trials (oracle/_ref, built from
+        /root/reference by oracle/Makefile) on the host cores, rank 0 only.
+
+Multi-GPU (torchrun): trials are split into contiguous blocks, one per rank,
+no data-path collective; total work fixed ("strong").
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "replica-spin updates/sec at N=2500, M=20, batched trials; 99% time-to-solution"
+UNIT = "replica-spin updates/s"
+
+# BASELINE.json configs; sc in sweeps.
+CONFIGS = {
+    "c1": dict(kind="gi", n_nodes=10, R=20, T=100, sc=1000,
+               desc="C1: GI n=10 -> N=100, M=20, 100 trials, 1000 sweeps"),
+    "c2": dict(kind="gi", n_nodes=20, R=20, T=1024, sc=2000,
+               desc="C2: GI n=20 -> N=400, M=20, 1024 trials, 2000 sweeps"),
+    "c3": dict(kind="gi", n_nodes=50, R=20, T=1024, sc=5000,
+               desc="C3: GI n=50 -> N=2500, M=20, 1024 trials, 5000 sweeps, TTS99"),
+    "c4": dict(kind="dense", n=8192, dense_kind=0, R=32, T=256, sc=2000,
+               desc="C4: dense int[-8,7] N=8192, M=32, 256 trials, 2000 sweeps"),
+    "c5": dict(kind="dense", n=32768, dense_kind=1, R=16, T=64, sc=1000,
+               desc="C5: SK +-1 N=32768, M=16, 64 trials, 1000 sweeps"),
+}
+GI_SEED, EDGE_P, C12, BASE_SEED = 7, 0.5, 1.0, 1000
+
+
+def build_model(cfg):
+    import paper_2302_12454_b200 as sq
+    if cfg["kind"] == "gi":
+        return sq.gi_ising(cfg["n_nodes"], EDGE_P, GI_SEED, True, C12, C12)
+    return sq.dense_ising(cfg["n"], cfg["dense_kind"], GI_SEED)
+
+
+def n_spins(cfg):
+    return cfg["n_nodes"] ** 2 if cfg["kind"] == "gi" else cfg["n"]
+
+
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled DURING the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.rows, self.proc = index, [], None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if not self.proc:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        rows = [r for r in self.rows if len(r) >= 8]
+        if not rows:
+            return None
+
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return None
+        sm = [num(r[0]) for r in rows if num(r[0])]
+        smax = max([num(r[1]) for r in rows if num(r[1])] or [0])
+        load = [s for s in sm if s >= 0.5 * smax] or sm
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[4 + i] == "Active"})
+        return {"sm_mhz": statistics.median(load) if load else None, "sm_max_mhz": smax,
+                "reasons": reasons, "samples": len(rows),
+                "power_w_max": max([num(r[2]) for r in rows if num(r[2])] or [0])}
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        d = json.load(open(path))
+        return d.get("hbm_gbs", 6650.0), d.get("bf16_tflops", 1590.0), "measured"
+    return 6650.0, 1590.0, "fallback"
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+# ---------------------------------------------------------------------------
+def reference_sample(cfg, workers, target_s):
+    """Time the reference's run_trials (oracle/_ref) on a bounded sample of
+    the workload: `workers` trials (one per thread) x S sweeps, S calibrated
+    so the sample takes about target_s seconds.  Per-sweep cost is
+    data-independent, so updates/s extrapolates linearly."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle_py
+    if not oracle_py.available("ref"):
+        o = oracle_py.Oracle("orc")
+        kind = "port"
+    else:
+        o = oracle_py.Oracle("ref")
+        kind = "reference"
+    R = cfg["R"]
+    N = n_spins(cfg)
+    if kind == "reference" and cfg["kind"] == "gi":
+        h, J, off = o.gi_ising(cfg["n_nodes"], EDGE_P, GI_SEED, True, C12, C12)
+
+        class _M:  # the reference's own instance
+            pass
+        m = _M()
+        m.h, m.J, m.offset = h, J, off
+    else:
+        m = build_model(cfg)
+    # calibrate single-thread cost per sweep
+    p_cal = oracle_py.params(R, 4)
+    t0 = time.perf_counter()
+    o.ssqa_run(m.h, m.J, m.offset, p_cal, 1, None, False, False)
+    per_sweep = max((time.perf_counter() - t0) / 5.0, 1e-6)
+    S = int(max(4, min(cfg["sc"], target_s / per_sweep)))
+    T = workers
+    if kind == "reference" and cfg["kind"] == "gi":
+        t_inst0 = time.perf_counter()
+        o.gi_ising(cfg["n_nodes"], EDGE_P, GI_SEED, True, C12, C12)
+        t_inst = time.perf_counter() - t_inst0
+        t0 = time.perf_counter()
+        o.run_trials(oracle_py.params(R, 1), n_nodes=cfg["n_nodes"], trials=T, ec=R * S,
+                     base_seed=BASE_SEED, workers=workers, gi_seed=GI_SEED)
+        wall = time.perf_counter() - t0 - t_inst
+        sample = (f"reference run_trials: {T} trials x {S} sweeps on {workers} threads "
+                  f"(of the {cfg['sc']}-sweep, {cfg['T']}-trial workload)")
+    else:
+        # dense configs (or no reference build): one ssqa_run per thread
+        import concurrent.futures as cf
+        p = oracle_py.params(R, S)
+        t0 = time.perf_counter()
+        with cf.ThreadPoolExecutor(workers) as ex:
+            list(ex.map(lambda s: o.ssqa_run(m.h, m.J, m.offset, p, BASE_SEED + s, None, False,
+                                             False), range(T)))
+        wall = time.perf_counter() - t0
+        sample = (f"{kind} ssqa_run: {T} trials x {S} sweeps on {workers} threads")
+    upd = float(N) * R * T * S
+    return dict(value=upd / wall, unit=UNIT, cores=workers, kind=kind, sample=sample,
+                cpu=cpu_model(), seconds=wall)
+
+
+def run_reference_arm(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    workers = os.cpu_count() or 1
+    per_step = max(2.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
+    vals = []
+    for i in range(args.warmup + args.steps):
+        s = reference_sample(cfg, workers, per_step)
+        if i >= args.warmup:
+            vals.append(s)
+    v = statistics.median(x["value"] for x in vals)
+    last = vals[-1]
+    N = n_spins(cfg)
+    ms = 1e3 * float(N) * cfg["R"] * cfg["T"] * cfg["sc"] / v
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (reference GI generator, instance seed 7)",
+        "config": {"workload": cfg["desc"], "n": N, "replicas": cfg["R"],
+                   "trials": cfg["T"], "sweeps": cfg["sc"]},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": last["cores"], "kind": last["kind"],
+                         "sample": last["sample"] + "; ms_per_step extrapolated to the full "
+                         "workload", "cpu": last["cpu"]},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+def run_ours(args, cfg):
+    import numpy as np
+    import torch
+
+    import paper_2302_12454_b200 as sq
+    from paper_2302_12454_b200 import _lib
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if not dist:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    R, T, sc = cfg["R"], cfg["T"], cfg["sc"]
+    N = n_spins(cfg)
+    # contiguous trial blocks per rank, seeds base + global trial index
+    lo = rank * T // world
+    hi = (rank + 1) * T // world
+    seeds = [BASE_SEED + t for t in range(lo, hi)]
+    engine = {"auto": _lib.ENGINE_AUTO, "simt": _lib.ENGINE_SIMT,
+              "tcgen05": _lib.ENGINE_TCGEN05}[args.engine]
+    m = build_model(cfg)
+    p = sq.SsqaParams(r=R, sc=sc)
+    prob = sq.Problem(m, local)
+    info = prob.info()
+    b = sq.Batch(prob, p, len(seeds), False, engine)
+    b.set_seeds(seeds)
+    eng_name = _lib.ENGINE_NAMES.get(b.engine, str(b.engine))
+
+    # ---- device-resident timing (value) ----
+    for _ in range(args.warmup):
+        b.launch(0.0 if cfg["kind"] == "gi" else None, False)
+        b.elapsed_ms()
+    clocks = ClockSampler(local)
+    barrier()
+    clocks.start()
+    times, launches = [], 0
+    for _ in range(args.steps):
+        barrier()
+        b.launch(0.0 if cfg["kind"] == "gi" else None, False)
+        times.append(b.elapsed_ms())
+        launches += b.launch_count()
+    barrier()
+    clk = clocks.stop()
+    res, best, _ = b.fetch(True, False)
+    reached = [bool(res[t].reached_target) for t in range(len(seeds))]
+    step_ms = max_over_ranks(statistics.mean(times))
+    upd_per_step = float(N) * R * T * sc
+    value = upd_per_step / (step_ms * 1e-3)
+
+    # ---- dominant kernel, live CUDA-event timing on the engine's stream ----
+    bf16_peak, hbm_peak, peak_kind = None, None, None
+    hbm_peak, bf16_peak, peak_kind = peaks()
+    int8_peak = 2.0 * bf16_peak  # TOPS: int8 dense = 2x bf16 dense on B200
+    cols = R * len(seeds)
+    ops_per_launch = 2.0 * N * N * cols  # unpadded algorithmic int8 MACs x 2
+    if b.engine == _lib.ENGINE_SIMT:
+        kname = "k_field_simt"
+        k_ms = b.profile_field(10)
+        ops = ops_per_launch
+    else:
+        kname = "k_sweep_tc (fused, persistent)"
+        k_ms = statistics.mean(times)
+        ops = ops_per_launch * (sc + 1)
+    achieved = ops / (k_ms * 1e-3) / 1e12
+    traffic = None
+    tfile = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tfile):
+        traffic = json.load(open(tfile)).get(f"{cfg_name(args)}:{eng_name}")
+    roofline = {"bound": "tensor", "achieved": achieved, "peak": int8_peak, "unit": "TOPS",
+                "frac": achieved / int8_peak, "traffic": traffic, "kernel": kname,
+                "kernel_ms": k_ms,
+                "peak_note": f"int8 dense = 2 x {peak_kind} bf16 dense ({bf16_peak} TF/s, "
+                             "MEASURED_PEAKS.json)"}
+
+    # ---- e2e through the public C-ABI call with host buffers ----
+    e2e_times = []
+    for i in range(args.warmup + args.steps):
+        barrier()
+        t0 = time.perf_counter()
+        out = sq.ssqa_run_batch(m, p, seeds, 0.0 if cfg["kind"] == "gi" else None,
+                                sq.RunOptions(False, False), engine, local)
+        dt = time.perf_counter() - t0
+        if i >= args.warmup:
+            e2e_times.append(dt)
+        if i == 0:
+            assert [o.best_energy for o in out] == [res[t].best_energy for t in range(len(seeds))]
+    e2e_s = max_over_ranks(statistics.mean(e2e_times))
+    npad = info["n_pad"]
+    h2d = npad * npad + 4 * npad + 8 * len(seeds) + 8 * (sc + 1)
+    d2h = len(seeds) * (8 + 4 + 4 + 8 + 8 + 8) + len(seeds) * N
+
+    # ---- TTS99 (amortised and reference-formula) ----
+    hits = sum(reached)
+    if dist:
+        t = torch.tensor([hits], dtype=torch.int64, device="cuda")
+        dist.all_reduce(t)
+        hits = int(t.item())
+    p_s = hits / T
+    t_trial = step_ms * 1e-3 / T * world  # device time per trial on one GPU
+    tts = sq.compute_tts(p_s, t_trial) if cfg["kind"] == "gi" else None
+
+    if rank == 0:
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            try:
+                cpu = reference_sample(cfg, os.cpu_count() or 1, args.cpu_seconds)
+            except Exception as e:  # reported, never fatal to the GPU number
+                cpu = {"error": str(e)}
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "int8 contraction (int32 acc) + f64 update",
+            "data": "synthetic (reference GI generator, instance seed 7; seeds 1000+t)"
+                    if cfg["kind"] == "gi" else "synthetic (CounterRng stream 8/9, seed 7)",
+            "config": {"workload": cfg["desc"], "n": N, "n_pad": npad, "replicas": R,
+                       "trials": T, "sweeps": sc, "engine": eng_name,
+                       "parallelism": f"trial-sharded x{world}",
+                       "l2": "no flush needed: per-step state (acc f64 "
+                             f"{8 * N * R * T / 2**20:.0f} MiB + spins) exceeds L2"
+                             if 8 * N * R * T > 126 * 2**20 else "state fits L2 (small config)"},
+            "roofline": roofline,
+            "e2e": {"value": upd_per_step / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h, "seconds_per_step": e2e_s},
+            "gpu_launches": launches,
+            "clocks": clk,
+            "tts": {"p_s": p_s, "hits": hits, "trials": T, "t_trial_s": t_trial,
+                    "tts99_s": None if tts is None else
+                    (tts.seconds if tts.kind == "finite" else tts.kind),
+                    "definition": "amortised: batch device time / trials per GPU"},
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    b.close()
+    prob.close()
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+def cfg_name(args):
+    return args.config
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--engine", default="auto", choices=["auto", "simt", "tcgen05"])
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        return run_reference_arm(args, cfg)
+    return run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,167 @@
+/*
+ * ssqa_cuda.h -- C ABI of the B200 SSQA engine (libssqa_b200.so).
+ *
+ * This is the drop-in boundary for the reference's annealing loop
+ * (/root/reference/proj).  The reference has no FFI of its own: its hot
+ * path is the C++ call chain ssqa_run -> run_lattice -> compute_fields /
+ * energies_from_fields / update_spins (src/annealer.cpp:216-361, 474-487)
+ * and its batched caller run_trials (src/bench.cpp:359-432).  Each entry
+ * point below names the reference interface it replaces.  The C++ facade in
+ * include/ssqa/*.hpp (same names as the reference headers) is built on top
+ * of these entry points; INTEGRATION.md shows the binding a maintainer adds.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only; all pointers are HOST pointers unless a
+ *    name says otherwise.  No exceptions cross the ABI.
+ *  - Every function returns SSQA_OK (0) or an error code; ssqa_last_error()
+ *    returns the calling thread's last message.  SSQA_EINVAL corresponds to
+ *    the reference's std::invalid_argument (annealer.cpp:25-30, 365-373),
+ *    SSQA_ERANGE to std::out_of_range, SSQA_ECUDA/SSQA_EUNSUP to failures the
+ *    reference cannot have (device errors; models the int8 engine cannot
+ *    represent exactly -- there is no CPU fallback).
+ *  - Lattice arrays use the reference ReplicaLattice layout [i*r + k]
+ *    (annealer.hpp:68-81); history is (delay+1) consecutive snapshots.
+ *  - A problem handle owns one device and one CUDA stream.  Distinct handles
+ *    may be used from distinct threads concurrently (the reference's
+ *    run_trials calls ssqa_run from W threads, bench.cpp:379-407).
+ */
+#ifndef SSQA_CUDA_H
+#define SSQA_CUDA_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SSQA_OK 0
+#define SSQA_EINVAL 1  /* std::invalid_argument in the reference */
+#define SSQA_ERANGE 2  /* std::out_of_range in the reference */
+#define SSQA_ECUDA 3   /* CUDA runtime / launch failure */
+#define SSQA_EUNSUP 4  /* model not exactly representable by the int8 engine */
+
+typedef struct ssqa_problem_s* ssqa_problem;
+typedef struct ssqa_batch_s* ssqa_batch;
+
+/* Mirrors ssqa::SsqaParams (annealer.hpp:14-30), field for field. */
+typedef struct {
+  int r;
+  double jperp_min;
+  double jperp_max;
+  int beta;
+  int tau;
+  int delay;
+  double i0;
+  double n_rnd;
+  double alpha;
+  long sc;
+  int bidirectional;
+} ssqa_params_c;
+
+/* Scalar fields of ssqa::AnnealResult (annealer.hpp:102-111).  wall_seconds
+ * of a batched run is the batch's device time divided by the trial count. */
+typedef struct {
+  double best_energy;
+  int best_replica;
+  int reached_target;
+  long first_hit_cycle;
+  long cycles_used;
+  double wall_seconds;
+} ssqa_result_c;
+
+/* Engine selection for ssqa_batch_create (SSQA_ENGINE_AUTO picks the
+ * tcgen05 kernel whenever the shape allows it). */
+#define SSQA_ENGINE_AUTO 0
+#define SSQA_ENGINE_SIMT 1    /* CUDA-core int8 field + fused epilogue */
+#define SSQA_ENGINE_TCGEN05 2 /* fused tcgen05/TMEM/TMA sweep kernel */
+
+const char* ssqa_last_error(void);
+const char* ssqa_version(void);
+
+/* ---- Problem: replaces DenseProblem (annealer.cpp:40-89) -------------------
+ * h[n], J[n*n] (dense, mirrored, zero diagonal: IsingModel storage,
+ * model.hpp:59-66) and offset are quantized once to int8 J' = J*2^p and
+ * int32 H' = h*2^p with the smallest p >= 0 that makes both integral, then
+ * uploaded to `device`.  Returns SSQA_EUNSUP if no such p keeps |J'| <= 127.
+ * The device copy is shared by every batch created on the handle. */
+int ssqa_problem_create(int n, const double* h, const double* J, double offset, int device,
+                        ssqa_problem* out);
+int ssqa_problem_destroy(ssqa_problem prob);
+/* Quantizer report: padded size, scale exponent p, max |J'|, max |H'|. */
+int ssqa_problem_info(ssqa_problem prob, int* n, int* n_pad, int* shift_p, int* max_abs_j,
+                      int* max_abs_h);
+
+/* Host-only dry run of the quantizer (no device touched): the scale and
+ * ranges ssqa_problem_create would use, or SSQA_EUNSUP with the reason. */
+int ssqa_quantize_info(int n, const double* h, const double* J, int* n_pad, int* shift_p,
+                       int* max_abs_j, int* max_abs_h);
+
+/* ---- Validation: SsqaParams::validate (annealer.cpp:365-373) ---------- */
+int ssqa_params_validate(const ssqa_params_c* p, int n);
+/* jperp_schedule (annealer.cpp:375-380); SSQA_EINVAL for cycle < 0. */
+int ssqa_jperp_schedule(long cycle, const ssqa_params_c* p, double* out);
+
+/* ---- One-shot runs: ssqa_run (annealer.cpp:474-487) over a batch of seeds.
+ * Trial t runs ssqa_run(model, p, seeds[t], target, {record_trace,
+ * stop_at_target}) exactly; results[t] gets the AnnealResult scalars,
+ * best_states[t*n..] (int8 +-1, may be NULL) the best state and
+ * trace[t*(sc+1)*r ..] (may be NULL unless record_trace) the TracePoint
+ * energies in the reference order (cycle-major, replica-minor; entries past
+ * a trial's cycles_used stay untouched). */
+int ssqa_run_batch(ssqa_problem prob, const ssqa_params_c* p, const uint64_t* seeds,
+                   int trials, int has_target, double target, int record_trace,
+                   int stop_at_target, int engine, ssqa_result_c* results,
+                   int8_t* best_states, double* trace);
+
+/* ---- Batches: device-resident state for `trials` x p->r replica columns.
+ * Replaces the per-trial ReplicaLattice of run_lattice (annealer.cpp:319-321);
+ * run_trials' thread pool (bench.cpp:399-407) becomes the batch. */
+int ssqa_batch_create(ssqa_problem prob, const ssqa_params_c* p, int trials, int record_trace,
+                      int engine, ssqa_batch* out);
+int ssqa_batch_destroy(ssqa_batch b);
+/* CUDA stream (cudaStream_t) the batch enqueues on; for event timing. */
+void* ssqa_batch_stream(ssqa_batch b);
+/* Engine the batch resolved to (SSQA_ENGINE_SIMT / SSQA_ENGINE_TCGEN05). */
+int ssqa_batch_engine(ssqa_batch b);
+/* Upload per-trial seeds (host array of `trials`). */
+int ssqa_batch_set_seeds(ssqa_batch b, const uint64_t* seeds);
+/* Asynchronous full run on the batch stream: init_lattice + run_lattice
+ * for every trial (annealer.cpp:313-361).  No host synchronisation. */
+int ssqa_batch_launch(ssqa_batch b, int has_target, double target, int stop_at_target);
+/* Wait for the batch stream and copy results back (as ssqa_run_batch). */
+int ssqa_batch_fetch(ssqa_batch b, ssqa_result_c* results, int8_t* best_states,
+                     double* trace);
+/* Number of kernel launches the last ssqa_batch_launch enqueued. */
+long ssqa_batch_launch_count(ssqa_batch b);
+/* Device time of the last ssqa_batch_launch (CUDA events recorded on the
+ * batch stream around everything the launch enqueued); waits for it. */
+int ssqa_batch_elapsed_ms(ssqa_batch b, double* ms);
+/* Measurement hook: time `iters` back-to-back launches of the engine's field
+ * contraction on the current state (CUDA events on the batch stream) and
+ * return the mean duration of one launch.  State is not modified. */
+int ssqa_batch_profile_field(ssqa_batch b, int iters, double* ms_per_launch);
+
+/* ---- Per-step API: init_lattice / ssqa_sweep / replica_energies
+ * (annealer.cpp:432-472), applied to every trial of the batch. ---------- */
+/* init_lattice(n, r, delay, seeds[t]) for each trial; lattice cycle = 0. */
+int ssqa_batch_init(ssqa_batch b);
+/* `count` consecutive ssqa_sweep calls with the batch's own jperp schedule
+ * (jperp_schedule(cycle, p), i0 = p->i0), starting at the lattice cycle. */
+int ssqa_batch_sweep(ssqa_batch b, long count);
+/* One ssqa_sweep with an explicit coupling strength and bound, as the
+ * reference per-step API allows (annealer.hpp:89-90, test_annealer.cpp:343-347). */
+int ssqa_batch_sweep_with(ssqa_batch b, double jperp, double i0);
+/* replica_energies of every trial's current state: out[t*r + k]. */
+int ssqa_batch_energies(ssqa_batch b, double* out);
+/* Read / write one trial's lattice in the reference layout.  hist holds
+ * (delay+1)*n*r doubles; cycle is ReplicaLattice::cycle. */
+int ssqa_batch_read_lattice(ssqa_batch b, int trial, double* sigma, double* acc, double* hist,
+                            long* cycle);
+int ssqa_batch_write_lattice(ssqa_batch b, int trial, const double* sigma, const double* acc,
+                             const double* hist, long cycle);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SSQA_CUDA_H */

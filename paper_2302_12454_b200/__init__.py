@@ -1,0 +1,17 @@
+"""B200-native SSQA engine (drop-in for the reference's annealing loop).
+
+The product is libssqa_b200.so (CUDA kernels for sm_100a behind the C ABI
+of include/ssqa_cuda.h, plus the C++ facade of include/ssqa/*.hpp).  This
+package is the Python view of the same ABI.
+"""
+from .api import (  # noqa: F401
+    AnnealResult, Batch, IsingModel, K_TARGET_TOL, Problem, ReplicaLattice, RunOptions,
+    SsqaParams, TracePoint, TrialOutcome, TtsValue, compute_tts, dense_ising, gi_ising,
+    init_lattice, ising_energy, jperp_schedule, replica_energies, run_trials, ssqa_run,
+    ssqa_run_batch, ssqa_sweep,
+)
+from ._lib import (  # noqa: F401
+    ENGINE_AUTO, ENGINE_SIMT, ENGINE_TCGEN05, SsqaError, SsqaInvalidArgument, lib,
+)
+
+__version__ = "0.1.0"

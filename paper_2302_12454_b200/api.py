@@ -1,0 +1,415 @@
+"""Python mirror of the reference annealer API, served by the B200 engine.
+
+Names, argument meaning and error behaviour follow the reference C++ API
+(proj/include/ssqa/annealer.hpp, bench.hpp): ``SsqaParams``, ``RunOptions``,
+``AnnealResult``, ``ReplicaLattice``, ``init_lattice``, ``ssqa_sweep``,
+``replica_energies``, ``jperp_schedule``, ``ssqa_run`` and ``run_trials``.
+std::invalid_argument surfaces as ``ValueError`` (``SsqaInvalidArgument``).
+Everything runs through the C ABI of include/ssqa_cuda.h; there is no Python
+or CPU compute path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+from . import _lib
+from ._lib import ENGINE_AUTO, ParamsC, ResultC, check, lib
+
+K_TARGET_TOL = 1e-9  # annealer.hpp:113
+
+
+def _dp(a: np.ndarray):
+    return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+@dataclass
+class SsqaParams:
+    """ssqa::SsqaParams (annealer.hpp:14-30); r and sc come from the caller."""
+    r: int = 0
+    jperp_min: float = 0.0
+    jperp_max: float = 0.5
+    beta: int = 3
+    tau: int = 100
+    delay: int = 1
+    i0: float = 2.0
+    n_rnd: float = 1.0
+    alpha: float = 1.0
+    sc: int = 0
+    bidirectional: bool = False
+
+    def cycles_per_iteration(self) -> int:
+        return self.tau * (self.beta + 1)
+
+    def iterations(self) -> int:
+        return self.sc // self.cycles_per_iteration()
+
+    def to_c(self) -> ParamsC:
+        return ParamsC(self.r, self.jperp_min, self.jperp_max, self.beta, self.tau, self.delay,
+                       self.i0, self.n_rnd, self.alpha, self.sc, int(self.bidirectional))
+
+    def validate(self, n: int) -> None:
+        check(lib().ssqa_params_validate(C.byref(self.to_c()), n))
+
+
+@dataclass
+class RunOptions:
+    record_trace: bool = False
+    stop_at_target: bool = True
+
+
+@dataclass
+class TracePoint:
+    cycle: int
+    replica: int
+    energy: float
+    jperp: float
+
+
+@dataclass
+class AnnealResult:
+    best_energy: float = 0.0
+    best_state: np.ndarray = field(default_factory=lambda: np.zeros(0, np.int8))
+    best_replica: int = 0
+    reached_target: bool = False
+    first_hit_cycle: int = -1
+    cycles_used: int = 0
+    trace_energy: np.ndarray = field(default_factory=lambda: np.zeros(0))
+    wall_seconds: float = 0.0
+
+    @property
+    def trace(self) -> List[TracePoint]:
+        """TracePoint list in the reference order (cycle-major, replica-minor)."""
+        raise NotImplementedError("use trace_energy (+ jperp_schedule) for bulk traces")
+
+
+class IsingModel:
+    """Dense mirrored Ising model, ssqa::IsingModel storage (model.hpp:45-67)."""
+
+    def __init__(self, n: int, offset: float = 0.0):
+        if n < 1:
+            raise ValueError("IsingModel needs n >= 1")
+        self.h = np.zeros(n)
+        self.J = np.zeros((n, n))
+        self.offset = float(offset)
+
+    @property
+    def n(self) -> int:
+        return len(self.h)
+
+    @classmethod
+    def from_arrays(cls, h, J, offset=0.0) -> "IsingModel":
+        m = cls(len(h), offset)
+        m.h = np.ascontiguousarray(h, dtype=np.float64).copy()
+        m.J = np.ascontiguousarray(J, dtype=np.float64).copy()
+        return m
+
+    def set_bias(self, i, v):
+        self.h[i] = v
+
+    def set_coupling(self, i, j, v):
+        if i == j:
+            raise ValueError("coupling needs i != j")
+        self.J[i, j] = v
+        self.J[j, i] = v
+
+
+def gi_ising(n_nodes: int, edge_prob: float = 0.5, seed: int = 0, permute: bool = True,
+             c1: float = 0.75, c2: float = 0.75) -> IsingModel:
+    """qubo_to_ising(build_gi_qubo(generate_gi(...))) -- gi.cpp:102-184."""
+    n = n_nodes * n_nodes
+    h = np.zeros(n)
+    J = np.zeros((n, n))
+    off = C.c_double()
+    check(lib().ssqa_gi_ising(n_nodes, edge_prob, seed, int(permute), c1, c2, _dp(h), _dp(J),
+                              C.byref(off)), host=True)
+    return IsingModel.from_arrays(h, J, off.value)
+
+
+def dense_ising(n: int, kind: int, seed: int) -> IsingModel:
+    """BASELINE configs C4 (kind 0, int[-8,7]) / C5 (kind 1, SK +-1)."""
+    h = np.zeros(n)
+    J = np.zeros((n, n))
+    off = C.c_double()
+    check(lib().ssqa_dense_ising(n, kind, seed, _dp(h), _dp(J), C.byref(off)), host=True)
+    return IsingModel.from_arrays(h, J, off.value)
+
+
+def ising_energy(m: IsingModel, spins) -> float:
+    s = np.ascontiguousarray(spins, dtype=np.int8)
+    out = C.c_double()
+    check(lib().ssqa_ising_energy(m.n, _dp(m.h), _dp(m.J), m.offset,
+                                  s.ctypes.data_as(C.POINTER(C.c_int8)), C.byref(out)), host=True)
+    return out.value
+
+
+def jperp_schedule(cycle: int, p: SsqaParams) -> float:
+    out = C.c_double()
+    check(lib().ssqa_jperp_schedule(cycle, C.byref(p.to_c()), C.byref(out)))
+    return out.value
+
+
+class Problem:
+    """Quantized model on one device (ssqa_problem_create)."""
+
+    def __init__(self, m: IsingModel, device: int = 0):
+        self.n = m.n
+        self._h = C.c_void_p()
+        check(lib().ssqa_problem_create(m.n, _dp(np.ascontiguousarray(m.h)),
+                                        _dp(np.ascontiguousarray(m.J)), m.offset, device,
+                                        C.byref(self._h)))
+
+    def info(self) -> dict:
+        v = [C.c_int() for _ in range(5)]
+        check(lib().ssqa_problem_info(self._h, *[C.byref(x) for x in v]))
+        return dict(zip(("n", "n_pad", "shift_p", "max_abs_j", "max_abs_h"), [x.value for x in v]))
+
+    def close(self):
+        if self._h:
+            lib().ssqa_problem_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Batch:
+    """Device-resident state for `trials` x p.r replica columns (ssqa_batch_*)."""
+
+    def __init__(self, prob: Problem, p: SsqaParams, trials: int, record_trace: bool = False,
+                 engine: int = ENGINE_AUTO):
+        self.prob, self.p, self.trials, self.record_trace = prob, p, trials, record_trace
+        self._b = C.c_void_p()
+        check(lib().ssqa_batch_create(prob._h, C.byref(p.to_c()), trials, int(record_trace),
+                                      engine, C.byref(self._b)))
+
+    @property
+    def engine(self) -> int:
+        return lib().ssqa_batch_engine(self._b)
+
+    @property
+    def stream(self) -> int:
+        return lib().ssqa_batch_stream(self._b) or 0
+
+    def set_seeds(self, seeds: Sequence[int]):
+        s = np.ascontiguousarray(np.asarray(seeds, dtype=np.uint64))
+        assert len(s) == self.trials
+        check(lib().ssqa_batch_set_seeds(self._b, s.ctypes.data_as(C.POINTER(C.c_uint64))))
+
+    def launch(self, target: Optional[float] = None, stop_at_target: bool = True):
+        check(lib().ssqa_batch_launch(self._b, int(target is not None),
+                                      0.0 if target is None else float(target),
+                                      int(stop_at_target)))
+
+    def launch_count(self) -> int:
+        return lib().ssqa_batch_launch_count(self._b)
+
+    def elapsed_ms(self) -> float:
+        out = C.c_double()
+        check(lib().ssqa_batch_elapsed_ms(self._b, C.byref(out)))
+        return out.value
+
+    def profile_field(self, iters: int = 20) -> float:
+        out = C.c_double()
+        check(lib().ssqa_batch_profile_field(self._b, iters, C.byref(out)))
+        return out.value
+
+    def fetch(self, best_states: bool = True, trace: bool = False):
+        T, n = self.trials, self.prob.n
+        res = (ResultC * T)()
+        best = np.zeros((T, n), np.int8) if best_states else None
+        tr = np.zeros((T, self.p.sc + 1, self.p.r)) if trace else None
+        check(lib().ssqa_batch_fetch(
+            self._b, res, best.ctypes.data_as(C.POINTER(C.c_int8)) if best is not None else None,
+            _dp(tr) if tr is not None else None))
+        return res, best, tr
+
+    # per-step API
+    def init(self):
+        check(lib().ssqa_batch_init(self._b))
+
+    def sweep(self, count: int = 1):
+        check(lib().ssqa_batch_sweep(self._b, count))
+
+    def sweep_with(self, jperp: float, i0: float):
+        check(lib().ssqa_batch_sweep_with(self._b, jperp, i0))
+
+    def energies(self) -> np.ndarray:
+        out = np.zeros((self.trials, self.p.r))
+        check(lib().ssqa_batch_energies(self._b, _dp(out)))
+        return out
+
+    def read_lattice(self, trial: int):
+        n, r, d = self.prob.n, self.p.r, self.p.delay
+        sigma, acc, hist = np.zeros(n * r), np.zeros(n * r), np.zeros((d + 1) * n * r)
+        cyc = C.c_long()
+        check(lib().ssqa_batch_read_lattice(self._b, trial, _dp(sigma), _dp(acc), _dp(hist),
+                                            C.byref(cyc)))
+        return sigma, acc, hist.reshape(d + 1, n * r), cyc.value
+
+    def write_lattice(self, trial: int, sigma, acc, hist, cycle: int):
+        s = np.ascontiguousarray(sigma, dtype=np.float64)
+        a = np.ascontiguousarray(acc, dtype=np.float64)
+        h = np.ascontiguousarray(hist, dtype=np.float64)
+        check(lib().ssqa_batch_write_lattice(self._b, trial, _dp(s), _dp(a), _dp(h), cycle))
+
+    def close(self):
+        if self._b:
+            lib().ssqa_batch_destroy(self._b)
+            self._b = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _results(res, best, tr, trials) -> List[AnnealResult]:
+    out = []
+    for t in range(trials):
+        r = res[t]
+        te = np.zeros(0)
+        if tr is not None:
+            te = tr[t, : r.cycles_used + 1].reshape(-1).copy()
+        out.append(AnnealResult(r.best_energy, best[t].copy() if best is not None else None,
+                                r.best_replica, bool(r.reached_target), r.first_hit_cycle,
+                                r.cycles_used, te, r.wall_seconds))
+    return out
+
+
+def ssqa_run_batch(m: IsingModel, p: SsqaParams, seeds: Sequence[int],
+                   target_energy: Optional[float] = None, opts: RunOptions = RunOptions(),
+                   engine: int = ENGINE_AUTO, device: int = 0,
+                   problem: Optional[Problem] = None) -> List[AnnealResult]:
+    """ssqa_run for every seed, as one device batch."""
+    p.validate(m.n)
+    prob = problem or Problem(m, device)
+    b = Batch(prob, p, len(seeds), opts.record_trace, engine)
+    try:
+        b.set_seeds(seeds)
+        b.launch(target_energy, opts.stop_at_target)
+        res, best, tr = b.fetch(True, opts.record_trace)
+        return _results(res, best, tr, len(seeds))
+    finally:
+        b.close()
+
+
+def ssqa_run(m: IsingModel, p: SsqaParams, seed: int, target_energy: Optional[float] = None,
+             opts: RunOptions = RunOptions(), engine: int = ENGINE_AUTO) -> AnnealResult:
+    """annealer.cpp:474-487."""
+    return ssqa_run_batch(m, p, [seed], target_energy, opts, engine)[0]
+
+
+@dataclass
+class ReplicaLattice:
+    """ssqa::ReplicaLattice (annealer.hpp:68-81), layout [i*replicas + k]."""
+    n: int
+    replicas: int
+    delay: int
+    cycle: int
+    sigma: np.ndarray
+    is_acc: np.ndarray
+    history: np.ndarray  # (delay+1, n*replicas)
+
+    def spin(self, i, k):
+        return self.sigma[i * self.replicas + k]
+
+    def acc(self, i, k):
+        return self.is_acc[i * self.replicas + k]
+
+    def delayed_sigma(self):
+        return self.history[self.cycle % (self.delay + 1)]
+
+
+def init_lattice(n: int, replicas: int, delay: int, seed: int,
+                 engine: int = ENGINE_AUTO) -> ReplicaLattice:
+    """annealer.cpp:432-447, evaluated by the device init kernel."""
+    prob = Problem(IsingModel(n))
+    p = SsqaParams(r=replicas, delay=delay, sc=1)
+    b = Batch(prob, p, 1, engine=engine)
+    b.set_seeds([seed])
+    b.init()
+    s, a, h, c = b.read_lattice(0)
+    return ReplicaLattice(n, replicas, delay, c, s, a, h)
+
+
+def ssqa_sweep(lat: ReplicaLattice, m: IsingModel, jperp: float, p: SsqaParams, seed: int,
+               cycle: int, engine: int = ENGINE_AUTO) -> None:
+    """annealer.cpp:449-463 (in place)."""
+    if lat.n != m.n or lat.replicas != p.r:
+        raise _lib.SsqaInvalidArgument(1, "lattice dimensions do not match model/params")
+    if cycle != lat.cycle:
+        raise _lib.SsqaInvalidArgument(1, "sweep cycle does not match lattice history")
+    q = SsqaParams(**{**p.__dict__, "sc": max(1, p.sc)})
+    b = Batch(Problem(m), q, 1, engine=engine)
+    b.set_seeds([seed])
+    b.write_lattice(0, lat.sigma, lat.is_acc, lat.history, lat.cycle)
+    b.sweep_with(jperp, p.i0)
+    s, a, h, c = b.read_lattice(0)
+    lat.sigma[:], lat.is_acc[:], lat.history[...], lat.cycle = s, a, h, c
+
+
+def replica_energies(lat: ReplicaLattice, m: IsingModel, engine: int = ENGINE_AUTO) -> np.ndarray:
+    """annealer.cpp:465-472."""
+    if lat.n != m.n:
+        raise _lib.SsqaInvalidArgument(1, "lattice does not match model")
+    p = SsqaParams(r=lat.replicas, delay=0, sc=1)
+    b = Batch(Problem(m), p, 1, engine=engine)
+    b.set_seeds([0])
+    b.write_lattice(0, lat.sigma, np.zeros_like(lat.sigma), lat.sigma[None, :], 0)
+    return b.energies()[0]
+
+
+# ---- bench.hpp: trial batteries and time-to-solution -------------------------
+
+@dataclass
+class TtsValue:
+    kind: str  # "finite" | "saturated" | "undefined"
+    seconds: float = 0.0
+
+
+def compute_tts(p_s: float, t_seconds: float, p_target: float = 0.99) -> TtsValue:
+    """bench.cpp:144-160."""
+    if not (0.0 < p_target < 1.0):
+        raise ValueError("p_target must lie in (0, 1)")
+    if not (0.0 <= p_s <= 1.0):
+        raise ValueError("p_s outside [0, 1]")
+    if t_seconds <= 0.0:
+        raise ValueError("t must be > 0")
+    if p_s == 0.0:
+        return TtsValue("undefined")
+    if p_s == 1.0:
+        return TtsValue("saturated", 0.0)
+    return TtsValue("finite", t_seconds * math.log(1.0 - p_target) / math.log(1.0 - p_s))
+
+
+@dataclass
+class TrialOutcome:
+    seed: int
+    reached_target: bool
+    first_hit_cycle: int
+    best_energy: float
+    wall_seconds: float
+
+
+def run_trials(m: IsingModel, p: SsqaParams, trials: int, ec: int, base_seed: int,
+               target: float = 0.0, p_target: float = 0.99, engine: int = ENGINE_AUTO,
+               device: int = 0):
+    """run_trials (bench.cpp:359-432) on a pinned instance: fixed budget
+    sc = ec / r, seeds base_seed + t, stop_at_target = false."""
+    q = SsqaParams(**{**p.__dict__, "sc": ec // p.r})
+    seeds = [base_seed + t for t in range(trials)]
+    res = ssqa_run_batch(m, q, seeds, target, RunOptions(False, False), engine, device)
+    outs = [TrialOutcome(s, r.reached_target, r.first_hit_cycle, r.best_energy, r.wall_seconds)
+            for s, r in zip(seeds, res)]
+    p_s = sum(o.reached_target for o in outs) / trials
+    t_mean = sum(o.wall_seconds for o in outs) / trials
+    return outs, p_s, t_mean, compute_tts(p_s, max(t_mean, 1e-12), p_target)

@@ -1,0 +1,614 @@
+// capi.cu -- the C ABI of include/ssqa_cuda.h: problem upload, batches, the
+// run loop (run_lattice, annealer.cpp:313-361) and the per-step parity API.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <string>
+#include <vector>
+
+#include "engine.h"
+#include "simt_kernels.cuh"
+#include "sweep_tc.h"
+
+using namespace ssqa_engine;
+
+namespace {
+
+thread_local std::string g_err;
+
+int set_err(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CU(call)                                                                    \
+  do {                                                                              \
+    cudaError_t e__ = (call);                                                       \
+    if (e__ != cudaSuccess)                                                         \
+      return set_err(SSQA_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e__)); \
+  } while (0)
+
+#define CHECK_LAUNCH()                                                                 \
+  do {                                                                                 \
+    cudaError_t e__ = cudaGetLastError();                                              \
+    if (e__ != cudaSuccess)                                                            \
+      return set_err(SSQA_ECUDA, std::string("kernel launch: ") + cudaGetErrorString(e__)); \
+  } while (0)
+
+constexpr long kMaxCycles = 1L << 31;  // annealer.cpp:20
+constexpr int kMaxReplicas = 1 << 12;  // annealer.cpp:21
+constexpr int kMaxSpins = 1 << 20;     // annealer.cpp:22
+constexpr double kTargetTol = 1e-9;    // annealer.hpp:113
+
+// annealer.cpp:25-30 + 365-373
+int validate(const ssqa_params_c* p, int n) {
+  if (!p) return set_err(SSQA_EINVAL, "null params");
+  if (n < 1 || n >= kMaxSpins) return set_err(SSQA_EINVAL, "spin count out of range");
+  if (p->sc < 1 || p->sc >= kMaxCycles) return set_err(SSQA_EINVAL, "sc out of range");
+  if (p->n_rnd < 0.0) return set_err(SSQA_EINVAL, "n_rnd must be >= 0");
+  if (p->alpha <= 0.0) return set_err(SSQA_EINVAL, "alpha must be > 0");
+  if (p->r < 1 || p->r >= kMaxReplicas)
+    return set_err(SSQA_EINVAL, "replica count out of range");
+  if (p->jperp_max < p->jperp_min) return set_err(SSQA_EINVAL, "jperp_max < jperp_min");
+  if (p->beta < 1) return set_err(SSQA_EINVAL, "beta must be >= 1");
+  if (p->tau < 1) return set_err(SSQA_EINVAL, "tau must be >= 1");
+  if (p->delay < 0) return set_err(SSQA_EINVAL, "delay must be >= 0");
+  if (p->i0 <= 0.0) return set_err(SSQA_EINVAL, "i0 must be > 0");
+  return SSQA_OK;
+}
+
+// annealer.cpp:375-380, evaluated on the host so the device sees the
+// reference's own doubles.
+double jperp_at(long cycle, const ssqa_params_c& p) {
+  long c = cycle % (long(p.tau) * (p.beta + 1));
+  long step = c / p.tau;
+  return p.jperp_min + double(step) * (p.jperp_max - p.jperp_min) / p.beta;
+}
+
+int num_sms(int device) {
+  int v = 148;
+  cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device);
+  return v;
+}
+
+// Column tiling: whole trials per tile, as few tiles as the SM count allows.
+Geom make_geom(int n, int npad, int R, int T, int sms, int engine) {
+  Geom g;
+  g.n = n;
+  g.npad = npad;
+  g.R = R;
+  g.T = T;
+  const int max_cols = 256;
+  int tpt = std::max(1, (T + sms - 1) / sms);
+  if (R <= max_cols) tpt = std::min(tpt, max_cols / R);
+  else tpt = 1;
+  tpt = std::max(1, std::min(tpt, T));
+  (void)engine;
+  g.tpt = tpt;
+  g.tile_cols = (tpt * R + 15) / 16 * 16;
+  g.ntiles = (T + tpt - 1) / tpt;
+  g.ccols = g.ntiles * g.tile_cols;
+  return g;
+}
+
+template <class T>
+int dalloc(T** p, size_t count) {
+  CU(cudaMalloc(reinterpret_cast<void**>(p), std::max<size_t>(count, 1) * sizeof(T)));
+  return SSQA_OK;
+}
+
+void dfree(void* p) {
+  if (p) cudaFree(p);
+}
+
+int8_t* slot_ptr(ssqa_batch_s* b, int s) { return b->d_sig + size_t(s) * b->slot_elems; }
+
+int pick_free(const ssqa_batch_s* b) {
+  for (int s = 0; s < b->nslots; ++s) {
+    if (s == b->cur) continue;
+    if (std::find(b->phys.begin(), b->phys.end(), s) != b->phys.end()) continue;
+    return s;
+  }
+  return -1;  // unreachable: nslots = delay + 3
+}
+
+// Give cur and every history snapshot its own slot so one trial's lattice
+// can be rewritten without touching the others (ssqa_batch_write_lattice).
+int normalize_slots(ssqa_batch_s* b) {
+  std::vector<int> roles;
+  roles.push_back(b->cur);
+  for (int s : b->phys) roles.push_back(s);
+  std::vector<int> sorted = roles;
+  std::sort(sorted.begin(), sorted.end());
+  if (std::adjacent_find(sorted.begin(), sorted.end()) == sorted.end()) return SSQA_OK;
+  int8_t* fresh = nullptr;
+  int rc = dalloc(&fresh, b->slot_elems * b->nslots);
+  if (rc) return rc;
+  for (size_t r = 0; r < roles.size(); ++r) {
+    CU(cudaMemcpyAsync(fresh + r * b->slot_elems, slot_ptr(b, roles[r]), b->slot_elems,
+                       cudaMemcpyDeviceToDevice, b->prob->stream));
+  }
+  CU(cudaStreamSynchronize(b->prob->stream));
+  cudaFree(b->d_sig);
+  b->d_sig = fresh;
+  b->cur = 0;
+  for (size_t s = 0; s < b->phys.size(); ++s) b->phys[s] = int(s) + 1;
+  return SSQA_OK;
+}
+
+// One SIMT sweep of the whole batch at b->cycle (update_spins semantics),
+// optionally followed by the scan.  do_update = 0 computes energies only.
+int simt_sweep(ssqa_batch_s* b, double jperp, double i0, int do_update, const ScanArgs* scan) {
+  const Geom& g = b->g;
+  cudaStream_t st = b->prob->stream;
+  launch_field_simt(g, b->prob->d_J, slot_ptr(b, b->cur), b->d_S, st);
+  CHECK_LAUNCH();
+  const int src = b->phys[size_t(b->cycle % (b->d + 1))];
+  const int dst = do_update ? pick_free(b) : b->cur;
+  StepArgs a{b->cycle, jperp, i0, b->p.n_rnd, b->p.alpha, b->p.bidirectional, do_update};
+  launch_energy_update_simt(g, b->d_S, b->prob->d_H, b->prob->q.scale, b->d_seeds,
+                            slot_ptr(b, b->cur), slot_ptr(b, src), slot_ptr(b, dst), b->d_acc,
+                            b->d_E, a, st);
+  CHECK_LAUNCH();
+  b->launches += 2;
+  if (scan) {
+    launch_scan(g, b->d_E, *scan, slot_ptr(b, b->cur), b->d_best_e, b->d_best_k, b->d_reached,
+                b->d_first_hit, b->d_cycles_used, b->d_active, b->d_best_state, b->d_trace, st);
+    CHECK_LAUNCH();
+    b->launches += 1;
+  }
+  if (do_update) {
+    b->phys[size_t(b->cycle % (b->d + 1))] = dst;
+    b->cur = dst;
+    b->cycle += 1;
+  }
+  return SSQA_OK;
+}
+
+int init_state(ssqa_batch_s* b) {
+  cudaStream_t st = b->prob->stream;
+  b->cur = 0;
+  std::fill(b->phys.begin(), b->phys.end(), 0);
+  b->cycle = 0;
+  launch_init(b->g, b->d_seeds, slot_ptr(b, 0), b->d_acc, st);
+  CHECK_LAUNCH();
+  b->launches += 1;
+  return SSQA_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ssqa_last_error(void) { return g_err.c_str(); }
+const char* ssqa_version(void) { return "ssqa-b200 0.1.0"; }
+
+int ssqa_params_validate(const ssqa_params_c* p, int n) { return validate(p, n); }
+
+int ssqa_jperp_schedule(long cycle, const ssqa_params_c* p, double* out) {
+  if (cycle < 0) return set_err(SSQA_EINVAL, "cycle must be >= 0");
+  *out = jperp_at(cycle, *p);
+  return SSQA_OK;
+}
+
+int ssqa_problem_create(int n, const double* h, const double* J, double offset, int device,
+                        ssqa_problem* out) {
+  if (!out || !h || !J) return set_err(SSQA_EINVAL, "null argument");
+  if (n < 1 || n >= kMaxSpins) return set_err(SSQA_EINVAL, "spin count out of range");
+  auto* pr = new ssqa_problem_s();
+  std::string why;
+  int rc = quantize(n, h, J, offset, &pr->q, &why);
+  if (rc) {
+    delete pr;
+    return set_err(rc, why);
+  }
+  pr->device = device;
+  cudaError_t e = cudaSetDevice(device);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&pr->stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess)
+    e = cudaMalloc(&pr->d_J, pr->q.J.size() * sizeof(int8_t));
+  if (e == cudaSuccess) e = cudaMalloc(&pr->d_H, pr->q.H.size() * sizeof(int32_t));
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(pr->d_J, pr->q.J.data(), pr->q.J.size(), cudaMemcpyHostToDevice,
+                        pr->stream);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(pr->d_H, pr->q.H.data(), pr->q.H.size() * sizeof(int32_t),
+                        cudaMemcpyHostToDevice, pr->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(pr->stream);
+  if (e != cudaSuccess) {
+    ssqa_problem_destroy(pr);
+    return set_err(SSQA_ECUDA, std::string("problem upload: ") + cudaGetErrorString(e));
+  }
+  *out = pr;
+  return SSQA_OK;
+}
+
+int ssqa_quantize_info(int n, const double* h, const double* J, int* n_pad, int* shift_p,
+                       int* max_abs_j, int* max_abs_h) {
+  if (!h || !J) return set_err(SSQA_EINVAL, "null argument");
+  if (n < 1 || n >= kMaxSpins) return set_err(SSQA_EINVAL, "spin count out of range");
+  Quantized q;
+  std::string why;
+  int rc = quantize(n, h, J, 0.0, &q, &why);
+  if (rc) return set_err(rc, why);
+  if (n_pad) *n_pad = q.npad;
+  if (shift_p) *shift_p = q.p;
+  if (max_abs_j) *max_abs_j = q.max_abs_j;
+  if (max_abs_h) *max_abs_h = q.max_abs_h;
+  return SSQA_OK;
+}
+
+int ssqa_problem_destroy(ssqa_problem pr) {
+  if (!pr) return SSQA_OK;
+  cudaSetDevice(pr->device);
+  dfree(pr->d_J);
+  dfree(pr->d_H);
+  if (pr->stream) cudaStreamDestroy(pr->stream);
+  delete pr;
+  return SSQA_OK;
+}
+
+int ssqa_problem_info(ssqa_problem pr, int* n, int* n_pad, int* shift_p, int* max_abs_j,
+                      int* max_abs_h) {
+  if (!pr) return set_err(SSQA_EINVAL, "null problem");
+  if (n) *n = pr->q.n;
+  if (n_pad) *n_pad = pr->q.npad;
+  if (shift_p) *shift_p = pr->q.p;
+  if (max_abs_j) *max_abs_j = pr->q.max_abs_j;
+  if (max_abs_h) *max_abs_h = pr->q.max_abs_h;
+  return SSQA_OK;
+}
+
+int ssqa_batch_create(ssqa_problem pr, const ssqa_params_c* p, int trials, int record_trace,
+                      int engine, ssqa_batch* out) {
+  if (!pr || !out) return set_err(SSQA_EINVAL, "null argument");
+  int rc = validate(p, pr->q.n);
+  if (rc) return rc;
+  if (trials < 1) return set_err(SSQA_EINVAL, "trials must be >= 1");
+  CU(cudaSetDevice(pr->device));
+  int eng = engine;
+  if (eng == SSQA_ENGINE_AUTO) eng = tc_supported(pr->q.npad, p->r) ? SSQA_ENGINE_TCGEN05
+                                                                    : SSQA_ENGINE_SIMT;
+  if (eng == SSQA_ENGINE_TCGEN05 && !tc_supported(pr->q.npad, p->r))
+    return set_err(SSQA_EUNSUP, "tcgen05 engine does not support this shape");
+  if (eng != SSQA_ENGINE_SIMT && eng != SSQA_ENGINE_TCGEN05)
+    return set_err(SSQA_EINVAL, "unknown engine");
+
+  auto* b = new ssqa_batch_s();
+  b->prob = pr;
+  b->p = *p;
+  b->engine = eng;
+  b->record_trace = record_trace;
+  b->d = p->delay;
+  b->nslots = p->delay + 3;
+  b->g = make_geom(pr->q.n, pr->q.npad, p->r, trials, num_sms(pr->device), eng);
+  b->slot_elems = size_t(b->g.ccols) * b->g.npad;
+  b->phys.assign(size_t(b->d) + 1, 0);
+  const int T = trials;
+  rc = SSQA_OK;
+  auto A = [&](auto** ptr, size_t count) {
+    if (rc == SSQA_OK) rc = dalloc(ptr, count);
+  };
+  A(&b->d_sig, b->slot_elems * b->nslots);
+  A(&b->d_acc, b->slot_elems);
+  A(&b->d_seeds, size_t(T));
+  A(&b->d_jperp, size_t(p->sc) + 1);
+  A(&b->d_E, size_t(b->g.ccols));
+  if (eng == SSQA_ENGINE_SIMT) A(&b->d_S, b->slot_elems);
+  A(&b->d_best_e, size_t(T));
+  A(&b->d_best_k, size_t(T));
+  A(&b->d_reached, size_t(T));
+  A(&b->d_first_hit, size_t(T));
+  A(&b->d_cycles_used, size_t(T));
+  A(&b->d_active, size_t(T));
+  A(&b->d_best_state, size_t(T) * pr->q.n);
+  if (record_trace) A(&b->d_trace, size_t(T) * (p->sc + 1) * p->r);
+  if (rc) {
+    ssqa_batch_destroy(b);
+    return rc;
+  }
+  std::vector<double> jp(size_t(p->sc) + 1);
+  for (long c = 0; c <= p->sc; ++c) jp[size_t(c)] = jperp_at(c, *p);
+  CU(cudaMemcpy(b->d_jperp, jp.data(), jp.size() * sizeof(double), cudaMemcpyHostToDevice));
+  CU(cudaMemset(b->d_sig, 0, b->slot_elems * b->nslots));
+  CU(cudaMemset(b->d_acc, 0, b->slot_elems * sizeof(double)));
+  CU(cudaEventCreate(&b->ev0));
+  CU(cudaEventCreate(&b->ev1));
+  *out = b;
+  return SSQA_OK;
+}
+
+int ssqa_batch_destroy(ssqa_batch b) {
+  if (!b) return SSQA_OK;
+  cudaSetDevice(b->prob->device);
+  cudaStreamSynchronize(b->prob->stream);
+  for (void* ptr : {(void*)b->d_sig, (void*)b->d_acc, (void*)b->d_seeds, (void*)b->d_jperp,
+                    (void*)b->d_S, (void*)b->d_E, (void*)b->d_best_e, (void*)b->d_best_k,
+                    (void*)b->d_reached, (void*)b->d_first_hit, (void*)b->d_cycles_used,
+                    (void*)b->d_active, (void*)b->d_best_state, (void*)b->d_trace})
+    dfree(ptr);
+  if (b->ev0) cudaEventDestroy(b->ev0);
+  if (b->ev1) cudaEventDestroy(b->ev1);
+  delete b;
+  return SSQA_OK;
+}
+
+void* ssqa_batch_stream(ssqa_batch b) { return b ? (void*)b->prob->stream : nullptr; }
+int ssqa_batch_engine(ssqa_batch b) { return b ? b->engine : -1; }
+long ssqa_batch_launch_count(ssqa_batch b) { return b ? b->launches : -1; }
+
+int ssqa_batch_elapsed_ms(ssqa_batch b, double* ms) {
+  if (!b || !ms) return set_err(SSQA_EINVAL, "null argument");
+  CU(cudaSetDevice(b->prob->device));
+  CU(cudaEventSynchronize(b->ev1));
+  float f = 0.f;
+  CU(cudaEventElapsedTime(&f, b->ev0, b->ev1));
+  *ms = double(f);
+  return SSQA_OK;
+}
+
+int ssqa_batch_profile_field(ssqa_batch b, int iters, double* ms_per_launch) {
+  if (!b || !ms_per_launch || iters < 1) return set_err(SSQA_EINVAL, "bad argument");
+  CU(cudaSetDevice(b->prob->device));
+  cudaStream_t st = b->prob->stream;
+  int32_t* S = b->d_S;
+  bool tmp = false;
+  if (!S) {
+    int rc = dalloc(&S, b->slot_elems);
+    if (rc) return rc;
+    tmp = true;
+  }
+  cudaEvent_t e0, e1;
+  CU(cudaEventCreate(&e0));
+  CU(cudaEventCreate(&e1));
+  CU(cudaEventRecord(e0, st));
+  for (int i = 0; i < iters; ++i) launch_field_simt(b->g, b->prob->d_J, slot_ptr(b, b->cur), S, st);
+  CHECK_LAUNCH();
+  CU(cudaEventRecord(e1, st));
+  CU(cudaEventSynchronize(e1));
+  float f = 0.f;
+  CU(cudaEventElapsedTime(&f, e0, e1));
+  *ms_per_launch = double(f) / iters;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  if (tmp) cudaFree(S);
+  return SSQA_OK;
+}
+
+int ssqa_batch_set_seeds(ssqa_batch b, const uint64_t* seeds) {
+  if (!b || !seeds) return set_err(SSQA_EINVAL, "null argument");
+  CU(cudaSetDevice(b->prob->device));
+  CU(cudaMemcpyAsync(b->d_seeds, seeds, size_t(b->g.T) * sizeof(uint64_t),
+                     cudaMemcpyHostToDevice, b->prob->stream));
+  CU(cudaStreamSynchronize(b->prob->stream));
+  b->seeds_set = true;
+  return SSQA_OK;
+}
+
+int ssqa_batch_launch(ssqa_batch b, int has_target, double target, int stop_at_target) {
+  if (!b) return set_err(SSQA_EINVAL, "null batch");
+  if (!b->seeds_set) return set_err(SSQA_EINVAL, "seeds not set");
+  CU(cudaSetDevice(b->prob->device));
+  cudaStream_t st = b->prob->stream;
+  b->launches = 0;
+  CU(cudaEventRecord(b->ev0, st));
+  launch_reset_results(b->g.T, b->p.sc, b->d_best_e, b->d_best_k, b->d_reached,
+                       b->d_first_hit, b->d_cycles_used, b->d_active, st);
+  CHECK_LAUNCH();
+  b->launches += 1;
+  int rc = init_state(b);
+  if (rc) return rc;
+  ScanArgs sa{};
+  sa.sc = b->p.sc;
+  sa.scale = b->prob->q.scale;
+  sa.offset = b->prob->q.offset;
+  sa.has_target = has_target;
+  sa.target_tol = target + kTargetTol;
+  sa.stop_at_target = stop_at_target;
+  sa.record_trace = b->record_trace;
+  if (b->engine == SSQA_ENGINE_TCGEN05) {
+    rc = tc_run(b, sa);
+    if (rc) return set_err(rc, tc_last_error());
+  } else {
+    for (long c = 0; c <= b->p.sc; ++c) {
+      sa.cycle = c;
+      const double jp = jperp_at(c, b->p);
+      rc = simt_sweep(b, jp, b->p.i0, c < b->p.sc ? 1 : 0, &sa);
+      if (rc) return rc;
+    }
+  }
+  CU(cudaEventRecord(b->ev1, st));
+  return SSQA_OK;
+}
+
+int ssqa_batch_fetch(ssqa_batch b, ssqa_result_c* results, int8_t* best_states,
+                     double* trace) {
+  if (!b) return set_err(SSQA_EINVAL, "null batch");
+  CU(cudaSetDevice(b->prob->device));
+  cudaStream_t st = b->prob->stream;
+  CU(cudaStreamSynchronize(st));
+  const int T = b->g.T;
+  float ms = 0.f;
+  CU(cudaEventElapsedTime(&ms, b->ev0, b->ev1));
+  if (results) {
+    std::vector<double> be(T);
+    std::vector<int> bk(T), re(T);
+    std::vector<long> fh(T), cu(T);
+    CU(cudaMemcpy(be.data(), b->d_best_e, T * sizeof(double), cudaMemcpyDeviceToHost));
+    CU(cudaMemcpy(bk.data(), b->d_best_k, T * sizeof(int), cudaMemcpyDeviceToHost));
+    CU(cudaMemcpy(re.data(), b->d_reached, T * sizeof(int), cudaMemcpyDeviceToHost));
+    CU(cudaMemcpy(fh.data(), b->d_first_hit, T * sizeof(long), cudaMemcpyDeviceToHost));
+    CU(cudaMemcpy(cu.data(), b->d_cycles_used, T * sizeof(long), cudaMemcpyDeviceToHost));
+    for (int t = 0; t < T; ++t) {
+      results[t].best_energy = be[t];
+      results[t].best_replica = bk[t];
+      results[t].reached_target = re[t];
+      results[t].first_hit_cycle = fh[t];
+      results[t].cycles_used = cu[t];
+      results[t].wall_seconds = 1e-3 * double(ms) / T;
+    }
+  }
+  if (best_states)
+    CU(cudaMemcpy(best_states, b->d_best_state, size_t(T) * b->g.n, cudaMemcpyDeviceToHost));
+  if (trace) {
+    if (!b->record_trace) return set_err(SSQA_EINVAL, "batch was created without a trace");
+    CU(cudaMemcpy(trace, b->d_trace, size_t(T) * (b->p.sc + 1) * b->p.r * sizeof(double),
+                  cudaMemcpyDeviceToHost));
+  }
+  return SSQA_OK;
+}
+
+int ssqa_run_batch(ssqa_problem prob, const ssqa_params_c* p, const uint64_t* seeds,
+                   int trials, int has_target, double target, int record_trace,
+                   int stop_at_target, int engine, ssqa_result_c* results,
+                   int8_t* best_states, double* trace) {
+  ssqa_batch b = nullptr;
+  int rc = ssqa_batch_create(prob, p, trials, record_trace, engine, &b);
+  if (rc) return rc;
+  rc = ssqa_batch_set_seeds(b, seeds);
+  if (!rc) rc = ssqa_batch_launch(b, has_target, target, stop_at_target);
+  if (!rc) rc = ssqa_batch_fetch(b, results, best_states, record_trace ? trace : nullptr);
+  std::string keep = g_err;
+  ssqa_batch_destroy(b);
+  g_err = keep;
+  return rc;
+}
+
+int ssqa_batch_init(ssqa_batch b) {
+  if (!b) return set_err(SSQA_EINVAL, "null batch");
+  if (!b->seeds_set) return set_err(SSQA_EINVAL, "seeds not set");
+  CU(cudaSetDevice(b->prob->device));
+  int rc = init_state(b);
+  if (rc) return rc;
+  CU(cudaStreamSynchronize(b->prob->stream));
+  return SSQA_OK;
+}
+
+int ssqa_batch_sweep_with(ssqa_batch b, double jperp, double i0) {
+  if (!b) return set_err(SSQA_EINVAL, "null batch");
+  CU(cudaSetDevice(b->prob->device));
+  int rc = b->engine == SSQA_ENGINE_TCGEN05 ? tc_sweep(b, jperp, i0)
+                                            : simt_sweep(b, jperp, i0, 1, nullptr);
+  if (rc) return rc == SSQA_ECUDA && b->engine == SSQA_ENGINE_TCGEN05
+                     ? set_err(rc, tc_last_error()) : rc;
+  CU(cudaStreamSynchronize(b->prob->stream));
+  return SSQA_OK;
+}
+
+int ssqa_batch_sweep(ssqa_batch b, long count) {
+  if (!b) return set_err(SSQA_EINVAL, "null batch");
+  for (long s = 0; s < count; ++s) {
+    if (b->cycle + 1 >= kMaxCycles) return set_err(SSQA_EINVAL, "cycle out of range");
+    int rc = ssqa_batch_sweep_with(b, jperp_at(b->cycle, b->p), b->p.i0);
+    if (rc) return rc;
+  }
+  return SSQA_OK;
+}
+
+int ssqa_batch_energies(ssqa_batch b, double* out) {
+  if (!b || !out) return set_err(SSQA_EINVAL, "null argument");
+  CU(cudaSetDevice(b->prob->device));
+  const Geom& g = b->g;
+  // fields + integer energies of the current state (no update, no scan)
+  cudaStream_t st = b->prob->stream;
+  int32_t* S = b->d_S;
+  bool tmp = false;
+  if (!S) {
+    int rc = dalloc(&S, b->slot_elems);
+    if (rc) return rc;
+    tmp = true;
+  }
+  launch_field_simt(g, b->prob->d_J, slot_ptr(b, b->cur), S, st);
+  CHECK_LAUNCH();
+  StepArgs a{b->cycle, 0.0, b->p.i0, b->p.n_rnd, b->p.alpha, 0, 0};
+  launch_energy_update_simt(g, S, b->prob->d_H, b->prob->q.scale, b->d_seeds,
+                            slot_ptr(b, b->cur), slot_ptr(b, b->cur), slot_ptr(b, b->cur),
+                            b->d_acc, b->d_E, a, st);
+  CHECK_LAUNCH();
+  std::vector<long long> E(g.ccols);
+  CU(cudaMemcpyAsync(E.data(), b->d_E, E.size() * sizeof(long long), cudaMemcpyDeviceToHost,
+                     st));
+  CU(cudaStreamSynchronize(st));
+  if (tmp) cudaFree(S);
+  const double scale = b->prob->q.scale, offset = b->prob->q.offset;
+  for (int t = 0; t < g.T; ++t)
+    for (int k = 0; k < g.R; ++k)
+      out[size_t(t) * g.R + k] = -0.5 * (double(E[col_of(g, t, k)]) * scale) + offset;
+  return SSQA_OK;
+}
+
+int ssqa_batch_read_lattice(ssqa_batch b, int trial, double* sigma, double* acc, double* hist,
+                            long* cycle) {
+  if (!b) return set_err(SSQA_EINVAL, "null batch");
+  if (trial < 0 || trial >= b->g.T) return set_err(SSQA_ERANGE, "trial index out of range");
+  CU(cudaSetDevice(b->prob->device));
+  CU(cudaStreamSynchronize(b->prob->stream));
+  const Geom& g = b->g;
+  const int n = g.n, R = g.R;
+  std::vector<int8_t> col(n);
+  std::vector<double> acol(n);
+  auto read_slot = [&](int slot, double* dst) -> int {
+    for (int k = 0; k < R; ++k) {
+      CU(cudaMemcpy(col.data(), slot_ptr(b, slot) + size_t(col_of(g, trial, k)) * g.npad, n,
+                    cudaMemcpyDeviceToHost));
+      for (int i = 0; i < n; ++i) dst[size_t(i) * R + k] = double(col[i]);
+    }
+    return SSQA_OK;
+  };
+  int rc;
+  if (sigma && (rc = read_slot(b->cur, sigma))) return rc;
+  if (hist)
+    for (int s = 0; s <= b->d; ++s)
+      if ((rc = read_slot(b->phys[s], hist + size_t(s) * n * R))) return rc;
+  if (acc) {
+    for (int k = 0; k < R; ++k) {
+      CU(cudaMemcpy(acol.data(), b->d_acc + size_t(col_of(g, trial, k)) * g.npad,
+                    n * sizeof(double), cudaMemcpyDeviceToHost));
+      for (int i = 0; i < n; ++i) acc[size_t(i) * R + k] = acol[i];
+    }
+  }
+  if (cycle) *cycle = b->cycle;
+  return SSQA_OK;
+}
+
+int ssqa_batch_write_lattice(ssqa_batch b, int trial, const double* sigma, const double* acc,
+                             const double* hist, long cycle) {
+  if (!b || !sigma || !acc || !hist) return set_err(SSQA_EINVAL, "null argument");
+  if (trial < 0 || trial >= b->g.T) return set_err(SSQA_ERANGE, "trial index out of range");
+  if (cycle < 0 || cycle >= kMaxCycles) return set_err(SSQA_EINVAL, "cycle out of range");
+  CU(cudaSetDevice(b->prob->device));
+  int rc = normalize_slots(b);
+  if (rc) return rc;
+  const Geom& g = b->g;
+  const int n = g.n, R = g.R;
+  std::vector<int8_t> col(g.npad, 0);
+  std::vector<double> acol(g.npad, 0.0);
+  auto write_slot = [&](int slot, const double* src) -> int {
+    for (int k = 0; k < R; ++k) {
+      for (int i = 0; i < n; ++i) {
+        const double v = src[size_t(i) * R + k];
+        if (v != 1.0 && v != -1.0) return set_err(SSQA_EINVAL, "spin entry not -1/+1");
+        col[i] = v > 0 ? 1 : -1;
+      }
+      CU(cudaMemcpy(slot_ptr(b, slot) + size_t(col_of(g, trial, k)) * g.npad, col.data(),
+                    g.npad, cudaMemcpyHostToDevice));
+    }
+    return SSQA_OK;
+  };
+  if ((rc = write_slot(b->cur, sigma))) return rc;
+  for (int s = 0; s <= b->d; ++s)
+    if ((rc = write_slot(b->phys[s], hist + size_t(s) * n * R))) return rc;
+  for (int k = 0; k < R; ++k) {
+    for (int i = 0; i < n; ++i) acol[i] = acc[size_t(i) * R + k];
+    CU(cudaMemcpy(b->d_acc + size_t(col_of(g, trial, k)) * g.npad, acol.data(),
+                  g.npad * sizeof(double), cudaMemcpyHostToDevice));
+  }
+  b->cycle = cycle;
+  return SSQA_OK;
+}
+
+}  // extern "C"

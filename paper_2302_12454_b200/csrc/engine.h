@@ -1,0 +1,90 @@
+// engine.h -- internal state behind the C ABI (include/ssqa_cuda.h).
+//
+// HBM layout:
+//   J'    int8  [npad][npad]        row i, column j (K-major for the field
+//                                    product); zero padding.
+//   H'    int32 [npad]
+//   sigma int8  [nslots][ccols][npad] spin columns, K-major (column = one
+//                                    (trial, replica)); padded spins are 0.
+//   acc   f64   [ccols][npad]       clamped accumulators (ReplicaLattice::is_acc)
+// Column c = tile*tile_cols + tl*R + k holds replica k of trial
+// t = tile*tpt + tl; a tile keeps whole trials so the Trotter neighbour
+// k+-1 (mod R) is always inside the tile.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/ssqa_cuda.h"
+
+namespace ssqa_engine {
+
+struct Geom {
+  int n = 0, npad = 0;     // spins, padded spins (multiple of 128)
+  int R = 0, T = 0;        // replicas, trials
+  int tpt = 0;             // trials per column tile
+  int tile_cols = 0;       // columns per tile (multiple of 16, >= tpt*R)
+  int ntiles = 0;
+  int ccols = 0;           // ntiles * tile_cols
+};
+
+struct Quantized {
+  int n = 0, npad = 0, p = 0, max_abs_j = 0, max_abs_h = 0;
+  double offset = 0.0, scale = 1.0;  // scale = 2^-p
+  std::vector<int8_t> J;             // [npad*npad]
+  std::vector<int32_t> H;            // [npad]
+};
+
+// Returns SSQA_OK or SSQA_EUNSUP with *why set.
+int quantize(int n, const double* h, const double* J, double offset, Quantized* q,
+             std::string* why);
+
+}  // namespace ssqa_engine
+
+struct ssqa_problem_s {
+  ssqa_engine::Quantized q;
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int8_t* d_J = nullptr;
+  int32_t* d_H = nullptr;
+};
+
+struct ssqa_batch_s {
+  ssqa_problem_s* prob = nullptr;
+  ssqa_params_c p{};
+  ssqa_engine::Geom g;
+  int engine = SSQA_ENGINE_SIMT;
+  int record_trace = 0;
+  int d = 0, nslots = 0;
+  size_t slot_elems = 0;  // ccols * npad
+
+  // lattice ring: cur = slot of sigma(cycle); phys[s] = slot of the
+  // reference history snapshot s (annealer.hpp:75)
+  int cur = 0;
+  std::vector<int> phys;
+  long cycle = 0;
+
+  int8_t* d_sig = nullptr;    // [nslots][ccols][npad]
+  double* d_acc = nullptr;    // [ccols][npad]
+  uint64_t* d_seeds = nullptr;
+  double* d_jperp = nullptr;  // [sc+1] jperp_schedule table
+  int32_t* d_S = nullptr;     // SIMT engine: integer fields [ccols][npad]
+  long long* d_E = nullptr;   // per-column integer energy sum E' [ccols]
+
+  // per-trial results
+  double* d_best_e = nullptr;
+  int* d_best_k = nullptr;
+  int* d_reached = nullptr;
+  long* d_first_hit = nullptr;
+  long* d_cycles_used = nullptr;
+  int* d_active = nullptr;
+  int8_t* d_best_state = nullptr;  // [T][n]
+  double* d_trace = nullptr;       // [T][sc+1][R]
+
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  long launches = 0;
+  bool seeds_set = false;
+};

@@ -1,0 +1,220 @@
+// simt_kernels.cu -- lattice init, per-trial scan and the CUDA-core sweep
+// engine (SSQA_ENGINE_SIMT).  The tcgen05 engine reuses init and scan.
+#include "simt_kernels.cuh"
+
+namespace ssqa_engine {
+
+using namespace ssqa_dev;
+
+// init_lattice (annealer.cpp:432-447): sigma = pm1(raw(spin_counter(0,k,i)))
+// under key (seed, kStreamSpinInit); acc = 0.  One block per column.
+__global__ void k_init(Geom g, const uint64_t* __restrict__ seeds, int8_t* __restrict__ sig,
+                       double* __restrict__ acc) {
+  const int col = blockIdx.x;
+  const ColInfo c = decode_col(g, col);
+  const uint64_t key = c.live ? rng_key(seeds[c.t], kStreamSpinInit) : 0;
+  int8_t* s = sig + size_t(col) * g.npad;
+  double* a = acc + size_t(col) * g.npad;
+  for (int i = threadIdx.x; i < g.npad; i += blockDim.x) {
+    int8_t v = 0;
+    if (c.live && i < g.n) {
+      v = (mix64(key + spin_counter(0, c.k, i) * kGolden) >> 63) ? 1 : -1;
+    }
+    s[i] = v;
+    a[i] = 0.0;
+  }
+}
+
+// Fresh AnnealResult per trial (annealer.cpp:323-324).
+__global__ void k_reset_results(int T, long sc, double* best_e, int* best_k, int* reached,
+                                long* first_hit, long* cycles_used, int* active) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= T) return;
+  best_e[t] = __longlong_as_double(0x7ff0000000000000ll);  // +inf
+  best_k[t] = 0;
+  reached[t] = 0;
+  first_hit[t] = -1;
+  cycles_used[t] = sc;
+  active[t] = 1;
+}
+
+// S[col][i] = sum_j J'[i][j] sigma[col][j]  (int8 x int8 -> int32).
+// 64 x 64 output tile per block, 4 x 4 per thread, 64-byte K chunks, dp4a.
+__global__ void __launch_bounds__(256) k_field_simt(Geom g, const int8_t* __restrict__ J,
+                                                    const int8_t* __restrict__ sig,
+                                                    int32_t* __restrict__ S) {
+  __shared__ int Js[kFB][kFB / 4 + 1];
+  __shared__ int Ss[kFB][kFB / 4 + 1];
+  const int i0 = blockIdx.x * kFB, c0 = blockIdx.y * kFB;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  int acc[4][4] = {};
+  const int lr = threadIdx.x >> 2, lq = (threadIdx.x & 3) * 4;  // row, word offset
+  for (int kk = 0; kk < g.npad; kk += kFB) {
+    const int4 jv = *reinterpret_cast<const int4*>(J + size_t(i0 + lr) * g.npad + kk + lq * 4);
+    int4 sv = make_int4(0, 0, 0, 0);
+    if (c0 + lr < g.ccols)
+      sv = *reinterpret_cast<const int4*>(sig + size_t(c0 + lr) * g.npad + kk + lq * 4);
+    Js[lr][lq + 0] = jv.x; Js[lr][lq + 1] = jv.y; Js[lr][lq + 2] = jv.z; Js[lr][lq + 3] = jv.w;
+    Ss[lr][lq + 0] = sv.x; Ss[lr][lq + 1] = sv.y; Ss[lr][lq + 2] = sv.z; Ss[lr][lq + 3] = sv.w;
+    __syncthreads();
+#pragma unroll 4
+    for (int w = 0; w < kFB / 4; ++w) {
+      int a[4], b[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) a[r] = Js[ty * 4 + r][w];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) b[r] = Ss[tx * 4 + r][w];
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[r][q] = __dp4a(a[r], b[q], acc[r][q]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int col = c0 + tx * 4 + q;
+    if (col < g.ccols) {
+      *reinterpret_cast<int4*>(S + size_t(col) * g.npad + i0 + ty * 4) =
+          make_int4(acc[0][q], acc[1][q], acc[2][q], acc[3][q]);
+    }
+  }
+}
+
+
+// energies_from_fields (annealer.cpp:246-256) as an integer sum, fused with
+// update_spins (annealer.cpp:258-300).  One block per column.
+__global__ void __launch_bounds__(256) k_energy_update_simt(
+    Geom g, const int32_t* __restrict__ S, const int32_t* __restrict__ H, double scale,
+    const uint64_t* __restrict__ seeds, const int8_t* __restrict__ sig_cur,
+    const int8_t* __restrict__ sig_src, int8_t* __restrict__ sig_dst, double* __restrict__ acc,
+    long long* __restrict__ E, StepArgs a) {
+  const int col = blockIdx.x;
+  const ColInfo c = decode_col(g, col);
+  const size_t base = size_t(col) * g.npad;
+  if (!c.live) {
+    if (a.do_update)
+      for (int i = threadIdx.x; i < g.npad; i += blockDim.x) sig_dst[base + i] = 0;
+    if (threadIdx.x == 0) E[col] = 0;
+    return;
+  }
+  const uint64_t key = rng_key(seeds[c.t], kStreamSweepNoise);
+  const UpdateConsts uc = make_consts(a.n_rnd, a.jperp, a.i0, a.alpha);
+  const int kup = (c.k + 1 == g.R) ? 0 : c.k + 1;
+  const int kdn = (c.k == 0) ? g.R - 1 : c.k - 1;
+  const size_t up_base = size_t(col_of(g, c.t, kup)) * g.npad;
+  const size_t dn_base = size_t(col_of(g, c.t, kdn)) * g.npad;
+  long long e = 0;
+  for (int i = threadIdx.x; i < g.npad; i += blockDim.x) {
+    if (i >= g.n) {
+      if (a.do_update) sig_dst[base + i] = 0;
+      continue;
+    }
+    const int s = S[base + i], h = H[i];
+    const int sg = sig_cur[base + i];
+    e += (long long)(sg * (s + 2 * h));
+    if (a.do_update) {
+      const double field = scaled(s + h, scale);
+      const uint32_t t5 = mix64_top5(key + spin_counter(uint64_t(a.cycle), c.k, i) * kGolden);
+      const int up = sig_src[up_base + i];
+      const int dn = a.bidirectional ? sig_src[dn_base + i] : 0;
+      const double nv = update_one(uc, field, noise_index(t5), up, dn, a.bidirectional != 0,
+                                   acc[base + i]);
+      acc[base + i] = nv;
+      sig_dst[base + i] = nv >= 0.0 ? 1 : -1;
+    }
+  }
+  // block reduction of the integer energy (exact, order-free)
+  __shared__ long long red[8];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = e;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    long long tot = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += red[w];
+    E[col] = tot;
+  }
+}
+
+
+// scan_state (annealer.cpp:327-345) for one trial per warp: energies of all
+// replicas in ascending k, strict-< best, first hit, optional trace; then
+// the warp snapshots the best column (best_state, annealer.cpp:334-337).
+__global__ void k_scan(Geom g, const long long* __restrict__ E, ScanArgs a,
+                       const int8_t* __restrict__ sig_cur, double* best_e, int* best_k,
+                       int* reached, long* first_hit, long* cycles_used, int* active,
+                       int8_t* __restrict__ best_state, double* __restrict__ trace) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  const int t = warp;
+  if (t >= g.T) return;
+  if (!active[t]) return;
+  int improved = -1;
+  if (lane == 0) {
+    double be = best_e[t];
+    int hit = reached[t];
+    for (int k = 0; k < g.R; ++k) {
+      const long long ep = E[col_of(g, t, k)];
+      const double ek = __dadd_rn(__dmul_rn(-0.5, scaled(ep, a.scale)), a.offset);
+      if (ek < be) {
+        be = ek;
+        improved = k;
+        if (a.has_target && !hit && be <= a.target_tol) {
+          hit = 1;
+          first_hit[t] = a.cycle;
+        }
+      }
+      if (a.record_trace) trace[(size_t(t) * (a.sc + 1) + a.cycle) * g.R + k] = ek;
+    }
+    best_e[t] = be;
+    if (improved >= 0) best_k[t] = improved;
+    reached[t] = hit;
+    if (a.stop_at_target && hit && a.cycle < a.sc) {
+      active[t] = 0;
+      cycles_used[t] = a.cycle;
+    }
+  }
+  improved = __shfl_sync(0xffffffffu, improved, 0);
+  if (improved >= 0) {
+    const int8_t* src = sig_cur + size_t(col_of(g, t, improved)) * g.npad;
+    int8_t* dst = best_state + size_t(t) * g.n;
+    for (int i = lane; i < g.n; i += 32) dst[i] = src[i];
+  }
+}
+
+
+void launch_init(const Geom& g, const uint64_t* seeds, int8_t* sig, double* acc,
+                 cudaStream_t st) {
+  k_init<<<g.ccols, 256, 0, st>>>(g, seeds, sig, acc);
+}
+
+void launch_reset_results(int T, long sc, double* best_e, int* best_k, int* reached,
+                          long* first_hit, long* cycles_used, int* active, cudaStream_t st) {
+  k_reset_results<<<(T + 127) / 128, 128, 0, st>>>(T, sc, best_e, best_k, reached, first_hit,
+                                                    cycles_used, active);
+}
+
+void launch_field_simt(const Geom& g, const int8_t* J, const int8_t* sig, int32_t* S,
+                       cudaStream_t st) {
+  dim3 grid(g.npad / kFB, (g.ccols + kFB - 1) / kFB);
+  k_field_simt<<<grid, 256, 0, st>>>(g, J, sig, S);
+}
+
+void launch_energy_update_simt(const Geom& g, const int32_t* S, const int32_t* H, double scale,
+                               const uint64_t* seeds, const int8_t* sig_cur,
+                               const int8_t* sig_src, int8_t* sig_dst, double* acc,
+                               long long* E, const StepArgs& a, cudaStream_t st) {
+  k_energy_update_simt<<<g.ccols, 256, 0, st>>>(g, S, H, scale, seeds, sig_cur, sig_src,
+                                                sig_dst, acc, E, a);
+}
+
+void launch_scan(const Geom& g, const long long* E, const ScanArgs& a, const int8_t* sig_cur,
+                 double* best_e, int* best_k, int* reached, long* first_hit, long* cycles_used,
+                 int* active, int8_t* best_state, double* trace, cudaStream_t st) {
+  const int wpb = 4;
+  k_scan<<<(g.T + wpb - 1) / wpb, 32 * wpb, 0, st>>>(g, E, a, sig_cur, best_e, best_k, reached,
+                                                     first_hit, cycles_used, active, best_state,
+                                                     trace);
+}
+
+}  // namespace ssqa_engine

@@ -1,0 +1,17 @@
+// sweep_tc.h -- the fused tcgen05 sweep engine (SSQA_ENGINE_TCGEN05).
+#pragma once
+
+#include "engine.h"
+#include "simt_kernels.cuh"
+
+namespace ssqa_engine {
+
+// True when the tcgen05 kernel handles this padded size / replica count.
+bool tc_supported(int npad, int r);
+// Full run: cycles 0..sc with scans (state already initialised).
+int tc_run(ssqa_batch_s* b, const ScanArgs& sa);
+// One sweep at b->cycle without a scan (per-step API).
+int tc_sweep(ssqa_batch_s* b, double jperp, double i0);
+const char* tc_last_error();
+
+}  // namespace ssqa_engine

@@ -1,0 +1,201 @@
+// host/annealer.cpp -- the reference annealer API (ssqa/annealer.hpp) on top
+// of the C ABI (include/ssqa_cuda.h).  The facade owns no numerics: it
+// converts types, forwards to the device engine and turns error codes back
+// into the reference's exceptions (annealer.cpp:25-30, 365-373).
+#include "ssqa/annealer.hpp"
+
+#include <memory>
+#include <stdexcept>
+#include <string>
+
+#include "ssqa_cuda.h"
+
+namespace ssqa {
+
+namespace {
+
+ssqa_params_c to_c(const SsqaParams& p) {
+  ssqa_params_c c{};
+  c.r = p.r;
+  c.jperp_min = p.jperp_min;
+  c.jperp_max = p.jperp_max;
+  c.beta = p.beta;
+  c.tau = p.tau;
+  c.delay = p.delay;
+  c.i0 = p.i0;
+  c.n_rnd = p.n_rnd;
+  c.alpha = p.alpha;
+  c.sc = p.sc;
+  c.bidirectional = p.bidirectional ? 1 : 0;
+  return c;
+}
+
+void check(int rc) {
+  if (rc == SSQA_OK) return;
+  const std::string msg = ssqa_last_error();
+  if (rc == SSQA_EINVAL || rc == SSQA_EUNSUP) throw std::invalid_argument(msg);
+  if (rc == SSQA_ERANGE) throw std::out_of_range(msg);
+  throw std::runtime_error(msg);
+}
+
+struct ProblemHandle {
+  ssqa_problem p = nullptr;
+  ~ProblemHandle() { ssqa_problem_destroy(p); }
+};
+struct BatchHandle {
+  ssqa_batch b = nullptr;
+  ~BatchHandle() { ssqa_batch_destroy(b); }
+};
+
+void upload(const IsingModel& m, int device, ProblemHandle& h) {
+  check(ssqa_problem_create(m.n(), m.biases().data(), m.coupling_data(), m.offset(), device,
+                            &h.p));
+}
+
+// A one-trial batch carrying an explicit lattice (per-step API).
+void load(BatchHandle& bh, ProblemHandle& ph, const ReplicaLattice& lat, SsqaParams p,
+          uint64_t seed) {
+  if (p.sc < 1) p.sc = 1;  // the per-step API never reads sc
+  ssqa_params_c c = to_c(p);
+  check(ssqa_batch_create(ph.p, &c, 1, 0, SSQA_ENGINE_AUTO, &bh.b));
+  check(ssqa_batch_set_seeds(bh.b, &seed));
+  std::vector<double> hist;
+  for (const auto& h : lat.history) hist.insert(hist.end(), h.begin(), h.end());
+  std::vector<double> acc = lat.is_acc;
+  if (acc.empty()) acc.assign(lat.sigma.size(), 0.0);
+  if (hist.empty())
+    for (int s = 0; s <= p.delay; ++s) hist.insert(hist.end(), lat.sigma.begin(), lat.sigma.end());
+  check(ssqa_batch_write_lattice(bh.b, 0, lat.sigma.data(), acc.data(), hist.data(), lat.cycle));
+}
+
+}  // namespace
+
+void SsqaParams::validate(int n) const {
+  ssqa_params_c c = to_c(*this);
+  check(ssqa_params_validate(&c, n));
+}
+
+double jperp_schedule(long cycle, const SsqaParams& p) {
+  ssqa_params_c c = to_c(p);
+  double v = 0.0;
+  check(ssqa_jperp_schedule(cycle, &c, &v));
+  return v;
+}
+
+const std::vector<double>& ReplicaLattice::delayed_sigma() const {
+  return history[size_t(cycle % (delay + 1))];
+}
+
+ReplicaLattice init_lattice(int n, int replicas, int delay, uint64_t seed) {
+  // The device init kernel needs a problem handle; any n-spin model does.
+  IsingModel blank(n);
+  ProblemHandle ph;
+  upload(blank, 0, ph);
+  SsqaParams p;
+  p.r = replicas;
+  p.delay = delay;
+  p.sc = 1;
+  ssqa_params_c c = to_c(p);
+  BatchHandle bh;
+  check(ssqa_batch_create(ph.p, &c, 1, 0, SSQA_ENGINE_AUTO, &bh.b));
+  check(ssqa_batch_set_seeds(bh.b, &seed));
+  check(ssqa_batch_init(bh.b));
+  ReplicaLattice lat;
+  lat.n = n;
+  lat.replicas = replicas;
+  lat.delay = delay;
+  const size_t nr = size_t(n) * replicas;
+  lat.sigma.resize(nr);
+  lat.is_acc.resize(nr);
+  std::vector<double> hist((size_t(delay) + 1) * nr);
+  check(ssqa_batch_read_lattice(bh.b, 0, lat.sigma.data(), lat.is_acc.data(), hist.data(),
+                                &lat.cycle));
+  for (int s = 0; s <= delay; ++s)
+    lat.history.emplace_back(hist.begin() + s * nr, hist.begin() + (s + 1) * nr);
+  return lat;
+}
+
+void ssqa_sweep(ReplicaLattice& lat, const IsingModel& m, double jperp, const SsqaParams& p,
+                uint64_t seed, long cycle) {
+  if (lat.n != m.n() || lat.replicas != p.r)
+    throw std::invalid_argument("lattice dimensions do not match model/params");
+  if (cycle != lat.cycle) throw std::invalid_argument("sweep cycle does not match lattice history");
+  ProblemHandle ph;
+  upload(m, 0, ph);
+  BatchHandle bh;
+  load(bh, ph, lat, p, seed);
+  check(ssqa_batch_sweep_with(bh.b, jperp, p.i0));
+  const size_t nr = lat.sigma.size();
+  std::vector<double> hist((size_t(lat.delay) + 1) * nr);
+  lat.is_acc.resize(nr);
+  check(ssqa_batch_read_lattice(bh.b, 0, lat.sigma.data(), lat.is_acc.data(), hist.data(),
+                                &lat.cycle));
+  lat.history.assign(size_t(lat.delay) + 1, {});
+  for (int s = 0; s <= lat.delay; ++s)
+    lat.history[size_t(s)].assign(hist.begin() + s * nr, hist.begin() + (s + 1) * nr);
+}
+
+std::vector<double> replica_energies(const ReplicaLattice& lat, const IsingModel& m) {
+  if (lat.n != m.n()) throw std::invalid_argument("lattice does not match model");
+  ProblemHandle ph;
+  upload(m, 0, ph);
+  SsqaParams p;
+  p.r = lat.replicas;
+  p.delay = 0;
+  ReplicaLattice flat = lat;
+  flat.delay = 0;
+  flat.history.clear();
+  flat.cycle = 0;
+  BatchHandle bh;
+  load(bh, ph, flat, p, 0);
+  std::vector<double> e(size_t(lat.replicas));
+  check(ssqa_batch_energies(bh.b, e.data()));
+  return e;
+}
+
+std::vector<AnnealResult> ssqa_run_batch(const IsingModel& m, const SsqaParams& p,
+                                         const std::vector<uint64_t>& seeds,
+                                         std::optional<double> target_energy,
+                                         const RunOptions& opts, const EngineOptions& eng) {
+  p.validate(m.n());
+  if (seeds.empty()) return {};
+  ProblemHandle ph;
+  upload(m, eng.device, ph);
+  const int T = int(seeds.size());
+  ssqa_params_c c = to_c(p);
+  std::vector<ssqa_result_c> res(seeds.size());
+  std::vector<int8_t> best(size_t(T) * m.n());
+  std::vector<double> trace;
+  if (opts.record_trace) trace.resize(size_t(T) * (p.sc + 1) * p.r);
+  check(ssqa_run_batch(ph.p, &c, seeds.data(), T, target_energy ? 1 : 0,
+                       target_energy.value_or(0.0), opts.record_trace ? 1 : 0,
+                       opts.stop_at_target ? 1 : 0, eng.engine, res.data(), best.data(),
+                       opts.record_trace ? trace.data() : nullptr));
+  std::vector<AnnealResult> out(seeds.size());
+  for (int t = 0; t < T; ++t) {
+    AnnealResult& a = out[size_t(t)];
+    a.best_energy = res[size_t(t)].best_energy;
+    a.best_replica = res[size_t(t)].best_replica;
+    a.reached_target = res[size_t(t)].reached_target != 0;
+    a.first_hit_cycle = res[size_t(t)].first_hit_cycle;
+    a.cycles_used = res[size_t(t)].cycles_used;
+    a.wall_seconds = res[size_t(t)].wall_seconds;
+    a.best_state.assign(best.begin() + size_t(t) * m.n(), best.begin() + size_t(t + 1) * m.n());
+    if (opts.record_trace) {
+      const double* tr = trace.data() + size_t(t) * (p.sc + 1) * p.r;
+      for (long cyc = 0; cyc <= a.cycles_used; ++cyc) {
+        const double jp = jperp_schedule(cyc, p);
+        for (int k = 0; k < p.r; ++k)
+          a.trace.push_back({cyc, k, tr[size_t(cyc) * p.r + k], jp});
+      }
+    }
+  }
+  return out;
+}
+
+AnnealResult ssqa_run(const IsingModel& m, const SsqaParams& p, uint64_t seed,
+                      std::optional<double> target_energy, const RunOptions& opts) {
+  return ssqa_run_batch(m, p, {seed}, target_energy, opts).front();
+}
+
+}  // namespace ssqa

@@ -1,0 +1,86 @@
+// host/instances.cpp -- C entry points of include/ssqa_host.h.
+#include <cstring>
+#include <exception>
+#include <stdexcept>
+#include <string>
+
+#include "ssqa/gi.hpp"
+#include "ssqa/model.hpp"
+#include "ssqa/rng.hpp"
+#include "ssqa_host.h"
+
+namespace {
+
+thread_local std::string g_host_err;
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const std::invalid_argument& e) {
+    g_host_err = e.what();
+    return 1;
+  } catch (const std::out_of_range& e) {
+    g_host_err = e.what();
+    return 2;
+  } catch (const std::exception& e) {
+    g_host_err = e.what();
+    return 3;
+  }
+}
+
+constexpr uint32_t kStreamDenseCoupling = 8;
+constexpr uint32_t kStreamDenseBias = 9;
+
+}  // namespace
+
+extern "C" {
+
+const char* ssqa_host_last_error(void) { return g_host_err.c_str(); }
+
+int ssqa_gi_ising(int n_nodes, double edge_prob, uint64_t seed, int permute, double c1,
+                  double c2, double* h, double* J, double* offset) {
+  return guard([&] {
+    ssqa::IsingModel m = ssqa::qubo_to_ising(
+        ssqa::build_gi_qubo(ssqa::generate_gi(n_nodes, edge_prob, seed, permute != 0, c1, c2)));
+    const int n = m.n();
+    std::memcpy(h, m.biases().data(), size_t(n) * sizeof(double));
+    std::memcpy(J, m.coupling_data(), size_t(n) * n * sizeof(double));
+    *offset = m.offset();
+  });
+}
+
+int ssqa_dense_ising(int n, int kind, uint64_t seed, double* h, double* J, double* offset) {
+  return guard([&] {
+    if (n < 1) throw std::invalid_argument("n must be >= 1");
+    if (kind != 0 && kind != 1) throw std::invalid_argument("kind must be 0 or 1");
+    const ssqa::CounterRng cj(seed, kStreamDenseCoupling), ch(seed, kStreamDenseBias);
+    for (int i = 0; i < n; ++i) {
+      J[size_t(i) * n + i] = 0.0;
+      h[i] = kind == 0 ? double(int(ch.below(uint64_t(i), 16)) - 8) : 0.0;
+      for (int j = i + 1; j < n; ++j) {
+        const uint64_t c = uint64_t(i) * uint64_t(n) + uint64_t(j);
+        const double v = kind == 0 ? double(int(cj.below(c, 16)) - 8)
+                                   : ((cj.raw(c) >> 63) ? 1.0 : -1.0);
+        J[size_t(i) * n + j] = v;
+        J[size_t(j) * n + i] = v;
+      }
+    }
+    *offset = 0.0;
+  });
+}
+
+int ssqa_ising_energy(int n, const double* h, const double* J, double offset,
+                      const int8_t* spins, double* out) {
+  return guard([&] {
+    ssqa::IsingModel m(n, offset);
+    for (int i = 0; i < n; ++i) {
+      m.set_bias(i, h[i]);
+      for (int j = i + 1; j < n; ++j) m.set_coupling(i, j, J[size_t(i) * n + j]);
+    }
+    *out = ssqa::ising_energy(m, ssqa::SpinVector(spins, spins + n));
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,303 @@
+"""Bit-exact parity of the CUDA engine against the CPU oracle and the
+reference's own fixtures.  Every call goes through the C ABI
+(include/ssqa_cuda.h) via paper_2302_12454_b200._lib.
+
+Bar: bitwise equality of spins, accumulators (as uint64 bit patterns),
+energies, traces, best states and per-trial outcomes -- the path is exact
+(SURVEY.md section 7), so there is no tolerance anywhere in this file.
+"""
+import numpy as np
+import pytest
+
+import paper_2302_12454_b200 as sq
+from paper_2302_12454_b200 import _lib
+from oracle_py import params
+
+pytestmark = pytest.mark.gpu
+
+ENGINES = [_lib.ENGINE_SIMT, _lib.ENGINE_TCGEN05]
+
+
+def engine_ok(engine, n=128, r=20):
+    """Probe whether `engine` accepts this shape (tcgen05 may not, yet)."""
+    m = sq.IsingModel(n)
+    prob = sq.Problem(m)
+    try:
+        b = sq.Batch(prob, sq.SsqaParams(r=r, sc=1), 1, engine=engine)
+        b.close()
+        return True
+    except _lib.SsqaInvalidArgument:
+        return False
+
+
+@pytest.fixture(params=ENGINES, ids=["simt", "tcgen05"])
+def engine(request):
+    if not engine_ok(request.param):
+        pytest.skip("engine unavailable for this build")
+    return request.param
+
+
+def bits(a):
+    return np.ascontiguousarray(a, dtype=np.float64).view(np.uint64)
+
+
+def to_sq(p):
+    return sq.SsqaParams(r=p.r, jperp_min=p.jperp_min, jperp_max=p.jperp_max, beta=p.beta,
+                         tau=p.tau, delay=p.delay, i0=p.i0, n_rnd=p.n_rnd, alpha=p.alpha,
+                         sc=p.sc, bidirectional=bool(p.bidirectional))
+
+
+def test_init_lattice_matches_oracle(orc, engine):
+    for n, r, d, T in [(1, 1, 0, 1), (100, 20, 1, 7), (130, 3, 2, 5), (300, 33, 1, 3)]:
+        prob = sq.Problem(sq.IsingModel(n))
+        b = sq.Batch(prob, sq.SsqaParams(r=r, delay=d, sc=1), T, engine=engine)
+        seeds = [1000 + 17 * t for t in range(T)]
+        b.set_seeds(seeds)
+        b.init()
+        for t in range(T):
+            s, a, h, c = b.read_lattice(t)
+            s0, a0, h0 = orc.init_lattice(n, r, d, seeds[t])
+            assert np.array_equal(s, s0) and np.array_equal(a, a0) and np.array_equal(h, h0)
+            assert c == 0
+
+
+def test_lattice_trajectories_match_reference(golden, engine):
+    """Per-step sigma / acc / energies against tests/golden/lattice_traj.npz."""
+    for name, c in golden("lattice_traj").items():
+        n, r, d = int(c["n"]), int(c["r"]), int(c["delay"])
+        m = sq.IsingModel.from_arrays(c["h"], c["J"], float(c["offset"]))
+        p = sq.SsqaParams(r=r, delay=d, alpha=float(c["alpha"]), bidirectional=bool(c["bidir"]),
+                          sc=1)
+        if str(c["kind"]) == "real":
+            with pytest.raises(ValueError):
+                sq.Problem(m)
+            continue
+        b = sq.Batch(sq.Problem(m), p, 1, engine=engine)
+        b.set_seeds([int(c["seed"])])
+        b.init()
+        s, a, h, cyc = b.read_lattice(0)
+        assert np.array_equal(s, c["sigma"][0]), name
+        for t in range(len(c["jperp"])):
+            b.sweep_with(float(c["jperp"][t]), float(c["i0"][t]))
+            s, a, h, cyc = b.read_lattice(0)
+            assert cyc == t + 1
+            assert np.array_equal(s, c["sigma"][t + 1]), (name, t)
+            assert np.array_equal(bits(a), bits(c["acc"][t + 1])), (name, t)
+            e = b.energies()[0]
+            assert np.array_equal(bits(e), bits(c["energy"][t])), (name, t)
+        assert np.array_equal(h, c["hist_final"]), name
+
+
+def test_batched_sweeps_match_oracle_per_trial(orc, engine):
+    """Many trials in one batch: every trial's lattice equals the oracle's,
+    step by step, on a GI instance (C1 shape, fewer trials)."""
+    m = sq.gi_ising(10, 0.5, 7, True, 1.0, 1.0)
+    for p in (params(20, 1), params(7, 1, delay=2, bidirectional=True), params(5, 1, delay=0)):
+        T = 9
+        seeds = [int(x) for x in np.random.default_rng(p.r).integers(0, 2 ** 63, T)]
+        b = sq.Batch(sq.Problem(m), to_sq(p), T, engine=engine)
+        b.set_seeds(seeds)
+        b.init()
+        states = [orc.init_lattice(m.n, p.r, p.delay, s) for s in seeds]
+        cyc = 0
+        for step in range(6):
+            b.sweep(25 if step else 1)
+            count = 25 if step else 1
+            for t in range(T):
+                s, a, h = states[t]
+                c0 = cyc
+                for c in range(c0, c0 + count):
+                    orc.ssqa_sweep(m.h, m.J, m.offset, orc.jperp_schedule(c, p), p, seeds[t], c,
+                                   s, a, h, c)
+            cyc += count
+            for t in (0, T // 2, T - 1):
+                s, a, h, c = b.read_lattice(t)
+                so, ao, ho = states[t]
+                assert c == cyc
+                assert np.array_equal(s, so) and np.array_equal(bits(a), bits(ao)), (p.r, t, cyc)
+                assert np.array_equal(h, ho)
+            e = b.energies()
+            for t in range(T):
+                eo = orc.replica_energies(m.h, m.J, m.offset, p.r, states[t][0])
+                assert np.array_equal(bits(e[t]), bits(eo))
+
+
+def test_runs_match_reference_fixtures(golden, engine):
+    """ssqa_run KATs incl. traces, best states, stop-at-target."""
+    gi = golden("gi_instances")
+    for name, c in golden("runs").items():
+        if name.startswith("gi"):
+            m = sq.gi_ising(int(c["n_nodes"]), 0.5, int(c["gi_seed"]), True, float(c["c"]),
+                            float(c["c"]))
+            kw = {k[2:]: (v.item() if hasattr(v, "item") else v)
+                  for k, v in c.items() if k.startswith("p_")}
+            p = sq.SsqaParams(**kw)
+            res = sq.ssqa_run(m, p, int(c["seed"]), float(c["target"]),
+                              sq.RunOptions(True, bool(c["stop"])), engine=engine)
+            assert res.reached_target == bool(c["reached"]), name
+            assert res.first_hit_cycle == int(c["first_hit"]), name
+            assert res.cycles_used == int(c["cycles_used"]), name
+        else:
+            m = sq.IsingModel.from_arrays(c["h"], c["J"], float(c["offset"]))
+            p = sq.SsqaParams(r=int(c["p_r"]), sc=int(c["p_sc"]), tau=int(c["p_tau"]))
+            res = sq.ssqa_run(m, p, int(c["seed"]), None, sq.RunOptions(True, False),
+                              engine=engine)
+            assert res.cycles_used == int(c["cycles_used"])
+        assert res.best_energy == float(c["best_energy"]), name
+        assert res.best_replica == int(c["best_replica"]), name
+        assert np.array_equal(res.best_state, c["best_state"]), name
+        assert np.array_equal(bits(res.trace_energy), bits(c["trace"])), name
+    _ = gi
+
+
+def test_run_trials_matches_reference_kat(golden, engine):
+    """run_trials({r=20, ec=20000, n=10, permute, c=1, gi_seed=7, 100 trials,
+    base 1000}) -> p_s 0.80 and identical per-trial outcomes."""
+    t = golden("trials")["trials_gi10"]
+    m = sq.gi_ising(10, 0.5, 7, True, 1.0, 1.0)
+    outs, p_s, t_mean, tts = sq.run_trials(m, sq.SsqaParams(r=20), 100, 20000, 1000,
+                                           engine=engine)
+    assert p_s == 0.80
+    assert [o.seed for o in outs] == [int(x) for x in t["seed"]]
+    assert [int(o.reached_target) for o in outs] == [int(x) for x in t["reached"]]
+    assert [o.first_hit_cycle for o in outs] == [int(x) for x in t["first_hit"]]
+    assert np.array_equal(bits([o.best_energy for o in outs]), bits(t["best_energy"]))
+    assert tts.kind == "finite" and t_mean > 0
+
+
+def test_full_runs_match_oracle_many_trials(orc, engine):
+    """A 48-trial batch at N=100 and N=400 (C1/C2 shapes, shortened): every
+    trial equals the oracle's ssqa_run."""
+    for nn, R, sc, T in [(10, 20, 300, 48), (20, 20, 60, 6)]:
+        m = sq.gi_ising(nn, 0.5, 7, True, 1.0, 1.0)
+        p = params(R, sc)
+        seeds = list(range(500, 500 + T))
+        res = sq.ssqa_run_batch(m, to_sq(p), seeds, 0.0, sq.RunOptions(True, False),
+                                engine=engine)
+        for t in range(0, T, 1 if T < 10 else 5):
+            o = orc.ssqa_run(m.h, m.J, m.offset, p, seeds[t], 0.0, True, False)
+            r = res[t]
+            assert (r.best_energy, r.best_replica, r.reached_target, r.first_hit_cycle,
+                    r.cycles_used) == (o.best_energy, o.best_replica, o.reached_target,
+                                       o.first_hit_cycle, o.cycles_used), t
+            assert np.array_equal(r.best_state, o.best_state)
+            assert np.array_equal(bits(r.trace_energy), bits(o.trace))
+
+
+def test_dense_integer_model_matches_oracle(orc, engine):
+    """C4-style dense int[-8,7] couplings (the reference's plain-double path)."""
+    m = sq.dense_ising(200, 0, 3)
+    p = params(8, 40, tau=5, bidirectional=True)
+    seeds = [11, 12, 13]
+    res = sq.ssqa_run_batch(m, to_sq(p), seeds, None, sq.RunOptions(True, False),
+                            engine=engine)
+    for t, s in enumerate(seeds):
+        o = orc.ssqa_run(m.h, m.J, m.offset, p, s, None, True, False)
+        assert res[t].best_energy == o.best_energy
+        assert np.array_equal(res[t].best_state, o.best_state)
+        assert np.array_equal(bits(res[t].trace_energy), bits(o.trace))
+
+
+def test_stop_at_target_and_unreachable(orc, engine):
+    # test_annealer.cpp:470-508: hit at cycle 0, unreachable targets, fixed budget
+    rng = np.random.default_rng(23)
+    h = rng.integers(-8, 9, 4) / 4.0
+    J = np.triu(rng.integers(-8, 9, (4, 4)) / 4.0, 1)
+    m = sq.IsingModel.from_arrays(h, J + J.T, 0.5)
+    p = sq.SsqaParams(r=3, sc=40)
+    lat = sq.init_lattice(4, 3, 1, 31)
+    e0 = sq.replica_energies(lat, m).min()
+    res = sq.ssqa_run(m, p, 31, float(e0), engine=engine)
+    assert res.reached_target and res.first_hit_cycle == 0 and res.cycles_used == 0
+    miss = sq.ssqa_run(m, p, 31, -1e6, engine=engine)
+    assert not miss.reached_target and miss.first_hit_cycle == -1 and miss.cycles_used == 40
+    q = params(3, 40)
+    for stop in (True, False):
+        o = orc.ssqa_run(m.h, m.J, m.offset, q, 31, -1.0, False, stop)
+        r = sq.ssqa_run(m, p, 31, -1.0, sq.RunOptions(False, stop), engine=engine)
+        assert (r.reached_target, r.first_hit_cycle, r.cycles_used, r.best_energy) == \
+            (o.reached_target, o.first_hit_cycle, o.cycles_used, o.best_energy)
+
+
+def test_device_kats_clamp_and_delay(engine):
+    # test_annealer.cpp:219-304 through the device per-step API
+    p = sq.SsqaParams(r=1, sc=4, n_rnd=0.0, delay=0, jperp_min=0.0, jperp_max=0.0)
+    up = sq.IsingModel(1)
+    up.set_bias(0, 5.0)
+    lat = sq.init_lattice(1, 1, 0, 3)
+    sq.ssqa_sweep(lat, up, 0.0, p, 3, 0, engine=engine)
+    assert lat.acc(0, 0) == 1.0 and lat.spin(0, 0) == 1.0
+    down = sq.IsingModel(1)
+    down.set_bias(0, -5.0)
+    lat = sq.init_lattice(1, 1, 0, 3)
+    sq.ssqa_sweep(lat, down, 0.0, p, 3, 0, engine=engine)
+    assert lat.acc(0, 0) == -2.0 and lat.spin(0, 0) == -1.0
+    half = sq.SsqaParams(**{**p.__dict__, "alpha": 0.5})
+    lat = sq.init_lattice(1, 1, 0, 3)
+    sq.ssqa_sweep(lat, up, 0.0, half, 3, 0, engine=engine)
+    assert lat.acc(0, 0) == 1.5
+    # delayed coupling, test_annealer.cpp:266-292
+    m = sq.IsingModel(1)
+    q = sq.SsqaParams(r=2, sc=4, n_rnd=0.0, delay=1)
+    lat = sq.init_lattice(1, 2, 1, 5)
+    lat.sigma[:] = [-1.0, -1.0]
+    lat.is_acc[:] = 0.0
+    lat.history[0] = [1.0, -1.0]
+    lat.history[1] = [-1.0, 1.0]
+    sq.ssqa_sweep(lat, m, 0.7, q, 5, 0, engine=engine)
+    assert lat.acc(0, 0) == -0.7 and lat.acc(0, 1) == 0.7
+    assert list(lat.sigma) == [-1.0, 1.0] and list(lat.history[0]) == [-1.0, 1.0]
+    assert lat.cycle == 1
+    sq.ssqa_sweep(lat, m, 0.7, q, 5, 1, engine=engine)
+    assert lat.acc(0, 0) == 0.0 and lat.spin(0, 0) == 1.0
+    with pytest.raises(ValueError):
+        sq.ssqa_sweep(lat, m, 0.7, q, 5, 7, engine=engine)  # cycle mismatch
+
+
+def test_unrepresentable_models_are_rejected():
+    m = sq.IsingModel(3)
+    m.set_coupling(0, 1, 0.1)
+    with pytest.raises(ValueError):
+        sq.Problem(m)
+
+
+def test_cpp_facade_program(tmp_path, orc):
+    """Compile a reference-style C++ caller against include/ssqa/*.hpp and
+    run it: the drop-in claim for C++ users."""
+    import os
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    src = tmp_path / "caller.cpp"
+    src.write_text(r'''
+#include <cstdio>
+#include "ssqa/annealer.hpp"
+#include "ssqa/bench.hpp"
+#include "ssqa/gi.hpp"
+using namespace ssqa;
+int main() {
+  IsingModel m = qubo_to_ising(build_gi_qubo(generate_gi(10, 0.5, 7, true, 1.0, 1.0)));
+  SsqaParams p; p.r = 20; p.sc = 1000;
+  RunOptions o; o.record_trace = true; o.stop_at_target = false;
+  AnnealResult r = ssqa_run(m, p, 123, 0.0, o);
+  std::printf("%d %ld %.17g %d %zu\n", int(r.reached_target), r.first_hit_cycle,
+              r.best_energy, r.best_replica, r.trace.size());
+  BenchConfig c; c.ssqa.r = 20; c.problem.n_nodes = 10; c.problem.permute = true;
+  c.problem.c1 = c.problem.c2 = 1.0; c.problem.fresh_instance = false; c.problem.gi_seed = 7;
+  c.trials = 100; c.ec = 20000; c.base_seed = 1000;
+  BenchRecord rec = run_trials(c);
+  std::printf("%.17g\n", rec.p_s);
+  bool threw = false;
+  try { SsqaParams bad; bad.r = 0; bad.sc = 5; ssqa_run(m, bad, 1); }
+  catch (const std::invalid_argument&) { threw = true; }
+  std::printf("%d\n", int(threw));
+  return 0;
+}
+''')
+    exe = tmp_path / "caller"
+    libdir = os.path.join(root, "paper_2302_12454_b200")
+    subprocess.run(["g++", "-std=c++17", "-O1", f"-I{root}/include", str(src), "-o", str(exe),
+                    f"-L{libdir}", "-lssqa_b200", f"-Wl,-rpath,{libdir}"], check=True)
+    out = subprocess.run([str(exe)], check=True, capture_output=True, text=True).stdout.split()
+    assert out[:5] == ["1", "304", "0", "4", "20020"]
+    assert float(out[5]) == 0.80
+    assert out[6] == "1"

@@ -1,0 +1,149 @@
+"""CPU-side checks of the product library (no GPU needed).
+
+* libssqa_b200.so loads and exports every symbol the include/*.h headers
+  declare (the drop-in boundary);
+* the host problem builders reproduce the reference's instances bit for bit
+  (tests/golden/gi_instances.npz, made from oracle/_ref);
+* the quantizer dry run, parameter validation and schedule follow the
+  reference (annealer.cpp:365-380).
+"""
+import ctypes
+import glob
+import hashlib
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_2302_12454_b200 as sq
+from paper_2302_12454_b200 import _lib
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_c_functions():
+    names = set()
+    for h in glob.glob(os.path.join(ROOT, "include", "*.h")):
+        src = open(h).read()
+        src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+        for m in re.finditer(r"^\s*[A-Za-z_][\w\s\*]*?\b(ssqa_\w+)\s*\(", src, flags=re.M):
+            names.add(m.group(1))
+    return sorted(names)
+
+
+def test_library_exports_every_declared_symbol():
+    L = ctypes.CDLL(_lib.LIB_PATH)
+    names = declared_c_functions()
+    assert len(names) >= 25
+    missing = [n for n in names if not hasattr(L, n)]
+    assert not missing, missing
+    # and the ctypes signature table covers them all
+    bound = {s[0] for s in _lib.SIGNATURES}
+    assert set(names) <= bound, set(names) - bound
+
+
+def test_library_exports_cpp_facade():
+    out = os.popen(f"nm -DC --defined-only {_lib.LIB_PATH}").read()
+    for sym in ("ssqa::ssqa_run(", "ssqa::ssqa_run_batch(", "ssqa::init_lattice(",
+                "ssqa::ssqa_sweep(", "ssqa::replica_energies(", "ssqa::run_trials(",
+                "ssqa::jperp_schedule(", "ssqa::qubo_to_ising(", "ssqa::generate_gi(",
+                "ssqa::build_gi_qubo(", "ssqa::compute_tts("):
+        assert sym in out, sym
+
+
+def test_gi_builder_matches_reference(golden):
+    for name, c in golden("gi_instances").items():
+        m = sq.gi_ising(int(c["n_nodes"]), 0.5, int(c["seed"]), bool(c["permute"]),
+                        float(c["c"]), float(c["c"]))
+        assert np.array_equal(m.h.view(np.uint64), c["h"].view(np.uint64)), name
+        assert m.offset == float(c["offset"]), name
+        assert hashlib.sha256(m.J.tobytes()).hexdigest() == str(c["J_sha"]), name
+
+
+def test_gi_builder_rejects_bad_arguments():
+    with pytest.raises(ValueError):
+        sq.gi_ising(0)
+    with pytest.raises(ValueError):
+        sq.gi_ising(3, edge_prob=1.5)
+    with pytest.raises(ValueError):
+        sq.gi_ising(3, c1=0.0)
+
+
+def test_dense_builders():
+    m = sq.dense_ising(64, 0, 11)
+    assert np.array_equal(m.J, m.J.T) and (np.diag(m.J) == 0).all()
+    assert m.J.min() >= -8 and m.J.max() <= 7 and m.h.min() >= -8 and m.h.max() <= 7
+    assert len(np.unique(m.J[np.triu_indices(64, 1)])) == 16
+    s = sq.dense_ising(64, 1, 11)
+    assert set(np.unique(s.J[np.triu_indices(64, 1)])) == {-1.0, 1.0} and (s.h == 0).all()
+    assert np.array_equal(sq.dense_ising(64, 0, 11).J, m.J)
+
+
+def _qinfo(h, J):
+    L = _lib.lib()
+    v = [ctypes.c_int() for _ in range(4)]
+    rc = L.ssqa_quantize_info(len(h), h.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                              J.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                              *[ctypes.byref(x) for x in v])
+    return rc, [x.value for x in v]
+
+
+def test_quantizer_scales():
+    m = sq.gi_ising(10, 0.5, 7, True, 1.0, 1.0)
+    rc, (npad, p, mj, mh) = _qinfo(m.h, m.J)
+    assert rc == 0 and (npad, p, mj) == (128, 2, 2)
+    m = sq.gi_ising(10, 0.5, 7, True, 0.75, 0.75)
+    rc, (npad, p, mj, mh) = _qinfo(m.h, m.J)
+    assert rc == 0 and p == 4 and mj == 6
+    m = sq.dense_ising(300, 0, 1)
+    rc, (npad, p, mj, mh) = _qinfo(m.h, m.J)
+    assert rc == 0 and (npad, p, mj) == (384, 0, 8)
+    # non-dyadic and out-of-range models are rejected (no CPU fallback)
+    h = np.zeros(3)
+    J = np.zeros((3, 3))
+    J[0, 1] = J[1, 0] = 0.1
+    assert _qinfo(h, J)[0] == _lib.SSQA_EUNSUP
+    J[0, 1] = J[1, 0] = 200.0
+    assert _qinfo(h, J)[0] == _lib.SSQA_EUNSUP
+    J[0, 1] = J[1, 0] = 1.0
+    J[0, 2] = J[2, 0] = 2.0 ** -7  # needs p = 7 -> J' = 128 > 127
+    assert _qinfo(h, J)[0] == _lib.SSQA_EUNSUP
+
+
+def test_params_validation_matches_reference():
+    # annealer.cpp:365-373 / test_annealer.cpp:142-164
+    ok = sq.SsqaParams(r=2, sc=10)
+    ok.validate(3)
+    for bad in (dict(r=0), dict(r=1 << 12), dict(sc=0), dict(sc=1 << 31), dict(jperp_max=-0.1),
+                dict(beta=0), dict(tau=0), dict(delay=-1), dict(i0=0.0), dict(alpha=0.0),
+                dict(n_rnd=-1.0)):
+        p = sq.SsqaParams(**{**ok.__dict__, **bad})
+        with pytest.raises(ValueError):
+            p.validate(3)
+    with pytest.raises(ValueError):
+        ok.validate(0)
+    with pytest.raises(ValueError):
+        ok.validate(1 << 20)
+
+
+def test_jperp_schedule_matches_oracle(orc):
+    from oracle_py import params
+    for kw in (dict(), dict(jperp_min=0.25, jperp_max=0.75, beta=1, tau=1),
+               dict(jperp_min=0.1, jperp_max=0.9, beta=7, tau=13)):
+        p = sq.SsqaParams(r=1, sc=1, **kw)
+        q = params(1, 1, **kw)
+        for c in list(range(0, 1200, 7)) + [399, 400, 401]:
+            assert sq.jperp_schedule(c, p) == orc.jperp_schedule(c, q)
+    with pytest.raises(ValueError):
+        sq.jperp_schedule(-1, sq.SsqaParams(r=1, sc=1))
+
+
+def test_compute_tts():
+    # bench.cpp:144-160
+    assert sq.compute_tts(1.0, 2.0).kind == "saturated"
+    assert sq.compute_tts(0.0, 2.0).kind == "undefined"
+    v = sq.compute_tts(0.5, 2.0)
+    assert v.kind == "finite" and v.seconds == pytest.approx(2.0 * np.log(0.01) / np.log(0.5))
+    with pytest.raises(ValueError):
+        sq.compute_tts(0.5, 0.0)
