@@ -271,9 +271,9 @@ int ssqa_batch_create(ssqa_problem pr, const ssqa_params_c* p, int trials, int r
   if (trials < 1) return set_err(SSQA_EINVAL, "trials must be >= 1");
   CU(cudaSetDevice(pr->device));
   int eng = engine;
-  if (eng == SSQA_ENGINE_AUTO) eng = tc_supported(pr->q.npad, p->r) ? SSQA_ENGINE_TCGEN05
+  if (eng == SSQA_ENGINE_AUTO) eng = tc_supported(pr->q.npad, p->r, p->delay) ? SSQA_ENGINE_TCGEN05
                                                                     : SSQA_ENGINE_SIMT;
-  if (eng == SSQA_ENGINE_TCGEN05 && !tc_supported(pr->q.npad, p->r))
+  if (eng == SSQA_ENGINE_TCGEN05 && !tc_supported(pr->q.npad, p->r, p->delay))
     return set_err(SSQA_EUNSUP, "tcgen05 engine does not support this shape");
   if (eng != SSQA_ENGINE_SIMT && eng != SSQA_ENGINE_TCGEN05)
     return set_err(SSQA_EINVAL, "unknown engine");

@@ -7,7 +7,7 @@
 namespace ssqa_engine {
 
 // True when the tcgen05 kernel handles this padded size / replica count.
-bool tc_supported(int npad, int r);
+bool tc_supported(int npad, int r, int delay);
 // Full run: cycles 0..sc with scans (state already initialised).
 int tc_run(ssqa_batch_s* b, const ScanArgs& sa);
 // One sweep at b->cycle without a scan (per-step API).

@@ -270,6 +270,7 @@ def test_cpp_facade_program(tmp_path, orc):
     src = tmp_path / "caller.cpp"
     src.write_text(r'''
 #include <cstdio>
+#include <stdexcept>
 #include "ssqa/annealer.hpp"
 #include "ssqa/bench.hpp"
 #include "ssqa/gi.hpp"
