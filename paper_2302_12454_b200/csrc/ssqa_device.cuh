@@ -98,9 +98,49 @@ __device__ __forceinline__ double update_one(const UpdateConsts& c, double field
   return (s >= c.i0) ? c.hi_clamp : ((s < c.lo_clamp) ? c.lo_clamp : s);
 }
 
+// update_one with the noise level chosen straight from the top five RNG
+// bits (branch-free selects): t5 < 14 -> noise[0], t5 < 23 -> noise[1],
+// else noise[2].
+__device__ __forceinline__ double update_fast(const UpdateConsts& c, double field,
+                                              uint32_t t5, int up, int dn, bool bidirectional,
+                                              double acc) {
+  const bool rest = t5 < 14u, neg = t5 < 23u;
+  double nz = neg ? c.noise[1] : c.noise[2];
+  nz = rest ? c.noise[0] : nz;
+  double input = __dadd_rn(field, nz);
+  input = __dadd_rn(input, up > 0 ? c.jp_pos : c.jp_neg);
+  if (bidirectional) input = __dadd_rn(input, dn > 0 ? c.jp_pos : c.jp_neg);
+  const double s = __dadd_rn(acc, input);
+  const double lo = (s < c.lo_clamp) ? c.lo_clamp : s;
+  return (s >= c.i0) ? c.hi_clamp : lo;
+}
+
 // Exact double of an integer field scaled by 2^-p (|v| < 2^53).
 __device__ __forceinline__ double scaled(long long v, double scale) {
   return __dmul_rn(double(v), scale);
+}
+
+// Exact v * 2^-p for int32 v without the XU-pipe I2F.F64: the bit pattern
+// hi:(v ^ 2^31) with hi = exponent of 2^(52-p) encodes (2^52 + v + 2^31) *
+// 2^-p exactly; subtracting (2^52 + 2^31) * 2^-p (exact, same binade) leaves
+// v * 2^-p.  magic_hi = 0x43300000 - (p << 20), magic = (2^52 + 2^31) * 2^-p.
+struct I2D {
+  uint32_t magic_hi;
+  double magic;
+};
+
+__host__ __device__ inline I2D make_i2d(int p) {
+  I2D c;
+  c.magic_hi = 0x43300000u - (uint32_t(p) << 20);
+  double m = 4503601774854144.0;  // 2^52 + 2^31
+  for (int k = 0; k < p; ++k) m *= 0.5;
+  c.magic = m;
+  return c;
+}
+
+__device__ __forceinline__ double scaled_i32(int v, const I2D& c) {
+  const double d = __hiloint2double(int(c.magic_hi), int(uint32_t(v) ^ 0x80000000u));
+  return __dsub_rn(d, c.magic);
 }
 
 }  // namespace ssqa_dev

@@ -25,6 +25,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <string>
 
 #include "sweep_tc.h"
@@ -35,8 +36,7 @@ namespace {
 
 constexpr int kBM = 128;          // rows (spins i) per MMA tile
 constexpr int kBK = 128;          // K bytes per stage (one 128B swizzle row)
-constexpr int kEpiWarps = 8;
-constexpr int kThreads = 32 * (2 + kEpiWarps);
+constexpr int kCW = 8;  // columns per epilogue chunk (one tcgen05.ld .x8)
 constexpr int kMaxDelay = 30;
 constexpr int kMaxCols = 256;
 constexpr int kMaxTrialsPerTile = 256;
@@ -47,6 +47,7 @@ struct TcParams {
   Geom g;
   const int32_t* H;
   double scale, offset;
+  int shift_p;
   const uint64_t* seeds;
   int8_t* sig;
   size_t slot_elems;
@@ -63,7 +64,7 @@ struct TcParams {
   double target_tol;
   int ring_cur;
   int ring_phys[kMaxDelay + 1];
-  int stages;
+  int stages, nslot;
   // per-trial results
   double* best_e;
   int* best_k;
@@ -106,20 +107,31 @@ __device__ __forceinline__ bool mbar_try(uint32_t a, uint32_t parity) {
   return ok != 0;
 }
 
-// Blocking wait with a watchdog: a pipeline that has not advanced for ~20 s
-// traps (kernel error) instead of hanging the device.
+__device__ __forceinline__ bool mbar_try_sleep(uint32_t a, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(a), "r"(parity), "r"(1000000u)
+      : "memory");
+  return ok != 0;
+}
+
+// Slow path of mbar_wait, kept out of line: sleeps in try_wait (suspend
+// hint 1 ms) and traps after ~20 s without progress instead of hanging the
+// device.
+__device__ __noinline__ void mbar_wait_slow(uint32_t a, uint32_t parity) {
+  const long long t0 = clock64();
+  while (!mbar_try_sleep(a, parity)) {
+    if (clock64() - t0 > 40000000000ll) __trap();
+  }
+}
+
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t a = smem_u32(bar);
-  if (mbar_try(a, parity)) return;
-  const long long t0 = clock64();
-  uint32_t n = 0;
-  while (!mbar_try(a, parity)) {
-    if ((++n & 1023u) == 0 && clock64() - t0 > 40000000000ll) {
-      printf("k_sweep_tc: mbarrier wait timed out (block %d thread %d)\n", blockIdx.x,
-             threadIdx.x);
-      __trap();
-    }
-  }
+  if (!mbar_try(a, parity)) mbar_wait_slow(a, parity);
 }
 
 __device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint64_t* bar, void* dst,
@@ -183,6 +195,15 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, int32_t (&v)[16]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, int32_t (&v)[8]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
 __device__ __forceinline__ void tc_fence_before() {
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
 }
@@ -190,8 +211,9 @@ __device__ __forceinline__ void tc_fence_after() {
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 }
 
+template <int EPI>
 __device__ __forceinline__ void epi_bar() {
-  asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
+  asm volatile("bar.sync 1, %0;" ::"n"(EPI * 32) : "memory");
 }
 
 // Spin-slot ring (same rule as the host's pick_free in capi.cu).
@@ -206,13 +228,42 @@ __host__ __device__ inline int ring_free(int cur, const int* phys, int d, int ns
 }
 
 // ------------------------------------------------------------- shared state
-struct ColTab {
-  uint64_t key;   // CounterRng(seed_t, kStreamSweepNoise).key()
-  uint64_t base;  // key + spin_counter(cycle, k, 0) * golden, for this cycle
-  long long E;    // integer energy sum of this cycle
-  int k, tl, up, dn;  // replica, trial-in-tile, neighbour columns (tile-local)
-  int live;
-};
+// Per-column tables (structure of arrays in smem, NT entries each):
+//   c_key  CounterRng(seed_t, kStreamSweepNoise).key()
+//   c_base key + spin_counter(cycle, k, 0) * golden for the current cycle
+//   c_off / c_up / c_dn  element offsets of this column and of its delayed
+//          Trotter neighbours k+1, k-1 (mod R) inside a spin slot
+//   c_kt   replica k | (trial-in-tile << 16);  c_flag bit0 live, bit1 update
+//   c_E    integer energy partials per TMEM lane quarter [4][NT]
+constexpr int kColBytes = 8 * 2 + 4 * 4;
+
+__device__ __forceinline__ int ld_s8(const int8_t* p) {
+  int v;
+  asm volatile("ld.global.s8 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ double ld_f64_stream(const double* p) {
+  double v;
+  asm volatile("ld.global.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ void st_f64_stream(double* p, double v) {
+  asm volatile("st.global.L1::no_allocate.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+__device__ __forceinline__ void st_f64_if(double* p, double v, bool pred) {
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t"
+      "@q st.global.L1::no_allocate.f64 [%0], %1;\n\t}" ::"l"(p),
+      "d"(v), "r"(int(pred))
+      : "memory");
+}
+__device__ __forceinline__ void st_s8_if(int8_t* p, int v, bool pred) {
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t"
+      "@q st.global.s8 [%0], %1;\n\t}" ::"l"(p),
+      "r"(v), "r"(int(pred))
+      : "memory");
+}
 
 struct TrialTab {
   double best_e;
@@ -221,39 +272,81 @@ struct TrialTab {
 };
 
 struct SmemCtl {
-  uint64_t full[16];
-  uint64_t empty[16];
-  uint64_t tfull[2];
-  uint64_t tempty[2];
+  uint64_t full[8];    // operand stages: TMA -> MMA
+  uint64_t empty[8];   // operand stages: MMA -> TMA
+  uint64_t tfull[2];   // accumulator: MMA -> epilogue
+  uint64_t tempty[2];  // accumulator: epilogue -> MMA
+  uint64_t afull[16];  // accumulator-state chunks: loader -> epilogue
+  uint64_t aempty[16]; // accumulator-state chunks: epilogue -> loader
+  uint64_t sfull[2];   // delayed-spin tile: loader -> epilogue
+  uint64_t sempty[2];  // delayed-spin tile: epilogue -> loader
   uint32_t tmem_base;
-  int ring_cur, ring_dst, any_active;
+  int ring_cur, any_active;
   int ring_phys[kMaxDelay + 1];
 };
 
-__global__ void __launch_bounds__(kThreads, 1)
+struct Layout {
+  int stages, nslot;
+  uint32_t a_bytes, b_bytes, acc_off, sig_off, ctl_off, tab_off, total;
+};
+
+__host__ __device__ inline Layout make_layout(int NT, int tpt, int stages, int nslot) {
+  Layout L;
+  L.stages = stages;
+  L.nslot = nslot;
+  L.a_bytes = kBM * kBK;
+  L.b_bytes = uint32_t(NT) * kBK;
+  uint32_t o = uint32_t(stages) * (L.a_bytes + L.b_bytes);
+  L.acc_off = o;
+  o += uint32_t(nslot) * kCW * kBM * 8;
+  L.sig_off = o;
+  o += 2u * uint32_t(NT) * kBM;
+  L.ctl_off = o;
+  o += uint32_t((sizeof(SmemCtl) + 127) / 128 * 128);
+  L.tab_off = o;
+  o += uint32_t(NT) * (kColBytes + 8 * 4) + 8 + uint32_t(tpt) * uint32_t(sizeof(TrialTab));
+  L.total = o + 1024;  // alignment slack
+  return L;
+}
+
+// Warp roles: 0 operand TMA producer, 1 TMEM allocator + MMA issuer,
+// 2 state loader (TMA of accumulator chunks and delayed-spin tiles),
+// 3 .. 3+EPI-1 epilogue (EPI/4 warps per TMEM lane quarter).
+template <int EPI>
+__global__ void __launch_bounds__(32 * (3 + EPI), 1)
     k_sweep_tc(const __grid_constant__ CUtensorMap tmJ, const __grid_constant__ CUtensorMap tmS,
+               const __grid_constant__ CUtensorMap tmSe, const __grid_constant__ CUtensorMap tmA,
                const TcParams P) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  // 1024-align the operand area (SWIZZLE_128B atoms)
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
+  // 1024-align by offsetting into the shared array itself, so every derived
+  // pointer keeps the shared address space (no generic loads)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const Geom& g = P.g;
   const int NT = g.tile_cols;
-  const int stages = P.stages;
-  const uint32_t a_bytes = kBM * kBK, b_bytes = uint32_t(NT) * kBK;
+  const Layout L = make_layout(NT, g.tpt, P.stages, P.nslot);
+  const int stages = L.stages, nslot = L.nslot;
   uint8_t* sA = smem;
-  uint8_t* sB = smem + size_t(stages) * a_bytes;
-  uint8_t* tail = sB + size_t(stages) * b_bytes;
-  SmemCtl* ctl = reinterpret_cast<SmemCtl*>(tail);
-  ColTab* cols = reinterpret_cast<ColTab*>(tail + ((sizeof(SmemCtl) + 15) / 16) * 16);
-  TrialTab* trials = reinterpret_cast<TrialTab*>(cols + NT);
+  uint8_t* sB = smem + size_t(stages) * L.a_bytes;
+  double* acc_ring = reinterpret_cast<double*>(smem + L.acc_off);  // [nslot][kCW][kBM]
+  int8_t* sig_tiles = reinterpret_cast<int8_t*>(smem + L.sig_off);  // [2][NT][kBM]
+  SmemCtl* ctl = reinterpret_cast<SmemCtl*>(smem + L.ctl_off);
+  uint8_t* tabs = smem + L.tab_off;
+  uint64_t* c_key = reinterpret_cast<uint64_t*>(tabs);
+  uint64_t* c_base = c_key + NT;
+  long long* c_E = reinterpret_cast<long long*>(c_base + NT);  // [4][NT]
+  uint32_t* c_off = reinterpret_cast<uint32_t*>(c_E + 4 * NT);  // column * npad (slot offset)
+  uint32_t* c_nbr = c_off + NT;  // (k+1 column)*kBM | (k-1 column)*kBM << 16, tile-local
+  int* c_kt = reinterpret_cast<int*>(c_nbr + NT);
+  int* c_flag = c_kt + NT;
+  TrialTab* trials = reinterpret_cast<TrialTab*>(c_flag + NT + (NT & 1));
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tile = blockIdx.x;
-  const int col0 = tile * NT;  // first global column of this tile
-  const int ntl = min(g.tpt, g.T - tile * g.tpt);  // live trials in this tile
+  const int col0 = tile * NT;
+  const int ntl = min(g.tpt, g.T - tile * g.tpt);
   const int NRT = g.npad / kBM, NKC = g.npad / kBK;
-  const int acc_cols = NT;  // TMEM columns per accumulator buffer
+  const int nchunk = NT / kCW;
+  const int acc_cols = NT;
 
   // ---- one-time setup ----
   if (threadIdx.x == 0) {
@@ -263,7 +356,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&ctl->tfull[b], 1);
-      mbar_init(&ctl->tempty[b], kEpiWarps);
+      mbar_init(&ctl->tempty[b], EPI);
+      mbar_init(&ctl->sfull[b], 1);
+      mbar_init(&ctl->sempty[b], EPI);
+    }
+    for (int s = 0; s < nslot; ++s) {
+      mbar_init(&ctl->afull[s], 1);
+      mbar_init(&ctl->aempty[s], 4);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     ctl->ring_cur = P.ring_cur;
@@ -274,6 +373,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     prefetch_tmap(&tmJ);
     prefetch_tmap(&tmS);
   }
+  if (warp == 2 && lane == 0) {
+    prefetch_tmap(&tmSe);
+    prefetch_tmap(&tmA);
+  }
   if (warp == 1) {
     const uint32_t ncols = (2 * acc_cols <= 256) ? 256u : 512u;
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -283,34 +386,28 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   for (int c = threadIdx.x; c < NT; c += blockDim.x) {
     const ColInfo ci = decode_col(g, col0 + c);
-    ColTab ct{};
-    ct.live = ci.live;
-    ct.k = ci.k;
-    ct.tl = ci.t - tile * g.tpt;
-    ct.key = ci.live ? rng_key(P.seeds[ci.t], kStreamSweepNoise) : 0;
+    const int tl = ci.t - tile * g.tpt;
+    c_key[c] = ci.live ? rng_key(P.seeds[ci.t], kStreamSweepNoise) : 0;
     const int kup = (ci.k + 1 == g.R) ? 0 : ci.k + 1;
     const int kdn = (ci.k == 0) ? g.R - 1 : ci.k - 1;
-    ct.up = ct.tl * g.R + kup;
-    ct.dn = ct.tl * g.R + kdn;
-    ct.E = 0;
-    cols[c] = ct;
+    c_off[c] = uint32_t(col0 + c) * uint32_t(g.npad);
+    c_nbr[c] = uint32_t(tl * g.R + kup) * kBM | (uint32_t(tl * g.R + kdn) * kBM << 16);
+    c_kt[c] = ci.k | (tl << 16);
+    c_flag[c] = ci.live ? 1 : 0;
   }
   for (int t = threadIdx.x; t < ntl; t += blockDim.x) {
     const int tg = tile * g.tpt + t;
     TrialTab tt{};
     tt.active = 1;
     tt.improved = -1;
-    if (!P.run_mode) {
-      trials[t] = tt;
-      continue;
+    if (P.run_mode) {
+      tt.best_e = P.best_e[tg];
+      tt.best_k = P.best_k[tg];
+      tt.reached = P.reached[tg];
+      tt.first_hit = P.first_hit[tg];
+      tt.cycles_used = P.cycles_used[tg];
+      tt.active = P.active[tg];
     }
-    tt.best_e = P.best_e[tg];
-    tt.best_k = P.best_k[tg];
-    tt.reached = P.reached[tg];
-    tt.first_hit = P.first_hit[tg];
-    tt.cycles_used = P.cycles_used[tg];
-    tt.active = P.active[tg];
-    tt.improved = -1;
     trials[t] = tt;
   }
   tc_fence_before();
@@ -319,8 +416,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem_base = ctl->tmem_base;
   const uint32_t idesc = idesc_i8(kBM, NT);
 
-  uint32_t it = 0;      // smem pipeline position (producer and MMA agree)
-  uint32_t acc_it = 0;  // accumulator position (MMA and epilogue agree)
+  uint32_t it = 0;      // operand stage sequence (producer == MMA)
+  uint32_t acc_it = 0;  // accumulator / row-tile sequence (MMA == loader == epilogue)
 
   for (long c = P.c_first; c <= P.c_last; ++c) {
     const bool do_update = c < P.sc;
@@ -330,7 +427,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (!ctl->any_active) break;
 
     if (warp == 0) {
-      // ===== TMA producer =====
+      // ===== operand TMA producer =====
       if (lane == 0) {
         const int yS = cur * g.ccols + col0;
         for (int rt = 0; rt < NRT; ++rt) {
@@ -338,9 +435,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int s = it % stages;
             const uint32_t ph = (it / stages) & 1;
             mbar_wait(&ctl->empty[s], ph ^ 1);
-            mbar_expect_tx(&ctl->full[s], a_bytes + b_bytes);
-            tma_load_2d(&tmJ, &ctl->full[s], sA + size_t(s) * a_bytes, kc * kBK, rt * kBM);
-            tma_load_2d(&tmS, &ctl->full[s], sB + size_t(s) * b_bytes, kc * kBK, yS);
+            mbar_expect_tx(&ctl->full[s], L.a_bytes + L.b_bytes);
+            tma_load_2d(&tmJ, &ctl->full[s], sA + size_t(s) * L.a_bytes, kc * kBK, rt * kBM);
+            tma_load_2d(&tmS, &ctl->full[s], sB + size_t(s) * L.b_bytes, kc * kBK, yS);
           }
         }
       }
@@ -359,8 +456,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t ph = (it / stages) & 1;
             mbar_wait(&ctl->full[s], ph);
             tc_fence_after();
-            const uint32_t a0 = smem_u32(sA + size_t(s) * a_bytes);
-            const uint32_t b0 = smem_u32(sB + size_t(s) * b_bytes);
+            const uint32_t a0 = smem_u32(sA + size_t(s) * L.a_bytes);
+            const uint32_t b0 = smem_u32(sB + size_t(s) * L.b_bytes);
 #pragma unroll
             for (int k = 0; k < kBK / 32; ++k) {
               mma_i8(d_tmem, umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32), idesc,
@@ -372,77 +469,124 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
       __syncwarp();
+    } else if (warp == 2) {
+      // ===== state loader: delayed-spin tile + accumulator chunks =====
+      if (lane == 0) {
+        const int ySrc = src * g.ccols + col0;
+        for (int rt = 0; rt < NRT; ++rt, ++acc_it) {
+          const int sb = acc_it & 1;
+          const uint32_t sph = (acc_it >> 1) & 1;
+          mbar_wait(&ctl->sempty[sb], sph ^ 1);
+          mbar_expect_tx(&ctl->sfull[sb], uint32_t(NT) * kBM);
+          tma_load_2d(&tmSe, &ctl->sfull[sb], sig_tiles + size_t(sb) * NT * kBM, rt * kBM, ySrc);
+          for (int ch = 0; ch < nchunk; ++ch) {
+            const uint32_t seq = acc_it * uint32_t(nchunk) + uint32_t(ch);
+            const int slot = int(seq % uint32_t(nslot));
+            const uint32_t ph = (seq / uint32_t(nslot)) & 1;
+            mbar_wait(&ctl->aempty[slot], ph ^ 1);
+            mbar_expect_tx(&ctl->afull[slot], kCW * kBM * 8);
+            tma_load_2d(&tmA, &ctl->afull[slot], acc_ring + size_t(slot) * kCW * kBM, rt * kBM,
+                        col0 + ch * kCW);
+          }
+        }
+      }
+      __syncwarp();
     } else {
       // ===== epilogue =====
-      const int ew = warp - 2;             // 0..7
-      const int q = warp & 3;              // TMEM lane quarter this warp may access
-      const int half = ew >> 2;            // column half
-      const int ncol_half = NT / 2;        // multiple of 8
-      // per-cycle RNG bases and energy reset
-      for (int cl = ew * 32 + lane; cl < NT; cl += kEpiWarps * 32) {
-        cols[cl].base = cols[cl].key + spin_counter(uint64_t(c), uint32_t(cols[cl].k), 0) *
-                                           kGolden;
-        cols[cl].E = 0;
+      const int ew = warp - 3;  // 0 .. EPI-1
+      const int q = warp & 3;   // TMEM lane quarter this warp may access
+      const int sub = ew >> 2;
+      constexpr int kSubs = EPI / 4;
+      for (int cl = ew * 32 + lane; cl < NT; cl += EPI * 32) {
+        const int k = c_kt[cl] & 0xffff, tl = c_kt[cl] >> 16;
+        c_base[cl] = c_key[cl] + spin_counter(uint64_t(c), uint32_t(k), 0) * kGolden;
+        const int live = c_flag[cl] & 1;
+        const int upd = live && do_update && (!P.run_mode || trials[tl].active);
+        c_flag[cl] = live | (upd << 1);
+        for (int qq = 0; qq < 4; ++qq) c_E[qq * NT + cl] = 0;
       }
-      epi_bar();
+      long long* q_sum = c_E + q * NT;
+      epi_bar<EPI>();
       const double jperp = P.run_mode ? P.jperp_tab[c] : P.jperp_fixed;
       const UpdateConsts uc = make_consts(P.n_rnd, jperp, P.i0, P.alpha);
+      const I2D i2d = make_i2d(P.shift_p);
+      const bool bidir = P.bidirectional != 0;
+      // sigma(c) is sign(acc(c)) once this kernel has updated the lattice;
+      // on the first cycle it comes from the spin slot (init / written state).
+      const bool sig_from_acc = c > P.c_first;
       const int8_t* sig_cur = P.sig + size_t(cur) * P.slot_elems;
-      const int8_t* sig_src = P.sig + size_t(src) * P.slot_elems;
       int8_t* sig_dst = P.sig + size_t(dst) * P.slot_elems;
       for (int rt = 0; rt < NRT; ++rt, ++acc_it) {
         const int buf = acc_it & 1;
         const uint32_t aph = (acc_it >> 1) & 1;
-        mbar_wait(&ctl->tfull[buf], aph);
-        tc_fence_after();
-        const int i = rt * kBM + q * 32 + lane;
+        const int il = q * 32 + lane;  // row within the tile
+        const int i = rt * kBM + il;
         const bool row_live = i < g.n;
-        const int h2 = row_live ? 2 * P.H[i] : 0;
         const int h1 = row_live ? P.H[i] : 0;
+        const int h2 = 2 * h1;
         const uint64_t iG = uint64_t(i) * kGolden;
         const uint32_t trow = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(buf * acc_cols);
-        for (int cb = half * ncol_half; cb < (half + 1) * ncol_half; cb += 16) {
-          int32_t v[16];
-          tmem_ld16(trow + uint32_t(cb), v);
-          const int nc = min(16, (half + 1) * ncol_half - cb);
+        const int8_t* stile = sig_tiles + size_t(buf) * NT * kBM;
+        mbar_wait(&ctl->sfull[buf], aph);
+        mbar_wait(&ctl->tfull[buf], aph);
+        tc_fence_after();
+        double* acc_i = P.acc + i;           // + column offset
+        int8_t* dst_i = sig_dst + i;
+        const int8_t* cur_i = sig_cur + i;
+        const int8_t* st_i = stile + il;
+        for (int ch = sub; ch < nchunk; ch += kSubs) {
+          const int cb = ch * kCW;
+          const uint32_t seq = acc_it * uint32_t(nchunk) + uint32_t(ch);
+          const int slot = int(seq % uint32_t(nslot));
+          const uint32_t ph = (seq / uint32_t(nslot)) & 1;
+          int32_t v[kCW];
+          tmem_ld8(trow + uint32_t(cb), v);
+          mbar_wait(&ctl->afull[slot], ph);
+          const double* ab = acc_ring + size_t(slot) * kCW * kBM + il;
+          int ep[kCW];
 #pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            if (j >= nc) continue;
+          for (int j = 0; j < kCW; ++j) {
             const int cl = cb + j;
-            const ColTab ct = cols[cl];
-            int ep = 0;
-            if (ct.live && row_live) {
-              const size_t gi = size_t(col0 + cl) * g.npad + i;
-              const int sgn = sig_cur[gi];
-              const int S = v[j];
-              ep = sgn * (S + h2);
-              if (do_update && trials[ct.tl].active) {
-                const double field = scaled(S + h1, P.scale);
-                const uint32_t t5 = mix64_top5(ct.base + iG);
-                const int up = sig_src[size_t(col0 + ct.up) * g.npad + i];
-                const int dn = P.bidirectional ? sig_src[size_t(col0 + ct.dn) * g.npad + i] : 0;
-                const double nv = update_one(uc, field, noise_index(t5), up, dn,
-                                             P.bidirectional != 0, P.acc[gi]);
-                P.acc[gi] = nv;
-                sig_dst[gi] = nv >= 0.0 ? 1 : -1;
-              }
-            }
-            const int wsum = __reduce_add_sync(0xffffffffu, ep);
-            if (lane == 0 && ct.live) atomicAdd(reinterpret_cast<unsigned long long*>(&cols[cl].E),
-                                                (unsigned long long)(long long)wsum);
+            const int fl = c_flag[cl];
+            const uint32_t coff = c_off[cl];
+            const uint32_t nb = c_nbr[cl];
+            const double a_old = ab[j * kBM];
+            int sg;
+            if (sig_from_acc) sg = a_old >= 0.0 ? 1 : -1;
+            else sg = ld_s8(cur_i + coff);
+            const int S = v[j];
+            ep[j] = (fl & 1) ? sg * (S + h2) : 0;
+            const int up = st_i[nb & 0xffffu];
+            const int dn = bidir ? int(st_i[nb >> 16]) : 0;
+            const double field = scaled_i32(S + h1, i2d);
+            const uint32_t t5 = mix64_top5(c_base[cl] + iG);
+            const double nv = update_fast(uc, field, t5, up, dn, bidir, a_old);
+            const bool w = (fl & 2) && row_live;
+            st_f64_if(acc_i + coff, nv, w);
+            st_s8_if(dst_i + coff, nv >= 0.0 ? 1 : -1, w);
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&ctl->aempty[slot]);
+#pragma unroll
+          for (int j = 0; j < kCW; ++j) {
+            const int wsum = __reduce_add_sync(0xffffffffu, ep[j]);
+            if (lane == 0) q_sum[cb + j] += wsum;
           }
         }
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&ctl->tempty[buf]);
+        if (lane == 0) {
+          mbar_arrive(&ctl->tempty[buf]);
+          mbar_arrive(&ctl->sempty[buf]);
+        }
       }
       asm volatile("fence.proxy.async.global;" ::: "memory");
     }
     __syncthreads();
 
     // ===== scan (annealer.cpp:327-345), one warp per trial =====
-    if (P.run_mode && warp >= 2) {
-      for (int t = warp - 2; t < ntl; t += kEpiWarps) {
+    if (P.run_mode && warp >= 3) {
+      for (int t = warp - 3; t < ntl; t += EPI) {
         TrialTab& tt = trials[t];
         if (!tt.active) continue;
         if (lane == 0) {
@@ -450,7 +594,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           int improved = -1;
           const int tg = tile * g.tpt + t;
           for (int k = 0; k < g.R; ++k) {
-            const long long ep = cols[t * g.R + k].E;
+            long long ep = 0;
+            for (int qq = 0; qq < 4; ++qq) ep += c_E[qq * NT + t * g.R + k];
             const double ek = __dadd_rn(__dmul_rn(-0.5, scaled(ep, P.scale)), P.offset);
             if (ek < be) {
               be = ek;
@@ -473,10 +618,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncwarp();
         const int improved = tt.improved;
         if (improved >= 0) {
-          const int8_t* s = P.sig + size_t(cur) * P.slot_elems +
-                            size_t(col0 + t * g.R + improved) * g.npad;
+          const int8_t* sp = P.sig + size_t(cur) * P.slot_elems +
+                             size_t(col0 + t * g.R + improved) * g.npad;
           int8_t* dstp = P.best_state + size_t(tile * g.tpt + t) * g.n;
-          for (int i = lane; i < g.n; i += 32) dstp[i] = s[i];
+          for (int i = lane; i < g.n; i += 32) dstp[i] = sp[i];
         }
         __syncwarp();
       }
@@ -494,7 +639,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
   }
 
-  // ---- write back per-trial results ----
   if (P.run_mode) {
     for (int t = threadIdx.x; t < ntl; t += blockDim.x) {
       const int tg = tile * g.tpt + t;
@@ -534,50 +678,71 @@ EncodeFn get_encode() {
   return fn;
 }
 
-// 2D int8 map: inner dim `inner` bytes (K), `rows` rows, box {128, box_rows}.
-bool make_map(CUtensorMap* m, void* base, uint64_t inner, uint64_t rows, uint32_t box_rows) {
+// 2D map over a row-major [rows][inner] array of `esize`-byte elements,
+// box {box_inner, box_rows}.
+bool make_map(CUtensorMap* m, void* base, CUtensorMapDataType dt, uint32_t esize,
+              uint64_t inner, uint64_t rows, uint32_t box_inner, uint32_t box_rows,
+              CUtensorMapSwizzle swz) {
   EncodeFn enc = get_encode();
   if (!enc) return false;
   cuuint64_t dims[2] = {inner, rows};
-  cuuint64_t strides[1] = {inner};
-  cuuint32_t box[2] = {uint32_t(kBK), box_rows};
+  cuuint64_t strides[1] = {inner * esize};
+  cuuint32_t box[2] = {box_inner, box_rows};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, base, dims, strides, box, estr,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+  CUresult r = enc(m, dt, 2, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
 
-int smem_bytes(int NT, int stages) {
-  return 1024 + stages * (kBM * kBK + NT * kBK) + int(((sizeof(SmemCtl) + 15) / 16) * 16) +
-         NT * int(sizeof(ColTab)) + kMaxTrialsPerTile * int(sizeof(TrialTab));
+Layout pick_layout(int NT, int tpt) {
+  // prefer >= 3 operand stages and >= 4 state slots inside ~220 KB
+  const uint32_t cap = 220 * 1024;
+  for (int stages = 4; stages >= 2; --stages)
+    for (int nslot = 8; nslot >= 4; nslot -= 2) {
+      Layout L = make_layout(NT, tpt, stages, nslot);
+      if (L.total <= cap) return L;
+    }
+  return make_layout(NT, tpt, 2, 2);
 }
 
-int pick_stages(int NT) {
-  int s = 8;
-  while (s > 2 && smem_bytes(NT, s) > 220 * 1024) --s;
-  return s;
+constexpr int kDefaultEpi = 12;
+
+template <int EPI>
+cudaError_t launch_variant(int grid, int smem, cudaStream_t st, const CUtensorMap* maps,
+                           const TcParams& P) {
+  cudaError_t e = cudaFuncSetAttribute(k_sweep_tc<EPI>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  k_sweep_tc<EPI><<<grid, 32 * (3 + EPI), smem, st>>>(maps[0], maps[1], maps[2], maps[3], P);
+  return cudaSuccess;
 }
 
 int launch(ssqa_batch_s* b, TcParams& P) {
   const Geom& g = b->g;
-  CUtensorMap tmJ, tmS;
-  if (!make_map(&tmJ, b->prob->d_J, uint64_t(g.npad), uint64_t(g.npad), kBM) ||
-      !make_map(&tmS, b->d_sig, uint64_t(g.npad), uint64_t(b->nslots) * g.ccols,
-                uint32_t(g.tile_cols))) {
+  CUtensorMap maps[4];
+  const uint64_t srows = uint64_t(b->nslots) * g.ccols;
+  if (!make_map(&maps[0], b->prob->d_J, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, g.npad, g.npad, kBK,
+                kBM, CU_TENSOR_MAP_SWIZZLE_128B) ||
+      !make_map(&maps[1], b->d_sig, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, g.npad, srows, kBK,
+                g.tile_cols, CU_TENSOR_MAP_SWIZZLE_128B) ||
+      !make_map(&maps[2], b->d_sig, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, g.npad, srows, kBM,
+                g.tile_cols, CU_TENSOR_MAP_SWIZZLE_NONE) ||
+      !make_map(&maps[3], b->d_acc, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, g.npad, g.ccols, kBM,
+                kCW, CU_TENSOR_MAP_SWIZZLE_NONE)) {
     g_tc_err = "cuTensorMapEncodeTiled failed";
     return SSQA_ECUDA;
   }
-  P.stages = pick_stages(g.tile_cols);
-  const int smem = smem_bytes(g.tile_cols, P.stages);
-  cudaError_t e = cudaFuncSetAttribute(k_sweep_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       smem);
-  if (e != cudaSuccess) {
-    g_tc_err = std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e);
-    return SSQA_ECUDA;
-  }
-  k_sweep_tc<<<g.ntiles, kThreads, smem, b->prob->stream>>>(tmJ, tmS, P);
-  e = cudaGetLastError();
+  const Layout L = pick_layout(g.tile_cols, g.tpt);
+  P.stages = L.stages;
+  P.nslot = L.nslot;
+  const int smem = int(L.total);
+  const char* env = getenv("SSQA_TC_EPI");
+  const int epi = env ? atoi(env) : kDefaultEpi;
+  cudaError_t e;
+  if (epi == 8) e = launch_variant<8>(g.ntiles, smem, b->prob->stream, maps, P);
+  else if (epi == 16) e = launch_variant<16>(g.ntiles, smem, b->prob->stream, maps, P);
+  else e = launch_variant<12>(g.ntiles, smem, b->prob->stream, maps, P);
+  if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) {
     g_tc_err = std::string("k_sweep_tc launch: ") + cudaGetErrorString(e);
     return SSQA_ECUDA;
@@ -592,6 +757,7 @@ TcParams base_params(ssqa_batch_s* b) {
   P.H = b->prob->d_H;
   P.scale = b->prob->q.scale;
   P.offset = b->prob->q.offset;
+  P.shift_p = b->prob->q.p;
   P.seeds = b->d_seeds;
   P.sig = b->d_sig;
   P.slot_elems = b->slot_elems;
