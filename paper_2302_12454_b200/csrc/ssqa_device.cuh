@@ -45,6 +45,15 @@ __device__ __forceinline__ uint32_t mix64_top5(uint64_t x0) {
   return top >> 27;
 }
 
+// mix64_top5 for an argument that already includes mix64's "+= golden".
+__device__ __forceinline__ uint32_t mix64_top5_pre(uint64_t x) {
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+  x ^= x >> 27;
+  const uint32_t lo = uint32_t(x), hi = uint32_t(x >> 32);
+  const uint32_t c2lo = 0x133111ebu, c2hi = 0x94d049bbu;
+  return (__umulhi(lo, c2lo) + lo * c2hi + hi * c2lo) >> 27;
+}
+
 // Noise level of update_spins (annealer.cpp:277-278):
 //   u = (raw >> 11) * 2^-53;  u < 7/16 -> 0,  u < 23/32 -> -1,  else +1.
 // Both thresholds are exact multiples of 2^-5, so the comparison reduces to

@@ -125,7 +125,17 @@ __device__ __forceinline__ bool mbar_try_sleep(uint32_t a, uint32_t parity) {
 __device__ __noinline__ void mbar_wait_slow(uint32_t a, uint32_t parity) {
   const long long t0 = clock64();
   while (!mbar_try_sleep(a, parity)) {
-    if (clock64() - t0 > 40000000000ll) __trap();
+    if (clock64() - t0 > 20000000000ll) {
+      if ((threadIdx.x & 31) == 0 || (threadIdx.x >> 5) < 3)
+        printf("k_sweep_tc watchdog: block %d warp %d lane %d stuck on mbarrier smem 0x%x "
+               "parity %u\n",
+               blockIdx.x, threadIdx.x >> 5, threadIdx.x & 31, a, parity);
+      // give every other stuck thread time to report before the trap
+      const long long t1 = clock64();
+      while (clock64() - t1 < 6000000000ll) {
+      }
+      __trap();
+    }
   }
 }
 
@@ -309,6 +319,68 @@ __host__ __device__ inline Layout make_layout(int NT, int tpt, int stages, int n
   return L;
 }
 
+// Per-thread row context for one row tile of the epilogue.
+struct EpiRow {
+  uint64_t acc_i, dst_i, cur_i;  // &acc[i], &sigma_dst[i], &sigma_cur[i] (+ column offset)
+  const int8_t* st_i;            // delayed-spin tile, row il
+  int h1, h2;
+  uint64_t iG;                   // i * golden
+  bool w_row;                    // spin row exists (i < n)
+};
+
+// All of this warp's kCW-column chunks of one row tile: TMEM fields,
+// staged accumulators, delayed neighbours -> exact update, predicated
+// stores, per-column warp energy sums.  BIDIR / SIGACC are hoisted out of
+// the column loop (SIGACC: sigma(c) = sign(acc(c)) instead of a load).
+template <bool BIDIR, bool SIGACC>
+__device__ __forceinline__ void epi_chunks(const EpiRow& er, const UpdateConsts& uc,
+                                           const I2D& i2d, SmemCtl* ctl,
+                                           const double* acc_ring, const int* c_flag,
+                                           const uint32_t* c_off, const uint32_t* c_nbr,
+                                           const uint64_t* c_base, long long* q_sum,
+                                           uint32_t trow, int sub, int nsubs, int nchunk,
+                                           int nps, uint32_t cnt0, int il, int lane) {
+  uint32_t cnt = cnt0;
+  for (int ch = sub; ch < nchunk; ch += nsubs, ++cnt) {
+    const int cb = ch * kCW;
+    const int slot = sub * nps + int(cnt % uint32_t(nps));
+    const uint32_t ph = (cnt / uint32_t(nps)) & 1;
+    int32_t v[kCW];
+    tmem_ld8(trow + uint32_t(cb), v);
+    mbar_wait(&ctl->afull[slot], ph);
+    const double* ab = acc_ring + size_t(slot) * kCW * kBM + il;
+    int ep[kCW];
+#pragma unroll
+    for (int j = 0; j < kCW; ++j) {
+      const int cl = cb + j;
+      const int fl = c_flag[cl];
+      const uint32_t coff = c_off[cl];
+      const uint32_t nb = c_nbr[cl];
+      const double a_old = ab[j * kBM];
+      int sg;
+      if (SIGACC) sg = a_old >= 0.0 ? 1 : -1;
+      else sg = ld_s8(reinterpret_cast<const int8_t*>(er.cur_i + coff));
+      const int S = v[j];
+      ep[j] = (fl & 1) ? sg * (S + er.h2) : 0;
+      const int up = er.st_i[nb & 0xffffu];
+      const int dn = BIDIR ? int(er.st_i[nb >> 16]) : 0;
+      const double field = scaled_i32(S + er.h1, i2d);
+      const uint32_t t5 = mix64_top5_pre(c_base[cl] + er.iG);
+      const double nv = update_fast(uc, field, t5, up, dn, BIDIR, a_old);
+      const bool w = (fl & 2) && er.w_row;
+      st_f64_if(reinterpret_cast<double*>(er.acc_i + uint64_t(coff) * 8u), nv, w);
+      st_s8_if(reinterpret_cast<int8_t*>(er.dst_i + uint64_t(coff)), nv >= 0.0 ? 1 : -1, w);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&ctl->aempty[slot]);
+#pragma unroll
+    for (int j = 0; j < kCW; ++j) {
+      const int wsum = __reduce_add_sync(0xffffffffu, ep[j]);
+      if (lane == 0) q_sum[cb + j] += wsum;
+    }
+  }
+}
+
 // Warp roles: 0 operand TMA producer, 1 TMEM allocator + MMA issuer,
 // 2 state loader (TMA of accumulator chunks and delayed-spin tiles),
 // 3 .. 3+EPI-1 epilogue (EPI/4 warps per TMEM lane quarter).
@@ -347,6 +419,9 @@ __global__ void __launch_bounds__(32 * (3 + EPI), 1)
   const int NRT = g.npad / kBM, NKC = g.npad / kBK;
   const int nchunk = NT / kCW;
   const int acc_cols = NT;
+  constexpr int nsubs = EPI / 4;         // epilogue subgroups (4 warps each)
+  const int nps = nslot / nsubs;         // ring slots per subgroup
+  auto chunks_of = [&](int sb) { return (nchunk - sb + nsubs - 1) / nsubs; };
 
   // ---- one-time setup ----
   if (threadIdx.x == 0) {
@@ -479,10 +554,15 @@ __global__ void __launch_bounds__(32 * (3 + EPI), 1)
           mbar_wait(&ctl->sempty[sb], sph ^ 1);
           mbar_expect_tx(&ctl->sfull[sb], uint32_t(NT) * kBM);
           tma_load_2d(&tmSe, &ctl->sfull[sb], sig_tiles + size_t(sb) * NT * kBM, rt * kBM, ySrc);
+          // chunk ch belongs to epilogue subgroup ch % nsubs and lands in that
+          // subgroup's own ring (slots [sub*nps, sub*nps + nps)): each slot is
+          // consumed, in order, by a single subgroup, so no consumer can ever
+          // wait on a slot barrier two phases ahead (parity aliasing).
           for (int ch = 0; ch < nchunk; ++ch) {
-            const uint32_t seq = acc_it * uint32_t(nchunk) + uint32_t(ch);
-            const int slot = int(seq % uint32_t(nslot));
-            const uint32_t ph = (seq / uint32_t(nslot)) & 1;
+            const int sb2 = ch % nsubs;
+            const uint32_t cnt = acc_it * uint32_t(chunks_of(sb2)) + uint32_t(ch / nsubs);
+            const int slot = sb2 * nps + int(cnt % uint32_t(nps));
+            const uint32_t ph = (cnt / uint32_t(nps)) & 1;
             mbar_wait(&ctl->aempty[slot], ph ^ 1);
             mbar_expect_tx(&ctl->afull[slot], kCW * kBM * 8);
             tma_load_2d(&tmA, &ctl->afull[slot], acc_ring + size_t(slot) * kCW * kBM, rt * kBM,
@@ -499,7 +579,8 @@ __global__ void __launch_bounds__(32 * (3 + EPI), 1)
       constexpr int kSubs = EPI / 4;
       for (int cl = ew * 32 + lane; cl < NT; cl += EPI * 32) {
         const int k = c_kt[cl] & 0xffff, tl = c_kt[cl] >> 16;
-        c_base[cl] = c_key[cl] + spin_counter(uint64_t(c), uint32_t(k), 0) * kGolden;
+        // key + spin_counter(c, k, 0) * golden, plus mix64's initial += golden
+        c_base[cl] = c_key[cl] + spin_counter(uint64_t(c), uint32_t(k), 0) * kGolden + kGolden;
         const int live = c_flag[cl] & 1;
         const int upd = live && do_update && (!P.run_mode || trials[tl].active);
         c_flag[cl] = live | (upd << 1);
@@ -530,48 +611,30 @@ __global__ void __launch_bounds__(32 * (3 + EPI), 1)
         mbar_wait(&ctl->sfull[buf], aph);
         mbar_wait(&ctl->tfull[buf], aph);
         tc_fence_after();
-        double* acc_i = P.acc + i;           // + column offset
-        int8_t* dst_i = sig_dst + i;
-        const int8_t* cur_i = sig_cur + i;
-        const int8_t* st_i = stile + il;
-        for (int ch = sub; ch < nchunk; ch += kSubs) {
-          const int cb = ch * kCW;
-          const uint32_t seq = acc_it * uint32_t(nchunk) + uint32_t(ch);
-          const int slot = int(seq % uint32_t(nslot));
-          const uint32_t ph = (seq / uint32_t(nslot)) & 1;
-          int32_t v[kCW];
-          tmem_ld8(trow + uint32_t(cb), v);
-          mbar_wait(&ctl->afull[slot], ph);
-          const double* ab = acc_ring + size_t(slot) * kCW * kBM + il;
-          int ep[kCW];
-#pragma unroll
-          for (int j = 0; j < kCW; ++j) {
-            const int cl = cb + j;
-            const int fl = c_flag[cl];
-            const uint32_t coff = c_off[cl];
-            const uint32_t nb = c_nbr[cl];
-            const double a_old = ab[j * kBM];
-            int sg;
-            if (sig_from_acc) sg = a_old >= 0.0 ? 1 : -1;
-            else sg = ld_s8(cur_i + coff);
-            const int S = v[j];
-            ep[j] = (fl & 1) ? sg * (S + h2) : 0;
-            const int up = st_i[nb & 0xffffu];
-            const int dn = bidir ? int(st_i[nb >> 16]) : 0;
-            const double field = scaled_i32(S + h1, i2d);
-            const uint32_t t5 = mix64_top5(c_base[cl] + iG);
-            const double nv = update_fast(uc, field, t5, up, dn, bidir, a_old);
-            const bool w = (fl & 2) && row_live;
-            st_f64_if(acc_i + coff, nv, w);
-            st_s8_if(dst_i + coff, nv >= 0.0 ? 1 : -1, w);
-          }
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&ctl->aempty[slot]);
-#pragma unroll
-          for (int j = 0; j < kCW; ++j) {
-            const int wsum = __reduce_add_sync(0xffffffffu, ep[j]);
-            if (lane == 0) q_sum[cb + j] += wsum;
-          }
+        EpiRow er;
+        er.acc_i = reinterpret_cast<uint64_t>(P.acc + i);
+        er.dst_i = reinterpret_cast<uint64_t>(sig_dst + i);
+        er.cur_i = reinterpret_cast<uint64_t>(sig_cur + i);
+        er.st_i = stile + il;
+        er.h1 = h1;
+        er.h2 = h2;
+        er.iG = iG;
+        er.w_row = row_live;
+        const uint32_t cnt0 = acc_it * uint32_t(chunks_of(sub));
+        if (bidir) {
+          if (sig_from_acc)
+            epi_chunks<true, true>(er, uc, i2d, ctl, acc_ring, c_flag, c_off, c_nbr, c_base, q_sum,
+                                   trow, sub, kSubs, nchunk, nps, cnt0, il, lane);
+          else
+            epi_chunks<true, false>(er, uc, i2d, ctl, acc_ring, c_flag, c_off, c_nbr, c_base, q_sum,
+                                    trow, sub, kSubs, nchunk, nps, cnt0, il, lane);
+        } else {
+          if (sig_from_acc)
+            epi_chunks<false, true>(er, uc, i2d, ctl, acc_ring, c_flag, c_off, c_nbr, c_base,
+                                    q_sum, trow, sub, kSubs, nchunk, nps, cnt0, il, lane);
+          else
+            epi_chunks<false, false>(er, uc, i2d, ctl, acc_ring, c_flag, c_off, c_nbr, c_base,
+                                     q_sum, trow, sub, kSubs, nchunk, nps, cnt0, il, lane);
         }
         tc_fence_before();
         __syncwarp();
@@ -694,15 +757,21 @@ bool make_map(CUtensorMap* m, void* base, CUtensorMapDataType dt, uint32_t esize
   return r == CUDA_SUCCESS;
 }
 
-Layout pick_layout(int NT, int tpt) {
-  // prefer >= 3 operand stages and >= 4 state slots inside ~220 KB
+// Operand stages and per-subgroup state-ring depth inside ~220 KB: prefer
+// >= 2 ring slots per subgroup (so the loader runs a chunk ahead), then as
+// many operand stages (<= 4) as fit.
+Layout pick_layout(int NT, int tpt, int nsubs) {
   const uint32_t cap = 220 * 1024;
-  for (int stages = 4; stages >= 2; --stages)
-    for (int nslot = 8; nslot >= 4; nslot -= 2) {
-      Layout L = make_layout(NT, tpt, stages, nslot);
-      if (L.total <= cap) return L;
+  for (int nps = 3; nps >= 1; --nps)
+    for (int stages = 4; stages >= 2; --stages) {
+      if (nps * nsubs > 16) continue;
+      Layout L = make_layout(NT, tpt, stages, nps * nsubs);
+      if (L.total <= cap && (nps >= 2 || stages >= 2)) {
+        if (nps >= 2 && stages < 3) continue;  // rather fewer slots than < 3 stages
+        return L;
+      }
     }
-  return make_layout(NT, tpt, 2, 2);
+  return make_layout(NT, tpt, 2, nsubs);
 }
 
 constexpr int kDefaultEpi = 12;
@@ -732,12 +801,13 @@ int launch(ssqa_batch_s* b, TcParams& P) {
     g_tc_err = "cuTensorMapEncodeTiled failed";
     return SSQA_ECUDA;
   }
-  const Layout L = pick_layout(g.tile_cols, g.tpt);
+  const char* env = getenv("SSQA_TC_EPI");
+  int epi = env ? atoi(env) : kDefaultEpi;
+  if (epi != 8 && epi != 12 && epi != 16) epi = kDefaultEpi;
+  const Layout L = pick_layout(g.tile_cols, g.tpt, epi / 4);
   P.stages = L.stages;
   P.nslot = L.nslot;
   const int smem = int(L.total);
-  const char* env = getenv("SSQA_TC_EPI");
-  const int epi = env ? atoi(env) : kDefaultEpi;
   cudaError_t e;
   if (epi == 8) e = launch_variant<8>(g.ntiles, smem, b->prob->stream, maps, P);
   else if (epi == 16) e = launch_variant<16>(g.ntiles, smem, b->prob->stream, maps, P);
