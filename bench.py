@@ -247,19 +247,15 @@ def run_ours(args, cfg):
         if dist:
             dist.barrier()
 
+    from paper_2302_12454_b200 import shard
+
     def max_over_ranks(x: float) -> float:
-        if not dist:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+        return shard.max_over_ranks(x, dist, "cuda")
 
     R, T, sc = cfg["R"], cfg["T"], cfg["sc"]
     N = n_spins(cfg)
     # contiguous trial blocks per rank, seeds base + global trial index
-    lo = rank * T // world
-    hi = (rank + 1) * T // world
-    seeds = [BASE_SEED + t for t in range(lo, hi)]
+    seeds = shard.shard_seeds(BASE_SEED, T, world, rank)
     engine = {"auto": _lib.ENGINE_AUTO, "simt": _lib.ENGINE_SIMT,
               "tcgen05": _lib.ENGINE_TCGEN05}[args.engine]
     m = build_model(cfg)
@@ -292,29 +288,49 @@ def run_ours(args, cfg):
     value = upd_per_step / (step_ms * 1e-3)
 
     # ---- dominant kernel, live CUDA-event timing on the engine's stream ----
-    bf16_peak, hbm_peak, peak_kind = None, None, None
+    # Roofline: per replica-spin update the path needs 2N
+    # int8 ops (tensor bound) and 16 B of accumulator state (f64 read+write)
+    # + 0.25 B of packed spins + N/(M*T) B of J streamed once per sweep
+    # (HBM bound); the binding one is reported, the other kept beside it.
     hbm_peak, bf16_peak, peak_kind = peaks()
     int8_peak = 2.0 * bf16_peak  # TOPS: int8 dense = 2x bf16 dense on B200
     cols = R * len(seeds)
-    ops_per_launch = 2.0 * N * N * cols  # unpadded algorithmic int8 MACs x 2
+    alg_bytes_per_update = 16.0 + 0.25 + float(N) / float(R * T)
+    updates_per_sweep = float(N) * cols
     if b.engine == _lib.ENGINE_SIMT:
         kname = "k_field_simt"
         k_ms = b.profile_field(10)
-        ops = ops_per_launch
+        ops = 2.0 * N * N * cols
+        launch_bytes = None
+        sweeps_per_launch = 1
     else:
-        kname = "k_sweep_tc (fused, persistent)"
+        kname = "k_sweep_tc (fused, persistent: whole run in one launch)"
         k_ms = statistics.mean(times)
-        ops = ops_per_launch * (sc + 1)
-    achieved = ops / (k_ms * 1e-3) / 1e12
+        ops = 2.0 * N * N * cols * (sc + 1)
+        sweeps_per_launch = sc
+        launch_bytes = alg_bytes_per_update * updates_per_sweep * sc
+    tensor_tops = ops / (k_ms * 1e-3) / 1e12
     traffic = None
     tfile = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tfile):
-        traffic = json.load(open(tfile)).get(f"{cfg_name(args)}:{eng_name}")
-    roofline = {"bound": "tensor", "achieved": achieved, "peak": int8_peak, "unit": "TOPS",
-                "frac": achieved / int8_peak, "traffic": traffic, "kernel": kname,
-                "kernel_ms": k_ms,
-                "peak_note": f"int8 dense = 2 x {peak_kind} bf16 dense ({bf16_peak} TF/s, "
-                             "MEASURED_PEAKS.json)"}
+        t = json.load(open(tfile)).get(f"{args.config}:{eng_name}")
+        if t:
+            traffic = t["dram_bytes_per_sweep"] * sweeps_per_launch
+    if launch_bytes is not None:
+        achieved = launch_bytes / (k_ms * 1e-3) / 1e9
+        roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                    "frac": achieved / hbm_peak, "traffic": traffic, "kernel": kname,
+                    "kernel_ms": k_ms, "alg_bytes_per_update": alg_bytes_per_update,
+                    "tensor": {"achieved": tensor_tops, "peak": int8_peak, "unit": "TOPS",
+                               "frac": tensor_tops / int8_peak},
+                    "peak_note": f"{peak_kind} HBM copy bandwidth (MEASURED_PEAKS.json); int8 "
+                                 f"dense = 2 x {peak_kind} bf16 ({bf16_peak} TF/s)"}
+    else:
+        roofline = {"bound": "tensor", "achieved": tensor_tops, "peak": int8_peak, "unit": "TOPS",
+                    "frac": tensor_tops / int8_peak, "traffic": traffic, "kernel": kname,
+                    "kernel_ms": k_ms,
+                    "peak_note": f"int8 dense = 2 x {peak_kind} bf16 dense ({bf16_peak} TF/s, "
+                                 "MEASURED_PEAKS.json)"}
 
     # ---- e2e through the public C-ABI call with host buffers ----
     e2e_times = []
@@ -334,11 +350,7 @@ def run_ours(args, cfg):
     d2h = len(seeds) * (8 + 4 + 4 + 8 + 8 + 8) + len(seeds) * N
 
     # ---- TTS99 (amortised and reference-formula) ----
-    hits = sum(reached)
-    if dist:
-        t = torch.tensor([hits], dtype=torch.int64, device="cuda")
-        dist.all_reduce(t)
-        hits = int(t.item())
+    hits = shard.sum_over_ranks(sum(reached), dist, "cuda")
     p_s = hits / T
     t_trial = step_ms * 1e-3 / T * world  # device time per trial on one GPU
     tts = sq.compute_tts(p_s, t_trial) if cfg["kind"] == "gi" else None

@@ -27,6 +27,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <string>
+#include <vector>
 
 #include "sweep_tc.h"
 
@@ -65,6 +66,8 @@ struct TcParams {
   int ring_cur;
   int ring_phys[kMaxDelay + 1];
   int stages, nslot;
+  long long* dbg;  // optional timeline (block 0): [role][rt_global][2] clock64 stamps
+  int dbg_rts;     // capacity in row tiles
   // per-trial results
   double* best_e;
   int* best_k;
@@ -151,6 +154,27 @@ __device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint64_t* ba
       " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(x), "r"(y)
       : "memory");
+}
+
+// Same with an L2 cache-policy hint (createpolicy descriptor).
+__device__ __forceinline__ void tma_load_2d_hint(const CUtensorMap* map, uint64_t* bar, void* dst,
+                                                 int x, int y, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      ".L2::cache_hint [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(x), "r"(y), "l"(policy)
+      : "memory");
+}
+
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
 }
 
 __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
@@ -260,11 +284,11 @@ __device__ __forceinline__ double ld_f64_stream(const double* p) {
 __device__ __forceinline__ void st_f64_stream(double* p, double v) {
   asm volatile("st.global.L1::no_allocate.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
 }
-__device__ __forceinline__ void st_f64_if(double* p, double v, bool pred) {
+__device__ __forceinline__ void st_f64_if(double* p, double v, bool pred, uint64_t pol) {
   asm volatile(
       "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t"
-      "@q st.global.L1::no_allocate.f64 [%0], %1;\n\t}" ::"l"(p),
-      "d"(v), "r"(int(pred))
+      "@q st.global.L1::no_allocate.L2::cache_hint.f64 [%0], %1, %3;\n\t}" ::"l"(p),
+      "d"(v), "r"(int(pred)), "l"(pol)
       : "memory");
 }
 __device__ __forceinline__ void st_s8_if(int8_t* p, int v, bool pred) {
@@ -325,6 +349,7 @@ struct EpiRow {
   const int8_t* st_i;            // delayed-spin tile, row il
   int h1, h2;
   uint64_t iG;                   // i * golden
+  uint64_t pol_stream;           // L2 evict_first policy for the accumulator stream
   bool w_row;                    // spin row exists (i < n)
 };
 
@@ -368,7 +393,7 @@ __device__ __forceinline__ void epi_chunks(const EpiRow& er, const UpdateConsts&
       const uint32_t t5 = mix64_top5_pre(c_base[cl] + er.iG);
       const double nv = update_fast(uc, field, t5, up, dn, BIDIR, a_old);
       const bool w = (fl & 2) && er.w_row;
-      st_f64_if(reinterpret_cast<double*>(er.acc_i + uint64_t(coff) * 8u), nv, w);
+      st_f64_if(reinterpret_cast<double*>(er.acc_i + uint64_t(coff) * 8u), nv, w, er.pol_stream);
       st_s8_if(reinterpret_cast<int8_t*>(er.dst_i + uint64_t(coff)), nv >= 0.0 ? 1 : -1, w);
     }
     __syncwarp();
@@ -380,6 +405,15 @@ __device__ __forceinline__ void epi_chunks(const EpiRow& er, const UpdateConsts&
     }
   }
 }
+
+// Debug timeline: role 0 MMA (start, commit), 1 loader (start, all issued),
+// 2 epilogue warp 3 (start incl. waits, done), 3 epilogue warp 3 (operands
+// ready, -).  Block 0, lane 0 only; no cost when P.dbg is null.
+#define DBG_STAMP(role, rtg, which)                                                    \
+  do {                                                                                 \
+    if (P.dbg && blockIdx.x == 0 && lane == 0 && int(rtg) < P.dbg_rts)                 \
+      P.dbg[(size_t(role) * P.dbg_rts + (rtg)) * 2 + (which)] = clock64();            \
+  } while (0)
 
 // Warp roles: 0 operand TMA producer, 1 TMEM allocator + MMA issuer,
 // 2 state loader (TMA of accumulator chunks and delayed-spin tiles),
@@ -505,13 +539,15 @@ __global__ void __launch_bounds__(32 * (3 + EPI), 1)
       // ===== operand TMA producer =====
       if (lane == 0) {
         const int yS = cur * g.ccols + col0;
+        const uint64_t pol_keep = policy_evict_last();
         for (int rt = 0; rt < NRT; ++rt) {
           for (int kc = 0; kc < NKC; ++kc, ++it) {
             const int s = it % stages;
             const uint32_t ph = (it / stages) & 1;
             mbar_wait(&ctl->empty[s], ph ^ 1);
             mbar_expect_tx(&ctl->full[s], L.a_bytes + L.b_bytes);
-            tma_load_2d(&tmJ, &ctl->full[s], sA + size_t(s) * L.a_bytes, kc * kBK, rt * kBM);
+            tma_load_2d_hint(&tmJ, &ctl->full[s], sA + size_t(s) * L.a_bytes, kc * kBK, rt * kBM,
+                             pol_keep);
             tma_load_2d(&tmS, &ctl->full[s], sB + size_t(s) * L.b_bytes, kc * kBK, yS);
           }
         }
@@ -525,6 +561,7 @@ __global__ void __launch_bounds__(32 * (3 + EPI), 1)
           const uint32_t aph = (acc_it >> 1) & 1;
           mbar_wait(&ctl->tempty[buf], aph ^ 1);
           tc_fence_after();
+          DBG_STAMP(0, acc_it, 0);
           const uint32_t d_tmem = tmem_base + uint32_t(buf * acc_cols);
           for (int kc = 0; kc < NKC; ++kc, ++it) {
             const int s = it % stages;
@@ -541,6 +578,7 @@ __global__ void __launch_bounds__(32 * (3 + EPI), 1)
             mma_commit(&ctl->empty[s]);
           }
           mma_commit(&ctl->tfull[buf]);
+          DBG_STAMP(0, acc_it, 1);
         }
       }
       __syncwarp();
@@ -548,10 +586,12 @@ __global__ void __launch_bounds__(32 * (3 + EPI), 1)
       // ===== state loader: delayed-spin tile + accumulator chunks =====
       if (lane == 0) {
         const int ySrc = src * g.ccols + col0;
+        const uint64_t pol_first = policy_evict_first();
         for (int rt = 0; rt < NRT; ++rt, ++acc_it) {
           const int sb = acc_it & 1;
           const uint32_t sph = (acc_it >> 1) & 1;
           mbar_wait(&ctl->sempty[sb], sph ^ 1);
+          DBG_STAMP(1, acc_it, 0);
           mbar_expect_tx(&ctl->sfull[sb], uint32_t(NT) * kBM);
           tma_load_2d(&tmSe, &ctl->sfull[sb], sig_tiles + size_t(sb) * NT * kBM, rt * kBM, ySrc);
           // chunk ch belongs to epilogue subgroup ch % nsubs and lands in that
@@ -565,9 +605,10 @@ __global__ void __launch_bounds__(32 * (3 + EPI), 1)
             const uint32_t ph = (cnt / uint32_t(nps)) & 1;
             mbar_wait(&ctl->aempty[slot], ph ^ 1);
             mbar_expect_tx(&ctl->afull[slot], kCW * kBM * 8);
-            tma_load_2d(&tmA, &ctl->afull[slot], acc_ring + size_t(slot) * kCW * kBM, rt * kBM,
-                        col0 + ch * kCW);
+            tma_load_2d_hint(&tmA, &ctl->afull[slot], acc_ring + size_t(slot) * kCW * kBM,
+                             rt * kBM, col0 + ch * kCW, pol_first);
           }
+          DBG_STAMP(1, acc_it, 1);
         }
       }
       __syncwarp();
@@ -595,6 +636,7 @@ __global__ void __launch_bounds__(32 * (3 + EPI), 1)
       // sigma(c) is sign(acc(c)) once this kernel has updated the lattice;
       // on the first cycle it comes from the spin slot (init / written state).
       const bool sig_from_acc = c > P.c_first;
+      const uint64_t pol_first = policy_evict_first();
       const int8_t* sig_cur = P.sig + size_t(cur) * P.slot_elems;
       int8_t* sig_dst = P.sig + size_t(dst) * P.slot_elems;
       for (int rt = 0; rt < NRT; ++rt, ++acc_it) {
@@ -608,9 +650,11 @@ __global__ void __launch_bounds__(32 * (3 + EPI), 1)
         const uint64_t iG = uint64_t(i) * kGolden;
         const uint32_t trow = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(buf * acc_cols);
         const int8_t* stile = sig_tiles + size_t(buf) * NT * kBM;
+        if (warp == 3) DBG_STAMP(2, acc_it, 0);
         mbar_wait(&ctl->sfull[buf], aph);
         mbar_wait(&ctl->tfull[buf], aph);
         tc_fence_after();
+        if (warp == 3) DBG_STAMP(3, acc_it, 0);
         EpiRow er;
         er.acc_i = reinterpret_cast<uint64_t>(P.acc + i);
         er.dst_i = reinterpret_cast<uint64_t>(sig_dst + i);
@@ -619,6 +663,7 @@ __global__ void __launch_bounds__(32 * (3 + EPI), 1)
         er.h1 = h1;
         er.h2 = h2;
         er.iG = iG;
+        er.pol_stream = pol_first;
         er.w_row = row_live;
         const uint32_t cnt0 = acc_it * uint32_t(chunks_of(sub));
         if (bidir) {
@@ -638,6 +683,7 @@ __global__ void __launch_bounds__(32 * (3 + EPI), 1)
         }
         tc_fence_before();
         __syncwarp();
+        if (warp == 3) DBG_STAMP(2, acc_it, 1);
         if (lane == 0) {
           mbar_arrive(&ctl->tempty[buf]);
           mbar_arrive(&ctl->sempty[buf]);
@@ -808,6 +854,15 @@ int launch(ssqa_batch_s* b, TcParams& P) {
   P.stages = L.stages;
   P.nslot = L.nslot;
   const int smem = int(L.total);
+  const char* trace_path = getenv("SSQA_TC_TRACE");
+  long long* dbg = nullptr;
+  const int dbg_rts = 4096;
+  if (trace_path) {
+    cudaMalloc(&dbg, sizeof(long long) * 4 * dbg_rts * 2);
+    cudaMemsetAsync(dbg, 0, sizeof(long long) * 4 * dbg_rts * 2, b->prob->stream);
+    P.dbg = dbg;
+    P.dbg_rts = dbg_rts;
+  }
   cudaError_t e;
   if (epi == 8) e = launch_variant<8>(g.ntiles, smem, b->prob->stream, maps, P);
   else if (epi == 16) e = launch_variant<16>(g.ntiles, smem, b->prob->stream, maps, P);
@@ -816,6 +871,16 @@ int launch(ssqa_batch_s* b, TcParams& P) {
   if (e != cudaSuccess) {
     g_tc_err = std::string("k_sweep_tc launch: ") + cudaGetErrorString(e);
     return SSQA_ECUDA;
+  }
+  if (dbg) {
+    std::vector<long long> h(size_t(4) * dbg_rts * 2);
+    cudaStreamSynchronize(b->prob->stream);
+    cudaMemcpy(h.data(), dbg, h.size() * sizeof(long long), cudaMemcpyDeviceToHost);
+    cudaFree(dbg);
+    if (FILE* f = fopen(trace_path, "wb")) {
+      fwrite(h.data(), sizeof(long long), h.size(), f);
+      fclose(f);
+    }
   }
   b->launches += 1;
   return SSQA_OK;

@@ -1,0 +1,94 @@
+"""world_size-2 gloo test of the multi-GPU trial-sharding host logic (CPU only).
+
+Each rank takes its contiguous trial block (paper_2302_12454_b200.shard), runs
+the CPU oracle on it as a stand-in for its device batch, and the gathered
+outcomes must equal a single-rank run of the whole battery bit for bit --
+the property the B200 path relies on (trial independence, bench.cpp:379-397).
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+from paper_2302_12454_b200.shard import shard_seeds, shard_trials
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, T, out_q):
+    import sys
+    import torch.distributed as dist
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    sys.path.insert(0, os.path.join(root, "oracle"))
+    from oracle_py import Oracle, params
+    from paper_2302_12454_b200.shard import gather_outcomes, max_over_ranks, sum_over_ranks
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    orc = Oracle("orc")
+    rng = np.random.default_rng(5)
+    n = 12
+    h = rng.integers(-8, 9, n) / 4.0
+    J = np.triu(rng.integers(-8, 9, (n, n)) / 4.0, 1)
+    J = J + J.T
+    p = params(4, 60, tau=7)
+    local = []
+    for s in shard_seeds(1000, T, world, rank):
+        r = orc.ssqa_run(h, J, 0.25, p, s, -3.0, False, False)
+        local.append((s, r.reached_target, r.first_hit_cycle, r.best_energy))
+    allo = gather_outcomes(local, dist)
+    tmax = max_over_ranks(float(rank + 1), dist)
+    hits = sum_over_ranks(sum(int(x[1]) for x in local), dist)
+    if rank == 0:
+        out_q.put((allo, tmax, hits))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_shard_blocks_cover_all_trials():
+    for T in (1, 7, 100, 1024):
+        for world in (1, 2, 3, 4, 8):
+            seen = []
+            for r in range(world):
+                lo, hi = shard_trials(T, world, r)
+                seen.extend(range(lo, hi))
+            assert seen == list(range(T))
+    with pytest.raises(ValueError):
+        shard_trials(10, 2, 2)
+
+
+def test_gloo_world2_matches_single_rank(orc):
+    T = 9
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, T, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    allo, tmax, hits = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert tmax == 2.0
+    # single-rank reference run of the same battery
+    from oracle_py import params
+    rng = np.random.default_rng(5)
+    n = 12
+    h = rng.integers(-8, 9, n) / 4.0
+    J = np.triu(rng.integers(-8, 9, (n, n)) / 4.0, 1)
+    J = J + J.T
+    p = params(4, 60, tau=7)
+    single = []
+    for s in range(1000, 1000 + T):
+        r = orc.ssqa_run(h, J, 0.25, p, s, -3.0, False, False)
+        single.append((s, r.reached_target, r.first_hit_cycle, r.best_energy))
+    assert allo == single
+    assert hits == sum(int(x[1]) for x in single)
