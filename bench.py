@@ -346,7 +346,10 @@ def run_ours(args, cfg):
             assert [o.best_energy for o in out] == [res[t].best_energy for t in range(len(seeds))]
     e2e_s = max_over_ranks(statistics.mean(e2e_times))
     npad = info["n_pad"]
-    h2d = npad * npad + 4 * npad + 8 * len(seeds) + 8 * (sc + 1)
+    # quantized upload: int8 J' (+ its FP4 image when the couplings allow it),
+    # int32 H', seeds, the jperp schedule table
+    fp4 = eng_name == "tcgen05" and info.get("fp4", 0)
+    h2d = npad * npad + (npad * npad // 2 if fp4 else 0) + 4 * npad + 8 * len(seeds) + 8 * (sc + 1)
     d2h = len(seeds) * (8 + 4 + 4 + 8 + 8 + 8) + len(seeds) * N
 
     # ---- TTS99 (amortised and reference-formula) ----

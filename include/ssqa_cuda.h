@@ -91,6 +91,11 @@ int ssqa_problem_destroy(ssqa_problem prob);
 int ssqa_problem_info(ssqa_problem prob, int* n, int* n_pad, int* shift_p, int* max_abs_j,
                       int* max_abs_h);
 
+/* 1 when the problem also holds an FP4 (e2m1) image of J' (couplings all in
+ * {0, +-1, +-2, +-3, +-4, +-6}); the tcgen05 engine then streams 4-bit
+ * operands (tcgen05.mma kind::mxf4 with unit block scales). */
+int ssqa_problem_fp4(ssqa_problem prob);
+
 /* Host-only dry run of the quantizer (no device touched): the scale and
  * ranges ssqa_problem_create would use, or SSQA_EUNSUP with the reason. */
 int ssqa_quantize_info(int n, const double* h, const double* J, int* n_pad, int* shift_p,

@@ -9,7 +9,8 @@ from __future__ import annotations
 import ctypes as C
 import os
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libssqa_b200.so")
+LIB_PATH = os.environ.get("SSQA_LIB_PATH") or os.path.join(
+    os.path.dirname(os.path.abspath(__file__)), "libssqa_b200.so")
 
 SSQA_OK, SSQA_EINVAL, SSQA_ERANGE, SSQA_ECUDA, SSQA_EUNSUP = 0, 1, 2, 3, 4
 ENGINE_AUTO, ENGINE_SIMT, ENGINE_TCGEN05 = 0, 1, 2
@@ -44,6 +45,7 @@ SIGNATURES = [
     ("ssqa_problem_destroy", C.c_int, [VP]),
     ("ssqa_problem_info", C.c_int, [VP, IP, IP, IP, IP, IP]),
     ("ssqa_quantize_info", C.c_int, [C.c_int, DP, DP, IP, IP, IP, IP]),
+    ("ssqa_problem_fp4", C.c_int, [VP]),
     ("ssqa_params_validate", C.c_int, [C.POINTER(ParamsC), C.c_int]),
     ("ssqa_jperp_schedule", C.c_int, [C.c_long, C.POINTER(ParamsC), DP]),
     ("ssqa_run_batch", C.c_int, [VP, C.POINTER(ParamsC), U64P, C.c_int, C.c_int, C.c_double,

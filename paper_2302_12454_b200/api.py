@@ -166,7 +166,10 @@ class Problem:
     def info(self) -> dict:
         v = [C.c_int() for _ in range(5)]
         check(lib().ssqa_problem_info(self._h, *[C.byref(x) for x in v]))
-        return dict(zip(("n", "n_pad", "shift_p", "max_abs_j", "max_abs_h"), [x.value for x in v]))
+        d = dict(zip(("n", "n_pad", "shift_p", "max_abs_j", "max_abs_h"), [x.value for x in v]))
+        # FP4 (e2m1) image uploaded when every coupling is 0, +-1, +-2, +-3, +-4 or +-6
+        d["fp4"] = int(lib().ssqa_problem_fp4(self._h))
+        return d
 
     def close(self):
         if self._h:

@@ -174,6 +174,7 @@ int init_state(ssqa_batch_s* b) {
   b->cur = 0;
   std::fill(b->phys.begin(), b->phys.end(), 0);
   b->cycle = 0;
+  b->lattice_stale = false;
   launch_init(b->g, b->d_seeds, slot_ptr(b, 0), b->d_acc, st);
   CHECK_LAUNCH();
   b->launches += 1;
@@ -218,6 +219,12 @@ int ssqa_problem_create(int n, const double* h, const double* J, double offset, 
   if (e == cudaSuccess)
     e = cudaMemcpyAsync(pr->d_H, pr->q.H.data(), pr->q.H.size() * sizeof(int32_t),
                         cudaMemcpyHostToDevice, pr->stream);
+  if (e == cudaSuccess && pr->q.fp4_ok) {
+    e = cudaMalloc(&pr->d_J4, pr->q.J4.size());
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(pr->d_J4, pr->q.J4.data(), pr->q.J4.size(), cudaMemcpyHostToDevice,
+                          pr->stream);
+  }
   if (e == cudaSuccess) e = cudaStreamSynchronize(pr->stream);
   if (e != cudaSuccess) {
     ssqa_problem_destroy(pr);
@@ -226,6 +233,8 @@ int ssqa_problem_create(int n, const double* h, const double* J, double offset, 
   *out = pr;
   return SSQA_OK;
 }
+
+int ssqa_problem_fp4(ssqa_problem pr) { return (pr && pr->q.fp4_ok) ? 1 : 0; }
 
 int ssqa_quantize_info(int n, const double* h, const double* J, int* n_pad, int* shift_p,
                        int* max_abs_j, int* max_abs_h) {
@@ -247,6 +256,7 @@ int ssqa_problem_destroy(ssqa_problem pr) {
   cudaSetDevice(pr->device);
   dfree(pr->d_J);
   dfree(pr->d_H);
+  dfree(pr->d_J4);
   if (pr->stream) cudaStreamDestroy(pr->stream);
   delete pr;
   return SSQA_OK;
@@ -299,6 +309,7 @@ int ssqa_batch_create(ssqa_problem pr, const ssqa_params_c* p, int trials, int r
   A(&b->d_jperp, size_t(p->sc) + 1);
   A(&b->d_E, size_t(b->g.ccols));
   if (eng == SSQA_ENGINE_SIMT) A(&b->d_S, b->slot_elems);
+  if (eng == SSQA_ENGINE_TCGEN05 && pr->q.fp4_ok) A(&b->d_sig4, b->slot_elems * b->nslots / 2);
   A(&b->d_best_e, size_t(T));
   A(&b->d_best_k, size_t(T));
   A(&b->d_reached, size_t(T));
@@ -315,6 +326,7 @@ int ssqa_batch_create(ssqa_problem pr, const ssqa_params_c* p, int trials, int r
   for (long c = 0; c <= p->sc; ++c) jp[size_t(c)] = jperp_at(c, *p);
   CU(cudaMemcpy(b->d_jperp, jp.data(), jp.size() * sizeof(double), cudaMemcpyHostToDevice));
   CU(cudaMemset(b->d_sig, 0, b->slot_elems * b->nslots));
+  if (b->d_sig4) CU(cudaMemset(b->d_sig4, 0, b->slot_elems * b->nslots / 2));
   CU(cudaMemset(b->d_acc, 0, b->slot_elems * sizeof(double)));
   CU(cudaEventCreate(&b->ev0));
   CU(cudaEventCreate(&b->ev1));
@@ -326,7 +338,7 @@ int ssqa_batch_destroy(ssqa_batch b) {
   if (!b) return SSQA_OK;
   cudaSetDevice(b->prob->device);
   cudaStreamSynchronize(b->prob->stream);
-  for (void* ptr : {(void*)b->d_sig, (void*)b->d_acc, (void*)b->d_seeds, (void*)b->d_jperp,
+  for (void* ptr : {(void*)b->d_sig, (void*)b->d_sig4, (void*)b->d_acc, (void*)b->d_seeds, (void*)b->d_jperp,
                     (void*)b->d_S, (void*)b->d_E, (void*)b->d_best_e, (void*)b->d_best_k,
                     (void*)b->d_reached, (void*)b->d_first_hit, (void*)b->d_cycles_used,
                     (void*)b->d_active, (void*)b->d_best_state, (void*)b->d_trace})
@@ -545,6 +557,8 @@ int ssqa_batch_read_lattice(ssqa_batch b, int trial, double* sigma, double* acc,
                             long* cycle) {
   if (!b) return set_err(SSQA_EINVAL, "null batch");
   if (trial < 0 || trial >= b->g.T) return set_err(SSQA_ERANGE, "trial index out of range");
+  if (b->lattice_stale)
+    return set_err(SSQA_EINVAL, "lattice state is not kept after a fused run; re-init first");
   CU(cudaSetDevice(b->prob->device));
   CU(cudaStreamSynchronize(b->prob->stream));
   const Geom& g = b->g;

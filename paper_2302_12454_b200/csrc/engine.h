@@ -36,6 +36,10 @@ struct Quantized {
   double offset = 0.0, scale = 1.0;  // scale = 2^-p
   std::vector<int8_t> J;             // [npad*npad]
   std::vector<int32_t> H;            // [npad]
+  // FP4 (e2m1) image of J' when every coupling is one of 0, +-1, +-2, +-3,
+  // +-4, +-6: two elements per byte, lower K index in the low nibble.
+  bool fp4_ok = false;
+  std::vector<uint8_t> J4;           // [npad * npad/2]
 };
 
 // Returns SSQA_OK or SSQA_EUNSUP with *why set.
@@ -50,6 +54,7 @@ struct ssqa_problem_s {
   cudaStream_t stream = nullptr;
   int8_t* d_J = nullptr;
   int32_t* d_H = nullptr;
+  uint8_t* d_J4 = nullptr;  // FP4 couplings (q.fp4_ok)
 };
 
 struct ssqa_batch_s {
@@ -68,6 +73,8 @@ struct ssqa_batch_s {
   long cycle = 0;
 
   int8_t* d_sig = nullptr;    // [nslots][ccols][npad]
+  uint8_t* d_sig4 = nullptr;  // FP4 spin slots [nslots][ccols][npad/2] (fused FP4 runs)
+  bool lattice_stale = false; // spins live in d_sig4 after an FP4 run
   double* d_acc = nullptr;    // [ccols][npad]
   uint64_t* d_seeds = nullptr;
   double* d_jperp = nullptr;  // [sc+1] jperp_schedule table

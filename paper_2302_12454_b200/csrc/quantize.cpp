@@ -76,6 +76,36 @@ int quantize(int n, const double* h, const double* J, double offset, Quantized* 
       if (std::abs(v) > q->max_abs_j) q->max_abs_j = std::abs(v);
     }
   }
+  // FP4 (e2m1) image: representable integers 0, 1, 2, 3, 4, 6 (+ sign).
+  {
+    auto code = [](int v) -> int {
+      const int a = v < 0 ? -v : v;
+      int c;
+      switch (a) {
+        case 0: c = 0; break;
+        case 1: c = 2; break;
+        case 2: c = 4; break;
+        case 3: c = 5; break;
+        case 4: c = 6; break;
+        case 6: c = 7; break;
+        default: return -1;
+      }
+      return c | (v < 0 ? 8 : 0);
+    };
+    q->fp4_ok = true;
+    q->J4.assign(size_t(q->npad) * (q->npad / 2), 0);
+    for (int i = 0; i < q->npad && q->fp4_ok; ++i) {
+      for (int j = 0; j < q->npad; ++j) {
+        const int c = code(q->J[size_t(i) * q->npad + j]);
+        if (c < 0) {
+          q->fp4_ok = false;
+          break;
+        }
+        q->J4[size_t(i) * (q->npad / 2) + j / 2] |= uint8_t(c << (4 * (j & 1)));
+      }
+    }
+    if (!q->fp4_ok) q->J4.clear();
+  }
   // |H'| < 2^29 keeps S + 2H' inside int32 for every n < 2^20.
   for (int i = 0; i < n; ++i) {
     double x = std::ldexp(h[i], p);

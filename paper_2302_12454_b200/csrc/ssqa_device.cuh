@@ -54,6 +54,17 @@ __device__ __forceinline__ uint32_t mix64_top5_pre(uint64_t x) {
   return (__umulhi(lo, c2lo) + lo * c2hi + hi * c2lo) >> 27;
 }
 
+// High 32 bits of the final splitmix product for an argument that already
+// includes mix64's "+= golden" (the top five bits decide the noise level;
+// comparing the whole word against t << 27 avoids the shift).
+__device__ __forceinline__ uint32_t mix64_top32_pre(uint64_t x) {
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+  x ^= x >> 27;
+  const uint32_t lo = uint32_t(x), hi = uint32_t(x >> 32);
+  const uint32_t c2lo = 0x133111ebu, c2hi = 0x94d049bbu;
+  return __umulhi(lo, c2lo) + lo * c2hi + hi * c2lo;
+}
+
 // Noise level of update_spins (annealer.cpp:277-278):
 //   u = (raw >> 11) * 2^-53;  u < 7/16 -> 0,  u < 23/32 -> -1,  else +1.
 // Both thresholds are exact multiples of 2^-5, so the comparison reduces to
@@ -124,11 +135,6 @@ __device__ __forceinline__ double update_fast(const UpdateConsts& c, double fiel
   return (s >= c.i0) ? c.hi_clamp : lo;
 }
 
-// Exact double of an integer field scaled by 2^-p (|v| < 2^53).
-__device__ __forceinline__ double scaled(long long v, double scale) {
-  return __dmul_rn(double(v), scale);
-}
-
 // Exact v * 2^-p for int32 v without the XU-pipe I2F.F64: the bit pattern
 // hi:(v ^ 2^31) with hi = exponent of 2^(52-p) encodes (2^52 + v + 2^31) *
 // 2^-p exactly; subtracting (2^52 + 2^31) * 2^-p (exact, same binade) leaves
@@ -150,6 +156,37 @@ __host__ __device__ inline I2D make_i2d(int p) {
 __device__ __forceinline__ double scaled_i32(int v, const I2D& c) {
   const double d = __hiloint2double(int(c.magic_hi), int(uint32_t(v) ^ 0x80000000u));
   return __dsub_rn(d, c.magic);
+}
+
+// Fast-path constants (valid when every parameter is finite and
+// n_rnd * 2^p is an integer NR): the noise joins the integer field
+// (field + n_rnd*nz == (S + H' + nz*NR) * 2^-p exactly), the coupling term
+// jperp * (+-1) is jperp with its sign bit flipped, and signs of finite,
+// never -0.0 accumulators come from the high word.
+struct FastConsts {
+  int nr;              // n_rnd * 2^p
+  uint32_t jp_hi, jp_lo;  // bits of jperp * 1.0
+  double i0, hi_clamp, lo_clamp;
+};
+
+template <bool BIDIR>
+__device__ __forceinline__ double update_fast2(const FastConsts& c, const I2D& i2d, int s_h1,
+                                               uint32_t top, int up, int dn, double acc) {
+  const int nzi = top < 0x70000000u ? 0 : (top < 0xB8000000u ? -c.nr : c.nr);
+  double input = scaled_i32(s_h1 + nzi, i2d);
+  input = __dadd_rn(input, __hiloint2double(int(c.jp_hi ^ (uint32_t(up) & 0x80000000u)),
+                                            int(c.jp_lo)));
+  if (BIDIR)
+    input = __dadd_rn(input, __hiloint2double(int(c.jp_hi ^ (uint32_t(dn) & 0x80000000u)),
+                                              int(c.jp_lo)));
+  const double s = __dadd_rn(acc, input);
+  const double lo = (s < c.lo_clamp) ? c.lo_clamp : s;
+  return (s >= c.i0) ? c.hi_clamp : lo;
+}
+
+// Exact double of an integer field scaled by 2^-p (|v| < 2^53).
+__device__ __forceinline__ double scaled(long long v, double scale) {
+  return __dmul_rn(double(v), scale);
 }
 
 }  // namespace ssqa_dev

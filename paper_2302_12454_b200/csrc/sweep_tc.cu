@@ -24,6 +24,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <string>
@@ -38,6 +39,13 @@ namespace {
 constexpr int kBM = 128;          // rows (spins i) per MMA tile
 constexpr int kBK = 128;          // K bytes per stage (one 128B swizzle row)
 constexpr int kCW = 8;  // columns per epilogue chunk (one tcgen05.ld .x8)
+#ifndef SSQA_ABL
+#define SSQA_ABL 0  // timing ablations (scripts/build_ablations.sh); 0 in the product
+#endif
+#ifndef SSQA_ENERGY_RED
+#define SSQA_ENERGY_RED 1  // 1: shuffle transpose-reduce, 0: per-column redux.sync
+#endif
+constexpr uint32_t kSfCol = 480;  // FP4 scale-factor TMEM columns [480, 512)
 constexpr int kMaxDelay = 30;
 constexpr int kMaxCols = 256;
 constexpr int kMaxTrialsPerTile = 256;
@@ -51,6 +59,7 @@ struct TcParams {
   int shift_p;
   const uint64_t* seeds;
   int8_t* sig;
+  uint8_t* sig_base;  // slots the kernel reads/writes (d_sig or the FP4 d_sig4)
   size_t slot_elems;
   int nslots, d;
   double* acc;
@@ -58,6 +67,9 @@ struct TcParams {
   double jperp_fixed;       // sweep mode
   double i0, n_rnd, alpha;
   int bidirectional;
+  int fast, nr;                 // fast epilogue (host-checked) and n_rnd * 2^p
+  int exp_flags;                // ablation experiments (SSQA_TC_EXP): 1 no epilogue math, 2 no MMA
+  double hi_clamp, lo_clamp;    // i0 - alpha, -i0 (formed on the host)
   long c_first, c_last;  // cycles handled: scans/updates for c in [c_first, c_last]
   long sc;               // update iff c < sc
   int run_mode;          // 1: scans + results; 0: plain sweeps (per-step API)
@@ -129,7 +141,7 @@ __device__ __noinline__ void mbar_wait_slow(uint32_t a, uint32_t parity) {
   const long long t0 = clock64();
   while (!mbar_try_sleep(a, parity)) {
     if (clock64() - t0 > 20000000000ll) {
-      if ((threadIdx.x & 31) == 0 || (threadIdx.x >> 5) < 3)
+      if ((threadIdx.x & 31) == 0)
         printf("k_sweep_tc watchdog: block %d warp %d lane %d stuck on mbarrier smem 0x%x "
                "parity %u\n",
                blockIdx.x, threadIdx.x >> 5, threadIdx.x & 31, a, parity);
@@ -211,6 +223,30 @@ __device__ __forceinline__ void mma_i8(uint32_t d_tmem, uint64_t a_desc, uint64_
       "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
 }
 
+// kind::mxf4 block-scaled MMA (A, B e2m1 packed, ue8m0 scales in TMEM).
+__host__ __device__ constexpr uint32_t idesc_mxf4(int M, int N) {
+  return (1u << 7) | (1u << 10) | (uint32_t(N >> 3) << 17) | (1u << 23) |
+         (uint32_t(M >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_mxf4(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                         uint32_t idesc, uint32_t accumulate, uint32_t sf_tmem) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%5], "
+      "p;\n\t}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate), "r"(sf_tmem));
+}
+
+__device__ __forceinline__ void tmem_st16_const(uint32_t taddr, uint32_t v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,"
+      "%1};" ::"r"(taddr),
+      "r"(v));
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile(
       "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
@@ -271,6 +307,31 @@ __host__ __device__ inline int ring_free(int cur, const int* phys, int d, int ns
 //   c_E    integer energy partials per TMEM lane quarter [4][NT]
 constexpr int kColBytes = 8 * 2 + 4 * 4;
 
+// warp sum without the compiler's divergence-check wrapper (all lanes converge)
+__device__ __forceinline__ int redux_add(int v) {
+  int r;
+  asm volatile("redux.sync.add.s32 %0, %1, 0xffffffff;" : "=r"(r) : "r"(v));
+  return r;
+}
+__device__ __forceinline__ void red_add_u32_if(uint32_t* p, uint32_t v, bool pred) {
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t"
+      "@q red.shared.add.u32 [%0], %1;\n\t}" ::"r"(smem_u32(p)),
+      "r"(v), "r"(int(pred))
+      : "memory");
+}
+__device__ __forceinline__ uint32_t ld_u8(const uint8_t* p) {
+  uint32_t v;
+  asm volatile("ld.global.u8 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ void st_u8_if(uint8_t* p, uint32_t v, bool pred) {
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t"
+      "@q st.global.u8 [%0], %1;\n\t}" ::"l"(p),
+      "r"(v), "r"(int(pred))
+      : "memory");
+}
 __device__ __forceinline__ int ld_s8(const int8_t* p) {
   int v;
   asm volatile("ld.global.s8 %0, [%1];" : "=r"(v) : "l"(p));
@@ -324,7 +385,8 @@ struct Layout {
   uint32_t a_bytes, b_bytes, acc_off, sig_off, ctl_off, tab_off, total;
 };
 
-__host__ __device__ inline Layout make_layout(int NT, int tpt, int stages, int nslot) {
+__host__ __device__ inline Layout make_layout(int NT, int tpt, int stages, int nslot,
+                                              int tile_row = kBM) {
   Layout L;
   L.stages = stages;
   L.nslot = nslot;
@@ -334,7 +396,7 @@ __host__ __device__ inline Layout make_layout(int NT, int tpt, int stages, int n
   L.acc_off = o;
   o += uint32_t(nslot) * kCW * kBM * 8;
   L.sig_off = o;
-  o += 2u * uint32_t(NT) * kBM;
+  o += 2u * uint32_t(NT) * uint32_t(tile_row);
   L.ctl_off = o;
   o += uint32_t((sizeof(SmemCtl) + 127) / 128 * 128);
   L.tab_off = o;
@@ -345,26 +407,32 @@ __host__ __device__ inline Layout make_layout(int NT, int tpt, int stages, int n
 
 // Per-thread row context for one row tile of the epilogue.
 struct EpiRow {
-  uint64_t acc_i, dst_i, cur_i;  // &acc[i], &sigma_dst[i], &sigma_cur[i] (+ column offset)
-  const int8_t* st_i;            // delayed-spin tile, row il
+  uint64_t acc_i;           // &acc[i] (+ column offset * 8)
+  uint64_t dst_i, cur_i;    // int8 slots: &sigma[i]; FP4 slots: &sigma4[i/2] (+ offset/2)
+  const uint8_t* st_i;      // delayed-spin tile, row il (FP4: byte il/2)
   int h1, h2;
-  uint64_t iG;                   // i * golden
-  uint64_t pol_stream;           // L2 evict_first policy for the accumulator stream
-  bool w_row;                    // spin row exists (i < n)
+  uint32_t nib_shift;       // FP4: 4 * (i & 1)
+  uint64_t iG;              // i * golden
+  uint64_t pol_stream;      // L2 evict_first policy for the accumulator stream
+  bool w_row;               // spin row exists (i < n)
 };
 
 // All of this warp's kCW-column chunks of one row tile: TMEM fields,
 // staged accumulators, delayed neighbours -> exact update, predicated
-// stores, per-column warp energy sums.  BIDIR / SIGACC are hoisted out of
-// the column loop (SIGACC: sigma(c) = sign(acc(c)) instead of a load).
-template <bool BIDIR, bool SIGACC>
+// stores, per-column warp energy sums.  Template switches are hoisted out of
+// the column loop:
+//   BIDIR   couple to k-1 as well as k+1
+//   SIGACC  sigma(c) = sign(acc(c)) instead of a load (all but the first sweep)
+//   FAST    host-checked fast arithmetic (update_fast2), int32 energy partials
+//   F4      FP4 operands: fp32 fields in TMEM, spins stored as e2m1 nibbles
+template <bool BIDIR, bool SIGACC, bool FAST, bool F4>
 __device__ __forceinline__ void epi_chunks(const EpiRow& er, const UpdateConsts& uc,
-                                           const I2D& i2d, SmemCtl* ctl,
-                                           const double* acc_ring, const int* c_flag,
-                                           const uint32_t* c_off, const uint32_t* c_nbr,
-                                           const uint64_t* c_base, long long* q_sum,
-                                           uint32_t trow, int sub, int nsubs, int nchunk,
-                                           int nps, uint32_t cnt0, int il, int lane) {
+                                           const FastConsts& fc, const I2D& i2d, SmemCtl* ctl,
+                                           const double* acc_ring, const uint32_t* c_off,
+                                           const uint32_t* c_nbr, const uint64_t* c_base,
+                                           long long* q_sum, uint32_t trow, int sub,
+                                           int nsubs, int nchunk, int nps, uint32_t cnt0, int il,
+                                           int lane) {
   uint32_t cnt = cnt0;
   for (int ch = sub; ch < nchunk; ch += nsubs, ++cnt) {
     const int cb = ch * kCW;
@@ -378,30 +446,112 @@ __device__ __forceinline__ void epi_chunks(const EpiRow& er, const UpdateConsts&
 #pragma unroll
     for (int j = 0; j < kCW; ++j) {
       const int cl = cb + j;
-      const int fl = c_flag[cl];
+      const uint32_t nb = c_nbr[cl];  // up | dn << 16 (tile-row units), bit 15 live, bit 31 update
       const uint32_t coff = c_off[cl];
-      const uint32_t nb = c_nbr[cl];
       const double a_old = ab[j * kBM];
-      int sg;
-      if (SIGACC) sg = a_old >= 0.0 ? 1 : -1;
-      else sg = ld_s8(reinterpret_cast<const int8_t*>(er.cur_i + coff));
-      const int S = v[j];
-      ep[j] = (fl & 1) ? sg * (S + er.h2) : 0;
-      const int up = er.st_i[nb & 0xffffu];
-      const int dn = BIDIR ? int(er.st_i[nb >> 16]) : 0;
-      const double field = scaled_i32(S + er.h1, i2d);
-      const uint32_t t5 = mix64_top5_pre(c_base[cl] + er.iG);
-      const double nv = update_fast(uc, field, t5, up, dn, BIDIR, a_old);
-      const bool w = (fl & 2) && er.w_row;
-      st_f64_if(reinterpret_cast<double*>(er.acc_i + uint64_t(coff) * 8u), nv, w, er.pol_stream);
-      st_s8_if(reinterpret_cast<int8_t*>(er.dst_i + uint64_t(coff)), nv >= 0.0 ? 1 : -1, w);
+      // FP4: the fp32 accumulator holds a small exact integer (|S| < 2^22);
+      // its bits after adding 1.5*2^23 are 0x4B400000 + S, and the bias is
+      // folded into the per-row constants h1/h2 (EpiRow).
+      const int S = F4 ? __float_as_int(__int_as_float(v[j]) + 12582912.0f) : v[j];
+      const int s2 = S + er.h2;
+      int ep_j;
+      if (SIGACC && FAST) {
+        const int m = __double2hiint(a_old) >> 31;  // sign of a finite, never -0.0 value
+        ep_j = (s2 ^ m) - m;
+      } else {
+        int sg;
+        if (SIGACC) {
+          sg = a_old >= 0.0 ? 1 : -1;
+        } else if (F4) {
+          const uint32_t bc = ld_u8(reinterpret_cast<const uint8_t*>(er.cur_i + (coff >> 1)));
+          sg = ((bc >> er.nib_shift) & 8u) ? -1 : 1;
+        } else {
+          sg = ld_s8(reinterpret_cast<const int8_t*>(er.cur_i + coff));
+        }
+        ep_j = sg * s2;
+      }
+      ep[j] = (nb & 0x8000u) ? ep_j : 0;
+      int up, dn = 0;
+      if (F4 && FAST) {
+        // update_fast2 only reads the sign bit: move the nibble's bit 3 there
+        up = int(uint32_t(er.st_i[nb & 0x7fffu]) << (28u - er.nib_shift));
+        if (BIDIR) dn = int(uint32_t(er.st_i[(nb >> 16) & 0x7fffu]) << (28u - er.nib_shift));
+      } else if (F4) {
+        const uint32_t bu = er.st_i[nb & 0x7fffu];
+        up = ((bu >> er.nib_shift) & 8u) ? -1 : 1;
+        if (BIDIR) dn = ((uint32_t(er.st_i[(nb >> 16) & 0x7fffu]) >> er.nib_shift) & 8u) ? -1 : 1;
+      } else {
+        up = int8_t(er.st_i[nb & 0x7fffu]);
+        if (BIDIR) dn = int8_t(er.st_i[(nb >> 16) & 0x7fffu]);
+      }
+      double nv;
+      uint32_t neg;  // 1 when the new spin is -1
+      if (FAST) {
+        const uint32_t top = mix64_top32_pre(c_base[cl] + er.iG);
+        nv = update_fast2<BIDIR>(fc, i2d, S + er.h1, top, up, dn, a_old);
+        neg = uint32_t(__double2hiint(nv)) >> 31;
+      } else {
+        const double field = scaled_i32(S + er.h1, i2d);
+        const uint32_t t5 = mix64_top5_pre(c_base[cl] + er.iG);
+        nv = update_fast(uc, field, t5, up, dn, BIDIR, a_old);
+        neg = nv >= 0.0 ? 0u : 1u;
+      }
+      const bool w = (nb & 0x80000000u) && er.w_row;
+      if (!(SSQA_ABL & 64))
+        st_f64_if(reinterpret_cast<double*>(er.acc_i + uint64_t(coff) * 8u), nv, w, er.pol_stream);
+      if (SSQA_ABL & 32) {
+      } else if (F4) {
+        // e2m1 +1 = 0x2, -1 = 0xA; even lanes store the byte of rows (i, i+1)
+        const uint32_t nib = 2u | (neg << 3);
+        const uint32_t hi = __shfl_xor_sync(0xffffffffu, nib, 1);
+        st_u8_if(reinterpret_cast<uint8_t*>(er.dst_i + (coff >> 1)), nib | (hi << 4),
+                 w && !(lane & 1));
+      } else {
+        st_s8_if(reinterpret_cast<int8_t*>(er.dst_i + uint64_t(coff)), int(1 - 2 * int(neg)), w);
+      }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&ctl->aempty[slot]);
+    if (SSQA_ABL & 16) {
+    } else if (FAST && (SSQA_ENERGY_RED == 1)) {
+      // transpose-reduce the 8 column partials across the warp with shuffles:
+      // after the five butterfly stages lane L holds the warp sum of column
+      // (L >> 2) & 7; lanes with L % 4 == 0 add it to the quarter's partial.
+      int a4[4], a2[2], a1;
+      const bool b16 = lane & 16, b8 = lane & 8, b4 = lane & 4;
 #pragma unroll
-    for (int j = 0; j < kCW; ++j) {
-      const int wsum = __reduce_add_sync(0xffffffffu, ep[j]);
-      if (lane == 0) q_sum[cb + j] += wsum;
+      for (int k = 0; k < 4; ++k) {
+        const int keep = b16 ? ep[k + 4] : ep[k];
+        const int send = b16 ? ep[k] : ep[k + 4];
+        a4[k] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+      }
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const int keep = b8 ? a4[k + 2] : a4[k];
+        const int send = b8 ? a4[k] : a4[k + 2];
+        a2[k] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+      }
+      {
+        const int keep = b4 ? a2[1] : a2[0];
+        const int send = b4 ? a2[0] : a2[1];
+        a1 = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+      }
+      a1 += __shfl_xor_sync(0xffffffffu, a1, 2);
+      a1 += __shfl_xor_sync(0xffffffffu, a1, 1);
+      // lane bits 4,3,2 select column bits 2,1,0
+      const int col = (b16 ? 4 : 0) + (b8 ? 2 : 0) + (b4 ? 1 : 0);
+      red_add_u32_if(reinterpret_cast<uint32_t*>(q_sum) + cb + col, uint32_t(a1),
+                     (lane & 3) == 0);
+    } else {
+#pragma unroll
+      for (int j = 0; j < kCW; ++j) {
+        const int wsum = redux_add(ep[j]);
+        if (FAST) {
+          red_add_u32_if(reinterpret_cast<uint32_t*>(q_sum) + cb + j, uint32_t(wsum), lane == 0);
+        } else {
+          if (lane == 0) q_sum[cb + j] += wsum;
+        }
+      }
     }
   }
 }
@@ -415,10 +565,10 @@ __device__ __forceinline__ void epi_chunks(const EpiRow& er, const UpdateConsts&
       P.dbg[(size_t(role) * P.dbg_rts + (rtg)) * 2 + (which)] = clock64();            \
   } while (0)
 
-// Warp roles: 0 operand TMA producer, 1 TMEM allocator + MMA issuer,
-// 2 state loader (TMA of accumulator chunks and delayed-spin tiles),
-// 3 .. 3+EPI-1 epilogue (EPI/4 warps per TMEM lane quarter).
-template <int EPI>
+// Warp roles: 0 .. EPI-1 epilogue (EPI/4 warps per TMEM lane quarter),
+// EPI operand TMA producer, EPI+1 TMEM allocator + MMA issuer, EPI+2 state
+// loader (TMA of accumulator chunks and delayed-spin tiles).
+template <int EPI, bool F4>
 __global__ void __launch_bounds__(32 * (3 + EPI), 1)
     k_sweep_tc(const __grid_constant__ CUtensorMap tmJ, const __grid_constant__ CUtensorMap tmS,
                const __grid_constant__ CUtensorMap tmSe, const __grid_constant__ CUtensorMap tmA,
@@ -429,12 +579,13 @@ __global__ void __launch_bounds__(32 * (3 + EPI), 1)
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const Geom& g = P.g;
   const int NT = g.tile_cols;
-  const Layout L = make_layout(NT, g.tpt, P.stages, P.nslot);
+  constexpr int kTileRow = F4 ? kBM / 2 : kBM;  // bytes per spin-tile row (128 spins)
+  const Layout L = make_layout(NT, g.tpt, P.stages, P.nslot, kTileRow);
   const int stages = L.stages, nslot = L.nslot;
   uint8_t* sA = smem;
   uint8_t* sB = smem + size_t(stages) * L.a_bytes;
   double* acc_ring = reinterpret_cast<double*>(smem + L.acc_off);  // [nslot][kCW][kBM]
-  int8_t* sig_tiles = reinterpret_cast<int8_t*>(smem + L.sig_off);  // [2][NT][kBM]
+  uint8_t* sig_tiles = smem + L.sig_off;  // [2][NT][kTileRow] delayed-spin tiles
   SmemCtl* ctl = reinterpret_cast<SmemCtl*>(smem + L.ctl_off);
   uint8_t* tabs = smem + L.tab_off;
   uint64_t* c_key = reinterpret_cast<uint64_t*>(tabs);
@@ -447,10 +598,16 @@ __global__ void __launch_bounds__(32 * (3 + EPI), 1)
   TrialTab* trials = reinterpret_cast<TrialTab*>(c_flag + NT + (NT & 1));
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // The single-lane pipeline roles take the highest warp indices: the warp
+  // scheduler favours higher warp ids, so the TMA producer, MMA issuer and
+  // state loader are never starved by the EPI busy epilogue warps.
+  constexpr int kWarpProducer = EPI, kWarpMma = EPI + 1, kWarpLoader = EPI + 2;
   const int tile = blockIdx.x;
   const int col0 = tile * NT;
-  const int ntl = min(g.tpt, g.T - tile * g.tpt);
-  const int NRT = g.npad / kBM, NKC = g.npad / kBK;
+  const int ntl = max(0, min(g.tpt, g.T - tile * g.tpt));
+  // one stage = 128 bytes of K per row: 128 int8 or 256 e2m1 couplings/spins
+  // (an FP4 row of npad = 128 is a partial chunk: TMA zero-fills the rest)
+  const int NRT = g.npad / kBM, NKC = F4 ? (g.npad + 2 * kBK - 1) / (2 * kBK) : g.npad / kBK;
   const int nchunk = NT / kCW;
   const int acc_cols = NT;
   constexpr int nsubs = EPI / 4;         // epilogue subgroups (4 warps each)
@@ -478,16 +635,16 @@ __global__ void __launch_bounds__(32 * (3 + EPI), 1)
     for (int q = 0; q <= P.d; ++q) ctl->ring_phys[q] = P.ring_phys[q];
     ctl->any_active = 1;
   }
-  if (warp == 0 && lane == 0) {
+  if (warp == kWarpProducer && lane == 0) {
     prefetch_tmap(&tmJ);
     prefetch_tmap(&tmS);
   }
-  if (warp == 2 && lane == 0) {
+  if (warp == kWarpLoader && lane == 0) {
     prefetch_tmap(&tmSe);
     prefetch_tmap(&tmA);
   }
-  if (warp == 1) {
-    const uint32_t ncols = (2 * acc_cols <= 256) ? 256u : 512u;
+  if (warp == kWarpMma) {
+    const uint32_t ncols = (F4 || 2 * acc_cols > 256) ? 512u : 256u;
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(&ctl->tmem_base)),
                  "r"(ncols));
@@ -500,7 +657,7 @@ __global__ void __launch_bounds__(32 * (3 + EPI), 1)
     const int kup = (ci.k + 1 == g.R) ? 0 : ci.k + 1;
     const int kdn = (ci.k == 0) ? g.R - 1 : ci.k - 1;
     c_off[c] = uint32_t(col0 + c) * uint32_t(g.npad);
-    c_nbr[c] = uint32_t(tl * g.R + kup) * kBM | (uint32_t(tl * g.R + kdn) * kBM << 16);
+    c_nbr[c] = uint32_t(tl * g.R + kup) * kTileRow | (uint32_t(tl * g.R + kdn) * kTileRow << 16);
     c_kt[c] = ci.k | (tl << 16);
     c_flag[c] = ci.live ? 1 : 0;
   }
@@ -523,7 +680,16 @@ __global__ void __launch_bounds__(32 * (3 + EPI), 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = ctl->tmem_base;
-  const uint32_t idesc = idesc_i8(kBM, NT);
+  const uint32_t idesc = F4 ? idesc_mxf4(kBM, NT) : idesc_i8(kBM, NT);
+  const uint32_t sf_tmem = tmem_base + kSfCol;  // unit (2^0) block scales for FP4
+  if (F4) {
+    // every ue8m0 scale factor is 127 = 2^0: fill the whole scale region
+    if (warp < 4) tmem_st16_const(tmem_base + (uint32_t(warp * 32) << 16) + kSfCol, 0x7F7F7F7Fu),
+                  tmem_st16_const(tmem_base + (uint32_t(warp * 32) << 16) + kSfCol + 16, 0x7F7F7F7Fu);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+  }
 
   uint32_t it = 0;      // operand stage sequence (producer == MMA)
   uint32_t acc_it = 0;  // accumulator / row-tile sequence (MMA == loader == epilogue)
@@ -535,7 +701,7 @@ __global__ void __launch_bounds__(32 * (3 + EPI), 1)
     const int dst = do_update ? ring_free(cur, ctl->ring_phys, P.d, P.nslots) : cur;
     if (!ctl->any_active) break;
 
-    if (warp == 0) {
+    if (warp == kWarpProducer) {
       // ===== operand TMA producer =====
       if (lane == 0) {
         const int yS = cur * g.ccols + col0;
@@ -553,7 +719,7 @@ __global__ void __launch_bounds__(32 * (3 + EPI), 1)
         }
       }
       __syncwarp();
-    } else if (warp == 1) {
+    } else if (warp == kWarpMma) {
       // ===== MMA issuer =====
       if (lane == 0) {
         for (int rt = 0; rt < NRT; ++rt, ++acc_it) {
@@ -570,10 +736,16 @@ __global__ void __launch_bounds__(32 * (3 + EPI), 1)
             tc_fence_after();
             const uint32_t a0 = smem_u32(sA + size_t(s) * L.a_bytes);
             const uint32_t b0 = smem_u32(sB + size_t(s) * L.b_bytes);
+            if (!(P.exp_flags & 2)) {
 #pragma unroll
-            for (int k = 0; k < kBK / 32; ++k) {
-              mma_i8(d_tmem, umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32), idesc,
-                     (kc | k) ? 1u : 0u);
+              for (int k = 0; k < kBK / 32; ++k) {
+                if (F4)
+                  mma_mxf4(d_tmem, umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32),
+                           idesc, (kc | k) ? 1u : 0u, sf_tmem);
+                else
+                  mma_i8(d_tmem, umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32),
+                         idesc, (kc | k) ? 1u : 0u);
+              }
             }
             mma_commit(&ctl->empty[s]);
           }
@@ -582,7 +754,7 @@ __global__ void __launch_bounds__(32 * (3 + EPI), 1)
         }
       }
       __syncwarp();
-    } else if (warp == 2) {
+    } else if (warp == kWarpLoader) {
       // ===== state loader: delayed-spin tile + accumulator chunks =====
       if (lane == 0) {
         const int ySrc = src * g.ccols + col0;
@@ -592,8 +764,9 @@ __global__ void __launch_bounds__(32 * (3 + EPI), 1)
           const uint32_t sph = (acc_it >> 1) & 1;
           mbar_wait(&ctl->sempty[sb], sph ^ 1);
           DBG_STAMP(1, acc_it, 0);
-          mbar_expect_tx(&ctl->sfull[sb], uint32_t(NT) * kBM);
-          tma_load_2d(&tmSe, &ctl->sfull[sb], sig_tiles + size_t(sb) * NT * kBM, rt * kBM, ySrc);
+          mbar_expect_tx(&ctl->sfull[sb], uint32_t(NT) * kTileRow);
+          tma_load_2d(&tmSe, &ctl->sfull[sb], sig_tiles + size_t(sb) * NT * kTileRow,
+                      rt * kTileRow, ySrc);
           // chunk ch belongs to epilogue subgroup ch % nsubs and lands in that
           // subgroup's own ring (slots [sub*nps, sub*nps + nps)): each slot is
           // consumed, in order, by a single subgroup, so no consumer can ever
@@ -614,7 +787,7 @@ __global__ void __launch_bounds__(32 * (3 + EPI), 1)
       __syncwarp();
     } else {
       // ===== epilogue =====
-      const int ew = warp - 3;  // 0 .. EPI-1
+      const int ew = warp;  // 0 .. EPI-1
       const int q = warp & 3;   // TMEM lane quarter this warp may access
       const int sub = ew >> 2;
       constexpr int kSubs = EPI / 4;
@@ -622,9 +795,9 @@ __global__ void __launch_bounds__(32 * (3 + EPI), 1)
         const int k = c_kt[cl] & 0xffff, tl = c_kt[cl] >> 16;
         // key + spin_counter(c, k, 0) * golden, plus mix64's initial += golden
         c_base[cl] = c_key[cl] + spin_counter(uint64_t(c), uint32_t(k), 0) * kGolden + kGolden;
-        const int live = c_flag[cl] & 1;
-        const int upd = live && do_update && (!P.run_mode || trials[tl].active);
-        c_flag[cl] = live | (upd << 1);
+        const uint32_t live = uint32_t(c_flag[cl] & 1);
+        const uint32_t upd = live && do_update && (!P.run_mode || trials[tl].active);
+        c_nbr[cl] = (c_nbr[cl] & 0x7fff7fffu) | (live << 15) | (upd << 31);
         for (int qq = 0; qq < 4; ++qq) c_E[qq * NT + cl] = 0;
       }
       long long* q_sum = c_E + q * NT;
@@ -633,12 +806,22 @@ __global__ void __launch_bounds__(32 * (3 + EPI), 1)
       const UpdateConsts uc = make_consts(P.n_rnd, jperp, P.i0, P.alpha);
       const I2D i2d = make_i2d(P.shift_p);
       const bool bidir = P.bidirectional != 0;
+      const bool fast = P.fast != 0;
+      FastConsts fc;
+      fc.nr = P.nr;
+      fc.jp_hi = uint32_t(__double2hiint(uc.jp_pos));
+      fc.jp_lo = uint32_t(__double2loint(uc.jp_pos));
+      fc.i0 = P.i0;
+      fc.hi_clamp = P.hi_clamp;
+      fc.lo_clamp = P.lo_clamp;
       // sigma(c) is sign(acc(c)) once this kernel has updated the lattice;
       // on the first cycle it comes from the spin slot (init / written state).
       const bool sig_from_acc = c > P.c_first;
       const uint64_t pol_first = policy_evict_first();
-      const int8_t* sig_cur = P.sig + size_t(cur) * P.slot_elems;
-      int8_t* sig_dst = P.sig + size_t(dst) * P.slot_elems;
+      // spin slots: int8 [ccols][npad], or FP4 nibbles [ccols][npad/2]
+      const size_t slot_bytes = F4 ? P.slot_elems / 2 : P.slot_elems;
+      const uint8_t* sig_cur = P.sig_base + size_t(cur) * slot_bytes;
+      uint8_t* sig_dst = P.sig_base + size_t(dst) * slot_bytes;
       for (int rt = 0; rt < NRT; ++rt, ++acc_it) {
         const int buf = acc_it & 1;
         const uint32_t aph = (acc_it >> 1) & 1;
@@ -649,41 +832,62 @@ __global__ void __launch_bounds__(32 * (3 + EPI), 1)
         const int h2 = 2 * h1;
         const uint64_t iG = uint64_t(i) * kGolden;
         const uint32_t trow = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(buf * acc_cols);
-        const int8_t* stile = sig_tiles + size_t(buf) * NT * kBM;
-        if (warp == 3) DBG_STAMP(2, acc_it, 0);
+        const uint8_t* stile = sig_tiles + size_t(buf) * NT * kTileRow;
+        if (warp == 0) DBG_STAMP(2, acc_it, 0);
         mbar_wait(&ctl->sfull[buf], aph);
         mbar_wait(&ctl->tfull[buf], aph);
         tc_fence_after();
-        if (warp == 3) DBG_STAMP(3, acc_it, 0);
+        if (warp == 0) DBG_STAMP(3, acc_it, 0);
         EpiRow er;
         er.acc_i = reinterpret_cast<uint64_t>(P.acc + i);
-        er.dst_i = reinterpret_cast<uint64_t>(sig_dst + i);
-        er.cur_i = reinterpret_cast<uint64_t>(sig_cur + i);
-        er.st_i = stile + il;
-        er.h1 = h1;
-        er.h2 = h2;
+        er.dst_i = reinterpret_cast<uint64_t>(sig_dst + (F4 ? i / 2 : i));
+        er.cur_i = reinterpret_cast<uint64_t>(sig_cur + (F4 ? i / 2 : i));
+        er.st_i = stile + (F4 ? il / 2 : il);
+        er.nib_shift = 4u * uint32_t(i & 1);
+        er.h1 = F4 ? h1 - 0x4B400000 : h1;
+        er.h2 = F4 ? h2 - 0x4B400000 : h2;
         er.iG = iG;
         er.pol_stream = pol_first;
         er.w_row = row_live;
         const uint32_t cnt0 = acc_it * uint32_t(chunks_of(sub));
-        if (bidir) {
-          if (sig_from_acc)
-            epi_chunks<true, true>(er, uc, i2d, ctl, acc_ring, c_flag, c_off, c_nbr, c_base, q_sum,
-                                   trow, sub, kSubs, nchunk, nps, cnt0, il, lane);
-          else
-            epi_chunks<true, false>(er, uc, i2d, ctl, acc_ring, c_flag, c_off, c_nbr, c_base, q_sum,
-                                    trow, sub, kSubs, nchunk, nps, cnt0, il, lane);
+#define SSQA_EPI(B, S, F)                                                                  \
+  epi_chunks<B, S, F, F4>(er, uc, fc, i2d, ctl, acc_ring, c_off, c_nbr, c_base, q_sum, trow, \
+                          sub, kSubs, nchunk, nps, cnt0, il, lane)
+        if (P.exp_flags & 1) {
+          // ablation: consume the chunks without the update arithmetic
+          uint32_t cnt = cnt0;
+          for (int ch = sub; ch < nchunk; ch += kSubs, ++cnt) {
+            const int slot = sub * nps + int(cnt % uint32_t(nps));
+            int32_t v[kCW];
+            tmem_ld8(trow + uint32_t(ch * kCW), v);
+            mbar_wait(&ctl->afull[slot], (cnt / uint32_t(nps)) & 1);
+            const double* ab = acc_ring + size_t(slot) * kCW * kBM + il;
+#pragma unroll
+            for (int j = 0; j < kCW; ++j) {
+              const uint32_t coff = c_off[ch * kCW + j];
+              st_f64_if(reinterpret_cast<double*>(er.acc_i + uint64_t(coff) * 8u),
+                        ab[j * kBM] + double(v[j]), false, pol_first);
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&ctl->aempty[slot]);
+          }
+        } else if (fast && sig_from_acc) {
+          if (bidir) SSQA_EPI(true, true, true);
+          else SSQA_EPI(false, true, true);
+        } else if (fast) {
+          if (bidir) SSQA_EPI(true, false, true);
+          else SSQA_EPI(false, false, true);
+        } else if (sig_from_acc) {
+          if (bidir) SSQA_EPI(true, true, false);
+          else SSQA_EPI(false, true, false);
         } else {
-          if (sig_from_acc)
-            epi_chunks<false, true>(er, uc, i2d, ctl, acc_ring, c_flag, c_off, c_nbr, c_base,
-                                    q_sum, trow, sub, kSubs, nchunk, nps, cnt0, il, lane);
-          else
-            epi_chunks<false, false>(er, uc, i2d, ctl, acc_ring, c_flag, c_off, c_nbr, c_base,
-                                     q_sum, trow, sub, kSubs, nchunk, nps, cnt0, il, lane);
+          if (bidir) SSQA_EPI(true, false, false);
+          else SSQA_EPI(false, false, false);
         }
+#undef SSQA_EPI
         tc_fence_before();
         __syncwarp();
-        if (warp == 3) DBG_STAMP(2, acc_it, 1);
+        if (warp == 0) DBG_STAMP(2, acc_it, 1);
         if (lane == 0) {
           mbar_arrive(&ctl->tempty[buf]);
           mbar_arrive(&ctl->sempty[buf]);
@@ -694,8 +898,8 @@ __global__ void __launch_bounds__(32 * (3 + EPI), 1)
     __syncthreads();
 
     // ===== scan (annealer.cpp:327-345), one warp per trial =====
-    if (P.run_mode && warp >= 3) {
-      for (int t = warp - 3; t < ntl; t += EPI) {
+    if (P.run_mode && warp < EPI) {
+      for (int t = warp; t < ntl; t += EPI) {
         TrialTab& tt = trials[t];
         if (!tt.active) continue;
         if (lane == 0) {
@@ -704,7 +908,9 @@ __global__ void __launch_bounds__(32 * (3 + EPI), 1)
           const int tg = tile * g.tpt + t;
           for (int k = 0; k < g.R; ++k) {
             long long ep = 0;
-            for (int qq = 0; qq < 4; ++qq) ep += c_E[qq * NT + t * g.R + k];
+            for (int qq = 0; qq < 4; ++qq)
+              ep += P.fast ? (long long)reinterpret_cast<const int*>(c_E + qq * NT)[t * g.R + k]
+                           : c_E[qq * NT + t * g.R + k];
             const double ek = __dadd_rn(__dmul_rn(-0.5, scaled(ep, P.scale)), P.offset);
             if (ek < be) {
               be = ek;
@@ -727,10 +933,16 @@ __global__ void __launch_bounds__(32 * (3 + EPI), 1)
         __syncwarp();
         const int improved = tt.improved;
         if (improved >= 0) {
-          const int8_t* sp = P.sig + size_t(cur) * P.slot_elems +
-                             size_t(col0 + t * g.R + improved) * g.npad;
           int8_t* dstp = P.best_state + size_t(tile * g.tpt + t) * g.n;
-          for (int i = lane; i < g.n; i += 32) dstp[i] = sp[i];
+          const size_t colg = size_t(col0 + t * g.R + improved);
+          if (F4) {
+            const uint8_t* sp = P.sig_base + size_t(cur) * (P.slot_elems / 2) + colg * (g.npad / 2);
+            for (int i = lane; i < g.n; i += 32)
+              dstp[i] = ((sp[i >> 1] >> (4 * (i & 1))) & 8) ? -1 : 1;
+          } else {
+            const int8_t* sp = P.sig + size_t(cur) * P.slot_elems + colg * g.npad;
+            for (int i = lane; i < g.n; i += 32) dstp[i] = sp[i];
+          }
         }
         __syncwarp();
       }
@@ -761,8 +973,8 @@ __global__ void __launch_bounds__(32 * (3 + EPI), 1)
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) {
-    const uint32_t ncols = (2 * acc_cols <= 256) ? 256u : 512u;
+  if (warp == kWarpMma) {
+    const uint32_t ncols = (F4 || 2 * acc_cols > 256) ? 512u : 256u;
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
                  "r"(ncols));
   }
@@ -806,51 +1018,70 @@ bool make_map(CUtensorMap* m, void* base, CUtensorMapDataType dt, uint32_t esize
 // Operand stages and per-subgroup state-ring depth inside ~220 KB: prefer
 // >= 2 ring slots per subgroup (so the loader runs a chunk ahead), then as
 // many operand stages (<= 4) as fit.
-Layout pick_layout(int NT, int tpt, int nsubs) {
+Layout pick_layout(int NT, int tpt, int nsubs, int tile_row) {
   const uint32_t cap = 220 * 1024;
   for (int nps = 3; nps >= 1; --nps)
     for (int stages = 4; stages >= 2; --stages) {
       if (nps * nsubs > 16) continue;
-      Layout L = make_layout(NT, tpt, stages, nps * nsubs);
+      Layout L = make_layout(NT, tpt, stages, nps * nsubs, tile_row);
       if (L.total <= cap && (nps >= 2 || stages >= 2)) {
         if (nps >= 2 && stages < 3) continue;  // rather fewer slots than < 3 stages
         return L;
       }
     }
-  return make_layout(NT, tpt, 2, nsubs);
+  return make_layout(NT, tpt, 2, nsubs, tile_row);
 }
 
 constexpr int kDefaultEpi = 12;
 
-template <int EPI>
+template <int EPI, bool F4>
 cudaError_t launch_variant(int grid, int smem, cudaStream_t st, const CUtensorMap* maps,
                            const TcParams& P) {
-  cudaError_t e = cudaFuncSetAttribute(k_sweep_tc<EPI>,
+  cudaError_t e = cudaFuncSetAttribute(k_sweep_tc<EPI, F4>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  k_sweep_tc<EPI><<<grid, 32 * (3 + EPI), smem, st>>>(maps[0], maps[1], maps[2], maps[3], P);
+  k_sweep_tc<EPI, F4><<<grid, 32 * (3 + EPI), smem, st>>>(maps[0], maps[1], maps[2], maps[3], P);
   return cudaSuccess;
 }
 
-int launch(ssqa_batch_s* b, TcParams& P) {
+// int8 spin slot -> FP4 (e2m1) slot: +1 -> 0x2, -1 -> 0xA, 0 -> 0x0.
+__global__ void k_pack_fp4(const int8_t* __restrict__ src, uint8_t* __restrict__ dst,
+                           size_t nbytes) {
+  for (size_t b = blockIdx.x * size_t(blockDim.x) + threadIdx.x; b < nbytes;
+       b += size_t(gridDim.x) * blockDim.x) {
+    auto code = [](int v) { return v > 0 ? 0x2u : (v < 0 ? 0xAu : 0x0u); };
+    dst[b] = uint8_t(code(src[2 * b]) | (code(src[2 * b + 1]) << 4));
+  }
+}
+
+int launch(ssqa_batch_s* b, TcParams& P, bool f4) {
   const Geom& g = b->g;
   CUtensorMap maps[4];
   const uint64_t srows = uint64_t(b->nslots) * g.ccols;
-  if (!make_map(&maps[0], b->prob->d_J, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, g.npad, g.npad, kBK,
-                kBM, CU_TENSOR_MAP_SWIZZLE_128B) ||
-      !make_map(&maps[1], b->d_sig, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, g.npad, srows, kBK,
+  // FP4 rows are npad/2 bytes (two e2m1 values per byte)
+  const uint64_t row_bytes = f4 ? uint64_t(g.npad) / 2 : uint64_t(g.npad);
+  void* Jsrc = f4 ? static_cast<void*>(b->prob->d_J4) : static_cast<void*>(b->prob->d_J);
+  void* Ssrc = f4 ? static_cast<void*>(b->d_sig4) : static_cast<void*>(b->d_sig);
+  const uint32_t tile_row = f4 ? kBM / 2 : kBM;
+  P.sig_base = static_cast<uint8_t*>(Ssrc);
+  if (!make_map(&maps[0], Jsrc, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, row_bytes, g.npad, kBK, kBM,
+                CU_TENSOR_MAP_SWIZZLE_128B) ||
+      !make_map(&maps[1], Ssrc, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, row_bytes, srows, kBK,
                 g.tile_cols, CU_TENSOR_MAP_SWIZZLE_128B) ||
-      !make_map(&maps[2], b->d_sig, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, g.npad, srows, kBM,
+      !make_map(&maps[2], Ssrc, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, row_bytes, srows, tile_row,
                 g.tile_cols, CU_TENSOR_MAP_SWIZZLE_NONE) ||
       !make_map(&maps[3], b->d_acc, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, g.npad, g.ccols, kBM,
                 kCW, CU_TENSOR_MAP_SWIZZLE_NONE)) {
     g_tc_err = "cuTensorMapEncodeTiled failed";
     return SSQA_ECUDA;
   }
-  const char* env = getenv("SSQA_TC_EPI");
-  int epi = env ? atoi(env) : kDefaultEpi;
-  if (epi != 8 && epi != 12 && epi != 16) epi = kDefaultEpi;
-  const Layout L = pick_layout(g.tile_cols, g.tpt, epi / 4);
+  const char* env_epi = getenv("SSQA_TC_EPI");
+  const int epi = (env_epi && atoi(env_epi) == 16) ? 16 : kDefaultEpi;
+  Layout L = pick_layout(g.tile_cols, g.tpt, epi / 4, int(tile_row));
+  if (const char* st = getenv("SSQA_TC_STAGES")) {  // experiment overrides
+    const char* np = getenv("SSQA_TC_NPS");
+    L = make_layout(g.tile_cols, g.tpt, atoi(st), (np ? atoi(np) : 1) * (epi / 4), int(tile_row));
+  }
   P.stages = L.stages;
   P.nslot = L.nslot;
   const int smem = int(L.total);
@@ -864,9 +1095,12 @@ int launch(ssqa_batch_s* b, TcParams& P) {
     P.dbg_rts = dbg_rts;
   }
   cudaError_t e;
-  if (epi == 8) e = launch_variant<8>(g.ntiles, smem, b->prob->stream, maps, P);
-  else if (epi == 16) e = launch_variant<16>(g.ntiles, smem, b->prob->stream, maps, P);
-  else e = launch_variant<12>(g.ntiles, smem, b->prob->stream, maps, P);
+  if (epi == 16)
+    e = f4 ? launch_variant<16, true>(g.ntiles, smem, b->prob->stream, maps, P)
+           : launch_variant<16, false>(g.ntiles, smem, b->prob->stream, maps, P);
+  else
+    e = f4 ? launch_variant<12, true>(g.ntiles, smem, b->prob->stream, maps, P)
+           : launch_variant<12, false>(g.ntiles, smem, b->prob->stream, maps, P);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) {
     g_tc_err = std::string("k_sweep_tc launch: ") + cudaGetErrorString(e);
@@ -886,6 +1120,23 @@ int launch(ssqa_batch_s* b, TcParams& P) {
   return SSQA_OK;
 }
 
+// The fast epilogue (update_fast2) is exact when every parameter is finite
+// (so no accumulator is ever NaN or -0.0), n_rnd * 2^p is a small integer and
+// the per-quarter int32 energy partials cannot overflow.
+bool fast_ok(const ssqa_batch_s* b, int* nr) {
+  const ssqa_params_c& p = b->p;
+  const Quantized& q = b->prob->q;
+  for (double v : {p.n_rnd, p.i0, p.alpha, p.jperp_min, p.jperp_max, p.i0 - p.alpha})
+    if (!std::isfinite(v)) return false;
+  const double x = std::ldexp(p.n_rnd, q.p);
+  if (x != std::floor(x) || std::fabs(x) >= double(1 << 28)) return false;
+  const double row_max = double(q.max_abs_j) * q.n + 2.0 * q.max_abs_h;
+  if (row_max + std::fabs(x) >= double(1u << 30)) return false;
+  if (double(q.npad) / 4.0 * row_max >= 2147483647.0) return false;
+  *nr = int(x);
+  return true;
+}
+
 TcParams base_params(ssqa_batch_s* b) {
   TcParams P{};
   P.g = b->g;
@@ -895,6 +1146,7 @@ TcParams base_params(ssqa_batch_s* b) {
   P.shift_p = b->prob->q.p;
   P.seeds = b->d_seeds;
   P.sig = b->d_sig;
+  P.sig_base = reinterpret_cast<uint8_t*>(b->d_sig);
   P.slot_elems = b->slot_elems;
   P.nslots = b->nslots;
   P.d = b->d;
@@ -904,6 +1156,10 @@ TcParams base_params(ssqa_batch_s* b) {
   P.n_rnd = b->p.n_rnd;
   P.alpha = b->p.alpha;
   P.bidirectional = b->p.bidirectional;
+  P.hi_clamp = b->p.i0 - b->p.alpha;
+  P.lo_clamp = -b->p.i0;
+  P.fast = fast_ok(b, &P.nr) ? 1 : 0;
+  if (const char* ex = getenv("SSQA_TC_EXP")) P.exp_flags = atoi(ex);
   P.ring_cur = b->cur;
   for (int q = 0; q <= b->d; ++q) P.ring_phys[q] = b->phys[size_t(q)];
   P.best_e = b->d_best_e;
@@ -947,9 +1203,26 @@ int tc_run(ssqa_batch_s* b, const ScanArgs& sa) {
   P.stop_at_target = sa.stop_at_target;
   P.record_trace = sa.record_trace;
   P.target_tol = sa.target_tol;
-  int rc = launch(b, P);
+  // FP4 operands when every coupling is e2m1-exact, fields stay below 2^22
+  // (exact fp32 accumulation and float->int conversion) and the tile leaves
+  // room for the scale-factor columns; SSQA_TC_FP4=0 forces int8.
+  const Quantized& q = b->prob->q;
+  const char* envf4 = getenv("SSQA_TC_FP4");
+  const bool f4 = q.fp4_ok && b->d_sig4 && double(q.max_abs_j) * q.n < double(1 << 22) &&
+                  2 * b->g.tile_cols <= int(kSfCol) && !(envf4 && envf4[0] == '0');
+  if (f4) {
+    const size_t bytes = size_t(b->nslots) * b->slot_elems / 2;
+    k_pack_fp4<<<1184, 256, 0, b->prob->stream>>>(b->d_sig, b->d_sig4, bytes);
+    if (cudaGetLastError() != cudaSuccess) {
+      g_tc_err = "k_pack_fp4 launch failed";
+      return SSQA_ECUDA;
+    }
+    b->launches += 1;
+  }
+  int rc = launch(b, P, f4);
   if (rc) return rc;
   advance_ring(b, b->p.sc);
+  b->lattice_stale = f4;
   return SSQA_OK;
 }
 
@@ -963,9 +1236,16 @@ int tc_sweep(ssqa_batch_s* b, double jperp, double i0) {
   P.c_last = b->cycle;
   P.sc = b->cycle + 1;  // exactly one update
   P.run_mode = 0;
+  P.fast = 0;  // hand-written lattices may hold any double: exact path only
   P.jperp_fixed = jperp;
   P.i0 = i0;
-  int rc = launch(b, P);
+  P.hi_clamp = i0 - b->p.alpha;
+  P.lo_clamp = -i0;
+  if (b->lattice_stale) {
+    g_tc_err = "lattice state is not kept after a fused run; re-init first";
+    return SSQA_EINVAL;
+  }
+  int rc = launch(b, P, false);
   if (rc) return rc;
   advance_ring(b, 1);
   return SSQA_OK;
