@@ -7,7 +7,7 @@
  * energies_from_fields / update_spins (src/annealer.cpp:216-361, 474-487)
  * and its batched caller run_trials (src/bench.cpp:359-432).  Each entry
  * point below names the reference interface it replaces.  The C++ facade in
- * include/ssqa/*.hpp (same names as the reference headers) is built on top
+ * include/ssqa/{rng,model,gi,annealer,bench}.hpp (same names as the reference headers) is built on top
  * of these entry points; INTEGRATION.md shows the binding a maintainer adds.
  *
  * Conventions
@@ -58,6 +58,19 @@ typedef struct {
   int bidirectional;
 } ssqa_params_c;
 
+/* Mirrors ssqa::SsaParams (annealer.hpp:38-50), field for field: the
+ * single-network engine whose accumulator bound climbs the geometric ladder
+ * i0_min, i0_min/beta, ... <= i0_max every tau cycles and wraps. */
+typedef struct {
+  double i0_min;
+  double i0_max;
+  double beta;
+  int tau;
+  double n_rnd;
+  double alpha;
+  long sc;
+} ssqa_ssa_params_c;
+
 /* Scalar fields of ssqa::AnnealResult (annealer.hpp:102-111).  wall_seconds
  * of a batched run is the batch's device time divided by the trial count. */
 typedef struct {
@@ -106,6 +119,16 @@ int ssqa_params_validate(const ssqa_params_c* p, int n);
 /* jperp_schedule (annealer.cpp:375-380); SSQA_EINVAL for cycle < 0. */
 int ssqa_jperp_schedule(long cycle, const ssqa_params_c* p, double* out);
 
+/* ---- SSA: SsaParams::validate / i0_levels (annealer.cpp:382-397) and
+ * i0_schedule (annealer.cpp:403-408).  SSQA_EINVAL for a ladder of more than
+ * 64 levels, as the reference; also for an empty ladder (NaN bounds), where
+ * the reference would divide by zero. */
+int ssqa_ssa_params_validate(const ssqa_ssa_params_c* p, int n);
+int ssqa_i0_schedule(long cycle, const ssqa_ssa_params_c* p, double* out);
+/* SsaParams::i0_levels (annealer.cpp:389-397): writes the ladder to
+ * levels[0..*count) (room for 64 doubles). */
+int ssqa_i0_levels(const ssqa_ssa_params_c* p, double* levels, int* count);
+
 /* ---- One-shot runs: ssqa_run (annealer.cpp:474-487) over a batch of seeds.
  * Trial t runs ssqa_run(model, p, seeds[t], target, {record_trace,
  * stop_at_target}) exactly; results[t] gets the AnnealResult scalars,
@@ -118,11 +141,25 @@ int ssqa_run_batch(ssqa_problem prob, const ssqa_params_c* p, const uint64_t* se
                    int stop_at_target, int engine, ssqa_result_c* results,
                    int8_t* best_states, double* trace);
 
+/* ssa_run (annealer.cpp:489-501) over a batch of seeds: the same lattice
+ * engine with r = 1, delay = 0, jperp = 0 and the per-cycle bound
+ * i0_schedule(cycle, p).  Arguments and outputs as ssqa_run_batch (trace
+ * holds sc+1 energies per trial; best_replica is always 0). */
+int ssqa_ssa_run_batch(ssqa_problem prob, const ssqa_ssa_params_c* p, const uint64_t* seeds,
+                       int trials, int has_target, double target, int record_trace,
+                       int stop_at_target, int engine, ssqa_result_c* results,
+                       int8_t* best_states, double* trace);
+
 /* ---- Batches: device-resident state for `trials` x p->r replica columns.
  * Replaces the per-trial ReplicaLattice of run_lattice (annealer.cpp:319-321);
  * run_trials' thread pool (bench.cpp:399-407) becomes the batch. */
 int ssqa_batch_create(ssqa_problem prob, const ssqa_params_c* p, int trials, int record_trace,
                       int engine, ssqa_batch* out);
+/* A batch of ssa_run trials (annealer.cpp:489-501); every batch entry point
+ * below applies, with r = 1 and delay = 0.  ssqa_batch_sweep follows the
+ * i0 ladder at the lattice cycle. */
+int ssqa_batch_create_ssa(ssqa_problem prob, const ssqa_ssa_params_c* p, int trials,
+                          int record_trace, int engine, ssqa_batch* out);
 int ssqa_batch_destroy(ssqa_batch b);
 /* CUDA stream (cudaStream_t) the batch enqueues on; for event timing. */
 void* ssqa_batch_stream(ssqa_batch b);

@@ -40,6 +40,17 @@ typedef struct {
   int bidirectional;
 } orc_ssqa_params;
 
+/* Mirrors ssqa::SsaParams (annealer.hpp:38-50). */
+typedef struct {
+  double i0_min;
+  double i0_max;
+  double beta;
+  int tau;
+  double n_rnd;
+  double alpha;
+  long sc;
+} orc_ssa_params;
+
 /* Mirrors the scalar fields of ssqa::AnnealResult (annealer.hpp:102-111). */
 typedef struct {
   double best_energy;
@@ -81,6 +92,10 @@ int ref_ssqa_run(int n, const double* h, const double* J, double offset,
                  const orc_ssqa_params* p, uint64_t seed, int has_target, double target,
                  int record_trace, int stop_at_target, orc_result* out, int8_t* best_state,
                  double* trace_energy);
+int ref_i0_schedule(long cycle, const orc_ssa_params* p, double* out);
+int ref_ssa_run(int n, const double* h, const double* J, double offset, const orc_ssa_params* p,
+                uint64_t seed, int has_target, double target, int record_trace,
+                int stop_at_target, orc_result* out, int8_t* best_state, double* trace_energy);
 int ref_gi_ising(int n_nodes, double edge_prob, uint64_t seed, int permute, double c1,
                  double c2, double* h, double* J, double* offset);
 int ref_run_trials(const orc_ssqa_params* p, int n_nodes, double edge_prob, int permute,
@@ -108,6 +123,10 @@ int orc_ssqa_run(int n, const double* h, const double* J, double offset,
                  const orc_ssqa_params* p, uint64_t seed, int has_target, double target,
                  int record_trace, int stop_at_target, orc_result* out, int8_t* best_state,
                  double* trace_energy);
+int orc_i0_schedule(long cycle, const orc_ssa_params* p, double* out);
+int orc_ssa_run(int n, const double* h, const double* J, double offset, const orc_ssa_params* p,
+                uint64_t seed, int has_target, double target, int record_trace,
+                int stop_at_target, orc_result* out, int8_t* best_state, double* trace_energy);
 
 #ifdef __cplusplus
 }

@@ -29,6 +29,13 @@ class OrcParams(C.Structure):
     ]
 
 
+class OrcSsaParams(C.Structure):
+    _fields_ = [
+        ("i0_min", C.c_double), ("i0_max", C.c_double), ("beta", C.c_double),
+        ("tau", C.c_int), ("n_rnd", C.c_double), ("alpha", C.c_double), ("sc", C.c_long),
+    ]
+
+
 class OrcResult(C.Structure):
     _fields_ = [
         ("best_energy", C.c_double), ("best_replica", C.c_int), ("reached_target", C.c_int),
@@ -71,6 +78,12 @@ def params(r, sc, jperp_min=0.0, jperp_max=0.5, beta=3, tau=100, delay=1, i0=2.0
     """Defaults mirror ssqa::SsqaParams (annealer.hpp:14-30)."""
     return OrcParams(r, jperp_min, jperp_max, beta, tau, delay, i0, n_rnd, alpha, sc,
                      int(bidirectional))
+
+
+def ssa_params(sc, i0_min=1.0, i0_max=16.0, beta=0.5, tau=10, n_rnd=1.0,
+               alpha=1.0) -> OrcSsaParams:
+    """Defaults mirror ssqa::SsaParams (annealer.hpp:38-50)."""
+    return OrcSsaParams(i0_min, i0_max, beta, tau, n_rnd, alpha, sc)
 
 
 @dataclass
@@ -179,6 +192,28 @@ class Oracle:
         best = np.zeros(n, dtype=np.int8)
         trace = np.zeros((p.sc + 1) * p.r if record_trace else 1)
         self._check(self._f("ssqa_run")(
+            n, _dp(np.ascontiguousarray(h, dtype=np.float64)),
+            _dp(np.ascontiguousarray(J, dtype=np.float64)), C.c_double(offset), C.byref(p),
+            C.c_uint64(seed), int(target is not None),
+            C.c_double(0.0 if target is None else target), int(record_trace),
+            int(stop_at_target), C.byref(res), best.ctypes.data_as(C.POINTER(C.c_int8)),
+            _dp(trace)))
+        return RunOut(res.best_energy, res.best_replica, bool(res.reached_target),
+                      res.first_hit_cycle, res.cycles_used, res.wall_seconds, best,
+                      trace[:res.trace_len] if record_trace else np.zeros(0))
+
+    def i0_schedule(self, cycle, p: OrcSsaParams) -> float:
+        out = C.c_double()
+        self._check(self._f("i0_schedule")(C.c_long(cycle), C.byref(p), C.byref(out)))
+        return out.value
+
+    def ssa_run(self, h, J, offset, p: OrcSsaParams, seed, target=None, record_trace=False,
+                stop_at_target=True) -> RunOut:
+        n = len(h)
+        res = OrcResult()
+        best = np.zeros(n, dtype=np.int8)
+        trace = np.zeros(p.sc + 1 if record_trace else 1)
+        self._check(self._f("ssa_run")(
             n, _dp(np.ascontiguousarray(h, dtype=np.float64)),
             _dp(np.ascontiguousarray(J, dtype=np.float64)), C.c_double(offset), C.byref(p),
             C.c_uint64(seed), int(target is not None),

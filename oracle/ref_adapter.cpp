@@ -62,6 +62,18 @@ ssqa_ref::SsqaParams make_params(const orc_ssqa_params* p) {
   return q;
 }
 
+ssqa_ref::SsaParams make_ssa(const orc_ssa_params* p) {
+  ssqa_ref::SsaParams q;
+  q.i0_min = p->i0_min;
+  q.i0_max = p->i0_max;
+  q.beta = p->beta;
+  q.tau = p->tau;
+  q.n_rnd = p->n_rnd;
+  q.alpha = p->alpha;
+  q.sc = p->sc;
+  return q;
+}
+
 void load_lattice(ssqa_ref::ReplicaLattice& lat, int n, int r, int d, const double* sigma,
                   const double* acc, const double* hist, long cycle) {
   const size_t nr = size_t(n) * r;
@@ -178,6 +190,37 @@ int ref_ssqa_run(int n, const double* h, const double* J, double offset,
     if (trace_energy) {
       for (size_t i = 0; i < res.trace.size(); ++i) trace_energy[i] = res.trace[i].energy;
     }
+  });
+}
+
+// annealer.cpp:403-408
+int ref_i0_schedule(long cycle, const orc_ssa_params* p, double* out) {
+  return guarded([&] { *out = ssqa_ref::i0_schedule(cycle, make_ssa(p)); });
+}
+
+// annealer.cpp:489-501 (ssa_run -> run_lattice)
+int ref_ssa_run(int n, const double* h, const double* J, double offset, const orc_ssa_params* p,
+                uint64_t seed, int has_target, double target, int record_trace,
+                int stop_at_target, orc_result* out, int8_t* best_state, double* trace_energy) {
+  return guarded([&] {
+    ssqa_ref::IsingModel m = make_model(n, h, J, offset);
+    ssqa_ref::RunOptions opts;
+    opts.record_trace = record_trace != 0;
+    opts.stop_at_target = stop_at_target != 0;
+    std::optional<double> tgt;
+    if (has_target) tgt = target;
+    ssqa_ref::AnnealResult res = ssqa_ref::ssa_run(m, make_ssa(p), seed, tgt, opts);
+    out->best_energy = res.best_energy;
+    out->best_replica = res.best_replica;
+    out->reached_target = res.reached_target;
+    out->first_hit_cycle = res.first_hit_cycle;
+    out->cycles_used = res.cycles_used;
+    out->trace_len = long(res.trace.size());
+    out->wall_seconds = res.wall_seconds;
+    if (best_state)
+      for (size_t i = 0; i < res.best_state.size(); ++i) best_state[i] = res.best_state[i];
+    if (trace_energy)
+      for (size_t i = 0; i < res.trace.size(); ++i) trace_energy[i] = res.trace[i].energy;
   });
 }
 

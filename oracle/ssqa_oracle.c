@@ -189,16 +189,16 @@ int orc_replica_energies(int n, const double* h, const double* J, double offset,
   return 0;
 }
 
-/* annealer.cpp:313-361 (run_lattice) via 474-487 (ssqa_run). */
-int orc_ssqa_run(int n, const double* h, const double* J, double offset,
-                 const orc_ssqa_params* p, uint64_t seed, int has_target, double target,
-                 int record_trace, int stop_at_target, orc_result* out, int8_t* best_state,
-                 double* trace_energy) {
-  int rc = validate(n, p);
-  if (rc) return rc;
+/* annealer.cpp:313-361 -- run_lattice, shared by SSQA and SSA. */
+typedef double (*cycle_fn)(long cycle, const void* ctx);
+
+static int run_lattice(int n, const double* h, const double* J, double offset, int r, int d,
+                       double n_rnd, double alpha, int bidirectional, long sc, cycle_fn jperp_f,
+                       cycle_fn i0_f, const void* ctx, uint64_t seed, int has_target,
+                       double target, int record_trace, int stop_at_target, orc_result* out,
+                       int8_t* best_state, double* trace_energy) {
   struct timespec t0, t1;
   clock_gettime(CLOCK_MONOTONIC, &t0);
-  const int r = p->r, d = p->delay;
   const size_t nr = (size_t)n * r;
   double* sigma = malloc(sizeof(double) * nr);
   double* acc = malloc(sizeof(double) * nr);
@@ -218,7 +218,7 @@ int orc_ssqa_run(int n, const double* h, const double* J, double offset,
 
   long cycle = 0;
   for (;; ++cycle) {
-    const int final_scan = (cycle == p->sc);
+    const int final_scan = (cycle == sc);
     /* scan_state, annealer.cpp:327-345 */
     compute_fields(n, r, h, J, sigma, fields);
     energies_from_fields(n, r, h, offset, sigma, fields, energy);
@@ -240,8 +240,8 @@ int orc_ssqa_run(int n, const double* h, const double* J, double offset,
     }
     if (final_scan) break;
     if (stop_at_target && out->reached_target) break; /* annealer.cpp:351 */
-    update_spins(n, r, d, sigma, acc, hist, fields, jperp_at(cycle, p), p->i0, p->n_rnd,
-                 p->alpha, p->bidirectional, noise_key, cycle);
+    update_spins(n, r, d, sigma, acc, hist, fields, jperp_f(cycle, ctx), i0_f(cycle, ctx), n_rnd,
+                 alpha, bidirectional, noise_key, cycle);
   }
   out->cycles_used = cycle;
   clock_gettime(CLOCK_MONOTONIC, &t1);
@@ -252,4 +252,79 @@ int orc_ssqa_run(int n, const double* h, const double* J, double offset,
   free(fields);
   free(energy);
   return 0;
+}
+
+static double ssqa_jperp(long c, const void* ctx) { return jperp_at(c, (const orc_ssqa_params*)ctx); }
+static double ssqa_i0(long c, const void* ctx) { (void)c; return ((const orc_ssqa_params*)ctx)->i0; }
+
+/* annealer.cpp:474-487 */
+int orc_ssqa_run(int n, const double* h, const double* J, double offset,
+                 const orc_ssqa_params* p, uint64_t seed, int has_target, double target,
+                 int record_trace, int stop_at_target, orc_result* out, int8_t* best_state,
+                 double* trace_energy) {
+  int rc = validate(n, p);
+  if (rc) return rc;
+  return run_lattice(n, h, J, offset, p->r, p->delay, p->n_rnd, p->alpha, p->bidirectional,
+                     p->sc, ssqa_jperp, ssqa_i0, p, seed, has_target, target, record_trace,
+                     stop_at_target, out, best_state, trace_energy);
+}
+
+/* annealer.cpp:382-408 -- SsaParams::validate, i0_levels, i0_schedule. */
+static int ssa_levels(const orc_ssa_params* p, double* levels, int* count) {
+  int k = 0;
+  for (double v = p->i0_min; v <= p->i0_max * (1.0 + 1e-12); v /= p->beta) {
+    levels[k++] = v;
+    if (k > 64) return fail(1, "i0 schedule has too many levels");
+  }
+  *count = k;
+  return 0;
+}
+
+static int ssa_validate(int n, const orc_ssa_params* p) {
+  if (n < 1 || n >= (1 << 20)) return fail(1, "spin count out of range");
+  if (p->sc < 1 || p->sc >= (1L << 31)) return fail(1, "sc out of range");
+  if (p->n_rnd < 0.0) return fail(1, "n_rnd must be >= 0");
+  if (p->alpha <= 0.0) return fail(1, "alpha must be > 0");
+  if (p->i0_min <= 0.0 || p->i0_min > p->i0_max) return fail(1, "need 0 < i0_min <= i0_max");
+  if (p->beta <= 0.0 || p->beta >= 1.0) return fail(1, "beta must be in (0, 1)");
+  if (p->tau < 1) return fail(1, "tau must be >= 1");
+  return 0;
+}
+
+typedef struct {
+  double levels[66];
+  int count;
+  int tau;
+} ssa_ctx;
+
+static double ssa_jperp(long c, const void* ctx) { (void)c; (void)ctx; return 0.0; }
+static double ssa_i0(long c, const void* ctx) {
+  const ssa_ctx* s = (const ssa_ctx*)ctx;
+  long cc = c % ((long)s->count * s->tau);
+  return s->levels[cc / s->tau];
+}
+
+int orc_i0_schedule(long cycle, const orc_ssa_params* p, double* out) {
+  if (cycle < 0) return fail(1, "cycle must be >= 0");
+  ssa_ctx s;
+  int rc = ssa_levels(p, s.levels, &s.count);
+  if (rc) return rc;
+  s.tau = p->tau;
+  *out = ssa_i0(cycle, &s);
+  return 0;
+}
+
+/* annealer.cpp:489-501 */
+int orc_ssa_run(int n, const double* h, const double* J, double offset, const orc_ssa_params* p,
+                uint64_t seed, int has_target, double target, int record_trace,
+                int stop_at_target, orc_result* out, int8_t* best_state, double* trace_energy) {
+  int rc = ssa_validate(n, p);
+  if (rc) return rc;
+  ssa_ctx s;
+  rc = ssa_levels(p, s.levels, &s.count);
+  if (rc) return rc;
+  s.tau = p->tau;
+  return run_lattice(n, h, J, offset, 1, 0, p->n_rnd, p->alpha, 0, p->sc, ssa_jperp, ssa_i0, &s,
+                     seed, has_target, target, record_trace, stop_at_target, out, best_state,
+                     trace_energy);
 }

@@ -6,9 +6,9 @@ package is the Python view of the same ABI.
 """
 from .api import (  # noqa: F401
     AnnealResult, Batch, IsingModel, K_TARGET_TOL, Problem, ReplicaLattice, RunOptions,
-    SsqaParams, TracePoint, TrialOutcome, TtsValue, compute_tts, dense_ising, gi_ising,
-    init_lattice, ising_energy, jperp_schedule, replica_energies, run_trials, ssqa_run,
-    ssqa_run_batch, ssqa_sweep,
+    SsaParams, SsqaParams, TracePoint, TrialOutcome, TtsValue, compute_tts, dense_ising,
+    gi_ising, i0_schedule, init_lattice, ising_energy, jperp_schedule, replica_energies,
+    run_trials, ssa_run, ssa_run_batch, ssqa_run, ssqa_run_batch, ssqa_sweep,
 )
 from ._lib import (  # noqa: F401
     ENGINE_AUTO, ENGINE_SIMT, ENGINE_TCGEN05, SsqaError, SsqaInvalidArgument, lib,

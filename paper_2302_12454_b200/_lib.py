@@ -27,6 +27,14 @@ class ParamsC(C.Structure):
     ]
 
 
+class SsaParamsC(C.Structure):
+    """ssqa_ssa_params_c == ssqa::SsaParams (annealer.hpp:38-50)."""
+    _fields_ = [
+        ("i0_min", C.c_double), ("i0_max", C.c_double), ("beta", C.c_double),
+        ("tau", C.c_int), ("n_rnd", C.c_double), ("alpha", C.c_double), ("sc", C.c_long),
+    ]
+
+
 class ResultC(C.Structure):
     """ssqa_result_c == scalar fields of ssqa::AnnealResult (annealer.hpp:102-111)."""
     _fields_ = [
@@ -50,6 +58,14 @@ SIGNATURES = [
     ("ssqa_jperp_schedule", C.c_int, [C.c_long, C.POINTER(ParamsC), DP]),
     ("ssqa_run_batch", C.c_int, [VP, C.POINTER(ParamsC), U64P, C.c_int, C.c_int, C.c_double,
                                  C.c_int, C.c_int, C.c_int, C.POINTER(ResultC), I8P, DP]),
+    ("ssqa_ssa_params_validate", C.c_int, [C.POINTER(SsaParamsC), C.c_int]),
+    ("ssqa_i0_schedule", C.c_int, [C.c_long, C.POINTER(SsaParamsC), DP]),
+    ("ssqa_i0_levels", C.c_int, [C.POINTER(SsaParamsC), DP, IP]),
+    ("ssqa_ssa_run_batch", C.c_int, [VP, C.POINTER(SsaParamsC), U64P, C.c_int, C.c_int,
+                                     C.c_double, C.c_int, C.c_int, C.c_int,
+                                     C.POINTER(ResultC), I8P, DP]),
+    ("ssqa_batch_create_ssa", C.c_int, [VP, C.POINTER(SsaParamsC), C.c_int, C.c_int, C.c_int,
+                                        C.POINTER(VP)]),
     ("ssqa_batch_create", C.c_int, [VP, C.POINTER(ParamsC), C.c_int, C.c_int, C.c_int,
                                     C.POINTER(VP)]),
     ("ssqa_batch_destroy", C.c_int, [VP]),

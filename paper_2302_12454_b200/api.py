@@ -1,9 +1,10 @@
 """Python mirror of the reference annealer API, served by the B200 engine.
 
 Names, argument meaning and error behaviour follow the reference C++ API
-(proj/include/ssqa/annealer.hpp, bench.hpp): ``SsqaParams``, ``RunOptions``,
-``AnnealResult``, ``ReplicaLattice``, ``init_lattice``, ``ssqa_sweep``,
-``replica_energies``, ``jperp_schedule``, ``ssqa_run`` and ``run_trials``.
+(proj/include/ssqa/annealer.hpp, bench.hpp): ``SsqaParams``, ``SsaParams``,
+``RunOptions``, ``AnnealResult``, ``ReplicaLattice``, ``init_lattice``,
+``ssqa_sweep``, ``replica_energies``, ``jperp_schedule``, ``i0_schedule``,
+``ssqa_run``, ``ssa_run`` and ``run_trials``.
 std::invalid_argument surfaces as ``ValueError`` (``SsqaInvalidArgument``).
 Everything runs through the C ABI of include/ssqa_cuda.h; there is no Python
 or CPU compute path.
@@ -18,7 +19,7 @@ from typing import List, Optional, Sequence
 import numpy as np
 
 from . import _lib
-from ._lib import ENGINE_AUTO, ParamsC, ResultC, check, lib
+from ._lib import ENGINE_AUTO, ParamsC, ResultC, SsaParamsC, check, lib
 
 K_TARGET_TOL = 1e-9  # annealer.hpp:113
 
@@ -54,6 +55,42 @@ class SsqaParams:
 
     def validate(self, n: int) -> None:
         check(lib().ssqa_params_validate(C.byref(self.to_c()), n))
+
+
+@dataclass
+class SsaParams:
+    """ssqa::SsaParams (annealer.hpp:38-50): one network whose accumulator
+    bound climbs i0_min, i0_min/beta, ... <= i0_max every tau cycles."""
+    i0_min: float = 1.0
+    i0_max: float = 16.0
+    beta: float = 0.5
+    tau: int = 10
+    n_rnd: float = 1.0
+    alpha: float = 1.0
+    sc: int = 0
+
+    def to_c(self) -> SsaParamsC:
+        return SsaParamsC(self.i0_min, self.i0_max, self.beta, self.tau, self.n_rnd,
+                          self.alpha, self.sc)
+
+    def i0_levels(self) -> List[float]:
+        buf = (C.c_double * 65)()
+        cnt = C.c_int()
+        check(lib().ssqa_i0_levels(C.byref(self.to_c()), buf, C.byref(cnt)))
+        return list(buf[: cnt.value])
+
+    def cycles_per_iteration(self) -> int:
+        return len(self.i0_levels()) * self.tau
+
+    def validate(self, n: int) -> None:
+        check(lib().ssqa_ssa_params_validate(C.byref(self.to_c()), n))
+
+
+def i0_schedule(cycle: int, p: SsaParams) -> float:
+    """annealer.cpp:403-408."""
+    out = C.c_double()
+    check(lib().ssqa_i0_schedule(cycle, C.byref(p.to_c()), C.byref(out)))
+    return out.value
 
 
 @dataclass
@@ -184,14 +221,21 @@ class Problem:
 
 
 class Batch:
-    """Device-resident state for `trials` x p.r replica columns (ssqa_batch_*)."""
+    """Device-resident state for `trials` x r replica columns (ssqa_batch_*).
+    An ``SsaParams`` batch is the SSA engine (r = 1, delay = 0)."""
 
-    def __init__(self, prob: Problem, p: SsqaParams, trials: int, record_trace: bool = False,
+    def __init__(self, prob: Problem, p, trials: int, record_trace: bool = False,
                  engine: int = ENGINE_AUTO):
         self.prob, self.p, self.trials, self.record_trace = prob, p, trials, record_trace
         self._b = C.c_void_p()
-        check(lib().ssqa_batch_create(prob._h, C.byref(p.to_c()), trials, int(record_trace),
-                                      engine, C.byref(self._b)))
+        if isinstance(p, SsaParams):
+            self.r, self.delay = 1, 0
+            check(lib().ssqa_batch_create_ssa(prob._h, C.byref(p.to_c()), trials,
+                                              int(record_trace), engine, C.byref(self._b)))
+        else:
+            self.r, self.delay = p.r, p.delay
+            check(lib().ssqa_batch_create(prob._h, C.byref(p.to_c()), trials,
+                                          int(record_trace), engine, C.byref(self._b)))
 
     @property
     def engine(self) -> int:
@@ -228,7 +272,7 @@ class Batch:
         T, n = self.trials, self.prob.n
         res = (ResultC * T)()
         best = np.zeros((T, n), np.int8) if best_states else None
-        tr = np.zeros((T, self.p.sc + 1, self.p.r)) if trace else None
+        tr = np.zeros((T, self.p.sc + 1, self.r)) if trace else None
         check(lib().ssqa_batch_fetch(
             self._b, res, best.ctypes.data_as(C.POINTER(C.c_int8)) if best is not None else None,
             _dp(tr) if tr is not None else None))
@@ -245,12 +289,12 @@ class Batch:
         check(lib().ssqa_batch_sweep_with(self._b, jperp, i0))
 
     def energies(self) -> np.ndarray:
-        out = np.zeros((self.trials, self.p.r))
+        out = np.zeros((self.trials, self.r))
         check(lib().ssqa_batch_energies(self._b, _dp(out)))
         return out
 
     def read_lattice(self, trial: int):
-        n, r, d = self.prob.n, self.p.r, self.p.delay
+        n, r, d = self.prob.n, self.r, self.delay
         sigma, acc, hist = np.zeros(n * r), np.zeros(n * r), np.zeros((d + 1) * n * r)
         cyc = C.c_long()
         check(lib().ssqa_batch_read_lattice(self._b, trial, _dp(sigma), _dp(acc), _dp(hist),
@@ -309,6 +353,29 @@ def ssqa_run(m: IsingModel, p: SsqaParams, seed: int, target_energy: Optional[fl
              opts: RunOptions = RunOptions(), engine: int = ENGINE_AUTO) -> AnnealResult:
     """annealer.cpp:474-487."""
     return ssqa_run_batch(m, p, [seed], target_energy, opts, engine)[0]
+
+
+def ssa_run_batch(m: IsingModel, p: SsaParams, seeds: Sequence[int],
+                  target_energy: Optional[float] = None, opts: RunOptions = RunOptions(),
+                  engine: int = ENGINE_AUTO, device: int = 0,
+                  problem: Optional[Problem] = None) -> List[AnnealResult]:
+    """ssa_run for every seed, as one device batch."""
+    p.validate(m.n)
+    prob = problem or Problem(m, device)
+    b = Batch(prob, p, len(seeds), opts.record_trace, engine)
+    try:
+        b.set_seeds(seeds)
+        b.launch(target_energy, opts.stop_at_target)
+        res, best, tr = b.fetch(True, opts.record_trace)
+        return _results(res, best, tr, len(seeds))
+    finally:
+        b.close()
+
+
+def ssa_run(m: IsingModel, p: SsaParams, seed: int, target_energy: Optional[float] = None,
+            opts: RunOptions = RunOptions(), engine: int = ENGINE_AUTO) -> AnnealResult:
+    """annealer.cpp:489-501."""
+    return ssa_run_batch(m, p, [seed], target_energy, opts, engine)[0]
 
 
 @dataclass
@@ -403,14 +470,19 @@ class TrialOutcome:
     wall_seconds: float
 
 
-def run_trials(m: IsingModel, p: SsqaParams, trials: int, ec: int, base_seed: int,
+def run_trials(m: IsingModel, p, trials: int, ec: int, base_seed: int,
                target: float = 0.0, p_target: float = 0.99, engine: int = ENGINE_AUTO,
                device: int = 0):
     """run_trials (bench.cpp:359-432) on a pinned instance: fixed budget
-    sc = ec / r, seeds base_seed + t, stop_at_target = false."""
-    q = SsqaParams(**{**p.__dict__, "sc": ec // p.r})
+    sc = ec / r (r = 1 for SsaParams, bench.cpp:362-363), seeds base_seed + t,
+    stop_at_target = false."""
     seeds = [base_seed + t for t in range(trials)]
-    res = ssqa_run_batch(m, q, seeds, target, RunOptions(False, False), engine, device)
+    if isinstance(p, SsaParams):
+        q = SsaParams(**{**p.__dict__, "sc": ec})
+        res = ssa_run_batch(m, q, seeds, target, RunOptions(False, False), engine, device)
+    else:
+        q = SsqaParams(**{**p.__dict__, "sc": ec // p.r})
+        res = ssqa_run_batch(m, q, seeds, target, RunOptions(False, False), engine, device)
     outs = [TrialOutcome(s, r.reached_target, r.first_hit_cycle, r.best_energy, r.wall_seconds)
             for s, r in zip(seeds, res)]
     p_s = sum(o.reached_target for o in outs) / trials

@@ -69,6 +69,43 @@ double jperp_at(long cycle, const ssqa_params_c& p) {
   return p.jperp_min + double(step) * (p.jperp_max - p.jperp_min) / p.beta;
 }
 
+// annealer.cpp:382-387 (SsaParams::validate) and 389-397 (i0_levels).
+int ssa_validate(const ssqa_ssa_params_c* p, int n) {
+  if (!p) return set_err(SSQA_EINVAL, "null params");
+  if (n < 1 || n >= kMaxSpins) return set_err(SSQA_EINVAL, "spin count out of range");
+  if (p->sc < 1 || p->sc >= kMaxCycles) return set_err(SSQA_EINVAL, "sc out of range");
+  if (p->n_rnd < 0.0) return set_err(SSQA_EINVAL, "n_rnd must be >= 0");
+  if (p->alpha <= 0.0) return set_err(SSQA_EINVAL, "alpha must be > 0");
+  if (p->i0_min <= 0.0 || p->i0_min > p->i0_max)
+    return set_err(SSQA_EINVAL, "need 0 < i0_min <= i0_max");
+  if (p->beta <= 0.0 || p->beta >= 1.0) return set_err(SSQA_EINVAL, "beta must be in (0, 1)");
+  if (p->tau < 1) return set_err(SSQA_EINVAL, "tau must be >= 1");
+  return SSQA_OK;
+}
+
+int ssa_levels(const ssqa_ssa_params_c* p, std::vector<double>* levels) {
+  levels->clear();
+  for (double v = p->i0_min; v <= p->i0_max * (1.0 + 1e-12); v /= p->beta) {
+    levels->push_back(v);
+    if (levels->size() > 64) return set_err(SSQA_EINVAL, "i0 schedule has too many levels");
+  }
+  // The reference would divide by zero here (NaN bounds); refuse instead.
+  if (levels->empty()) return set_err(SSQA_EINVAL, "i0 schedule is empty");
+  return SSQA_OK;
+}
+
+// annealer.cpp:403-408
+double i0_level_at(long cycle, const std::vector<double>& levels, int tau) {
+  const long c = cycle % (long(levels.size()) * tau);
+  return levels[size_t(c / tau)];
+}
+
+// The accumulator bound of cycle c: the constant p.i0 of ssqa_run
+// (annealer.cpp:485) or the SSA ladder (annealer.cpp:499).
+double i0_at(const ssqa_batch_s* b, long cycle) {
+  return b->ssa ? i0_level_at(cycle, b->ssa_levels, b->ssa_tau) : b->p.i0;
+}
+
 int num_sms(int device) {
   int v = 148;
   cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device);
@@ -273,11 +310,15 @@ int ssqa_problem_info(ssqa_problem pr, int* n, int* n_pad, int* shift_p, int* ma
   return SSQA_OK;
 }
 
-int ssqa_batch_create(ssqa_problem pr, const ssqa_params_c* p, int trials, int record_trace,
-                      int engine, ssqa_batch* out) {
-  if (!pr || !out) return set_err(SSQA_EINVAL, "null argument");
-  int rc = validate(p, pr->q.n);
-  if (rc) return rc;
+}  // extern "C"
+
+namespace {
+
+// Shared by ssqa_batch_create and ssqa_batch_create_ssa; `levels`/`tau`
+// describe an SSA bound ladder (levels == nullptr for SSQA batches).
+int create_batch(ssqa_problem pr, const ssqa_params_c* p, int trials, int record_trace,
+                 int engine, const std::vector<double>* levels, int tau, ssqa_batch* out) {
+  int rc = SSQA_OK;
   if (trials < 1) return set_err(SSQA_EINVAL, "trials must be >= 1");
   CU(cudaSetDevice(pr->device));
   int eng = engine;
@@ -291,6 +332,11 @@ int ssqa_batch_create(ssqa_problem pr, const ssqa_params_c* p, int trials, int r
   auto* b = new ssqa_batch_s();
   b->prob = pr;
   b->p = *p;
+  if (levels) {
+    b->ssa = true;
+    b->ssa_levels = *levels;
+    b->ssa_tau = tau;
+  }
   b->engine = eng;
   b->record_trace = record_trace;
   b->d = p->delay;
@@ -318,6 +364,7 @@ int ssqa_batch_create(ssqa_problem pr, const ssqa_params_c* p, int trials, int r
   A(&b->d_active, size_t(T));
   A(&b->d_best_state, size_t(T) * pr->q.n);
   if (record_trace) A(&b->d_trace, size_t(T) * (p->sc + 1) * p->r);
+  if (levels) A(&b->d_i0, size_t(p->sc) + 1);
   if (rc) {
     ssqa_batch_destroy(b);
     return rc;
@@ -325,6 +372,11 @@ int ssqa_batch_create(ssqa_problem pr, const ssqa_params_c* p, int trials, int r
   std::vector<double> jp(size_t(p->sc) + 1);
   for (long c = 0; c <= p->sc; ++c) jp[size_t(c)] = jperp_at(c, *p);
   CU(cudaMemcpy(b->d_jperp, jp.data(), jp.size() * sizeof(double), cudaMemcpyHostToDevice));
+  if (levels) {
+    std::vector<double> i0t(size_t(p->sc) + 1);
+    for (long c = 0; c <= p->sc; ++c) i0t[size_t(c)] = i0_at(b, c);
+    CU(cudaMemcpy(b->d_i0, i0t.data(), i0t.size() * sizeof(double), cudaMemcpyHostToDevice));
+  }
   CU(cudaMemset(b->d_sig, 0, b->slot_elems * b->nslots));
   if (b->d_sig4) CU(cudaMemset(b->d_sig4, 0, b->slot_elems * b->nslots / 2));
   CU(cudaMemset(b->d_acc, 0, b->slot_elems * sizeof(double)));
@@ -334,11 +386,91 @@ int ssqa_batch_create(ssqa_problem pr, const ssqa_params_c* p, int trials, int r
   return SSQA_OK;
 }
 
+}  // namespace
+
+extern "C" {
+
+int ssqa_batch_create(ssqa_problem pr, const ssqa_params_c* p, int trials, int record_trace,
+                      int engine, ssqa_batch* out) {
+  if (!pr || !out) return set_err(SSQA_EINVAL, "null argument");
+  int rc = validate(p, pr->q.n);
+  if (rc) return rc;
+  return create_batch(pr, p, trials, record_trace, engine, nullptr, 1, out);
+}
+
+int ssqa_ssa_params_validate(const ssqa_ssa_params_c* p, int n) {
+  int rc = ssa_validate(p, n);
+  if (rc) return rc;
+  std::vector<double> levels;
+  return ssa_levels(p, &levels);
+}
+
+int ssqa_i0_schedule(long cycle, const ssqa_ssa_params_c* p, double* out) {
+  if (!p || !out) return set_err(SSQA_EINVAL, "null argument");
+  if (cycle < 0) return set_err(SSQA_EINVAL, "cycle must be >= 0");
+  std::vector<double> levels;
+  int rc = ssa_levels(p, &levels);
+  if (rc) return rc;
+  *out = i0_level_at(cycle, levels, p->tau);
+  return SSQA_OK;
+}
+
+int ssqa_i0_levels(const ssqa_ssa_params_c* p, double* out, int* count) {
+  if (!p || !out || !count) return set_err(SSQA_EINVAL, "null argument");
+  std::vector<double> levels;
+  int rc = ssa_levels(p, &levels);
+  if (rc) return rc;
+  std::copy(levels.begin(), levels.end(), out);
+  *count = int(levels.size());
+  return SSQA_OK;
+}
+
+int ssqa_batch_create_ssa(ssqa_problem pr, const ssqa_ssa_params_c* p, int trials,
+                          int record_trace, int engine, ssqa_batch* out) {
+  if (!pr || !out) return set_err(SSQA_EINVAL, "null argument");
+  int rc = ssa_validate(p, pr->q.n);
+  if (rc) return rc;
+  std::vector<double> levels;
+  rc = ssa_levels(p, &levels);
+  if (rc) return rc;
+  // LatticeRunSpec of ssa_run (annealer.cpp:492-500): one replica, no delay,
+  // jperp == 0 (jperp_schedule of this struct is +0.0 at every cycle).
+  ssqa_params_c q{};
+  q.r = 1;
+  q.jperp_min = 0.0;
+  q.jperp_max = 0.0;
+  q.beta = 1;
+  q.tau = 1;
+  q.delay = 0;
+  q.i0 = levels[0];
+  q.n_rnd = p->n_rnd;
+  q.alpha = p->alpha;
+  q.sc = p->sc;
+  q.bidirectional = 0;
+  return create_batch(pr, &q, trials, record_trace, engine, &levels, p->tau, out);
+}
+
+int ssqa_ssa_run_batch(ssqa_problem prob, const ssqa_ssa_params_c* p, const uint64_t* seeds,
+                       int trials, int has_target, double target, int record_trace,
+                       int stop_at_target, int engine, ssqa_result_c* results,
+                       int8_t* best_states, double* trace) {
+  ssqa_batch b = nullptr;
+  int rc = ssqa_batch_create_ssa(prob, p, trials, record_trace, engine, &b);
+  if (rc) return rc;
+  rc = ssqa_batch_set_seeds(b, seeds);
+  if (!rc) rc = ssqa_batch_launch(b, has_target, target, stop_at_target);
+  if (!rc) rc = ssqa_batch_fetch(b, results, best_states, record_trace ? trace : nullptr);
+  std::string keep = g_err;
+  ssqa_batch_destroy(b);
+  g_err = keep;
+  return rc;
+}
+
 int ssqa_batch_destroy(ssqa_batch b) {
   if (!b) return SSQA_OK;
   cudaSetDevice(b->prob->device);
   cudaStreamSynchronize(b->prob->stream);
-  for (void* ptr : {(void*)b->d_sig, (void*)b->d_sig4, (void*)b->d_acc, (void*)b->d_seeds, (void*)b->d_jperp,
+  for (void* ptr : {(void*)b->d_sig, (void*)b->d_sig4, (void*)b->d_acc, (void*)b->d_seeds, (void*)b->d_jperp, (void*)b->d_i0,
                     (void*)b->d_S, (void*)b->d_E, (void*)b->d_best_e, (void*)b->d_best_k,
                     (void*)b->d_reached, (void*)b->d_first_hit, (void*)b->d_cycles_used,
                     (void*)b->d_active, (void*)b->d_best_state, (void*)b->d_trace})
@@ -429,7 +561,7 @@ int ssqa_batch_launch(ssqa_batch b, int has_target, double target, int stop_at_t
     for (long c = 0; c <= b->p.sc; ++c) {
       sa.cycle = c;
       const double jp = jperp_at(c, b->p);
-      rc = simt_sweep(b, jp, b->p.i0, c < b->p.sc ? 1 : 0, &sa);
+      rc = simt_sweep(b, jp, i0_at(b, c), c < b->p.sc ? 1 : 0, &sa);
       if (rc) return rc;
     }
   }
@@ -515,7 +647,7 @@ int ssqa_batch_sweep(ssqa_batch b, long count) {
   if (!b) return set_err(SSQA_EINVAL, "null batch");
   for (long s = 0; s < count; ++s) {
     if (b->cycle + 1 >= kMaxCycles) return set_err(SSQA_EINVAL, "cycle out of range");
-    int rc = ssqa_batch_sweep_with(b, jperp_at(b->cycle, b->p), b->p.i0);
+    int rc = ssqa_batch_sweep_with(b, jperp_at(b->cycle, b->p), i0_at(b, b->cycle));
     if (rc) return rc;
   }
   return SSQA_OK;

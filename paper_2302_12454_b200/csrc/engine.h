@@ -78,6 +78,12 @@ struct ssqa_batch_s {
   double* d_acc = nullptr;    // [ccols][npad]
   uint64_t* d_seeds = nullptr;
   double* d_jperp = nullptr;  // [sc+1] jperp_schedule table
+  // SSA batches (annealer.cpp:489-501): R = 1, delay = 0, jperp = 0 and the
+  // accumulator bound follows i0_schedule (annealer.cpp:403-408) per cycle.
+  bool ssa = false;
+  int ssa_tau = 1;
+  std::vector<double> ssa_levels;  // SsaParams::i0_levels()
+  double* d_i0 = nullptr;          // [sc+1] i0_schedule table (SSA only)
   int32_t* d_S = nullptr;     // SIMT engine: integer fields [ccols][npad]
   long long* d_E = nullptr;   // per-column integer energy sum E' [ccols]
 

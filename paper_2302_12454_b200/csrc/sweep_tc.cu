@@ -47,6 +47,7 @@ constexpr int kCW = 8;  // columns per epilogue chunk (one tcgen05.ld .x8)
 #endif
 constexpr uint32_t kSfCol = 480;  // FP4 scale-factor TMEM columns [480, 512)
 constexpr int kMaxDelay = 30;
+constexpr int kMaxRowGroups = 64;
 constexpr int kMaxCols = 256;
 constexpr int kMaxTrialsPerTile = 256;
 
@@ -64,6 +65,7 @@ struct TcParams {
   int nslots, d;
   double* acc;
   const double* jperp_tab;  // per-cycle jperp (run mode)
+  const double* i0_tab;     // per-cycle bound (SSA run mode), else nullptr
   double jperp_fixed;       // sweep mode
   double i0, n_rnd, alpha;
   int bidirectional;
@@ -298,14 +300,18 @@ __host__ __device__ inline int ring_free(int cur, const int* phys, int d, int ns
 }
 
 // ------------------------------------------------------------- shared state
-// Per-column tables (structure of arrays in smem, NT entries each):
+// Per-column tables in smem, NT entries each:
+//   c_col  what the epilogue reads per update, one 16-byte load (ColTab)
 //   c_key  CounterRng(seed_t, kStreamSweepNoise).key()
-//   c_base key + spin_counter(cycle, k, 0) * golden for the current cycle
-//   c_off / c_up / c_dn  element offsets of this column and of its delayed
-//          Trotter neighbours k+1, k-1 (mod R) inside a spin slot
-//   c_kt   replica k | (trial-in-tile << 16);  c_flag bit0 live, bit1 update
+//   c_kt   replica k | (trial-in-tile << 16);  c_flag bit0 live
 //   c_E    integer energy partials per TMEM lane quarter [4][NT]
-constexpr int kColBytes = 8 * 2 + 4 * 4;
+struct __align__(16) ColTab {
+  uint64_t base;  // key + spin_counter(cycle, k, 0) * golden + golden (mix64's first add)
+  uint32_t off;   // column * npad: element offset of the column inside a spin slot
+  uint32_t nbr;   // up | dn << 16: delayed Trotter neighbours k+1, k-1 (mod R) as byte
+                  // offsets into the delayed-spin tile; bit 31 = update this column
+};
+constexpr int kColBytes = 16 + 8 + 4 * 2;
 
 // warp sum without the compiler's divergence-check wrapper (all lanes converge)
 __device__ __forceinline__ int redux_add(int v) {
@@ -352,6 +358,13 @@ __device__ __forceinline__ void st_f64_if(double* p, double v, bool pred, uint64
       "d"(v), "r"(int(pred)), "l"(pol)
       : "memory");
 }
+__device__ __forceinline__ void st_u32_if(uint32_t* p, uint32_t v, bool pred) {
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t"
+      "@q st.global.u32 [%0], %1;\n\t}" ::"l"(p),
+      "r"(v), "r"(int(pred))
+      : "memory");
+}
 __device__ __forceinline__ void st_s8_if(int8_t* p, int v, bool pred) {
   asm volatile(
       "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t"
@@ -375,10 +388,21 @@ struct SmemCtl {
   uint64_t aempty[16]; // accumulator-state chunks: epilogue -> loader
   uint64_t sfull[2];   // delayed-spin tile: loader -> epilogue
   uint64_t sempty[2];  // delayed-spin tile: epilogue -> loader
+  // "rows ready": the epilogue has written (and proxy-fenced) spin rows and
+  // accumulators of row-tile group b in the current pass; the producer, MMA
+  // issuer and state loader of the next pass wait on it (one phase per pass).
+  uint64_t rready[kMaxRowGroups];
   uint32_t tmem_base;
-  int ring_cur, any_active;
-  int ring_phys[kMaxDelay + 1];
+  long last_pass;  // last cycle any role may start (stop-at-target drain)
+  // slot ring per role (producer, loader, epilogue): [0] = cur, [1 + q] = phys[q]
+  int ring[3][kMaxDelay + 2];
 };
+
+__device__ __forceinline__ void ring_advance(int* r, long c, int d, int nslots) {
+  const int dst = ring_free(r[0], r + 1, d, nslots);
+  r[1 + int(c % (d + 1))] = dst;
+  r[0] = dst;
+}
 
 struct Layout {
   int stages, nslot;
@@ -415,7 +439,17 @@ struct EpiRow {
   uint64_t iG;              // i * golden
   uint64_t pol_stream;      // L2 evict_first policy for the accumulator stream
   bool w_row;               // spin row exists (i < n)
+  uint8_t* dst_w;           // FP4 word stores: byte of rows (warp row 0) + 8*(lane&3)
+  uint32_t nib_live;        // FP4 word stores: nibble mask of the live rows of that word
 };
+
+// Spread the 8 bits of b to bit 4k+3 of a word of e2m1 +-1 nibbles (0x2 / 0xA).
+__device__ __forceinline__ uint32_t nibbles_pm1(uint32_t b) {
+  uint32_t x = (b | (b << 12)) & 0x000F000Fu;
+  x = (x | (x << 6)) & 0x03030303u;
+  x = (x | (x << 3)) & 0x11111111u;
+  return (x << 3) | 0x22222222u;
+}
 
 // All of this warp's kCW-column chunks of one row tile: TMEM fields,
 // staged accumulators, delayed neighbours -> exact update, predicated
@@ -428,36 +462,47 @@ struct EpiRow {
 template <bool BIDIR, bool SIGACC, bool FAST, bool F4>
 __device__ __forceinline__ void epi_chunks(const EpiRow& er, const UpdateConsts& uc,
                                            const FastConsts& fc, const I2D& i2d, SmemCtl* ctl,
-                                           const double* acc_ring, const uint32_t* c_off,
-                                           const uint32_t* c_nbr, const uint64_t* c_base,
+                                           const double* acc_ring, const ColTab* c_col,
                                            long long* q_sum, uint32_t trow, int sub,
                                            int nsubs, int nchunk, int nps, uint32_t cnt0, int il,
                                            int lane) {
-  uint32_t cnt = cnt0;
-  for (int ch = sub; ch < nchunk; ch += nsubs, ++cnt) {
+  // this subgroup's ring position: slot sub*nps + cnt % nps, parity (cnt / nps) & 1
+  int sidx = int(cnt0 % uint32_t(nps));
+  uint32_t ph = (cnt0 / uint32_t(nps)) & 1;
+  // FP4 spin words: lane L writes 8 rows of column L >> 2
+  constexpr bool kWordSt = F4 && FAST;
+  const int wj = lane >> 2;
+  for (int ch = sub; ch < nchunk; ch += nsubs) {
     const int cb = ch * kCW;
-    const int slot = sub * nps + int(cnt % uint32_t(nps));
-    const uint32_t ph = (cnt / uint32_t(nps)) & 1;
+    const int slot = sub * nps + sidx;
     int32_t v[kCW];
     tmem_ld8(trow + uint32_t(cb), v);
     mbar_wait(&ctl->afull[slot], ph);
+    if (++sidx == nps) {
+      sidx = 0;
+      ph ^= 1;
+    }
     const double* ab = acc_ring + size_t(slot) * kCW * kBM + il;
     int ep[kCW];
+    uint32_t ball[kCW];
 #pragma unroll
     for (int j = 0; j < kCW; ++j) {
       const int cl = cb + j;
-      const uint32_t nb = c_nbr[cl];  // up | dn << 16 (tile-row units), bit 15 live, bit 31 update
-      const uint32_t coff = c_off[cl];
+      const uint4 ct = *reinterpret_cast<const uint4*>(c_col + cl);
+      const uint64_t cbase = (uint64_t(ct.y) << 32) | ct.x;
+      const uint32_t coff = ct.z;
+      const uint32_t nb = ct.w;
       const double a_old = ab[j * kBM];
       // FP4: the fp32 accumulator holds a small exact integer (|S| < 2^22);
       // its bits after adding 1.5*2^23 are 0x4B400000 + S, and the bias is
       // folded into the per-row constants h1/h2 (EpiRow).
       const int S = F4 ? __float_as_int(__int_as_float(v[j]) + 12582912.0f) : v[j];
       const int s2 = S + er.h2;
-      int ep_j;
+      // Energy partials of every column, padding included: the scan reads only
+      // live columns, and padded rows contribute 0 (J', H' rows are zero).
       if (SIGACC && FAST) {
         const int m = __double2hiint(a_old) >> 31;  // sign of a finite, never -0.0 value
-        ep_j = (s2 ^ m) - m;
+        ep[j] = (s2 ^ m) - m;
       } else {
         int sg;
         if (SIGACC) {
@@ -468,31 +513,30 @@ __device__ __forceinline__ void epi_chunks(const EpiRow& er, const UpdateConsts&
         } else {
           sg = ld_s8(reinterpret_cast<const int8_t*>(er.cur_i + coff));
         }
-        ep_j = sg * s2;
+        ep[j] = sg * s2;
       }
-      ep[j] = (nb & 0x8000u) ? ep_j : 0;
       int up, dn = 0;
       if (F4 && FAST) {
         // update_fast2 only reads the sign bit: move the nibble's bit 3 there
-        up = int(uint32_t(er.st_i[nb & 0x7fffu]) << (28u - er.nib_shift));
+        up = int(uint32_t(er.st_i[nb & 0xffffu]) << (28u - er.nib_shift));
         if (BIDIR) dn = int(uint32_t(er.st_i[(nb >> 16) & 0x7fffu]) << (28u - er.nib_shift));
       } else if (F4) {
-        const uint32_t bu = er.st_i[nb & 0x7fffu];
+        const uint32_t bu = er.st_i[nb & 0xffffu];
         up = ((bu >> er.nib_shift) & 8u) ? -1 : 1;
         if (BIDIR) dn = ((uint32_t(er.st_i[(nb >> 16) & 0x7fffu]) >> er.nib_shift) & 8u) ? -1 : 1;
       } else {
-        up = int8_t(er.st_i[nb & 0x7fffu]);
+        up = int8_t(er.st_i[nb & 0xffffu]);
         if (BIDIR) dn = int8_t(er.st_i[(nb >> 16) & 0x7fffu]);
       }
       double nv;
       uint32_t neg;  // 1 when the new spin is -1
       if (FAST) {
-        const uint32_t top = mix64_top32_pre(c_base[cl] + er.iG);
+        const uint32_t top = mix64_top32_pre(cbase + er.iG);
         nv = update_fast2<BIDIR>(fc, i2d, S + er.h1, top, up, dn, a_old);
         neg = uint32_t(__double2hiint(nv)) >> 31;
       } else {
         const double field = scaled_i32(S + er.h1, i2d);
-        const uint32_t t5 = mix64_top5_pre(c_base[cl] + er.iG);
+        const uint32_t t5 = mix64_top5_pre(cbase + er.iG);
         nv = update_fast(uc, field, t5, up, dn, BIDIR, a_old);
         neg = nv >= 0.0 ? 0u : 1u;
       }
@@ -500,6 +544,8 @@ __device__ __forceinline__ void epi_chunks(const EpiRow& er, const UpdateConsts&
       if (!(SSQA_ABL & 64))
         st_f64_if(reinterpret_cast<double*>(er.acc_i + uint64_t(coff) * 8u), nv, w, er.pol_stream);
       if (SSQA_ABL & 32) {
+      } else if (kWordSt) {
+        ball[j] = __ballot_sync(0xffffffffu, neg != 0u);
       } else if (F4) {
         // e2m1 +1 = 0x2, -1 = 0xA; even lanes store the byte of rows (i, i+1)
         const uint32_t nib = 2u | (neg << 3);
@@ -509,6 +555,18 @@ __device__ __forceinline__ void epi_chunks(const EpiRow& er, const UpdateConsts&
       } else {
         st_s8_if(reinterpret_cast<int8_t*>(er.dst_i + uint64_t(coff)), int(1 - 2 * int(neg)), w);
       }
+    }
+    if (kWordSt && !(SSQA_ABL & 32)) {
+      // ball[j] bit r = sign of row r of column cb+j; lane L stores the e2m1
+      // nibbles of rows 8*(L&3) .. +7 of column cb + (L>>2) as one 32-bit word
+      const uint32_t a0 = (wj & 1) ? ball[1] : ball[0], a1 = (wj & 1) ? ball[3] : ball[2];
+      const uint32_t a2 = (wj & 1) ? ball[5] : ball[4], a3 = (wj & 1) ? ball[7] : ball[6];
+      const uint32_t b0 = (wj & 2) ? a1 : a0, b1 = (wj & 2) ? a3 : a2;
+      const uint32_t mm = (wj & 4) ? b1 : b0;
+      const uint32_t word = nibbles_pm1((mm >> (8 * (lane & 3))) & 0xffu) & er.nib_live;
+      const uint2 cw = *reinterpret_cast<const uint2*>(&c_col[cb + wj].off);
+      st_u32_if(reinterpret_cast<uint32_t*>(er.dst_w + (cw.x >> 1)), word,
+                (cw.y & 0x80000000u) && er.nib_live);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&ctl->aempty[slot]);
@@ -588,12 +646,10 @@ __global__ void __launch_bounds__(32 * (3 + EPI), 1)
   uint8_t* sig_tiles = smem + L.sig_off;  // [2][NT][kTileRow] delayed-spin tiles
   SmemCtl* ctl = reinterpret_cast<SmemCtl*>(smem + L.ctl_off);
   uint8_t* tabs = smem + L.tab_off;
-  uint64_t* c_key = reinterpret_cast<uint64_t*>(tabs);
-  uint64_t* c_base = c_key + NT;
-  long long* c_E = reinterpret_cast<long long*>(c_base + NT);  // [4][NT]
-  uint32_t* c_off = reinterpret_cast<uint32_t*>(c_E + 4 * NT);  // column * npad (slot offset)
-  uint32_t* c_nbr = c_off + NT;  // (k+1 column)*kBM | (k-1 column)*kBM << 16, tile-local
-  int* c_kt = reinterpret_cast<int*>(c_nbr + NT);
+  ColTab* c_col = reinterpret_cast<ColTab*>(tabs);
+  uint64_t* c_key = reinterpret_cast<uint64_t*>(c_col + NT);
+  long long* c_E = reinterpret_cast<long long*>(c_key + NT);  // [4][NT]
+  int* c_kt = reinterpret_cast<int*>(c_E + 4 * NT);
   int* c_flag = c_kt + NT;
   TrialTab* trials = reinterpret_cast<TrialTab*>(c_flag + NT + (NT & 1));
 
@@ -613,6 +669,11 @@ __global__ void __launch_bounds__(32 * (3 + EPI), 1)
   constexpr int nsubs = EPI / 4;         // epilogue subgroups (4 warps each)
   const int nps = nslot / nsubs;         // ring slots per subgroup
   auto chunks_of = [&](int sb) { return (nchunk - sb + nsubs - 1) / nsubs; };
+  // row tiles per "rows ready" barrier (at most kMaxRowGroups barriers)
+  const int rgroup = (NRT + kMaxRowGroups - 1) / kMaxRowGroups;
+  const int nrg = (NRT + rgroup - 1) / rgroup;
+  // spin rows covered by one K chunk of the operand stream
+  constexpr int kKRows = F4 ? 2 * kBK : kBK;
 
   // ---- one-time setup ----
   if (threadIdx.x == 0) {
@@ -630,10 +691,14 @@ __global__ void __launch_bounds__(32 * (3 + EPI), 1)
       mbar_init(&ctl->afull[s], 1);
       mbar_init(&ctl->aempty[s], 4);
     }
+    for (int b = 0; b < nrg; ++b)
+      mbar_init(&ctl->rready[b], EPI * (min(NRT, (b + 1) * rgroup) - b * rgroup));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    ctl->ring_cur = P.ring_cur;
-    for (int q = 0; q <= P.d; ++q) ctl->ring_phys[q] = P.ring_phys[q];
-    ctl->any_active = 1;
+    for (int r = 0; r < 3; ++r) {
+      ctl->ring[r][0] = P.ring_cur;
+      for (int q = 0; q <= P.d; ++q) ctl->ring[r][1 + q] = P.ring_phys[q];
+    }
+    ctl->last_pass = P.c_last;
   }
   if (warp == kWarpProducer && lane == 0) {
     prefetch_tmap(&tmJ);
@@ -656,8 +721,9 @@ __global__ void __launch_bounds__(32 * (3 + EPI), 1)
     c_key[c] = ci.live ? rng_key(P.seeds[ci.t], kStreamSweepNoise) : 0;
     const int kup = (ci.k + 1 == g.R) ? 0 : ci.k + 1;
     const int kdn = (ci.k == 0) ? g.R - 1 : ci.k - 1;
-    c_off[c] = uint32_t(col0 + c) * uint32_t(g.npad);
-    c_nbr[c] = uint32_t(tl * g.R + kup) * kTileRow | (uint32_t(tl * g.R + kdn) * kTileRow << 16);
+    c_col[c].base = 0;
+    c_col[c].off = uint32_t(col0 + c) * uint32_t(g.npad);
+    c_col[c].nbr = uint32_t(tl * g.R + kup) * kTileRow | (uint32_t(tl * g.R + kdn) * kTileRow << 16);
     c_kt[c] = ci.k | (tl << 16);
     c_flag[c] = ci.live ? 1 : 0;
   }
@@ -694,34 +760,58 @@ __global__ void __launch_bounds__(32 * (3 + EPI), 1)
   uint32_t it = 0;      // operand stage sequence (producer == MMA)
   uint32_t acc_it = 0;  // accumulator / row-tile sequence (MMA == loader == epilogue)
 
-  for (long c = P.c_first; c <= P.c_last; ++c) {
-    const bool do_update = c < P.sc;
-    const int cur = ctl->ring_cur;
-    const int src = ctl->ring_phys[c % (P.d + 1)];
-    const int dst = do_update ? ring_free(cur, ctl->ring_phys, P.d, P.nslots) : cur;
-    if (!ctl->any_active) break;
+  // Passes are pipelined across roles: pass c+1's operand loads, MMAs and
+  // state loads start as soon as the rows they read were written in pass c
+  // (ctl->rready, one phase per pass), while the epilogue is still finishing
+  // pass c and scanning it.  A pass that starts before the scan of the pass
+  // before it has decided to stop is drained by the epilogue without work.
+  // rows_wait(s, b): group b of pass index s (= c - c_first) is complete.
+  auto rows_wait = [&](long s, int b) { mbar_wait(&ctl->rready[b], uint32_t(s) & 1u); };
+  auto stop_at = [&](long c) { return c > *reinterpret_cast<volatile long*>(&ctl->last_pass); };
 
-    if (warp == kWarpProducer) {
-      // ===== operand TMA producer =====
-      if (lane == 0) {
-        const int yS = cur * g.ccols + col0;
-        const uint64_t pol_keep = policy_evict_last();
+  if (warp == kWarpProducer) {
+    // ===== operand TMA producer =====
+    if (lane == 0) {
+      int* ring = ctl->ring[0];
+      const uint64_t pol_keep = policy_evict_last();
+      for (long c = P.c_first; c <= P.c_last; ++c) {
+        const long s = c - P.c_first;
+        int waited = 0;
+        if (s > 0) {
+          rows_wait(s - 1, 0);
+          waited = 1;
+          if (stop_at(c)) break;
+        }
+        const int yS = ring[0] * g.ccols + col0;
         for (int rt = 0; rt < NRT; ++rt) {
           for (int kc = 0; kc < NKC; ++kc, ++it) {
-            const int s = it % stages;
+            if (s > 0 && rt == 0) {
+              // the spin rows of this K chunk were written by pass c-1
+              const int need = min(nrg - 1, min(NRT - 1, ((kc + 1) * kKRows - 1) / kBM) / rgroup);
+              while (waited <= need) rows_wait(s - 1, waited++);
+            }
+            const int st = it % stages;
             const uint32_t ph = (it / stages) & 1;
-            mbar_wait(&ctl->empty[s], ph ^ 1);
-            mbar_expect_tx(&ctl->full[s], L.a_bytes + L.b_bytes);
-            tma_load_2d_hint(&tmJ, &ctl->full[s], sA + size_t(s) * L.a_bytes, kc * kBK, rt * kBM,
+            mbar_wait(&ctl->empty[st], ph ^ 1);
+            mbar_expect_tx(&ctl->full[st], L.a_bytes + L.b_bytes);
+            tma_load_2d_hint(&tmJ, &ctl->full[st], sA + size_t(st) * L.a_bytes, kc * kBK, rt * kBM,
                              pol_keep);
-            tma_load_2d(&tmS, &ctl->full[s], sB + size_t(s) * L.b_bytes, kc * kBK, yS);
+            tma_load_2d(&tmS, &ctl->full[st], sB + size_t(st) * L.b_bytes, kc * kBK, yS);
           }
         }
+        if (c < P.sc) ring_advance(ring, c, P.d, P.nslots);
       }
-      __syncwarp();
-    } else if (warp == kWarpMma) {
-      // ===== MMA issuer =====
-      if (lane == 0) {
+    }
+    __syncwarp();
+  } else if (warp == kWarpMma) {
+    // ===== MMA issuer =====
+    if (lane == 0) {
+      for (long c = P.c_first; c <= P.c_last; ++c) {
+        const long s = c - P.c_first;
+        if (s > 0) {
+          rows_wait(s - 1, 0);
+          if (stop_at(c)) break;
+        }
         for (int rt = 0; rt < NRT; ++rt, ++acc_it) {
           const int buf = acc_it & 1;
           const uint32_t aph = (acc_it >> 1) & 1;
@@ -730,12 +820,12 @@ __global__ void __launch_bounds__(32 * (3 + EPI), 1)
           DBG_STAMP(0, acc_it, 0);
           const uint32_t d_tmem = tmem_base + uint32_t(buf * acc_cols);
           for (int kc = 0; kc < NKC; ++kc, ++it) {
-            const int s = it % stages;
+            const int st = it % stages;
             const uint32_t ph = (it / stages) & 1;
-            mbar_wait(&ctl->full[s], ph);
+            mbar_wait(&ctl->full[st], ph);
             tc_fence_after();
-            const uint32_t a0 = smem_u32(sA + size_t(s) * L.a_bytes);
-            const uint32_t b0 = smem_u32(sB + size_t(s) * L.b_bytes);
+            const uint32_t a0 = smem_u32(sA + size_t(st) * L.a_bytes);
+            const uint32_t b0 = smem_u32(sB + size_t(st) * L.b_bytes);
             if (!(P.exp_flags & 2)) {
 #pragma unroll
               for (int k = 0; k < kBK / 32; ++k) {
@@ -747,19 +837,33 @@ __global__ void __launch_bounds__(32 * (3 + EPI), 1)
                          idesc, (kc | k) ? 1u : 0u);
               }
             }
-            mma_commit(&ctl->empty[s]);
+            mma_commit(&ctl->empty[st]);
           }
           mma_commit(&ctl->tfull[buf]);
           DBG_STAMP(0, acc_it, 1);
         }
       }
-      __syncwarp();
-    } else if (warp == kWarpLoader) {
-      // ===== state loader: delayed-spin tile + accumulator chunks =====
-      if (lane == 0) {
-        const int ySrc = src * g.ccols + col0;
-        const uint64_t pol_first = policy_evict_first();
+    }
+    __syncwarp();
+  } else if (warp == kWarpLoader) {
+    // ===== state loader: delayed-spin tile + accumulator chunks =====
+    if (lane == 0) {
+      int* ring = ctl->ring[1];
+      const uint64_t pol_first = policy_evict_first();
+      for (long c = P.c_first; c <= P.c_last; ++c) {
+        const long s = c - P.c_first;
+        int waited = 0;
+        if (s > 0) {
+          rows_wait(s - 1, 0);
+          waited = 1;
+          if (stop_at(c)) break;
+        }
+        const int ySrc = ring[1 + int(c % (P.d + 1))] * g.ccols + col0;
         for (int rt = 0; rt < NRT; ++rt, ++acc_it) {
+          // accumulators (and, for delay 0, the neighbour spins) of these rows
+          // were written by pass c-1
+          if (s > 0)
+            while (waited <= rt / rgroup) rows_wait(s - 1, waited++);
           const int sb = acc_it & 1;
           const uint32_t sph = (acc_it >> 1) & 1;
           mbar_wait(&ctl->sempty[sb], sph ^ 1);
@@ -783,27 +887,39 @@ __global__ void __launch_bounds__(32 * (3 + EPI), 1)
           }
           DBG_STAMP(1, acc_it, 1);
         }
+        if (c < P.sc) ring_advance(ring, c, P.d, P.nslots);
       }
-      __syncwarp();
-    } else {
-      // ===== epilogue =====
-      const int ew = warp;  // 0 .. EPI-1
-      const int q = warp & 3;   // TMEM lane quarter this warp may access
-      const int sub = ew >> 2;
-      constexpr int kSubs = EPI / 4;
-      for (int cl = ew * 32 + lane; cl < NT; cl += EPI * 32) {
-        const int k = c_kt[cl] & 0xffff, tl = c_kt[cl] >> 16;
-        // key + spin_counter(c, k, 0) * golden, plus mix64's initial += golden
-        c_base[cl] = c_key[cl] + spin_counter(uint64_t(c), uint32_t(k), 0) * kGolden + kGolden;
-        const uint32_t live = uint32_t(c_flag[cl] & 1);
-        const uint32_t upd = live && do_update && (!P.run_mode || trials[tl].active);
-        c_nbr[cl] = (c_nbr[cl] & 0x7fff7fffu) | (live << 15) | (upd << 31);
-        for (int qq = 0; qq < 4; ++qq) c_E[qq * NT + cl] = 0;
+    }
+    __syncwarp();
+  } else {
+    // ===== epilogue =====
+    const int ew = warp;  // 0 .. EPI-1
+    const int q = warp & 3;   // TMEM lane quarter this warp may access
+    const int sub = ew >> 2;
+    constexpr int kSubs = EPI / 4;
+    int* ring = ctl->ring[2];
+    bool drain = false;  // every trial of the tile has stopped: consume only
+    for (long c = P.c_first; c <= P.c_last; ++c) {
+      if (stop_at(c)) break;
+      const bool do_update = c < P.sc;
+      const int cur = ring[0];
+      const int dst = do_update ? ring_free(cur, ring + 1, P.d, P.nslots) : cur;
+      if (!drain) {
+        for (int cl = ew * 32 + lane; cl < NT; cl += EPI * 32) {
+          const int k = c_kt[cl] & 0xffff, tl = c_kt[cl] >> 16;
+          // key + spin_counter(c, k, 0) * golden, plus mix64's initial += golden
+          c_col[cl].base = c_key[cl] + spin_counter(uint64_t(c), uint32_t(k), 0) * kGolden + kGolden;
+          const uint32_t live = uint32_t(c_flag[cl] & 1);
+          const uint32_t upd = live && do_update && (!P.run_mode || trials[tl].active);
+          c_col[cl].nbr = (c_col[cl].nbr & 0x7fffffffu) | (upd << 31);
+          for (int qq = 0; qq < 4; ++qq) c_E[qq * NT + cl] = 0;
+        }
       }
       long long* q_sum = c_E + q * NT;
       epi_bar<EPI>();
       const double jperp = P.run_mode ? P.jperp_tab[c] : P.jperp_fixed;
-      const UpdateConsts uc = make_consts(P.n_rnd, jperp, P.i0, P.alpha);
+      const double i0c = (P.run_mode && P.i0_tab) ? P.i0_tab[c] : P.i0;
+      const UpdateConsts uc = make_consts(P.n_rnd, jperp, i0c, P.alpha);
       const I2D i2d = make_i2d(P.shift_p);
       const bool bidir = P.bidirectional != 0;
       const bool fast = P.fast != 0;
@@ -811,9 +927,9 @@ __global__ void __launch_bounds__(32 * (3 + EPI), 1)
       fc.nr = P.nr;
       fc.jp_hi = uint32_t(__double2hiint(uc.jp_pos));
       fc.jp_lo = uint32_t(__double2loint(uc.jp_pos));
-      fc.i0 = P.i0;
-      fc.hi_clamp = P.hi_clamp;
-      fc.lo_clamp = P.lo_clamp;
+      fc.i0 = i0c;
+      fc.hi_clamp = (P.run_mode && P.i0_tab) ? __dsub_rn(i0c, P.alpha) : P.hi_clamp;
+      fc.lo_clamp = -i0c;
       // sigma(c) is sign(acc(c)) once this kernel has updated the lattice;
       // on the first cycle it comes from the spin slot (init / written state).
       const bool sig_from_acc = c > P.c_first;
@@ -828,9 +944,6 @@ __global__ void __launch_bounds__(32 * (3 + EPI), 1)
         const int il = q * 32 + lane;  // row within the tile
         const int i = rt * kBM + il;
         const bool row_live = i < g.n;
-        const int h1 = row_live ? P.H[i] : 0;
-        const int h2 = 2 * h1;
-        const uint64_t iG = uint64_t(i) * kGolden;
         const uint32_t trow = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(buf * acc_cols);
         const uint8_t* stile = sig_tiles + size_t(buf) * NT * kTileRow;
         if (warp == 0) DBG_STAMP(2, acc_it, 0);
@@ -838,127 +951,161 @@ __global__ void __launch_bounds__(32 * (3 + EPI), 1)
         mbar_wait(&ctl->tfull[buf], aph);
         tc_fence_after();
         if (warp == 0) DBG_STAMP(3, acc_it, 0);
-        EpiRow er;
-        er.acc_i = reinterpret_cast<uint64_t>(P.acc + i);
-        er.dst_i = reinterpret_cast<uint64_t>(sig_dst + (F4 ? i / 2 : i));
-        er.cur_i = reinterpret_cast<uint64_t>(sig_cur + (F4 ? i / 2 : i));
-        er.st_i = stile + (F4 ? il / 2 : il);
-        er.nib_shift = 4u * uint32_t(i & 1);
-        er.h1 = F4 ? h1 - 0x4B400000 : h1;
-        er.h2 = F4 ? h2 - 0x4B400000 : h2;
-        er.iG = iG;
-        er.pol_stream = pol_first;
-        er.w_row = row_live;
         const uint32_t cnt0 = acc_it * uint32_t(chunks_of(sub));
-#define SSQA_EPI(B, S, F)                                                                  \
-  epi_chunks<B, S, F, F4>(er, uc, fc, i2d, ctl, acc_ring, c_off, c_nbr, c_base, q_sum, trow, \
-                          sub, kSubs, nchunk, nps, cnt0, il, lane)
-        if (P.exp_flags & 1) {
-          // ablation: consume the chunks without the update arithmetic
+        if (drain || (P.exp_flags & 1)) {
+          // consume the chunks without the update arithmetic (drain, or the
+          // ablation of the update math)
           uint32_t cnt = cnt0;
           for (int ch = sub; ch < nchunk; ch += kSubs, ++cnt) {
             const int slot = sub * nps + int(cnt % uint32_t(nps));
-            int32_t v[kCW];
-            tmem_ld8(trow + uint32_t(ch * kCW), v);
             mbar_wait(&ctl->afull[slot], (cnt / uint32_t(nps)) & 1);
-            const double* ab = acc_ring + size_t(slot) * kCW * kBM + il;
+            if (!drain) {
+              int32_t v[kCW];
+              tmem_ld8(trow + uint32_t(ch * kCW), v);
+              const double* ab = acc_ring + size_t(slot) * kCW * kBM + il;
 #pragma unroll
-            for (int j = 0; j < kCW; ++j) {
-              const uint32_t coff = c_off[ch * kCW + j];
-              st_f64_if(reinterpret_cast<double*>(er.acc_i + uint64_t(coff) * 8u),
-                        ab[j * kBM] + double(v[j]), false, pol_first);
+              for (int j = 0; j < kCW; ++j) {
+                const uint32_t coff = c_col[ch * kCW + j].off;
+                st_f64_if(reinterpret_cast<double*>(P.acc + i + uint64_t(coff)),
+                          ab[j * kBM] + double(v[j]), false, pol_first);
+              }
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&ctl->aempty[slot]);
           }
-        } else if (fast && sig_from_acc) {
-          if (bidir) SSQA_EPI(true, true, true);
-          else SSQA_EPI(false, true, true);
-        } else if (fast) {
-          if (bidir) SSQA_EPI(true, false, true);
-          else SSQA_EPI(false, false, true);
-        } else if (sig_from_acc) {
-          if (bidir) SSQA_EPI(true, true, false);
-          else SSQA_EPI(false, true, false);
         } else {
-          if (bidir) SSQA_EPI(true, false, false);
-          else SSQA_EPI(false, false, false);
-        }
+          const int h1 = row_live ? P.H[i] : 0;
+          const int h2 = 2 * h1;
+          EpiRow er;
+          er.acc_i = reinterpret_cast<uint64_t>(P.acc + i);
+          er.dst_i = reinterpret_cast<uint64_t>(sig_dst + (F4 ? i / 2 : i));
+          er.cur_i = reinterpret_cast<uint64_t>(sig_cur + (F4 ? i / 2 : i));
+          er.st_i = stile + (F4 ? il / 2 : il);
+          er.nib_shift = 4u * uint32_t(i & 1);
+          er.h1 = F4 ? h1 - 0x4B400000 : h1;
+          er.h2 = F4 ? h2 - 0x4B400000 : h2;
+          er.iG = uint64_t(i) * kGolden;
+          er.pol_stream = pol_first;
+          er.w_row = row_live;
+          {
+            const int r0 = rt * kBM + q * 32 + 8 * (lane & 3);  // first row of this lane's word
+            const int nl = min(8, max(0, g.n - r0));
+            er.nib_live = nl >= 8 ? 0xffffffffu : ((1u << (4 * nl)) - 1u);
+            er.dst_w = sig_dst + (rt * kBM + q * 32) / 2 + 4 * (lane & 3);
+          }
+#define SSQA_EPI(B, S, F)                                                                  \
+  epi_chunks<B, S, F, F4>(er, uc, fc, i2d, ctl, acc_ring, c_col, q_sum, trow, \
+                          sub, kSubs, nchunk, nps, cnt0, il, lane)
+          if (fast && sig_from_acc) {
+            if (bidir) SSQA_EPI(true, true, true);
+            else SSQA_EPI(false, true, true);
+          } else if (fast) {
+            if (bidir) SSQA_EPI(true, false, true);
+            else SSQA_EPI(false, false, true);
+          } else if (sig_from_acc) {
+            if (bidir) SSQA_EPI(true, true, false);
+            else SSQA_EPI(false, true, false);
+          } else {
+            if (bidir) SSQA_EPI(true, false, false);
+            else SSQA_EPI(false, false, false);
+          }
 #undef SSQA_EPI
+        }
         tc_fence_before();
+        // this warp's spin rows and accumulators of row tile rt are in global
+        // memory: make them visible to the TMA (async proxy) reads of pass c+1
+        asm volatile("fence.proxy.async.global;" ::: "memory");
         __syncwarp();
         if (warp == 0) DBG_STAMP(2, acc_it, 1);
         if (lane == 0) {
           mbar_arrive(&ctl->tempty[buf]);
           mbar_arrive(&ctl->sempty[buf]);
+          mbar_arrive(&ctl->rready[rt / rgroup]);
         }
       }
-      asm volatile("fence.proxy.async.global;" ::: "memory");
-    }
-    __syncthreads();
+      epi_bar<EPI>();
 
-    // ===== scan (annealer.cpp:327-345), one warp per trial =====
-    if (P.run_mode && warp < EPI) {
-      for (int t = warp; t < ntl; t += EPI) {
-        TrialTab& tt = trials[t];
-        if (!tt.active) continue;
-        if (lane == 0) {
-          double be = tt.best_e;
-          int improved = -1;
+      // ===== scan (annealer.cpp:327-345), one warp per trial, lanes over replicas =====
+      if (P.run_mode && !drain) {
+        for (int t = ew; t < ntl; t += EPI) {
+          TrialTab& tt = trials[t];
+          if (!tt.active) continue;
           const int tg = tile * g.tpt + t;
-          for (int k = 0; k < g.R; ++k) {
+          // The reference walks k = 0..R-1 keeping the first strict improvement;
+          // that is the first k reaching min_k e_k, if that beats best_e.
+          double bmin = __longlong_as_double(0x7ff0000000000000LL);  // +inf
+          int bk = 0x7fffffff;
+          for (int k = lane; k < g.R; k += 32) {
             long long ep = 0;
             for (int qq = 0; qq < 4; ++qq)
               ep += P.fast ? (long long)reinterpret_cast<const int*>(c_E + qq * NT)[t * g.R + k]
                            : c_E[qq * NT + t * g.R + k];
             const double ek = __dadd_rn(__dmul_rn(-0.5, scaled(ep, P.scale)), P.offset);
-            if (ek < be) {
-              be = ek;
-              improved = k;
-              if (P.has_target && !tt.reached && be <= P.target_tol) {
-                tt.reached = 1;
-                tt.first_hit = c;
-              }
-            }
             if (P.record_trace) P.trace[(size_t(tg) * (P.sc + 1) + c) * g.R + k] = ek;
+            if (ek < bmin) {
+              bmin = ek;
+              bk = k;
+            }
           }
-          tt.best_e = be;
-          if (improved >= 0) tt.best_k = improved;
-          tt.improved = improved;
-          if (P.stop_at_target && tt.reached && c < P.sc) {
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            const double ov = __shfl_xor_sync(0xffffffffu, bmin, o);
+            const int ok = __shfl_xor_sync(0xffffffffu, bk, o);
+            if (ov < bmin || (ov == bmin && ok < bk)) {
+              bmin = ov;
+              bk = ok;
+            }
+          }
+          const int improved = bmin < tt.best_e ? bk : -1;
+          __syncwarp();
+          if (lane == 0 && improved >= 0) {
+            tt.best_e = bmin;
+            tt.best_k = improved;
+            if (P.has_target && !tt.reached && bmin <= P.target_tol) {
+              tt.reached = 1;
+              tt.first_hit = c;
+            }
+          }
+          if (lane == 0 && P.stop_at_target && tt.reached && c < P.sc) {
             tt.active = 0;
             tt.cycles_used = c;
           }
-        }
-        __syncwarp();
-        const int improved = tt.improved;
-        if (improved >= 0) {
-          int8_t* dstp = P.best_state + size_t(tile * g.tpt + t) * g.n;
-          const size_t colg = size_t(col0 + t * g.R + improved);
-          if (F4) {
-            const uint8_t* sp = P.sig_base + size_t(cur) * (P.slot_elems / 2) + colg * (g.npad / 2);
-            for (int i = lane; i < g.n; i += 32)
-              dstp[i] = ((sp[i >> 1] >> (4 * (i & 1))) & 8) ? -1 : 1;
-          } else {
-            const int8_t* sp = P.sig + size_t(cur) * P.slot_elems + colg * g.npad;
-            for (int i = lane; i < g.n; i += 32) dstp[i] = sp[i];
+          if (improved >= 0) {
+            int8_t* dstp = P.best_state + size_t(tg) * g.n;
+            const size_t colg = size_t(col0 + t * g.R + improved);
+            if (F4) {
+              const uint8_t* sp = P.sig_base + size_t(cur) * (P.slot_elems / 2) + colg * (g.npad / 2);
+              for (int i = lane; i < g.n; i += 32)
+                dstp[i] = ((sp[i >> 1] >> (4 * (i & 1))) & 8) ? -1 : 1;
+            } else {
+              const int8_t* sp = P.sig + size_t(cur) * P.slot_elems + colg * g.npad;
+              for (int i = lane; i < g.n; i += 32) dstp[i] = sp[i];
+            }
           }
+          __syncwarp();
         }
-        __syncwarp();
+      }
+      epi_bar<EPI>();
+      if (ew == 0 && lane == 0) {
+        if (do_update) ring_advance(ring, c, P.d, P.nslots);
+        if (P.run_mode && !drain) {
+          int any = 0;
+          for (int t = 0; t < ntl; ++t) any |= trials[t].active;
+          // nothing left to anneal: the other roles may already be in pass
+          // c+1 -- let it run (drained) and stop everyone after it
+          if (!any && c < P.c_last) ctl->last_pass = c + 1;
+        }
+      }
+      epi_bar<EPI>();
+      if (P.run_mode && !drain && c + 1 == *reinterpret_cast<volatile long*>(&ctl->last_pass) &&
+          c + 1 <= P.c_last) {
+        int any = 0;
+        for (int t = 0; t < ntl; ++t) any |= trials[t].active;
+        drain = !any;
       }
     }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      if (do_update) {
-        ctl->ring_phys[c % (P.d + 1)] = dst;
-        ctl->ring_cur = dst;
-      }
-      int any = 0;
-      for (int t = 0; t < ntl; ++t) any |= trials[t].active;
-      ctl->any_active = P.run_mode ? any : 1;
-    }
-    __syncthreads();
   }
+  __syncthreads();
 
   if (P.run_mode) {
     for (int t = threadIdx.x; t < ntl; t += blockDim.x) {
@@ -1128,6 +1275,8 @@ bool fast_ok(const ssqa_batch_s* b, int* nr) {
   const Quantized& q = b->prob->q;
   for (double v : {p.n_rnd, p.i0, p.alpha, p.jperp_min, p.jperp_max, p.i0 - p.alpha})
     if (!std::isfinite(v)) return false;
+  for (double v : b->ssa_levels)
+    if (!std::isfinite(v) || !std::isfinite(v - p.alpha)) return false;
   const double x = std::ldexp(p.n_rnd, q.p);
   if (x != std::floor(x) || std::fabs(x) >= double(1 << 28)) return false;
   const double row_max = double(q.max_abs_j) * q.n + 2.0 * q.max_abs_h;
@@ -1152,6 +1301,7 @@ TcParams base_params(ssqa_batch_s* b) {
   P.d = b->d;
   P.acc = b->d_acc;
   P.jperp_tab = b->d_jperp;
+  P.i0_tab = b->d_i0;
   P.i0 = b->p.i0;
   P.n_rnd = b->p.n_rnd;
   P.alpha = b->p.alpha;

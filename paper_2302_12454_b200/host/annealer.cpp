@@ -30,6 +30,18 @@ ssqa_params_c to_c(const SsqaParams& p) {
   return c;
 }
 
+ssqa_ssa_params_c to_c(const SsaParams& p) {
+  ssqa_ssa_params_c c{};
+  c.i0_min = p.i0_min;
+  c.i0_max = p.i0_max;
+  c.beta = p.beta;
+  c.tau = p.tau;
+  c.n_rnd = p.n_rnd;
+  c.alpha = p.alpha;
+  c.sc = p.sc;
+  return c;
+}
+
 void check(int rc) {
   if (rc == SSQA_OK) return;
   const std::string msg = ssqa_last_error();
@@ -153,6 +165,39 @@ std::vector<double> replica_energies(const ReplicaLattice& lat, const IsingModel
   return e;
 }
 
+namespace {
+
+// Batch outputs -> AnnealResult (trace rows carry `r` energies per cycle and
+// the jperp the reference records with them, annealer.cpp:343).
+template <class JperpAt>
+std::vector<AnnealResult> to_results(int T, int n, int r, long sc,
+                                     const std::vector<ssqa_result_c>& res,
+                                     const std::vector<int8_t>& best,
+                                     const std::vector<double>& trace, bool record_trace,
+                                     JperpAt jperp_at) {
+  std::vector<AnnealResult> out(static_cast<size_t>(T));
+  for (int t = 0; t < T; ++t) {
+    AnnealResult& a = out[size_t(t)];
+    a.best_energy = res[size_t(t)].best_energy;
+    a.best_replica = res[size_t(t)].best_replica;
+    a.reached_target = res[size_t(t)].reached_target != 0;
+    a.first_hit_cycle = res[size_t(t)].first_hit_cycle;
+    a.cycles_used = res[size_t(t)].cycles_used;
+    a.wall_seconds = res[size_t(t)].wall_seconds;
+    a.best_state.assign(best.begin() + size_t(t) * n, best.begin() + size_t(t + 1) * n);
+    if (record_trace) {
+      const double* tr = trace.data() + size_t(t) * (sc + 1) * r;
+      for (long cyc = 0; cyc <= a.cycles_used; ++cyc) {
+        const double jp = jperp_at(cyc);
+        for (int k = 0; k < r; ++k) a.trace.push_back({cyc, k, tr[size_t(cyc) * r + k], jp});
+      }
+    }
+  }
+  return out;
+}
+
+}  // namespace
+
 std::vector<AnnealResult> ssqa_run_batch(const IsingModel& m, const SsqaParams& p,
                                          const std::vector<uint64_t>& seeds,
                                          std::optional<double> target_energy,
@@ -171,31 +216,62 @@ std::vector<AnnealResult> ssqa_run_batch(const IsingModel& m, const SsqaParams& 
                        target_energy.value_or(0.0), opts.record_trace ? 1 : 0,
                        opts.stop_at_target ? 1 : 0, eng.engine, res.data(), best.data(),
                        opts.record_trace ? trace.data() : nullptr));
-  std::vector<AnnealResult> out(seeds.size());
-  for (int t = 0; t < T; ++t) {
-    AnnealResult& a = out[size_t(t)];
-    a.best_energy = res[size_t(t)].best_energy;
-    a.best_replica = res[size_t(t)].best_replica;
-    a.reached_target = res[size_t(t)].reached_target != 0;
-    a.first_hit_cycle = res[size_t(t)].first_hit_cycle;
-    a.cycles_used = res[size_t(t)].cycles_used;
-    a.wall_seconds = res[size_t(t)].wall_seconds;
-    a.best_state.assign(best.begin() + size_t(t) * m.n(), best.begin() + size_t(t + 1) * m.n());
-    if (opts.record_trace) {
-      const double* tr = trace.data() + size_t(t) * (p.sc + 1) * p.r;
-      for (long cyc = 0; cyc <= a.cycles_used; ++cyc) {
-        const double jp = jperp_schedule(cyc, p);
-        for (int k = 0; k < p.r; ++k)
-          a.trace.push_back({cyc, k, tr[size_t(cyc) * p.r + k], jp});
-      }
-    }
-  }
-  return out;
+  return to_results(T, m.n(), p.r, p.sc, res, best, trace, opts.record_trace,
+                    [&p](long c) { return jperp_schedule(c, p); });
 }
 
 AnnealResult ssqa_run(const IsingModel& m, const SsqaParams& p, uint64_t seed,
                       std::optional<double> target_energy, const RunOptions& opts) {
   return ssqa_run_batch(m, p, {seed}, target_energy, opts).front();
+}
+
+std::vector<double> SsaParams::i0_levels() const {
+  ssqa_ssa_params_c c = to_c(*this);
+  double buf[65];
+  int count = 0;
+  check(ssqa_i0_levels(&c, buf, &count));
+  return std::vector<double>(buf, buf + count);
+}
+
+long SsaParams::cycles_per_iteration() const { return long(i0_levels().size()) * tau; }
+
+void SsaParams::validate(int n) const {
+  ssqa_ssa_params_c c = to_c(*this);
+  check(ssqa_ssa_params_validate(&c, n));
+}
+
+double i0_schedule(long cycle, const SsaParams& p) {
+  ssqa_ssa_params_c c = to_c(p);
+  double v = 0.0;
+  check(ssqa_i0_schedule(cycle, &c, &v));
+  return v;
+}
+
+std::vector<AnnealResult> ssa_run_batch(const IsingModel& m, const SsaParams& p,
+                                        const std::vector<uint64_t>& seeds,
+                                        std::optional<double> target_energy,
+                                        const RunOptions& opts, const EngineOptions& eng) {
+  p.validate(m.n());
+  if (seeds.empty()) return {};
+  ProblemHandle ph;
+  upload(m, eng.device, ph);
+  const int T = int(seeds.size());
+  ssqa_ssa_params_c c = to_c(p);
+  std::vector<ssqa_result_c> res(seeds.size());
+  std::vector<int8_t> best(size_t(T) * m.n());
+  std::vector<double> trace;
+  if (opts.record_trace) trace.resize(size_t(T) * (p.sc + 1));
+  check(ssqa_ssa_run_batch(ph.p, &c, seeds.data(), T, target_energy ? 1 : 0,
+                           target_energy.value_or(0.0), opts.record_trace ? 1 : 0,
+                           opts.stop_at_target ? 1 : 0, eng.engine, res.data(), best.data(),
+                           opts.record_trace ? trace.data() : nullptr));
+  return to_results(T, m.n(), 1, p.sc, res, best, trace, opts.record_trace,
+                    [](long) { return 0.0; });
+}
+
+AnnealResult ssa_run(const IsingModel& m, const SsaParams& p, uint64_t seed,
+                     std::optional<double> target_energy, const RunOptions& opts) {
+  return ssa_run_batch(m, p, {seed}, target_energy, opts).front();
 }
 
 }  // namespace ssqa

@@ -103,16 +103,25 @@ TtsValue compute_tts(double p_s, double t_seconds, double p_target) {
 
 BenchRecord run_trials(const BenchConfig& cfg) {
   cfg.validate();
-  if (cfg.engine != Engine::kSsqa)
-    throw std::invalid_argument("the B200 engine runs the replica engine (ssqa) only");
+  if (cfg.engine == Engine::kSa)
+    throw std::invalid_argument("the B200 engine runs the lattice engines (ssqa, ssa) only");
+  const bool ssa = cfg.engine == Engine::kSsa;
   const bool gi = cfg.problem.n_nodes > 0;
-  const long budget = cfg.ec / cfg.ssqa.r;
+  const int r = ssa ? 1 : cfg.ssqa.r;  // bench.cpp:362-363
+  const long budget = cfg.ec / r;
   SsqaParams p = cfg.ssqa;
   p.sc = budget;
+  SsaParams ps = cfg.ssa;
+  ps.sc = budget;
   RunOptions opts;
   opts.stop_at_target = false;
   EngineOptions eng;
   eng.device = cfg.device;
+  // run_engine (bench.cpp:332-357) for a set of seeds on one model.
+  auto run = [&](const IsingModel& m, const std::vector<uint64_t>& s, double target) {
+    return ssa ? ssa_run_batch(m, ps, s, target, opts, eng)
+               : ssqa_run_batch(m, p, s, target, opts, eng);
+  };
 
   std::vector<uint64_t> seeds(size_t(cfg.trials));
   for (int t = 0; t < cfg.trials; ++t) seeds[size_t(t)] = cfg.base_seed + uint64_t(t);
@@ -129,22 +138,22 @@ BenchRecord run_trials(const BenchConfig& cfg) {
       target = *cfg.problem.target_energy;
     }
     n = m.n();
-    results = ssqa_run_batch(m, p, seeds, target, opts, eng);
+    results = run(m, seeds, target);
   } else {
     // Fresh instance per trial (bench.cpp:387-389): one device run each.
     const CounterRng inst(cfg.base_seed, kStreamTrialInstance);
     for (int t = 0; t < cfg.trials; ++t) {
       IsingModel m = gi_model(cfg.problem, inst.raw(uint64_t(t)));
       n = m.n();
-      results.push_back(ssqa_run_batch(m, p, {seeds[size_t(t)]}, 0.0, opts, eng).front());
+      results.push_back(run(m, {seeds[size_t(t)]}, 0.0).front());
     }
   }
   BenchRecord rec;
   rec.engine = cfg.engine;
   rec.n = n;
-  rec.r = cfg.ssqa.r;
-  rec.ec = compute_ec(cfg.ssqa.r, budget);
-  rec.tau = cfg.ssqa.tau;
+  rec.r = r;
+  rec.ec = ssa ? cfg.ec : compute_ec(r, budget);  // bench.cpp:414-417
+  rec.tau = ssa ? cfg.ssa.tau : cfg.ssqa.tau;
   rec.trials = cfg.trials;
   rec.base_seed = cfg.base_seed;
   int hits = 0;

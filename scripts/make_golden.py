@@ -18,7 +18,7 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, os.path.join(ROOT, "oracle"))
-from oracle_py import Oracle, params  # noqa: E402
+from oracle_py import Oracle, params, ssa_params  # noqa: E402
 
 OUT = os.path.join(ROOT, "tests", "golden")
 
@@ -154,6 +154,49 @@ def runs(ref: Oracle):
     return out
 
 
+def ssa_runs(ref: Oracle):
+    """ssa_run (annealer.cpp:489-501) on GI instances and random models, plus
+    i0_schedule values (annealer.cpp:382-408)."""
+    out = {}
+    cases = [
+        ("gi10", (10, 7, 1.0), dict(sc=2000), 1, True, False),
+        ("gi10_tau25", (10, 7, 1.0), dict(sc=3000, tau=25), 1, True, False),
+        ("gi10_stop", (10, 7, 1.0), dict(sc=3000, tau=25), 1, True, True),
+        ("gi10_flat", (10, 7, 1.0), dict(sc=500, i0_min=2.0, i0_max=2.0), 2, True, False),
+        ("gi10_coarse", (10, 7, 0.75), dict(sc=800, beta=0.3, i0_max=12.0, tau=7, n_rnd=2.0),
+         4, True, False),
+        ("gi20", (20, 7, 1.0), dict(sc=2000, tau=25), 5, True, False),
+    ]
+    for name, (nn, gseed, c), pk, seed, trace, stop in cases:
+        h, J, off = ref.gi_ising(nn, 0.5, gseed, True, c, c)
+        p = ssa_params(**pk)
+        res = ref.ssa_run(h, J, off, p, seed, 0.0, trace, stop)
+        out[name] = dict(n_nodes=nn, gi_seed=gseed, c=c, seed=np.uint64(seed), target=0.0,
+                         stop=int(stop), **{f"p_{k}": v for k, v in pk.items()},
+                         best_energy=res.best_energy, reached=int(res.reached_target),
+                         first_hit=res.first_hit_cycle, cycles_used=res.cycles_used,
+                         best_state=res.best_state, trace=res.trace)
+    rng = np.random.default_rng(11)
+    for ci in range(3):
+        n = int(rng.integers(3, 12))
+        h, J, off = random_model(rng, n, "quarter")
+        p = ssa_params(120, tau=int(rng.integers(2, 9)))
+        seed = int(rng.integers(0, 2**63))
+        res = ref.ssa_run(h, J, off, p, seed, None, True, False)
+        out[f"rand{ci}"] = dict(h=h, J=J, offset=off, seed=np.uint64(seed), p_sc=p.sc,
+                                p_tau=p.tau, best_energy=res.best_energy,
+                                best_state=res.best_state, trace=res.trace,
+                                cycles_used=res.cycles_used)
+    sched = [dict(), dict(i0_max=10.0), dict(i0_min=0.5, i0_max=8.0), dict(beta=0.3),
+             dict(tau=3, beta=0.7, i0_max=40.0)]
+    for si, pk in enumerate(sched):
+        p = ssa_params(1, **pk)
+        cyc = np.arange(0, 400, dtype=np.int64)
+        out[f"sched{si}"] = dict(**{f"p_{k}": v for k, v in pk.items()}, cycles=cyc,
+                                 i0=np.array([ref.i0_schedule(int(c), p) for c in cyc]))
+    return out
+
+
 def trials(ref: Oracle):
     """run_trials KAT (bench.cpp:359-432)."""
     outs, ps, tm, tts = ref.run_trials(params(20, 1), n_nodes=10, trials=100, ec=20000,
@@ -172,8 +215,12 @@ def trials(ref: Oracle):
 def main():
     ref = Oracle("ref")
     os.makedirs(OUT, exist_ok=True)
-    for fname, fn in [("lattice_traj", lattice_trajectories), ("gi_instances", gi_instances),
-                      ("runs", runs), ("trials", trials)]:
+    jobs = [("lattice_traj", lattice_trajectories), ("gi_instances", gi_instances),
+            ("runs", runs), ("trials", trials), ("ssa_runs", ssa_runs)]
+    only = set(sys.argv[1:])
+    for fname, fn in jobs:
+        if only and fname not in only:
+            continue
         data = fn(ref)
         flat = {}
         for case, rec in data.items():

@@ -11,7 +11,7 @@ import pytest
 
 import paper_2302_12454_b200 as sq
 from paper_2302_12454_b200 import _lib
-from oracle_py import params
+from oracle_py import params, ssa_params
 
 pytestmark = pytest.mark.gpu
 
@@ -291,6 +291,15 @@ int main() {
   try { SsqaParams bad; bad.r = 0; bad.sc = 5; ssqa_run(m, bad, 1); }
   catch (const std::invalid_argument&) { threw = true; }
   std::printf("%d\n", int(threw));
+  SsaParams s; s.sc = 3000; s.tau = 25;
+  AnnealResult a = ssa_run(m, s, 1, 0.0, o);
+  std::printf("%d %ld %.17g %zu\n", int(a.reached_target), a.first_hit_cycle, a.best_energy,
+              a.trace.size());
+  BenchConfig cs = c; cs.engine = Engine::kSsa; cs.ssa.tau = 25; cs.trials = 20; cs.ec = 3000;
+  BenchRecord rs = run_trials(cs);
+  std::printf("%d %ld %d %d\n", rs.r, rs.ec, rs.tau, int(rs.per_trial.size()));
+  for (const TrialOutcome& t : rs.per_trial)
+    std::printf("%d %ld %.17g\n", int(t.reached_target), t.first_hit_cycle, t.best_energy);
   return 0;
 }
 ''')
@@ -302,3 +311,143 @@ int main() {
     assert out[:5] == ["1", "304", "0", "4", "20020"]
     assert float(out[5]) == 0.80
     assert out[6] == "1"
+    # ssa_run on the same instance (reference fixture ssa_runs/gi10_tau25: hit at 1629)
+    assert out[7:9] == ["1", "1629"] and out[10] == "3001"
+    assert out[11:15] == ["1", "3000", "25", "20"]
+    p = ssa_params(3000, tau=25)
+    m_h, m_J, m_off = _gi10()
+    rows = out[15:]
+    for t in range(20):
+        o = orc.ssa_run(m_h, m_J, m_off, p, 1000 + t, 0.0, False, False)
+        assert (rows[3 * t] == "1", int(rows[3 * t + 1]), float(rows[3 * t + 2])) == \
+            (o.reached_target, o.first_hit_cycle, o.best_energy), t
+
+
+def _gi10():
+    m = sq.gi_ising(10, 0.5, 7, True, 1.0, 1.0)
+    return m.h, m.J, m.offset
+
+
+# ---- SSA engine (annealer.cpp:489-501): r = 1, jperp = 0, i0 ladder ----
+
+def to_sq_ssa(p):
+    return sq.SsaParams(i0_min=p.i0_min, i0_max=p.i0_max, beta=p.beta, tau=p.tau,
+                        n_rnd=p.n_rnd, alpha=p.alpha, sc=p.sc)
+
+
+def test_ssa_runs_match_reference_fixtures(golden, engine):
+    for name, c in golden("ssa_runs").items():
+        if name.startswith("sched"):
+            continue
+        kw = {k[2:]: v.item() for k, v in c.items() if k.startswith("p_")}
+        p = sq.SsaParams(**kw)
+        if "h" in c:
+            m = sq.IsingModel.from_arrays(c["h"], c["J"], float(c["offset"]))
+            res = sq.ssa_run(m, p, int(c["seed"]), None, sq.RunOptions(True, False),
+                             engine=engine)
+        else:
+            m = sq.gi_ising(int(c["n_nodes"]), 0.5, int(c["gi_seed"]), True, float(c["c"]),
+                            float(c["c"]))
+            res = sq.ssa_run(m, p, int(c["seed"]), float(c["target"]),
+                             sq.RunOptions(True, bool(c["stop"])), engine=engine)
+            assert res.reached_target == bool(c["reached"]), name
+            assert res.first_hit_cycle == int(c["first_hit"]), name
+        assert res.cycles_used == int(c["cycles_used"]), name
+        assert res.best_energy == float(c["best_energy"]), name
+        assert res.best_replica == 0, name
+        assert np.array_equal(res.best_state, c["best_state"]), name
+        assert np.array_equal(bits(res.trace_energy), bits(c["trace"])), name
+
+
+def test_ssa_equals_one_replica_ssqa(engine):
+    # test_annealer.cpp:440-468, on the device
+    m = sq.gi_ising(10, 0.5, 7, True, 1.0, 1.0)
+    opts = sq.RunOptions(True, False)
+    a = sq.ssa_run(m, sq.SsaParams(i0_min=2.0, i0_max=2.0, sc=60), 21, None, opts,
+                   engine=engine)
+    b = sq.ssqa_run(m, sq.SsqaParams(r=1, delay=0, jperp_min=0.0, jperp_max=0.0, i0=2.0,
+                                     sc=60), 21, None, opts, engine=engine)
+    assert a.best_energy == b.best_energy and a.cycles_used == b.cycles_used
+    assert np.array_equal(a.best_state, b.best_state)
+    assert np.array_equal(bits(a.trace_energy), bits(b.trace_energy))
+
+
+def test_ssa_many_trials_match_oracle(orc, engine):
+    """Batches wider than the SM count (several single-replica trials per
+    column tile) at N=100 and N=400."""
+    for nn, sc, T, kw in [(10, 400, 300, dict(tau=7)), (20, 120, 9, dict(beta=0.3, i0_max=30.0)),
+                          (10, 250, 40, dict(tau=3, beta=0.7, i0_max=40.0, n_rnd=2.0))]:
+        m = sq.gi_ising(nn, 0.5, 7, True, 1.0, 1.0)
+        p = ssa_params(sc, **kw)
+        seeds = list(range(900, 900 + T))
+        res = sq.ssa_run_batch(m, to_sq_ssa(p), seeds, 0.0, sq.RunOptions(True, False),
+                               engine=engine)
+        for t in range(0, T, 1 if T < 50 else 7):
+            o = orc.ssa_run(m.h, m.J, m.offset, p, seeds[t], 0.0, True, False)
+            r = res[t]
+            assert (r.best_energy, r.reached_target, r.first_hit_cycle, r.cycles_used) == \
+                (o.best_energy, o.reached_target, o.first_hit_cycle, o.cycles_used), t
+            assert np.array_equal(r.best_state, o.best_state)
+            assert np.array_equal(bits(r.trace_energy), bits(o.trace))
+
+
+def test_ssa_batch_sweeps_follow_the_ladder(orc, engine):
+    """Per-step API on an SSA batch: ssqa_batch_sweep uses i0_schedule(cycle)."""
+    m = sq.gi_ising(10, 0.5, 7, True, 1.0, 1.0)
+    p = sq.SsaParams(tau=2, sc=50)
+    q = params(1, 50, jperp_min=0.0, jperp_max=0.0, delay=0)
+    prob = sq.Problem(m)
+    b = sq.Batch(prob, p, 3, engine=engine)
+    seeds = [5, 6, 7]
+    b.set_seeds(seeds)
+    b.init()
+    states = [orc.init_lattice(m.n, 1, 0, s) for s in seeds]
+    cyc = 0
+    for step in range(12):
+        b.sweep(1)
+        i0 = sq.i0_schedule(cyc, p)
+        for t, s in enumerate(seeds):
+            sg, ac, hi = states[t]
+            q.i0 = i0
+            orc.ssqa_sweep(m.h, m.J, m.offset, 0.0, q, s, cyc, sg, ac, hi, cyc)
+        cyc += 1
+        for t in range(3):
+            sg, ac, hi, c = b.read_lattice(t)
+            assert c == cyc
+            assert np.array_equal(bits(sg), bits(states[t][0])), (step, t)
+            assert np.array_equal(bits(ac), bits(states[t][1])), (step, t)
+
+
+def test_ssa_run_trials_matches_oracle(orc, engine):
+    m = sq.gi_ising(10, 0.5, 7, True, 1.0, 1.0)
+    outs, p_s, t_mean, tts = sq.run_trials(m, sq.SsaParams(tau=25), 24, 3000, 1000,
+                                           engine=engine)
+    p = ssa_params(3000, tau=25)
+    hits = 0
+    for t, o in enumerate(outs):
+        r = orc.ssa_run(m.h, m.J, m.offset, p, 1000 + t, 0.0, False, False)
+        assert (o.seed, o.reached_target, o.first_hit_cycle, o.best_energy) == \
+            (1000 + t, r.reached_target, r.first_hit_cycle, r.best_energy)
+        hits += r.reached_target
+    assert p_s == hits / 24
+
+
+def test_stop_at_target_many_tiles_drain(orc, engine):
+    """300 trials (3 per column tile) with stop_at_target: tiles whose trials
+    have all stopped end early (one drained pass) while others keep running;
+    every trial still equals the oracle's ssqa_run."""
+    m = sq.gi_ising(10, 0.5, 7, True, 1.0, 1.0)
+    p = params(20, 1500)
+    seeds = list(range(7000, 7300))
+    res = sq.ssqa_run_batch(m, to_sq(p), seeds, 0.0, sq.RunOptions(True, True), engine=engine)
+    stopped = 0
+    for t in range(0, 300, 3):
+        o = orc.ssqa_run(m.h, m.J, m.offset, p, seeds[t], 0.0, True, True)
+        r = res[t]
+        assert (r.best_energy, r.best_replica, r.reached_target, r.first_hit_cycle,
+                r.cycles_used) == (o.best_energy, o.best_replica, o.reached_target,
+                                   o.first_hit_cycle, o.cycles_used), t
+        assert np.array_equal(r.best_state, o.best_state)
+        assert np.array_equal(bits(r.trace_energy), bits(o.trace))
+        stopped += r.cycles_used < 1500
+    assert stopped > 10

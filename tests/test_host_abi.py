@@ -48,7 +48,8 @@ def test_library_exports_cpp_facade():
     for sym in ("ssqa::ssqa_run(", "ssqa::ssqa_run_batch(", "ssqa::init_lattice(",
                 "ssqa::ssqa_sweep(", "ssqa::replica_energies(", "ssqa::run_trials(",
                 "ssqa::jperp_schedule(", "ssqa::qubo_to_ising(", "ssqa::generate_gi(",
-                "ssqa::build_gi_qubo(", "ssqa::compute_tts("):
+                "ssqa::build_gi_qubo(", "ssqa::compute_tts(", "ssqa::ssa_run(",
+                "ssqa::ssa_run_batch(", "ssqa::i0_schedule(", "ssqa::SsaParams::i0_levels("):
         assert sym in out, sym
 
 
@@ -137,6 +138,31 @@ def test_jperp_schedule_matches_oracle(orc):
             assert sq.jperp_schedule(c, p) == orc.jperp_schedule(c, q)
     with pytest.raises(ValueError):
         sq.jperp_schedule(-1, sq.SsqaParams(r=1, sc=1))
+
+
+def test_ssa_params_match_reference(orc):
+    # annealer.cpp:382-408 / test_annealer.cpp:101-126, 166-185
+    from oracle_py import ssa_params
+    p = sq.SsaParams(sc=1)
+    assert p.i0_levels() == [1, 2, 4, 8, 16] and p.cycles_per_iteration() == 50
+    assert [sq.i0_schedule(c, p) for c in (0, 9, 10, 49, 50)] == [1.0, 1.0, 2.0, 16.0, 1.0]
+    assert sq.SsaParams(sc=1, i0_max=10.0).i0_levels() == [1, 2, 4, 8]
+    assert sq.SsaParams(sc=1, i0_min=0.5, i0_max=8.0).i0_levels() == [0.5, 1, 2, 4, 8]
+    assert len(sq.SsaParams(sc=1, beta=0.3).i0_levels()) == 3
+    with pytest.raises(ValueError):
+        sq.i0_schedule(-1, p)
+    for kw in (dict(), dict(tau=3, beta=0.7, i0_max=40.0), dict(i0_min=0.3, i0_max=0.3)):
+        q = sq.SsaParams(sc=1, **kw)
+        o = ssa_params(1, **kw)
+        for c in range(0, 500, 3):
+            assert sq.i0_schedule(c, q) == orc.i0_schedule(c, o)
+    ok = sq.SsaParams(sc=10)
+    ok.validate(3)
+    for bad in (dict(i0_min=0.0), dict(i0_min=32.0), dict(beta=1.0), dict(beta=0.0),
+                dict(tau=0), dict(sc=0), dict(alpha=0.0), dict(n_rnd=-1.0),
+                dict(i0_min=1e-30, i0_max=1e30), dict(i0_min=float("nan"))):
+        with pytest.raises(ValueError):
+            sq.SsaParams(**{**ok.__dict__, **bad}).validate(3)
 
 
 def test_compute_tts():

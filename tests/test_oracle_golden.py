@@ -10,7 +10,7 @@
 import numpy as np
 import pytest
 
-from oracle_py import params
+from oracle_py import params, ssa_params
 
 STREAM_SPIN_INIT, STREAM_SWEEP_NOISE, STREAM_SA_PICK, STREAM_GI_EDGES = 1, 2, 3, 5
 
@@ -281,3 +281,106 @@ def test_reference_gi_instances_match_golden(ref, golden):
                                  float(c["c"]), float(c["c"]))
         assert np.array_equal(h, c["h"]) and off == float(c["offset"])
         assert hashlib.sha256(J.tobytes()).hexdigest() == str(c["J_sha"])
+
+
+# ---- SSA engine (annealer.cpp:382-408, 489-501) ----
+
+def test_i0_ladder_kats(orc):
+    # test_annealer.cpp:101-126
+    p = ssa_params(1)
+    assert [orc.i0_schedule(c, p) for c in (0, 9, 10, 49, 50)] == [1.0, 1.0, 2.0, 16.0, 1.0]
+    assert orc.i0_schedule(123, p) == orc.i0_schedule(23, p)
+    from oracle_py import OracleError
+    with pytest.raises(OracleError):
+        orc.i0_schedule(-1, p)
+    levels = lambda q: sorted({orc.i0_schedule(c, q) for c in range(0, 70 * q.tau, q.tau)})  # noqa: E731
+    assert levels(ssa_params(1, i0_max=10.0)) == [1, 2, 4, 8]
+    assert levels(ssa_params(1, i0_min=0.5, i0_max=8.0)) == [0.5, 1, 2, 4, 8]
+    assert len(levels(ssa_params(1, beta=0.3))) == 3
+
+
+def test_i0_schedule_matches_golden(orc, golden):
+    for name, c in golden("ssa_runs").items():
+        if not name.startswith("sched"):
+            continue
+        kw = {k[2:]: v.item() for k, v in c.items() if k.startswith("p_")}
+        p = ssa_params(1, **kw)
+        got = np.array([orc.i0_schedule(int(cy), p) for cy in c["cycles"]])
+        assert np.array_equal(got.view(np.uint64), c["i0"].view(np.uint64)), name
+
+
+def test_ssa_validation_rejects(orc):
+    # test_annealer.cpp:166-185 (through ssa_run)
+    h, J = np.zeros(3), np.zeros((3, 3))
+    from oracle_py import OracleError
+    orc.ssa_run(h, J, 0.0, ssa_params(10), 1)
+    for bad in (dict(i0_min=0.0), dict(i0_min=32.0), dict(beta=1.0), dict(beta=0.0),
+                dict(tau=0), dict(sc=0), dict(i0_min=1e-30, i0_max=1e30, beta=0.5),
+                dict(alpha=0.0), dict(n_rnd=-1.0)):
+        kw = dict(sc=10)
+        kw.update(bad)
+        with pytest.raises(OracleError):
+            orc.ssa_run(h, J, 0.0, ssa_params(**kw), 1)
+
+
+def _ssa_case(c, gi):
+    if "h" in c:
+        return c["h"], c["J"], float(c["offset"])
+    key = f"gi_{int(c['n_nodes'])}_{int(c['gi_seed'])}_1_{float(c['c'])}"
+    inst = gi[key]
+    J = inst.get("J")
+    if J is None:
+        J = _product_gi(inst)
+    return inst["h"], J, float(inst["offset"])
+
+
+def ssa_case_params(c):
+    kw = {k[2:]: v.item() for k, v in c.items() if k.startswith("p_")}
+    return ssa_params(**kw)
+
+
+def test_oracle_matches_golden_ssa_runs(orc, golden):
+    gi = golden("gi_instances")
+    for name, c in golden("ssa_runs").items():
+        if name.startswith("sched"):
+            continue
+        h, J, off = _ssa_case(c, gi)
+        p = ssa_case_params(c)
+        if "target" in c:
+            res = orc.ssa_run(h, J, off, p, int(c["seed"]), float(c["target"]), True,
+                              bool(c["stop"]))
+            assert res.reached_target == bool(c["reached"]), name
+            assert res.first_hit_cycle == int(c["first_hit"]), name
+        else:
+            res = orc.ssa_run(h, J, off, p, int(c["seed"]), None, True, False)
+        assert res.cycles_used == int(c["cycles_used"]), name
+        assert res.best_energy == float(c["best_energy"]), name
+        assert np.array_equal(res.best_state, c["best_state"]), name
+        assert np.array_equal(res.trace.view(np.uint64), c["trace"].view(np.uint64)), name
+
+
+def test_ssa_equals_one_replica_ssqa(orc, golden):
+    # test_annealer.cpp:440-468: a flat ladder is SSQA with r = 1, delay 0, jperp 0
+    inst = golden("gi_instances")["gi_10_7_1_1.0"]
+    h, J, off = inst["h"], inst["J"], float(inst["offset"])
+    a = orc.ssa_run(h, J, off, ssa_params(60, i0_min=2.0, i0_max=2.0), 21, None, True, False)
+    b = orc.ssqa_run(h, J, off, params(1, 60, jperp_min=0.0, jperp_max=0.0, delay=0, i0=2.0),
+                     21, None, True, False)
+    assert np.array_equal(a.trace.view(np.uint64), b.trace.view(np.uint64))
+    assert np.array_equal(a.best_state, b.best_state) and a.cycles_used == b.cycles_used
+
+
+def test_ssa_oracle_matches_reference_live(orc, ref):
+    rng = np.random.default_rng(99)
+    for trial in range(5):
+        n = int(rng.integers(1, 20))
+        h = rng.uniform(-2, 2, n)
+        J = np.triu(rng.uniform(-2, 2, (n, n)), 1)
+        J = J + J.T
+        p = ssa_params(90, tau=int(rng.integers(1, 9)), beta=float(rng.uniform(0.2, 0.9)),
+                       i0_max=float(rng.uniform(2, 40)), n_rnd=float(rng.uniform(0, 2)))
+        seed = int(rng.integers(0, 2 ** 63))
+        a = ref.ssa_run(h, J, 0.5, p, seed, None, True, False)
+        b = orc.ssa_run(h, J, 0.5, p, seed, None, True, False)
+        assert np.array_equal(a.trace.view(np.uint64), b.trace.view(np.uint64))
+        assert np.array_equal(a.best_state, b.best_state)
