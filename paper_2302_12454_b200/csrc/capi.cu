@@ -21,7 +21,7 @@ namespace {
 thread_local std::string g_err;
 
 int set_err(int code, const std::string& msg) {
-  g_err = msg;
+  g_err = code == SSQA_ECUDA ? msg + tc_watchdog_message() : msg;
   return code;
 }
 
@@ -363,6 +363,7 @@ int create_batch(ssqa_problem pr, const ssqa_params_c* p, int trials, int record
   A(&b->d_cycles_used, size_t(T));
   A(&b->d_active, size_t(T));
   A(&b->d_best_state, size_t(T) * pr->q.n);
+  if (eng == SSQA_ENGINE_TCGEN05) A(&b->d_best_packed, size_t(T) * pr->q.npad);
   if (record_trace) A(&b->d_trace, size_t(T) * (p->sc + 1) * p->r);
   if (levels) A(&b->d_i0, size_t(p->sc) + 1);
   if (rc) {
@@ -473,7 +474,8 @@ int ssqa_batch_destroy(ssqa_batch b) {
   for (void* ptr : {(void*)b->d_sig, (void*)b->d_sig4, (void*)b->d_acc, (void*)b->d_seeds, (void*)b->d_jperp, (void*)b->d_i0,
                     (void*)b->d_S, (void*)b->d_E, (void*)b->d_best_e, (void*)b->d_best_k,
                     (void*)b->d_reached, (void*)b->d_first_hit, (void*)b->d_cycles_used,
-                    (void*)b->d_active, (void*)b->d_best_state, (void*)b->d_trace})
+                    (void*)b->d_active, (void*)b->d_best_state, (void*)b->d_best_packed,
+                    (void*)b->d_trace})
     dfree(ptr);
   if (b->ev0) cudaEventDestroy(b->ev0);
   if (b->ev1) cudaEventDestroy(b->ev1);

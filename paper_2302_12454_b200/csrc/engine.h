@@ -95,6 +95,7 @@ struct ssqa_batch_s {
   long* d_cycles_used = nullptr;
   int* d_active = nullptr;
   int8_t* d_best_state = nullptr;  // [T][n]
+  uint8_t* d_best_packed = nullptr; // tcgen05: best spin column as stored in a slot [T][npad]
   double* d_trace = nullptr;       // [T][sc+1][R]
 
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;

@@ -26,6 +26,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstring>
 #include <cstdlib>
 #include <string>
 #include <vector>
@@ -90,6 +91,7 @@ struct TcParams {
   long* cycles_used;
   int* active;
   int8_t* best_state;
+  uint8_t* best_packed;  // [T][npad] bytes: best spin column in slot format
   double* trace;
 };
 
@@ -136,29 +138,38 @@ __device__ __forceinline__ bool mbar_try_sleep(uint32_t a, uint32_t parity) {
   return ok != 0;
 }
 
-// Slow path of mbar_wait, kept out of line: sleeps in try_wait (suspend
-// hint 1 ms) and traps after ~20 s without progress instead of hanging the
-// device.
-__device__ __noinline__ void mbar_wait_slow(uint32_t a, uint32_t parity) {
-  const long long t0 = clock64();
-  while (!mbar_try_sleep(a, parity)) {
-    if (clock64() - t0 > 20000000000ll) {
-      if ((threadIdx.x & 31) == 0)
-        printf("k_sweep_tc watchdog: block %d warp %d lane %d stuck on mbarrier smem 0x%x "
-               "parity %u\n",
-               blockIdx.x, threadIdx.x >> 5, threadIdx.x & 31, a, parity);
-      // give every other stuck thread time to report before the trap
-      const long long t1 = clock64();
-      while (clock64() - t1 < 6000000000ll) {
-      }
-      __trap();
-    }
+// Watchdog record in mapped host memory (set by tc_watchdog_init): a wait
+// that makes no progress for ~20 s writes who is stuck and traps instead of
+// hanging the device; the host prints the record when the launch fails.
+// Everything here is inline -- no printf/ABI calls -- so the warp roles keep
+// their own setmaxnreg register budgets.
+struct WatchdogRec {
+  int fired, block, warp, lane;
+  unsigned addr, parity;
+};
+__device__ WatchdogRec* g_watchdog = nullptr;
+
+__device__ __forceinline__ void watchdog_fire(uint32_t a, uint32_t parity) {
+  WatchdogRec* w = g_watchdog;
+  if (w && atomicCAS(&w->fired, 0, 1) == 0) {
+    volatile WatchdogRec* v = w;
+    v->block = blockIdx.x;
+    v->warp = threadIdx.x >> 5;
+    v->lane = threadIdx.x & 31;
+    v->addr = a;
+    v->parity = parity;
+    __threadfence_system();
   }
+  __trap();
 }
 
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t a = smem_u32(bar);
-  if (!mbar_try(a, parity)) mbar_wait_slow(a, parity);
+  if (mbar_try(a, parity)) return;
+  // sleep in try_wait (suspend hint 1 ms)
+  const long long t0 = clock64();
+  while (!mbar_try_sleep(a, parity))
+    if (clock64() - t0 > 20000000000ll) watchdog_fire(a, parity);
 }
 
 __device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint64_t* bar, void* dst,
@@ -358,6 +369,24 @@ __device__ __forceinline__ void st_f64_if(double* p, double v, bool pred, uint64
       "d"(v), "r"(int(pred)), "l"(pol)
       : "memory");
 }
+// Ballot of a register != 0 in plain PTX: no divergence check, and the
+// predicate never has to survive to a deferred VOTE.
+__device__ __forceinline__ uint32_t ballot_nz(uint32_t v) {
+  uint32_t r;
+  asm(
+      "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %1, 0;\n\t"
+      "vote.sync.ballot.b32 %0, p, 0xffffffff;\n\t}"
+      : "=r"(r)
+      : "r"(v));
+  return r;
+}
+__device__ __forceinline__ uint4 lds128(const void* p) {
+  uint4 v;
+  asm("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "r"(smem_u32(p)));
+  return v;
+}
 __device__ __forceinline__ void st_u32_if(uint32_t* p, uint32_t v, bool pred) {
   asm volatile(
       "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t"
@@ -392,6 +421,7 @@ struct SmemCtl {
   // accumulators of row-tile group b in the current pass; the producer, MMA
   // issuer and state loader of the next pass wait on it (one phase per pass).
   uint64_t rready[kMaxRowGroups];
+  uint64_t done;       // epilogue finished (TMEM may be released)
   uint32_t tmem_base;
   long last_pass;  // last cycle any role may start (stop-at-target drain)
   // slot ring per role (producer, loader, epilogue): [0] = cur, [1 + q] = phys[q]
@@ -488,7 +518,7 @@ __device__ __forceinline__ void epi_chunks(const EpiRow& er, const UpdateConsts&
 #pragma unroll
     for (int j = 0; j < kCW; ++j) {
       const int cl = cb + j;
-      const uint4 ct = *reinterpret_cast<const uint4*>(c_col + cl);
+      const uint4 ct = lds128(c_col + cl);
       const uint64_t cbase = (uint64_t(ct.y) << 32) | ct.x;
       const uint32_t coff = ct.z;
       const uint32_t nb = ct.w;
@@ -614,6 +644,42 @@ __device__ __forceinline__ void epi_chunks(const EpiRow& er, const UpdateConsts&
   }
 }
 
+// Best-state snapshots during the run copy the packed spin column (npad
+// bytes int8, npad/2 bytes FP4; 16-byte aligned) with vector loads/stores;
+// expand_best_state turns it into the int8 +-1 best_state once at the end.
+template <bool F4>
+__device__ __forceinline__ void snap_best_state(const TcParams& P, int cur, size_t colg,
+                                                int trial, int npad, int lane) {
+  const size_t nb = F4 ? size_t(npad) / 2 : size_t(npad);
+  const uint4* src = reinterpret_cast<const uint4*>(P.sig_base + size_t(cur) * (F4 ? P.slot_elems / 2 : P.slot_elems) + colg * nb);
+  uint4* dst = reinterpret_cast<uint4*>(P.best_packed + size_t(trial) * npad);
+  const int nv = int(nb / 16);
+  for (int v0 = 0; v0 < nv; v0 += 128) {
+    uint4 r[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int v = v0 + u * 32 + lane;
+      if (v < nv) r[u] = src[v];
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int v = v0 + u * 32 + lane;
+      if (v < nv) dst[v] = r[u];
+    }
+  }
+}
+
+template <bool F4>
+__device__ __forceinline__ void expand_best_state(const TcParams& P, int trial, int n, int npad,
+                                                  int lane) {
+  const uint8_t* src = P.best_packed + size_t(trial) * npad;
+  int8_t* dst = P.best_state + size_t(trial) * n;
+  for (int i = lane; i < n; i += 32) {
+    const uint32_t b = src[F4 ? i >> 1 : i];
+    dst[i] = F4 ? (((b >> (4 * (i & 1))) & 8u) ? -1 : 1) : int8_t(b);
+  }
+}
+
 // Debug timeline: role 0 MMA (start, commit), 1 loader (start, all issued),
 // 2 epilogue warp 3 (start incl. waits, done), 3 epilogue warp 3 (operands
 // ready, -).  Block 0, lane 0 only; no cost when P.dbg is null.
@@ -623,11 +689,20 @@ __device__ __forceinline__ void epi_chunks(const EpiRow& er, const UpdateConsts&
       P.dbg[(size_t(role) * P.dbg_rts + (rtg)) * 2 + (which)] = clock64();            \
   } while (0)
 
+// Registers per thread after setmaxnreg: control warpgroup / epilogue
+// warpgroups.  setmaxnreg moves registers inside the CTA's launch pool, so
+// (EPI * kEpi + 4 * kCtl) * 32 must not exceed (EPI + 4) * 32 * launch regs:
+// EPI 12 launches at 128 (pool 65536 -> 160), EPI 16 at 96 (pool 61440 -> 112).
+constexpr int kCtlRegs = 32;
+template <int EPI> struct EpiRegs { static constexpr int value = EPI == 16 ? 112 : 160; };
+static_assert((12 * EpiRegs<12>::value + 4 * kCtlRegs) * 32 <= 16 * 32 * 128, "EPI 12 pool");
+static_assert((16 * EpiRegs<16>::value + 4 * kCtlRegs) * 32 <= 20 * 32 * 96, "EPI 16 pool");
+
 // Warp roles: 0 .. EPI-1 epilogue (EPI/4 warps per TMEM lane quarter),
 // EPI operand TMA producer, EPI+1 TMEM allocator + MMA issuer, EPI+2 state
 // loader (TMA of accumulator chunks and delayed-spin tiles).
 template <int EPI, bool F4>
-__global__ void __launch_bounds__(32 * (3 + EPI), 1)
+__global__ void __launch_bounds__(32 * (4 + EPI), 1)
     k_sweep_tc(const __grid_constant__ CUtensorMap tmJ, const __grid_constant__ CUtensorMap tmS,
                const __grid_constant__ CUtensorMap tmSe, const __grid_constant__ CUtensorMap tmA,
                const TcParams P) {
@@ -653,7 +728,9 @@ __global__ void __launch_bounds__(32 * (3 + EPI), 1)
   int* c_flag = c_kt + NT;
   TrialTab* trials = reinterpret_cast<TrialTab*>(c_flag + NT + (NT & 1));
 
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // warp index broadcast from lane 0: provably warp-uniform for ptxas (role
+  // branches and setmaxnreg must be warp-uniform)
+  const int warp = __shfl_sync(0xffffffffu, int(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
   // The single-lane pipeline roles take the highest warp indices: the warp
   // scheduler favours higher warp ids, so the TMA producer, MMA issuer and
   // state loader are never starved by the EPI busy epilogue warps.
@@ -693,6 +770,7 @@ __global__ void __launch_bounds__(32 * (3 + EPI), 1)
     }
     for (int b = 0; b < nrg; ++b)
       mbar_init(&ctl->rready[b], EPI * (min(NRT, (b + 1) * rgroup) - b * rgroup));
+    mbar_init(&ctl->done, EPI);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     for (int r = 0; r < 3; ++r) {
       ctl->ring[r][0] = P.ring_cur;
@@ -757,6 +835,13 @@ __global__ void __launch_bounds__(32 * (3 + EPI), 1)
     tc_fence_after();
   }
 
+  // Register split between the warpgroups (inside each role's branch, so
+  // ptxas budgets each role's code separately): the control warpgroup
+  // (producer, MMA issuer, loader, one idle warp) runs single-lane loops in
+  // few registers and hands the rest to the epilogue warpgroups.
+#define SSQA_CTL_REGS() asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(kCtlRegs))
+#define SSQA_EPI_REGS() asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(EpiRegs<EPI>::value))
+
   uint32_t it = 0;      // operand stage sequence (producer == MMA)
   uint32_t acc_it = 0;  // accumulator / row-tile sequence (MMA == loader == epilogue)
 
@@ -771,6 +856,7 @@ __global__ void __launch_bounds__(32 * (3 + EPI), 1)
 
   if (warp == kWarpProducer) {
     // ===== operand TMA producer =====
+    SSQA_CTL_REGS();
     if (lane == 0) {
       int* ring = ctl->ring[0];
       const uint64_t pol_keep = policy_evict_last();
@@ -805,6 +891,7 @@ __global__ void __launch_bounds__(32 * (3 + EPI), 1)
     __syncwarp();
   } else if (warp == kWarpMma) {
     // ===== MMA issuer =====
+    SSQA_CTL_REGS();
     if (lane == 0) {
       for (long c = P.c_first; c <= P.c_last; ++c) {
         const long s = c - P.c_first;
@@ -845,8 +932,14 @@ __global__ void __launch_bounds__(32 * (3 + EPI), 1)
       }
     }
     __syncwarp();
+    mbar_wait(&ctl->done, 0);
+    tc_fence_after();
+    const uint32_t ncols = (F4 || 2 * acc_cols > 256) ? 512u : 256u;
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(ncols));
   } else if (warp == kWarpLoader) {
     // ===== state loader: delayed-spin tile + accumulator chunks =====
+    SSQA_CTL_REGS();
     if (lane == 0) {
       int* ring = ctl->ring[1];
       const uint64_t pol_first = policy_evict_first();
@@ -891,8 +984,11 @@ __global__ void __launch_bounds__(32 * (3 + EPI), 1)
       }
     }
     __syncwarp();
+  } else if (warp >= EPI) {
+    SSQA_CTL_REGS();  // the idle fourth warp of the control warpgroup
   } else {
     // ===== epilogue =====
+    SSQA_EPI_REGS();
     const int ew = warp;  // 0 .. EPI-1
     const int q = warp & 3;   // TMEM lane quarter this warp may access
     const int sub = ew >> 2;
@@ -1070,18 +1166,8 @@ __global__ void __launch_bounds__(32 * (3 + EPI), 1)
             tt.active = 0;
             tt.cycles_used = c;
           }
-          if (improved >= 0) {
-            int8_t* dstp = P.best_state + size_t(tg) * g.n;
-            const size_t colg = size_t(col0 + t * g.R + improved);
-            if (F4) {
-              const uint8_t* sp = P.sig_base + size_t(cur) * (P.slot_elems / 2) + colg * (g.npad / 2);
-              for (int i = lane; i < g.n; i += 32)
-                dstp[i] = ((sp[i >> 1] >> (4 * (i & 1))) & 8) ? -1 : 1;
-            } else {
-              const int8_t* sp = P.sig + size_t(cur) * P.slot_elems + colg * g.npad;
-              for (int i = lane; i < g.n; i += 32) dstp[i] = sp[i];
-            }
-          }
+          if (improved >= 0)
+            snap_best_state<F4>(P, cur, size_t(col0 + t * g.R + improved), tg, g.npad, lane);
           __syncwarp();
         }
       }
@@ -1104,28 +1190,30 @@ __global__ void __launch_bounds__(32 * (3 + EPI), 1)
         drain = !any;
       }
     }
-  }
-  __syncthreads();
-
-  if (P.run_mode) {
-    for (int t = threadIdx.x; t < ntl; t += blockDim.x) {
-      const int tg = tile * g.tpt + t;
-      P.best_e[tg] = trials[t].best_e;
-      P.best_k[tg] = trials[t].best_k;
-      P.reached[tg] = trials[t].reached;
-      P.first_hit[tg] = trials[t].first_hit;
-      P.cycles_used[tg] = trials[t].cycles_used;
-      P.active[tg] = trials[t].active;
+    // results of this CTA's trials (the epilogue warps own the trial table)
+    epi_bar<EPI>();
+    if (P.run_mode) {
+      for (int t = ew; t < ntl; t += EPI)
+        expand_best_state<F4>(P, tile * g.tpt + t, g.n, g.npad, lane);
+      for (int t = ew * 32 + lane; t < ntl; t += 32 * EPI) {
+        const int tg = tile * g.tpt + t;
+        P.best_e[tg] = trials[t].best_e;
+        P.best_k[tg] = trials[t].best_k;
+        P.reached[tg] = trials[t].reached;
+        P.first_hit[tg] = trials[t].first_hit;
+        P.cycles_used[tg] = trials[t].cycles_used;
+        P.active[tg] = trials[t].active;
+      }
     }
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&ctl->done);
   }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == kWarpMma) {
-    const uint32_t ncols = (F4 || 2 * acc_cols > 256) ? 512u : 256u;
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
-                 "r"(ncols));
-  }
+  // No code after the role branches: each role runs to the end on its own
+  // register budget (the MMA warp releases TMEM once the epilogue is done).
 }
+#undef SSQA_CTL_REGS
+#undef SSQA_EPI_REGS
 
 // ------------------------------------------------------------------- host side
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
@@ -1179,7 +1267,9 @@ Layout pick_layout(int NT, int tpt, int nsubs, int tile_row) {
   return make_layout(NT, tpt, 2, nsubs, tile_row);
 }
 
-constexpr int kDefaultEpi = 12;
+// 16 epilogue warps (4 per scheduler): the update chain is latency-bound,
+// so more resident warps beat more registers per warp (C3: -5 %/sweep vs 12).
+constexpr int kDefaultEpi = 16;
 
 template <int EPI, bool F4>
 cudaError_t launch_variant(int grid, int smem, cudaStream_t st, const CUtensorMap* maps,
@@ -1187,7 +1277,7 @@ cudaError_t launch_variant(int grid, int smem, cudaStream_t st, const CUtensorMa
   cudaError_t e = cudaFuncSetAttribute(k_sweep_tc<EPI, F4>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  k_sweep_tc<EPI, F4><<<grid, 32 * (3 + EPI), smem, st>>>(maps[0], maps[1], maps[2], maps[3], P);
+  k_sweep_tc<EPI, F4><<<grid, 32 * (4 + EPI), smem, st>>>(maps[0], maps[1], maps[2], maps[3], P);
   return cudaSuccess;
 }
 
@@ -1201,7 +1291,29 @@ __global__ void k_pack_fp4(const int8_t* __restrict__ src, uint8_t* __restrict__
   }
 }
 
+// Mapped host record of the device watchdog (see watchdog_fire); one per
+// process, bound to every device the engine launches on.
+WatchdogRec* g_host_wd = nullptr;
+unsigned long long g_wd_devices = 0;  // bit d: g_watchdog set on device d
+
+void watchdog_bind(int device) {
+  if (device < 0 || device >= 64 || (g_wd_devices >> device) & 1ull) return;
+  if (!g_host_wd) {
+    void* h = nullptr;
+    if (cudaHostAlloc(&h, sizeof(WatchdogRec), cudaHostAllocMapped | cudaHostAllocPortable) !=
+        cudaSuccess)
+      return;
+    std::memset(h, 0, sizeof(WatchdogRec));
+    g_host_wd = static_cast<WatchdogRec*>(h);
+  }
+  void* d = nullptr;
+  if (cudaHostGetDevicePointer(&d, g_host_wd, 0) != cudaSuccess) return;
+  if (cudaMemcpyToSymbol(g_watchdog, &d, sizeof(d)) == cudaSuccess)
+    g_wd_devices |= 1ull << device;
+}
+
 int launch(ssqa_batch_s* b, TcParams& P, bool f4) {
+  watchdog_bind(b->prob->device);
   const Geom& g = b->g;
   CUtensorMap maps[4];
   const uint64_t srows = uint64_t(b->nslots) * g.ccols;
@@ -1223,7 +1335,7 @@ int launch(ssqa_batch_s* b, TcParams& P, bool f4) {
     return SSQA_ECUDA;
   }
   const char* env_epi = getenv("SSQA_TC_EPI");
-  const int epi = (env_epi && atoi(env_epi) == 16) ? 16 : kDefaultEpi;
+  const int epi = env_epi ? (atoi(env_epi) == 12 ? 12 : 16) : kDefaultEpi;
   Layout L = pick_layout(g.tile_cols, g.tpt, epi / 4, int(tile_row));
   if (const char* st = getenv("SSQA_TC_STAGES")) {  // experiment overrides
     const char* np = getenv("SSQA_TC_NPS");
@@ -1319,6 +1431,7 @@ TcParams base_params(ssqa_batch_s* b) {
   P.cycles_used = b->d_cycles_used;
   P.active = b->d_active;
   P.best_state = b->d_best_state;
+  P.best_packed = b->d_best_packed;
   P.trace = b->d_trace;
   return P;
 }
@@ -1402,5 +1515,16 @@ int tc_sweep(ssqa_batch_s* b, double jperp, double i0) {
 }
 
 const char* tc_last_error() { return g_tc_err.c_str(); }
+
+std::string tc_watchdog_message() {
+  if (!g_host_wd || !reinterpret_cast<volatile WatchdogRec*>(g_host_wd)->fired) return "";
+  const volatile WatchdogRec* w = g_host_wd;
+  char buf[160];
+  std::snprintf(buf, sizeof(buf),
+                " [k_sweep_tc watchdog: block %d warp %d lane %d stuck on mbarrier smem 0x%x "
+                "parity %u]",
+                w->block, w->warp, w->lane, w->addr, w->parity);
+  return buf;
+}
 
 }  // namespace ssqa_engine

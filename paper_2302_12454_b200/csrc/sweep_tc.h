@@ -1,6 +1,8 @@
 // sweep_tc.h -- the fused tcgen05 sweep engine (SSQA_ENGINE_TCGEN05).
 #pragma once
 
+#include <string>
+
 #include "engine.h"
 #include "simt_kernels.cuh"
 
@@ -13,5 +15,7 @@ int tc_run(ssqa_batch_s* b, const ScanArgs& sa);
 // One sweep at b->cycle without a scan (per-step API).
 int tc_sweep(ssqa_batch_s* b, double jperp, double i0);
 const char* tc_last_error();
+// Non-empty after a kernel watchdog fired: who was stuck on which mbarrier.
+std::string tc_watchdog_message();
 
 }  // namespace ssqa_engine
