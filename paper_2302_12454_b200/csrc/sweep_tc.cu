@@ -41,7 +41,10 @@ constexpr int kBM = 128;          // rows (spins i) per MMA tile
 constexpr int kBK = 128;          // K bytes per stage (one 128B swizzle row)
 constexpr int kCW = 8;  // columns per epilogue chunk (one tcgen05.ld .x8)
 #ifndef SSQA_ABL
-#define SSQA_ABL 0  // timing ablations (scripts/build_ablations.sh); 0 in the product
+// Timing ablations (scripts/build_ablations.sh), 0 in the product: 16 no energy
+// reduction, 32 no spin store, 64 no accumulator store, 128 no accumulator
+// stream (stale smem), 256 no TMEM load.
+#define SSQA_ABL 0
 #endif
 #ifndef SSQA_ENERGY_RED
 #define SSQA_ENERGY_RED 1  // 1: shuffle transpose-reduce, 0: per-column redux.sync
@@ -141,15 +144,16 @@ __device__ __forceinline__ bool mbar_try_sleep(uint32_t a, uint32_t parity) {
 // Watchdog record in mapped host memory (set by tc_watchdog_init): a wait
 // that makes no progress for ~20 s writes who is stuck and traps instead of
 // hanging the device; the host prints the record when the launch fails.
-// Everything here is inline -- no printf/ABI calls -- so the warp roles keep
-// their own setmaxnreg register budgets.
+// No printf: a vprintf call in the kernel makes ptxas budget every role at
+// the smallest setmaxnreg count; a plain out-of-line function (the cold
+// path) keeps the per-role budgets and the hot loops short.
 struct WatchdogRec {
   int fired, block, warp, lane;
   unsigned addr, parity;
 };
 __device__ WatchdogRec* g_watchdog = nullptr;
 
-__device__ __forceinline__ void watchdog_fire(uint32_t a, uint32_t parity) {
+__device__ __noinline__ void watchdog_fire(uint32_t a, uint32_t parity) {
   WatchdogRec* w = g_watchdog;
   if (w && atomicCAS(&w->fired, 0, 1) == 0) {
     volatile WatchdogRec* v = w;
@@ -506,8 +510,13 @@ __device__ __forceinline__ void epi_chunks(const EpiRow& er, const UpdateConsts&
     const int cb = ch * kCW;
     const int slot = sub * nps + sidx;
     int32_t v[kCW];
-    tmem_ld8(trow + uint32_t(cb), v);
-    mbar_wait(&ctl->afull[slot], ph);
+    if (SSQA_ABL & 256) {
+#pragma unroll
+      for (int j = 0; j < kCW; ++j) v[j] = int(trow) + cb + j;
+    } else {
+      tmem_ld8(trow + uint32_t(cb), v);
+    }
+    if (!(SSQA_ABL & 128)) mbar_wait(&ctl->afull[slot], ph);
     if (++sidx == nps) {
       sidx = 0;
       ph ^= 1;
@@ -599,7 +608,7 @@ __device__ __forceinline__ void epi_chunks(const EpiRow& er, const UpdateConsts&
                 (cw.y & 0x80000000u) && er.nib_live);
     }
     __syncwarp();
-    if (lane == 0) mbar_arrive(&ctl->aempty[slot]);
+    if (lane == 0 && !(SSQA_ABL & 128)) mbar_arrive(&ctl->aempty[slot]);
     if (SSQA_ABL & 16) {
     } else if (FAST && (SSQA_ENERGY_RED == 1)) {
       // transpose-reduce the 8 column partials across the warp with shuffles:
@@ -968,7 +977,7 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
           // subgroup's own ring (slots [sub*nps, sub*nps + nps)): each slot is
           // consumed, in order, by a single subgroup, so no consumer can ever
           // wait on a slot barrier two phases ahead (parity aliasing).
-          for (int ch = 0; ch < nchunk; ++ch) {
+          for (int ch = 0; ch < nchunk && !(SSQA_ABL & 128); ++ch) {
             const int sb2 = ch % nsubs;
             const uint32_t cnt = acc_it * uint32_t(chunks_of(sb2)) + uint32_t(ch / nsubs);
             const int slot = sb2 * nps + int(cnt % uint32_t(nps));

@@ -1,0 +1,4 @@
+#!/bin/bash
+cd "$GRAFT_REPO_ROOT" || cd /root/repo
+timeout 120 python scripts/prof_run.py c3 tcgen05 300 2>&1 | tail -1
+for a in 256 384; do SSQA_LIB_PATH=ablbuild/libssqa_abl$a.so timeout 120 python scripts/prof_run.py c3 tcgen05 300 2>&1 | tail -1; done
