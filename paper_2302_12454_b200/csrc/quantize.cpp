@@ -10,9 +10,14 @@
 // -- the only rounding left is the final "+ offset", which the device
 // performs with the same operands.  Models with no such p (non-dyadic
 // couplings) or |J'| > 127 are rejected: the engine has no CPU fallback.
+#include <algorithm>
+#include <atomic>
+#include <climits>
 #include <cmath>
 #include <cstdlib>
 #include <string>
+#include <thread>
+#include <vector>
 
 #include "engine.h"
 
@@ -23,18 +28,46 @@ namespace {
 // Smallest p in [0, 62] with v * 2^p integral, or -1.
 int dyadic_exponent(double v) {
   if (!std::isfinite(v)) return -1;
-  if (v == 0.0) return 0;
-  for (int p = 0; p <= 62; ++p) {
+  if (v == std::floor(v)) return 0;  // integers (every BASELINE coupling)
+  for (int p = 1; p <= 62; ++p) {
     double x = std::ldexp(v, p);
     if (x == std::floor(x)) return p;
   }
   return -1;
 }
 
+// f(lo, hi) over [0, n) on all hardware threads (n up to 2^20 rows).
+template <class F>
+void parallel_for(int n, F&& f) {
+  const int nt = std::max(1, std::min<int>(int(std::thread::hardware_concurrency()), n / 32 + 1));
+  if (nt == 1) {
+    f(0, n);
+    return;
+  }
+  std::vector<std::thread> th;
+  for (int t = 0; t < nt; ++t) {
+    const int lo = int(int64_t(n) * t / nt), hi = int(int64_t(n) * (t + 1) / nt);
+    th.emplace_back([&f, lo, hi] { f(lo, hi); });
+  }
+  for (auto& x : th) x.join();
+}
+
+void atomic_max(std::atomic<int>& a, int v) {
+  int cur = a.load();
+  while (v > cur && !a.compare_exchange_weak(cur, v)) {
+  }
+}
+void atomic_min(std::atomic<long long>& a, long long v) {
+  long long cur = a.load();
+  while (v < cur && !a.compare_exchange_weak(cur, v)) {
+  }
+}
+
 }  // namespace
 
 int quantize(int n, const double* h, const double* J, double offset, Quantized* q,
              std::string* why) {
+  // scale exponent: the largest dyadic exponent of any bias or coupling
   int p = 0;
   for (int i = 0; i < n; ++i) {
     int e = dyadic_exponent(h[i]);
@@ -44,14 +77,31 @@ int quantize(int n, const double* h, const double* J, double offset, Quantized* 
     }
     if (e > p) p = e;
   }
-  for (size_t v = 0; v < size_t(n) * n; ++v) {
-    int e = dyadic_exponent(J[v]);
-    if (e < 0) {
+  {
+    std::atomic<int> pmax{p};
+    std::atomic<long long> bad{LLONG_MAX};  // first non-dyadic coupling (row-major index)
+    parallel_for(n, [&](int lo, int hi) {
+      int pl = 0;
+      for (int r = lo; r < hi; ++r) {
+        const double* row = J + size_t(r) * n;
+        for (int c = 0; c < n; ++c) {
+          const int e = dyadic_exponent(row[c]);
+          if (e < 0) {
+            atomic_min(bad, (long long)r * n + c);
+            break;
+          }
+          if (e > pl) pl = e;
+        }
+      }
+      atomic_max(pmax, pl);
+    });
+    if (bad.load() != LLONG_MAX) {
+      const long long v = bad.load();
       *why = "coupling " + std::to_string(v / n) + "," + std::to_string(v % n) +
              " is not a dyadic rational";
       return SSQA_EUNSUP;
     }
-    if (e > p) p = e;
+    p = pmax.load();
   }
   q->n = n;
   q->npad = (n + 127) / 128 * 128;
@@ -63,46 +113,65 @@ int quantize(int n, const double* h, const double* J, double offset, Quantized* 
   q->max_abs_j = 0;
   q->max_abs_h = 0;
   // Row i of J' holds the coefficients the reference multiplies into field
-  // i: jpad[j*stride + i] = coupling_row(j)[i] (annealer.cpp:52-55, 107).
-  for (int i = 0; i < n; ++i) {
-    for (int j = 0; j < n; ++j) {
-      double x = std::ldexp(J[size_t(j) * n + i], p);
-      if (std::fabs(x) > 127.0) {
-        *why = "coupling magnitude exceeds int8 at scale 2^" + std::to_string(p);
-        return SSQA_EUNSUP;
+  // i: jpad[j*stride + i] = coupling_row(j)[i] (annealer.cpp:52-55, 107) --
+  // a transpose of the (row-major) model matrix, done in 64x64 blocks.
+  {
+    constexpr int kB = 64;
+    const int nb = (n + kB - 1) / kB;
+    std::atomic<int> maxj{0};
+    std::atomic<bool> overflow{false};
+    parallel_for(nb, [&](int lo, int hi) {
+      int ml = 0;
+      for (int bi = lo; bi < hi; ++bi) {
+        const int i0 = bi * kB, i1 = std::min(n, i0 + kB);
+        for (int j0 = 0; j0 < n; j0 += kB) {
+          const int j1 = std::min(n, j0 + kB);
+          for (int j = j0; j < j1; ++j) {
+            const double* src = J + size_t(j) * n;
+            for (int i = i0; i < i1; ++i) {
+              const double x = p ? std::ldexp(src[i], p) : src[i];
+              if (std::fabs(x) > 127.0) {
+                overflow = true;
+                return;
+              }
+              const int v = int(x);
+              q->J[size_t(i) * q->npad + j] = int8_t(v);
+              ml = std::max(ml, std::abs(v));
+            }
+          }
+        }
       }
-      int v = int(x);
-      q->J[size_t(i) * q->npad + j] = int8_t(v);
-      if (std::abs(v) > q->max_abs_j) q->max_abs_j = std::abs(v);
+      atomic_max(maxj, ml);
+    });
+    if (overflow.load()) {
+      *why = "coupling magnitude exceeds int8 at scale 2^" + std::to_string(p);
+      return SSQA_EUNSUP;
     }
+    q->max_abs_j = maxj.load();
   }
   // FP4 (e2m1) image: representable integers 0, 1, 2, 3, 4, 6 (+ sign).
   {
-    auto code = [](int v) -> int {
-      const int a = v < 0 ? -v : v;
-      int c;
-      switch (a) {
-        case 0: c = 0; break;
-        case 1: c = 2; break;
-        case 2: c = 4; break;
-        case 3: c = 5; break;
-        case 4: c = 6; break;
-        case 6: c = 7; break;
-        default: return -1;
-      }
-      return c | (v < 0 ? 8 : 0);
-    };
-    q->fp4_ok = true;
-    q->J4.assign(size_t(q->npad) * (q->npad / 2), 0);
-    for (int i = 0; i < q->npad && q->fp4_ok; ++i) {
-      for (int j = 0; j < q->npad; ++j) {
-        const int c = code(q->J[size_t(i) * q->npad + j]);
-        if (c < 0) {
-          q->fp4_ok = false;
-          break;
+    static const int kCode[9] = {0, 2, 4, 5, 6, -1, 7, -1, -1};  // |v| -> e2m1 magnitude code
+    q->fp4_ok = q->max_abs_j <= 6 && q->max_abs_j != 5;
+    if (q->fp4_ok) {
+      q->J4.assign(size_t(q->npad) * (q->npad / 2), 0);
+      std::atomic<bool> ok{true};
+      parallel_for(q->npad, [&](int lo, int hi) {
+        for (int i = lo; i < hi; ++i) {
+          const int8_t* row = &q->J[size_t(i) * q->npad];
+          uint8_t* out = &q->J4[size_t(i) * (q->npad / 2)];
+          for (int j = 0; j < q->npad; ++j) {
+            const int v = row[j];
+            const int c = kCode[v < 0 ? -v : v];
+            if (c < 0) {
+              ok = false;
+              return;
+            }
+            out[j / 2] |= uint8_t((c | (v < 0 ? 8 : 0)) << (4 * (j & 1)));
+          }
         }
-        q->J4[size_t(i) * (q->npad / 2) + j / 2] |= uint8_t(c << (4 * (j & 1)));
-      }
+      });
+      q->fp4_ok = ok.load();
     }
     if (!q->fp4_ok) q->J4.clear();
   }

@@ -1,6 +1,9 @@
 // host/instances.cpp -- C entry points of include/ssqa_host.h.
+#include <algorithm>
 #include <cstring>
 #include <exception>
+#include <thread>
+#include <vector>
 #include <stdexcept>
 #include <string>
 
@@ -33,6 +36,18 @@ int guard(F&& f) {
 constexpr uint32_t kStreamDenseCoupling = 8;
 constexpr uint32_t kStreamDenseBias = 9;
 
+// Run f(lo, hi) over [0, n) on all hardware threads.
+template <class F>
+void parallel_rows(int n, F&& f) {
+  const int nt = std::max(1, std::min<int>(int(std::thread::hardware_concurrency()), n / 64 + 1));
+  std::vector<std::thread> th;
+  for (int t = 0; t < nt; ++t) {
+    const int lo = int(int64_t(n) * t / nt), hi = int(int64_t(n) * (t + 1) / nt);
+    th.emplace_back([&f, lo, hi] { f(lo, hi); });
+  }
+  for (auto& x : th) x.join();
+}
+
 }  // namespace
 
 extern "C" {
@@ -56,17 +71,22 @@ int ssqa_dense_ising(int n, int kind, uint64_t seed, double* h, double* J, doubl
     if (n < 1) throw std::invalid_argument("n must be >= 1");
     if (kind != 0 && kind != 1) throw std::invalid_argument("kind must be 0 or 1");
     const ssqa::CounterRng cj(seed, kStreamDenseCoupling), ch(seed, kStreamDenseBias);
-    for (int i = 0; i < n; ++i) {
-      J[size_t(i) * n + i] = 0.0;
-      h[i] = kind == 0 ? double(int(ch.below(uint64_t(i), 16)) - 8) : 0.0;
-      for (int j = i + 1; j < n; ++j) {
-        const uint64_t c = uint64_t(i) * uint64_t(n) + uint64_t(j);
-        const double v = kind == 0 ? double(int(cj.below(c, 16)) - 8)
-                                   : ((cj.raw(c) >> 63) ? 1.0 : -1.0);
-        J[size_t(i) * n + j] = v;
-        J[size_t(j) * n + i] = v;
+    // Coupling (i, j), i < j, is drawn at counter i*n + j; every row is
+    // filled independently (the mirror entries recompute their draw), so the
+    // matrix is written sequentially by all threads.
+    auto draw = [&](int a, int b) {  // a < b
+      const uint64_t c = uint64_t(a) * uint64_t(n) + uint64_t(b);
+      return kind == 0 ? double(int(cj.below(c, 16)) - 8) : ((cj.raw(c) >> 63) ? 1.0 : -1.0);
+    };
+    parallel_rows(n, [&](int lo, int hi) {
+      for (int i = lo; i < hi; ++i) {
+        double* row = J + size_t(i) * n;
+        h[i] = kind == 0 ? double(int(ch.below(uint64_t(i), 16)) - 8) : 0.0;
+        for (int j = 0; j < i; ++j) row[j] = draw(j, i);
+        row[i] = 0.0;
+        for (int j = i + 1; j < n; ++j) row[j] = draw(i, j);
       }
-    }
+    });
     *offset = 0.0;
   });
 }
