@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <string>
@@ -113,7 +114,11 @@ int num_sms(int device) {
 }
 
 // Column tiling: whole trials per tile, as few tiles as the SM count allows.
-Geom make_geom(int n, int npad, int R, int T, int sms, int engine) {
+// tcgen05 engine, large problems: when there are few column tiles and many
+// row tiles, widen the tiles (more trials per tile -> each J' row tile is
+// streamed by fewer CTAs, larger MMA N) and split each tile's rows over rs
+// CTAs (row split, one CTA per SM).  fp4: FP4 operands need tile_cols <= 240.
+Geom make_geom(int n, int npad, int R, int T, int sms, int engine, bool fp4) {
   Geom g;
   g.n = n;
   g.npad = npad;
@@ -124,11 +129,30 @@ Geom make_geom(int n, int npad, int R, int T, int sms, int engine) {
   if (R <= max_cols) tpt = std::min(tpt, max_cols / R);
   else tpt = 1;
   tpt = std::max(1, std::min(tpt, T));
-  (void)engine;
+  int rs = 1;
+  const int nrt = npad / 128;
+  if (engine == SSQA_ENGINE_TCGEN05 && R <= max_cols) {
+    const int cap = fp4 ? 240 : max_cols;
+    const int wide = std::max(1, std::min(T, cap / R));
+    const int wtiles = (T + wide - 1) / wide;
+    // worth it when the wide tiling still fills the SMs with >= 2 parts per tile
+    if (nrt >= 16 && wide > tpt && wtiles * 2 <= sms) {
+      tpt = wide;
+      rs = std::min(nrt, sms / wtiles);
+    }
+    if (const char* env = getenv("SSQA_TC_RS")) {  // test / tuning override
+      const int want = atoi(env);
+      if (want >= 1) {
+        const int tiles = (T + tpt - 1) / tpt;
+        rs = std::max(1, std::min({want, nrt, std::max(1, sms / tiles)}));
+      }
+    }
+  }
   g.tpt = tpt;
   g.tile_cols = (tpt * R + 15) / 16 * 16;
   g.ntiles = (T + tpt - 1) / tpt;
   g.ccols = g.ntiles * g.tile_cols;
+  g.rs = rs;
   return g;
 }
 
@@ -341,7 +365,7 @@ int create_batch(ssqa_problem pr, const ssqa_params_c* p, int trials, int record
   b->record_trace = record_trace;
   b->d = p->delay;
   b->nslots = p->delay + 3;
-  b->g = make_geom(pr->q.n, pr->q.npad, p->r, trials, num_sms(pr->device), eng);
+  b->g = make_geom(pr->q.n, pr->q.npad, p->r, trials, num_sms(pr->device), eng, pr->q.fp4_ok);
   b->slot_elems = size_t(b->g.ccols) * b->g.npad;
   b->phys.assign(size_t(b->d) + 1, 0);
   const int T = trials;
@@ -471,7 +495,7 @@ int ssqa_batch_destroy(ssqa_batch b) {
   if (!b) return SSQA_OK;
   cudaSetDevice(b->prob->device);
   cudaStreamSynchronize(b->prob->stream);
-  for (void* ptr : {(void*)b->d_sig, (void*)b->d_sig4, (void*)b->d_acc, (void*)b->d_seeds, (void*)b->d_jperp, (void*)b->d_i0,
+  for (void* ptr : {(void*)b->d_sig, (void*)b->d_sig4, (void*)b->d_acc, (void*)b->d_seeds, (void*)b->d_jperp, (void*)b->d_i0, b->d_split,
                     (void*)b->d_S, (void*)b->d_E, (void*)b->d_best_e, (void*)b->d_best_k,
                     (void*)b->d_reached, (void*)b->d_first_hit, (void*)b->d_cycles_used,
                     (void*)b->d_active, (void*)b->d_best_state, (void*)b->d_best_packed,

@@ -27,8 +27,11 @@ struct Geom {
   int R = 0, T = 0;        // replicas, trials
   int tpt = 0;             // trials per column tile
   int tile_cols = 0;       // columns per tile (multiple of 16, >= tpt*R)
-  int ntiles = 0;
+  int ntiles = 0;          // column tiles
   int ccols = 0;           // ntiles * tile_cols
+  // tcgen05 row split: each column tile is processed by rs CTAs, CTA b owning
+  // a contiguous range of row tiles (rs = 1: one CTA runs all rows).
+  int rs = 1;
 };
 
 struct Quantized {
@@ -78,6 +81,11 @@ struct ssqa_batch_s {
   double* d_acc = nullptr;    // [ccols][npad]
   uint64_t* d_seeds = nullptr;
   double* d_jperp = nullptr;  // [sc+1] jperp_schedule table
+  // tcgen05 row split (g.rs > 1): cross-CTA state, zeroed per launch --
+  //   gE [2][ccols] int64 energy sums, rows [ntiles][npad/128] row-ready
+  //   pass stamps, arrive [ntiles] pass arrivals, scan [ntiles] scan stamps
+  void* d_split = nullptr;
+  size_t split_bytes = 0;
   // SSA batches (annealer.cpp:489-501): R = 1, delay = 0, jperp = 0 and the
   // accumulator bound follows i0_schedule (annealer.cpp:403-408) per cycle.
   bool ssa = false;

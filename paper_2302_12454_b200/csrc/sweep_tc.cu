@@ -96,7 +96,35 @@ struct TcParams {
   int8_t* best_state;
   uint8_t* best_packed;  // [T][npad] bytes: best spin column in slot format
   double* trace;
+  // row split (g.rs > 1): see ssqa_batch_s::d_split
+  unsigned long long* gE;  // [2][ccols]
+  int* g_rows;             // [ntiles][npad/128] pass stamp s+1: rows of pass s written
+  unsigned* g_arrive;      // [ntiles] CTAs of the column tile done with their pass
+  long long* g_scan;       // [ntiles] (s+1) | stop << 62 once pass s is scanned
 };
+
+// gpu-scope release/acquire helpers for the row-split protocol
+__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ long long ld_acquire_gpu(const long long* p) {
+  long long v;
+  asm volatile("ld.acquire.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_gpu(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void st_release_gpu(long long* p, long long v) {
+  asm volatile("st.release.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned atom_add_acq_rel_gpu(unsigned* p, unsigned v) {
+  unsigned old;
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
 
 // ---------------------------------------------------------------- PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -428,6 +456,8 @@ struct SmemCtl {
   uint64_t done;       // epilogue finished (TMEM may be released)
   uint32_t tmem_base;
   long last_pass;  // last cycle any role may start (stop-at-target drain)
+  int scan_me;     // row split: this CTA scans the pass (last arrival)
+  int scan_stop;   // row split: the column tile's trials have all stopped
   // slot ring per role (producer, loader, epilogue): [0] = cur, [1 + q] = phys[q]
   int ring[3][kMaxDelay + 2];
 };
@@ -744,12 +774,19 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
   // scheduler favours higher warp ids, so the TMA producer, MMA issuer and
   // state loader are never starved by the EPI busy epilogue warps.
   constexpr int kWarpProducer = EPI, kWarpMma = EPI + 1, kWarpLoader = EPI + 2;
-  const int tile = blockIdx.x;
+  // CTA = (column tile, row part): with a row split (g.rs > 1) the rs CTAs of
+  // a column tile share its columns and own contiguous ranges of row tiles.
+  const int RS = g.rs;
+  const bool split = RS > 1;
+  const int tile = blockIdx.x / RS, part = blockIdx.x % RS;
   const int col0 = tile * NT;
   const int ntl = max(0, min(g.tpt, g.T - tile * g.tpt));
+  const int NRT_all = g.npad / kBM;
+  const int rt_lo = int((long long)NRT_all * part / RS);
+  const int NRT = int((long long)NRT_all * (part + 1) / RS) - rt_lo;  // row tiles of this CTA
   // one stage = 128 bytes of K per row: 128 int8 or 256 e2m1 couplings/spins
   // (an FP4 row of npad = 128 is a partial chunk: TMA zero-fills the rest)
-  const int NRT = g.npad / kBM, NKC = F4 ? (g.npad + 2 * kBK - 1) / (2 * kBK) : g.npad / kBK;
+  const int NKC = F4 ? (g.npad + 2 * kBK - 1) / (2 * kBK) : g.npad / kBK;
   const int nchunk = NT / kCW;
   const int acc_cols = NT;
   constexpr int nsubs = EPI / 4;         // epilogue subgroups (4 warps each)
@@ -882,15 +919,23 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
           for (int kc = 0; kc < NKC; ++kc, ++it) {
             if (s > 0 && rt == 0) {
               // the spin rows of this K chunk were written by pass c-1
-              const int need = min(nrg - 1, min(NRT - 1, ((kc + 1) * kKRows - 1) / kBM) / rgroup);
-              while (waited <= need) rows_wait(s - 1, waited++);
+              if (split) {
+                // ... by the CTAs owning them (row-ready pass stamps)
+                const int r1 = min(NRT_all, ((kc + 1) * kKRows + kBM - 1) / kBM);
+                for (int r = kc * kKRows / kBM; r < r1; ++r)
+                  while (ld_acquire_gpu(&P.g_rows[tile * NRT_all + r]) < int(s)) __nanosleep(64);
+                asm volatile("fence.proxy.async.global;" ::: "memory");
+              } else {
+                const int need = min(nrg - 1, min(NRT - 1, ((kc + 1) * kKRows - 1) / kBM) / rgroup);
+                while (waited <= need) rows_wait(s - 1, waited++);
+              }
             }
             const int st = it % stages;
             const uint32_t ph = (it / stages) & 1;
             mbar_wait(&ctl->empty[st], ph ^ 1);
             mbar_expect_tx(&ctl->full[st], L.a_bytes + L.b_bytes);
-            tma_load_2d_hint(&tmJ, &ctl->full[st], sA + size_t(st) * L.a_bytes, kc * kBK, rt * kBM,
-                             pol_keep);
+            tma_load_2d_hint(&tmJ, &ctl->full[st], sA + size_t(st) * L.a_bytes, kc * kBK,
+                             (rt_lo + rt) * kBM, pol_keep);
             tma_load_2d(&tmS, &ctl->full[st], sB + size_t(st) * L.b_bytes, kc * kBK, yS);
           }
         }
@@ -972,7 +1017,7 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
           DBG_STAMP(1, acc_it, 0);
           mbar_expect_tx(&ctl->sfull[sb], uint32_t(NT) * kTileRow);
           tma_load_2d(&tmSe, &ctl->sfull[sb], sig_tiles + size_t(sb) * NT * kTileRow,
-                      rt * kTileRow, ySrc);
+                      (rt_lo + rt) * kTileRow, ySrc);
           // chunk ch belongs to epilogue subgroup ch % nsubs and lands in that
           // subgroup's own ring (slots [sub*nps, sub*nps + nps)): each slot is
           // consumed, in order, by a single subgroup, so no consumer can ever
@@ -985,7 +1030,7 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
             mbar_wait(&ctl->aempty[slot], ph ^ 1);
             mbar_expect_tx(&ctl->afull[slot], kCW * kBM * 8);
             tma_load_2d_hint(&tmA, &ctl->afull[slot], acc_ring + size_t(slot) * kCW * kBM,
-                             rt * kBM, col0 + ch * kCW, pol_first);
+                             (rt_lo + rt) * kBM, col0 + ch * kCW, pol_first);
           }
           DBG_STAMP(1, acc_it, 1);
         }
@@ -994,7 +1039,23 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
     }
     __syncwarp();
   } else if (warp >= EPI) {
-    SSQA_CTL_REGS();  // the idle fourth warp of the control warpgroup
+    // ===== row-ready publisher (row split only): once this CTA's epilogue has
+    // written a group of its row tiles in pass c, stamp them for the other
+    // CTAs of the column tile (their producers load all rows of sigma) =====
+    SSQA_CTL_REGS();
+    if (split && lane == 0) {
+      for (long c = P.c_first; c <= P.c_last; ++c) {
+        const long s = c - P.c_first;
+        if (s > 0 && stop_at(c)) break;
+        for (int b = 0; b < nrg; ++b) {
+          rows_wait(s, b);
+          __threadfence();
+          const int r1 = min(NRT, (b + 1) * rgroup);
+          for (int r = b * rgroup; r < r1; ++r)
+            st_release_gpu(&P.g_rows[tile * NRT_all + rt_lo + r], int(s + 1));
+        }
+      }
+    }
   } else {
     // ===== epilogue =====
     SSQA_EPI_REGS();
@@ -1047,7 +1108,7 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
         const int buf = acc_it & 1;
         const uint32_t aph = (acc_it >> 1) & 1;
         const int il = q * 32 + lane;  // row within the tile
-        const int i = rt * kBM + il;
+        const int i = (rt_lo + rt) * kBM + il;
         const bool row_live = i < g.n;
         const uint32_t trow = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(buf * acc_cols);
         const uint8_t* stile = sig_tiles + size_t(buf) * NT * kTileRow;
@@ -1093,10 +1154,10 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
           er.pol_stream = pol_first;
           er.w_row = row_live;
           {
-            const int r0 = rt * kBM + q * 32 + 8 * (lane & 3);  // first row of this lane's word
+            const int r0 = (rt_lo + rt) * kBM + q * 32 + 8 * (lane & 3);  // first row of the word
             const int nl = min(8, max(0, g.n - r0));
             er.nib_live = nl >= 8 ? 0xffffffffu : ((1u << (4 * nl)) - 1u);
-            er.dst_w = sig_dst + (rt * kBM + q * 32) / 2 + 4 * (lane & 3);
+            er.dst_w = sig_dst + ((rt_lo + rt) * kBM + q * 32) / 2 + 4 * (lane & 3);
           }
 #define SSQA_EPI(B, S, F)                                                                  \
   epi_chunks<B, S, F, F4>(er, uc, fc, i2d, ctl, acc_ring, c_col, q_sum, trow, \
@@ -1129,9 +1190,47 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
         }
       }
       epi_bar<EPI>();
+      const long s_idx = c - P.c_first;
+      // energy partial sum of tile column cl over this CTA's rows
+      auto cta_energy = [&](int cl) -> long long {
+        long long ep = 0;
+        for (int qq = 0; qq < 4; ++qq)
+          ep += P.fast ? (long long)reinterpret_cast<const int*>(c_E + qq * NT)[cl]
+                       : c_E[qq * NT + cl];
+        return ep;
+      };
+      unsigned long long* gE_pass = split ? P.gE + size_t(s_idx & 1) * g.ccols + col0 : nullptr;
+      bool do_scan = P.run_mode && !drain;
+      if (split && P.run_mode && !drain) {
+        // Row split: add this CTA's row partials to the column tile's pass
+        // sums; the last CTA of the tile to arrive scans the pass.
+        for (int cl = ew * 32 + lane; cl < NT; cl += EPI * 32)
+          atomicAdd(gE_pass + cl, static_cast<unsigned long long>(cta_energy(cl)));
+        __threadfence();
+        epi_bar<EPI>();
+        if (ew == 0 && lane == 0) {
+          const unsigned old = atom_add_acq_rel_gpu(&P.g_arrive[tile], 1u);
+          ctl->scan_me = old == unsigned((s_idx + 1) * RS - 1);
+        }
+        epi_bar<EPI>();
+        do_scan = ctl->scan_me != 0;
+        if (do_scan) {
+          // the trial table as the previous pass's scanner left it
+          for (int t = ew * 32 + lane; t < ntl; t += 32 * EPI) {
+            const int tg = tile * g.tpt + t;
+            trials[t].best_e = __ldcg(P.best_e + tg);
+            trials[t].best_k = __ldcg(P.best_k + tg);
+            trials[t].reached = __ldcg(P.reached + tg);
+            trials[t].first_hit = __ldcg(reinterpret_cast<const long long*>(P.first_hit) + tg);
+            trials[t].cycles_used = __ldcg(reinterpret_cast<const long long*>(P.cycles_used) + tg);
+            trials[t].active = __ldcg(P.active + tg);
+          }
+          epi_bar<EPI>();
+        }
+      }
 
       // ===== scan (annealer.cpp:327-345), one warp per trial, lanes over replicas =====
-      if (P.run_mode && !drain) {
+      if (do_scan) {
         for (int t = ew; t < ntl; t += EPI) {
           TrialTab& tt = trials[t];
           if (!tt.active) continue;
@@ -1141,10 +1240,8 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
           double bmin = __longlong_as_double(0x7ff0000000000000LL);  // +inf
           int bk = 0x7fffffff;
           for (int k = lane; k < g.R; k += 32) {
-            long long ep = 0;
-            for (int qq = 0; qq < 4; ++qq)
-              ep += P.fast ? (long long)reinterpret_cast<const int*>(c_E + qq * NT)[t * g.R + k]
-                           : c_E[qq * NT + t * g.R + k];
+            const long long ep = split ? (long long)__ldcg(gE_pass + t * g.R + k)
+                                       : cta_energy(t * g.R + k);
             const double ek = __dadd_rn(__dmul_rn(-0.5, scaled(ep, P.scale)), P.offset);
             if (P.record_trace) P.trace[(size_t(tg) * (P.sc + 1) + c) * g.R + k] = ek;
             if (ek < bmin) {
@@ -1181,11 +1278,48 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
         }
       }
       epi_bar<EPI>();
+      if (split && P.run_mode && !drain) {
+        if (do_scan) {
+          // publish the scan: trial table -> global, clear the pass sums
+          for (int t = ew * 32 + lane; t < ntl; t += 32 * EPI) {
+            const int tg = tile * g.tpt + t;
+            P.best_e[tg] = trials[t].best_e;
+            P.best_k[tg] = trials[t].best_k;
+            P.reached[tg] = trials[t].reached;
+            P.first_hit[tg] = trials[t].first_hit;
+            P.cycles_used[tg] = trials[t].cycles_used;
+            P.active[tg] = trials[t].active;
+          }
+          for (int cl = ew * 32 + lane; cl < NT; cl += EPI * 32) gE_pass[cl] = 0ull;
+          __threadfence();
+          epi_bar<EPI>();
+          if (ew == 0 && lane == 0) {
+            int any = 0;
+            for (int t = 0; t < ntl; ++t) any |= trials[t].active;
+            st_release_gpu(&P.g_scan[tile], (s_idx + 1) | (any ? 0ll : (1ll << 62)));
+          }
+        }
+        // every CTA of the column tile: the scan of this pass decides which
+        // trials still update
+        if (ew == 0 && lane == 0) {
+          long long v;
+          while (((v = ld_acquire_gpu(&P.g_scan[tile])) & ((1ll << 62) - 1)) < s_idx + 1)
+            __nanosleep(128);
+          ctl->scan_stop = int((v >> 62) & 1);
+        }
+        epi_bar<EPI>();
+        if (!do_scan)
+          for (int t = ew * 32 + lane; t < ntl; t += 32 * EPI)
+            trials[t].active = __ldcg(P.active + tile * g.tpt + t);
+      }
+      epi_bar<EPI>();
       if (ew == 0 && lane == 0) {
         if (do_update) ring_advance(ring, c, P.d, P.nslots);
         if (P.run_mode && !drain) {
           int any = 0;
-          for (int t = 0; t < ntl; ++t) any |= trials[t].active;
+          if (split) any = !ctl->scan_stop;
+          else
+            for (int t = 0; t < ntl; ++t) any |= trials[t].active;
           // nothing left to anneal: the other roles may already be in pass
           // c+1 -- let it run (drained) and stop everyone after it
           if (!any && c < P.c_last) ctl->last_pass = c + 1;
@@ -1195,15 +1329,19 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
       if (P.run_mode && !drain && c + 1 == *reinterpret_cast<volatile long*>(&ctl->last_pass) &&
           c + 1 <= P.c_last) {
         int any = 0;
-        for (int t = 0; t < ntl; ++t) any |= trials[t].active;
+        if (split) any = !ctl->scan_stop;
+        else
+          for (int t = 0; t < ntl; ++t) any |= trials[t].active;
         drain = !any;
       }
     }
     // results of this CTA's trials (the epilogue warps own the trial table)
     epi_bar<EPI>();
-    if (P.run_mode) {
+    if (P.run_mode && part == 0) {
       for (int t = ew; t < ntl; t += EPI)
         expand_best_state<F4>(P, tile * g.tpt + t, g.n, g.npad, lane);
+    }
+    if (P.run_mode && !split) {  // with a row split the scanners keep global current
       for (int t = ew * 32 + lane; t < ntl; t += 32 * EPI) {
         const int tg = tile * g.tpt + t;
         P.best_e[tg] = trials[t].best_e;
@@ -1343,6 +1481,28 @@ int launch(ssqa_batch_s* b, TcParams& P, bool f4) {
     g_tc_err = "cuTensorMapEncodeTiled failed";
     return SSQA_ECUDA;
   }
+  if (g.rs > 1) {
+    // row-split synchronisation state, zeroed for every launch
+    const int nrt_all = g.npad / kBM;
+    const size_t bytes = size_t(2) * g.ccols * 8 + size_t(g.ntiles) * 8 +
+                         size_t(g.ntiles) * nrt_all * 4 + size_t(g.ntiles) * 4 + 64;
+    if (b->split_bytes < bytes) {
+      if (b->d_split) cudaFree(b->d_split);
+      b->d_split = nullptr;
+      b->split_bytes = 0;
+      if (cudaMalloc(&b->d_split, bytes) != cudaSuccess) {
+        g_tc_err = "row-split state allocation failed";
+        return SSQA_ECUDA;
+      }
+      b->split_bytes = bytes;
+    }
+    cudaMemsetAsync(b->d_split, 0, bytes, b->prob->stream);
+    uint8_t* base = static_cast<uint8_t*>(b->d_split);
+    P.gE = reinterpret_cast<unsigned long long*>(base);
+    P.g_scan = reinterpret_cast<long long*>(base + size_t(2) * g.ccols * 8);
+    P.g_rows = reinterpret_cast<int*>(base + size_t(2) * g.ccols * 8 + size_t(g.ntiles) * 8);
+    P.g_arrive = reinterpret_cast<unsigned*>(P.g_rows + size_t(g.ntiles) * nrt_all);
+  }
   const char* env_epi = getenv("SSQA_TC_EPI");
   const int epi = env_epi ? (atoi(env_epi) == 12 ? 12 : 16) : kDefaultEpi;
   Layout L = pick_layout(g.tile_cols, g.tpt, epi / 4, int(tile_row));
@@ -1363,12 +1523,15 @@ int launch(ssqa_batch_s* b, TcParams& P, bool f4) {
     P.dbg_rts = dbg_rts;
   }
   cudaError_t e;
+  // one persistent CTA per (column tile, row part); every CTA must be
+  // resident (the row split synchronises across CTAs): grid <= SM count
+  const int grid = g.ntiles * g.rs;
   if (epi == 16)
-    e = f4 ? launch_variant<16, true>(g.ntiles, smem, b->prob->stream, maps, P)
-           : launch_variant<16, false>(g.ntiles, smem, b->prob->stream, maps, P);
+    e = f4 ? launch_variant<16, true>(grid, smem, b->prob->stream, maps, P)
+           : launch_variant<16, false>(grid, smem, b->prob->stream, maps, P);
   else
-    e = f4 ? launch_variant<12, true>(g.ntiles, smem, b->prob->stream, maps, P)
-           : launch_variant<12, false>(g.ntiles, smem, b->prob->stream, maps, P);
+    e = f4 ? launch_variant<12, true>(grid, smem, b->prob->stream, maps, P)
+           : launch_variant<12, false>(grid, smem, b->prob->stream, maps, P);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) {
     g_tc_err = std::string("k_sweep_tc launch: ") + cudaGetErrorString(e);

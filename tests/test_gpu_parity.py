@@ -451,3 +451,80 @@ def test_stop_at_target_many_tiles_drain(orc, engine):
         assert np.array_equal(bits(r.trace_energy), bits(o.trace))
         stopped += r.cycles_used < 1500
     assert stopped > 10
+
+
+# ---- tcgen05 row split: rs CTAs per column tile (cross-CTA row readiness,
+# global energy sums, scan by the last arriving CTA) ----
+
+@pytest.fixture
+def row_split(monkeypatch):
+    def force(rs):
+        monkeypatch.setenv("SSQA_TC_RS", str(rs))
+    return force
+
+
+@pytest.mark.parametrize("rs", [2, 3, 4])
+def test_row_split_runs_match_oracle(orc, row_split, rs):
+    if not engine_ok(_lib.ENGINE_TCGEN05):
+        pytest.skip("tcgen05 engine unavailable")
+    row_split(rs)
+    cases = [(sq.gi_ising(20, 0.5, 7, True, 1.0, 1.0), params(20, 60), [41, 42, 43, 44, 45, 46]),
+             (sq.dense_ising(400, 0, 5), params(6, 30, tau=4, bidirectional=True), [7, 8, 9])]
+    for m, p, seeds in cases:
+        # a target trial 0 reaches, so stop_at_target freezes some trials early
+        hit = orc.ssqa_run(m.h, m.J, m.offset, p, seeds[0], None, False, False).best_energy
+        for target, stop in ((-1e9, False), (float(hit), True)):
+            res = sq.ssqa_run_batch(m, to_sq(p), seeds, target, sq.RunOptions(True, stop),
+                                    engine=_lib.ENGINE_TCGEN05)
+            for t, sd in enumerate(seeds):
+                o = orc.ssqa_run(m.h, m.J, m.offset, p, sd, target, True, stop)
+                r = res[t]
+                assert (r.best_energy, r.best_replica, r.reached_target, r.first_hit_cycle,
+                        r.cycles_used) == (o.best_energy, o.best_replica, o.reached_target,
+                                           o.first_hit_cycle, o.cycles_used), (rs, m.n, stop, t)
+                assert np.array_equal(r.best_state, o.best_state)
+                assert np.array_equal(bits(r.trace_energy), bits(o.trace))
+
+
+def test_row_split_per_step_sweeps(orc, row_split):
+    if not engine_ok(_lib.ENGINE_TCGEN05):
+        pytest.skip("tcgen05 engine unavailable")
+    row_split(3)
+    m = sq.dense_ising(400, 0, 11)
+    p = params(5, 10, delay=2)
+    prob = sq.Problem(m)
+    b = sq.Batch(prob, to_sq(p), 2, engine=_lib.ENGINE_TCGEN05)
+    seeds = [3, 4]
+    b.set_seeds(seeds)
+    b.init()
+    states = [orc.init_lattice(m.n, 5, 2, s) for s in seeds]
+    cyc = 0
+    for step in range(6):
+        jp = orc.jperp_schedule(cyc, p)
+        b.sweep(1)
+        for t, s in enumerate(seeds):
+            sg, ac, hi = states[t]
+            orc.ssqa_sweep(m.h, m.J, m.offset, jp, p, s, cyc, sg, ac, hi, cyc)
+        cyc += 1
+        for t in range(2):
+            sg, ac, hi, c = b.read_lattice(t)
+            assert c == cyc
+            assert np.array_equal(bits(sg), bits(states[t][0])), (step, t)
+            assert np.array_equal(bits(ac), bits(states[t][1])), (step, t)
+
+
+def test_wide_row_split_default_heuristic(orc):
+    """N=2048 dense: the default geometry widens the column tile to all 16
+    trials and splits its 16 row tiles over 16 CTAs."""
+    if not engine_ok(_lib.ENGINE_TCGEN05):
+        pytest.skip("tcgen05 engine unavailable")
+    m = sq.dense_ising(2048, 0, 3)
+    p = params(8, 12, tau=3)
+    seeds = list(range(60, 76))
+    res = sq.ssqa_run_batch(m, to_sq(p), seeds, None, sq.RunOptions(True, False),
+                            engine=_lib.ENGINE_TCGEN05)
+    for t in (0, 7, 15):
+        o = orc.ssqa_run(m.h, m.J, m.offset, p, seeds[t], None, True, False)
+        assert res[t].best_energy == o.best_energy and res[t].best_replica == o.best_replica
+        assert np.array_equal(res[t].best_state, o.best_state)
+        assert np.array_equal(bits(res[t].trace_energy), bits(o.trace))
