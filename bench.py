@@ -184,10 +184,20 @@ def reference_sample(cfg, workers, target_s):
         import concurrent.futures as cf
         p = oracle_py.params(R, S)
         t0 = time.perf_counter()
-        with cf.ThreadPoolExecutor(workers) as ex:
-            list(ex.map(lambda s: o.ssqa_run(m.h, m.J, m.offset, p, BASE_SEED + s, None, False,
-                                             False), range(T)))
-        wall = time.perf_counter() - t0
+        if kind == "reference":
+            # one shared reference model for all threads (a dense N=32768
+            # IsingModel is 8.6 GB: one per call would not fit)
+            t_m0 = time.perf_counter()
+            o.ssqa_run_many(m.h, m.J, m.offset, oracle_py.params(R, 1), [BASE_SEED], 1)
+            t_model = time.perf_counter() - t_m0  # model build + a 1-sweep run
+            t0 = time.perf_counter()
+            o.ssqa_run_many(m.h, m.J, m.offset, p, [BASE_SEED + s for s in range(T)], workers)
+            wall = time.perf_counter() - t0 - t_model
+        else:
+            with cf.ThreadPoolExecutor(workers) as ex:
+                list(ex.map(lambda s: o.ssqa_run(m.h, m.J, m.offset, p, BASE_SEED + s, None,
+                                                 False, False), range(T)))
+            wall = time.perf_counter() - t0
         sample = (f"{kind} ssqa_run: {T} trials x {S} sweeps on {workers} threads")
     upd = float(N) * R * T * S
     return dict(value=upd / wall, unit=UNIT, cores=workers, kind=kind, sample=sample,

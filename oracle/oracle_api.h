@@ -92,6 +92,9 @@ int ref_ssqa_run(int n, const double* h, const double* J, double offset,
                  const orc_ssqa_params* p, uint64_t seed, int has_target, double target,
                  int record_trace, int stop_at_target, orc_result* out, int8_t* best_state,
                  double* trace_energy);
+int ref_ssqa_run_many(int n, const double* h, const double* J, double offset,
+                      const orc_ssqa_params* p, const uint64_t* seeds, int trials, int workers,
+                      double* best_energy);
 int ref_i0_schedule(long cycle, const orc_ssa_params* p, double* out);
 int ref_ssa_run(int n, const double* h, const double* J, double offset, const orc_ssa_params* p,
                 uint64_t seed, int has_target, double target, int record_trace,

@@ -225,6 +225,17 @@ class Oracle:
                       trace[:res.trace_len] if record_trace else np.zeros(0))
 
     # ---- reference-only helpers ----
+    def ssqa_run_many(self, h, J, offset, p: OrcParams, seeds, workers):
+        """ref_ssqa_run_many: every seed on `workers` threads, one shared model."""
+        assert self.kind == "ref"
+        s = np.ascontiguousarray(np.asarray(seeds, dtype=np.uint64))
+        out = np.zeros(len(s))
+        self._check(self.lib.ref_ssqa_run_many(
+            len(h), _dp(np.ascontiguousarray(h, dtype=np.float64)),
+            _dp(np.ascontiguousarray(J, dtype=np.float64)), C.c_double(offset), C.byref(p),
+            s.ctypes.data_as(C.POINTER(C.c_uint64)), len(s), workers, _dp(out)))
+        return out
+
     def gi_ising(self, n_nodes, edge_prob, seed, permute, c1, c2):
         assert self.kind == "ref"
         n = n_nodes * n_nodes

@@ -10,6 +10,8 @@
 #include <exception>
 #include <stdexcept>
 #include <string>
+#include <thread>
+#include <vector>
 
 #include "ssqa/annealer.hpp"
 #include "ssqa/bench.hpp"
@@ -221,6 +223,36 @@ int ref_ssa_run(int n, const double* h, const double* J, double offset, const or
       for (size_t i = 0; i < res.best_state.size(); ++i) best_state[i] = res.best_state[i];
     if (trace_energy)
       for (size_t i = 0; i < res.trace.size(); ++i) trace_energy[i] = res.trace[i].energy;
+  });
+}
+
+// ssqa_run (annealer.cpp:474-487) for every seed on `workers` threads over ONE
+// shared model (as run_trials shares its problem, bench.cpp:365-407); used by
+// bench.py's CPU baseline for the dense configs, whose model is too large
+// to rebuild per call.  best_energy[t] receives each trial's best energy.
+int ref_ssqa_run_many(int n, const double* h, const double* J, double offset,
+                      const orc_ssqa_params* p, const uint64_t* seeds, int trials, int workers,
+                      double* best_energy) {
+  return guarded([&] {
+    const ssqa_ref::IsingModel m = make_model(n, h, J, offset);
+    const ssqa_ref::SsqaParams q = make_params(p);
+    ssqa_ref::RunOptions opts;
+    opts.record_trace = false;
+    opts.stop_at_target = false;
+    std::vector<std::thread> th;
+    std::vector<std::string> errs(size_t(std::max(1, workers)));
+    for (int w = 0; w < std::max(1, workers); ++w)
+      th.emplace_back([&, w] {
+        try {
+          for (int t = w; t < trials; t += std::max(1, workers))
+            best_energy[t] = ssqa_ref::ssqa_run(m, q, seeds[t], {}, opts).best_energy;
+        } catch (const std::exception& e) {
+          errs[size_t(w)] = e.what();
+        }
+      });
+    for (auto& x : th) x.join();
+    for (const auto& e : errs)
+      if (!e.empty()) throw std::runtime_error(e);
   });
 }
 

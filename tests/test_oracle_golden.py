@@ -384,3 +384,31 @@ def test_ssa_oracle_matches_reference_live(orc, ref):
         b = orc.ssa_run(h, J, 0.5, p, seed, None, True, False)
         assert np.array_equal(a.trace.view(np.uint64), b.trace.view(np.uint64))
         assert np.array_equal(a.best_state, b.best_state)
+
+
+def test_numpy_lattice_matches_oracle(orc, golden):
+    """oracle/lattice_np.py (the vectorised checker used at full BASELINE
+    sizes) against the C restatement: traces, best states, hits, stops."""
+    import lattice_np as lnp
+    import paper_2302_12454_b200 as sq
+    inst = golden("gi_instances")["gi_10_7_1_1.0"]
+    cases = [(inst["h"], inst["J"], float(inst["offset"]), dict(r=20, sc=300), [123, 5], 0.0, True),
+             (inst["h"], inst["J"], float(inst["offset"]), dict(r=7, sc=120, delay=2,
+                                                                bidirectional=True), [9], None,
+              False)]
+    m = sq.dense_ising(256, 0, 3)
+    cases.append((m.h, m.J, m.offset, dict(r=6, sc=40, tau=4), [1, 2, 3], None, False))
+    m1 = sq.dense_ising(200, 1, 4)
+    cases.append((m1.h, m1.J, m1.offset, dict(r=4, sc=30, tau=2, n_rnd=2.0), [8], None, False))
+    for h, J, off, kw, seeds, target, stop in cases:
+        p = params(**kw)
+        got = lnp.run_lattice(h, J, off, p.r, p.delay, p.n_rnd, p.alpha, bool(p.bidirectional),
+                              p.sc, lnp.jperp_schedule(p), lambda c: p.i0, seeds, target, stop)
+        for t, s in enumerate(seeds):
+            o = orc.ssqa_run(h, J, off, p, s, target, True, stop)
+            g = got[t]
+            assert (g.best_energy, g.best_replica, g.reached_target, g.first_hit_cycle,
+                    g.cycles_used) == (o.best_energy, o.best_replica, o.reached_target,
+                                       o.first_hit_cycle, o.cycles_used), (kw, s)
+            assert np.array_equal(g.best_state, o.best_state)
+            assert np.array_equal(g.trace.reshape(-1).view(np.uint64), o.trace.view(np.uint64))
