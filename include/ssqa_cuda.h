@@ -165,6 +165,9 @@ int ssqa_batch_destroy(ssqa_batch b);
 void* ssqa_batch_stream(ssqa_batch b);
 /* Engine the batch resolved to (SSQA_ENGINE_SIMT / SSQA_ENGINE_TCGEN05). */
 int ssqa_batch_engine(ssqa_batch b);
+/* Bits per coupling/spin operand the contraction streams: 4 (e2m1 FP4,
+ * tcgen05 kind::mxf4) or 8 (int8). */
+int ssqa_batch_operand_bits(ssqa_batch b);
 /* Upload per-trial seeds (host array of `trials`). */
 int ssqa_batch_set_seeds(ssqa_batch b, const uint64_t* seeds);
 /* Asynchronous full run on the batch stream: init_lattice + run_lattice

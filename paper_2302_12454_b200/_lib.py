@@ -71,6 +71,7 @@ SIGNATURES = [
     ("ssqa_batch_destroy", C.c_int, [VP]),
     ("ssqa_batch_stream", VP, [VP]),
     ("ssqa_batch_engine", C.c_int, [VP]),
+    ("ssqa_batch_operand_bits", C.c_int, [VP]),
     ("ssqa_batch_set_seeds", C.c_int, [VP, U64P]),
     ("ssqa_batch_launch", C.c_int, [VP, C.c_int, C.c_double, C.c_int]),
     ("ssqa_batch_fetch", C.c_int, [VP, C.POINTER(ResultC), I8P, DP]),

@@ -242,6 +242,11 @@ class Batch:
         return lib().ssqa_batch_engine(self._b)
 
     @property
+    def operand_bits(self) -> int:
+        """4 (FP4 e2m1 operands) or 8 (int8) for the contraction."""
+        return lib().ssqa_batch_operand_bits(self._b)
+
+    @property
     def stream(self) -> int:
         return lib().ssqa_batch_stream(self._b) or 0
 

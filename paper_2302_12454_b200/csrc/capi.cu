@@ -509,6 +509,10 @@ int ssqa_batch_destroy(ssqa_batch b) {
 
 void* ssqa_batch_stream(ssqa_batch b) { return b ? (void*)b->prob->stream : nullptr; }
 int ssqa_batch_engine(ssqa_batch b) { return b ? b->engine : -1; }
+int ssqa_batch_operand_bits(ssqa_batch b) {
+  if (!b) return -1;
+  return (b->engine == SSQA_ENGINE_TCGEN05 && tc_uses_fp4(b)) ? 4 : 8;
+}
 long ssqa_batch_launch_count(ssqa_batch b) { return b ? b->launches : -1; }
 
 int ssqa_batch_elapsed_ms(ssqa_batch b, double* ms) {

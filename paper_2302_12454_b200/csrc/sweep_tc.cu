@@ -1620,6 +1620,16 @@ void advance_ring(ssqa_batch_s* b, long count) {
 
 }  // namespace
 
+// FP4 operands when every coupling is e2m1-exact, fields stay below 2^22
+// (exact fp32 accumulation and float->int conversion) and the tile leaves
+// room for the scale-factor columns; SSQA_TC_FP4=0 forces int8.
+bool tc_uses_fp4(const ssqa_batch_s* b) {
+  const Quantized& q = b->prob->q;
+  const char* envf4 = getenv("SSQA_TC_FP4");
+  return q.fp4_ok && b->d_sig4 && double(q.max_abs_j) * q.n < double(1 << 22) &&
+         2 * b->g.tile_cols <= int(kSfCol) && !(envf4 && envf4[0] == '0');
+}
+
 bool tc_supported(int npad, int r, int delay) {
   return npad >= kBM && npad % kBM == 0 && r >= 1 && r <= kMaxCols && delay <= kMaxDelay;
 }
@@ -1641,10 +1651,7 @@ int tc_run(ssqa_batch_s* b, const ScanArgs& sa) {
   // FP4 operands when every coupling is e2m1-exact, fields stay below 2^22
   // (exact fp32 accumulation and float->int conversion) and the tile leaves
   // room for the scale-factor columns; SSQA_TC_FP4=0 forces int8.
-  const Quantized& q = b->prob->q;
-  const char* envf4 = getenv("SSQA_TC_FP4");
-  const bool f4 = q.fp4_ok && b->d_sig4 && double(q.max_abs_j) * q.n < double(1 << 22) &&
-                  2 * b->g.tile_cols <= int(kSfCol) && !(envf4 && envf4[0] == '0');
+  const bool f4 = tc_uses_fp4(b);
   if (f4) {
     const size_t bytes = size_t(b->nslots) * b->slot_elems / 2;
     k_pack_fp4<<<1184, 256, 0, b->prob->stream>>>(b->d_sig, b->d_sig4, bytes);

@@ -10,6 +10,8 @@ namespace ssqa_engine {
 
 // True when the tcgen05 kernel handles this padded size / replica count.
 bool tc_supported(int npad, int r, int delay);
+// Operand format a fused run of this batch streams: FP4 (e2m1) or int8.
+bool tc_uses_fp4(const ssqa_batch_s* b);
 // Full run: cycles 0..sc with scans (state already initialised).
 int tc_run(ssqa_batch_s* b, const ScanArgs& sa);
 // One sweep at b->cycle without a scan (per-step API).
