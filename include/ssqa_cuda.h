@@ -186,6 +186,30 @@ int ssqa_batch_elapsed_ms(ssqa_batch b, double* ms);
  * return the mean duration of one launch.  State is not modified. */
 int ssqa_batch_profile_field(ssqa_batch b, int iters, double* ms_per_launch);
 
+/* ---- GPU row shards (J' row-sharded across GPUs) ------
+ * Every GPU g of G holds the same problem and a batch with the same seeds and
+ * params; ssqa_batch_set_shard(b, g, G) makes it update only spin rows
+ * [g*npad/G, (g+1)*npad/G).  Per cycle c = 0..sc:
+ *   ssqa_batch_shard_pass(b, chunk)   contraction of its rows against the full
+ *       sigma(c), update of its rows, and packs sigma(c+1) of its rows
+ *       (1 bit per spin) plus its per-column int64 energy partials into
+ *       `chunk` (device memory, ssqa_batch_shard_bytes(b) bytes);
+ *   all-gather of the G chunks (e.g. ncclAllGather, in shard order);
+ *   ssqa_batch_shard_merge(b, chunks) unpacks every shard's rows into
+ *       sigma(c+1), sums the energy partials and scans cycle c
+ *       (best tracking, trace, stop-at-target) exactly as run_lattice.
+ * Bracket the cycles with ssqa_batch_shard_begin (reset + init_lattice) and
+ * ssqa_batch_shard_end; ssqa_batch_fetch then returns the results (identical
+ * on every GPU).  All calls enqueue on ssqa_batch_stream(b); order the
+ * collective on that stream.  tcgen05 engine, int8 operands; npad/128 must
+ * be divisible by G. */
+int ssqa_batch_set_shard(ssqa_batch b, int shard, int nshards);
+long ssqa_batch_shard_bytes(ssqa_batch b);
+int ssqa_batch_shard_begin(ssqa_batch b, int has_target, double target, int stop_at_target);
+int ssqa_batch_shard_pass(ssqa_batch b, void* chunk);
+int ssqa_batch_shard_merge(ssqa_batch b, const void* chunks);
+int ssqa_batch_shard_end(ssqa_batch b);
+
 /* ---- Per-step API: init_lattice / ssqa_sweep / replica_energies
  * (annealer.cpp:432-472), applied to every trial of the batch. ---------- */
 /* init_lattice(n, r, delay, seeds[t]) for each trial; lattice cycle = 0. */

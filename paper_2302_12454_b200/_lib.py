@@ -78,6 +78,12 @@ SIGNATURES = [
     ("ssqa_batch_launch_count", C.c_long, [VP]),
     ("ssqa_batch_elapsed_ms", C.c_int, [VP, DP]),
     ("ssqa_batch_profile_field", C.c_int, [VP, C.c_int, DP]),
+    ("ssqa_batch_set_shard", C.c_int, [VP, C.c_int, C.c_int]),
+    ("ssqa_batch_shard_bytes", C.c_long, [VP]),
+    ("ssqa_batch_shard_begin", C.c_int, [VP, C.c_int, C.c_double, C.c_int]),
+    ("ssqa_batch_shard_pass", C.c_int, [VP, VP]),
+    ("ssqa_batch_shard_merge", C.c_int, [VP, VP]),
+    ("ssqa_batch_shard_end", C.c_int, [VP]),
     ("ssqa_batch_init", C.c_int, [VP]),
     ("ssqa_batch_sweep", C.c_int, [VP, C.c_long]),
     ("ssqa_batch_sweep_with", C.c_int, [VP, C.c_double, C.c_double]),

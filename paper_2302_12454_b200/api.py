@@ -283,6 +283,27 @@ class Batch:
             _dp(tr) if tr is not None else None))
         return res, best, tr
 
+    # GPU row shards (ssqa_batch_set_shard ... in include/ssqa_cuda.h)
+    def set_shard(self, shard: int, nshards: int):
+        check(lib().ssqa_batch_set_shard(self._b, shard, nshards))
+
+    def shard_bytes(self) -> int:
+        return int(lib().ssqa_batch_shard_bytes(self._b))
+
+    def shard_begin(self, target: Optional[float] = None, stop_at_target: bool = True):
+        check(lib().ssqa_batch_shard_begin(self._b, int(target is not None),
+                                           0.0 if target is None else float(target),
+                                           int(stop_at_target)))
+
+    def shard_pass(self, chunk_ptr: int):
+        check(lib().ssqa_batch_shard_pass(self._b, C.c_void_p(chunk_ptr)))
+
+    def shard_merge(self, chunks_ptr: int):
+        check(lib().ssqa_batch_shard_merge(self._b, C.c_void_p(chunks_ptr)))
+
+    def shard_end(self):
+        check(lib().ssqa_batch_shard_end(self._b))
+
     # per-step API
     def init(self):
         check(lib().ssqa_batch_init(self._b))

@@ -652,6 +652,104 @@ int ssqa_run_batch(ssqa_problem prob, const ssqa_params_c* p, const uint64_t* se
   return rc;
 }
 
+// ---- GPU row shards ------------------------------------
+int ssqa_batch_set_shard(ssqa_batch b, int shard, int nshards) {
+  if (!b) return set_err(SSQA_EINVAL, "null batch");
+  if (nshards < 1 || shard < 0 || shard >= nshards)
+    return set_err(SSQA_EINVAL, "shard index out of range");
+  if (b->engine != SSQA_ENGINE_TCGEN05)
+    return set_err(SSQA_EUNSUP, "row shards need the tcgen05 engine");
+  const int nrt = b->g.npad / 128;
+  if (nrt % nshards != 0)
+    return set_err(SSQA_EUNSUP, "padded spin count / 128 must divide into the shards");
+  if (b->d > 30) return set_err(SSQA_EUNSUP, "tcgen05 engine supports delay <= 30");
+  b->shard = shard;
+  b->nshards = nshards;
+  return SSQA_OK;
+}
+
+long ssqa_batch_shard_bytes(ssqa_batch b) {
+  if (!b) return -1;
+  const long rows = long(b->g.npad) / b->nshards;
+  return long(b->g.ccols) * (rows / 32) * 4 + long(b->g.ccols) * 8;
+}
+
+int ssqa_batch_shard_begin(ssqa_batch b, int has_target, double target, int stop_at_target) {
+  if (!b) return set_err(SSQA_EINVAL, "null batch");
+  if (!b->seeds_set) return set_err(SSQA_EINVAL, "seeds not set");
+  CU(cudaSetDevice(b->prob->device));
+  cudaStream_t st = b->prob->stream;
+  b->launches = 0;
+  CU(cudaEventRecord(b->ev0, st));
+  launch_reset_results(b->g.T, b->p.sc, b->d_best_e, b->d_best_k, b->d_reached,
+                       b->d_first_hit, b->d_cycles_used, b->d_active, st);
+  CHECK_LAUNCH();
+  b->launches += 1;
+  int rc = init_state(b);
+  if (rc) return rc;
+  b->sh_has_target = has_target;
+  b->sh_target_tol = target + kTargetTol;
+  b->sh_stop = stop_at_target;
+  return SSQA_OK;
+}
+
+int ssqa_batch_shard_pass(ssqa_batch b, void* chunk) {
+  if (!b || !chunk) return set_err(SSQA_EINVAL, "null argument");
+  if (b->cycle > b->p.sc) return set_err(SSQA_EINVAL, "run already complete");
+  CU(cudaSetDevice(b->prob->device));
+  cudaStream_t st = b->prob->stream;
+  const int nrt = b->g.npad / 128 / b->nshards;
+  CU(cudaMemsetAsync(b->d_E, 0, size_t(b->g.ccols) * sizeof(long long), st));
+  int rc = tc_shard_pass(b, b->shard * nrt, nrt, reinterpret_cast<unsigned long long*>(b->d_E));
+  if (rc) return set_err(rc, tc_last_error());
+  // sigma(c+1) rows of this shard sit in the slot the kernel picked (ring rule)
+  const int dst = b->cycle < b->p.sc ? pick_free(b) : b->cur;
+  launch_shard_pack(b->g, slot_ptr(b, dst), b->shard * nrt * 128, nrt * 128,
+                    reinterpret_cast<const unsigned long long*>(b->d_E), chunk, st);
+  CHECK_LAUNCH();
+  b->launches += 2;
+  return SSQA_OK;
+}
+
+int ssqa_batch_shard_merge(ssqa_batch b, const void* chunks) {
+  if (!b || !chunks) return set_err(SSQA_EINVAL, "null argument");
+  if (b->cycle > b->p.sc) return set_err(SSQA_EINVAL, "run already complete");
+  CU(cudaSetDevice(b->prob->device));
+  cudaStream_t st = b->prob->stream;
+  const bool upd = b->cycle < b->p.sc;
+  const int dst = upd ? pick_free(b) : b->cur;
+  launch_shard_unpack(b->g, slot_ptr(b, dst), chunks, size_t(ssqa_batch_shard_bytes(b)),
+                      b->nshards, b->g.npad / b->nshards, upd, b->d_E, st);
+  CHECK_LAUNCH();
+  ScanArgs sa{};
+  sa.cycle = b->cycle;
+  sa.sc = b->p.sc;
+  sa.scale = b->prob->q.scale;
+  sa.offset = b->prob->q.offset;
+  sa.has_target = b->sh_has_target;
+  sa.target_tol = b->sh_target_tol;
+  sa.stop_at_target = b->sh_stop;
+  sa.record_trace = b->record_trace;
+  launch_scan(b->g, b->d_E, sa, slot_ptr(b, b->cur), b->d_best_e, b->d_best_k, b->d_reached,
+              b->d_first_hit, b->d_cycles_used, b->d_active, b->d_best_state, b->d_trace, st);
+  CHECK_LAUNCH();
+  b->launches += 2;
+  if (upd) {
+    b->phys[size_t(b->cycle % (b->d + 1))] = dst;
+    b->cur = dst;
+  }
+  b->cycle += 1;  // sc + 1 marks the run complete
+  return SSQA_OK;
+}
+
+int ssqa_batch_shard_end(ssqa_batch b) {
+  if (!b) return set_err(SSQA_EINVAL, "null batch");
+  CU(cudaSetDevice(b->prob->device));
+  CU(cudaEventRecord(b->ev1, b->prob->stream));
+  b->cycle = b->p.sc;
+  return SSQA_OK;
+}
+
 int ssqa_batch_init(ssqa_batch b) {
   if (!b) return set_err(SSQA_EINVAL, "null batch");
   if (!b->seeds_set) return set_err(SSQA_EINVAL, "seeds not set");

@@ -86,6 +86,11 @@ struct ssqa_batch_s {
   //   pass stamps, arrive [ntiles] pass arrivals, scan [ntiles] scan stamps
   void* d_split = nullptr;
   size_t split_bytes = 0;
+  // GPU row shard (ssqa_batch_set_shard): this batch updates row tiles
+  // [shard * nrt / nshards, (shard + 1) * nrt / nshards) of every column
+  int shard = 0, nshards = 1;
+  int sh_has_target = 0, sh_stop = 0;
+  double sh_target_tol = 0.0;
   // SSA batches (annealer.cpp:489-501): R = 1, delay = 0, jperp = 0 and the
   // accumulator bound follows i0_schedule (annealer.cpp:403-408) per cycle.
   bool ssa = false;

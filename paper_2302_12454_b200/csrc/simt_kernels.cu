@@ -183,6 +183,79 @@ __global__ void k_scan(Geom g, const long long* __restrict__ E, ScanArgs a,
 }
 
 
+// ---- GPU row shards: exchange chunk of one shard =
+// [ccols][nwords] bit-packed spin rows (bit r of word w: row row0 + 32w + r
+// is +1) followed by [ccols] int64 energy partials.
+__global__ void k_shard_pack(Geom g, const int8_t* __restrict__ slot, int row0, int nwords,
+                             const unsigned long long* __restrict__ E, uint8_t* __restrict__ chunk) {
+  uint32_t* bits = reinterpret_cast<uint32_t*>(chunk);
+  long long* e_out = reinterpret_cast<long long*>(chunk + size_t(g.ccols) * nwords * 4);
+  const size_t total = size_t(g.ccols) * nwords;
+  for (size_t x = blockIdx.x * size_t(blockDim.x) + threadIdx.x; x < total;
+       x += size_t(gridDim.x) * blockDim.x) {
+    const int col = int(x / nwords), w = int(x % nwords);
+    const int4* src = reinterpret_cast<const int4*>(slot + size_t(col) * g.npad + row0 + 32 * w);
+    const int4 a = src[0], b = src[1];
+    const uint32_t v[8] = {uint32_t(a.x), uint32_t(a.y), uint32_t(a.z), uint32_t(a.w),
+                           uint32_t(b.x), uint32_t(b.y), uint32_t(b.z), uint32_t(b.w)};
+    uint32_t word = 0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+#pragma unroll
+      for (int y = 0; y < 4; ++y) word |= uint32_t(int8_t(v[q] >> (8 * y)) > 0) << (4 * q + y);
+    bits[x] = word;
+  }
+  for (int col = blockIdx.x * blockDim.x + threadIdx.x; col < g.ccols; col += gridDim.x * blockDim.x)
+    e_out[col] = static_cast<long long>(E[col]);
+}
+
+__global__ void k_shard_unpack(Geom g, int8_t* __restrict__ slot, const uint8_t* __restrict__ all,
+                               size_t chunk_bytes, int nshards, int rows_per_shard,
+                               int with_spins, long long* __restrict__ E) {
+  const int nwords = rows_per_shard / 32;
+  if (with_spins) {
+    const size_t total = size_t(nshards) * g.ccols * nwords;
+    for (size_t x = blockIdx.x * size_t(blockDim.x) + threadIdx.x; x < total;
+         x += size_t(gridDim.x) * blockDim.x) {
+      const int sh = int(x / (size_t(g.ccols) * nwords));
+      const size_t r = x % (size_t(g.ccols) * nwords);
+      const int col = int(r / nwords), w = int(r % nwords);
+      const uint32_t word = reinterpret_cast<const uint32_t*>(all + size_t(sh) * chunk_bytes)[r];
+      uint32_t v[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        uint32_t b4 = 0;
+#pragma unroll
+        for (int y = 0; y < 4; ++y) b4 |= (((word >> (4 * q + y)) & 1u) ? 0x01u : 0xFFu) << (8 * y);
+        v[q] = b4;
+      }
+      int4* dst = reinterpret_cast<int4*>(slot + size_t(col) * g.npad + size_t(sh) * rows_per_shard +
+                                          32 * w);
+      dst[0] = make_int4(int(v[0]), int(v[1]), int(v[2]), int(v[3]));
+      dst[1] = make_int4(int(v[4]), int(v[5]), int(v[6]), int(v[7]));
+    }
+  }
+  for (int col = blockIdx.x * blockDim.x + threadIdx.x; col < g.ccols; col += gridDim.x * blockDim.x) {
+    long long e = 0;
+    for (int sh = 0; sh < nshards; ++sh)
+      e += reinterpret_cast<const long long*>(all + size_t(sh) * chunk_bytes +
+                                              size_t(g.ccols) * nwords * 4)[col];
+    E[col] = e;
+  }
+}
+
+void launch_shard_pack(const Geom& g, const int8_t* slot, int row0, int rows,
+                       const unsigned long long* E, void* chunk, cudaStream_t st) {
+  k_shard_pack<<<1184, 256, 0, st>>>(g, slot, row0, rows / 32, E, static_cast<uint8_t*>(chunk));
+}
+
+void launch_shard_unpack(const Geom& g, int8_t* slot, const void* all, size_t chunk_bytes,
+                         int nshards, int rows_per_shard, bool with_spins, long long* E,
+                         cudaStream_t st) {
+  k_shard_unpack<<<1184, 256, 0, st>>>(g, slot, static_cast<const uint8_t*>(all), chunk_bytes,
+                                       nshards, rows_per_shard, with_spins ? 1 : 0, E);
+}
+
 void launch_init(const Geom& g, const uint64_t* seeds, int8_t* sig, double* acc,
                  cudaStream_t st) {
   k_init<<<g.ccols, 256, 0, st>>>(g, seeds, sig, acc);

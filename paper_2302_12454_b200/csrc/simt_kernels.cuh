@@ -54,6 +54,14 @@ struct ScanArgs {
 
 void launch_init(const Geom& g, const uint64_t* seeds, int8_t* sig, double* acc,
                  cudaStream_t st);
+// GPU row shards: pack rows [row0, row0+rows) of every column of an int8
+// spin slot (bit-packed) plus the energy partials into one exchange chunk;
+// unpack all shards' chunks into the slot and sum their energy partials.
+void launch_shard_pack(const Geom& g, const int8_t* slot, int row0, int rows,
+                       const unsigned long long* E, void* chunk, cudaStream_t st);
+void launch_shard_unpack(const Geom& g, int8_t* slot, const void* all, size_t chunk_bytes,
+                         int nshards, int rows_per_shard, bool with_spins, long long* E,
+                         cudaStream_t st);
 void launch_reset_results(int T, long sc, double* best_e, int* best_k, int* reached,
                           long* first_hit, long* cycles_used, int* active, cudaStream_t st);
 void launch_field_simt(const Geom& g, const int8_t* J, const int8_t* sig, int32_t* S,

@@ -78,7 +78,9 @@ struct TcParams {
   double hi_clamp, lo_clamp;    // i0 - alpha, -i0 (formed on the host)
   long c_first, c_last;  // cycles handled: scans/updates for c in [c_first, c_last]
   long sc;               // update iff c < sc
-  int run_mode;          // 1: scans + results; 0: plain sweeps (per-step API)
+  int run_mode;          // 1: scans + results; 0: plain sweeps (per-step API);
+                         // 2: one pass over a row shard (energy partials -> gE, no scan)
+  int shard_rt0, shard_nrt;  // run_mode 2: the shard's row tiles
   int has_target, stop_at_target, record_trace;
   double target_tol;
   int ring_cur;
@@ -782,8 +784,12 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
   const int col0 = tile * NT;
   const int ntl = max(0, min(g.tpt, g.T - tile * g.tpt));
   const int NRT_all = g.npad / kBM;
-  const int rt_lo = int((long long)NRT_all * part / RS);
-  const int NRT = int((long long)NRT_all * (part + 1) / RS) - rt_lo;  // row tiles of this CTA
+  const bool scan_mode = P.run_mode == 1;   // scans, results, row-split protocol
+  const bool shard_mode = P.run_mode == 2;  // one pass over the rows of a GPU shard
+  const int rt_base = shard_mode ? P.shard_rt0 : 0;
+  const int rt_span = shard_mode ? P.shard_nrt : NRT_all;
+  const int rt_lo = rt_base + int((long long)rt_span * part / RS);
+  const int NRT = rt_base + int((long long)rt_span * (part + 1) / RS) - rt_lo;  // this CTA's
   // one stage = 128 bytes of K per row: 128 int8 or 256 e2m1 couplings/spins
   // (an FP4 row of npad = 128 is a partial chunk: TMA zero-fills the rest)
   const int NKC = F4 ? (g.npad + 2 * kBK - 1) / (2 * kBK) : g.npad / kBK;
@@ -1043,7 +1049,7 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
     // written a group of its row tiles in pass c, stamp them for the other
     // CTAs of the column tile (their producers load all rows of sigma) =====
     SSQA_CTL_REGS();
-    if (split && lane == 0) {
+    if (split && scan_mode && lane == 0) {
       for (long c = P.c_first; c <= P.c_last; ++c) {
         const long s = c - P.c_first;
         if (s > 0 && stop_at(c)) break;
@@ -1200,8 +1206,14 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
         return ep;
       };
       unsigned long long* gE_pass = split ? P.gE + size_t(s_idx & 1) * g.ccols + col0 : nullptr;
-      bool do_scan = P.run_mode && !drain;
-      if (split && P.run_mode && !drain) {
+      bool do_scan = scan_mode && !drain;
+      if (shard_mode) {
+        // GPU row shard: this CTA's row partials of the pass energies; the
+        // host all-gathers them with the shard's spin rows and scans
+        for (int cl = ew * 32 + lane; cl < NT; cl += EPI * 32)
+          atomicAdd(P.gE + col0 + cl, static_cast<unsigned long long>(cta_energy(cl)));
+      }
+      if (split && scan_mode && !drain) {
         // Row split: add this CTA's row partials to the column tile's pass
         // sums; the last CTA of the tile to arrive scans the pass.
         for (int cl = ew * 32 + lane; cl < NT; cl += EPI * 32)
@@ -1278,7 +1290,7 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
         }
       }
       epi_bar<EPI>();
-      if (split && P.run_mode && !drain) {
+      if (split && scan_mode && !drain) {
         if (do_scan) {
           // publish the scan: trial table -> global, clear the pass sums
           for (int t = ew * 32 + lane; t < ntl; t += 32 * EPI) {
@@ -1315,7 +1327,7 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
       epi_bar<EPI>();
       if (ew == 0 && lane == 0) {
         if (do_update) ring_advance(ring, c, P.d, P.nslots);
-        if (P.run_mode && !drain) {
+        if (scan_mode && !drain) {
           int any = 0;
           if (split) any = !ctl->scan_stop;
           else
@@ -1326,7 +1338,7 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
         }
       }
       epi_bar<EPI>();
-      if (P.run_mode && !drain && c + 1 == *reinterpret_cast<volatile long*>(&ctl->last_pass) &&
+      if (scan_mode && !drain && c + 1 == *reinterpret_cast<volatile long*>(&ctl->last_pass) &&
           c + 1 <= P.c_last) {
         int any = 0;
         if (split) any = !ctl->scan_stop;
@@ -1337,11 +1349,11 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
     }
     // results of this CTA's trials (the epilogue warps own the trial table)
     epi_bar<EPI>();
-    if (P.run_mode && part == 0) {
+    if (scan_mode && part == 0) {
       for (int t = ew; t < ntl; t += EPI)
         expand_best_state<F4>(P, tile * g.tpt + t, g.n, g.npad, lane);
     }
-    if (P.run_mode && !split) {  // with a row split the scanners keep global current
+    if (scan_mode && !split) {  // with a row split the scanners keep global current
       for (int t = ew * 32 + lane; t < ntl; t += 32 * EPI) {
         const int tg = tile * g.tpt + t;
         P.best_e[tg] = trials[t].best_e;
@@ -1461,7 +1473,7 @@ void watchdog_bind(int device) {
 
 int launch(ssqa_batch_s* b, TcParams& P, bool f4) {
   watchdog_bind(b->prob->device);
-  const Geom& g = b->g;
+  const Geom& g = P.g;  // the batch geometry (a shard pass may use its own row split)
   CUtensorMap maps[4];
   const uint64_t srows = uint64_t(b->nslots) * g.ccols;
   // FP4 rows are npad/2 bytes (two e2m1 values per byte)
@@ -1481,7 +1493,7 @@ int launch(ssqa_batch_s* b, TcParams& P, bool f4) {
     g_tc_err = "cuTensorMapEncodeTiled failed";
     return SSQA_ECUDA;
   }
-  if (g.rs > 1) {
+  if (g.rs > 1 && P.run_mode == 1) {
     // row-split synchronisation state, zeroed for every launch
     const int nrt_all = g.npad / kBM;
     const size_t bytes = size_t(2) * g.ccols * 8 + size_t(g.ntiles) * 8 +
@@ -1690,6 +1702,28 @@ int tc_sweep(ssqa_batch_s* b, double jperp, double i0) {
   int rc = launch(b, P, false);
   if (rc) return rc;
   advance_ring(b, 1);
+  return SSQA_OK;
+}
+
+int tc_shard_pass(ssqa_batch_s* b, int rt0, int nrt, unsigned long long* gE) {
+  if (b->d > kMaxDelay) {
+    g_tc_err = "tcgen05 engine supports delay <= 30";
+    return SSQA_EUNSUP;
+  }
+  TcParams P = base_params(b);
+  P.c_first = b->cycle;
+  P.c_last = b->cycle;
+  P.sc = b->p.sc;  // cycle sc scans without an update
+  P.run_mode = 2;
+  P.shard_rt0 = rt0;
+  P.shard_nrt = nrt;
+  P.gE = gE;
+  // row split of the shard's rows over the SMs the column tiles leave free
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, b->prob->device);
+  P.g.rs = std::max(1, std::min(nrt, sms / std::max(1, P.g.ntiles)));
+  int rc = launch(b, P, false);
+  if (rc) return rc;
   return SSQA_OK;
 }
 

@@ -16,6 +16,11 @@ bool tc_uses_fp4(const ssqa_batch_s* b);
 int tc_run(ssqa_batch_s* b, const ScanArgs& sa);
 // One sweep at b->cycle without a scan (per-step API).
 int tc_sweep(ssqa_batch_s* b, double jperp, double i0);
+// GPU row shard: one pass at b->cycle over row tiles [rt0, rt0 + nrt) with
+// int8 spin slots (sigma(c+1) of those rows, acc), the pass energies' row
+// partials added into gE[ccols] (zeroed by the caller); the ring is not
+// advanced (the caller merges all shards' rows first).
+int tc_shard_pass(ssqa_batch_s* b, int rt0, int nrt, unsigned long long* gE);
 const char* tc_last_error();
 // Non-empty after a kernel watchdog fired: who was stuck on which mbarrier.
 std::string tc_watchdog_message();

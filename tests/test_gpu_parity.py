@@ -528,3 +528,44 @@ def test_wide_row_split_default_heuristic(orc):
         assert res[t].best_energy == o.best_energy and res[t].best_replica == o.best_replica
         assert np.array_equal(res[t].best_state, o.best_state)
         assert np.array_equal(bits(res[t].trace_energy), bits(o.trace))
+
+
+# ---- GPU row shards: per-cycle pass / all-gather / merge ----
+
+@pytest.mark.parametrize("nshards", [1, 2, 4])
+def test_row_shards_emulated_match_oracle(orc, nshards):
+    """Every shard of a G-way J' row shard (run one after another on one GPU,
+    exchanging through one buffer) equals the oracle's ssqa_run."""
+    if not engine_ok(_lib.ENGINE_TCGEN05):
+        pytest.skip("tcgen05 engine unavailable")
+    from paper_2302_12454_b200.rowshard import run_emulated_shards
+    cases = [(sq.gi_ising(20, 0.5, 7, True, 1.0, 1.0), params(20, 40), [31, 32, 33], True),
+             (sq.dense_ising(512, 0, 9), params(6, 25, tau=3, delay=2, bidirectional=True),
+              [5, 6], False)]
+    for m, p, seeds, stop in cases:
+        target = float(orc.ssqa_run(m.h, m.J, m.offset, p, seeds[0], None, False,
+                                    False).best_energy) if stop else None
+        runs = run_emulated_shards(m, to_sq(p), seeds, nshards, target,
+                                   sq.RunOptions(True, stop))
+        for t, sd in enumerate(seeds):
+            o = orc.ssqa_run(m.h, m.J, m.offset, p, sd, target, True, stop)
+            for g, res in enumerate(runs):
+                r = res[t]
+                assert (r.best_energy, r.best_replica, r.reached_target, r.first_hit_cycle,
+                        r.cycles_used) == (o.best_energy, o.best_replica, o.reached_target,
+                                           o.first_hit_cycle, o.cycles_used), (nshards, g, t)
+                assert np.array_equal(r.best_state, o.best_state), (nshards, g, t)
+                assert np.array_equal(bits(r.trace_energy), bits(o.trace)), (nshards, g, t)
+
+
+def test_row_sharded_single_rank(orc):
+    if not engine_ok(_lib.ENGINE_TCGEN05):
+        pytest.skip("tcgen05 engine unavailable")
+    from paper_2302_12454_b200.rowshard import run_row_sharded
+    m = sq.dense_ising(256, 0, 2)
+    p = params(8, 30, tau=5)
+    res = run_row_sharded(m, to_sq(p), [3, 4], None, sq.RunOptions(True, False))
+    for t, sd in enumerate([3, 4]):
+        o = orc.ssqa_run(m.h, m.J, m.offset, p, sd, None, True, False)
+        assert res[t].best_energy == o.best_energy
+        assert np.array_equal(bits(res[t].trace_energy), bits(o.trace))

@@ -92,3 +92,72 @@ def test_gloo_world2_matches_single_rank(orc):
         single.append((s, r.reached_target, r.first_hit_cycle, r.best_energy))
     assert allo == single
     assert hits == sum(int(x[1]) for x in single)
+
+
+# ---- J' row shards: the per-cycle exchange loop (rowshard.shard_cycles) ----
+
+class _FakeShardBatch:
+    """Stands in for a device batch on CPU: shard_pass writes a chunk that
+    encodes (rank, cycle); shard_merge checks every shard's chunk arrived in
+    shard order for the same cycle."""
+
+    def __init__(self, buf, rank, world, nbytes):
+        self.buf, self.rank, self.world, self.nb = buf, rank, world, nbytes
+        self.cycle = 0
+        self.merged = []
+
+    def shard_bytes(self):
+        return self.nb
+
+    def shard_pass(self, ptr):
+        off = ptr - self.buf.data_ptr()
+        assert off == self.rank * self.nb
+        self.buf[off:off + self.nb] = (self.rank * 16 + self.cycle) % 251
+
+    def shard_merge(self, ptr):
+        assert ptr == self.buf.data_ptr()
+        got = [int(self.buf[g * self.nb]) for g in range(self.world)]
+        assert got == [(g * 16 + self.cycle) % 251 for g in range(self.world)], got
+        self.merged.append(self.cycle)
+        self.cycle += 1
+
+
+def _shard_worker(rank, world, port, cycles, out_q):
+    import sys
+    import torch
+    import torch.distributed as dist
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    from paper_2302_12454_b200.rowshard import shard_cycles
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    nb = 96
+    buf = torch.zeros(world * nb, dtype=torch.uint8)
+    b = _FakeShardBatch(buf, rank, world, nb)
+
+    def all_gather(out, mine):
+        parts = [torch.empty_like(mine) for _ in range(world)]
+        dist.all_gather(parts, mine.clone())
+        out.copy_(torch.cat(parts))
+
+    shard_cycles(b, buf, rank, world, cycles, all_gather)
+    out_q.put((rank, b.merged))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_row_shard_exchange_gloo_world2():
+    """world_size 2 (gloo, CPU): every cycle each rank passes into its own
+    chunk, the all-gather leaves the chunks in rank order, and every rank
+    merges all of them for the same cycle (host logic of rowshard)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_shard_worker, args=(r, 2, port, 5, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    got = dict(q.get(timeout=120) for _ in range(2))
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    assert got == {0: list(range(5)), 1: list(range(5))}
