@@ -100,6 +100,15 @@ const char* ssqa_version(void);
 int ssqa_problem_create(int n, const double* h, const double* J, double offset, int device,
                         ssqa_problem* out);
 int ssqa_problem_destroy(ssqa_problem prob);
+/* Fresh instances per trial (run_trials with fresh_instance, bench.cpp:387-389):
+ * `count` models of n spins -- h[count*n], J[count*n*n], offsets[count] --
+ * quantized at one common scale and stacked on the device.  A batch on such
+ * a problem must have trials == count; trial t anneals instance t (tcgen05
+ * engine, one trial per column tile).  ssqa_problem_count() is 1 for
+ * ssqa_problem_create problems. */
+int ssqa_problem_create_many(int count, int n, const double* h, const double* J,
+                             const double* offsets, int device, ssqa_problem* out);
+int ssqa_problem_count(ssqa_problem prob);
 /* Quantizer report: padded size, scale exponent p, max |J'|, max |H'|. */
 int ssqa_problem_info(ssqa_problem prob, int* n, int* n_pad, int* shift_p, int* max_abs_j,
                       int* max_abs_h);

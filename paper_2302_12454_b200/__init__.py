@@ -8,7 +8,8 @@ from .api import (  # noqa: F401
     AnnealResult, Batch, IsingModel, K_TARGET_TOL, Problem, ReplicaLattice, RunOptions,
     SsaParams, SsqaParams, TracePoint, TrialOutcome, TtsValue, compute_tts, dense_ising,
     gi_ising, i0_schedule, init_lattice, ising_energy, jperp_schedule, replica_energies,
-    run_trials, ssa_run, ssa_run_batch, ssqa_run, ssqa_run_batch, ssqa_sweep,
+    run_trials, run_trials_fresh, ssa_run, ssa_run_batch, ssqa_run, ssqa_run_batch, ssqa_sweep,
+    trial_instance_seeds,
 )
 from ._lib import (  # noqa: F401
     ENGINE_AUTO, ENGINE_SIMT, ENGINE_TCGEN05, SsqaError, SsqaInvalidArgument, lib,

@@ -51,6 +51,9 @@ SIGNATURES = [
     ("ssqa_version", C.c_char_p, []),
     ("ssqa_problem_create", C.c_int, [C.c_int, DP, DP, C.c_double, C.c_int, C.POINTER(VP)]),
     ("ssqa_problem_destroy", C.c_int, [VP]),
+    ("ssqa_problem_create_many", C.c_int, [C.c_int, C.c_int, DP, DP, DP, C.c_int,
+                                           C.POINTER(VP)]),
+    ("ssqa_problem_count", C.c_int, [VP]),
     ("ssqa_problem_info", C.c_int, [VP, IP, IP, IP, IP, IP]),
     ("ssqa_quantize_info", C.c_int, [C.c_int, DP, DP, IP, IP, IP, IP]),
     ("ssqa_problem_fp4", C.c_int, [VP]),

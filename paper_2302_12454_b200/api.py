@@ -200,6 +200,22 @@ class Problem:
                                         _dp(np.ascontiguousarray(m.J)), m.offset, device,
                                         C.byref(self._h)))
 
+    @classmethod
+    def from_models(cls, models: Sequence[IsingModel], device: int = 0) -> "Problem":
+        """One problem holding a fresh instance per trial
+        (ssqa_problem_create_many; a batch on it runs trial t on models[t])."""
+        self = cls.__new__(cls)
+        n = models[0].n
+        assert all(mm.n == n for mm in models), "instances must have the same size"
+        self.n = n
+        self._h = C.c_void_p()
+        h = np.ascontiguousarray(np.concatenate([mm.h for mm in models]))
+        J = np.ascontiguousarray(np.concatenate([mm.J.reshape(-1) for mm in models]))
+        off = np.ascontiguousarray([mm.offset for mm in models], dtype=np.float64)
+        check(lib().ssqa_problem_create_many(len(models), n, _dp(h), _dp(J), _dp(off), device,
+                                             C.byref(self._h)))
+        return self
+
     def info(self) -> dict:
         v = [C.c_int() for _ in range(5)]
         check(lib().ssqa_problem_info(self._h, *[C.byref(x) for x in v]))
@@ -494,6 +510,47 @@ class TrialOutcome:
     first_hit_cycle: int
     best_energy: float
     wall_seconds: float
+
+
+def _mix64(x: int) -> int:
+    """rng.hpp:10-15 on Python ints."""
+    M = (1 << 64) - 1
+    x = (x + 0x9E3779B97F4A7C15) & M
+    x = ((x ^ (x >> 30)) * 0xBF58476D1CE4E5B9) & M
+    x = ((x ^ (x >> 27)) * 0x94D049BB133111EB) & M
+    return x ^ (x >> 31)
+
+
+def trial_instance_seeds(base_seed: int, trials: int) -> List[int]:
+    """CounterRng(base_seed, kStreamTrialInstance).raw(t) (rng.hpp:30-38),
+    the GI instance seed of trial t in run_trials (bench.cpp:373, 389)."""
+    key = _mix64(_mix64(base_seed) ^ ((1 << 32) + 7))
+    return [_mix64((key + t * 0x9E3779B97F4A7C15) & ((1 << 64) - 1)) for t in range(trials)]
+
+
+def run_trials_fresh(n_nodes: int, p, trials: int, ec: int, base_seed: int,
+                     edge_prob: float = 0.5, permute: bool = False, c1: float = 0.75,
+                     c2: float = 0.75, p_target: float = 0.99, device: int = 0):
+    """run_trials (bench.cpp:359-432) with a fresh GI instance per trial (the
+    reference default, bench.hpp:28): instance t from seed
+    CounterRng(base_seed, kStreamTrialInstance).raw(t), target 0, the whole
+    battery as one multi-instance device batch."""
+    seeds = [base_seed + t for t in range(trials)]
+    models = [gi_ising(n_nodes, edge_prob, s, permute, c1, c2)
+              for s in trial_instance_seeds(base_seed, trials)]
+    prob = Problem.from_models(models, device)
+    if isinstance(p, SsaParams):
+        q = SsaParams(**{**p.__dict__, "sc": ec})
+        res = ssa_run_batch(models[0], q, seeds, 0.0, RunOptions(False, False), problem=prob)
+    else:
+        q = SsqaParams(**{**p.__dict__, "sc": ec // p.r})
+        res = ssqa_run_batch(models[0], q, seeds, 0.0, RunOptions(False, False), problem=prob)
+    prob.close()
+    outs = [TrialOutcome(s, r.reached_target, r.first_hit_cycle, r.best_energy, r.wall_seconds)
+            for s, r in zip(seeds, res)]
+    p_s = sum(o.reached_target for o in outs) / trials
+    t_mean = sum(o.wall_seconds for o in outs) / trials
+    return outs, p_s, t_mean, compute_tts(p_s, max(t_mean, 1e-12), p_target)
 
 
 def run_trials(m: IsingModel, p, trials: int, ec: int, base_seed: int,

@@ -118,7 +118,7 @@ int num_sms(int device) {
 // row tiles, widen the tiles (more trials per tile -> each J' row tile is
 // streamed by fewer CTAs, larger MMA N) and split each tile's rows over rs
 // CTAs (row split, one CTA per SM).  fp4: FP4 operands need tile_cols <= 240.
-Geom make_geom(int n, int npad, int R, int T, int sms, int engine, bool fp4) {
+Geom make_geom(int n, int npad, int R, int T, int sms, int engine, bool fp4, bool per_trial) {
   Geom g;
   g.n = n;
   g.npad = npad;
@@ -129,9 +129,10 @@ Geom make_geom(int n, int npad, int R, int T, int sms, int engine, bool fp4) {
   if (R <= max_cols) tpt = std::min(tpt, max_cols / R);
   else tpt = 1;
   tpt = std::max(1, std::min(tpt, T));
+  if (per_trial) tpt = 1;  // multi-instance problems: each tile reads its trial's J'
   int rs = 1;
   const int nrt = npad / 128;
-  if (engine == SSQA_ENGINE_TCGEN05 && R <= max_cols) {
+  if (engine == SSQA_ENGINE_TCGEN05 && R <= max_cols && !per_trial) {
     const int cap = fp4 ? 240 : max_cols;
     const int wide = std::max(1, std::min(T, cap / R));
     const int wtiles = (T + wide - 1) / wide;
@@ -297,6 +298,81 @@ int ssqa_problem_create(int n, const double* h, const double* J, double offset, 
 
 int ssqa_problem_fp4(ssqa_problem pr) { return (pr && pr->q.fp4_ok) ? 1 : 0; }
 
+int ssqa_problem_create_many(int count, int n, const double* h, const double* J,
+                             const double* offsets, int device, ssqa_problem* out) {
+  if (!out || !h || !J || !offsets) return set_err(SSQA_EINVAL, "null argument");
+  if (count < 1) return set_err(SSQA_EINVAL, "count must be >= 1");
+  if (n < 1 || n >= kMaxSpins) return set_err(SSQA_EINVAL, "spin count out of range");
+  const size_t nn = size_t(n) * n;
+  // one scale for all instances: the largest exponent any of them needs
+  std::vector<ssqa_engine::Quantized> qs(static_cast<size_t>(count));
+  std::string why;
+  int p = 0;
+  for (int c = 0; c < count; ++c) {
+    int rc = quantize(n, h + size_t(c) * n, J + size_t(c) * nn, offsets[c], &qs[size_t(c)], &why);
+    if (rc) return set_err(rc, "instance " + std::to_string(c) + ": " + why);
+    p = std::max(p, qs[size_t(c)].p);
+  }
+  for (int c = 0; c < count; ++c)
+    if (qs[size_t(c)].p != p) {
+      int rc = quantize(n, h + size_t(c) * n, J + size_t(c) * nn, offsets[c], &qs[size_t(c)],
+                        &why, p);
+      if (rc) return set_err(rc, "instance " + std::to_string(c) + ": " + why);
+    }
+  auto* pr = new ssqa_problem_s();
+  pr->q = qs[0];
+  pr->count = count;
+  bool fp4 = true;
+  for (auto& q : qs) {
+    pr->q.max_abs_j = std::max(pr->q.max_abs_j, q.max_abs_j);
+    pr->q.max_abs_h = std::max(pr->q.max_abs_h, q.max_abs_h);
+    fp4 = fp4 && q.fp4_ok;
+    pr->offsets.push_back(q.offset);
+  }
+  pr->q.fp4_ok = fp4;
+  const size_t npad = size_t(pr->q.npad);
+  pr->q.J.resize(size_t(count) * npad * npad);
+  pr->q.H.resize(size_t(count) * npad);
+  if (fp4) pr->q.J4.resize(size_t(count) * npad * (npad / 2));
+  else pr->q.J4.clear();
+  for (int c = 1; c < count; ++c) {
+    const Quantized& q = qs[size_t(c)];
+    std::copy(q.J.begin(), q.J.end(), pr->q.J.begin() + size_t(c) * npad * npad);
+    std::copy(q.H.begin(), q.H.end(), pr->q.H.begin() + size_t(c) * npad);
+    if (fp4) std::copy(q.J4.begin(), q.J4.end(), pr->q.J4.begin() + size_t(c) * npad * (npad / 2));
+  }
+  qs.clear();
+  pr->device = device;
+  cudaError_t e = cudaSetDevice(device);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&pr->stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaMalloc(&pr->d_J, pr->q.J.size());
+  if (e == cudaSuccess) e = cudaMalloc(&pr->d_H, pr->q.H.size() * sizeof(int32_t));
+  if (e == cudaSuccess) e = cudaMalloc(&pr->d_offsets, size_t(count) * sizeof(double));
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(pr->d_J, pr->q.J.data(), pr->q.J.size(), cudaMemcpyHostToDevice, pr->stream);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(pr->d_H, pr->q.H.data(), pr->q.H.size() * sizeof(int32_t),
+                        cudaMemcpyHostToDevice, pr->stream);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(pr->d_offsets, pr->offsets.data(), size_t(count) * sizeof(double),
+                        cudaMemcpyHostToDevice, pr->stream);
+  if (e == cudaSuccess && fp4) {
+    e = cudaMalloc(&pr->d_J4, pr->q.J4.size());
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(pr->d_J4, pr->q.J4.data(), pr->q.J4.size(), cudaMemcpyHostToDevice,
+                          pr->stream);
+  }
+  if (e == cudaSuccess) e = cudaStreamSynchronize(pr->stream);
+  if (e != cudaSuccess) {
+    ssqa_problem_destroy(pr);
+    return set_err(SSQA_ECUDA, std::string("problem upload: ") + cudaGetErrorString(e));
+  }
+  *out = pr;
+  return SSQA_OK;
+}
+
+int ssqa_problem_count(ssqa_problem pr) { return pr ? pr->count : 0; }
+
 int ssqa_quantize_info(int n, const double* h, const double* J, int* n_pad, int* shift_p,
                        int* max_abs_j, int* max_abs_h) {
   if (!h || !J) return set_err(SSQA_EINVAL, "null argument");
@@ -318,6 +394,7 @@ int ssqa_problem_destroy(ssqa_problem pr) {
   dfree(pr->d_J);
   dfree(pr->d_H);
   dfree(pr->d_J4);
+  dfree(pr->d_offsets);
   if (pr->stream) cudaStreamDestroy(pr->stream);
   delete pr;
   return SSQA_OK;
@@ -344,12 +421,20 @@ int create_batch(ssqa_problem pr, const ssqa_params_c* p, int trials, int record
                  int engine, const std::vector<double>* levels, int tau, ssqa_batch* out) {
   int rc = SSQA_OK;
   if (trials < 1) return set_err(SSQA_EINVAL, "trials must be >= 1");
+  if (pr->count > 1) {
+    if (trials != pr->count)
+      return set_err(SSQA_EINVAL, "a multi-instance problem needs one trial per instance");
+    if (engine == SSQA_ENGINE_SIMT)
+      return set_err(SSQA_EUNSUP, "multi-instance problems need the tcgen05 engine");
+  }
   CU(cudaSetDevice(pr->device));
   int eng = engine;
   if (eng == SSQA_ENGINE_AUTO) eng = tc_supported(pr->q.npad, p->r, p->delay) ? SSQA_ENGINE_TCGEN05
                                                                     : SSQA_ENGINE_SIMT;
   if (eng == SSQA_ENGINE_TCGEN05 && !tc_supported(pr->q.npad, p->r, p->delay))
     return set_err(SSQA_EUNSUP, "tcgen05 engine does not support this shape");
+  if (pr->count > 1 && eng != SSQA_ENGINE_TCGEN05)
+    return set_err(SSQA_EUNSUP, "multi-instance problems need the tcgen05 engine");
   if (eng != SSQA_ENGINE_SIMT && eng != SSQA_ENGINE_TCGEN05)
     return set_err(SSQA_EINVAL, "unknown engine");
 
@@ -365,7 +450,8 @@ int create_batch(ssqa_problem pr, const ssqa_params_c* p, int trials, int record
   b->record_trace = record_trace;
   b->d = p->delay;
   b->nslots = p->delay + 3;
-  b->g = make_geom(pr->q.n, pr->q.npad, p->r, trials, num_sms(pr->device), eng, pr->q.fp4_ok);
+  b->g = make_geom(pr->q.n, pr->q.npad, p->r, trials, num_sms(pr->device), eng, pr->q.fp4_ok,
+                   pr->count > 1);
   b->slot_elems = size_t(b->g.ccols) * b->g.npad;
   b->phys.assign(size_t(b->d) + 1, 0);
   const int T = trials;
@@ -527,6 +613,7 @@ int ssqa_batch_elapsed_ms(ssqa_batch b, double* ms) {
 
 int ssqa_batch_profile_field(ssqa_batch b, int iters, double* ms_per_launch) {
   if (!b || !ms_per_launch || iters < 1) return set_err(SSQA_EINVAL, "bad argument");
+  if (b->prob->count > 1) return set_err(SSQA_EUNSUP, "field profile of a multi-instance batch");
   CU(cudaSetDevice(b->prob->device));
   cudaStream_t st = b->prob->stream;
   int32_t* S = b->d_S;
@@ -662,6 +749,7 @@ int ssqa_batch_set_shard(ssqa_batch b, int shard, int nshards) {
   const int nrt = b->g.npad / 128;
   if (nrt % nshards != 0)
     return set_err(SSQA_EUNSUP, "padded spin count / 128 must divide into the shards");
+  if (b->prob->count > 1) return set_err(SSQA_EUNSUP, "row shards of a multi-instance problem");
   if (b->d > 30) return set_err(SSQA_EUNSUP, "tcgen05 engine supports delay <= 30");
   b->shard = shard;
   b->nshards = nshards;
@@ -783,6 +871,7 @@ int ssqa_batch_sweep(ssqa_batch b, long count) {
 
 int ssqa_batch_energies(ssqa_batch b, double* out) {
   if (!b || !out) return set_err(SSQA_EINVAL, "null argument");
+  if (b->prob->count > 1) return set_err(SSQA_EUNSUP, "energies of a multi-instance batch");
   CU(cudaSetDevice(b->prob->device));
   const Geom& g = b->g;
   // fields + integer energies of the current state (no update, no scan)

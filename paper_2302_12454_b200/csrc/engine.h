@@ -45,14 +45,21 @@ struct Quantized {
   std::vector<uint8_t> J4;           // [npad * npad/2]
 };
 
-// Returns SSQA_OK or SSQA_EUNSUP with *why set.
+// Returns SSQA_OK or SSQA_EUNSUP with *why set.  p_min: lower bound of the
+// scale exponent (several instances quantized at one common scale).
 int quantize(int n, const double* h, const double* J, double offset, Quantized* q,
-             std::string* why);
+             std::string* why, int p_min = 0);
 
 }  // namespace ssqa_engine
 
 struct ssqa_problem_s {
-  ssqa_engine::Quantized q;
+  ssqa_engine::Quantized q;  // instance 0 (scale, ranges over all instances)
+  // Multi-instance problems (ssqa_problem_create_many): `count` models of the
+  // same size at one scale 2^-p, stacked in d_J / d_J4 [count][npad][...] and
+  // d_H [count][npad]; trial t of a batch anneals instance t.
+  int count = 1;
+  std::vector<double> offsets;
+  double* d_offsets = nullptr;
   int device = 0;
   cudaStream_t stream = nullptr;
   int8_t* d_J = nullptr;

@@ -66,9 +66,10 @@ void atomic_min(std::atomic<long long>& a, long long v) {
 }  // namespace
 
 int quantize(int n, const double* h, const double* J, double offset, Quantized* q,
-             std::string* why) {
+             std::string* why, int p_min) {
   // scale exponent: the largest dyadic exponent of any bias or coupling
-  int p = 0;
+  // (at least p_min, so several instances can share one scale)
+  int p = std::max(0, p_min);
   for (int i = 0; i < n; ++i) {
     int e = dyadic_exponent(h[i]);
     if (e < 0) {

@@ -81,6 +81,8 @@ struct TcParams {
   int run_mode;          // 1: scans + results; 0: plain sweeps (per-step API);
                          // 2: one pass over a row shard (energy partials -> gE, no scan)
   int shard_rt0, shard_nrt;  // run_mode 2: the shard's row tiles
+  int multi;                 // multi-instance problem: tile t = trial t = instance t
+  const double* offsets;     // multi: per-instance offsets
   int has_target, stop_at_target, record_trace;
   double target_tol;
   int ring_cur;
@@ -793,6 +795,8 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
   // one stage = 128 bytes of K per row: 128 int8 or 256 e2m1 couplings/spins
   // (an FP4 row of npad = 128 is a partial chunk: TMA zero-fills the rest)
   const int NKC = F4 ? (g.npad + 2 * kBK - 1) / (2 * kBK) : g.npad / kBK;
+  // multi-instance problems: this tile's trial anneals its own J', H', offset
+  const int j_row0 = P.multi ? tile * g.npad : 0;
   const int nchunk = NT / kCW;
   const int acc_cols = NT;
   constexpr int nsubs = EPI / 4;         // epilogue subgroups (4 warps each)
@@ -941,7 +945,7 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
             mbar_wait(&ctl->empty[st], ph ^ 1);
             mbar_expect_tx(&ctl->full[st], L.a_bytes + L.b_bytes);
             tma_load_2d_hint(&tmJ, &ctl->full[st], sA + size_t(st) * L.a_bytes, kc * kBK,
-                             (rt_lo + rt) * kBM, pol_keep);
+                             j_row0 + (rt_lo + rt) * kBM, pol_keep);
             tma_load_2d(&tmS, &ctl->full[st], sB + size_t(st) * L.b_bytes, kc * kBK, yS);
           }
         }
@@ -1146,7 +1150,7 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
             if (lane == 0) mbar_arrive(&ctl->aempty[slot]);
           }
         } else {
-          const int h1 = row_live ? P.H[i] : 0;
+          const int h1 = row_live ? P.H[j_row0 + i] : 0;
           const int h2 = 2 * h1;
           EpiRow er;
           er.acc_i = reinterpret_cast<uint64_t>(P.acc + i);
@@ -1254,7 +1258,8 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
           for (int k = lane; k < g.R; k += 32) {
             const long long ep = split ? (long long)__ldcg(gE_pass + t * g.R + k)
                                        : cta_energy(t * g.R + k);
-            const double ek = __dadd_rn(__dmul_rn(-0.5, scaled(ep, P.scale)), P.offset);
+            const double ek = __dadd_rn(__dmul_rn(-0.5, scaled(ep, P.scale)),
+                                        P.multi ? P.offsets[tg] : P.offset);
             if (P.record_trace) P.trace[(size_t(tg) * (P.sc + 1) + c) * g.R + k] = ek;
             if (ek < bmin) {
               bmin = ek;
@@ -1482,8 +1487,8 @@ int launch(ssqa_batch_s* b, TcParams& P, bool f4) {
   void* Ssrc = f4 ? static_cast<void*>(b->d_sig4) : static_cast<void*>(b->d_sig);
   const uint32_t tile_row = f4 ? kBM / 2 : kBM;
   P.sig_base = static_cast<uint8_t*>(Ssrc);
-  if (!make_map(&maps[0], Jsrc, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, row_bytes, g.npad, kBK, kBM,
-                CU_TENSOR_MAP_SWIZZLE_128B) ||
+  if (!make_map(&maps[0], Jsrc, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, row_bytes,
+                uint64_t(g.npad) * b->prob->count, kBK, kBM, CU_TENSOR_MAP_SWIZZLE_128B) ||
       !make_map(&maps[1], Ssrc, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, row_bytes, srows, kBK,
                 g.tile_cols, CU_TENSOR_MAP_SWIZZLE_128B) ||
       !make_map(&maps[2], Ssrc, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, row_bytes, srows, tile_row,
@@ -1586,6 +1591,8 @@ TcParams base_params(ssqa_batch_s* b) {
   TcParams P{};
   P.g = b->g;
   P.H = b->prob->d_H;
+  P.multi = b->prob->count > 1 ? 1 : 0;
+  P.offsets = b->prob->d_offsets;
   P.scale = b->prob->q.scale;
   P.offset = b->prob->q.offset;
   P.shift_p = b->prob->q.p;

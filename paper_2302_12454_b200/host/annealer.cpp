@@ -64,6 +64,23 @@ void upload(const IsingModel& m, int device, ProblemHandle& h) {
                             &h.p));
 }
 
+// One problem holding every model (one per trial): ssqa_problem_create_many.
+void upload_many(const std::vector<IsingModel>& ms, int device, ProblemHandle& h) {
+  if (ms.empty()) throw std::invalid_argument("no models");
+  const int n = ms.front().n();
+  std::vector<double> hs, js, offs;
+  hs.reserve(ms.size() * size_t(n));
+  js.reserve(ms.size() * size_t(n) * n);
+  for (const IsingModel& m : ms) {
+    if (m.n() != n) throw std::invalid_argument("instances must have the same size");
+    hs.insert(hs.end(), m.biases().begin(), m.biases().end());
+    js.insert(js.end(), m.coupling_data(), m.coupling_data() + size_t(n) * n);
+    offs.push_back(m.offset());
+  }
+  check(ssqa_problem_create_many(int(ms.size()), n, hs.data(), js.data(), offs.data(), device,
+                                 &h.p));
+}
+
 // A one-trial batch carrying an explicit lattice (per-step API).
 void load(BatchHandle& bh, ProblemHandle& ph, const ReplicaLattice& lat, SsqaParams p,
           uint64_t seed) {
@@ -225,6 +242,31 @@ AnnealResult ssqa_run(const IsingModel& m, const SsqaParams& p, uint64_t seed,
   return ssqa_run_batch(m, p, {seed}, target_energy, opts).front();
 }
 
+std::vector<AnnealResult> ssqa_run_instances(const std::vector<IsingModel>& models,
+                                             const SsqaParams& p,
+                                             const std::vector<uint64_t>& seeds,
+                                             std::optional<double> target_energy,
+                                             const RunOptions& opts, const EngineOptions& eng) {
+  if (models.size() != seeds.size()) throw std::invalid_argument("one model per seed");
+  if (seeds.empty()) return {};
+  const int n = models.front().n();
+  p.validate(n);
+  ProblemHandle ph;
+  upload_many(models, eng.device, ph);
+  const int T = int(seeds.size());
+  ssqa_params_c c = to_c(p);
+  std::vector<ssqa_result_c> res(seeds.size());
+  std::vector<int8_t> best(size_t(T) * n);
+  std::vector<double> trace;
+  if (opts.record_trace) trace.resize(size_t(T) * (p.sc + 1) * p.r);
+  check(ssqa_run_batch(ph.p, &c, seeds.data(), T, target_energy ? 1 : 0,
+                       target_energy.value_or(0.0), opts.record_trace ? 1 : 0,
+                       opts.stop_at_target ? 1 : 0, eng.engine, res.data(), best.data(),
+                       opts.record_trace ? trace.data() : nullptr));
+  return to_results(T, n, p.r, p.sc, res, best, trace, opts.record_trace,
+                    [&p](long c) { return jperp_schedule(c, p); });
+}
+
 std::vector<double> SsaParams::i0_levels() const {
   ssqa_ssa_params_c c = to_c(*this);
   double buf[65];
@@ -272,6 +314,31 @@ std::vector<AnnealResult> ssa_run_batch(const IsingModel& m, const SsaParams& p,
 AnnealResult ssa_run(const IsingModel& m, const SsaParams& p, uint64_t seed,
                      std::optional<double> target_energy, const RunOptions& opts) {
   return ssa_run_batch(m, p, {seed}, target_energy, opts).front();
+}
+
+std::vector<AnnealResult> ssa_run_instances(const std::vector<IsingModel>& models,
+                                            const SsaParams& p,
+                                            const std::vector<uint64_t>& seeds,
+                                            std::optional<double> target_energy,
+                                            const RunOptions& opts, const EngineOptions& eng) {
+  if (models.size() != seeds.size()) throw std::invalid_argument("one model per seed");
+  if (seeds.empty()) return {};
+  const int n = models.front().n();
+  p.validate(n);
+  ProblemHandle ph;
+  upload_many(models, eng.device, ph);
+  const int T = int(seeds.size());
+  ssqa_ssa_params_c c = to_c(p);
+  std::vector<ssqa_result_c> res(seeds.size());
+  std::vector<int8_t> best(size_t(T) * n);
+  std::vector<double> trace;
+  if (opts.record_trace) trace.resize(size_t(T) * (p.sc + 1));
+  check(ssqa_ssa_run_batch(ph.p, &c, seeds.data(), T, target_energy ? 1 : 0,
+                           target_energy.value_or(0.0), opts.record_trace ? 1 : 0,
+                           opts.stop_at_target ? 1 : 0, eng.engine, res.data(), best.data(),
+                           opts.record_trace ? trace.data() : nullptr));
+  return to_results(T, n, 1, p.sc, res, best, trace, opts.record_trace,
+                    [](long) { return 0.0; });
 }
 
 }  // namespace ssqa

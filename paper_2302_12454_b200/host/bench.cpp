@@ -140,12 +140,19 @@ BenchRecord run_trials(const BenchConfig& cfg) {
     n = m.n();
     results = run(m, seeds, target);
   } else {
-    // Fresh instance per trial (bench.cpp:387-389): one device run each.
+    // Fresh instance per trial (bench.cpp:387-389): every trial's GI instance
+    // in one multi-instance problem, the whole battery in one device batch.
     const CounterRng inst(cfg.base_seed, kStreamTrialInstance);
-    for (int t = 0; t < cfg.trials; ++t) {
-      IsingModel m = gi_model(cfg.problem, inst.raw(uint64_t(t)));
-      n = m.n();
-      results.push_back(run(m, {seeds[size_t(t)]}, 0.0).front());
+    std::vector<IsingModel> models;
+    models.reserve(size_t(cfg.trials));
+    for (int t = 0; t < cfg.trials; ++t) models.push_back(gi_model(cfg.problem, inst.raw(uint64_t(t))));
+    n = models.front().n();
+    if (ssa || (p.r <= 256 && p.delay <= 30)) {
+      results = ssa ? ssa_run_instances(models, ps, seeds, 0.0, opts, eng)
+                    : ssqa_run_instances(models, p, seeds, 0.0, opts, eng);
+    } else {  // shapes only the SIMT engine takes: one device run per instance
+      for (int t = 0; t < cfg.trials; ++t)
+        results.push_back(run(models[size_t(t)], {seeds[size_t(t)]}, 0.0).front());
     }
   }
   BenchRecord rec;

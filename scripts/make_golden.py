@@ -212,11 +212,30 @@ def trials(ref: Oracle):
         outcomes_fnv=np.uint64(fnv1a(buf)))}
 
 
+def trials_fresh(ref: Oracle):
+    """run_trials with a fresh GI instance per trial (the reference default,
+    bench.hpp:28; instance seeds CounterRng(base_seed, 7).raw(t), bench.cpp:389)."""
+    out = {}
+    cases = [("fresh_gi10", dict(n_nodes=10, trials=64, ec=20000, base_seed=1000, permute=False,
+                                 c1=0.75, c2=0.75), 20),
+             ("fresh_gi20", dict(n_nodes=20, trials=24, ec=10000, base_seed=77, permute=True,
+                                 c1=1.0, c2=1.0), 20)]
+    for name, kw, r in cases:
+        outs, ps, tm, tts = ref.run_trials(params(r, 1), workers=8, fresh_instance=True, **kw)
+        out[name] = dict(**{f"k_{k}": v for k, v in kw.items()}, r=r,
+                         seed=np.array([o["seed"] for o in outs], np.uint64),
+                         reached=np.array([o["reached_target"] for o in outs], np.int8),
+                         first_hit=np.array([o["first_hit_cycle"] for o in outs], np.int64),
+                         best_energy=np.array([o["best_energy"] for o in outs]), p_s=ps)
+    return out
+
+
 def main():
     ref = Oracle("ref")
     os.makedirs(OUT, exist_ok=True)
     jobs = [("lattice_traj", lattice_trajectories), ("gi_instances", gi_instances),
-            ("runs", runs), ("trials", trials), ("ssa_runs", ssa_runs)]
+            ("runs", runs), ("trials", trials), ("ssa_runs", ssa_runs),
+            ("trials_fresh", trials_fresh)]
     only = set(sys.argv[1:])
     for fname, fn in jobs:
         if only and fname not in only:

@@ -300,6 +300,12 @@ int main() {
   std::printf("%d %ld %d %d\n", rs.r, rs.ec, rs.tau, int(rs.per_trial.size()));
   for (const TrialOutcome& t : rs.per_trial)
     std::printf("%d %ld %.17g\n", int(t.reached_target), t.first_hit_cycle, t.best_energy);
+  BenchConfig cf; cf.ssqa.r = 20; cf.problem.n_nodes = 10; cf.trials = 64; cf.ec = 20000;
+  cf.base_seed = 1000;  // reference defaults: fresh instances, permute off, c1 = c2 = 0.75
+  BenchRecord rf = run_trials(cf);
+  std::printf("FRESH %.17g\n", rf.p_s);
+  for (const TrialOutcome& t : rf.per_trial)
+    std::printf("F %d %ld %.17g\n", int(t.reached_target), t.first_hit_cycle, t.best_energy);
   return 0;
 }
 ''')
@@ -316,11 +322,30 @@ int main() {
     assert out[11:15] == ["1", "3000", "25", "20"]
     p = ssa_params(3000, tau=25)
     m_h, m_J, m_off = _gi10()
-    rows = out[15:]
+    fi = out.index("FRESH")
+    rows = out[15:fi]
+    fresh = golden_fresh()["fresh_gi10"]
+    assert float(out[fi + 1]) == float(fresh["p_s"])
+    fr = out[fi + 2:]
+    for t in range(64):
+        assert fr[4 * t] == "F"
+        assert (int(fr[4 * t + 1]), int(fr[4 * t + 2]), float(fr[4 * t + 3])) == (
+            int(fresh["reached"][t]), int(fresh["first_hit"][t]), float(fresh["best_energy"][t]))
     for t in range(20):
         o = orc.ssa_run(m_h, m_J, m_off, p, 1000 + t, 0.0, False, False)
         assert (rows[3 * t] == "1", int(rows[3 * t + 1]), float(rows[3 * t + 2])) == \
             (o.reached_target, o.first_hit_cycle, o.best_energy), t
+
+
+def golden_fresh():
+    import os
+    z = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden",
+                             "trials_fresh.npz"))
+    out = {}
+    for key in z.files:
+        case, field = key.split("/", 1)
+        out.setdefault(case, {})[field] = z[key]
+    return out
 
 
 def _gi10():
@@ -569,3 +594,46 @@ def test_row_sharded_single_rank(orc):
         o = orc.ssqa_run(m.h, m.J, m.offset, p, sd, None, True, False)
         assert res[t].best_energy == o.best_energy
         assert np.array_equal(bits(res[t].trace_energy), bits(o.trace))
+
+
+# ---- fresh instance per trial (bench.hpp:28, bench.cpp:387-389) in one batch ----
+
+def test_fresh_instance_run_trials_matches_reference(golden):
+    """run_trials with fresh_instance: every trial's own GI instance in one
+    multi-instance problem, one device batch; per-trial outcomes equal the
+    reference run_trials (fixture from oracle/_ref)."""
+    if not engine_ok(_lib.ENGINE_TCGEN05):
+        pytest.skip("tcgen05 engine unavailable")
+    for name, c in golden("trials_fresh").items():
+        kw = {k[2:]: (v.item() if hasattr(v, "item") else v) for k, v in c.items()
+              if k.startswith("k_")}
+        outs, p_s, t_mean, tts = sq.run_trials_fresh(
+            int(kw["n_nodes"]), sq.SsqaParams(r=int(c["r"])), int(kw["trials"]), int(kw["ec"]),
+            int(kw["base_seed"]), permute=bool(kw["permute"]), c1=float(kw["c1"]),
+            c2=float(kw["c2"]))
+        assert [o.seed for o in outs] == [int(x) for x in c["seed"]], name
+        assert [int(o.reached_target) for o in outs] == [int(x) for x in c["reached"]], name
+        assert [o.first_hit_cycle for o in outs] == [int(x) for x in c["first_hit"]], name
+        assert np.array_equal(bits([o.best_energy for o in outs]), bits(c["best_energy"])), name
+        assert p_s == float(c["p_s"]), name
+
+
+def test_multi_instance_batch_matches_oracle(orc):
+    """Direct multi-instance batch: trial t on instance t, traces and best
+    states against the oracle's ssqa_run on that instance."""
+    if not engine_ok(_lib.ENGINE_TCGEN05):
+        pytest.skip("tcgen05 engine unavailable")
+    models = [sq.dense_ising(300, 0, s) for s in (1, 2, 3)]
+    p = params(6, 30, tau=4, bidirectional=True)
+    seeds = [11, 12, 13]
+    prob = sq.Problem.from_models(models)
+    assert _lib.lib().ssqa_problem_count(prob._h) == 3
+    res = sq.ssqa_run_batch(models[0], to_sq(p), seeds, None, sq.RunOptions(True, False),
+                            problem=prob)
+    for t, (m, s) in enumerate(zip(models, seeds)):
+        o = orc.ssqa_run(m.h, m.J, m.offset, p, s, None, True, False)
+        assert res[t].best_energy == o.best_energy, t
+        assert np.array_equal(res[t].best_state, o.best_state), t
+        assert np.array_equal(bits(res[t].trace_energy), bits(o.trace)), t
+    with pytest.raises(ValueError):  # one trial per instance
+        sq.Batch(prob, to_sq(p), 2)
