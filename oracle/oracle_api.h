@@ -95,6 +95,10 @@ int ref_ssqa_run(int n, const double* h, const double* J, double offset,
 int ref_ssqa_run_many(int n, const double* h, const double* J, double offset,
                       const orc_ssqa_params* p, const uint64_t* seeds, int trials, int workers,
                       double* best_energy);
+long ref_bench_manifest(const orc_ssqa_params* p, int n_nodes, double edge_prob, int permute,
+                        double c1, double c2, int fresh_instance, uint64_t gi_seed, int trials,
+                        long ec, double p_target, uint64_t base_seed, int workers, char* buf,
+                        long cap);
 int ref_i0_schedule(long cycle, const orc_ssa_params* p, double* out);
 int ref_ssa_run(int n, const double* h, const double* J, double offset, const orc_ssa_params* p,
                 uint64_t seed, int has_target, double target, int record_trace,

@@ -236,6 +236,24 @@ class Oracle:
             s.ctypes.data_as(C.POINTER(C.c_uint64)), len(s), workers, _dp(out)))
         return out
 
+    def bench_manifest(self, p: OrcParams, n_nodes, trials, ec, base_seed, workers,
+                       edge_prob=0.5, permute=False, c1=0.75, c2=0.75, fresh_instance=True,
+                       gi_seed=0, p_target=0.99) -> str:
+        """The reference's make_manifest("bench", ...) of a run_trials, as JSON text."""
+        assert self.kind == "ref"
+        cap = 1 << 22
+        buf = C.create_string_buffer(cap)
+        f = self.lib.ref_bench_manifest
+        f.restype = C.c_long
+        f.argtypes = [C.POINTER(OrcParams), C.c_int, C.c_double, C.c_int, C.c_double,
+                      C.c_double, C.c_int, C.c_uint64, C.c_int, C.c_long, C.c_double,
+                      C.c_uint64, C.c_int, C.c_char_p, C.c_long]
+        n = f(C.byref(p), n_nodes, edge_prob, int(permute), c1, c2, int(fresh_instance),
+              gi_seed, trials, ec, p_target, base_seed, workers, buf, cap)
+        if n < 0:
+            raise OracleError(2, self.lib.ref_last_error().decode())
+        return buf.value.decode()
+
     def gi_ising(self, n_nodes, edge_prob, seed, permute, c1, c2):
         assert self.kind == "ref"
         n = n_nodes * n_nodes

@@ -309,4 +309,36 @@ int ref_run_trials(const orc_ssqa_params* p, int n_nodes, double edge_prob, int 
   });
 }
 
+// make_manifest("bench", ...) of a run_trials (bench.cpp:519-531) serialised
+// to `buf` (manifest replay fixture for the facade's replay_manifest).
+long ref_bench_manifest(const orc_ssqa_params* p, int n_nodes, double edge_prob, int permute,
+                        double c1, double c2, int fresh_instance, uint64_t gi_seed, int trials,
+                        long ec, double p_target, uint64_t base_seed, int workers, char* buf,
+                        long cap) {
+  long len = -1;
+  int rc = guarded([&] {
+    ssqa_ref::BenchConfig cfg;
+    cfg.engine = ssqa_ref::Engine::kSsqa;
+    cfg.ssqa = make_params(p);
+    cfg.problem.n_nodes = n_nodes;
+    cfg.problem.edge_prob = edge_prob;
+    cfg.problem.permute = permute != 0;
+    cfg.problem.c1 = c1;
+    cfg.problem.c2 = c2;
+    cfg.problem.fresh_instance = fresh_instance != 0;
+    cfg.problem.gi_seed = gi_seed;
+    cfg.trials = trials;
+    cfg.ec = ec;
+    cfg.p_target = p_target;
+    cfg.base_seed = base_seed;
+    cfg.workers = workers;
+    ssqa_ref::BenchRecord rec = ssqa_ref::run_trials(cfg);
+    const std::string js = ssqa_ref::make_manifest("bench", cfg, {}, {rec}, {}).dump(1);
+    len = long(js.size());
+    if (len + 1 > cap) throw std::runtime_error("buffer too small");
+    std::memcpy(buf, js.c_str(), size_t(len) + 1);
+  });
+  return rc ? -1 : len;
+}
+
 }  // extern "C"

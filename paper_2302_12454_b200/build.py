@@ -26,6 +26,14 @@ CUDA_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
                      f"-I{os.path.join(ROOT, 'include')}", f"-I{CSRC}"]
 CXX_FLAGS = ["-O3", "-std=c++17", "-fPIC", "-Wall", f"-I{os.path.join(ROOT, 'include')}",
              f"-I{CSRC}", "-I/usr/local/cuda/include"]
+# nlohmann/json (manifests in include/ssqa/bench.hpp), as the reference uses it;
+# the image ships 3.11.3 with cuDNN's frontend headers
+JSON_DIRS = [os.environ.get("SSQA_JSON_INCLUDE", ""),
+             "/opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/thirdparty"]
+JSON_INC = next((d for d in JSON_DIRS if d and os.path.exists(os.path.join(d, "nlohmann",
+                                                                           "json.hpp"))), None)
+if JSON_INC:
+    CXX_FLAGS.append(f"-I{JSON_INC}")
 
 
 def _sources():

@@ -230,6 +230,21 @@ def trials_fresh(ref: Oracle):
     return out
 
 
+def manifests(ref: Oracle):
+    """Manifests written by the reference (make_manifest, bench.cpp:519-531),
+    replayed bitwise by the facade's replay_manifest in the GPU tests."""
+    for name, kw in [("manifest_fresh", dict(n_nodes=10, trials=12, ec=20000, base_seed=500)),
+                     ("manifest_pinned", dict(n_nodes=10, trials=20, ec=20000, base_seed=1000,
+                                              permute=True, c1=1.0, c2=1.0,
+                                              fresh_instance=False, gi_seed=7))]:
+        js = ref.bench_manifest(params(20, 1), workers=8, **kw)
+        path = os.path.join(OUT, name + ".json")
+        with open(path, "w") as f:
+            f.write(js)
+        print(f"wrote {path}: {len(js)} bytes")
+    return {}
+
+
 def main():
     ref = Oracle("ref")
     os.makedirs(OUT, exist_ok=True)
@@ -237,10 +252,12 @@ def main():
             ("runs", runs), ("trials", trials), ("ssa_runs", ssa_runs),
             ("trials_fresh", trials_fresh)]
     only = set(sys.argv[1:])
-    for fname, fn in jobs:
+    for fname, fn in jobs + [("manifests", manifests)]:
         if only and fname not in only:
             continue
         data = fn(ref)
+        if not data:
+            continue
         flat = {}
         for case, rec in data.items():
             for k, v in rec.items():

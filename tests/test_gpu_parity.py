@@ -637,3 +637,52 @@ def test_multi_instance_batch_matches_oracle(orc):
         assert np.array_equal(bits(res[t].trace_energy), bits(o.trace)), t
     with pytest.raises(ValueError):  # one trial per instance
         sq.Batch(prob, to_sq(p), 2)
+
+
+def test_cpp_manifest_replay(tmp_path):
+    """Manifests (bench.cpp:519-584): the reference-written fixtures replay
+    bitwise through the facade's replay_manifest on the GPU; a manifest the
+    facade writes replays too; a tampered outcome is reported."""
+    import os
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    from paper_2302_12454_b200 import build as bld
+    if not bld.JSON_INC:
+        pytest.skip("nlohmann/json not available")
+    src = tmp_path / "replay.cpp"
+    src.write_text(r'''
+#include <cstdio>
+#include <fstream>
+#include "ssqa/bench.hpp"
+using namespace ssqa;
+int main(int argc, char** argv) {
+  for (int a = 1; a < argc; ++a) {
+    std::ifstream f(argv[a]);
+    nlohmann::json m = nlohmann::json::parse(f);
+    ReplayResult r = replay_manifest(m);
+    std::printf("REF %d %s\n", int(r.match), r.mismatch.empty() ? "-" : r.mismatch.c_str());
+  }
+  BenchConfig c; c.ssqa.r = 16; c.problem.n_nodes = 10; c.trials = 10; c.ec = 16 * 800;
+  c.base_seed = 99;
+  BenchRecord rec = run_trials(c);
+  nlohmann::json m = make_manifest("bench", c, {}, {rec}, {"results.csv"});
+  nlohmann::json back = nlohmann::json::parse(m.dump());
+  std::printf("OWN %d\n", int(replay_manifest(back).match));
+  back["records"][0]["per_trial"][3]["best_energy"] = 1e300;
+  ReplayResult bad = replay_manifest(back);
+  std::printf("BAD %d %s\n", int(bad.match), bad.mismatch.c_str());
+  return 0;
+}
+''')
+    exe = tmp_path / "replay"
+    libdir = os.path.join(root, "paper_2302_12454_b200")
+    subprocess.run(["g++", "-std=c++17", "-O1", f"-I{root}/include", f"-I{bld.JSON_INC}",
+                    str(src), "-o", str(exe), f"-L{libdir}", "-lssqa_b200",
+                    f"-Wl,-rpath,{libdir}"], check=True)
+    gold = os.path.join(root, "tests", "golden")
+    out = subprocess.run([str(exe), os.path.join(gold, "manifest_fresh.json"),
+                          os.path.join(gold, "manifest_pinned.json")], check=True,
+                         capture_output=True, text=True).stdout.splitlines()
+    assert out[0] == "REF 1 -" and out[1] == "REF 1 -", out
+    assert out[2] == "OWN 1", out
+    assert out[3].startswith("BAD 0 trial 3 of record 0"), out
