@@ -133,8 +133,13 @@ Geom make_geom(int n, int npad, int R, int T, int sms, int engine, bool fp4, boo
   int rs = 1;
   const int nrt = npad / 128;
   if (engine == SSQA_ENGINE_TCGEN05 && R <= max_cols && !per_trial) {
-    const int cap = fp4 ? 240 : max_cols;
-    const int wide = std::max(1, std::min(T, cap / R));
+    // FP4 tiles <= 240 columns (scale-factor TMEM columns); int8 tiles <= 192:
+    // smaller operand stages leave room for a deeper TMA pipeline (C4 measured:
+    // 0.76 ms/sweep at 192 columns vs 0.84 at 256)
+    const int cap = fp4 ? 240 : 192;
+    int wide = std::max(1, std::min(T, cap / R));
+    if (const char* env = getenv("SSQA_TC_WIDE"))  // tuning override: trials per wide tile
+      wide = std::max(1, std::min(wide, atoi(env)));
     const int wtiles = (T + wide - 1) / wide;
     // worth it when the wide tiling still fills the SMs with >= 2 parts per tile
     if (nrt >= 16 && wide > tpt && wtiles * 2 <= sms) {

@@ -1418,7 +1418,7 @@ bool make_map(CUtensorMap* m, void* base, CUtensorMapDataType dt, uint32_t esize
 // >= 2 ring slots per subgroup (so the loader runs a chunk ahead), then as
 // many operand stages (<= 4) as fit.
 Layout pick_layout(int NT, int tpt, int nsubs, int tile_row) {
-  const uint32_t cap = 220 * 1024;
+  const uint32_t cap = 226 * 1024;  // of 227 KB dynamic shared memory per CTA
   for (int nps = 3; nps >= 1; --nps)
     for (int stages = 4; stages >= 2; --stages) {
       if (nps * nsubs > 16) continue;

@@ -1,0 +1,8 @@
+#!/bin/bash
+cd "$GRAFT_REPO_ROOT" || cd /root/repo
+mkdir -p gpurun_out
+TAG=${1:-nl}
+for c in c4 c5; do
+  timeout 300 python scripts/prof_run.py $c tcgen05 6 > gpurun_out/pre_${TAG}_$c.log 2>&1 && \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_sweep -s 1 -c 1 -o gpurun_out/prof_${TAG}_$c python scripts/prof_run.py $c tcgen05 6 > gpurun_out/ncu_${TAG}_$c.log 2>&1; tail -1 gpurun_out/ncu_${TAG}_$c.log
+done
