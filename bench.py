@@ -310,7 +310,8 @@ def run_rows(args, cfg):
         torch.cuda.synchronize()
         e2e_times.append(time.perf_counter() - t0)
     e2e_s = shard.max_over_ranks(statistics.mean(e2e_times), dist, "cuda")
-    h2d = prob.info()["n_pad"] ** 2 + 4 * prob.info()["n_pad"] + 8 * T + 8 * (sc + 1)
+    # the model's double couplings (quantized on the device) + H' + seeds + schedule
+    h2d = 8 * N * N + 4 * prob.info()["n_pad"] + 8 * T + 8 * (sc + 1)
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
@@ -480,7 +481,8 @@ def run_ours(args, cfg):
     # quantized upload: int8 J' (+ its FP4 image when the couplings allow it),
     # int32 H', seeds, the jperp schedule table
     fp4 = eng_name == "tcgen05" and info.get("fp4", 0)
-    h2d = npad * npad + (npad * npad // 2 if fp4 else 0) + 4 * npad + 8 * len(seeds) + 8 * (sc + 1)
+    # the model's double couplings (quantized on the device) + H' + seeds + schedule
+    h2d = 8 * N * N + 4 * npad + 8 * len(seeds) + 8 * (sc + 1)
     d2h = len(seeds) * (8 + 4 + 4 + 8 + 8 + 8) + len(seeds) * N
 
     # ---- TTS99 (amortised and reference-formula) ----

@@ -12,6 +12,7 @@
 #include <vector>
 
 #include "engine.h"
+#include "quantize_kernels.cuh"
 #include "simt_kernels.cuh"
 #include "sweep_tc.h"
 
@@ -267,35 +268,109 @@ int ssqa_problem_create(int n, const double* h, const double* J, double offset, 
                         ssqa_problem* out) {
   if (!out || !h || !J) return set_err(SSQA_EINVAL, "null argument");
   if (n < 1 || n >= kMaxSpins) return set_err(SSQA_EINVAL, "spin count out of range");
-  auto* pr = new ssqa_problem_s();
-  std::string why;
-  int rc = quantize(n, h, J, offset, &pr->q, &why);
-  if (rc) {
-    delete pr;
-    return set_err(rc, why);
+  // The quantizer of csrc/quantize.cpp, run on the device: the doubles are
+  // uploaded once, scanned for the scale, scaled + transposed into J' and
+  // packed into the FP4 image there (quantize_kernels.cu); only the n biases
+  // and a few scalars go through the host.
+  int p = 0;
+  for (int i = 0; i < n; ++i) {
+    const int e = dyadic_exponent_of(h[i]);
+    if (e < 0) return set_err(SSQA_EUNSUP, "bias " + std::to_string(i) + " is not a dyadic rational");
+    p = std::max(p, e);
   }
+  auto* pr = new ssqa_problem_s();
+  Quantized& q = pr->q;
+  q.n = n;
+  q.npad = (n + 127) / 128 * 128;
+  q.offset = offset;
   pr->device = device;
+  const size_t nn = size_t(n) * n, np2 = size_t(q.npad) * q.npad;
+  double* d_Jd = nullptr;
+  int* d_stats = nullptr;  // [0] pmax, [1] maxabs, [2] overflow, [3] not_fp4, [4..5] bad (u64)
+  int st[6] = {0, 0, 0, 0, 0, 0};
+  std::string fail;
+  auto cleanup = [&]() {
+    if (d_Jd) cudaFree(d_Jd);
+    if (d_stats) cudaFree(d_stats);
+  };
   cudaError_t e = cudaSetDevice(device);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&pr->stream, cudaStreamNonBlocking);
-  if (e == cudaSuccess)
-    e = cudaMalloc(&pr->d_J, pr->q.J.size() * sizeof(int8_t));
-  if (e == cudaSuccess) e = cudaMalloc(&pr->d_H, pr->q.H.size() * sizeof(int32_t));
-  if (e == cudaSuccess)
-    e = cudaMemcpyAsync(pr->d_J, pr->q.J.data(), pr->q.J.size(), cudaMemcpyHostToDevice,
-                        pr->stream);
-  if (e == cudaSuccess)
-    e = cudaMemcpyAsync(pr->d_H, pr->q.H.data(), pr->q.H.size() * sizeof(int32_t),
-                        cudaMemcpyHostToDevice, pr->stream);
-  if (e == cudaSuccess && pr->q.fp4_ok) {
-    e = cudaMalloc(&pr->d_J4, pr->q.J4.size());
-    if (e == cudaSuccess)
-      e = cudaMemcpyAsync(pr->d_J4, pr->q.J4.data(), pr->q.J4.size(), cudaMemcpyHostToDevice,
-                          pr->stream);
+  if (e == cudaSuccess) e = cudaMalloc(&d_Jd, nn * sizeof(double));
+  if (e == cudaSuccess) e = cudaMalloc(&d_stats, sizeof(st));
+  if (e == cudaSuccess) e = cudaMalloc(&pr->d_J, np2);
+  if (e == cudaSuccess) {
+    const unsigned long long none = ~0ull;
+    cudaMemsetAsync(d_stats, 0, sizeof(st), pr->stream);
+    cudaMemcpyAsync(d_stats + 4, &none, sizeof(none), cudaMemcpyHostToDevice, pr->stream);
+    e = cudaMemcpyAsync(d_Jd, J, nn * sizeof(double), cudaMemcpyHostToDevice, pr->stream);
+  }
+  if (e == cudaSuccess) {
+    launch_qscan(d_Jd, nn, d_stats, reinterpret_cast<unsigned long long*>(d_stats + 4),
+                 pr->stream);
+    e = cudaMemcpyAsync(st, d_stats, sizeof(st), cudaMemcpyDeviceToHost, pr->stream);
   }
   if (e == cudaSuccess) e = cudaStreamSynchronize(pr->stream);
+  if (e == cudaSuccess) {
+    unsigned long long bad;
+    std::memcpy(&bad, st + 4, sizeof bad);
+    if (bad != ~0ull) {
+      fail = "coupling " + std::to_string(bad / n) + "," + std::to_string(bad % n) +
+             " is not a dyadic rational";
+    } else {
+      p = std::max(p, st[0]);
+      launch_qtranspose(d_Jd, n, q.npad, std::ldexp(1.0, p), pr->d_J, d_stats + 1, d_stats + 2,
+                        pr->stream);
+      e = cudaMemcpyAsync(st, d_stats, sizeof(st), cudaMemcpyDeviceToHost, pr->stream);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(pr->stream);
+      if (e == cudaSuccess && st[2])
+        fail = "coupling magnitude exceeds int8 at scale 2^" + std::to_string(p);
+    }
+  }
+  if (e == cudaSuccess && fail.empty()) {
+    q.p = p;
+    q.scale = std::ldexp(1.0, -p);
+    q.max_abs_j = st[1];
+    // biases: H' = h * 2^p, |H'| < 2^29 keeps S + 2H' inside int32
+    std::vector<int32_t> H(size_t(q.npad), 0);
+    for (int i = 0; i < n && fail.empty(); ++i) {
+      const double x = std::ldexp(h[i], p);
+      if (std::fabs(x) >= double(1 << 29))
+        fail = "bias magnitude exceeds the int32 field range at scale 2^" + std::to_string(p);
+      else
+        H[size_t(i)] = int32_t(x);
+      q.max_abs_h = std::max(q.max_abs_h, std::abs(H[size_t(i)]));
+    }
+    if (fail.empty()) {
+      e = cudaMalloc(&pr->d_H, H.size() * sizeof(int32_t));
+      if (e == cudaSuccess)
+        e = cudaMemcpyAsync(pr->d_H, H.data(), H.size() * sizeof(int32_t),
+                            cudaMemcpyHostToDevice, pr->stream);
+      // FP4 (e2m1) image when every coupling is 0, +-1, +-2, +-3, +-4 or +-6
+      q.fp4_ok = q.max_abs_j <= 6 && q.max_abs_j != 5;
+      if (e == cudaSuccess && q.fp4_ok) {
+        e = cudaMalloc(&pr->d_J4, np2 / 2);
+        if (e == cudaSuccess) {
+          launch_qfp4(pr->d_J, np2, pr->d_J4, d_stats + 3, pr->stream);
+          e = cudaMemcpyAsync(st, d_stats, sizeof(st), cudaMemcpyDeviceToHost, pr->stream);
+        }
+        if (e == cudaSuccess) e = cudaStreamSynchronize(pr->stream);
+        if (e == cudaSuccess && st[3]) {
+          q.fp4_ok = false;
+          cudaFree(pr->d_J4);
+          pr->d_J4 = nullptr;
+        }
+      }
+      if (e == cudaSuccess) e = cudaStreamSynchronize(pr->stream);
+    }
+  }
+  cleanup();
   if (e != cudaSuccess) {
     ssqa_problem_destroy(pr);
     return set_err(SSQA_ECUDA, std::string("problem upload: ") + cudaGetErrorString(e));
+  }
+  if (!fail.empty()) {
+    ssqa_problem_destroy(pr);
+    return set_err(SSQA_EUNSUP, fail);
   }
   *out = pr;
   return SSQA_OK;

@@ -49,6 +49,8 @@ struct Quantized {
 // scale exponent (several instances quantized at one common scale).
 int quantize(int n, const double* h, const double* J, double offset, Quantized* q,
              std::string* why, int p_min = 0);
+// Smallest p in [0, 62] with v * 2^p integral, or -1 (the quantizer's rule).
+int dyadic_exponent_of(double v);
 
 }  // namespace ssqa_engine
 

@@ -13,6 +13,7 @@
 #include <algorithm>
 #include <atomic>
 #include <climits>
+#include <cstring>
 #include <cmath>
 #include <cstdlib>
 #include <string>
@@ -25,15 +26,20 @@ namespace ssqa_engine {
 
 namespace {
 
-// Smallest p in [0, 62] with v * 2^p integral, or -1.
+// Smallest p in [0, 62] with v * 2^p integral, or -1.  Read off the IEEE
+// bits: v = F * 2^(E - 1075) with F the significand (implicit 1 for normal
+// numbers), so the lowest set bit of v has weight 2^(E - 1075 + ctz(F)).
 int dyadic_exponent(double v) {
-  if (!std::isfinite(v)) return -1;
-  if (v == std::floor(v)) return 0;  // integers (every BASELINE coupling)
-  for (int p = 1; p <= 62; ++p) {
-    double x = std::ldexp(v, p);
-    if (x == std::floor(x)) return p;
-  }
-  return -1;
+  uint64_t b;
+  std::memcpy(&b, &v, sizeof b);
+  const int E = int((b >> 52) & 0x7ff);
+  if (E == 0x7ff) return -1;  // inf / nan
+  uint64_t F = b & ((1ull << 52) - 1);
+  if (E == 0 && F == 0) return 0;  // +-0
+  if (E != 0) F |= 1ull << 52;
+  const int low = (E == 0 ? 1 : E) - 1075 + __builtin_ctzll(F);
+  const int p = low >= 0 ? 0 : -low;
+  return p <= 62 ? p : -1;
 }
 
 // f(lo, hi) over [0, n) on all hardware threads (n up to 2^20 rows).
@@ -64,6 +70,8 @@ void atomic_min(std::atomic<long long>& a, long long v) {
 }
 
 }  // namespace
+
+int dyadic_exponent_of(double v) { return dyadic_exponent(v); }
 
 int quantize(int n, const double* h, const double* J, double offset, Quantized* q,
              std::string* why, int p_min) {
@@ -119,6 +127,7 @@ int quantize(int n, const double* h, const double* J, double offset, Quantized* 
   {
     constexpr int kB = 64;
     const int nb = (n + kB - 1) / kB;
+    const double up = std::ldexp(1.0, p);
     std::atomic<int> maxj{0};
     std::atomic<bool> overflow{false};
     parallel_for(nb, [&](int lo, int hi) {
@@ -130,7 +139,7 @@ int quantize(int n, const double* h, const double* J, double offset, Quantized* 
           for (int j = j0; j < j1; ++j) {
             const double* src = J + size_t(j) * n;
             for (int i = i0; i < i1; ++i) {
-              const double x = p ? std::ldexp(src[i], p) : src[i];
+              const double x = src[i] * up;  // exact: a power-of-two scale of a dyadic value
               if (std::fabs(x) > 127.0) {
                 overflow = true;
                 return;

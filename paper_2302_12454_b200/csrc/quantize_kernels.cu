@@ -1,0 +1,113 @@
+// quantize_kernels.cu -- the quantizer of csrc/quantize.cpp on the device:
+// the model's double couplings are uploaded once and scanned, scaled,
+// transposed and packed where they will be used (ssqa_problem_create).
+// Same rules as the host quantizer: the smallest p >= 0 making every
+// coupling and bias an integer, J'[i][j] = J[j][i] * 2^p as int8 (|J'| <=
+// 127, else unsupported), and the FP4 (e2m1) image when every J' is one of
+// 0, +-1, +-2, +-3, +-4, +-6.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "quantize_kernels.cuh"
+
+namespace ssqa_engine {
+
+namespace {
+
+// Smallest p with v * 2^p integral (the IEEE bits: v = F * 2^(E-1075)), -1
+// for inf / nan, 99 beyond the 62 the engine allows.
+__device__ __forceinline__ int dyadic_exp_dev(double v) {
+  const uint64_t b = uint64_t(__double_as_longlong(v));
+  const int E = int((b >> 52) & 0x7ff);
+  if (E == 0x7ff) return -1;
+  uint64_t F = b & ((1ull << 52) - 1);
+  if (E == 0 && F == 0) return 0;
+  if (E != 0) F |= 1ull << 52;
+  const int low = (E == 0 ? 1 : E) - 1075 + __ffsll((long long)F) - 1;
+  const int p = low >= 0 ? 0 : -low;
+  return p <= 62 ? p : 99;
+}
+
+__global__ void k_qscan(const double* __restrict__ J, size_t count, int* __restrict__ pmax,
+                        unsigned long long* __restrict__ bad) {
+  int local = 0;
+  for (size_t x = blockIdx.x * size_t(blockDim.x) + threadIdx.x; x < count;
+       x += size_t(gridDim.x) * blockDim.x) {
+    const int e = dyadic_exp_dev(J[x]);
+    if (e < 0 || e > 62) atomicMin(bad, static_cast<unsigned long long>(x));
+    else local = max(local, e);
+  }
+  for (int o = 16; o > 0; o >>= 1) local = max(local, __shfl_xor_sync(0xffffffffu, local, o));
+  if ((threadIdx.x & 31) == 0 && local > 0) atomicMax(pmax, local);
+}
+
+// J'[i][j] = J[j][i] * up through a 32x32 shared tile (coalesced both ways).
+__global__ void k_qtranspose(const double* __restrict__ J, int n, int npad, double up,
+                             int8_t* __restrict__ Jq, int* __restrict__ maxabs,
+                             int* __restrict__ overflow) {
+  __shared__ int8_t tile[32][33];
+  const int i0 = blockIdx.x * 32, j0 = blockIdx.y * 32;
+  int local = 0, bad = 0;
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int j = j0 + r, i = i0 + threadIdx.x;
+    int v = 0;
+    if (j < n && i < n) {
+      const double x = J[size_t(j) * n + i] * up;  // exact: a power-of-two scale
+      if (fabs(x) > 127.0) bad = 1;
+      else v = int(x);
+    }
+    tile[r][threadIdx.x] = int8_t(v);
+    local = max(local, abs(v));
+  }
+  __syncthreads();
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int i = i0 + r, j = j0 + threadIdx.x;
+    if (i < npad && j < npad) Jq[size_t(i) * npad + j] = tile[threadIdx.x][r];
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    local = max(local, __shfl_xor_sync(0xffffffffu, local, o));
+    bad |= __shfl_xor_sync(0xffffffffu, bad, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (local > 0) atomicMax(maxabs, local);
+    if (bad) atomicOr(overflow, 1);
+  }
+}
+
+// e2m1 image, two couplings per byte (lower K index in the low nibble).
+__global__ void k_qfp4(const int8_t* __restrict__ Jq, size_t pairs, uint8_t* __restrict__ J4,
+                       int* __restrict__ not_fp4) {
+  // |v| -> e2m1 magnitude code (0, 1, 2, 3, 4, 6 representable)
+  constexpr int kCode[8] = {0, 2, 4, 5, 6, -1, 7, -1};
+  for (size_t x = blockIdx.x * size_t(blockDim.x) + threadIdx.x; x < pairs;
+       x += size_t(gridDim.x) * blockDim.x) {
+    const int a = Jq[2 * x], b = Jq[2 * x + 1];
+    const int ma = a < 0 ? -a : a, mb = b < 0 ? -b : b;
+    const int ca = ma < 8 ? kCode[ma] : -1, cb = mb < 8 ? kCode[mb] : -1;
+    if (ca < 0 || cb < 0) {
+      atomicOr(not_fp4, 1);
+      continue;
+    }
+    J4[x] = uint8_t((ca | (a < 0 ? 8 : 0)) | ((cb | (b < 0 ? 8 : 0)) << 4));
+  }
+}
+
+}  // namespace
+
+void launch_qscan(const double* J, size_t count, int* pmax, unsigned long long* bad,
+                  cudaStream_t st) {
+  k_qscan<<<1184, 256, 0, st>>>(J, count, pmax, bad);
+}
+
+void launch_qtranspose(const double* J, int n, int npad, double up, int8_t* Jq, int* maxabs,
+                       int* overflow, cudaStream_t st) {
+  dim3 grid(npad / 32, npad / 32), block(32, 8);
+  k_qtranspose<<<grid, block, 0, st>>>(J, n, npad, up, Jq, maxabs, overflow);
+}
+
+void launch_qfp4(const int8_t* Jq, size_t elems, uint8_t* J4, int* not_fp4, cudaStream_t st) {
+  k_qfp4<<<1184, 256, 0, st>>>(Jq, elems / 2, J4, not_fp4);
+}
+
+}  // namespace ssqa_engine

@@ -686,3 +686,38 @@ int main(int argc, char** argv) {
     assert out[0] == "REF 1 -" and out[1] == "REF 1 -", out
     assert out[2] == "OWN 1", out
     assert out[3].startswith("BAD 0 trial 3 of record 0"), out
+
+
+def test_device_quantizer_matches_host_quantizer():
+    """ssqa_problem_create quantizes on the device: same scale, ranges, FP4
+    decision and rejections as the host quantizer (ssqa_quantize_info)."""
+    import ctypes as C
+    L = _lib.lib()
+    rng = np.random.default_rng(3)
+    models = [sq.gi_ising(10, 0.5, 7, True, 1.0, 1.0), sq.gi_ising(12, 0.5, 4, False, 0.75, 0.75),
+              sq.dense_ising(300, 0, 1), sq.dense_ising(257, 1, 2)]
+    h = rng.integers(-8, 9, 130) / 8.0
+    J = np.triu(rng.integers(-6, 7, (130, 130)) / 4.0, 1)
+    models.append(sq.IsingModel.from_arrays(h, J + J.T, 0.5))
+    for m in models:
+        prob = sq.Problem(m)
+        dev = prob.info()
+        v = [C.c_int() for _ in range(4)]
+        dp = lambda a: np.ascontiguousarray(a).ctypes.data_as(C.POINTER(C.c_double))  # noqa: E731
+        assert L.ssqa_quantize_info(m.n, dp(m.h), dp(m.J), *[C.byref(x) for x in v]) == 0
+        assert (dev["n_pad"], dev["shift_p"], dev["max_abs_j"], dev["max_abs_h"]) == \
+            tuple(x.value for x in v), m.n
+        Jq = np.abs(m.J * 2.0 ** dev["shift_p"])
+        assert dev["fp4"] == int(bool(np.isin(Jq, [0, 1, 2, 3, 4, 6]).all()))
+    bad = sq.IsingModel(4)
+    bad.set_coupling(0, 1, float("inf"))  # (0.1 is dyadic as a double: 2^-55 * integer)
+    with pytest.raises(ValueError, match="not a dyadic"):
+        sq.Problem(bad)
+    tiny = sq.IsingModel(4)
+    tiny.set_coupling(0, 1, 0.1)  # needs p = 55: far beyond int8
+    with pytest.raises(ValueError, match="exceeds int8"):
+        sq.Problem(tiny)
+    big = sq.IsingModel(4)
+    big.set_coupling(1, 2, 200.0)
+    with pytest.raises(ValueError, match="exceeds int8"):
+        sq.Problem(big)
