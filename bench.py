@@ -478,10 +478,8 @@ def run_ours(args, cfg):
             assert [o.best_energy for o in out] == [res[t].best_energy for t in range(len(seeds))]
     e2e_s = max_over_ranks(statistics.mean(e2e_times))
     npad = info["n_pad"]
-    # quantized upload: int8 J' (+ its FP4 image when the couplings allow it),
-    # int32 H', seeds, the jperp schedule table
-    fp4 = eng_name == "tcgen05" and info.get("fp4", 0)
-    # the model's double couplings (quantized on the device) + H' + seeds + schedule
+    # the model's double couplings (quantized on the device) + int32 H' + seeds +
+    # the jperp schedule table
     h2d = 8 * N * N + 4 * npad + 8 * len(seeds) + 8 * (sc + 1)
     d2h = len(seeds) * (8 + 4 + 4 + 8 + 8 + 8) + len(seeds) * N
 
