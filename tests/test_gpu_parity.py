@@ -721,3 +721,44 @@ def test_device_quantizer_matches_host_quantizer():
     big.set_coupling(1, 2, 200.0)
     with pytest.raises(ValueError, match="exceeds int8"):
         sq.Problem(big)
+
+
+# ---- shape edge cases (each against the oracle, bitwise) ----
+
+@pytest.mark.parametrize("shape", [
+    dict(n=1, R=3, d=1, T=2, sc=20, bidir=False),        # a single spin
+    dict(n=130, R=256, d=1, T=2, sc=12, bidir=False),    # a full 256-column tile per trial
+    dict(n=129, R=17, d=30, T=3, sc=40, bidir=True),     # deepest delay ring, odd R
+    dict(n=100, R=4, d=0, T=149, sc=15, bidir=False),    # more column tiles than SMs
+    dict(n=200, R=300, d=1, T=2, sc=8, bidir=False),     # R > 256: the SIMT engine
+], ids=["n1", "R256", "delay30", "T149", "R300-simt"])
+def test_shape_edges_match_oracle(orc, shape):
+    n, R = shape["n"], shape["R"]
+    rng = np.random.default_rng(n + R)
+    h = rng.integers(-4, 5, n) / 2.0
+    J = np.triu(rng.integers(-2, 3, (n, n)) / 2.0, 1)
+    m = sq.IsingModel.from_arrays(h, J + J.T, 0.25)
+    p = params(R, shape["sc"], tau=3, delay=shape["d"], bidirectional=shape["bidir"])
+    seeds = [int(s) for s in rng.integers(0, 2 ** 62, shape["T"])]
+    res = sq.ssqa_run_batch(m, to_sq(p), seeds, None, sq.RunOptions(True, False))
+    for t in sorted({0, shape["T"] - 1}):
+        o = orc.ssqa_run(m.h, m.J, m.offset, p, seeds[t], None, True, False)
+        assert (res[t].best_energy, res[t].best_replica) == (o.best_energy, o.best_replica)
+        assert np.array_equal(res[t].best_state, o.best_state)
+        assert np.array_equal(bits(res[t].trace_energy), bits(o.trace))
+
+
+def test_fp4_bidirectional_matches_oracle(orc):
+    """FP4 operands (couplings in {0, +-1, +-2}) with the bidirectional coupling."""
+    if not engine_ok(_lib.ENGINE_TCGEN05):
+        pytest.skip("tcgen05 engine unavailable")
+    m = sq.gi_ising(16, 0.5, 3, True, 1.0, 1.0)
+    assert sq.Problem(m).info()["fp4"] == 1
+    p = params(12, 50, tau=4, delay=2, bidirectional=True)
+    seeds = [71, 72, 73]
+    res = sq.ssqa_run_batch(m, to_sq(p), seeds, 0.0, sq.RunOptions(True, False),
+                            engine=_lib.ENGINE_TCGEN05)
+    for t, s in enumerate(seeds):
+        o = orc.ssqa_run(m.h, m.J, m.offset, p, s, 0.0, True, False)
+        assert res[t].best_energy == o.best_energy
+        assert np.array_equal(bits(res[t].trace_energy), bits(o.trace))
