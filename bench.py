@@ -500,7 +500,8 @@ def run_ours(args, cfg):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-            "dtype": "int8 contraction (int32 acc) + f64 update",
+            "dtype": ("fp4 (e2m1) contraction (exact f32 acc)" if op_bits == 4 else
+                      "int8 contraction (int32 acc)") + " + f64 update",
             "data": "synthetic (reference GI generator, instance seed 7; seeds 1000+t)"
                     if cfg["kind"] == "gi" else "synthetic (CounterRng stream 8/9, seed 7)",
             "config": {"workload": cfg["desc"], "n": N, "n_pad": npad, "replicas": R,
