@@ -43,7 +43,8 @@ constexpr int kCW = 8;  // columns per epilogue chunk (one tcgen05.ld .x8)
 #ifndef SSQA_ABL
 // Timing ablations (scripts/build_ablations.sh), 0 in the product: 16 no energy
 // reduction, 32 no spin store, 64 no accumulator store, 128 no accumulator
-// stream (stale smem), 256 no TMEM load.
+// stream (stale smem), 256 no TMEM load, 512 no counter RNG (placeholder noise),
+// 1024 spin words built but not stored, 2048 no ballots (spin words from one lane).
 #define SSQA_ABL 0
 #endif
 #ifndef SSQA_ENERGY_RED
@@ -370,8 +371,7 @@ __device__ __forceinline__ void red_add_u32_if(uint32_t* p, uint32_t v, bool pre
   asm volatile(
       "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t"
       "@q red.shared.add.u32 [%0], %1;\n\t}" ::"r"(smem_u32(p)),
-      "r"(v), "r"(int(pred))
-      : "memory");
+      "r"(v), "r"(int(pred)));
 }
 __device__ __forceinline__ uint32_t ld_u8(const uint8_t* p) {
   uint32_t v;
@@ -382,8 +382,7 @@ __device__ __forceinline__ void st_u8_if(uint8_t* p, uint32_t v, bool pred) {
   asm volatile(
       "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t"
       "@q st.global.u8 [%0], %1;\n\t}" ::"l"(p),
-      "r"(v), "r"(int(pred))
-      : "memory");
+      "r"(v), "r"(int(pred)));
 }
 __device__ __forceinline__ int ld_s8(const int8_t* p) {
   int v;
@@ -402,9 +401,15 @@ __device__ __forceinline__ void st_f64_if(double* p, double v, bool pred, uint64
   asm volatile(
       "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t"
       "@q st.global.L1::no_allocate.L2::cache_hint.f64 [%0], %1, %3;\n\t}" ::"l"(p),
-      "d"(v), "r"(int(pred)), "l"(pol)
-      : "memory");
+      "d"(v), "r"(int(pred)), "l"(pol));
 }
+// The global stores / shared reductions of the epilogue carry no "memory"
+// clobber: nothing in the thread reads those addresses back, and the
+// ordering that matters -- proxy fences, mbarrier arrives, named barriers --
+// is between volatile asm statements, which keep their relative order.  A
+// clobber would stop the compiler from hoisting the next element's shared
+// loads above each store (C3: the spin-word and accumulator stores cost ~30 %).
+
 // Ballot of a register != 0 in plain PTX: no divergence check, and the
 // predicate never has to survive to a deferred VOTE.
 __device__ __forceinline__ uint32_t ballot_nz(uint32_t v) {
@@ -415,6 +420,27 @@ __device__ __forceinline__ uint32_t ballot_nz(uint32_t v) {
       : "=r"(r)
       : "r"(v));
   return r;
+}
+// Warp collectives in plain PTX (no compiler divergence checks / predicate
+// juggling around them; the epilogue's warps are always converged here).
+#ifndef SSQA_PTX_COLL
+#define SSQA_PTX_COLL 1  // bit 0: PTX ballot (C3: -2.6 %/sweep), bit 1: PTX shuffles
+#endif
+__device__ __forceinline__ int shfl_xor_i(int v, int m) {
+#if SSQA_PTX_COLL & 2
+  int r;
+  asm volatile("shfl.sync.bfly.b32 %0, %1, %2, 0x1f, 0xffffffff;" : "=r"(r) : "r"(v), "r"(m));
+  return r;
+#else
+  return __shfl_xor_sync(0xffffffffu, v, m);
+#endif
+}
+__device__ __forceinline__ uint32_t ballot_neg(uint32_t neg) {
+#if SSQA_PTX_COLL & 1
+  return ballot_nz(neg);
+#else
+  return __ballot_sync(0xffffffffu, neg != 0u);
+#endif
 }
 __device__ __forceinline__ uint4 lds128(const void* p) {
   uint4 v;
@@ -427,15 +453,13 @@ __device__ __forceinline__ void st_u32_if(uint32_t* p, uint32_t v, bool pred) {
   asm volatile(
       "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t"
       "@q st.global.u32 [%0], %1;\n\t}" ::"l"(p),
-      "r"(v), "r"(int(pred))
-      : "memory");
+      "r"(v), "r"(int(pred)));
 }
 __device__ __forceinline__ void st_s8_if(int8_t* p, int v, bool pred) {
   asm volatile(
       "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t"
       "@q st.global.s8 [%0], %1;\n\t}" ::"l"(p),
-      "r"(v), "r"(int(pred))
-      : "memory");
+      "r"(v), "r"(int(pred)));
 }
 
 struct TrialTab {
@@ -604,7 +628,8 @@ __device__ __forceinline__ void epi_chunks(const EpiRow& er, const UpdateConsts&
       double nv;
       uint32_t neg;  // 1 when the new spin is -1
       if (FAST) {
-        const uint32_t top = mix64_top32_pre(cbase + er.iG);
+        const uint32_t top = (SSQA_ABL & 512) ? uint32_t(cbase) ^ uint32_t(er.iG)
+                                              : mix64_top32_pre(cbase + er.iG);
         nv = update_fast2<BIDIR>(fc, i2d, S + er.h1, top, up, dn, a_old);
         neg = uint32_t(__double2hiint(nv)) >> 31;
       } else {
@@ -618,7 +643,7 @@ __device__ __forceinline__ void epi_chunks(const EpiRow& er, const UpdateConsts&
         st_f64_if(reinterpret_cast<double*>(er.acc_i + uint64_t(coff) * 8u), nv, w, er.pol_stream);
       if (SSQA_ABL & 32) {
       } else if (kWordSt) {
-        ball[j] = __ballot_sync(0xffffffffu, neg != 0u);
+        ball[j] = (SSQA_ABL & 2048) ? neg : ballot_neg(neg);
       } else if (F4) {
         // e2m1 +1 = 0x2, -1 = 0xA; even lanes store the byte of rows (i, i+1)
         const uint32_t nib = 2u | (neg << 3);
@@ -638,8 +663,11 @@ __device__ __forceinline__ void epi_chunks(const EpiRow& er, const UpdateConsts&
       const uint32_t mm = (wj & 4) ? b1 : b0;
       const uint32_t word = nibbles_pm1((mm >> (8 * (lane & 3))) & 0xffu) & er.nib_live;
       const uint2 cw = *reinterpret_cast<const uint2*>(&c_col[cb + wj].off);
-      st_u32_if(reinterpret_cast<uint32_t*>(er.dst_w + (cw.x >> 1)), word,
-                (cw.y & 0x80000000u) && er.nib_live);
+      if (SSQA_ABL & 1024) {
+      } else {
+        st_u32_if(reinterpret_cast<uint32_t*>(er.dst_w + (cw.x >> 1)), word,
+                  (cw.y & 0x80000000u) && er.nib_live);
+      }
     }
     __syncwarp();
     if (lane == 0 && !(SSQA_ABL & 128)) mbar_arrive(&ctl->aempty[slot]);
@@ -654,21 +682,21 @@ __device__ __forceinline__ void epi_chunks(const EpiRow& er, const UpdateConsts&
       for (int k = 0; k < 4; ++k) {
         const int keep = b16 ? ep[k + 4] : ep[k];
         const int send = b16 ? ep[k] : ep[k + 4];
-        a4[k] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+        a4[k] = keep + shfl_xor_i(send, 16);
       }
 #pragma unroll
       for (int k = 0; k < 2; ++k) {
         const int keep = b8 ? a4[k + 2] : a4[k];
         const int send = b8 ? a4[k] : a4[k + 2];
-        a2[k] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+        a2[k] = keep + shfl_xor_i(send, 8);
       }
       {
         const int keep = b4 ? a2[1] : a2[0];
         const int send = b4 ? a2[0] : a2[1];
-        a1 = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+        a1 = keep + shfl_xor_i(send, 4);
       }
-      a1 += __shfl_xor_sync(0xffffffffu, a1, 2);
-      a1 += __shfl_xor_sync(0xffffffffu, a1, 1);
+      a1 += shfl_xor_i(a1, 2);
+      a1 += shfl_xor_i(a1, 1);
       // lane bits 4,3,2 select column bits 2,1,0
       const int col = (b16 ? 4 : 0) + (b8 ? 2 : 0) + (b4 ? 1 : 0);
       red_add_u32_if(reinterpret_cast<uint32_t*>(q_sum) + cb + col, uint32_t(a1),
