@@ -413,9 +413,13 @@ def run_ours(args, cfg):
     # dense tensor peak of the operand format the kernel streams: int8 = 2x
     # bf16, FP4 (kind::mxf4) = 4x bf16 on B200
     op_bits = b.operand_bits
+    # FP4 pair operands (J' = A1 + A2, problem info fp4 == 2): two kind::mxf4
+    # MMAs per coupling block, i.e. twice the FP4 ops of a single image
+    planes = 2 if (op_bits == 4 and info.get("fp4") == 2) else 1
     tc_mult = 4.0 if op_bits == 4 else 2.0
     tc_peak = tc_mult * bf16_peak
-    tc_name = "fp4 (e2m1)" if op_bits == 4 else "int8"
+    tc_name = ("fp4 pair (e2m1, J'=A1+A2)" if planes == 2 else "fp4 (e2m1)") if op_bits == 4 \
+        else "int8"
     cols = R * len(seeds)
     # algorithmic bytes (format independent): f64 acc
     # read+write, bit-packed spins, int8 J streamed once per sweep
@@ -430,7 +434,7 @@ def run_ours(args, cfg):
     else:
         kname = "k_sweep_tc (fused, persistent: whole run in one launch)"
         k_ms = statistics.mean(times)
-        ops = 2.0 * N * N * cols * (sc + 1)
+        ops = 2.0 * N * N * cols * (sc + 1) * planes
         sweeps_per_launch = sc
         launch_bytes = alg_bytes_per_update * updates_per_sweep * sc
     tensor_tops = ops / (k_ms * 1e-3) / 1e12
@@ -500,7 +504,7 @@ def run_ours(args, cfg):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-            "dtype": ("fp4 (e2m1) contraction (exact f32 acc)" if op_bits == 4 else
+            "dtype": (f"{tc_name} contraction (exact f32 acc)" if op_bits == 4 else
                       "int8 contraction (int32 acc)") + " + f64 update",
             "data": "synthetic (reference GI generator, instance seed 7; seeds 1000+t)"
                     if cfg["kind"] == "gi" else "synthetic (CounterRng stream 8/9, seed 7)",

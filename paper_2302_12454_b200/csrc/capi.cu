@@ -360,6 +360,22 @@ int ssqa_problem_create(int n, const double* h, const double* J, double offset, 
           pr->d_J4 = nullptr;
         }
       }
+      // otherwise the FP4 pair image J' = A1 + A2 (|J'| <= 12, != 11)
+      if (e == cudaSuccess && !q.fp4_ok && fp4x2_splittable(q.max_abs_j)) {
+        st[3] = 0;
+        e = cudaMemcpyAsync(d_stats + 3, st + 3, sizeof(int), cudaMemcpyHostToDevice, pr->stream);
+        if (e == cudaSuccess) e = cudaMalloc(&pr->d_J4, np2);
+        if (e == cudaSuccess) {
+          launch_qfp4x2(pr->d_J, q.npad, pr->d_J4, d_stats + 3, pr->stream);
+          e = cudaMemcpyAsync(st, d_stats, sizeof(st), cudaMemcpyDeviceToHost, pr->stream);
+        }
+        if (e == cudaSuccess) e = cudaStreamSynchronize(pr->stream);
+        q.fp4x2_ok = e == cudaSuccess && !st[3];
+        if (!q.fp4x2_ok && pr->d_J4) {
+          cudaFree(pr->d_J4);
+          pr->d_J4 = nullptr;
+        }
+      }
       if (e == cudaSuccess) e = cudaStreamSynchronize(pr->stream);
     }
   }
@@ -376,7 +392,9 @@ int ssqa_problem_create(int n, const double* h, const double* J, double offset, 
   return SSQA_OK;
 }
 
-int ssqa_problem_fp4(ssqa_problem pr) { return (pr && pr->q.fp4_ok) ? 1 : 0; }
+int ssqa_problem_fp4(ssqa_problem pr) {
+  return !pr ? 0 : pr->q.fp4_ok ? 1 : pr->q.fp4x2_ok ? 2 : 0;
+}
 
 int ssqa_problem_create_many(int count, int n, const double* h, const double* J,
                              const double* offsets, int device, ssqa_problem* out) {
@@ -410,17 +428,32 @@ int ssqa_problem_create_many(int count, int n, const double* h, const double* J,
     pr->offsets.push_back(q.offset);
   }
   pr->q.fp4_ok = fp4;
+  // no common single image: the pair image when every instance splits
+  bool fp4x2 = !fp4 && fp4x2_splittable(pr->q.max_abs_j);
+  pr->q.fp4x2_ok = fp4x2;
   const size_t npad = size_t(pr->q.npad);
   pr->q.J.resize(size_t(count) * npad * npad);
   pr->q.H.resize(size_t(count) * npad);
   if (fp4) pr->q.J4.resize(size_t(count) * npad * (npad / 2));
+  else if (fp4x2) pr->q.J4.resize(size_t(count) * npad * npad);
   else pr->q.J4.clear();
-  for (int c = 1; c < count; ++c) {
+  for (int c = 0; c < count; ++c) {
     const Quantized& q = qs[size_t(c)];
-    std::copy(q.J.begin(), q.J.end(), pr->q.J.begin() + size_t(c) * npad * npad);
-    std::copy(q.H.begin(), q.H.end(), pr->q.H.begin() + size_t(c) * npad);
-    if (fp4) std::copy(q.J4.begin(), q.J4.end(), pr->q.J4.begin() + size_t(c) * npad * (npad / 2));
+    if (c > 0) {
+      std::copy(q.J.begin(), q.J.end(), pr->q.J.begin() + size_t(c) * npad * npad);
+      std::copy(q.H.begin(), q.H.end(), pr->q.H.begin() + size_t(c) * npad);
+      if (fp4) std::copy(q.J4.begin(), q.J4.end(), pr->q.J4.begin() + size_t(c) * npad * (npad / 2));
+    }
+    if (fp4x2) {
+      std::vector<uint8_t> img;
+      if (build_fp4x2(q, &img))
+        std::copy(img.begin(), img.end(), pr->q.J4.begin() + size_t(c) * npad * npad);
+      else
+        fp4x2 = false;
+    }
   }
+  pr->q.fp4x2_ok = fp4x2;
+  if (!fp4 && !fp4x2) pr->q.J4.clear();
   qs.clear();
   pr->device = device;
   cudaError_t e = cudaSetDevice(device);
@@ -436,7 +469,7 @@ int ssqa_problem_create_many(int count, int n, const double* h, const double* J,
   if (e == cudaSuccess)
     e = cudaMemcpyAsync(pr->d_offsets, pr->offsets.data(), size_t(count) * sizeof(double),
                         cudaMemcpyHostToDevice, pr->stream);
-  if (e == cudaSuccess && fp4) {
+  if (e == cudaSuccess && (fp4 || fp4x2)) {
     e = cudaMalloc(&pr->d_J4, pr->q.J4.size());
     if (e == cudaSuccess)
       e = cudaMemcpyAsync(pr->d_J4, pr->q.J4.data(), pr->q.J4.size(), cudaMemcpyHostToDevice,
@@ -530,7 +563,8 @@ int create_batch(ssqa_problem pr, const ssqa_params_c* p, int trials, int record
   b->record_trace = record_trace;
   b->d = p->delay;
   b->nslots = p->delay + 3;
-  b->g = make_geom(pr->q.n, pr->q.npad, p->r, trials, num_sms(pr->device), eng, pr->q.fp4_ok,
+  const bool any_fp4 = pr->q.fp4_ok || pr->q.fp4x2_ok;
+  b->g = make_geom(pr->q.n, pr->q.npad, p->r, trials, num_sms(pr->device), eng, any_fp4,
                    pr->count > 1);
   b->slot_elems = size_t(b->g.ccols) * b->g.npad;
   b->phys.assign(size_t(b->d) + 1, 0);
@@ -545,7 +579,7 @@ int create_batch(ssqa_problem pr, const ssqa_params_c* p, int trials, int record
   A(&b->d_jperp, size_t(p->sc) + 1);
   A(&b->d_E, size_t(b->g.ccols));
   if (eng == SSQA_ENGINE_SIMT) A(&b->d_S, b->slot_elems);
-  if (eng == SSQA_ENGINE_TCGEN05 && pr->q.fp4_ok) A(&b->d_sig4, b->slot_elems * b->nslots / 2);
+  if (eng == SSQA_ENGINE_TCGEN05 && any_fp4) A(&b->d_sig4, b->slot_elems * b->nslots / 2);
   A(&b->d_best_e, size_t(T));
   A(&b->d_best_k, size_t(T));
   A(&b->d_reached, size_t(T));

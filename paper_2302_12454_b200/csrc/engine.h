@@ -42,8 +42,23 @@ struct Quantized {
   // FP4 (e2m1) image of J' when every coupling is one of 0, +-1, +-2, +-3,
   // +-4, +-6: two elements per byte, lower K index in the low nibble.
   bool fp4_ok = false;
-  std::vector<uint8_t> J4;           // [npad * npad/2]
+  // FP4 pair image (fp4x2_ok, when fp4_ok is not): J' = A1 + A2 with both
+  // planes e2m1-exact integers (|J'| <= 12, != 11).  Per K chunk of 128
+  // couplings a row holds 64 bytes of A1 nibbles, then 64 bytes of A2
+  // nibbles, so one 128-byte TMA row feeds both MMAs of the chunk.
+  bool fp4x2_ok = false;
+  std::vector<uint8_t> J4;           // [npad * npad/2] (fp4_ok) or [npad * npad] (fp4x2_ok)
 };
+
+// e2m1 magnitude codes (0, 1, 2, 3, 4, 6 -> 0, 2, 4, 5, 6, 7) of the FP4 pair
+// split |v| = a + b, a >= b, for |v| <= 12; -1 where no split exists (11).
+constexpr int kFp4x2A[13] = {0, 2, 4, 5, 6, 6, 7, 7, 7, 7, 7, -1, 7};
+constexpr int kFp4x2B[13] = {0, 0, 0, 0, 0, 2, 0, 2, 4, 5, 6, -1, 7};
+inline bool fp4x2_splittable(int max_abs) { return max_abs <= 12 && max_abs != 11; }
+// Byte offsets of coupling j's A1 / A2 nibbles inside a pair-image row, and
+// the nibble shift.
+inline size_t fp4x2_byte_a(int j) { return size_t(j >> 7) * 128 + size_t((j & 127) >> 1); }
+inline int fp4x2_shift(int j) { return 4 * (j & 1); }
 
 // Returns SSQA_OK or SSQA_EUNSUP with *why set.  p_min: lower bound of the
 // scale exponent (several instances quantized at one common scale).
@@ -51,6 +66,8 @@ int quantize(int n, const double* h, const double* J, double offset, Quantized* 
              std::string* why, int p_min = 0);
 // Smallest p in [0, 62] with v * 2^p integral, or -1 (the quantizer's rule).
 int dyadic_exponent_of(double v);
+// FP4 pair image of q.J (see Quantized::fp4x2_ok); false if some |J'| has no split.
+bool build_fp4x2(const Quantized& q, std::vector<uint8_t>* out);
 
 }  // namespace ssqa_engine
 
@@ -66,7 +83,7 @@ struct ssqa_problem_s {
   cudaStream_t stream = nullptr;
   int8_t* d_J = nullptr;
   int32_t* d_H = nullptr;
-  uint8_t* d_J4 = nullptr;  // FP4 couplings (q.fp4_ok)
+  uint8_t* d_J4 = nullptr;  // FP4 couplings (q.fp4_ok) or the FP4 pair image (q.fp4x2_ok)
 };
 
 struct ssqa_batch_s {

@@ -71,6 +71,31 @@ void atomic_min(std::atomic<long long>& a, long long v) {
 
 }  // namespace
 
+bool build_fp4x2(const Quantized& q, std::vector<uint8_t>* out) {
+  out->assign(size_t(q.npad) * q.npad, 0);
+  std::atomic<bool> ok{true};
+  parallel_for(q.npad, [&](int lo, int hi) {
+    for (int i = lo; i < hi; ++i) {
+      const int8_t* row = &q.J[size_t(i) * q.npad];
+      uint8_t* o = out->data() + size_t(i) * q.npad;
+      for (int j = 0; j < q.npad; ++j) {
+        const int v = row[j];
+        const int m = v < 0 ? -v : v;
+        if (m > 12 || kFp4x2A[m] < 0) {
+          ok = false;
+          return;
+        }
+        const uint32_t s = v < 0 ? 8u : 0u;
+        const size_t a = fp4x2_byte_a(j);
+        const int sh = fp4x2_shift(j);
+        if (kFp4x2A[m]) o[a] |= uint8_t((uint32_t(kFp4x2A[m]) | s) << sh);
+        if (kFp4x2B[m]) o[a + 64] |= uint8_t((uint32_t(kFp4x2B[m]) | s) << sh);
+      }
+    }
+  });
+  return ok.load();
+}
+
 int dyadic_exponent_of(double v) { return dyadic_exponent(v); }
 
 int quantize(int n, const double* h, const double* J, double offset, Quantized* q,
@@ -184,6 +209,12 @@ int quantize(int n, const double* h, const double* J, double offset, Quantized* 
       q->fp4_ok = ok.load();
     }
     if (!q->fp4_ok) q->J4.clear();
+  }
+  // FP4 pair image when the single one does not exist: J' = A1 + A2.
+  q->fp4x2_ok = false;
+  if (!q->fp4_ok && fp4x2_splittable(q->max_abs_j)) {
+    q->fp4x2_ok = build_fp4x2(*q, &q->J4);
+    if (!q->fp4x2_ok) q->J4.clear();
   }
   // |H'| < 2^29 keeps S + 2H' inside int32 for every n < 2^20.
   for (int i = 0; i < n; ++i) {

@@ -93,7 +93,41 @@ __global__ void k_qfp4(const int8_t* __restrict__ Jq, size_t pairs, uint8_t* __r
   }
 }
 
+// FP4 pair image (engine.h Quantized::fp4x2_ok): one thread per output byte
+// pair (A1 byte, A2 byte) = two couplings of a row; not_split <- 1 if any
+// |J'| has no split (11, or > 12).
+__global__ void k_qfp4x2(const int8_t* __restrict__ Jq, int npad, uint8_t* __restrict__ J4,
+                         int* __restrict__ not_split) {
+  constexpr int kA[13] = {0, 2, 4, 5, 6, 6, 7, 7, 7, 7, 7, 0, 7};
+  constexpr int kB[13] = {0, 0, 0, 0, 0, 2, 0, 2, 4, 5, 6, 0, 7};
+  const size_t pairs = size_t(npad) * (npad / 2);
+  for (size_t x = blockIdx.x * size_t(blockDim.x) + threadIdx.x; x < pairs;
+       x += size_t(gridDim.x) * blockDim.x) {
+    const size_t i = x / (npad / 2);
+    const int j = int(x % (npad / 2)) * 2;  // couplings j, j+1 of row i
+    uint32_t a = 0, b = 0;
+    for (int u = 0; u < 2; ++u) {
+      const int v = Jq[i * npad + j + u];
+      int m = v < 0 ? -v : v;
+      if (m == 11 || m > 12) {
+        atomicOr(not_split, 1);
+        m = 0;
+      }
+      const uint32_t s = v < 0 ? 8u : 0u;
+      if (kA[m]) a |= (uint32_t(kA[m]) | s) << (4 * u);
+      if (kB[m]) b |= (uint32_t(kB[m]) | s) << (4 * u);
+    }
+    const size_t o = i * npad + size_t(j >> 7) * 128 + size_t((j & 127) >> 1);
+    J4[o] = uint8_t(a);
+    J4[o + 64] = uint8_t(b);
+  }
+}
+
 }  // namespace
+
+void launch_qfp4x2(const int8_t* Jq, int npad, uint8_t* J4, int* not_split, cudaStream_t st) {
+  k_qfp4x2<<<1184, 256, 0, st>>>(Jq, npad, J4, not_split);
+}
 
 void launch_qscan(const double* J, size_t count, int* pmax, unsigned long long* bad,
                   cudaStream_t st) {

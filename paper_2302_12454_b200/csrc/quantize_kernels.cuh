@@ -19,4 +19,8 @@ void launch_qtranspose(const double* J, int n, int npad, double up, int8_t* Jq, 
 // J4 <- e2m1 image of Jq (elems couplings), not_fp4 <- 1 if any is not exact.
 void launch_qfp4(const int8_t* Jq, size_t elems, uint8_t* J4, int* not_fp4, cudaStream_t st);
 
+// J4 <- FP4 pair image of Jq (npad x npad bytes; engine.h Quantized::fp4x2_ok);
+// not_split <- 1 if some |Jq| has no split (the image is then unusable).
+void launch_qfp4x2(const int8_t* Jq, int npad, uint8_t* J4, int* not_split, cudaStream_t st);
+
 }  // namespace ssqa_engine

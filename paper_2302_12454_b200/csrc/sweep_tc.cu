@@ -89,6 +89,7 @@ struct TcParams {
   int ring_cur;
   int ring_phys[kMaxDelay + 1];
   int stages, nslot;
+  int pair;  // FP4 pair operands (Quantized::fp4x2_ok): J' = A1 + A2, spins in SWIZZLE_64B stages
   long long* dbg;  // optional timeline (block 0): [role][rt_global][2] clock64 stamps
   int dbg_rts;     // capacity in row tiles
   // per-trial results
@@ -254,6 +255,18 @@ __device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
   d |= uint64_t(1024 >> 4) << 32;
   d |= uint64_t(1) << 46;
   d |= uint64_t(2) << 61;
+  return d;
+}
+
+// K-major, SWIZZLE_64B descriptor (FP4 pair spin stages: 64-byte rows, 8-row
+// atoms of 512 B; layout type 4).
+__device__ __forceinline__ uint64_t umma_desc_sw64(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= uint64_t((saddr >> 4) & 0x3FFF);
+  d |= uint64_t(1) << 16;
+  d |= uint64_t(512 >> 4) << 32;
+  d |= uint64_t(1) << 46;
+  d |= uint64_t(4) << 61;
   return d;
 }
 
@@ -501,13 +514,14 @@ struct Layout {
   uint32_t a_bytes, b_bytes, acc_off, sig_off, ctl_off, tab_off, total;
 };
 
+// b_row: operand bytes per spin column and stage (kBK; 64 for FP4 pairs).
 __host__ __device__ inline Layout make_layout(int NT, int tpt, int stages, int nslot,
-                                              int tile_row = kBM) {
+                                              int tile_row = kBM, int b_row = kBK) {
   Layout L;
   L.stages = stages;
   L.nslot = nslot;
   L.a_bytes = kBM * kBK;
-  L.b_bytes = uint32_t(NT) * kBK;
+  L.b_bytes = uint32_t(NT) * uint32_t(b_row);
   uint32_t o = uint32_t(stages) * (L.a_bytes + L.b_bytes);
   L.acc_off = o;
   o += uint32_t(nslot) * kCW * kBM * 8;
@@ -784,7 +798,11 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
   const Geom& g = P.g;
   const int NT = g.tile_cols;
   constexpr int kTileRow = F4 ? kBM / 2 : kBM;  // bytes per spin-tile row (128 spins)
-  const Layout L = make_layout(NT, g.tpt, P.stages, P.nslot, kTileRow);
+  // FP4 pairs: a stage is K = 128 couplings -- one 128-byte J'' row holding
+  // 64 bytes of A1 and 64 bytes of A2 nibbles -- against 64 bytes of spins
+  const bool pair = F4 && P.pair != 0;
+  const int b_row = pair ? kBK / 2 : kBK;
+  const Layout L = make_layout(NT, g.tpt, P.stages, P.nslot, kTileRow, b_row);
   const int stages = L.stages, nslot = L.nslot;
   uint8_t* sA = smem;
   uint8_t* sB = smem + size_t(stages) * L.a_bytes;
@@ -822,7 +840,7 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
   const int NRT = rt_base + int((long long)rt_span * (part + 1) / RS) - rt_lo;  // this CTA's
   // one stage = 128 bytes of K per row: 128 int8 or 256 e2m1 couplings/spins
   // (an FP4 row of npad = 128 is a partial chunk: TMA zero-fills the rest)
-  const int NKC = F4 ? (g.npad + 2 * kBK - 1) / (2 * kBK) : g.npad / kBK;
+  const int NKC = (F4 && !pair) ? (g.npad + 2 * kBK - 1) / (2 * kBK) : g.npad / kBK;
   // multi-instance problems: this tile's trial anneals its own J', H', offset
   const int j_row0 = P.multi ? tile * g.npad : 0;
   const int nchunk = NT / kCW;
@@ -834,7 +852,7 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
   const int rgroup = (NRT + kMaxRowGroups - 1) / kMaxRowGroups;
   const int nrg = (NRT + rgroup - 1) / rgroup;
   // spin rows covered by one K chunk of the operand stream
-  constexpr int kKRows = F4 ? 2 * kBK : kBK;
+  const int kKRows = (F4 && !pair) ? 2 * kBK : kBK;
 
   // ---- one-time setup ----
   if (threadIdx.x == 0) {
@@ -974,7 +992,7 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
             mbar_expect_tx(&ctl->full[st], L.a_bytes + L.b_bytes);
             tma_load_2d_hint(&tmJ, &ctl->full[st], sA + size_t(st) * L.a_bytes, kc * kBK,
                              j_row0 + (rt_lo + rt) * kBM, pol_keep);
-            tma_load_2d(&tmS, &ctl->full[st], sB + size_t(st) * L.b_bytes, kc * kBK, yS);
+            tma_load_2d(&tmS, &ctl->full[st], sB + size_t(st) * L.b_bytes, kc * b_row, yS);
           }
         }
         if (c < P.sc) ring_advance(ring, c, P.d, P.nslots);
@@ -1005,7 +1023,14 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
             tc_fence_after();
             const uint32_t a0 = smem_u32(sA + size_t(st) * L.a_bytes);
             const uint32_t b0 = smem_u32(sB + size_t(st) * L.b_bytes);
-            if (!(P.exp_flags & 2)) {
+            if (pair && !(P.exp_flags & 2)) {
+              // A sub-blocks [A1 k0, A1 k1, A2 k0, A2 k1] against spin
+              // sub-blocks [k0, k1, k0, k1]: S = A1 sigma + A2 sigma
+#pragma unroll
+              for (int k = 0; k < kBK / 32; ++k)
+                mma_mxf4(d_tmem, umma_desc_sw128(a0 + k * 32), umma_desc_sw64(b0 + (k & 1) * 32),
+                         idesc, (kc | k) ? 1u : 0u, sf_tmem);
+            } else if (!(P.exp_flags & 2)) {
 #pragma unroll
               for (int k = 0; k < kBK / 32; ++k) {
                 if (F4)
@@ -1445,18 +1470,27 @@ bool make_map(CUtensorMap* m, void* base, CUtensorMapDataType dt, uint32_t esize
 // Operand stages and per-subgroup state-ring depth inside ~220 KB: prefer
 // >= 2 ring slots per subgroup (so the loader runs a chunk ahead), then as
 // many operand stages (<= 4) as fit.
-Layout pick_layout(int NT, int tpt, int nsubs, int tile_row) {
+// FP4 pair stages are half as deep in K (and in bytes): up to 6 of them.
+Layout pick_layout(int NT, int tpt, int nsubs, int tile_row, int b_row) {
   const uint32_t cap = 226 * 1024;  // of 227 KB dynamic shared memory per CTA
+  const int max_stages = b_row < kBK ? 6 : 4;
+  if (b_row < kBK)  // operand-feed-bound shapes: deep operand pipeline first
+    for (int stages = max_stages; stages >= 4; --stages)
+      for (int nps = 3; nps >= 1; --nps) {
+        if (nps * nsubs > 16) continue;
+        Layout L = make_layout(NT, tpt, stages, nps * nsubs, tile_row, b_row);
+        if (L.total <= cap) return L;
+      }
   for (int nps = 3; nps >= 1; --nps)
-    for (int stages = 4; stages >= 2; --stages) {
+    for (int stages = max_stages; stages >= 2; --stages) {
       if (nps * nsubs > 16) continue;
-      Layout L = make_layout(NT, tpt, stages, nps * nsubs, tile_row);
+      Layout L = make_layout(NT, tpt, stages, nps * nsubs, tile_row, b_row);
       if (L.total <= cap && (nps >= 2 || stages >= 2)) {
         if (nps >= 2 && stages < 3) continue;  // rather fewer slots than < 3 stages
         return L;
       }
     }
-  return make_layout(NT, tpt, 2, nsubs, tile_row);
+  return make_layout(NT, tpt, 2, nsubs, tile_row, b_row);
 }
 
 // 16 epilogue warps (4 per scheduler): the update chain is latency-bound,
@@ -1512,13 +1546,18 @@ int launch(ssqa_batch_s* b, TcParams& P, bool f4) {
   // FP4 rows are npad/2 bytes (two e2m1 values per byte)
   const uint64_t row_bytes = f4 ? uint64_t(g.npad) / 2 : uint64_t(g.npad);
   void* Jsrc = f4 ? static_cast<void*>(b->prob->d_J4) : static_cast<void*>(b->prob->d_J);
+  // FP4 pair image: rows of npad bytes (two planes); spin stages of 64 bytes
+  const bool pair = f4 && b->prob->q.fp4x2_ok;
+  P.pair = pair ? 1 : 0;
+  const uint64_t j_row_bytes = pair ? uint64_t(g.npad) : row_bytes;
+  const uint32_t b_row = pair ? kBK / 2 : kBK;
   void* Ssrc = f4 ? static_cast<void*>(b->d_sig4) : static_cast<void*>(b->d_sig);
   const uint32_t tile_row = f4 ? kBM / 2 : kBM;
   P.sig_base = static_cast<uint8_t*>(Ssrc);
-  if (!make_map(&maps[0], Jsrc, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, row_bytes,
+  if (!make_map(&maps[0], Jsrc, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, j_row_bytes,
                 uint64_t(g.npad) * b->prob->count, kBK, kBM, CU_TENSOR_MAP_SWIZZLE_128B) ||
-      !make_map(&maps[1], Ssrc, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, row_bytes, srows, kBK,
-                g.tile_cols, CU_TENSOR_MAP_SWIZZLE_128B) ||
+      !make_map(&maps[1], Ssrc, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, row_bytes, srows, b_row,
+                g.tile_cols, pair ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B) ||
       !make_map(&maps[2], Ssrc, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, row_bytes, srows, tile_row,
                 g.tile_cols, CU_TENSOR_MAP_SWIZZLE_NONE) ||
       !make_map(&maps[3], b->d_acc, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, g.npad, g.ccols, kBM,
@@ -1550,10 +1589,11 @@ int launch(ssqa_batch_s* b, TcParams& P, bool f4) {
   }
   const char* env_epi = getenv("SSQA_TC_EPI");
   const int epi = env_epi ? (atoi(env_epi) == 12 ? 12 : 16) : kDefaultEpi;
-  Layout L = pick_layout(g.tile_cols, g.tpt, epi / 4, int(tile_row));
+  Layout L = pick_layout(g.tile_cols, g.tpt, epi / 4, int(tile_row), int(b_row));
   if (const char* st = getenv("SSQA_TC_STAGES")) {  // experiment overrides
     const char* np = getenv("SSQA_TC_NPS");
-    L = make_layout(g.tile_cols, g.tpt, atoi(st), (np ? atoi(np) : 1) * (epi / 4), int(tile_row));
+    L = make_layout(g.tile_cols, g.tpt, atoi(st), (np ? atoi(np) : 1) * (epi / 4), int(tile_row),
+                    int(b_row));
   }
   P.stages = L.stages;
   P.nslot = L.nslot;
@@ -1673,7 +1713,7 @@ void advance_ring(ssqa_batch_s* b, long count) {
 bool tc_uses_fp4(const ssqa_batch_s* b) {
   const Quantized& q = b->prob->q;
   const char* envf4 = getenv("SSQA_TC_FP4");
-  return q.fp4_ok && b->d_sig4 && double(q.max_abs_j) * q.n < double(1 << 22) &&
+  return (q.fp4_ok || q.fp4x2_ok) && b->d_sig4 && double(q.max_abs_j) * q.n < double(1 << 22) &&
          2 * b->g.tile_cols <= int(kSfCol) && !(envf4 && envf4[0] == '0');
 }
 

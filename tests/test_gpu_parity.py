@@ -184,8 +184,19 @@ def test_full_runs_match_oracle_many_trials(orc, engine):
             assert np.array_equal(bits(r.trace_energy), bits(o.trace))
 
 
-def test_dense_integer_model_matches_oracle(orc, engine):
-    """C4-style dense int[-8,7] couplings (the reference's plain-double path)."""
+@pytest.fixture(params=["auto", "int8"])
+def operands(request, monkeypatch):
+    """tcgen05 operand format: the engine's choice (FP4, FP4 pair) or int8."""
+    if request.param == "int8":
+        monkeypatch.setenv("SSQA_TC_FP4", "0")
+    return request.param
+
+
+def test_dense_integer_model_matches_oracle(orc, engine, operands):
+    """C4-style dense int[-8,7] couplings (the reference's plain-double path);
+    on tcgen05 as FP4 pairs (J' = A1 + A2) and as int8."""
+    if operands == "int8" and engine != _lib.ENGINE_TCGEN05:
+        pytest.skip("operand format applies to tcgen05 only")
     m = sq.dense_ising(200, 0, 3)
     p = params(8, 40, tau=5, bidirectional=True)
     seeds = [11, 12, 13]
@@ -489,7 +500,7 @@ def row_split(monkeypatch):
 
 
 @pytest.mark.parametrize("rs", [2, 3, 4])
-def test_row_split_runs_match_oracle(orc, row_split, rs):
+def test_row_split_runs_match_oracle(orc, row_split, rs, operands):
     if not engine_ok(_lib.ENGINE_TCGEN05):
         pytest.skip("tcgen05 engine unavailable")
     row_split(rs)
@@ -708,7 +719,9 @@ def test_device_quantizer_matches_host_quantizer():
         assert (dev["n_pad"], dev["shift_p"], dev["max_abs_j"], dev["max_abs_h"]) == \
             tuple(x.value for x in v), m.n
         Jq = np.abs(m.J * 2.0 ** dev["shift_p"])
-        assert dev["fp4"] == int(bool(np.isin(Jq, [0, 1, 2, 3, 4, 6]).all()))
+        single = bool(np.isin(Jq, [0, 1, 2, 3, 4, 6]).all())
+        pair = bool(np.isin(Jq, [0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 12]).all())
+        assert dev["fp4"] == (1 if single else 2 if pair else 0)
     bad = sq.IsingModel(4)
     bad.set_coupling(0, 1, float("inf"))  # (0.1 is dyadic as a double: 2^-55 * integer)
     with pytest.raises(ValueError, match="not a dyadic"):
@@ -762,3 +775,31 @@ def test_fp4_bidirectional_matches_oracle(orc):
         o = orc.ssqa_run(m.h, m.J, m.offset, p, s, 0.0, True, False)
         assert res[t].best_energy == o.best_energy
         assert np.array_equal(bits(res[t].trace_energy), bits(o.trace))
+
+
+@pytest.mark.parametrize("n,R,T,rs", [(300, 8, 5, 1), (640, 12, 24, 4)], ids=["tile", "split"])
+def test_fp4_pair_operands_match_oracle(orc, row_split, n, R, T, rs):
+    """Couplings |J'| <= 12 (not 11) run as FP4 pairs J' = A1 + A2 (two
+    kind::mxf4 MMAs per spin sub-block); |J'| = 11 falls back to int8."""
+    if not engine_ok(_lib.ENGINE_TCGEN05):
+        pytest.skip("tcgen05 engine unavailable")
+    if rs > 1:
+        row_split(rs)
+    rng = np.random.default_rng(n)
+    vals = np.array([-12, -10, -9, -8, -7, -5, -3, -1, 0, 1, 2, 4, 5, 6, 7, 8, 9, 10, 12])
+    J = np.triu(rng.choice(vals, (n, n)) / 4.0, 1)
+    h = rng.integers(-40, 41, n) / 4.0
+    m = sq.IsingModel.from_arrays(h, J + J.T, 1.5)
+    assert sq.Problem(m).info()["fp4"] == 2
+    p = params(R, 30, tau=4, bidirectional=(rs == 1))
+    seeds = [int(s) for s in rng.integers(0, 2 ** 40, T)]
+    res = sq.ssqa_run_batch(m, to_sq(p), seeds, None, sq.RunOptions(True, False),
+                            engine=_lib.ENGINE_TCGEN05)
+    for t in sorted({0, T // 2, T - 1}):
+        o = orc.ssqa_run(m.h, m.J, m.offset, p, seeds[t], None, True, False)
+        assert (res[t].best_energy, res[t].best_replica) == (o.best_energy, o.best_replica), t
+        assert np.array_equal(res[t].best_state, o.best_state), t
+        assert np.array_equal(bits(res[t].trace_energy), bits(o.trace)), t
+    J11 = J.copy()
+    J11[0, 1] = 11 / 4.0
+    assert sq.Problem(sq.IsingModel.from_arrays(h, J11 + J11.T, 1.5)).info()["fp4"] == 0
