@@ -144,8 +144,11 @@ Geom make_geom(int n, int npad, int R, int T, int sms, int engine, bool fp4, boo
     const int wtiles = (T + wide - 1) / wide;
     // worth it when the wide tiling still fills the SMs with >= 2 parts per tile
     if (nrt >= 16 && wide > tpt && wtiles * 2 <= sms) {
-      tpt = wide;
+      tpt = (T + wtiles - 1) / wtiles;  // as even as the tile count allows
       rs = std::min(nrt, sms / wtiles);
+      // an even part count lets the parts run as CTA pairs (M = 256 MMAs);
+      // worth one idle SM per tile from 5 parts up
+      if (rs >= 5 && (rs & 1) && nrt % 2 == 0) rs -= 1;
     }
     if (const char* env = getenv("SSQA_TC_RS")) {  // test / tuning override
       const int want = atoi(env);

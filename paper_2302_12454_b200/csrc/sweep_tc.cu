@@ -75,7 +75,8 @@ struct TcParams {
   double i0, n_rnd, alpha;
   int bidirectional;
   int fast, nr;                 // fast epilogue (host-checked) and n_rnd * 2^p
-  int exp_flags;                // ablation experiments (SSQA_TC_EXP): 1 no epilogue math, 2 no MMA
+  int exp_flags;                // ablation experiments (SSQA_TC_EXP): 1 no epilogue math, 2 no MMA,
+                                // 4 no operand TMA (MMAs on stale stages)
   double hi_clamp, lo_clamp;    // i0 - alpha, -i0 (formed on the host)
   long c_first, c_last;  // cycles handled: scans/updates for c in [c_first, c_last]
   long sc;               // update iff c < sc
@@ -90,6 +91,11 @@ struct TcParams {
   int ring_phys[kMaxDelay + 1];
   int stages, nslot;
   int pair;  // FP4 pair operands (Quantized::fp4x2_ok): J' = A1 + A2, spins in SWIZZLE_64B stages
+  // Table epilogue (fast mode, tab_w > 0; see TabConsts): integer fields
+  // X >= tab_hi / X < tab_lo1 clamp without FP64, the others read
+  // fl(fl(X 2^-p + jperp u) [+ jperp d]) from a per-cycle smem table of tab_w
+  // entries per neighbour-sign combination
+  int tab_lo1, tab_hi, tab_w;
   long long* dbg;  // optional timeline (block 0): [role][rt_global][2] clock64 stamps
   int dbg_rts;     // capacity in row tiles
   // per-trial results
@@ -277,14 +283,6 @@ __host__ __device__ constexpr uint32_t idesc_i8(int M, int N) {
          (uint32_t(M >> 4) << 24);
 }
 
-__device__ __forceinline__ void mma_i8(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
-                                       uint32_t idesc, uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
-      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
-}
 
 // kind::mxf4 block-scaled MMA (A, B e2m1 packed, ue8m0 scales in TMEM).
 __host__ __device__ constexpr uint32_t idesc_mxf4(int M, int N) {
@@ -292,15 +290,6 @@ __host__ __device__ constexpr uint32_t idesc_mxf4(int M, int N) {
          (uint32_t(M >> 4) << 24);
 }
 
-__device__ __forceinline__ void mma_mxf4(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
-                                         uint32_t idesc, uint32_t accumulate, uint32_t sf_tmem) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%5], "
-      "p;\n\t}" ::"r"(d_tmem),
-      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate), "r"(sf_tmem));
-}
 
 __device__ __forceinline__ void tmem_st16_const(uint32_t taddr, uint32_t v) {
   asm volatile(
@@ -310,12 +299,113 @@ __device__ __forceinline__ void tmem_st16_const(uint32_t taddr, uint32_t v) {
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
 
-__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+
+// ---- MMA issue from a whole, converged warp: one lane is elected inside the
+// asm, so every operand stays warp-uniform (uniform registers, no per-MMA
+// R2UR / elect loop around a single-lane branch).  Measured on B200
+// (scripts/mma_peak.cu): a single-lane issuer sustains ~66 % (N = 224) /
+// ~43 % (N = 144) of the kind::mxf4 rate behind per-stage mbarriers, the
+// warp-wide issuer 100 % / 95 %.
+// CTA pairs (cta_group::2): two CTAs of a cluster run M = 256 MMAs, each
+// holding its own 128 J' rows and half of the spin columns; the leader (rank
+// 0) issues the MMAs, whose commits arrive on both CTAs' barriers.
+template <bool CTA2>
+__device__ __forceinline__ void mma_i8_w(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                         uint32_t idesc, uint32_t accumulate) {
+  if (CTA2)
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\telect.sync _|e, 0xffffffff;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
+  else
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\telect.sync _|e, 0xffffffff;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+
+template <bool CTA2>
+__device__ __forceinline__ void mma_mxf4_w(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                           uint32_t idesc, uint32_t accumulate, uint32_t sf_tmem) {
+  if (CTA2)
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\telect.sync _|e, 0xffffffff;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], "
+        "[%5], p;\n\t}" ::"r"(d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate), "r"(sf_tmem));
+  else
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\telect.sync _|e, 0xffffffff;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], "
+        "[%5], p;\n\t}" ::"r"(d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate), "r"(sf_tmem));
+}
+
+// Commit (from the whole warp, one elected lane); with CTA pairs the arrive
+// lands on the barrier at the same smem offset in both CTAs.
+template <bool CTA2>
+__device__ __forceinline__ void mma_commit_w(uint64_t* bar) {
+  if (CTA2)
+    asm volatile(
+        "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+        " [%0], %1;\n\t}" ::"r"(smem_u32(bar)),
+        "h"(uint16_t(3))
+        : "memory");
+  else
+    asm volatile(
+        "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(
+            smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
+// shared::cluster address of the same smem location in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t mapa_rank(uint32_t saddr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
+               : "memory");
+}
+
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;"
+               ::: "memory");
+}
+
+// TMA tile load into this CTA's smem whose completion (complete_tx) is
+// counted on the pair leader's barrier (cluster address).
+__device__ __forceinline__ void tma_load_2d_pair(const CUtensorMap* map, uint32_t bar_cluster,
+                                                 void* dst, int x, int y) {
   asm volatile(
-      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-          smem_u32(bar))
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_cluster), "r"(x), "r"(y)
       : "memory");
 }
+__device__ __forceinline__ void tma_load_2d_pair_hint(const CUtensorMap* map, uint32_t bar_cluster,
+                                                      void* dst, int x, int y, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      ".L2::cache_hint [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_cluster), "r"(x), "r"(y), "l"(policy)
+      : "memory");
+}
+
 
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, int32_t (&v)[16]) {
   asm volatile(
@@ -511,17 +601,19 @@ __device__ __forceinline__ void ring_advance(int* r, long c, int d, int nslots) 
 
 struct Layout {
   int stages, nslot;
-  uint32_t a_bytes, b_bytes, acc_off, sig_off, ctl_off, tab_off, total;
+  uint32_t a_bytes, b_bytes, acc_off, sig_off, ctl_off, tab_off, ytab_off, total;
 };
 
-// b_row: operand bytes per spin column and stage (kBK; 64 for FP4 pairs).
+// b_row: operand bytes per spin column and stage (kBK; 64 for FP4 pairs);
+// b_cols: spin columns per operand stage (NT; NT/2 for CTA pairs).
 __host__ __device__ inline Layout make_layout(int NT, int tpt, int stages, int nslot,
-                                              int tile_row = kBM, int b_row = kBK) {
+                                              int tile_row = kBM, int b_row = kBK,
+                                              int b_cols = -1, int tab_bytes = 0) {
   Layout L;
   L.stages = stages;
   L.nslot = nslot;
   L.a_bytes = kBM * kBK;
-  L.b_bytes = uint32_t(NT) * uint32_t(b_row);
+  L.b_bytes = uint32_t(b_cols < 0 ? NT : b_cols) * uint32_t(b_row);
   uint32_t o = uint32_t(stages) * (L.a_bytes + L.b_bytes);
   L.acc_off = o;
   o += uint32_t(nslot) * kCW * kBM * 8;
@@ -531,6 +623,9 @@ __host__ __device__ inline Layout make_layout(int NT, int tpt, int stages, int n
   o += uint32_t((sizeof(SmemCtl) + 127) / 128 * 128);
   L.tab_off = o;
   o += uint32_t(NT) * (kColBytes + 8 * 4) + 8 + uint32_t(tpt) * uint32_t(sizeof(TrialTab));
+  o = (o + 15u) & ~15u;
+  L.ytab_off = o;
+  o += uint32_t(tab_bytes);
   L.total = o + 1024;  // alignment slack
   return L;
 }
@@ -549,6 +644,26 @@ struct EpiRow {
   uint32_t nib_live;        // FP4 word stores: nibble mask of the live rows of that word
 };
 
+// Table epilogue constants for one cycle.  With X = S + H' + noise * NR the
+// integer field, the reference's update is y = fl(fl(X 2^-p + jperp u)
+// [+ jperp d]), s = fl(acc + y), then the clamp.  For X >= hi the sum s is
+// at least i0 whatever acc and the neighbours are (host bound, 1 of margin
+// over every rounding), for X < lo1 it is below -i0: no FP64 at all.  In
+// between y comes from ytab[combo * w + X - lo1] (combo: bit 0 = sigma_up
+// negative, bit 1 = sigma_dn negative), built per cycle with the reference's
+// own operations, and the only FP64 instruction left is s = acc + y; the
+// clamp compares the bit patterns (i0 > 0 > -i0, no NaN, no -0.0).  The
+// FP64 units share the tensor core's issue path on B200: while MMAs run an
+// FP64 add costs ~10x (scripts/dadd_probe.cu).
+struct TabConsts {
+  int lo1, hi, w;
+  long long i0_bits;          // s >= i0   <=>  (int64) bits(s) >= i0_bits
+  unsigned long long lo_bits; // s < -i0   <=>  (uint64) bits(s) > lo_bits
+  long long hic_bits;         // bits(i0 - alpha), bits(-i0)
+  long long loc_bits;
+  const double* ytab;
+};
+
 // Spread the 8 bits of b to bit 4k+3 of a word of e2m1 +-1 nibbles (0x2 / 0xA).
 __device__ __forceinline__ uint32_t nibbles_pm1(uint32_t b) {
   uint32_t x = (b | (b << 12)) & 0x000F000Fu;
@@ -563,11 +678,12 @@ __device__ __forceinline__ uint32_t nibbles_pm1(uint32_t b) {
 // the column loop:
 //   BIDIR   couple to k-1 as well as k+1
 //   SIGACC  sigma(c) = sign(acc(c)) instead of a load (all but the first sweep)
-//   FAST    host-checked fast arithmetic (update_fast2), int32 energy partials
+//   FAST    host-checked table epilogue (TabConsts), int32 energy partials
 //   F4      FP4 operands: fp32 fields in TMEM, spins stored as e2m1 nibbles
 template <bool BIDIR, bool SIGACC, bool FAST, bool F4>
 __device__ __forceinline__ void epi_chunks(const EpiRow& er, const UpdateConsts& uc,
-                                           const FastConsts& fc, const I2D& i2d, SmemCtl* ctl,
+                                           const FastConsts& fc, const TabConsts& tc,
+                                           const I2D& i2d, SmemCtl* ctl,
                                            const double* acc_ring, const ColTab* c_col,
                                            long long* q_sum, uint32_t trow, int sub,
                                            int nsubs, int nchunk, int nps, uint32_t cnt0, int il,
@@ -596,25 +712,94 @@ __device__ __forceinline__ void epi_chunks(const EpiRow& er, const UpdateConsts&
     const double* ab = acc_ring + size_t(slot) * kCW * kBM + il;
     int ep[kCW];
     uint32_t ball[kCW];
+    if (FAST) {
+      // table epilogue (TabConsts); pass 1: integer fields, energies, table positions
+      int X[kCW];
+      uint32_t cmb = 0, midm = 0;
 #pragma unroll
-    for (int j = 0; j < kCW; ++j) {
-      const int cl = cb + j;
-      const uint4 ct = lds128(c_col + cl);
-      const uint64_t cbase = (uint64_t(ct.y) << 32) | ct.x;
-      const uint32_t coff = ct.z;
-      const uint32_t nb = ct.w;
-      const double a_old = ab[j * kBM];
-      // FP4: the fp32 accumulator holds a small exact integer (|S| < 2^22);
-      // its bits after adding 1.5*2^23 are 0x4B400000 + S, and the bias is
-      // folded into the per-row constants h1/h2 (EpiRow).
-      const int S = F4 ? __float_as_int(__int_as_float(v[j]) + 12582912.0f) : v[j];
-      const int s2 = S + er.h2;
-      // Energy partials of every column, padding included: the scan reads only
-      // live columns, and padded rows contribute 0 (J', H' rows are zero).
-      if (SIGACC && FAST) {
-        const int m = __double2hiint(a_old) >> 31;  // sign of a finite, never -0.0 value
-        ep[j] = (s2 ^ m) - m;
-      } else {
+      for (int j = 0; j < kCW; ++j) {
+        const uint4 ct = lds128(c_col + cb + j);
+        const uint64_t cbase = (uint64_t(ct.y) << 32) | ct.x;
+        const double a_old = ab[j * kBM];
+        const int S = F4 ? __float_as_int(__int_as_float(v[j]) + 12582912.0f) : v[j];
+        const int s2 = S + er.h2;
+        if (SIGACC) {
+          const int m = __double2hiint(a_old) >> 31;
+          ep[j] = (s2 ^ m) - m;
+        } else {
+          int sg;
+          if (F4) {
+            const uint32_t bc = ld_u8(reinterpret_cast<const uint8_t*>(er.cur_i + (ct.z >> 1)));
+            sg = ((bc >> er.nib_shift) & 8u) ? -1 : 1;
+          } else {
+            sg = ld_s8(reinterpret_cast<const int8_t*>(er.cur_i + ct.z));
+          }
+          ep[j] = sg * s2;
+        }
+        uint32_t neg_up, neg_dn = 0;
+        if (F4) {
+          neg_up = (uint32_t(er.st_i[ct.w & 0xffffu]) >> er.nib_shift) >> 3 & 1u;
+          if (BIDIR) neg_dn = (uint32_t(er.st_i[(ct.w >> 16) & 0x7fffu]) >> er.nib_shift) >> 3 & 1u;
+        } else {
+          neg_up = uint32_t(int8_t(er.st_i[ct.w & 0xffffu])) >> 31;
+          if (BIDIR) neg_dn = uint32_t(int8_t(er.st_i[(ct.w >> 16) & 0x7fffu])) >> 31;
+        }
+        const uint32_t top = (SSQA_ABL & 512) ? uint32_t(cbase) ^ uint32_t(er.iG)
+                                              : mix64_top32_pre(cbase + er.iG);
+        const int nzi = top < 0x70000000u ? 0 : (top < 0xB8000000u ? -fc.nr : fc.nr);
+        X[j] = S + er.h1 + nzi;
+        cmb |= (neg_up | (neg_dn << 1)) << (2 * j);
+        midm |= uint32_t(unsigned(X[j] - tc.lo1) < unsigned(tc.w)) << j;
+      }
+      // pass 2: new accumulators; the table path only where a lane needs it
+      const bool any_mid = ballot_nz(midm) != 0u;
+#pragma unroll
+      for (int j = 0; j < kCW; ++j) {
+        const uint2 cw = *reinterpret_cast<const uint2*>(&c_col[cb + j].off);
+        const bool pos = X[j] >= tc.hi;
+        long long res = pos ? tc.hic_bits : tc.loc_bits;
+        if (any_mid) {
+          const bool mid = (midm >> j) & 1u;
+          const int e = int((cmb >> (2 * j)) & 3u) * tc.w + (mid ? X[j] - tc.lo1 : 0);
+          const double sd = __dadd_rn(ab[j * kBM], tc.ytab[e]);
+          const long long sb = __double_as_longlong(sd);
+          const bool ge = sb >= tc.i0_bits;
+          const bool lt = static_cast<unsigned long long>(sb) > tc.lo_bits;
+          const long long r2 = ge ? tc.hic_bits : (lt ? tc.loc_bits : sb);
+          res = mid ? r2 : res;
+        }
+        const uint32_t neg = uint32_t(static_cast<unsigned long long>(res) >> 63);
+        const bool w = (cw.y & 0x80000000u) && er.w_row;
+        if (!(SSQA_ABL & 64))
+          st_f64_if(reinterpret_cast<double*>(er.acc_i + uint64_t(cw.x) * 8u),
+                    __longlong_as_double(res), w, er.pol_stream);
+        if (SSQA_ABL & 32) {
+        } else if (kWordSt) {
+          ball[j] = (SSQA_ABL & 2048) ? neg : ballot_neg(neg);
+        } else if (F4) {
+          const uint32_t nib = 2u | (neg << 3);
+          const uint32_t hi = __shfl_xor_sync(0xffffffffu, nib, 1);
+          st_u8_if(reinterpret_cast<uint8_t*>(er.dst_i + (cw.x >> 1)), nib | (hi << 4),
+                   w && !(lane & 1));
+        } else {
+          st_s8_if(reinterpret_cast<int8_t*>(er.dst_i + uint64_t(cw.x)), int(1 - 2 * int(neg)), w);
+        }
+      }
+    } else {
+      // exact path for any finite or non-finite double (hand-written lattices)
+#pragma unroll
+      for (int j = 0; j < kCW; ++j) {
+        const int cl = cb + j;
+        const uint4 ct = lds128(c_col + cl);
+        const uint64_t cbase = (uint64_t(ct.y) << 32) | ct.x;
+        const uint32_t coff = ct.z;
+        const uint32_t nb = ct.w;
+        const double a_old = ab[j * kBM];
+        // FP4: the fp32 accumulator holds a small exact integer (|S| < 2^22);
+        // its bits after adding 1.5*2^23 are 0x4B400000 + S, and the bias is
+        // folded into the per-row constants h1/h2 (EpiRow).
+        const int S = F4 ? __float_as_int(__int_as_float(v[j]) + 12582912.0f) : v[j];
+        const int s2 = S + er.h2;
         int sg;
         if (SIGACC) {
           sg = a_old >= 0.0 ? 1 : -1;
@@ -624,48 +809,35 @@ __device__ __forceinline__ void epi_chunks(const EpiRow& er, const UpdateConsts&
         } else {
           sg = ld_s8(reinterpret_cast<const int8_t*>(er.cur_i + coff));
         }
+        // energy partials of every column, padding included: the scan reads
+        // only live columns, and padded rows contribute 0 (J', H' rows are zero)
         ep[j] = sg * s2;
-      }
-      int up, dn = 0;
-      if (F4 && FAST) {
-        // update_fast2 only reads the sign bit: move the nibble's bit 3 there
-        up = int(uint32_t(er.st_i[nb & 0xffffu]) << (28u - er.nib_shift));
-        if (BIDIR) dn = int(uint32_t(er.st_i[(nb >> 16) & 0x7fffu]) << (28u - er.nib_shift));
-      } else if (F4) {
-        const uint32_t bu = er.st_i[nb & 0xffffu];
-        up = ((bu >> er.nib_shift) & 8u) ? -1 : 1;
-        if (BIDIR) dn = ((uint32_t(er.st_i[(nb >> 16) & 0x7fffu]) >> er.nib_shift) & 8u) ? -1 : 1;
-      } else {
-        up = int8_t(er.st_i[nb & 0xffffu]);
-        if (BIDIR) dn = int8_t(er.st_i[(nb >> 16) & 0x7fffu]);
-      }
-      double nv;
-      uint32_t neg;  // 1 when the new spin is -1
-      if (FAST) {
-        const uint32_t top = (SSQA_ABL & 512) ? uint32_t(cbase) ^ uint32_t(er.iG)
-                                              : mix64_top32_pre(cbase + er.iG);
-        nv = update_fast2<BIDIR>(fc, i2d, S + er.h1, top, up, dn, a_old);
-        neg = uint32_t(__double2hiint(nv)) >> 31;
-      } else {
+        int up, dn = 0;
+        if (F4) {
+          const uint32_t bu = er.st_i[nb & 0xffffu];
+          up = ((bu >> er.nib_shift) & 8u) ? -1 : 1;
+          if (BIDIR) dn = ((uint32_t(er.st_i[(nb >> 16) & 0x7fffu]) >> er.nib_shift) & 8u) ? -1 : 1;
+        } else {
+          up = int8_t(er.st_i[nb & 0xffffu]);
+          if (BIDIR) dn = int8_t(er.st_i[(nb >> 16) & 0x7fffu]);
+        }
         const double field = scaled_i32(S + er.h1, i2d);
         const uint32_t t5 = mix64_top5_pre(cbase + er.iG);
-        nv = update_fast(uc, field, t5, up, dn, BIDIR, a_old);
-        neg = nv >= 0.0 ? 0u : 1u;
-      }
-      const bool w = (nb & 0x80000000u) && er.w_row;
-      if (!(SSQA_ABL & 64))
-        st_f64_if(reinterpret_cast<double*>(er.acc_i + uint64_t(coff) * 8u), nv, w, er.pol_stream);
-      if (SSQA_ABL & 32) {
-      } else if (kWordSt) {
-        ball[j] = (SSQA_ABL & 2048) ? neg : ballot_neg(neg);
-      } else if (F4) {
-        // e2m1 +1 = 0x2, -1 = 0xA; even lanes store the byte of rows (i, i+1)
-        const uint32_t nib = 2u | (neg << 3);
-        const uint32_t hi = __shfl_xor_sync(0xffffffffu, nib, 1);
-        st_u8_if(reinterpret_cast<uint8_t*>(er.dst_i + (coff >> 1)), nib | (hi << 4),
-                 w && !(lane & 1));
-      } else {
-        st_s8_if(reinterpret_cast<int8_t*>(er.dst_i + uint64_t(coff)), int(1 - 2 * int(neg)), w);
+        const double nv = update_fast(uc, field, t5, up, dn, BIDIR, a_old);
+        const uint32_t neg = nv >= 0.0 ? 0u : 1u;
+        const bool w = (nb & 0x80000000u) && er.w_row;
+        if (!(SSQA_ABL & 64))
+          st_f64_if(reinterpret_cast<double*>(er.acc_i + uint64_t(coff) * 8u), nv, w, er.pol_stream);
+        if (SSQA_ABL & 32) {
+        } else if (F4) {
+          // e2m1 +1 = 0x2, -1 = 0xA; even lanes store the byte of rows (i, i+1)
+          const uint32_t nib = 2u | (neg << 3);
+          const uint32_t hi = __shfl_xor_sync(0xffffffffu, nib, 1);
+          st_u8_if(reinterpret_cast<uint8_t*>(er.dst_i + (coff >> 1)), nib | (hi << 4),
+                   w && !(lane & 1));
+        } else {
+          st_s8_if(reinterpret_cast<int8_t*>(er.dst_i + uint64_t(coff)), int(1 - 2 * int(neg)), w);
+        }
       }
     }
     if (kWordSt && !(SSQA_ABL & 32)) {
@@ -786,7 +958,8 @@ static_assert((16 * EpiRegs<16>::value + 4 * kCtlRegs) * 32 <= 20 * 32 * 96, "EP
 // Warp roles: 0 .. EPI-1 epilogue (EPI/4 warps per TMEM lane quarter),
 // EPI operand TMA producer, EPI+1 TMEM allocator + MMA issuer, EPI+2 state
 // loader (TMA of accumulator chunks and delayed-spin tiles).
-template <int EPI, bool F4>
+// CTA2: row-split CTA pairs (clusters of 2) sharing M = 256 MMAs.
+template <int EPI, bool F4, bool CTA2>
 __global__ void __launch_bounds__(32 * (4 + EPI), 1)
     k_sweep_tc(const __grid_constant__ CUtensorMap tmJ, const __grid_constant__ CUtensorMap tmS,
                const __grid_constant__ CUtensorMap tmSe, const __grid_constant__ CUtensorMap tmA,
@@ -802,7 +975,8 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
   // 64 bytes of A1 and 64 bytes of A2 nibbles -- against 64 bytes of spins
   const bool pair = F4 && P.pair != 0;
   const int b_row = pair ? kBK / 2 : kBK;
-  const Layout L = make_layout(NT, g.tpt, P.stages, P.nslot, kTileRow, b_row);
+  const Layout L = make_layout(NT, g.tpt, P.stages, P.nslot, kTileRow, b_row, CTA2 ? NT / 2 : NT,
+                               P.fast ? (P.bidirectional ? 4 : 2) * P.tab_w * 8 : 0);
   const int stages = L.stages, nslot = L.nslot;
   uint8_t* sA = smem;
   uint8_t* sB = smem + size_t(stages) * L.a_bytes;
@@ -816,6 +990,7 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
   int* c_kt = reinterpret_cast<int*>(c_E + 4 * NT);
   int* c_flag = c_kt + NT;
   TrialTab* trials = reinterpret_cast<TrialTab*>(c_flag + NT + (NT & 1));
+  double* ytab = reinterpret_cast<double*>(smem + L.ytab_off);  // TabConsts::ytab
 
   // warp index broadcast from lane 0: provably warp-uniform for ptxas (role
   // branches and setmaxnreg must be warp-uniform)
@@ -836,8 +1011,18 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
   const bool shard_mode = P.run_mode == 2;  // one pass over the rows of a GPU shard
   const int rt_base = shard_mode ? P.shard_rt0 : 0;
   const int rt_span = shard_mode ? P.shard_nrt : NRT_all;
-  const int rt_lo = rt_base + int((long long)rt_span * part / RS);
-  const int NRT = rt_base + int((long long)rt_span * (part + 1) / RS) - rt_lo;  // this CTA's
+  // CTA pairs: parts 2p, 2p+1 of a column tile form a cluster (rank = part & 1,
+  // the leader is rank 0); pair p owns row tiles [2 u_lo, 2 u_hi), rank 0 the
+  // first half and rank 1 the second -- equal counts, as one M = 256 MMA
+  // covers a row tile of each.
+  const uint32_t crank = CTA2 ? uint32_t(part & 1) : 0u;
+  const bool leader = crank == 0;
+  const int u_lo = int((long long)(rt_span / 2) * (part / 2) / (RS / 2 > 0 ? RS / 2 : 1));
+  const int u_hi = int((long long)(rt_span / 2) * (part / 2 + 1) / (RS / 2 > 0 ? RS / 2 : 1));
+  const int rt_lo = CTA2 ? rt_base + 2 * u_lo + int(crank) * (u_hi - u_lo)
+                         : rt_base + int((long long)rt_span * part / RS);
+  const int NRT = CTA2 ? u_hi - u_lo
+                       : rt_base + int((long long)rt_span * (part + 1) / RS) - rt_lo;  // this CTA's
   // one stage = 128 bytes of K per row: 128 int8 or 256 e2m1 couplings/spins
   // (an FP4 row of npad = 128 is a partial chunk: TMA zero-fills the rest)
   const int NKC = (F4 && !pair) ? (g.npad + 2 * kBK - 1) / (2 * kBK) : g.npad / kBK;
@@ -862,7 +1047,7 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&ctl->tfull[b], 1);
-      mbar_init(&ctl->tempty[b], EPI);
+      mbar_init(&ctl->tempty[b], CTA2 ? 2 * EPI : EPI);  // pair: both CTAs' epilogues
       mbar_init(&ctl->sfull[b], 1);
       mbar_init(&ctl->sempty[b], EPI);
     }
@@ -890,10 +1075,17 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
   }
   if (warp == kWarpMma) {
     const uint32_t ncols = (F4 || 2 * acc_cols > 256) ? 512u : 256u;
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(&ctl->tmem_base)),
-                 "r"(ncols));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if (CTA2) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(&ctl->tmem_base)),
+                   "r"(ncols));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(&ctl->tmem_base)),
+                   "r"(ncols));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
   }
   for (int c = threadIdx.x; c < NT; c += blockDim.x) {
     const ColInfo ci = decode_col(g, col0 + c);
@@ -923,17 +1115,22 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
     trials[t] = tt;
   }
   tc_fence_before();
-  __syncthreads();
+  // pair: barriers initialised and TMEM allocated in both CTAs before any
+  // cross-CTA arrive, commit or TMA
+  if (CTA2) cluster_sync_all();
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = ctl->tmem_base;
-  const uint32_t idesc = F4 ? idesc_mxf4(kBM, NT) : idesc_i8(kBM, NT);
+  constexpr int kMmaM = CTA2 ? 2 * kBM : kBM;
+  const uint32_t idesc = F4 ? idesc_mxf4(kMmaM, NT) : idesc_i8(kMmaM, NT);
   const uint32_t sf_tmem = tmem_base + kSfCol;  // unit (2^0) block scales for FP4
   if (F4) {
     // every ue8m0 scale factor is 127 = 2^0: fill the whole scale region
     if (warp < 4) tmem_st16_const(tmem_base + (uint32_t(warp * 32) << 16) + kSfCol, 0x7F7F7F7Fu),
                   tmem_st16_const(tmem_base + (uint32_t(warp * 32) << 16) + kSfCol + 16, 0x7F7F7F7Fu);
     tc_fence_before();
-    __syncthreads();
+    if (CTA2) cluster_sync_all();  // the leader's MMAs read both CTAs' scales
+    else __syncthreads();
     tc_fence_after();
   }
 
@@ -989,20 +1186,35 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
             const int st = it % stages;
             const uint32_t ph = (it / stages) & 1;
             mbar_wait(&ctl->empty[st], ph ^ 1);
-            mbar_expect_tx(&ctl->full[st], L.a_bytes + L.b_bytes);
-            tma_load_2d_hint(&tmJ, &ctl->full[st], sA + size_t(st) * L.a_bytes, kc * kBK,
-                             j_row0 + (rt_lo + rt) * kBM, pol_keep);
-            tma_load_2d(&tmS, &ctl->full[st], sB + size_t(st) * L.b_bytes, kc * b_row, yS);
+            if (P.exp_flags & 4) {
+              if (!CTA2 || leader) mbar_arrive(&ctl->full[st]);
+            } else if (CTA2) {
+              // both CTAs' tiles complete on the leader's barrier: its own J'
+              // rows and half of the spin columns from each CTA
+              const uint32_t bar = mapa_rank(smem_u32(&ctl->full[st]), 0);
+              if (leader) mbar_expect_tx(&ctl->full[st], 2 * (L.a_bytes + L.b_bytes));
+              tma_load_2d_pair_hint(&tmJ, bar, sA + size_t(st) * L.a_bytes, kc * kBK,
+                                    j_row0 + (rt_lo + rt) * kBM, pol_keep);
+              tma_load_2d_pair(&tmS, bar, sB + size_t(st) * L.b_bytes, kc * b_row,
+                               yS + int(crank) * (NT / 2));
+            } else {
+              mbar_expect_tx(&ctl->full[st], L.a_bytes + L.b_bytes);
+              tma_load_2d_hint(&tmJ, &ctl->full[st], sA + size_t(st) * L.a_bytes, kc * kBK,
+                               j_row0 + (rt_lo + rt) * kBM, pol_keep);
+              tma_load_2d(&tmS, &ctl->full[st], sB + size_t(st) * L.b_bytes, kc * b_row, yS);
+            }
           }
         }
         if (c < P.sc) ring_advance(ring, c, P.d, P.nslots);
       }
     }
     __syncwarp();
+    if (CTA2) cluster_sync_all();  // no CTA leaves while its pair may still signal it
   } else if (warp == kWarpMma) {
-    // ===== MMA issuer =====
+    // ===== MMA issuer (the pair's leader only; the whole warp runs the loop,
+    // one elected lane issues) =====
     SSQA_CTL_REGS();
-    if (lane == 0) {
+    if (leader) {
       for (long c = P.c_first; c <= P.c_last; ++c) {
         const long s = c - P.c_first;
         if (s > 0) {
@@ -1021,29 +1233,33 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
             const uint32_t ph = (it / stages) & 1;
             mbar_wait(&ctl->full[st], ph);
             tc_fence_after();
-            const uint32_t a0 = smem_u32(sA + size_t(st) * L.a_bytes);
+            // descriptors of the stage; the K sub-blocks advance the start
+            // address by 32 B (+2 in the >>4 field)
+            const uint64_t ad = umma_desc_sw128(smem_u32(sA + size_t(st) * L.a_bytes));
             const uint32_t b0 = smem_u32(sB + size_t(st) * L.b_bytes);
             if (pair && !(P.exp_flags & 2)) {
               // A sub-blocks [A1 k0, A1 k1, A2 k0, A2 k1] against spin
               // sub-blocks [k0, k1, k0, k1]: S = A1 sigma + A2 sigma
+              const uint64_t bd = umma_desc_sw64(b0);
 #pragma unroll
               for (int k = 0; k < kBK / 32; ++k)
-                mma_mxf4(d_tmem, umma_desc_sw128(a0 + k * 32), umma_desc_sw64(b0 + (k & 1) * 32),
-                         idesc, (kc | k) ? 1u : 0u, sf_tmem);
+                mma_mxf4_w<CTA2>(d_tmem, ad + uint64_t(2 * k), bd + uint64_t(2 * (k & 1)), idesc,
+                                 (kc | k) ? 1u : 0u, sf_tmem);
             } else if (!(P.exp_flags & 2)) {
+              const uint64_t bd = umma_desc_sw128(b0);
 #pragma unroll
               for (int k = 0; k < kBK / 32; ++k) {
                 if (F4)
-                  mma_mxf4(d_tmem, umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32),
-                           idesc, (kc | k) ? 1u : 0u, sf_tmem);
+                  mma_mxf4_w<CTA2>(d_tmem, ad + uint64_t(2 * k), bd + uint64_t(2 * k), idesc,
+                                   (kc | k) ? 1u : 0u, sf_tmem);
                 else
-                  mma_i8(d_tmem, umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32),
-                         idesc, (kc | k) ? 1u : 0u);
+                  mma_i8_w<CTA2>(d_tmem, ad + uint64_t(2 * k), bd + uint64_t(2 * k), idesc,
+                                 (kc | k) ? 1u : 0u);
               }
             }
-            mma_commit(&ctl->empty[st]);
+            mma_commit_w<CTA2>(&ctl->empty[st]);
           }
-          mma_commit(&ctl->tfull[buf]);
+          mma_commit_w<CTA2>(&ctl->tfull[buf]);
           DBG_STAMP(0, acc_it, 1);
         }
       }
@@ -1052,8 +1268,14 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
     mbar_wait(&ctl->done, 0);
     tc_fence_after();
     const uint32_t ncols = (F4 || 2 * acc_cols > 256) ? 512u : 256u;
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
-                 "r"(ncols));
+    if (CTA2) {
+      cluster_sync_all();  // both CTAs' epilogues are done with the pair's TMEM
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                   "r"(ncols));
+    } else {
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                   "r"(ncols));
+    }
   } else if (warp == kWarpLoader) {
     // ===== state loader: delayed-spin tile + accumulator chunks =====
     SSQA_CTL_REGS();
@@ -1101,6 +1323,7 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
       }
     }
     __syncwarp();
+    if (CTA2) cluster_sync_all();
   } else if (warp >= EPI) {
     // ===== row-ready publisher (row split only): once this CTA's epilogue has
     // written a group of its row tiles in pass c, stamp them for the other
@@ -1119,6 +1342,8 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
         }
       }
     }
+    __syncwarp();
+    if (CTA2) cluster_sync_all();
   } else {
     // ===== epilogue =====
     SSQA_EPI_REGS();
@@ -1133,6 +1358,21 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
       const bool do_update = c < P.sc;
       const int cur = ring[0];
       const int dst = do_update ? ring_free(cur, ring + 1, P.d, P.nslots) : cur;
+      if (!drain && P.fast) {
+        // this cycle's table of fl(fl(X 2^-p + jperp u) [+ jperp d]) (TabConsts),
+        // with the reference's own operations (annealer.cpp:276-284)
+        const double jp = P.run_mode ? P.jperp_tab[c] : P.jperp_fixed;
+        const double jpos = __dmul_rn(jp, 1.0), jneg = __dmul_rn(jp, -1.0);
+        const I2D i2 = make_i2d(P.shift_p);
+        const int ncmb = P.bidirectional ? 4 : 2;
+        for (int e = ew * 32 + lane; e < ncmb * P.tab_w; e += EPI * 32) {
+          const int cmb = e / P.tab_w;
+          double in = scaled_i32(P.tab_lo1 + (e - cmb * P.tab_w), i2);
+          in = __dadd_rn(in, (cmb & 1) ? jneg : jpos);
+          if (P.bidirectional) in = __dadd_rn(in, (cmb & 2) ? jneg : jpos);
+          ytab[e] = in;
+        }
+      }
       if (!drain) {
         for (int cl = ew * 32 + lane; cl < NT; cl += EPI * 32) {
           const int k = c_kt[cl] & 0xffff, tl = c_kt[cl] >> 16;
@@ -1159,6 +1399,15 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
       fc.i0 = i0c;
       fc.hi_clamp = (P.run_mode && P.i0_tab) ? __dsub_rn(i0c, P.alpha) : P.hi_clamp;
       fc.lo_clamp = -i0c;
+      TabConsts tc;
+      tc.lo1 = P.tab_lo1;
+      tc.hi = P.tab_hi;
+      tc.w = P.tab_w;
+      tc.i0_bits = __double_as_longlong(i0c);
+      tc.lo_bits = static_cast<unsigned long long>(__double_as_longlong(fc.lo_clamp));
+      tc.hic_bits = __double_as_longlong(fc.hi_clamp);
+      tc.loc_bits = __double_as_longlong(fc.lo_clamp);
+      tc.ytab = ytab;
       // sigma(c) is sign(acc(c)) once this kernel has updated the lattice;
       // on the first cycle it comes from the spin slot (init / written state).
       const bool sig_from_acc = c > P.c_first;
@@ -1223,7 +1472,7 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
             er.dst_w = sig_dst + ((rt_lo + rt) * kBM + q * 32) / 2 + 4 * (lane & 3);
           }
 #define SSQA_EPI(B, S, F)                                                                  \
-  epi_chunks<B, S, F, F4>(er, uc, fc, i2d, ctl, acc_ring, c_col, q_sum, trow, \
+  epi_chunks<B, S, F, F4>(er, uc, fc, tc, i2d, ctl, acc_ring, c_col, q_sum, trow, \
                           sub, kSubs, nchunk, nps, cnt0, il, lane)
           if (fast && sig_from_acc) {
             if (bidir) SSQA_EPI(true, true, true);
@@ -1247,7 +1496,8 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
         __syncwarp();
         if (warp == 0) DBG_STAMP(2, acc_it, 1);
         if (lane == 0) {
-          mbar_arrive(&ctl->tempty[buf]);
+          if (CTA2 && !leader) mbar_arrive_cluster(mapa_rank(smem_u32(&ctl->tempty[buf]), 0));
+          else mbar_arrive(&ctl->tempty[buf]);
           mbar_arrive(&ctl->sempty[buf]);
           mbar_arrive(&ctl->rready[rt / rgroup]);
         }
@@ -1425,6 +1675,7 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
     tc_fence_before();
     __syncwarp();
     if (lane == 0) mbar_arrive(&ctl->done);
+    if (CTA2) cluster_sync_all();
   }
   // No code after the role branches: each role runs to the end on its own
   // register budget (the MMA warp releases TMEM once the epilogue is done).
@@ -1471,26 +1722,27 @@ bool make_map(CUtensorMap* m, void* base, CUtensorMapDataType dt, uint32_t esize
 // >= 2 ring slots per subgroup (so the loader runs a chunk ahead), then as
 // many operand stages (<= 4) as fit.
 // FP4 pair stages are half as deep in K (and in bytes): up to 6 of them.
-Layout pick_layout(int NT, int tpt, int nsubs, int tile_row, int b_row) {
+Layout pick_layout(int NT, int tpt, int nsubs, int tile_row, int b_row, int b_cols,
+                   int tab_bytes) {
   const uint32_t cap = 226 * 1024;  // of 227 KB dynamic shared memory per CTA
   const int max_stages = b_row < kBK ? 6 : 4;
   if (b_row < kBK)  // operand-feed-bound shapes: deep operand pipeline first
     for (int stages = max_stages; stages >= 4; --stages)
       for (int nps = 3; nps >= 1; --nps) {
         if (nps * nsubs > 16) continue;
-        Layout L = make_layout(NT, tpt, stages, nps * nsubs, tile_row, b_row);
+        Layout L = make_layout(NT, tpt, stages, nps * nsubs, tile_row, b_row, b_cols, tab_bytes);
         if (L.total <= cap) return L;
       }
   for (int nps = 3; nps >= 1; --nps)
     for (int stages = max_stages; stages >= 2; --stages) {
       if (nps * nsubs > 16) continue;
-      Layout L = make_layout(NT, tpt, stages, nps * nsubs, tile_row, b_row);
+      Layout L = make_layout(NT, tpt, stages, nps * nsubs, tile_row, b_row, b_cols, tab_bytes);
       if (L.total <= cap && (nps >= 2 || stages >= 2)) {
         if (nps >= 2 && stages < 3) continue;  // rather fewer slots than < 3 stages
         return L;
       }
     }
-  return make_layout(NT, tpt, 2, nsubs, tile_row, b_row);
+  return make_layout(NT, tpt, 2, nsubs, tile_row, b_row, b_cols, tab_bytes);
 }
 
 // 16 epilogue warps (4 per scheduler): the update chain is latency-bound,
@@ -1500,11 +1752,40 @@ constexpr int kDefaultEpi = 16;
 template <int EPI, bool F4>
 cudaError_t launch_variant(int grid, int smem, cudaStream_t st, const CUtensorMap* maps,
                            const TcParams& P) {
-  cudaError_t e = cudaFuncSetAttribute(k_sweep_tc<EPI, F4>,
+  cudaError_t e = cudaFuncSetAttribute(k_sweep_tc<EPI, F4, false>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  k_sweep_tc<EPI, F4><<<grid, 32 * (4 + EPI), smem, st>>>(maps[0], maps[1], maps[2], maps[3], P);
+  k_sweep_tc<EPI, F4, false><<<grid, 32 * (4 + EPI), smem, st>>>(maps[0], maps[1], maps[2],
+                                                                   maps[3], P);
   return cudaSuccess;
+}
+
+// CTA-pair variant: clusters of 2.  Every CTA must be resident at once (the
+// row split synchronises across CTAs), so the launch is refused
+// (cudaErrorNotSupported) unless grid/2 clusters fit on the device.
+template <bool F4>
+cudaError_t launch_variant_pair(int grid, int smem, cudaStream_t st, const CUtensorMap* maps,
+                                const TcParams& P) {
+  auto kern = k_sweep_tc<16, F4, true>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(unsigned(grid));
+  cfg.blockDim = dim3(32 * (4 + 16));
+  cfg.dynamicSmemBytes = size_t(smem);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int clusters = 0;
+  e = cudaOccupancyMaxActiveClusters(&clusters, kern, &cfg);
+  if (e != cudaSuccess) return e;
+  if (2 * clusters < grid) return cudaErrorNotSupported;
+  return cudaLaunchKernelEx(&cfg, kern, maps[0], maps[1], maps[2], maps[3], P);
 }
 
 // int8 spin slot -> FP4 (e2m1) slot: +1 -> 0x2, -1 -> 0xA, 0 -> 0x0.
@@ -1589,15 +1870,34 @@ int launch(ssqa_batch_s* b, TcParams& P, bool f4) {
   }
   const char* env_epi = getenv("SSQA_TC_EPI");
   const int epi = env_epi ? (atoi(env_epi) == 12 ? 12 : 16) : kDefaultEpi;
-  Layout L = pick_layout(g.tile_cols, g.tpt, epi / 4, int(tile_row), int(b_row));
-  if (const char* st = getenv("SSQA_TC_STAGES")) {  // experiment overrides
-    const char* np = getenv("SSQA_TC_NPS");
-    L = make_layout(g.tile_cols, g.tpt, atoi(st), (np ? atoi(np) : 1) * (epi / 4), int(tile_row),
-                    int(b_row));
+  // CTA pairs (M = 256 MMAs, each CTA streams half of the spin columns): the
+  // fused run's row split with an even number of parts per column tile and
+  // of row tiles; SSQA_TC_CTA2=0 turns them off
+  bool cta2 = P.run_mode == 1 && g.rs > 1 && g.rs % 2 == 0 && (g.npad / kBM) % 2 == 0 &&
+              epi == 16;
+  if (const char* e2 = getenv("SSQA_TC_CTA2")) cta2 = cta2 && atoi(e2) != 0;
+  Layout L;
+  auto setup = [&](bool pairs) {
+    const int b_cols = pairs ? g.tile_cols / 2 : g.tile_cols;
+    if (!make_map(&maps[1], Ssrc, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, row_bytes, srows, b_row,
+                  uint32_t(b_cols), pair ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B))
+      return false;
+    const int tab_bytes = P.fast ? (P.bidirectional ? 4 : 2) * P.tab_w * 8 : 0;
+    L = pick_layout(g.tile_cols, g.tpt, epi / 4, int(tile_row), int(b_row), b_cols, tab_bytes);
+    if (const char* st = getenv("SSQA_TC_STAGES")) {  // experiment overrides
+      const char* np = getenv("SSQA_TC_NPS");
+      L = make_layout(g.tile_cols, g.tpt, atoi(st), (np ? atoi(np) : 1) * (epi / 4),
+                      int(tile_row), int(b_row), b_cols, tab_bytes);
+    }
+    P.stages = L.stages;
+    P.nslot = L.nslot;
+    return true;
+  };
+  if (!setup(cta2)) {
+    g_tc_err = "cuTensorMapEncodeTiled failed";
+    return SSQA_ECUDA;
   }
-  P.stages = L.stages;
-  P.nslot = L.nslot;
-  const int smem = int(L.total);
+  int smem = int(L.total);
   const char* trace_path = getenv("SSQA_TC_TRACE");
   long long* dbg = nullptr;
   const int dbg_rts = 4096;
@@ -1611,7 +1911,18 @@ int launch(ssqa_batch_s* b, TcParams& P, bool f4) {
   // one persistent CTA per (column tile, row part); every CTA must be
   // resident (the row split synchronises across CTAs): grid <= SM count
   const int grid = g.ntiles * g.rs;
-  if (epi == 16)
+  if (cta2) {
+    e = f4 ? launch_variant_pair<true>(grid, smem, b->prob->stream, maps, P)
+           : launch_variant_pair<false>(grid, smem, b->prob->stream, maps, P);
+    if (e == cudaErrorNotSupported) {  // the pairs do not all fit at once: single CTAs
+      cudaGetLastError();
+      cta2 = false;
+      setup(false);
+      smem = int(L.total);
+    }
+  }
+  if (cta2) {
+  } else if (epi == 16)
     e = f4 ? launch_variant<16, true>(grid, smem, b->prob->stream, maps, P)
            : launch_variant<16, false>(grid, smem, b->prob->stream, maps, P);
   else
@@ -1636,10 +1947,13 @@ int launch(ssqa_batch_s* b, TcParams& P, bool f4) {
   return SSQA_OK;
 }
 
-// The fast epilogue (update_fast2) is exact when every parameter is finite
-// (so no accumulator is ever NaN or -0.0), n_rnd * 2^p is a small integer and
-// the per-quarter int32 energy partials cannot overflow.
-bool fast_ok(const ssqa_batch_s* b, int* nr) {
+// The fast (table) epilogue is exact when every parameter is finite (so no
+// accumulator is ever NaN or -0.0), i0 > 0, n_rnd * 2^p is a small integer,
+// the per-quarter int32 energy partials cannot overflow and the table of the
+// undecided fields fits (TabConsts): fields X 2^-p >= B = i0 + 2 |jperp| +
+// max |acc| + 1 clamp high whatever the rest, X 2^-p <= -B clamp low.
+constexpr int kTabMaxW = 255;
+bool fast_ok(const ssqa_batch_s* b, TcParams* P) {
   const ssqa_params_c& p = b->p;
   const Quantized& q = b->prob->q;
   for (double v : {p.n_rnd, p.i0, p.alpha, p.jperp_min, p.jperp_max, p.i0 - p.alpha})
@@ -1651,7 +1965,28 @@ bool fast_ok(const ssqa_batch_s* b, int* nr) {
   const double row_max = double(q.max_abs_j) * q.n + 2.0 * q.max_abs_h;
   if (row_max + std::fabs(x) >= double(1u << 30)) return false;
   if (double(q.npad) / 4.0 * row_max >= 2147483647.0) return false;
-  *nr = int(x);
+  // run-wide bounds: the largest i0, |accumulator| and |jperp| of any cycle
+  double i0max = p.i0, accmax = std::max(p.i0, std::fabs(p.i0 - p.alpha)), jpmax = 0.0;
+  if (b->ssa) {
+    i0max = 0.0;
+    for (double v : b->ssa_levels) {
+      i0max = std::max(i0max, v);
+      accmax = std::max(accmax, std::max(v, std::fabs(v - p.alpha)));
+    }
+  } else {
+    jpmax = std::max(std::fabs(p.jperp_min), std::fabs(p.jperp_max));
+  }
+  if (!(i0max > 0.0)) return false;
+  for (double v : b->ssa_levels)
+    if (!(v > 0.0)) return false;
+  const double bound = std::ldexp(i0max + 2.0 * jpmax + accmax + 1.0, q.p);
+  if (!(bound < double(kTabMaxW))) return false;
+  const int thi = int(std::ceil(bound));
+  if (2 * thi - 1 > kTabMaxW) return false;
+  P->nr = int(x);
+  P->tab_hi = thi;
+  P->tab_lo1 = 1 - thi;
+  P->tab_w = 2 * thi - 1;
   return true;
 }
 
@@ -1679,7 +2014,7 @@ TcParams base_params(ssqa_batch_s* b) {
   P.bidirectional = b->p.bidirectional;
   P.hi_clamp = b->p.i0 - b->p.alpha;
   P.lo_clamp = -b->p.i0;
-  P.fast = fast_ok(b, &P.nr) ? 1 : 0;
+  P.fast = fast_ok(b, &P) ? 1 : 0;
   if (const char* ex = getenv("SSQA_TC_EXP")) P.exp_flags = atoi(ex);
   P.ring_cur = b->cur;
   for (int q = 0; q <= b->d; ++q) P.ring_phys[q] = b->phys[size_t(q)];

@@ -499,10 +499,20 @@ def row_split(monkeypatch):
     return force
 
 
+@pytest.fixture(params=["pairs", "single"])
+def cta_pairs(request, monkeypatch):
+    """Even row splits run as CTA pairs (cta_group::2, M = 256) unless off."""
+    if request.param == "single":
+        monkeypatch.setenv("SSQA_TC_CTA2", "0")
+    return request.param
+
+
 @pytest.mark.parametrize("rs", [2, 3, 4])
-def test_row_split_runs_match_oracle(orc, row_split, rs, operands):
+def test_row_split_runs_match_oracle(orc, row_split, rs, operands, cta_pairs):
     if not engine_ok(_lib.ENGINE_TCGEN05):
         pytest.skip("tcgen05 engine unavailable")
+    if rs == 3 and cta_pairs == "pairs":
+        pytest.skip("odd splits never pair")
     row_split(rs)
     cases = [(sq.gi_ising(20, 0.5, 7, True, 1.0, 1.0), params(20, 60), [41, 42, 43, 44, 45, 46]),
              (sq.dense_ising(400, 0, 5), params(6, 30, tau=4, bidirectional=True), [7, 8, 9])]
