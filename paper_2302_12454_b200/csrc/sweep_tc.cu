@@ -96,6 +96,7 @@ struct TcParams {
   // fl(fl(X 2^-p + jperp u) [+ jperp d]) from a per-cycle smem table of tab_w
   // entries per neighbour-sign combination
   int tab_lo1, tab_hi, tab_w;
+  int pf_dist;  // J' L2 prefetch distance in K chunks (0: off)
   long long* dbg;  // optional timeline (block 0): [role][rt_global][2] clock64 stamps
   int dbg_rts;     // capacity in row tiles
   // per-trial results
@@ -233,6 +234,15 @@ __device__ __forceinline__ void tma_load_2d_hint(const CUtensorMap* map, uint64_
       ".L2::cache_hint [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(x), "r"(y), "l"(policy)
       : "memory");
+}
+
+// L2 prefetch of a tensor tile (no smem, no barrier): pulls the J' rows a few
+// stages ahead of the TMA loads, so those hit L2 when J' streams from HBM.
+__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* map, int x, int y) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(x), "r"(y)
+               : "memory");
 }
 
 __device__ __forceinline__ uint64_t policy_evict_first() {
@@ -638,6 +648,7 @@ struct EpiRow {
   int h1, h2;
   uint32_t nib_shift;       // FP4: 4 * (i & 1)
   uint64_t iG;              // i * golden
+  uint32_t iG_lo, iG_hi;    // the same, pinned in registers (opaque to rematerialisation)
   uint64_t pol_stream;      // L2 evict_first policy for the accumulator stream
   bool w_row;               // spin row exists (i < n)
   uint8_t* dst_w;           // FP4 word stores: byte of rows (warp row 0) + 8*(lane&3)
@@ -663,6 +674,16 @@ struct TabConsts {
   long long loc_bits;
   const double* ytab;
 };
+
+// a + (hi:lo) as one add / add-with-carry pair
+__device__ __forceinline__ uint64_t add64_pair(uint64_t a, uint32_t lo, uint32_t hi) {
+  uint64_t r;
+  asm("{\n\t.reg .u32 l, h;\n\tmov.b64 {l, h}, %1;\n\tadd.cc.u32 l, l, %2;\n\t"
+      "addc.u32 h, h, %3;\n\tmov.b64 %0, {l, h};\n\t}"
+      : "=l"(r)
+      : "l"(a), "r"(lo), "r"(hi));
+  return r;
+}
 
 // Spread the 8 bits of b to bit 4k+3 of a word of e2m1 +-1 nibbles (0x2 / 0xA).
 __device__ __forceinline__ uint32_t nibbles_pm1(uint32_t b) {
@@ -715,17 +736,19 @@ __device__ __forceinline__ void epi_chunks(const EpiRow& er, const UpdateConsts&
     if (FAST) {
       // table epilogue (TabConsts); pass 1: integer fields, energies, table positions
       int X[kCW];
+      double ao[kCW];
       uint32_t cmb = 0, midm = 0;
 #pragma unroll
       for (int j = 0; j < kCW; ++j) {
         const uint4 ct = lds128(c_col + cb + j);
         const uint64_t cbase = (uint64_t(ct.y) << 32) | ct.x;
         const double a_old = ab[j * kBM];
+        ao[j] = a_old;
         const int S = F4 ? __float_as_int(__int_as_float(v[j]) + 12582912.0f) : v[j];
         const int s2 = S + er.h2;
         if (SIGACC) {
-          const int m = __double2hiint(a_old) >> 31;
-          ep[j] = (s2 ^ m) - m;
+          // sign of a finite, never -0.0 accumulator: s2 * (+-1) on the FMA pipe
+          ep[j] = s2 * ((__double2hiint(a_old) >> 30) | 1);
         } else {
           int sg;
           if (F4) {
@@ -744,8 +767,8 @@ __device__ __forceinline__ void epi_chunks(const EpiRow& er, const UpdateConsts&
           neg_up = uint32_t(int8_t(er.st_i[ct.w & 0xffffu])) >> 31;
           if (BIDIR) neg_dn = uint32_t(int8_t(er.st_i[(ct.w >> 16) & 0x7fffu])) >> 31;
         }
-        const uint32_t top = (SSQA_ABL & 512) ? uint32_t(cbase) ^ uint32_t(er.iG)
-                                              : mix64_top32_pre(cbase + er.iG);
+        const uint32_t top = (SSQA_ABL & 512) ? uint32_t(cbase) ^ er.iG_lo
+                                              : mix64_top32_pre(add64_pair(cbase, er.iG_lo, er.iG_hi));
         const int nzi = top < 0x70000000u ? 0 : (top < 0xB8000000u ? -fc.nr : fc.nr);
         X[j] = S + er.h1 + nzi;
         cmb |= (neg_up | (neg_dn << 1)) << (2 * j);
@@ -761,7 +784,7 @@ __device__ __forceinline__ void epi_chunks(const EpiRow& er, const UpdateConsts&
         if (any_mid) {
           const bool mid = (midm >> j) & 1u;
           const int e = int((cmb >> (2 * j)) & 3u) * tc.w + (mid ? X[j] - tc.lo1 : 0);
-          const double sd = __dadd_rn(ab[j * kBM], tc.ytab[e]);
+          const double sd = __dadd_rn(ao[j], tc.ytab[e]);
           const long long sb = __double_as_longlong(sd);
           const bool ge = sb >= tc.i0_bits;
           const bool lt = static_cast<unsigned long long>(sb) > tc.lo_bits;
@@ -1185,6 +1208,13 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
             }
             const int st = it % stages;
             const uint32_t ph = (it / stages) & 1;
+            if (P.pf_dist > 0) {
+              // J' tile pf_dist chunks ahead (the next row tile's first chunks
+              // near the end of this one)
+              int pk = kc + P.pf_dist, prt = rt;
+              if (pk >= NKC) pk -= NKC, ++prt;
+              if (prt < NRT) tma_prefetch_2d(&tmJ, pk * kBK, j_row0 + (rt_lo + prt) * kBM);
+            }
             mbar_wait(&ctl->empty[st], ph ^ 1);
             if (P.exp_flags & 4) {
               if (!CTA2 || leader) mbar_arrive(&ctl->full[st]);
@@ -1463,6 +1493,8 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
           er.h1 = F4 ? h1 - 0x4B400000 : h1;
           er.h2 = F4 ? h2 - 0x4B400000 : h2;
           er.iG = uint64_t(i) * kGolden;
+          asm volatile("mov.b32 %0, %1;" : "=r"(er.iG_lo) : "r"(uint32_t(er.iG)));
+          asm volatile("mov.b32 %0, %1;" : "=r"(er.iG_hi) : "r"(uint32_t(er.iG >> 32)));
           er.pol_stream = pol_first;
           er.w_row = row_live;
           {
@@ -1721,12 +1753,14 @@ bool make_map(CUtensorMap* m, void* base, CUtensorMapDataType dt, uint32_t esize
 // Operand stages and per-subgroup state-ring depth inside ~220 KB: prefer
 // >= 2 ring slots per subgroup (so the loader runs a chunk ahead), then as
 // many operand stages (<= 4) as fit.
-// FP4 pair stages are half as deep in K (and in bytes): up to 6 of them.
+// deep: operand-feed-bound shapes (row splits, FP4 pairs) -- as many operand
+// stages as fit (up to 8: the bytes in flight set the J' / spin stream
+// rate), then accumulator-ring slots.
 Layout pick_layout(int NT, int tpt, int nsubs, int tile_row, int b_row, int b_cols,
-                   int tab_bytes) {
+                   int tab_bytes, bool deep) {
   const uint32_t cap = 226 * 1024;  // of 227 KB dynamic shared memory per CTA
-  const int max_stages = b_row < kBK ? 6 : 4;
-  if (b_row < kBK)  // operand-feed-bound shapes: deep operand pipeline first
+  const int max_stages = deep ? 8 : 4;
+  if (deep)
     for (int stages = max_stages; stages >= 4; --stages)
       for (int nps = 3; nps >= 1; --nps) {
         if (nps * nsubs > 16) continue;
@@ -1883,7 +1917,8 @@ int launch(ssqa_batch_s* b, TcParams& P, bool f4) {
                   uint32_t(b_cols), pair ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B))
       return false;
     const int tab_bytes = P.fast ? (P.bidirectional ? 4 : 2) * P.tab_w * 8 : 0;
-    L = pick_layout(g.tile_cols, g.tpt, epi / 4, int(tile_row), int(b_row), b_cols, tab_bytes);
+    L = pick_layout(g.tile_cols, g.tpt, epi / 4, int(tile_row), int(b_row), b_cols, tab_bytes,
+                    pair || g.rs > 1);
     if (const char* st = getenv("SSQA_TC_STAGES")) {  // experiment overrides
       const char* np = getenv("SSQA_TC_NPS");
       L = make_layout(g.tile_cols, g.tpt, atoi(st), (np ? atoi(np) : 1) * (epi / 4),
@@ -2016,6 +2051,8 @@ TcParams base_params(ssqa_batch_s* b) {
   P.lo_clamp = -b->p.i0;
   P.fast = fast_ok(b, &P) ? 1 : 0;
   if (const char* ex = getenv("SSQA_TC_EXP")) P.exp_flags = atoi(ex);
+  P.pf_dist = 0;  // measured: prefetching J' rows costs more L2 bandwidth than it saves (C4, C5)
+  if (const char* pf = getenv("SSQA_TC_PF")) P.pf_dist = atoi(pf);
   P.ring_cur = b->cur;
   for (int q = 0; q <= b->d; ++q) P.ring_phys[q] = b->phys[size_t(q)];
   P.best_e = b->d_best_e;
