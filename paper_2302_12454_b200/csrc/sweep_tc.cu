@@ -1307,11 +1307,16 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
                    "r"(ncols));
     }
   } else if (warp == kWarpLoader) {
-    // ===== state loader: delayed-spin tile + accumulator chunks =====
+    // ===== state loader: delayed-spin tile + accumulator chunks.  Lane sb
+    // feeds epilogue subgroup sb's accumulator ring on its own, so one slow
+    // subgroup never holds back the others' loads; lane 0 also loads the
+    // delayed-spin tiles and keeps the slot ring. =====
     SSQA_CTL_REGS();
-    if (lane == 0) {
+    if (lane < nsubs) {
+      const int sb2 = lane;
       int* ring = ctl->ring[1];
       const uint64_t pol_first = policy_evict_first();
+      const uint32_t my_chunks = uint32_t(chunks_of(sb2));
       for (long c = P.c_first; c <= P.c_last; ++c) {
         const long s = c - P.c_first;
         int waited = 0;
@@ -1326,20 +1331,21 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
           // were written by pass c-1
           if (s > 0)
             while (waited <= rt / rgroup) rows_wait(s - 1, waited++);
-          const int sb = acc_it & 1;
-          const uint32_t sph = (acc_it >> 1) & 1;
-          mbar_wait(&ctl->sempty[sb], sph ^ 1);
-          DBG_STAMP(1, acc_it, 0);
-          mbar_expect_tx(&ctl->sfull[sb], uint32_t(NT) * kTileRow);
-          tma_load_2d(&tmSe, &ctl->sfull[sb], sig_tiles + size_t(sb) * NT * kTileRow,
-                      (rt_lo + rt) * kTileRow, ySrc);
+          if (sb2 == 0) {
+            const int sb = acc_it & 1;
+            const uint32_t sph = (acc_it >> 1) & 1;
+            mbar_wait(&ctl->sempty[sb], sph ^ 1);
+            DBG_STAMP(1, acc_it, 0);
+            mbar_expect_tx(&ctl->sfull[sb], uint32_t(NT) * kTileRow);
+            tma_load_2d(&tmSe, &ctl->sfull[sb], sig_tiles + size_t(sb) * NT * kTileRow,
+                        (rt_lo + rt) * kTileRow, ySrc);
+          }
           // chunk ch belongs to epilogue subgroup ch % nsubs and lands in that
           // subgroup's own ring (slots [sub*nps, sub*nps + nps)): each slot is
           // consumed, in order, by a single subgroup, so no consumer can ever
           // wait on a slot barrier two phases ahead (parity aliasing).
-          for (int ch = 0; ch < nchunk && !(SSQA_ABL & 128); ++ch) {
-            const int sb2 = ch % nsubs;
-            const uint32_t cnt = acc_it * uint32_t(chunks_of(sb2)) + uint32_t(ch / nsubs);
+          for (int ch = sb2; ch < nchunk && !(SSQA_ABL & 128); ch += nsubs) {
+            const uint32_t cnt = acc_it * my_chunks + uint32_t(ch / nsubs);
             const int slot = sb2 * nps + int(cnt % uint32_t(nps));
             const uint32_t ph = (cnt / uint32_t(nps)) & 1;
             mbar_wait(&ctl->aempty[slot], ph ^ 1);
@@ -1347,9 +1353,12 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
             tma_load_2d_hint(&tmA, &ctl->afull[slot], acc_ring + size_t(slot) * kCW * kBM,
                              (rt_lo + rt) * kBM, col0 + ch * kCW, pol_first);
           }
-          DBG_STAMP(1, acc_it, 1);
+          if (sb2 == 0) DBG_STAMP(1, acc_it, 1);
         }
-        if (c < P.sc) ring_advance(ring, c, P.d, P.nslots);
+        // every lane has read this cycle's ring entry before lane 0 moves it
+        __syncwarp((1u << nsubs) - 1u);
+        if (sb2 == 0 && c < P.sc) ring_advance(ring, c, P.d, P.nslots);
+        __syncwarp((1u << nsubs) - 1u);
       }
     }
     __syncwarp();
@@ -1750,9 +1759,9 @@ bool make_map(CUtensorMap* m, void* base, CUtensorMapDataType dt, uint32_t esize
   return r == CUDA_SUCCESS;
 }
 
-// Operand stages and per-subgroup state-ring depth inside ~220 KB: prefer
-// >= 2 ring slots per subgroup (so the loader runs a chunk ahead), then as
-// many operand stages (<= 4) as fit.
+// Operand stages and per-subgroup state-ring depth inside ~226 KB: prefer
+// deep accumulator rings (up to 3 slots per subgroup, so the loader runs
+// chunks ahead of the HBM latency), then as many operand stages (<= 4) as fit.
 // deep: operand-feed-bound shapes (row splits, FP4 pairs) -- as many operand
 // stages as fit (up to 8: the bytes in flight set the J' / spin stream
 // rate), then accumulator-ring slots.
@@ -1771,10 +1780,9 @@ Layout pick_layout(int NT, int tpt, int nsubs, int tile_row, int b_row, int b_co
     for (int stages = max_stages; stages >= 2; --stages) {
       if (nps * nsubs > 16) continue;
       Layout L = make_layout(NT, tpt, stages, nps * nsubs, tile_row, b_row, b_cols, tab_bytes);
-      if (L.total <= cap && (nps >= 2 || stages >= 2)) {
-        if (nps >= 2 && stages < 3) continue;  // rather fewer slots than < 3 stages
-        return L;
-      }
+      // the epilogue-bound shapes want the accumulator stream deep (C3: 3 ring
+      // slots per subgroup and 2 operand stages 218 us/sweep, 2 and 3: 222)
+      if (L.total <= cap) return L;
     }
   return make_layout(NT, tpt, 2, nsubs, tile_row, b_row, b_cols, tab_bytes);
 }
