@@ -97,6 +97,7 @@ struct TcParams {
   // entries per neighbour-sign combination
   int tab_lo1, tab_hi, tab_w;
   int pf_dist;  // J' L2 prefetch distance in K chunks (0: off)
+  int use_tab;  // fast mode: table epilogue (row splits) instead of update_fast2
   long long* dbg;  // optional timeline (block 0): [role][rt_global][2] clock64 stamps
   int dbg_rts;     // capacity in row tiles
   // per-trial results
@@ -701,7 +702,7 @@ __device__ __forceinline__ uint32_t nibbles_pm1(uint32_t b) {
 //   SIGACC  sigma(c) = sign(acc(c)) instead of a load (all but the first sweep)
 //   FAST    host-checked table epilogue (TabConsts), int32 energy partials
 //   F4      FP4 operands: fp32 fields in TMEM, spins stored as e2m1 nibbles
-template <bool BIDIR, bool SIGACC, bool FAST, bool F4>
+template <bool BIDIR, bool SIGACC, bool FAST, bool F4, bool TAB>
 __device__ __forceinline__ void epi_chunks(const EpiRow& er, const UpdateConsts& uc,
                                            const FastConsts& fc, const TabConsts& tc,
                                            const I2D& i2d, SmemCtl* ctl,
@@ -733,7 +734,7 @@ __device__ __forceinline__ void epi_chunks(const EpiRow& er, const UpdateConsts&
     const double* ab = acc_ring + size_t(slot) * kCW * kBM + il;
     int ep[kCW];
     uint32_t ball[kCW];
-    if (FAST) {
+    if (FAST && TAB) {
       // table epilogue (TabConsts); pass 1: integer fields, energies, table positions
       int X[kCW];
       double ao[kCW];
@@ -806,6 +807,58 @@ __device__ __forceinline__ void epi_chunks(const EpiRow& er, const UpdateConsts&
                    w && !(lane & 1));
         } else {
           st_s8_if(reinterpret_cast<int8_t*>(er.dst_i + uint64_t(cw.x)), int(1 - 2 * int(neg)), w);
+        }
+      }
+    } else if (FAST) {
+      // FP64 epilogue (update_fast2): fewer instructions than the table path,
+      // best where the MMAs leave the FP64 units mostly free (no row split)
+#pragma unroll
+      for (int j = 0; j < kCW; ++j) {
+        const uint4 ct = lds128(c_col + cb + j);
+        const uint64_t cbase = (uint64_t(ct.y) << 32) | ct.x;
+        const uint32_t coff = ct.z;
+        const uint32_t nb = ct.w;
+        const double a_old = ab[j * kBM];
+        const int S = F4 ? __float_as_int(__int_as_float(v[j]) + 12582912.0f) : v[j];
+        const int s2 = S + er.h2;
+        if (SIGACC) {
+          ep[j] = s2 * ((__double2hiint(a_old) >> 30) | 1);
+        } else {
+          int sg;
+          if (F4) {
+            const uint32_t bc = ld_u8(reinterpret_cast<const uint8_t*>(er.cur_i + (coff >> 1)));
+            sg = ((bc >> er.nib_shift) & 8u) ? -1 : 1;
+          } else {
+            sg = ld_s8(reinterpret_cast<const int8_t*>(er.cur_i + coff));
+          }
+          ep[j] = sg * s2;
+        }
+        int up, dn = 0;
+        if (F4) {
+          // update_fast2 only reads the sign bit: move the nibble's bit 3 there
+          up = int(uint32_t(er.st_i[nb & 0xffffu]) << (28u - er.nib_shift));
+          if (BIDIR) dn = int(uint32_t(er.st_i[(nb >> 16) & 0x7fffu]) << (28u - er.nib_shift));
+        } else {
+          up = int8_t(er.st_i[nb & 0xffffu]);
+          if (BIDIR) dn = int8_t(er.st_i[(nb >> 16) & 0x7fffu]);
+        }
+        const uint32_t top = (SSQA_ABL & 512) ? uint32_t(cbase) ^ er.iG_lo
+                                              : mix64_top32_pre(add64_pair(cbase, er.iG_lo, er.iG_hi));
+        const double nv = update_fast2<BIDIR>(fc, i2d, S + er.h1, top, up, dn, a_old);
+        const uint32_t neg = uint32_t(__double2hiint(nv)) >> 31;
+        const bool w = (nb & 0x80000000u) && er.w_row;
+        if (!(SSQA_ABL & 64))
+          st_f64_if(reinterpret_cast<double*>(er.acc_i + uint64_t(coff) * 8u), nv, w, er.pol_stream);
+        if (SSQA_ABL & 32) {
+        } else if (kWordSt) {
+          ball[j] = (SSQA_ABL & 2048) ? neg : ballot_neg(neg);
+        } else if (F4) {
+          const uint32_t nib = 2u | (neg << 3);
+          const uint32_t hi = __shfl_xor_sync(0xffffffffu, nib, 1);
+          st_u8_if(reinterpret_cast<uint8_t*>(er.dst_i + (coff >> 1)), nib | (hi << 4),
+                   w && !(lane & 1));
+        } else {
+          st_s8_if(reinterpret_cast<int8_t*>(er.dst_i + uint64_t(coff)), int(1 - 2 * int(neg)), w);
         }
       }
     } else {
@@ -999,7 +1052,7 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
   const bool pair = F4 && P.pair != 0;
   const int b_row = pair ? kBK / 2 : kBK;
   const Layout L = make_layout(NT, g.tpt, P.stages, P.nslot, kTileRow, b_row, CTA2 ? NT / 2 : NT,
-                               P.fast ? (P.bidirectional ? 4 : 2) * P.tab_w * 8 : 0);
+                               P.use_tab ? (P.bidirectional ? 4 : 2) * P.tab_w * 8 : 0);
   const int stages = L.stages, nslot = L.nslot;
   uint8_t* sA = smem;
   uint8_t* sB = smem + size_t(stages) * L.a_bytes;
@@ -1397,7 +1450,7 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
       const bool do_update = c < P.sc;
       const int cur = ring[0];
       const int dst = do_update ? ring_free(cur, ring + 1, P.d, P.nslots) : cur;
-      if (!drain && P.fast) {
+      if (!drain && P.fast && P.use_tab) {
         // this cycle's table of fl(fl(X 2^-p + jperp u) [+ jperp d]) (TabConsts),
         // with the reference's own operations (annealer.cpp:276-284)
         const double jp = P.run_mode ? P.jperp_tab[c] : P.jperp_fixed;
@@ -1512,22 +1565,26 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
             er.nib_live = nl >= 8 ? 0xffffffffu : ((1u << (4 * nl)) - 1u);
             er.dst_w = sig_dst + ((rt_lo + rt) * kBM + q * 32) / 2 + 4 * (lane & 3);
           }
-#define SSQA_EPI(B, S, F)                                                                  \
-  epi_chunks<B, S, F, F4>(er, uc, fc, tc, i2d, ctl, acc_ring, c_col, q_sum, trow, \
-                          sub, kSubs, nchunk, nps, cnt0, il, lane)
+#define SSQA_EPI(B, S, F, T)                                                               \
+  epi_chunks<B, S, F, F4, T>(er, uc, fc, tc, i2d, ctl, acc_ring, c_col, q_sum, trow, \
+                             sub, kSubs, nchunk, nps, cnt0, il, lane)
+#define SSQA_EPI_FAST(B, S)        \
+  if (P.use_tab) SSQA_EPI(B, S, true, true); \
+  else SSQA_EPI(B, S, true, false)
           if (fast && sig_from_acc) {
-            if (bidir) SSQA_EPI(true, true, true);
-            else SSQA_EPI(false, true, true);
+            if (bidir) SSQA_EPI_FAST(true, true);
+            else SSQA_EPI_FAST(false, true);
           } else if (fast) {
-            if (bidir) SSQA_EPI(true, false, true);
-            else SSQA_EPI(false, false, true);
+            if (bidir) SSQA_EPI_FAST(true, false);
+            else SSQA_EPI_FAST(false, false);
           } else if (sig_from_acc) {
-            if (bidir) SSQA_EPI(true, true, false);
-            else SSQA_EPI(false, true, false);
+            if (bidir) SSQA_EPI(true, true, false, false);
+            else SSQA_EPI(false, true, false, false);
           } else {
-            if (bidir) SSQA_EPI(true, false, false);
-            else SSQA_EPI(false, false, false);
+            if (bidir) SSQA_EPI(true, false, false, false);
+            else SSQA_EPI(false, false, false, false);
           }
+#undef SSQA_EPI_FAST
 #undef SSQA_EPI
         }
         tc_fence_before();
@@ -1864,6 +1921,11 @@ void watchdog_bind(int device) {
 int launch(ssqa_batch_s* b, TcParams& P, bool f4) {
   watchdog_bind(b->prob->device);
   const Geom& g = P.g;  // the batch geometry (a shard pass may use its own row split)
+  // Table epilogue for row splits: their MMAs keep the tensor core busy, and
+  // the FP64 units share its issue path; the FP64 epilogue is cheaper where
+  // they are mostly free (C3: 1146 vs 1178 ms/step).  SSQA_TC_TAB=0/1 forces.
+  P.use_tab = (P.fast && P.tab_w > 0 && g.rs > 1) ? 1 : 0;
+  if (const char* t = getenv("SSQA_TC_TAB")) P.use_tab = (P.fast && P.tab_w > 0 && atoi(t)) ? 1 : 0;
   CUtensorMap maps[4];
   const uint64_t srows = uint64_t(b->nslots) * g.ccols;
   // FP4 rows are npad/2 bytes (two e2m1 values per byte)
@@ -1924,7 +1986,7 @@ int launch(ssqa_batch_s* b, TcParams& P, bool f4) {
     if (!make_map(&maps[1], Ssrc, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, row_bytes, srows, b_row,
                   uint32_t(b_cols), pair ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B))
       return false;
-    const int tab_bytes = P.fast ? (P.bidirectional ? 4 : 2) * P.tab_w * 8 : 0;
+    const int tab_bytes = P.use_tab ? (P.bidirectional ? 4 : 2) * P.tab_w * 8 : 0;
     L = pick_layout(g.tile_cols, g.tpt, epi / 4, int(tile_row), int(b_row), b_cols, tab_bytes,
                     pair || g.rs > 1);
     if (const char* st = getenv("SSQA_TC_STAGES")) {  // experiment overrides
@@ -2019,17 +2081,18 @@ bool fast_ok(const ssqa_batch_s* b, TcParams* P) {
   } else {
     jpmax = std::max(std::fabs(p.jperp_min), std::fabs(p.jperp_max));
   }
-  if (!(i0max > 0.0)) return false;
-  for (double v : b->ssa_levels)
-    if (!(v > 0.0)) return false;
-  const double bound = std::ldexp(i0max + 2.0 * jpmax + accmax + 1.0, q.p);
-  if (!(bound < double(kTabMaxW))) return false;
-  const int thi = int(std::ceil(bound));
-  if (2 * thi - 1 > kTabMaxW) return false;
   P->nr = int(x);
-  P->tab_hi = thi;
-  P->tab_lo1 = 1 - thi;
-  P->tab_w = 2 * thi - 1;
+  // table epilogue when i0 > 0 and the undecided band fits (else tab_w = 0)
+  P->tab_w = 0;
+  bool pos = i0max > 0.0;
+  for (double v : b->ssa_levels) pos = pos && v > 0.0;
+  const double bound = std::ldexp(i0max + 2.0 * jpmax + accmax + 1.0, q.p);
+  if (pos && bound < double(kTabMaxW) && 2 * int(std::ceil(bound)) - 1 <= kTabMaxW) {
+    const int thi = int(std::ceil(bound));
+    P->tab_hi = thi;
+    P->tab_lo1 = 1 - thi;
+    P->tab_w = 2 * thi - 1;
+  }
   return true;
 }
 

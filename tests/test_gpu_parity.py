@@ -165,9 +165,20 @@ def test_run_trials_matches_reference_kat(golden, engine):
     assert tts.kind == "finite" and t_mean > 0
 
 
-def test_full_runs_match_oracle_many_trials(orc, engine):
+@pytest.fixture(params=["auto", "table", "fp64"])
+def epilogue(request, monkeypatch):
+    """tcgen05 fast epilogue: the engine's choice, the table path (integer
+    clamps + per-cycle smem table) or the FP64 path (update_fast2)."""
+    if request.param != "auto":
+        monkeypatch.setenv("SSQA_TC_TAB", "1" if request.param == "table" else "0")
+    return request.param
+
+
+def test_full_runs_match_oracle_many_trials(orc, engine, epilogue):
     """A 48-trial batch at N=100 and N=400 (C1/C2 shapes, shortened): every
     trial equals the oracle's ssqa_run."""
+    if epilogue != "auto" and engine != _lib.ENGINE_TCGEN05:
+        pytest.skip("epilogue variants apply to tcgen05 only")
     for nn, R, sc, T in [(10, 20, 300, 48), (20, 20, 60, 6)]:
         m = sq.gi_ising(nn, 0.5, 7, True, 1.0, 1.0)
         p = params(R, sc)
@@ -508,11 +519,13 @@ def cta_pairs(request, monkeypatch):
 
 
 @pytest.mark.parametrize("rs", [2, 3, 4])
-def test_row_split_runs_match_oracle(orc, row_split, rs, operands, cta_pairs):
+def test_row_split_runs_match_oracle(orc, row_split, rs, operands, cta_pairs, epilogue):
     if not engine_ok(_lib.ENGINE_TCGEN05):
         pytest.skip("tcgen05 engine unavailable")
     if rs == 3 and cta_pairs == "pairs":
         pytest.skip("odd splits never pair")
+    if epilogue == "table" or (epilogue == "fp64" and (operands, cta_pairs) != ("auto", "pairs")):
+        pytest.skip("row splits default to the table epilogue; FP64 checked once")
     row_split(rs)
     cases = [(sq.gi_ising(20, 0.5, 7, True, 1.0, 1.0), params(20, 60), [41, 42, 43, 44, 45, 46]),
              (sq.dense_ising(400, 0, 5), params(6, 30, tau=4, bidirectional=True), [7, 8, 9])]
