@@ -84,6 +84,11 @@ class ClockSampler:
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            # nvidia-smi needs ~0.1-0.5 s to start: wait for its first sample so a
+            # short timed region (C1: ~20 ms) still sits between samples
+            t0 = time.time()
+            while not self.rows and time.time() - t0 < 3.0:
+                time.sleep(0.01)
         except (OSError, FileNotFoundError):
             self.proc = None
 

@@ -76,7 +76,8 @@ struct TcParams {
   int bidirectional;
   int fast, nr;                 // fast epilogue (host-checked) and n_rnd * 2^p
   int exp_flags;                // ablation experiments (SSQA_TC_EXP): 1 no epilogue math, 2 no MMA,
-                                // 4 no operand TMA (MMAs on stale stages)
+                                // 4 no operand TMA (MMAs on stale stages), 8 no J'
+                                // loads, 16 no spin loads (single CTAs only)
   double hi_clamp, lo_clamp;    // i0 - alpha, -i0 (formed on the host)
   long c_first, c_last;  // cycles handled: scans/updates for c in [c_first, c_last]
   long sc;               // update iff c < sc
@@ -98,6 +99,7 @@ struct TcParams {
   int tab_lo1, tab_hi, tab_w;
   int pf_dist;  // J' L2 prefetch distance in K chunks (0: off)
   int use_tab;  // fast mode: table epilogue (row splits) instead of update_fast2
+  int mc_q;     // CL == 2: column tiles per cluster (= ntiles), sharing each J' tile
   long long* dbg;  // optional timeline (block 0): [role][rt_global][2] clock64 stamps
   int dbg_rts;     // capacity in row tiles
   // per-trial results
@@ -373,6 +375,27 @@ __device__ __forceinline__ void mma_commit_w(uint64_t* bar) {
         "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(
             smem_u32(bar))
         : "memory");
+}
+
+// J' tile multicast to the CTAs of `mask` (same smem offset and barrier in each)
+__device__ __forceinline__ void tma_load_2d_mc(const CUtensorMap* map, uint64_t* bar, void* dst,
+                                               int x, int y, uint16_t mask, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      ".multicast::cluster.L2::cache_hint [%0], [%1, {%4, %5}], [%2], %3, %6;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "h"(mask), "r"(x), "r"(y),
+      "l"(policy)
+      : "memory");
+}
+
+// Commit arriving on the barrier at the same offset in every CTA of `mask`.
+__device__ __forceinline__ void mma_commit_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;\n\t}" ::"r"(smem_u32(bar)),
+      "h"(mask)
+      : "memory");
 }
 
 __device__ __forceinline__ uint32_t cluster_rank() {
@@ -1034,12 +1057,15 @@ static_assert((16 * EpiRegs<16>::value + 4 * kCtlRegs) * 32 <= 20 * 32 * 96, "EP
 // Warp roles: 0 .. EPI-1 epilogue (EPI/4 warps per TMEM lane quarter),
 // EPI operand TMA producer, EPI+1 TMEM allocator + MMA issuer, EPI+2 state
 // loader (TMA of accumulator chunks and delayed-spin tiles).
-// CTA2: row-split CTA pairs (clusters of 2) sharing M = 256 MMAs.
-template <int EPI, bool F4, bool CTA2>
+// CL: cluster mode -- 0 none; 1 CTA pairs (clusters of 2 row parts sharing
+// M = 256 MMAs); 2 J' multicast (clusters of the column tiles of one row part:
+// the leader loads each J' tile once and multicasts it to every CTA).
+template <int EPI, bool F4, int CL>
 __global__ void __launch_bounds__(32 * (4 + EPI), 1)
     k_sweep_tc(const __grid_constant__ CUtensorMap tmJ, const __grid_constant__ CUtensorMap tmS,
                const __grid_constant__ CUtensorMap tmSe, const __grid_constant__ CUtensorMap tmA,
                const TcParams P) {
+  constexpr bool CTA2 = CL == 1, MC = CL == 2;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-align by offsetting into the shared array itself, so every derived
   // pointer keeps the shared address space (no generic loads)
@@ -1079,7 +1105,9 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
   // a column tile share its columns and own contiguous ranges of row tiles.
   const int RS = g.rs;
   const bool split = RS > 1;
-  const int tile = blockIdx.x / RS, part = blockIdx.x % RS;
+  // MC: blockIdx = part * ntiles + tile, one cluster per row part
+  const int tile = MC ? int(blockIdx.x) % P.mc_q : int(blockIdx.x) / RS;
+  const int part = MC ? int(blockIdx.x) / P.mc_q : int(blockIdx.x) % RS;
   const int col0 = tile * NT;
   const int ntl = max(0, min(g.tpt, g.T - tile * g.tpt));
   const int NRT_all = g.npad / kBM;
@@ -1091,8 +1119,9 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
   // the leader is rank 0); pair p owns row tiles [2 u_lo, 2 u_hi), rank 0 the
   // first half and rank 1 the second -- equal counts, as one M = 256 MMA
   // covers a row tile of each.
-  const uint32_t crank = CTA2 ? uint32_t(part & 1) : 0u;
+  const uint32_t crank = CTA2 ? uint32_t(part & 1) : (MC ? uint32_t(tile) : 0u);
   const bool leader = crank == 0;
+  const uint16_t mc_all = uint16_t((1u << (MC ? P.mc_q : 1)) - 1u);
   const int u_lo = int((long long)(rt_span / 2) * (part / 2) / (RS / 2 > 0 ? RS / 2 : 1));
   const int u_hi = int((long long)(rt_span / 2) * (part / 2 + 1) / (RS / 2 > 0 ? RS / 2 : 1));
   const int rt_lo = CTA2 ? rt_base + 2 * u_lo + int(crank) * (u_hi - u_lo)
@@ -1119,7 +1148,8 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < stages; ++s) {
       mbar_init(&ctl->full[s], 1);
-      mbar_init(&ctl->empty[s], 1);
+      // MC: the leader reuses a stage once every CTA of the cluster is done with it
+      mbar_init(&ctl->empty[s], (MC && leader) ? uint32_t(P.mc_q) : 1u);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&ctl->tfull[b], 1);
@@ -1191,9 +1221,9 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
     trials[t] = tt;
   }
   tc_fence_before();
-  // pair: barriers initialised and TMEM allocated in both CTAs before any
+  // clusters: barriers initialised and TMEM allocated in every CTA before any
   // cross-CTA arrive, commit or TMA
-  if (CTA2) cluster_sync_all();
+  if (CL) cluster_sync_all();
   else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = ctl->tmem_base;
@@ -1271,6 +1301,13 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
             mbar_wait(&ctl->empty[st], ph ^ 1);
             if (P.exp_flags & 4) {
               if (!CTA2 || leader) mbar_arrive(&ctl->full[st]);
+            } else if (MC) {
+              // the leader's J' tile lands in every CTA of the cluster
+              mbar_expect_tx(&ctl->full[st], L.a_bytes + L.b_bytes);
+              if (leader)
+                tma_load_2d_mc(&tmJ, &ctl->full[st], sA + size_t(st) * L.a_bytes, kc * kBK,
+                               j_row0 + (rt_lo + rt) * kBM, mc_all, pol_keep);
+              tma_load_2d(&tmS, &ctl->full[st], sB + size_t(st) * L.b_bytes, kc * b_row, yS);
             } else if (CTA2) {
               // both CTAs' tiles complete on the leader's barrier: its own J'
               // rows and half of the spin columns from each CTA
@@ -1281,10 +1318,14 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
               tma_load_2d_pair(&tmS, bar, sB + size_t(st) * L.b_bytes, kc * b_row,
                                yS + int(crank) * (NT / 2));
             } else {
-              mbar_expect_tx(&ctl->full[st], L.a_bytes + L.b_bytes);
-              tma_load_2d_hint(&tmJ, &ctl->full[st], sA + size_t(st) * L.a_bytes, kc * kBK,
-                               j_row0 + (rt_lo + rt) * kBM, pol_keep);
-              tma_load_2d(&tmS, &ctl->full[st], sB + size_t(st) * L.b_bytes, kc * b_row, yS);
+              // ablations 8 / 16: skip the J' / spin loads (stale smem operands)
+              const bool la = !(P.exp_flags & 8), lb = !(P.exp_flags & 16);
+              mbar_expect_tx(&ctl->full[st], (la ? L.a_bytes : 0u) + (lb ? L.b_bytes : 0u));
+              if (la)
+                tma_load_2d_hint(&tmJ, &ctl->full[st], sA + size_t(st) * L.a_bytes, kc * kBK,
+                                 j_row0 + (rt_lo + rt) * kBM, pol_keep);
+              if (lb)
+                tma_load_2d(&tmS, &ctl->full[st], sB + size_t(st) * L.b_bytes, kc * b_row, yS);
             }
           }
         }
@@ -1292,12 +1333,12 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
       }
     }
     __syncwarp();
-    if (CTA2) cluster_sync_all();  // no CTA leaves while its pair may still signal it
+    if (CL) cluster_sync_all();  // no CTA leaves while its cluster may still signal it
   } else if (warp == kWarpMma) {
     // ===== MMA issuer (the pair's leader only; the whole warp runs the loop,
     // one elected lane issues) =====
     SSQA_CTL_REGS();
-    if (leader) {
+    if (!CTA2 || leader) {
       for (long c = P.c_first; c <= P.c_last; ++c) {
         const long s = c - P.c_first;
         if (s > 0) {
@@ -1340,7 +1381,10 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
                                  (kc | k) ? 1u : 0u);
               }
             }
-            mma_commit_w<CTA2>(&ctl->empty[st]);
+            if (MC)  // free the stage here and at the leader, which refills it
+              mma_commit_mc(&ctl->empty[st], uint16_t(leader ? 1u : (1u | (1u << crank))));
+            else
+              mma_commit_w<CTA2>(&ctl->empty[st]);
           }
           mma_commit_w<CTA2>(&ctl->tfull[buf]);
           DBG_STAMP(0, acc_it, 1);
@@ -1356,6 +1400,7 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
       asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
                    "r"(ncols));
     } else {
+      if (MC) cluster_sync_all();
       asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
                    "r"(ncols));
     }
@@ -1415,7 +1460,7 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
       }
     }
     __syncwarp();
-    if (CTA2) cluster_sync_all();
+    if (CL) cluster_sync_all();
   } else if (warp >= EPI) {
     // ===== row-ready publisher (row split only): once this CTA's epilogue has
     // written a group of its row tiles in pass c, stamp them for the other
@@ -1435,7 +1480,7 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
       }
     }
     __syncwarp();
-    if (CTA2) cluster_sync_all();
+    if (CL) cluster_sync_all();
   } else {
     // ===== epilogue =====
     SSQA_EPI_REGS();
@@ -1739,12 +1784,14 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
           else
             for (int t = 0; t < ntl; ++t) any |= trials[t].active;
           // nothing left to anneal: the other roles may already be in pass
-          // c+1 -- let it run (drained) and stop everyone after it
-          if (!any && c < P.c_last) ctl->last_pass = c + 1;
+          // c+1 -- let it run (drained) and stop everyone after it.  MC: the
+          // cluster shares every J' stage, so its CTAs run all passes (drained)
+          if (!any && c < P.c_last && !MC) ctl->last_pass = c + 1;
         }
       }
       epi_bar<EPI>();
-      if (scan_mode && !drain && c + 1 == *reinterpret_cast<volatile long*>(&ctl->last_pass) &&
+      if (scan_mode && !drain &&
+          (MC || c + 1 == *reinterpret_cast<volatile long*>(&ctl->last_pass)) &&
           c + 1 <= P.c_last) {
         int any = 0;
         if (split) any = !ctl->scan_stop;
@@ -1773,7 +1820,7 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
     tc_fence_before();
     __syncwarp();
     if (lane == 0) mbar_arrive(&ctl->done);
-    if (CTA2) cluster_sync_all();
+    if (CL) cluster_sync_all();
   }
   // No code after the role branches: each role runs to the end on its own
   // register budget (the MMA warp releases TMEM once the epilogue is done).
@@ -1851,21 +1898,49 @@ constexpr int kDefaultEpi = 16;
 template <int EPI, bool F4>
 cudaError_t launch_variant(int grid, int smem, cudaStream_t st, const CUtensorMap* maps,
                            const TcParams& P) {
-  cudaError_t e = cudaFuncSetAttribute(k_sweep_tc<EPI, F4, false>,
+  cudaError_t e = cudaFuncSetAttribute(k_sweep_tc<EPI, F4, 0>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  k_sweep_tc<EPI, F4, false><<<grid, 32 * (4 + EPI), smem, st>>>(maps[0], maps[1], maps[2],
-                                                                   maps[3], P);
+  k_sweep_tc<EPI, F4, 0><<<grid, 32 * (4 + EPI), smem, st>>>(maps[0], maps[1], maps[2],
+                                                               maps[3], P);
   return cudaSuccess;
 }
 
-// CTA-pair variant: clusters of 2.  Every CTA must be resident at once (the
-// row split synchronises across CTAs), so the launch is refused
-// (cudaErrorNotSupported) unless grid/2 clusters fit on the device.
-template <bool F4>
+// How many clusters of `csize` CTAs of the cluster variant fit at once.
+template <bool F4, int CL>
+int max_clusters(int smem, int csize) {
+  auto kern = k_sweep_tc<16, F4, CL>;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
+      cudaSuccess)
+    return 0;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(unsigned(csize));
+  cfg.blockDim = dim3(32 * (4 + 16));
+  cfg.dynamicSmemBytes = size_t(smem);
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = unsigned(csize);
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int clusters = 0;
+  if (cudaOccupancyMaxActiveClusters(&clusters, kern, &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return clusters;
+}
+
+// Cluster variants: CTA pairs (CL 1, clusters of 2) and J' multicast (CL 2,
+// clusters of mc_q).  Every CTA must be resident at once (the row split
+// synchronises across CTAs), so the launch is refused (cudaErrorNotSupported)
+// unless all grid / csize clusters fit on the device.
+template <bool F4, int CL>
 cudaError_t launch_variant_pair(int grid, int smem, cudaStream_t st, const CUtensorMap* maps,
                                 const TcParams& P) {
-  auto kern = k_sweep_tc<16, F4, true>;
+  auto kern = k_sweep_tc<16, F4, CL>;
+  const int csize = CL == 1 ? 2 : P.mc_q;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
@@ -1875,7 +1950,7 @@ cudaError_t launch_variant_pair(int grid, int smem, cudaStream_t st, const CUten
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.x = unsigned(csize);
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
@@ -1883,7 +1958,7 @@ cudaError_t launch_variant_pair(int grid, int smem, cudaStream_t st, const CUten
   int clusters = 0;
   e = cudaOccupancyMaxActiveClusters(&clusters, kern, &cfg);
   if (e != cudaSuccess) return e;
-  if (2 * clusters < grid) return cudaErrorNotSupported;
+  if (csize * clusters < grid) return cudaErrorNotSupported;
   return cudaLaunchKernelEx(&cfg, kern, maps[0], maps[1], maps[2], maps[3], P);
 }
 
@@ -1980,6 +2055,14 @@ int launch(ssqa_batch_s* b, TcParams& P, bool f4) {
   bool cta2 = P.run_mode == 1 && g.rs > 1 && g.rs % 2 == 0 && (g.npad / kBM) % 2 == 0 &&
               epi == 16;
   if (const char* e2 = getenv("SSQA_TC_CTA2")) cta2 = cta2 && atoi(e2) != 0;
+  // J' multicast clusters (all column tiles of a row part), opt-in with
+  // SSQA_TC_MC=1: they cut the L2 reads of J' by the tile count but not the
+  // bytes each SM takes in, which is what limits the MMAs (C5: 927 us/sweep
+  // against 533 with CTA pairs, whose MMAs read half of B from the peer SM)
+  bool mc = P.run_mode == 1 && g.rs > 1 && g.ntiles >= 2 && g.ntiles <= 8 && epi == 16;
+  const char* e3 = getenv("SSQA_TC_MC");
+  mc = mc && e3 && atoi(e3) != 0;
+  if (mc) cta2 = false;
   Layout L;
   auto setup = [&](bool pairs) {
     const int b_cols = pairs ? g.tile_cols / 2 : g.tile_cols;
@@ -2015,10 +2098,32 @@ int launch(ssqa_batch_s* b, TcParams& P, bool f4) {
   cudaError_t e;
   // one persistent CTA per (column tile, row part); every CTA must be
   // resident (the row split synchronises across CTAs): grid <= SM count
-  const int grid = g.ntiles * g.rs;
-  if (cta2) {
-    e = f4 ? launch_variant_pair<true>(grid, smem, b->prob->stream, maps, P)
-           : launch_variant_pair<false>(grid, smem, b->prob->stream, maps, P);
+  int grid = g.ntiles * g.rs;
+  if (mc) {
+    // as many row parts as clusters fit at once (a cluster of ntiles CTAs must
+    // sit inside one GPC)
+    P.mc_q = g.ntiles;
+    const int fit = f4 ? max_clusters<true, 2>(smem, P.mc_q) : max_clusters<false, 2>(smem, P.mc_q);
+    if (fit >= 2) {
+      const int rs0 = P.g.rs;
+      P.g.rs = std::min(P.g.rs, fit);  // g aliases P.g
+      grid = g.ntiles * g.rs;
+      e = f4 ? launch_variant_pair<true, 2>(grid, smem, b->prob->stream, maps, P)
+             : launch_variant_pair<false, 2>(grid, smem, b->prob->stream, maps, P);
+      if (e == cudaErrorNotSupported) {
+        cudaGetLastError();
+        mc = false;
+        P.g.rs = rs0;
+        grid = g.ntiles * g.rs;
+      }
+    } else {
+      mc = false;
+    }
+  }
+  if (mc) {
+  } else if (cta2) {
+    e = f4 ? launch_variant_pair<true, 1>(grid, smem, b->prob->stream, maps, P)
+           : launch_variant_pair<false, 1>(grid, smem, b->prob->stream, maps, P);
     if (e == cudaErrorNotSupported) {  // the pairs do not all fit at once: single CTAs
       cudaGetLastError();
       cta2 = false;
@@ -2026,7 +2131,7 @@ int launch(ssqa_batch_s* b, TcParams& P, bool f4) {
       smem = int(L.total);
     }
   }
-  if (cta2) {
+  if (mc || cta2) {
   } else if (epi == 16)
     e = f4 ? launch_variant<16, true>(grid, smem, b->prob->stream, maps, P)
            : launch_variant<16, false>(grid, smem, b->prob->stream, maps, P);

@@ -510,9 +510,13 @@ def row_split(monkeypatch):
     return force
 
 
-@pytest.fixture(params=["pairs", "single"])
+@pytest.fixture(params=["mc", "pairs", "single"])
 def cta_pairs(request, monkeypatch):
-    """Even row splits run as CTA pairs (cta_group::2, M = 256) unless off."""
+    """Row-split clusters: J' multicast across the column tiles of a row part
+    (2..8 tiles, opt-in), CTA pairs (cta_group::2, M = 256, even splits, the
+    default) or none."""
+    if request.param == "mc":
+        monkeypatch.setenv("SSQA_TC_MC", "1")
     if request.param == "single":
         monkeypatch.setenv("SSQA_TC_CTA2", "0")
     return request.param
