@@ -892,6 +892,12 @@ int ssqa_batch_shard_begin(ssqa_batch b, int has_target, double target, int stop
   b->launches += 1;
   int rc = init_state(b);
   if (rc) return rc;
+  // FP4 / FP4-pair operands: the passes read and write the FP4 spin slots
+  if (tc_uses_fp4(b)) {
+    launch_pack_fp4(b->d_sig, b->d_sig4, size_t(b->nslots) * b->slot_elems / 2, st);
+    CHECK_LAUNCH();
+    b->launches += 1;
+  }
   b->sh_has_target = has_target;
   b->sh_target_tol = target + kTargetTol;
   b->sh_stop = stop_at_target;
@@ -909,8 +915,12 @@ int ssqa_batch_shard_pass(ssqa_batch b, void* chunk) {
   if (rc) return set_err(rc, tc_last_error());
   // sigma(c+1) rows of this shard sit in the slot the kernel picked (ring rule)
   const int dst = b->cycle < b->p.sc ? pick_free(b) : b->cur;
-  launch_shard_pack(b->g, slot_ptr(b, dst), b->shard * nrt * 128, nrt * 128,
-                    reinterpret_cast<const unsigned long long*>(b->d_E), chunk, st);
+  if (tc_uses_fp4(b))
+    launch_shard_pack_fp4(b->g, b->d_sig4 + size_t(dst) * b->slot_elems / 2, b->shard * nrt * 128,
+                          nrt * 128, reinterpret_cast<const unsigned long long*>(b->d_E), chunk, st);
+  else
+    launch_shard_pack(b->g, slot_ptr(b, dst), b->shard * nrt * 128, nrt * 128,
+                      reinterpret_cast<const unsigned long long*>(b->d_E), chunk, st);
   CHECK_LAUNCH();
   b->launches += 2;
   return SSQA_OK;
@@ -923,7 +933,8 @@ int ssqa_batch_shard_merge(ssqa_batch b, const void* chunks) {
   cudaStream_t st = b->prob->stream;
   const bool upd = b->cycle < b->p.sc;
   const int dst = upd ? pick_free(b) : b->cur;
-  launch_shard_unpack(b->g, slot_ptr(b, dst), chunks, size_t(ssqa_batch_shard_bytes(b)),
+  uint8_t* dst4 = tc_uses_fp4(b) ? b->d_sig4 + size_t(dst) * b->slot_elems / 2 : nullptr;
+  launch_shard_unpack(b->g, slot_ptr(b, dst), dst4, chunks, size_t(ssqa_batch_shard_bytes(b)),
                       b->nshards, b->g.npad / b->nshards, upd, b->d_E, st);
   CHECK_LAUNCH();
   ScanArgs sa{};

@@ -209,7 +209,34 @@ __global__ void k_shard_pack(Geom g, const int8_t* __restrict__ slot, int row0, 
     e_out[col] = static_cast<long long>(E[col]);
 }
 
-__global__ void k_shard_unpack(Geom g, int8_t* __restrict__ slot, const uint8_t* __restrict__ all,
+// FP4 spin slots (two e2m1 nibbles per byte, lower row in the low nibble,
+// bit 3 = negative): the same bit-packed chunk from 16 bytes per 32 rows.
+__global__ void k_shard_pack_fp4(Geom g, const uint8_t* __restrict__ slot4, int row0, int nwords,
+                                 const unsigned long long* __restrict__ E,
+                                 uint8_t* __restrict__ chunk) {
+  uint32_t* bits = reinterpret_cast<uint32_t*>(chunk);
+  long long* e_out = reinterpret_cast<long long*>(chunk + size_t(g.ccols) * nwords * 4);
+  const size_t total = size_t(g.ccols) * nwords;
+  for (size_t x = blockIdx.x * size_t(blockDim.x) + threadIdx.x; x < total;
+       x += size_t(gridDim.x) * blockDim.x) {
+    const int col = int(x / nwords), w = int(x % nwords);
+    const int4 a = *reinterpret_cast<const int4*>(slot4 + size_t(col) * (g.npad / 2) +
+                                                  (row0 + 32 * w) / 2);
+    const uint32_t v[4] = {uint32_t(a.x), uint32_t(a.y), uint32_t(a.z), uint32_t(a.w)};
+    uint32_t word = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int y = 0; y < 8; ++y)  // nibble y of word q = row 8q + y; positive when bit 3 clear
+        word |= uint32_t(((v[q] >> (4 * y + 3)) & 1u) == 0u) << (8 * q + y);
+    bits[x] = word;
+  }
+  for (int col = blockIdx.x * blockDim.x + threadIdx.x; col < g.ccols; col += gridDim.x * blockDim.x)
+    e_out[col] = static_cast<long long>(E[col]);
+}
+
+__global__ void k_shard_unpack(Geom g, int8_t* __restrict__ slot, uint8_t* __restrict__ slot4,
+                               const uint8_t* __restrict__ all,
                                size_t chunk_bytes, int nshards, int rows_per_shard,
                                int with_spins, long long* __restrict__ E) {
   const int nwords = rows_per_shard / 32;
@@ -233,6 +260,20 @@ __global__ void k_shard_unpack(Geom g, int8_t* __restrict__ slot, const uint8_t*
                                           32 * w);
       dst[0] = make_int4(int(v[0]), int(v[1]), int(v[2]), int(v[3]));
       dst[1] = make_int4(int(v[4]), int(v[5]), int(v[6]), int(v[7]));
+      if (slot4) {  // the FP4 image for the next pass's MMAs (+1 -> 0x2, -1 -> 0xA)
+        uint32_t n4[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          uint32_t x4 = 0;
+#pragma unroll
+          for (int y = 0; y < 8; ++y)
+            x4 |= (((word >> (8 * q + y)) & 1u) ? 0x2u : 0xAu) << (4 * y);
+          n4[q] = x4;
+        }
+        *reinterpret_cast<int4*>(slot4 + size_t(col) * (g.npad / 2) +
+                                 (size_t(sh) * rows_per_shard + 32 * w) / 2) =
+            make_int4(int(n4[0]), int(n4[1]), int(n4[2]), int(n4[3]));
+      }
     }
   }
   for (int col = blockIdx.x * blockDim.x + threadIdx.x; col < g.ccols; col += gridDim.x * blockDim.x) {
@@ -249,10 +290,16 @@ void launch_shard_pack(const Geom& g, const int8_t* slot, int row0, int rows,
   k_shard_pack<<<1184, 256, 0, st>>>(g, slot, row0, rows / 32, E, static_cast<uint8_t*>(chunk));
 }
 
-void launch_shard_unpack(const Geom& g, int8_t* slot, const void* all, size_t chunk_bytes,
-                         int nshards, int rows_per_shard, bool with_spins, long long* E,
-                         cudaStream_t st) {
-  k_shard_unpack<<<1184, 256, 0, st>>>(g, slot, static_cast<const uint8_t*>(all), chunk_bytes,
+void launch_shard_pack_fp4(const Geom& g, const uint8_t* slot4, int row0, int rows,
+                           const unsigned long long* E, void* chunk, cudaStream_t st) {
+  k_shard_pack_fp4<<<1184, 256, 0, st>>>(g, slot4, row0, rows / 32, E,
+                                         static_cast<uint8_t*>(chunk));
+}
+
+void launch_shard_unpack(const Geom& g, int8_t* slot, uint8_t* slot4, const void* all,
+                         size_t chunk_bytes, int nshards, int rows_per_shard, bool with_spins,
+                         long long* E, cudaStream_t st) {
+  k_shard_unpack<<<1184, 256, 0, st>>>(g, slot, slot4, static_cast<const uint8_t*>(all), chunk_bytes,
                                        nshards, rows_per_shard, with_spins ? 1 : 0, E);
 }
 

@@ -59,9 +59,13 @@ void launch_init(const Geom& g, const uint64_t* seeds, int8_t* sig, double* acc,
 // unpack all shards' chunks into the slot and sum their energy partials.
 void launch_shard_pack(const Geom& g, const int8_t* slot, int row0, int rows,
                        const unsigned long long* E, void* chunk, cudaStream_t st);
-void launch_shard_unpack(const Geom& g, int8_t* slot, const void* all, size_t chunk_bytes,
-                         int nshards, int rows_per_shard, bool with_spins, long long* E,
-                         cudaStream_t st);
+// FP4 slot variant of launch_shard_pack (tcgen05 FP4 / FP4-pair shard passes).
+void launch_shard_pack_fp4(const Geom& g, const uint8_t* slot4, int row0, int rows,
+                           const unsigned long long* E, void* chunk, cudaStream_t st);
+// slot4 (nullable): also write the FP4 image of the gathered spins.
+void launch_shard_unpack(const Geom& g, int8_t* slot, uint8_t* slot4, const void* all,
+                         size_t chunk_bytes, int nshards, int rows_per_shard, bool with_spins,
+                         long long* E, cudaStream_t st);
 void launch_reset_results(int T, long sc, double* best_e, int* best_k, int* reached,
                           long* first_hit, long* cycles_used, int* active, cudaStream_t st);
 void launch_field_simt(const Geom& g, const int8_t* J, const int8_t* sig, int32_t* S,

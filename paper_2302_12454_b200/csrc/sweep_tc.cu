@@ -2258,6 +2258,10 @@ void advance_ring(ssqa_batch_s* b, long count) {
 // FP4 operands when every coupling is e2m1-exact, fields stay below 2^22
 // (exact fp32 accumulation and float->int conversion) and the tile leaves
 // room for the scale-factor columns; SSQA_TC_FP4=0 forces int8.
+void launch_pack_fp4(const int8_t* src, uint8_t* dst, size_t bytes, cudaStream_t st) {
+  k_pack_fp4<<<1184, 256, 0, st>>>(src, dst, bytes);
+}
+
 bool tc_uses_fp4(const ssqa_batch_s* b) {
   const Quantized& q = b->prob->q;
   const char* envf4 = getenv("SSQA_TC_FP4");
@@ -2289,7 +2293,7 @@ int tc_run(ssqa_batch_s* b, const ScanArgs& sa) {
   const bool f4 = tc_uses_fp4(b);
   if (f4) {
     const size_t bytes = size_t(b->nslots) * b->slot_elems / 2;
-    k_pack_fp4<<<1184, 256, 0, b->prob->stream>>>(b->d_sig, b->d_sig4, bytes);
+    launch_pack_fp4(b->d_sig, b->d_sig4, bytes, b->prob->stream);
     if (cudaGetLastError() != cudaSuccess) {
       g_tc_err = "k_pack_fp4 launch failed";
       return SSQA_ECUDA;
@@ -2345,7 +2349,9 @@ int tc_shard_pass(ssqa_batch_s* b, int rt0, int nrt, unsigned long long* gE) {
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, b->prob->device);
   P.g.rs = std::max(1, std::min(nrt, sms / std::max(1, P.g.ntiles)));
-  int rc = launch(b, P, false);
+  // FP4 / FP4-pair operands when the problem has them (the merge keeps the
+  // FP4 slots current, ssqa_batch_shard_begin packs the initial state)
+  int rc = launch(b, P, tc_uses_fp4(b));
   if (rc) return rc;
   return SSQA_OK;
 }

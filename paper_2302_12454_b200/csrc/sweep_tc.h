@@ -12,12 +12,15 @@ namespace ssqa_engine {
 bool tc_supported(int npad, int r, int delay);
 // Operand format a fused run of this batch streams: FP4 (e2m1) or int8.
 bool tc_uses_fp4(const ssqa_batch_s* b);
+// int8 spin slots -> FP4 (e2m1) slots, `bytes` FP4 bytes (two spins each).
+void launch_pack_fp4(const int8_t* src, uint8_t* dst, size_t bytes, cudaStream_t st);
 // Full run: cycles 0..sc with scans (state already initialised).
 int tc_run(ssqa_batch_s* b, const ScanArgs& sa);
 // One sweep at b->cycle without a scan (per-step API).
 int tc_sweep(ssqa_batch_s* b, double jperp, double i0);
 // GPU row shard: one pass at b->cycle over row tiles [rt0, rt0 + nrt) with
-// int8 spin slots (sigma(c+1) of those rows, acc), the pass energies' row
+// the batch's operand format (int8 slots, or FP4 slots when tc_uses_fp4:
+// sigma(c+1) of those rows, acc), the pass energies' row
 // partials added into gE[ccols] (zeroed by the caller); the ring is not
 // advanced (the caller merges all shards' rows first).
 int tc_shard_pass(ssqa_batch_s* b, int rt0, int nrt, unsigned long long* gE);

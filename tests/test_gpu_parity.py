@@ -596,9 +596,10 @@ def test_wide_row_split_default_heuristic(orc):
 # ---- GPU row shards: per-cycle pass / all-gather / merge ----
 
 @pytest.mark.parametrize("nshards", [1, 2, 4])
-def test_row_shards_emulated_match_oracle(orc, nshards):
+def test_row_shards_emulated_match_oracle(orc, nshards, operands):
     """Every shard of a G-way J' row shard (run one after another on one GPU,
-    exchanging through one buffer) equals the oracle's ssqa_run."""
+    exchanging through one buffer) equals the oracle's ssqa_run -- with FP4 /
+    FP4-pair shard passes (GI / dense couplings) and forced int8."""
     if not engine_ok(_lib.ENGINE_TCGEN05):
         pytest.skip("tcgen05 engine unavailable")
     from paper_2302_12454_b200.rowshard import run_emulated_shards
