@@ -33,6 +33,8 @@ import sys
 import threading
 import time
 
+import numpy as np
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
@@ -60,6 +62,25 @@ def build_model(cfg):
     if cfg["kind"] == "gi":
         return sq.gi_ising(cfg["n_nodes"], EDGE_P, GI_SEED, True, C12, C12)
     return sq.dense_ising(cfg["n"], cfg["dense_kind"], GI_SEED)
+
+
+def pin_model(m):
+    """The e2e leg copies the model from PINNED host memory (the contract's
+    host->device input copy): move h and J into page-locked buffers once,
+    outside the timed region, so the per-call upload runs at DMA speed."""
+    import torch
+    m.pinned = False
+    try:
+        for name in ("h", "J"):
+            a = np.ascontiguousarray(getattr(m, name), dtype=np.float64)
+            t = torch.empty(a.shape, dtype=torch.float64, pin_memory=True)
+            t.numpy()[...] = a
+            setattr(m, name, t.numpy())
+            setattr(m, "_pinned_" + name, t)  # keeps the page-locked storage alive
+        m.pinned = True
+    except RuntimeError:  # no driver: pageable arrays stay
+        pass
+    return m
 
 
 def n_spins(cfg):
@@ -268,7 +289,7 @@ def run_rows(args, cfg):
     R, T, sc = cfg["R"], cfg["T"], cfg["sc"]
     N = n_spins(cfg)
     seeds = [BASE_SEED + t for t in range(T)]
-    m = build_model(cfg)
+    m = pin_model(build_model(cfg))
     p = sq.SsqaParams(r=R, sc=sc)
     target = 0.0 if cfg["kind"] == "gi" else None
     prob = sq.Problem(m, local)
@@ -380,7 +401,7 @@ def run_ours(args, cfg):
     seeds = shard.shard_seeds(BASE_SEED, T, world, rank)
     engine = {"auto": _lib.ENGINE_AUTO, "simt": _lib.ENGINE_SIMT,
               "tcgen05": _lib.ENGINE_TCGEN05}[args.engine]
-    m = build_model(cfg)
+    m = pin_model(build_model(cfg))
     p = sq.SsqaParams(r=R, sc=sc)
     prob = sq.Problem(m, local)
     info = prob.info()
@@ -521,7 +542,8 @@ def run_ours(args, cfg):
                              if 8 * N * R * T > 126 * 2**20 else "state fits L2 (small config)"},
             "roofline": roofline,
             "e2e": {"value": upd_per_step / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": d2h, "seconds_per_step": e2e_s},
+                    "d2h_bytes_per_step": d2h, "seconds_per_step": e2e_s,
+                    "h2d_source": "pinned" if m.pinned else "pageable"},
             "gpu_launches": launches,
             "clocks": clk,
             "tts": {"p_s": p_s, "hits": hits, "trials": T, "t_trial_s": t_trial,

@@ -91,6 +91,16 @@ typedef struct {
 const char* ssqa_last_error(void);
 const char* ssqa_version(void);
 
+/* ---- Device memory pool (no reference counterpart: the reference's lattice
+ * lives in std::vector, annealer.cpp:432-447) ---------------------------------
+ * Problem and batch buffers come from a process-wide caching allocator:
+ * destroyed handles return their blocks to it and the next handle of the same
+ * shape reuses them, so repeated ssqa_run_batch calls pay no cudaMalloc /
+ * cudaFree.  Blocks are released when an allocation would otherwise fail, or
+ * here.  ssqa_pool_trim returns the bytes released (device -1: all devices). */
+long long ssqa_pool_trim(int device);
+int ssqa_pool_stats(int device, long long* cached_bytes, long long* in_use_bytes);
+
 /* ---- Problem: replaces DenseProblem (annealer.cpp:40-89) -------------------
  * h[n], J[n*n] (dense, mirrored, zero diagonal: IsingModel storage,
  * model.hpp:59-66) and offset are quantized once to int8 J' = J*2^p and
@@ -218,6 +228,27 @@ int ssqa_batch_shard_begin(ssqa_batch b, int has_target, double target, int stop
 int ssqa_batch_shard_pass(ssqa_batch b, void* chunk);
 int ssqa_batch_shard_merge(ssqa_batch b, const void* chunks);
 int ssqa_batch_shard_end(ssqa_batch b);
+
+/* Peer push instead of a collective library: the pack kernel of
+ * ssqa_batch_shard_pass_to stores this shard's chunk straight into dests[d]
+ * (this shard's slot in GPU d's exchange region, a peer pointer from
+ * ssqa_ipc_open -- NVLink stores) and its last block raises *flags[d] = epoch
+ * (system-scope release); ssqa_batch_shard_merge_from waits until its own
+ * flags[0..G) all reach epoch (system-scope acquire) and merges `chunks`.
+ * Use epoch = cycle + 1 and two exchange regions by epoch parity: a GPU can
+ * only write epoch e + 2 after every GPU has merged epoch e.  ndest <= 8. */
+int ssqa_batch_shard_pass_to(ssqa_batch b, void* const* dests, unsigned* const* flags, int ndest,
+                             unsigned epoch);
+int ssqa_batch_shard_merge_from(ssqa_batch b, const void* chunks, const unsigned* flags,
+                                int nflags, unsigned epoch);
+/* Exchange regions: a zeroed device block of its own (CUDA IPC maps whole
+ * allocations), its 64-byte IPC handle, and the peer mapping of a handle
+ * from another process of the node. */
+int ssqa_exchange_alloc(int device, long long bytes, void** dev_ptr_out);
+int ssqa_exchange_free(void* dev_ptr);
+int ssqa_ipc_handle(const void* dev_ptr, void* handle_out);
+int ssqa_ipc_open(const void* handle, int device, void** dev_ptr_out);
+int ssqa_ipc_close(void* dev_ptr);
 
 /* ---- Per-step API: init_lattice / ssqa_sweep / replica_energies
  * (annealer.cpp:432-472), applied to every trial of the batch. ---------- */

@@ -49,6 +49,8 @@ IP, LP = C.POINTER(C.c_int), C.POINTER(C.c_long)
 SIGNATURES = [
     ("ssqa_last_error", C.c_char_p, []),
     ("ssqa_version", C.c_char_p, []),
+    ("ssqa_pool_trim", C.c_longlong, [C.c_int]),
+    ("ssqa_pool_stats", C.c_int, [C.c_int, C.POINTER(C.c_longlong), C.POINTER(C.c_longlong)]),
     ("ssqa_problem_create", C.c_int, [C.c_int, DP, DP, C.c_double, C.c_int, C.POINTER(VP)]),
     ("ssqa_problem_destroy", C.c_int, [VP]),
     ("ssqa_problem_create_many", C.c_int, [C.c_int, C.c_int, DP, DP, DP, C.c_int,
@@ -86,6 +88,13 @@ SIGNATURES = [
     ("ssqa_batch_shard_begin", C.c_int, [VP, C.c_int, C.c_double, C.c_int]),
     ("ssqa_batch_shard_pass", C.c_int, [VP, VP]),
     ("ssqa_batch_shard_merge", C.c_int, [VP, VP]),
+    ("ssqa_batch_shard_pass_to", C.c_int, [VP, C.POINTER(VP), C.POINTER(VP), C.c_int, C.c_uint]),
+    ("ssqa_batch_shard_merge_from", C.c_int, [VP, VP, VP, C.c_int, C.c_uint]),
+    ("ssqa_exchange_alloc", C.c_int, [C.c_int, C.c_longlong, C.POINTER(VP)]),
+    ("ssqa_exchange_free", C.c_int, [VP]),
+    ("ssqa_ipc_handle", C.c_int, [VP, C.c_char_p]),
+    ("ssqa_ipc_open", C.c_int, [C.c_char_p, C.c_int, C.POINTER(VP)]),
+    ("ssqa_ipc_close", C.c_int, [VP]),
     ("ssqa_batch_shard_end", C.c_int, [VP]),
     ("ssqa_batch_init", C.c_int, [VP]),
     ("ssqa_batch_sweep", C.c_int, [VP, C.c_long]),

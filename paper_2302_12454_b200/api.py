@@ -317,6 +317,20 @@ class Batch:
     def shard_merge(self, chunks_ptr: int):
         check(lib().ssqa_batch_shard_merge(self._b, C.c_void_p(chunks_ptr)))
 
+    def shard_pass_to(self, dests: Sequence[int], flags: Sequence[int], epoch: int):
+        """Peer push: pack this shard's chunk straight into every dests[d] and
+        raise *flags[d] = epoch (ssqa_batch_shard_pass_to)."""
+        n = len(dests)
+        d = (C.c_void_p * n)(*[C.c_void_p(x) for x in dests])
+        f = (C.c_void_p * n)(*[C.c_void_p(x) for x in flags])
+        check(lib().ssqa_batch_shard_pass_to(self._b, d, f, n, C.c_uint(epoch & 0xFFFFFFFF)))
+
+    def shard_merge_from(self, chunks_ptr: int, flags_ptr: int, nflags: int, epoch: int):
+        """Wait for every shard's flag to reach epoch, then merge."""
+        check(lib().ssqa_batch_shard_merge_from(self._b, C.c_void_p(chunks_ptr),
+                                                C.c_void_p(flags_ptr), nflags,
+                                                C.c_uint(epoch & 0xFFFFFFFF)))
+
     def shard_end(self):
         check(lib().ssqa_batch_shard_end(self._b))
 
@@ -486,6 +500,18 @@ def replica_energies(lat: ReplicaLattice, m: IsingModel, engine: int = ENGINE_AU
 class TtsValue:
     kind: str  # "finite" | "saturated" | "undefined"
     seconds: float = 0.0
+
+
+def pool_stats(device: int = 0) -> dict:
+    """Bytes the engine's device pool caches / hands out (csrc/devpool.h)."""
+    c, u = C.c_longlong(0), C.c_longlong(0)
+    lib().ssqa_pool_stats(device, C.byref(c), C.byref(u))
+    return {"cached": int(c.value), "in_use": int(u.value)}
+
+
+def pool_trim(device: int = -1) -> int:
+    """Release the pool's cached device blocks; returns the bytes released."""
+    return int(lib().ssqa_pool_trim(device))
 
 
 def compute_tts(p_s: float, t_seconds: float, p_target: float = 0.99) -> TtsValue:

@@ -1,5 +1,6 @@
 // capi.cu -- the C ABI of include/ssqa_cuda.h: problem upload, batches, the
 // run loop (run_lattice, annealer.cpp:313-361) and the per-step parity API.
+#include "devpool.h"
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -168,12 +169,12 @@ Geom make_geom(int n, int npad, int R, int T, int sms, int engine, bool fp4, boo
 
 template <class T>
 int dalloc(T** p, size_t count) {
-  CU(cudaMalloc(reinterpret_cast<void**>(p), std::max<size_t>(count, 1) * sizeof(T)));
+  CU(pmalloc(reinterpret_cast<void**>(p), std::max<size_t>(count, 1) * sizeof(T)));
   return SSQA_OK;
 }
 
 void dfree(void* p) {
-  if (p) cudaFree(p);
+  if (p) pool_free(p);
 }
 
 int8_t* slot_ptr(ssqa_batch_s* b, int s) { return b->d_sig + size_t(s) * b->slot_elems; }
@@ -204,7 +205,7 @@ int normalize_slots(ssqa_batch_s* b) {
                        cudaMemcpyDeviceToDevice, b->prob->stream));
   }
   CU(cudaStreamSynchronize(b->prob->stream));
-  cudaFree(b->d_sig);
+  pool_free(b->d_sig);
   b->d_sig = fresh;
   b->cur = 0;
   for (size_t s = 0; s < b->phys.size(); ++s) b->phys[s] = int(s) + 1;
@@ -293,14 +294,14 @@ int ssqa_problem_create(int n, const double* h, const double* J, double offset, 
   int st[6] = {0, 0, 0, 0, 0, 0};
   std::string fail;
   auto cleanup = [&]() {
-    if (d_Jd) cudaFree(d_Jd);
-    if (d_stats) cudaFree(d_stats);
+    if (d_Jd) pool_free(d_Jd);
+    if (d_stats) pool_free(d_stats);
   };
   cudaError_t e = cudaSetDevice(device);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&pr->stream, cudaStreamNonBlocking);
-  if (e == cudaSuccess) e = cudaMalloc(&d_Jd, nn * sizeof(double));
-  if (e == cudaSuccess) e = cudaMalloc(&d_stats, sizeof(st));
-  if (e == cudaSuccess) e = cudaMalloc(&pr->d_J, np2);
+  if (e == cudaSuccess) e = pmalloc(&d_Jd, nn * sizeof(double));
+  if (e == cudaSuccess) e = pmalloc(&d_stats, sizeof(st));
+  if (e == cudaSuccess) e = pmalloc(&pr->d_J, np2);
   if (e == cudaSuccess) {
     const unsigned long long none = ~0ull;
     cudaMemsetAsync(d_stats, 0, sizeof(st), pr->stream);
@@ -344,14 +345,14 @@ int ssqa_problem_create(int n, const double* h, const double* J, double offset, 
       q.max_abs_h = std::max(q.max_abs_h, std::abs(H[size_t(i)]));
     }
     if (fail.empty()) {
-      e = cudaMalloc(&pr->d_H, H.size() * sizeof(int32_t));
+      e = pmalloc(&pr->d_H, H.size() * sizeof(int32_t));
       if (e == cudaSuccess)
         e = cudaMemcpyAsync(pr->d_H, H.data(), H.size() * sizeof(int32_t),
                             cudaMemcpyHostToDevice, pr->stream);
       // FP4 (e2m1) image when every coupling is 0, +-1, +-2, +-3, +-4 or +-6
       q.fp4_ok = q.max_abs_j <= 6 && q.max_abs_j != 5;
       if (e == cudaSuccess && q.fp4_ok) {
-        e = cudaMalloc(&pr->d_J4, np2 / 2);
+        e = pmalloc(&pr->d_J4, np2 / 2);
         if (e == cudaSuccess) {
           launch_qfp4(pr->d_J, np2, pr->d_J4, d_stats + 3, pr->stream);
           e = cudaMemcpyAsync(st, d_stats, sizeof(st), cudaMemcpyDeviceToHost, pr->stream);
@@ -359,7 +360,7 @@ int ssqa_problem_create(int n, const double* h, const double* J, double offset, 
         if (e == cudaSuccess) e = cudaStreamSynchronize(pr->stream);
         if (e == cudaSuccess && st[3]) {
           q.fp4_ok = false;
-          cudaFree(pr->d_J4);
+          pool_free(pr->d_J4);
           pr->d_J4 = nullptr;
         }
       }
@@ -367,7 +368,7 @@ int ssqa_problem_create(int n, const double* h, const double* J, double offset, 
       if (e == cudaSuccess && !q.fp4_ok && fp4x2_splittable(q.max_abs_j)) {
         st[3] = 0;
         e = cudaMemcpyAsync(d_stats + 3, st + 3, sizeof(int), cudaMemcpyHostToDevice, pr->stream);
-        if (e == cudaSuccess) e = cudaMalloc(&pr->d_J4, np2);
+        if (e == cudaSuccess) e = pmalloc(&pr->d_J4, np2);
         if (e == cudaSuccess) {
           launch_qfp4x2(pr->d_J, q.npad, pr->d_J4, d_stats + 3, pr->stream);
           e = cudaMemcpyAsync(st, d_stats, sizeof(st), cudaMemcpyDeviceToHost, pr->stream);
@@ -375,7 +376,7 @@ int ssqa_problem_create(int n, const double* h, const double* J, double offset, 
         if (e == cudaSuccess) e = cudaStreamSynchronize(pr->stream);
         q.fp4x2_ok = e == cudaSuccess && !st[3];
         if (!q.fp4x2_ok && pr->d_J4) {
-          cudaFree(pr->d_J4);
+          pool_free(pr->d_J4);
           pr->d_J4 = nullptr;
         }
       }
@@ -461,9 +462,9 @@ int ssqa_problem_create_many(int count, int n, const double* h, const double* J,
   pr->device = device;
   cudaError_t e = cudaSetDevice(device);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&pr->stream, cudaStreamNonBlocking);
-  if (e == cudaSuccess) e = cudaMalloc(&pr->d_J, pr->q.J.size());
-  if (e == cudaSuccess) e = cudaMalloc(&pr->d_H, pr->q.H.size() * sizeof(int32_t));
-  if (e == cudaSuccess) e = cudaMalloc(&pr->d_offsets, size_t(count) * sizeof(double));
+  if (e == cudaSuccess) e = pmalloc(&pr->d_J, pr->q.J.size());
+  if (e == cudaSuccess) e = pmalloc(&pr->d_H, pr->q.H.size() * sizeof(int32_t));
+  if (e == cudaSuccess) e = pmalloc(&pr->d_offsets, size_t(count) * sizeof(double));
   if (e == cudaSuccess)
     e = cudaMemcpyAsync(pr->d_J, pr->q.J.data(), pr->q.J.size(), cudaMemcpyHostToDevice, pr->stream);
   if (e == cudaSuccess)
@@ -473,7 +474,7 @@ int ssqa_problem_create_many(int count, int n, const double* h, const double* J,
     e = cudaMemcpyAsync(pr->d_offsets, pr->offsets.data(), size_t(count) * sizeof(double),
                         cudaMemcpyHostToDevice, pr->stream);
   if (e == cudaSuccess && (fp4 || fp4x2)) {
-    e = cudaMalloc(&pr->d_J4, pr->q.J4.size());
+    e = pmalloc(&pr->d_J4, pr->q.J4.size());
     if (e == cudaSuccess)
       e = cudaMemcpyAsync(pr->d_J4, pr->q.J4.data(), pr->q.J4.size(), cudaMemcpyHostToDevice,
                           pr->stream);
@@ -507,6 +508,8 @@ int ssqa_quantize_info(int n, const double* h, const double* J, int* n_pad, int*
 int ssqa_problem_destroy(ssqa_problem pr) {
   if (!pr) return SSQA_OK;
   cudaSetDevice(pr->device);
+  // blocks go back to the pool (devpool.h): nothing may still read them
+  if (pr->stream) cudaStreamSynchronize(pr->stream);
   dfree(pr->d_J);
   dfree(pr->d_H);
   dfree(pr->d_J4);
@@ -702,7 +705,7 @@ int ssqa_batch_destroy(ssqa_batch b) {
                     (void*)b->d_S, (void*)b->d_E, (void*)b->d_best_e, (void*)b->d_best_k,
                     (void*)b->d_reached, (void*)b->d_first_hit, (void*)b->d_cycles_used,
                     (void*)b->d_active, (void*)b->d_best_state, (void*)b->d_best_packed,
-                    (void*)b->d_trace})
+                    (void*)b->d_trace, (void*)b->d_push_ctr})
     dfree(ptr);
   if (b->ev0) cudaEventDestroy(b->ev0);
   if (b->ev1) cudaEventDestroy(b->ev1);
@@ -753,7 +756,7 @@ int ssqa_batch_profile_field(ssqa_batch b, int iters, double* ms_per_launch) {
   *ms_per_launch = double(f) / iters;
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
-  if (tmp) cudaFree(S);
+  if (tmp) pool_free(S);
   return SSQA_OK;
 }
 
@@ -904,8 +907,11 @@ int ssqa_batch_shard_begin(ssqa_batch b, int has_target, double target, int stop
   return SSQA_OK;
 }
 
-int ssqa_batch_shard_pass(ssqa_batch b, void* chunk) {
-  if (!b || !chunk) return set_err(SSQA_EINVAL, "null argument");
+}  // extern "C"
+
+namespace {
+
+int shard_pass(ssqa_batch b, const PeerPush& pp) {
   if (b->cycle > b->p.sc) return set_err(SSQA_EINVAL, "run already complete");
   CU(cudaSetDevice(b->prob->device));
   cudaStream_t st = b->prob->stream;
@@ -917,17 +923,16 @@ int ssqa_batch_shard_pass(ssqa_batch b, void* chunk) {
   const int dst = b->cycle < b->p.sc ? pick_free(b) : b->cur;
   if (tc_uses_fp4(b))
     launch_shard_pack_fp4(b->g, b->d_sig4 + size_t(dst) * b->slot_elems / 2, b->shard * nrt * 128,
-                          nrt * 128, reinterpret_cast<const unsigned long long*>(b->d_E), chunk, st);
+                          nrt * 128, reinterpret_cast<const unsigned long long*>(b->d_E), pp, st);
   else
     launch_shard_pack(b->g, slot_ptr(b, dst), b->shard * nrt * 128, nrt * 128,
-                      reinterpret_cast<const unsigned long long*>(b->d_E), chunk, st);
+                      reinterpret_cast<const unsigned long long*>(b->d_E), pp, st);
   CHECK_LAUNCH();
   b->launches += 2;
   return SSQA_OK;
 }
 
-int ssqa_batch_shard_merge(ssqa_batch b, const void* chunks) {
-  if (!b || !chunks) return set_err(SSQA_EINVAL, "null argument");
+int shard_merge(ssqa_batch b, const void* chunks, const PeerWait& pw) {
   if (b->cycle > b->p.sc) return set_err(SSQA_EINVAL, "run already complete");
   CU(cudaSetDevice(b->prob->device));
   cudaStream_t st = b->prob->stream;
@@ -935,7 +940,7 @@ int ssqa_batch_shard_merge(ssqa_batch b, const void* chunks) {
   const int dst = upd ? pick_free(b) : b->cur;
   uint8_t* dst4 = tc_uses_fp4(b) ? b->d_sig4 + size_t(dst) * b->slot_elems / 2 : nullptr;
   launch_shard_unpack(b->g, slot_ptr(b, dst), dst4, chunks, size_t(ssqa_batch_shard_bytes(b)),
-                      b->nshards, b->g.npad / b->nshards, upd, b->d_E, st);
+                      b->nshards, b->g.npad / b->nshards, upd, b->d_E, pw, st);
   CHECK_LAUNCH();
   ScanArgs sa{};
   sa.cycle = b->cycle;
@@ -955,6 +960,88 @@ int ssqa_batch_shard_merge(ssqa_batch b, const void* chunks) {
     b->cur = dst;
   }
   b->cycle += 1;  // sc + 1 marks the run complete
+  return SSQA_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int ssqa_batch_shard_pass(ssqa_batch b, void* chunk) {
+  if (!b || !chunk) return set_err(SSQA_EINVAL, "null argument");
+  PeerPush pp{};
+  pp.dst[0] = static_cast<uint8_t*>(chunk);
+  pp.n = 1;
+  return shard_pass(b, pp);
+}
+
+int ssqa_batch_shard_merge(ssqa_batch b, const void* chunks) {
+  if (!b || !chunks) return set_err(SSQA_EINVAL, "null argument");
+  return shard_merge(b, chunks, PeerWait{nullptr, 0u, 0});
+}
+
+int ssqa_batch_shard_pass_to(ssqa_batch b, void* const* dests, unsigned* const* flags, int ndest,
+                             unsigned epoch) {
+  if (!b || !dests || !flags) return set_err(SSQA_EINVAL, "null argument");
+  if (ndest < 1 || ndest > kMaxPeers) return set_err(SSQA_EINVAL, "1..8 destinations");
+  CU(cudaSetDevice(b->prob->device));
+  if (!b->d_push_ctr) {
+    int rc = dalloc(&b->d_push_ctr, 1);
+    if (rc) return rc;
+    CU(cudaMemsetAsync(b->d_push_ctr, 0, sizeof(unsigned), b->prob->stream));
+  }
+  PeerPush pp{};
+  for (int d = 0; d < ndest; ++d) {
+    if (!dests[d] || !flags[d]) return set_err(SSQA_EINVAL, "null destination");
+    pp.dst[d] = static_cast<uint8_t*>(dests[d]);
+    pp.flag[d] = flags[d];
+  }
+  pp.n = ndest;
+  pp.counter = b->d_push_ctr;
+  pp.epoch = epoch;
+  return shard_pass(b, pp);
+}
+
+int ssqa_batch_shard_merge_from(ssqa_batch b, const void* chunks, const unsigned* flags,
+                                int nflags, unsigned epoch) {
+  if (!b || !chunks || !flags) return set_err(SSQA_EINVAL, "null argument");
+  if (nflags != b->nshards) return set_err(SSQA_EINVAL, "one flag per shard");
+  return shard_merge(b, chunks, PeerWait{flags, epoch, nflags});
+}
+
+int ssqa_exchange_alloc(int device, long long bytes, void** dev_ptr_out) {
+  if (!dev_ptr_out || bytes < 1) return set_err(SSQA_EINVAL, "bad argument");
+  CU(cudaSetDevice(device));
+  CU(cudaMalloc(dev_ptr_out, size_t(bytes)));  // its own allocation: IPC needs the base
+  CU(cudaMemset(*dev_ptr_out, 0, size_t(bytes)));
+  return SSQA_OK;
+}
+
+int ssqa_exchange_free(void* dev_ptr) {
+  if (dev_ptr) CU(cudaFree(dev_ptr));
+  return SSQA_OK;
+}
+
+int ssqa_ipc_handle(const void* dev_ptr, void* handle_out) {
+  if (!dev_ptr || !handle_out) return set_err(SSQA_EINVAL, "null argument");
+  cudaIpcMemHandle_t h;
+  CU(cudaIpcGetMemHandle(&h, const_cast<void*>(dev_ptr)));
+  std::memcpy(handle_out, &h, sizeof(h));
+  return SSQA_OK;
+}
+
+int ssqa_ipc_open(const void* handle, int device, void** dev_ptr_out) {
+  if (!handle || !dev_ptr_out) return set_err(SSQA_EINVAL, "null argument");
+  CU(cudaSetDevice(device));
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof(h));
+  CU(cudaIpcOpenMemHandle(dev_ptr_out, h, cudaIpcMemLazyEnablePeerAccess));
+  return SSQA_OK;
+}
+
+int ssqa_ipc_close(void* dev_ptr) {
+  if (!dev_ptr) return set_err(SSQA_EINVAL, "null argument");
+  CU(cudaIpcCloseMemHandle(dev_ptr));
   return SSQA_OK;
 }
 
@@ -1022,7 +1109,7 @@ int ssqa_batch_energies(ssqa_batch b, double* out) {
   CU(cudaMemcpyAsync(E.data(), b->d_E, E.size() * sizeof(long long), cudaMemcpyDeviceToHost,
                      st));
   CU(cudaStreamSynchronize(st));
-  if (tmp) cudaFree(S);
+  if (tmp) pool_free(S);
   const double scale = b->prob->q.scale, offset = b->prob->q.offset;
   for (int t = 0; t < g.T; ++t)
     for (int k = 0; k < g.R; ++k)

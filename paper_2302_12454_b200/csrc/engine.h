@@ -124,7 +124,8 @@ struct ssqa_batch_s {
   std::vector<double> ssa_levels;  // SsaParams::i0_levels()
   double* d_i0 = nullptr;          // [sc+1] i0_schedule table (SSA only)
   int32_t* d_S = nullptr;     // SIMT engine: integer fields [ccols][npad]
-  long long* d_E = nullptr;   // per-column integer energy sum E' [ccols]
+  long long* d_E = nullptr;
+  unsigned* d_push_ctr = nullptr;  // peer push: blocks done in the current pack (ssqa_batch_shard_pass_to)   // per-column integer energy sum E' [ccols]
 
   // per-trial results
   double* d_best_e = nullptr;

@@ -186,10 +186,36 @@ __global__ void k_scan(Geom g, const long long* __restrict__ E, ScanArgs a,
 // ---- GPU row shards: exchange chunk of one shard =
 // [ccols][nwords] bit-packed spin rows (bit r of word w: row row0 + 32w + r
 // is +1) followed by [ccols] int64 energy partials.
+// Peer push (ssqa_batch_shard_pass_to): the chunk goes straight into every
+// destination -- the shard's slot of each GPU's exchange region, peer memory
+// over NVLink -- and the last block to finish raises each destination's flag
+// for this shard to `epoch` (system-scope release after every block's
+// system-scope fence): the all-gather is the pack kernel's own stores.
+__device__ __forceinline__ void push_word(const PeerPush& pp, size_t byte_off, uint32_t v) {
+  for (int d = 0; d < pp.n; ++d) *reinterpret_cast<uint32_t*>(pp.dst[d] + byte_off) = v;
+}
+__device__ __forceinline__ void push_i64(const PeerPush& pp, size_t byte_off, long long v) {
+  for (int d = 0; d < pp.n; ++d) *reinterpret_cast<long long*>(pp.dst[d] + byte_off) = v;
+}
+__device__ __forceinline__ void push_signal(const PeerPush& pp) {
+  if (!pp.counter) return;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    const unsigned done = atomicAdd(pp.counter, 1u);
+    if (done == gridDim.x - 1) {  // every block's stores are fenced: publish
+      __threadfence_system();
+      for (int d = 0; d < pp.n; ++d)
+        asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(pp.flag[d]), "r"(pp.epoch)
+                     : "memory");
+      *pp.counter = 0u;  // next pass
+    }
+  }
+}
+
 __global__ void k_shard_pack(Geom g, const int8_t* __restrict__ slot, int row0, int nwords,
-                             const unsigned long long* __restrict__ E, uint8_t* __restrict__ chunk) {
-  uint32_t* bits = reinterpret_cast<uint32_t*>(chunk);
-  long long* e_out = reinterpret_cast<long long*>(chunk + size_t(g.ccols) * nwords * 4);
+                             const unsigned long long* __restrict__ E, PeerPush pp) {
+  const size_t e_off = size_t(g.ccols) * nwords * 4;
   const size_t total = size_t(g.ccols) * nwords;
   for (size_t x = blockIdx.x * size_t(blockDim.x) + threadIdx.x; x < total;
        x += size_t(gridDim.x) * blockDim.x) {
@@ -203,19 +229,18 @@ __global__ void k_shard_pack(Geom g, const int8_t* __restrict__ slot, int row0, 
     for (int q = 0; q < 8; ++q)
 #pragma unroll
       for (int y = 0; y < 4; ++y) word |= uint32_t(int8_t(v[q] >> (8 * y)) > 0) << (4 * q + y);
-    bits[x] = word;
+    push_word(pp, x * 4, word);
   }
   for (int col = blockIdx.x * blockDim.x + threadIdx.x; col < g.ccols; col += gridDim.x * blockDim.x)
-    e_out[col] = static_cast<long long>(E[col]);
+    push_i64(pp, e_off + size_t(col) * 8, static_cast<long long>(E[col]));
+  push_signal(pp);
 }
 
 // FP4 spin slots (two e2m1 nibbles per byte, lower row in the low nibble,
 // bit 3 = negative): the same bit-packed chunk from 16 bytes per 32 rows.
 __global__ void k_shard_pack_fp4(Geom g, const uint8_t* __restrict__ slot4, int row0, int nwords,
-                                 const unsigned long long* __restrict__ E,
-                                 uint8_t* __restrict__ chunk) {
-  uint32_t* bits = reinterpret_cast<uint32_t*>(chunk);
-  long long* e_out = reinterpret_cast<long long*>(chunk + size_t(g.ccols) * nwords * 4);
+                                 const unsigned long long* __restrict__ E, PeerPush pp) {
+  const size_t e_off = size_t(g.ccols) * nwords * 4;
   const size_t total = size_t(g.ccols) * nwords;
   for (size_t x = blockIdx.x * size_t(blockDim.x) + threadIdx.x; x < total;
        x += size_t(gridDim.x) * blockDim.x) {
@@ -229,16 +254,29 @@ __global__ void k_shard_pack_fp4(Geom g, const uint8_t* __restrict__ slot4, int 
 #pragma unroll
       for (int y = 0; y < 8; ++y)  // nibble y of word q = row 8q + y; positive when bit 3 clear
         word |= uint32_t(((v[q] >> (4 * y + 3)) & 1u) == 0u) << (8 * q + y);
-    bits[x] = word;
+    push_word(pp, x * 4, word);
   }
   for (int col = blockIdx.x * blockDim.x + threadIdx.x; col < g.ccols; col += gridDim.x * blockDim.x)
-    e_out[col] = static_cast<long long>(E[col]);
+    push_i64(pp, e_off + size_t(col) * 8, static_cast<long long>(E[col]));
+  push_signal(pp);
 }
 
 __global__ void k_shard_unpack(Geom g, int8_t* __restrict__ slot, uint8_t* __restrict__ slot4,
                                const uint8_t* __restrict__ all,
                                size_t chunk_bytes, int nshards, int rows_per_shard,
-                               int with_spins, long long* __restrict__ E) {
+                               int with_spins, long long* __restrict__ E, PeerWait pw) {
+  if (pw.flags) {
+    // peer push: every shard's chunk of this epoch has landed once its flag
+    // reads `epoch` (system-scope acquire)
+    if (threadIdx.x < pw.n) {
+      unsigned v;
+      do {
+        asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(pw.flags + threadIdx.x)
+                     : "memory");
+      } while (int(v - pw.epoch) < 0);
+    }
+    __syncthreads();
+  }
   const int nwords = rows_per_shard / 32;
   if (with_spins) {
     const size_t total = size_t(nshards) * g.ccols * nwords;
@@ -286,21 +324,20 @@ __global__ void k_shard_unpack(Geom g, int8_t* __restrict__ slot, uint8_t* __res
 }
 
 void launch_shard_pack(const Geom& g, const int8_t* slot, int row0, int rows,
-                       const unsigned long long* E, void* chunk, cudaStream_t st) {
-  k_shard_pack<<<1184, 256, 0, st>>>(g, slot, row0, rows / 32, E, static_cast<uint8_t*>(chunk));
+                       const unsigned long long* E, const PeerPush& pp, cudaStream_t st) {
+  k_shard_pack<<<1184, 256, 0, st>>>(g, slot, row0, rows / 32, E, pp);
 }
 
 void launch_shard_pack_fp4(const Geom& g, const uint8_t* slot4, int row0, int rows,
-                           const unsigned long long* E, void* chunk, cudaStream_t st) {
-  k_shard_pack_fp4<<<1184, 256, 0, st>>>(g, slot4, row0, rows / 32, E,
-                                         static_cast<uint8_t*>(chunk));
+                           const unsigned long long* E, const PeerPush& pp, cudaStream_t st) {
+  k_shard_pack_fp4<<<1184, 256, 0, st>>>(g, slot4, row0, rows / 32, E, pp);
 }
 
 void launch_shard_unpack(const Geom& g, int8_t* slot, uint8_t* slot4, const void* all,
                          size_t chunk_bytes, int nshards, int rows_per_shard, bool with_spins,
-                         long long* E, cudaStream_t st) {
+                         long long* E, const PeerWait& pw, cudaStream_t st) {
   k_shard_unpack<<<1184, 256, 0, st>>>(g, slot, slot4, static_cast<const uint8_t*>(all), chunk_bytes,
-                                       nshards, rows_per_shard, with_spins ? 1 : 0, E);
+                                       nshards, rows_per_shard, with_spins ? 1 : 0, E, pw);
 }
 
 void launch_init(const Geom& g, const uint64_t* seeds, int8_t* sig, double* acc,

@@ -57,15 +57,32 @@ void launch_init(const Geom& g, const uint64_t* seeds, int8_t* sig, double* acc,
 // GPU row shards: pack rows [row0, row0+rows) of every column of an int8
 // spin slot (bit-packed) plus the energy partials into one exchange chunk;
 // unpack all shards' chunks into the slot and sum their energy partials.
+// Where a shard's exchange chunk goes: n destinations (the caller's own
+// buffer, or the shard's slot in every GPU's exchange region through peer
+// pointers); counter != nullptr: the last block then raises flag[d] = epoch.
+constexpr int kMaxPeers = 8;
+struct PeerPush {
+  uint8_t* dst[kMaxPeers];
+  unsigned* flag[kMaxPeers];
+  unsigned* counter;
+  unsigned epoch;
+  int n;
+};
+// Before unpacking: wait until flags[0..n) all reach epoch (flags == nullptr: no wait).
+struct PeerWait {
+  const unsigned* flags;
+  unsigned epoch;
+  int n;
+};
 void launch_shard_pack(const Geom& g, const int8_t* slot, int row0, int rows,
-                       const unsigned long long* E, void* chunk, cudaStream_t st);
+                       const unsigned long long* E, const PeerPush& pp, cudaStream_t st);
 // FP4 slot variant of launch_shard_pack (tcgen05 FP4 / FP4-pair shard passes).
 void launch_shard_pack_fp4(const Geom& g, const uint8_t* slot4, int row0, int rows,
-                           const unsigned long long* E, void* chunk, cudaStream_t st);
+                           const unsigned long long* E, const PeerPush& pp, cudaStream_t st);
 // slot4 (nullable): also write the FP4 image of the gathered spins.
 void launch_shard_unpack(const Geom& g, int8_t* slot, uint8_t* slot4, const void* all,
                          size_t chunk_bytes, int nshards, int rows_per_shard, bool with_spins,
-                         long long* E, cudaStream_t st);
+                         long long* E, const PeerWait& pw, cudaStream_t st);
 void launch_reset_results(int T, long sc, double* best_e, int* best_k, int* reached,
                           long* first_hit, long* cycles_used, int* active, cudaStream_t st);
 void launch_field_simt(const Geom& g, const int8_t* J, const int8_t* sig, int32_t* S,

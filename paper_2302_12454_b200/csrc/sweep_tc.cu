@@ -20,6 +20,7 @@
 // Between sweeps the CTA synchronises once, scans its trials
 // (annealer.cpp:327-345) and advances the spin-slot ring.  No grid-wide sync:
 // a tile's columns depend only on its own spins (F[:, cols] = J' sigma[:, cols]).
+#include "devpool.h"
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -2031,10 +2032,13 @@ int launch(ssqa_batch_s* b, TcParams& P, bool f4) {
     const size_t bytes = size_t(2) * g.ccols * 8 + size_t(g.ntiles) * 8 +
                          size_t(g.ntiles) * nrt_all * 4 + size_t(g.ntiles) * 4 + 64;
     if (b->split_bytes < bytes) {
-      if (b->d_split) cudaFree(b->d_split);
+      if (b->d_split) {
+        cudaStreamSynchronize(b->prob->stream);  // the last launch may still use it
+        pool_free(b->d_split);
+      }
       b->d_split = nullptr;
       b->split_bytes = 0;
-      if (cudaMalloc(&b->d_split, bytes) != cudaSuccess) {
+      if (pmalloc(&b->d_split, bytes) != cudaSuccess) {
         g_tc_err = "row-split state allocation failed";
         return SSQA_ECUDA;
       }
@@ -2090,7 +2094,7 @@ int launch(ssqa_batch_s* b, TcParams& P, bool f4) {
   long long* dbg = nullptr;
   const int dbg_rts = 4096;
   if (trace_path) {
-    cudaMalloc(&dbg, sizeof(long long) * 4 * dbg_rts * 2);
+    pmalloc(&dbg, sizeof(long long) * 4 * dbg_rts * 2);
     cudaMemsetAsync(dbg, 0, sizeof(long long) * 4 * dbg_rts * 2, b->prob->stream);
     P.dbg = dbg;
     P.dbg_rts = dbg_rts;
@@ -2147,7 +2151,7 @@ int launch(ssqa_batch_s* b, TcParams& P, bool f4) {
     std::vector<long long> h(size_t(4) * dbg_rts * 2);
     cudaStreamSynchronize(b->prob->stream);
     cudaMemcpy(h.data(), dbg, h.size() * sizeof(long long), cudaMemcpyDeviceToHost);
-    cudaFree(dbg);
+    pool_free(dbg);
     if (FILE* f = fopen(trace_path, "wb")) {
       fwrite(h.data(), sizeof(long long), h.size(), f);
       fclose(f);

@@ -8,14 +8,23 @@ partials -- after which every GPU holds the full sigma(c+1), sums the
 energies and scans the cycle exactly as run_lattice (annealer.cpp:313-361).
 Results are identical on every GPU and bitwise equal to the unsharded run.
 
-`run_row_sharded` drives it over torch.distributed (NCCL, one process per
-GPU): the all-gather is in place and is ordered on the engine's own CUDA
-stream.  `run_emulated_shards` runs G shards on ONE GPU, one after the
-other on the problem's stream with a shared exchange buffer, so the shard
-data path is exercised without any kernel waiting on another.
+`run_row_sharded` drives it over torch.distributed, one process per GPU,
+with one of two exchanges:
+* "nccl": an in-place ncclAllGather ordered on the engine's own CUDA stream;
+* "p2p": no collective library -- every GPU allocates an exchange region
+  (two halves by epoch parity + one flag per shard), maps its peers' regions
+  through CUDA IPC, and the shard pass's pack kernel stores its chunk straight
+  into every region over NVLink and raises the flags (ssqa_batch_shard_pass_to);
+  the merge waits on its own flags (ssqa_batch_shard_merge_from).
+`run_emulated_shards` runs G shards on ONE GPU, one after the other on the
+problem's stream (all passes of a cycle, then all merges), with either
+exchange, so the shard data path is exercised without any kernel waiting on
+another.
 """
 from __future__ import annotations
 
+import ctypes as C
+from dataclasses import dataclass
 from typing import List, Optional, Sequence
 
 from . import _lib
@@ -36,6 +45,69 @@ def shard_cycles(b, buf, rank: int, world: int, cycles: int, all_gather) -> None
         b.shard_merge(buf.data_ptr())
 
 
+@dataclass(frozen=True)
+class P2PLayout:
+    """One GPU's exchange region for G shards of `chunk` bytes: two data
+    halves (epoch parity) of G chunks in shard order, then G u32 flags."""
+    nshards: int
+    chunk: int
+
+    @property
+    def stride(self) -> int:  # chunk slot, 256-byte aligned
+        return (self.chunk + 255) // 256 * 256
+
+    @property
+    def half(self) -> int:
+        return self.nshards * self.stride
+
+    @property
+    def flags_off(self) -> int:
+        return 2 * self.half
+
+    @property
+    def total(self) -> int:
+        return self.flags_off + 256
+
+    def cycle_args(self, rank: int, epoch: int, bases: Sequence[int]):
+        """Pointers for one cycle of shard `rank`: its chunk's destination in
+        every region, the flag it raises in every region, and its own region's
+        chunks and flags for the merge."""
+        par = (epoch & 1) * self.half
+        dests = [b + par + rank * self.stride for b in bases]
+        flags = [b + self.flags_off + 4 * rank for b in bases]
+        return dests, flags, bases[rank] + par, bases[rank] + self.flags_off
+
+
+def shard_cycles_p2p(b, layout: P2PLayout, rank: int, bases: Sequence[int], cycles: int) -> None:
+    """The per-cycle exchange of one shard over peer memory (epoch = cycle + 1)."""
+    for c in range(cycles):
+        dests, flags, mine, own_flags = layout.cycle_args(rank, c + 1, bases)
+        b.shard_pass_to(dests, flags, c + 1)
+        b.shard_merge_from(mine, own_flags, layout.nshards, c + 1)
+
+
+class ExchangeRegion:
+    """A zeroed device block of its own (ssqa_exchange_alloc), IPC-shareable."""
+
+    def __init__(self, nbytes: int, device: int):
+        self.ptr = C.c_void_p()
+        _lib.check(_lib.lib().ssqa_exchange_alloc(device, nbytes, C.byref(self.ptr)))
+
+    @property
+    def base(self) -> int:
+        return int(self.ptr.value)
+
+    def handle(self) -> bytes:
+        h = C.create_string_buffer(64)
+        _lib.check(_lib.lib().ssqa_ipc_handle(self.ptr, h))
+        return h.raw
+
+    def close(self):
+        if self.ptr:
+            _lib.lib().ssqa_exchange_free(self.ptr)
+            self.ptr = C.c_void_p()
+
+
 def _finish(b: Batch, trials: int, opts: RunOptions) -> List[AnnealResult]:
     b.shard_end()
     res, best, tr = b.fetch(True, opts.record_trace)
@@ -44,10 +116,10 @@ def _finish(b: Batch, trials: int, opts: RunOptions) -> List[AnnealResult]:
 
 def run_row_sharded(m: IsingModel, p: SsqaParams, seeds: Sequence[int],
                     target: Optional[float] = None, opts: RunOptions = RunOptions(),
-                    device: int = 0, group=None) -> List[AnnealResult]:
+                    device: int = 0, group=None, exchange: str = "nccl") -> List[AnnealResult]:
     """ssqa_run for every seed with J' rows sharded over the ranks of `group`
     (the default process group when torch.distributed is initialised, else a
-    single shard)."""
+    single shard); exchange "nccl" (all-gather) or "p2p" (peer push)."""
     import torch
     import torch.distributed as dist
     p.validate(m.n)
@@ -57,6 +129,9 @@ def run_row_sharded(m: IsingModel, p: SsqaParams, seeds: Sequence[int],
     b = Batch(prob, p, len(seeds), opts.record_trace, _lib.ENGINE_TCGEN05)
     try:
         b.set_shard(rank, world)
+        if exchange == "p2p":
+            b.set_seeds(seeds)
+            return _run_p2p(b, p, seeds, target, opts, device, group, world, rank)
         buf = torch.empty(world * b.shard_bytes(), dtype=torch.uint8, device=f"cuda:{device}")
         stream = torch.cuda.ExternalStream(b.stream, device=f"cuda:{device}")
 
@@ -73,9 +148,41 @@ def run_row_sharded(m: IsingModel, p: SsqaParams, seeds: Sequence[int],
         prob.close()
 
 
+def _run_p2p(b, p, seeds, target, opts, device, group, world, rank):
+    import torch.distributed as dist
+    layout = P2PLayout(world, b.shard_bytes())
+    region = ExchangeRegion(layout.total, device)
+    opened = []
+    try:
+        handles = [None] * world
+        if world > 1:
+            dist.all_gather_object(handles, region.handle(), group=group)
+        bases = []
+        for g in range(world):
+            if g == rank:
+                bases.append(region.base)
+            else:
+                ptr = C.c_void_p()
+                _lib.check(_lib.lib().ssqa_ipc_open(handles[g], device, C.byref(ptr)))
+                opened.append(ptr)
+                bases.append(int(ptr.value))
+        if world > 1:
+            dist.barrier(group=group)  # every region is zeroed and mapped
+        b.shard_begin(target, opts.stop_at_target)
+        shard_cycles_p2p(b, layout, rank, bases, p.sc + 1)
+        out = _finish(b, len(seeds), opts)
+        if world > 1:
+            dist.barrier(group=group)  # no peer still writes into this region
+        return out
+    finally:
+        for ptr in opened:
+            _lib.lib().ssqa_ipc_close(ptr)
+        region.close()
+
+
 def run_emulated_shards(m: IsingModel, p: SsqaParams, seeds: Sequence[int], nshards: int,
                         target: Optional[float] = None, opts: RunOptions = RunOptions(),
-                        device: int = 0) -> List[List[AnnealResult]]:
+                        device: int = 0, exchange: str = "nccl") -> List[List[AnnealResult]]:
     """The G-shard data path on one GPU: G shard batches over one problem
     (one CUDA stream, so everything runs in order), exchanging through one
     buffer laid out as the all-gather would leave it.  Returns every shard's
@@ -90,9 +197,25 @@ def run_emulated_shards(m: IsingModel, p: SsqaParams, seeds: Sequence[int], nsha
             b.set_shard(g, nshards)
             b.set_seeds(seeds)
         nb = shards[0].shard_bytes()
-        buf = torch.empty(nshards * nb, dtype=torch.uint8, device=f"cuda:{device}")
         for b in shards:
             b.shard_begin(target, opts.stop_at_target)
+        if exchange == "p2p":
+            # one region per emulated GPU, all on this device
+            layout = P2PLayout(nshards, nb)
+            regions = [ExchangeRegion(layout.total, device) for _ in range(nshards)]
+            try:
+                bases = [r.base for r in regions]
+                for c in range(p.sc + 1):
+                    args = [layout.cycle_args(g, c + 1, bases) for g in range(nshards)]
+                    for g, b in enumerate(shards):
+                        b.shard_pass_to(args[g][0], args[g][1], c + 1)
+                    for g, b in enumerate(shards):
+                        b.shard_merge_from(args[g][2], args[g][3], nshards, c + 1)
+                return [_finish(b, len(seeds), opts) for b in shards]
+            finally:
+                for r in regions:
+                    r.close()
+        buf = torch.empty(nshards * nb, dtype=torch.uint8, device=f"cuda:{device}")
         for _ in range(p.sc + 1):
             for g, b in enumerate(shards):
                 b.shard_pass(buf[g * nb:].data_ptr())

@@ -165,20 +165,28 @@ def test_run_trials_matches_reference_kat(golden, engine):
     assert tts.kind == "finite" and t_mean > 0
 
 
-@pytest.fixture(params=["auto", "table", "fp64"])
-def epilogue(request, monkeypatch):
-    """tcgen05 fast epilogue: the engine's choice, the table path (integer
-    clamps + per-cycle smem table) or the FP64 path (update_fast2)."""
-    if request.param != "auto":
-        monkeypatch.setenv("SSQA_TC_TAB", "1" if request.param == "table" else "0")
-    return request.param
+EPILOGUES = [("simt", "auto"), ("tcgen05", "auto"), ("tcgen05", "table"), ("tcgen05", "fp64")]
 
 
-def test_full_runs_match_oracle_many_trials(orc, engine, epilogue):
+@pytest.fixture(params=EPILOGUES, ids=["-".join(e) for e in EPILOGUES])
+def engine_epi(request, monkeypatch):
+    """Engine and tcgen05 fast epilogue: the engine's choice, the table path
+    (integer clamps + per-cycle smem table) or the FP64 path (update_fast2)."""
+    eng, epi = request.param
+    engine = ENGINES[0] if eng == "simt" else ENGINES[1]
+    if not engine_ok(engine):
+        pytest.skip("engine unavailable for this build")
+    if epi == "table":
+        monkeypatch.setenv("SSQA_TC_TAB", "1")
+    elif epi == "fp64":
+        monkeypatch.setenv("SSQA_TC_TAB", "0")
+    return engine
+
+
+def test_full_runs_match_oracle_many_trials(orc, engine_epi):
     """A 48-trial batch at N=100 and N=400 (C1/C2 shapes, shortened): every
     trial equals the oracle's ssqa_run."""
-    if epilogue != "auto" and engine != _lib.ENGINE_TCGEN05:
-        pytest.skip("epilogue variants apply to tcgen05 only")
+    engine = engine_epi
     for nn, R, sc, T in [(10, 20, 300, 48), (20, 20, 60, 6)]:
         m = sq.gi_ising(nn, 0.5, 7, True, 1.0, 1.0)
         p = params(R, sc)
@@ -203,11 +211,16 @@ def operands(request, monkeypatch):
     return request.param
 
 
-def test_dense_integer_model_matches_oracle(orc, engine, operands):
+@pytest.mark.parametrize("engine,ops", [(ENGINES[0], "auto"), (ENGINES[1], "auto"),
+                                        (ENGINES[1], "int8")],
+                         ids=["simt", "tcgen05", "tcgen05-int8"])
+def test_dense_integer_model_matches_oracle(orc, monkeypatch, engine, ops):
     """C4-style dense int[-8,7] couplings (the reference's plain-double path);
     on tcgen05 as FP4 pairs (J' = A1 + A2) and as int8."""
-    if operands == "int8" and engine != _lib.ENGINE_TCGEN05:
-        pytest.skip("operand format applies to tcgen05 only")
+    if not engine_ok(engine):
+        pytest.skip("engine unavailable for this build")
+    if ops == "int8":
+        monkeypatch.setenv("SSQA_TC_FP4", "0")
     m = sq.dense_ising(200, 0, 3)
     p = params(8, 40, tau=5, bidirectional=True)
     seeds = [11, 12, 13]
@@ -510,26 +523,34 @@ def row_split(monkeypatch):
     return force
 
 
-@pytest.fixture(params=["mc", "pairs", "single"])
-def cta_pairs(request, monkeypatch):
-    """Row-split clusters: J' multicast across the column tiles of a row part
-    (2..8 tiles, opt-in), CTA pairs (cta_group::2, M = 256, even splits, the
-    default) or none."""
-    if request.param == "mc":
-        monkeypatch.setenv("SSQA_TC_MC", "1")
-    if request.param == "single":
-        monkeypatch.setenv("SSQA_TC_CTA2", "0")
-    return request.param
+def _row_split_cases():
+    """(rs, operands, cluster, epilogue) combinations that exist: every split
+    with both operand formats and every cluster mode (odd splits never pair),
+    on the default table epilogue; the FP64 epilogue once per even split."""
+    out = []
+    for rs in (2, 3, 4):
+        for ops in ("auto", "int8"):
+            for cl in ("mc", "pairs", "single"):
+                if not (rs == 3 and cl == "pairs"):
+                    out.append((rs, ops, cl, "auto"))
+        if rs % 2 == 0:
+            out.append((rs, "auto", "pairs", "fp64"))
+    return out
 
 
-@pytest.mark.parametrize("rs", [2, 3, 4])
-def test_row_split_runs_match_oracle(orc, row_split, rs, operands, cta_pairs, epilogue):
+@pytest.mark.parametrize("rs,operands,cluster,epi", _row_split_cases(),
+                         ids=["-".join(map(str, c)) for c in _row_split_cases()])
+def test_row_split_runs_match_oracle(orc, row_split, monkeypatch, rs, operands, cluster, epi):
     if not engine_ok(_lib.ENGINE_TCGEN05):
         pytest.skip("tcgen05 engine unavailable")
-    if rs == 3 and cta_pairs == "pairs":
-        pytest.skip("odd splits never pair")
-    if epilogue == "table" or (epilogue == "fp64" and (operands, cta_pairs) != ("auto", "pairs")):
-        pytest.skip("row splits default to the table epilogue; FP64 checked once")
+    if operands == "int8":
+        monkeypatch.setenv("SSQA_TC_FP4", "0")
+    if cluster == "mc":
+        monkeypatch.setenv("SSQA_TC_MC", "1")
+    if cluster == "single":
+        monkeypatch.setenv("SSQA_TC_CTA2", "0")
+    if epi == "fp64":
+        monkeypatch.setenv("SSQA_TC_TAB", "0")
     row_split(rs)
     cases = [(sq.gi_ising(20, 0.5, 7, True, 1.0, 1.0), params(20, 60), [41, 42, 43, 44, 45, 46]),
              (sq.dense_ising(400, 0, 5), params(6, 30, tau=4, bidirectional=True), [7, 8, 9])]
@@ -831,3 +852,54 @@ def test_fp4_pair_operands_match_oracle(orc, row_split, n, R, T, rs):
     J11 = J.copy()
     J11[0, 1] = 11 / 4.0
     assert sq.Problem(sq.IsingModel.from_arrays(h, J11 + J11.T, 1.5)).info()["fp4"] == 0
+
+
+@pytest.mark.gpu
+def test_pool_reuse_keeps_results_identical(orc):
+    """Repeated public calls reuse the pool's blocks (csrc/devpool.h): a second
+    batch of the same shape allocates nothing new, starts from recycled
+    (dirty) memory and still equals the oracle bit for bit."""
+    m = sq.gi_ising(10, 0.5, 7, True, 1.0, 1.0)
+    p = params(20, 120)
+    seeds = list(range(40, 52))
+    first = sq.ssqa_run_batch(m, to_sq(p), seeds, 0.0, sq.RunOptions(True, False))
+    st1 = sq.pool_stats(0)
+    assert st1["cached"] > 0
+    second = sq.ssqa_run_batch(m, to_sq(p), seeds, 0.0, sq.RunOptions(True, False))
+    st2 = sq.pool_stats(0)
+    assert st2 == st1  # every block came from, and went back to, the cache
+    for t in (0, 5, 11):
+        o = orc.ssqa_run(m.h, m.J, m.offset, p, seeds[t], 0.0, True, False)
+        for r in (first[t], second[t]):
+            assert (r.best_energy, r.best_replica, r.first_hit_cycle) == \
+                (o.best_energy, o.best_replica, o.first_hit_cycle)
+            assert np.array_equal(bits(r.trace_energy), bits(o.trace))
+    assert sq.pool_trim(0) == st2["cached"]
+    assert sq.pool_stats(0)["cached"] == 0
+
+
+@pytest.mark.gpu
+def test_fused_run_leaves_exact_lattice(orc, monkeypatch):
+    """The fused run (one launch, all sweeps): the lattice it leaves behind --
+    spins, history and every accumulator bit -- equals the oracle's after sc
+    sweeps (int8 operands keep the lattice; FP4 runs mark it stale)."""
+    if not engine_ok(_lib.ENGINE_TCGEN05):
+        pytest.skip("tcgen05 engine unavailable")
+    monkeypatch.setenv("SSQA_TC_FP4", "0")
+    m = sq.gi_ising(10, 0.5, 7, True, 1.0, 1.0)
+    for p in (params(20, 130), params(6, 90, delay=2, bidirectional=True)):
+        T = 5
+        seeds = [77 + 3 * t for t in range(T)]
+        b = sq.Batch(sq.Problem(m), to_sq(p), T, engine=_lib.ENGINE_TCGEN05)
+        b.set_seeds(seeds)
+        b.launch(None, False)
+        for t in (0, 2, 4):
+            s, a, h = orc.init_lattice(m.n, p.r, p.delay, seeds[t])
+            for c in range(p.sc):
+                orc.ssqa_sweep(m.h, m.J, m.offset, orc.jperp_schedule(c, p), p, seeds[t], c,
+                               s, a, h, c)
+            sg, ac, hi, cyc = b.read_lattice(t)
+            assert cyc == p.sc
+            assert np.array_equal(sg, s) and np.array_equal(bits(ac), bits(a)), (p.r, t)
+            assert np.array_equal(hi, h)
+        b.close()
