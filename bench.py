@@ -270,7 +270,8 @@ def run_rows(args, cfg):
 
     import paper_2302_12454_b200 as sq
     from paper_2302_12454_b200 import _lib, shard
-    from paper_2302_12454_b200.rowshard import run_row_sharded, shard_cycles
+    from paper_2302_12454_b200.rowshard import (ExchangeRegion, P2PLayout, run_row_sharded,
+                                                shard_cycles, shard_cycles_p2p)
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -298,6 +299,24 @@ def run_rows(args, cfg):
     b.set_seeds(seeds)
     buf = torch.empty(world * b.shard_bytes(), dtype=torch.uint8, device=f"cuda:{local}")
     stream = torch.cuda.ExternalStream(b.stream, device=f"cuda:{local}")
+    p2p = args.exchange == "p2p"
+    if p2p:  # exchange regions mapped across the ranks (CUDA IPC), peer push
+        import ctypes as C
+        layout = P2PLayout(world, b.shard_bytes())
+        region = ExchangeRegion(layout.total, local)
+        handles = [None] * world
+        if dist:
+            dist.all_gather_object(handles, region.handle())
+        bases, opened = [], []
+        for g in range(world):
+            if g == rank:
+                bases.append(region.base)
+            else:
+                ptr = C.c_void_p()
+                _lib.check(_lib.lib().ssqa_ipc_open(handles[g], local, C.byref(ptr)))
+                opened.append(ptr)
+                bases.append(int(ptr.value))
+        epoch = [0]
 
     def all_gather(out, mine):
         with torch.cuda.stream(stream):
@@ -305,7 +324,10 @@ def run_rows(args, cfg):
 
     def step():
         b.shard_begin(target, False)
-        shard_cycles(b, buf, rank, world, sc + 1, all_gather)
+        if p2p:
+            epoch[0] = shard_cycles_p2p(b, layout, rank, bases, sc + 1, epoch[0])
+        else:
+            shard_cycles(b, buf, rank, world, sc + 1, all_gather)
         b.shard_end()
         return b.elapsed_ms()
 
@@ -332,7 +354,8 @@ def run_rows(args, cfg):
     for i in range(max(1, args.steps)):
         barrier()
         t0 = time.perf_counter()
-        run_row_sharded(m, p, seeds, target, sq.RunOptions(False, False), local)
+        run_row_sharded(m, p, seeds, target, sq.RunOptions(False, False), local,
+                        exchange=args.exchange)
         torch.cuda.synchronize()
         e2e_times.append(time.perf_counter() - t0)
     e2e_s = shard.max_over_ranks(statistics.mean(e2e_times), dist, "cuda")
@@ -343,16 +366,18 @@ def run_rows(args, cfg):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-            "dtype": "int8 contraction (int32 acc) + f64 update",
+            "dtype": ("fp4" if b.operand_bits == 4 else "int8") + " contraction + f64 update",
             "data": "synthetic (seeded dense instance generator, seed 7)",
             "config": {"workload": cfg["desc"], "n": N, "replicas": R, "trials": T,
                        "sweeps": sc, "engine": "tcgen05 row shards",
-                       "parallelism": f"J rows x{world} (NCCL all-gather per cycle)",
+                       "parallelism": f"J rows x{world} (" + ("peer push over NVLink"
+                                      if p2p else "NCCL all-gather") + " per cycle)",
                        "l2": "no flush needed: per-step state exceeds L2"},
             "roofline": {"bound": "tensor", "achieved": tensor_tops, "peak": tc_peak,
                          "unit": "TOPS", "frac": tensor_tops / tc_peak, "traffic": None,
                          "kernel": "k_sweep_tc (one pass per cycle, own rows)",
-                         "operands": "int8",
+                         "operands": "int8-equivalent ops (the passes stream the problem's "
+                                     f"{b.operand_bits}-bit operand image)",
                          "peak_note": f"int8 dense = 2 x {peak_kind} bf16 ({bf16_peak} TF/s)"},
             "e2e": {"value": float(N) * R * T * sc / e2e_s, "unit": UNIT,
                     "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(T * (N + 40)),
@@ -361,6 +386,12 @@ def run_rows(args, cfg):
             "clocks": clk,
         }
         print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()  # no peer still pushes into this rank's region
+    if p2p:
+        for ptr in opened:
+            _lib.lib().ssqa_ipc_close(ptr)
+        region.close()
     b.close()
     prob.close()
     if dist:
@@ -576,6 +607,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--shard", default="trials", choices=["trials", "rows"],
                     help="multi-GPU layout: trial blocks per GPU (default) or J' rows per GPU")
+    ap.add_argument("--exchange", default="nccl", choices=["nccl", "p2p"],
+                    help="--shard rows: NCCL all-gather or peer push over NVLink (CUDA IPC)")
     args = ap.parse_args()
     if args.warmup < 3:
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)

@@ -1012,13 +1012,17 @@ int ssqa_batch_shard_merge_from(ssqa_batch b, const void* chunks, const unsigned
 int ssqa_exchange_alloc(int device, long long bytes, void** dev_ptr_out) {
   if (!dev_ptr_out || bytes < 1) return set_err(SSQA_EINVAL, "bad argument");
   CU(cudaSetDevice(device));
-  CU(cudaMalloc(dev_ptr_out, size_t(bytes)));  // its own allocation: IPC needs the base
+  // a pool block is a cudaMalloc allocation of its own: IPC maps it from its base
+  CU(pmalloc(dev_ptr_out, size_t(bytes)));
   CU(cudaMemset(*dev_ptr_out, 0, size_t(bytes)));
   return SSQA_OK;
 }
 
 int ssqa_exchange_free(void* dev_ptr) {
-  if (dev_ptr) CU(cudaFree(dev_ptr));
+  if (dev_ptr) {
+    CU(cudaDeviceSynchronize());  // no kernel of this process still uses it
+    pool_free(dev_ptr);
+  }
   return SSQA_OK;
 }
 

@@ -78,12 +78,19 @@ class P2PLayout:
         return dests, flags, bases[rank] + par, bases[rank] + self.flags_off
 
 
-def shard_cycles_p2p(b, layout: P2PLayout, rank: int, bases: Sequence[int], cycles: int) -> None:
-    """The per-cycle exchange of one shard over peer memory (epoch = cycle + 1)."""
-    for c in range(cycles):
-        dests, flags, mine, own_flags = layout.cycle_args(rank, c + 1, bases)
-        b.shard_pass_to(dests, flags, c + 1)
-        b.shard_merge_from(mine, own_flags, layout.nshards, c + 1)
+def shard_cycles_p2p(b, layout: P2PLayout, rank: int, bases: Sequence[int], cycles: int,
+                     epoch0: int = 0) -> int:
+    """The per-cycle exchange of one shard over peer memory.  Epochs keep
+    counting across runs on the same regions (epoch0 = the last one used):
+    a flag left at an old epoch can never satisfy a new wait.  Returns the
+    last epoch."""
+    e = epoch0
+    for _ in range(cycles):
+        e += 1
+        dests, flags, mine, own_flags = layout.cycle_args(rank, e, bases)
+        b.shard_pass_to(dests, flags, e)
+        b.shard_merge_from(mine, own_flags, layout.nshards, e)
+    return e
 
 
 class ExchangeRegion:

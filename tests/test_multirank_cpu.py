@@ -161,3 +161,53 @@ def test_row_shard_exchange_gloo_world2():
         pr.join(timeout=60)
         assert pr.exitcode == 0
     assert got == {0: list(range(5)), 1: list(range(5))}
+
+
+def _p2p_worker(rank, world, port, out_q):
+    import torch.distributed as dist
+    from paper_2302_12454_b200.rowshard import P2PLayout
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    layout = P2PLayout(world, 12345)
+    # stand-ins for the region bases each rank maps (its own + IPC peers)
+    mine = 1 << 40 | rank << 32
+    bases = [None] * world
+    dist.all_gather_object(bases, mine)
+    plan = {}
+    for epoch in (1, 2, 3):
+        plan[epoch] = layout.cycle_args(rank, epoch, bases)
+    out_q.put((rank, bases, plan))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_peer_push_layout_agrees_across_ranks():
+    """world_size-2 gloo run of the peer-push bookkeeping (rowshard.P2PLayout):
+    where rank r pushes its chunk and flag in region d is exactly where rank
+    d's merge reads shard r, the two epoch parities never overlap, and the
+    flags sit past both data halves."""
+    world = 2
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_p2p_worker, args=(r, world, port, q)) for r in range(world)]
+    for pr in ps:
+        pr.start()
+    got = dict((r, (b, pl)) for r, b, pl in (q.get(timeout=120) for _ in range(world)))
+    for pr in ps:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    from paper_2302_12454_b200.rowshard import P2PLayout
+    layout = P2PLayout(world, 12345)
+    assert got[0][0] == got[1][0]  # every rank sees the same bases
+    for epoch in (1, 2, 3):
+        for r in range(world):
+            dests, flags, _, _ = got[r][1][epoch]
+            for d in range(world):
+                _, _, chunks_d, flags_d = got[d][1][epoch]
+                assert dests[d] == chunks_d + r * layout.stride
+                assert flags[d] == flags_d + 4 * r
+                assert dests[d] + layout.chunk <= got[d][0][d] + layout.flags_off
+        a = got[0][1][epoch][2]
+        b = got[0][1][epoch + 1][2] if epoch < 3 else got[0][1][epoch - 1][2]
+        assert abs(a - b) == layout.half  # consecutive epochs use the two halves
