@@ -241,6 +241,23 @@ int ssqa_batch_shard_pass_to(ssqa_batch b, void* const* dests, unsigned* const* 
                              unsigned epoch);
 int ssqa_batch_shard_merge_from(ssqa_batch b, const void* chunks, const unsigned* flags,
                                 int nflags, unsigned epoch);
+/* The exchange fused into the shard pass itself (FP4 operands with the table
+ * epilogue: ssqa_batch_shard_direct_ok): the tcgen05 epilogue stores every
+ * spin word of its rows into its own FP4 slot AND into each peer's
+ * (peer_sig4[d] = peer d's ssqa_batch_sig4 pointer, IPC-mapped; same slot
+ * ring on every GPU), its last CTA pushes the per-column int64 energy
+ * partials to peer_parts[d] (this shard's row of peer d's parts half for the
+ * epoch's parity) and raises *flags[d] = epoch.  ssqa_batch_shard_merge_direct
+ * waits on its own G flags, sums the G int64 partial rows at `parts`
+ * (part_stride bytes apart), refreshes the int8 slot from the FP4 slot and
+ * scans.
+ * No pack kernel, no staging buffer, no collective call. */
+int ssqa_batch_shard_direct_ok(ssqa_batch b);
+int ssqa_batch_sig4(ssqa_batch b, void** dev_ptr_out);
+int ssqa_batch_shard_pass_direct(ssqa_batch b, void* const* peer_sig4, void* const* peer_parts,
+                                 unsigned* const* flags, int npeer, unsigned epoch);
+int ssqa_batch_shard_merge_direct(ssqa_batch b, const void* parts, long long part_stride,
+                                  const unsigned* flags, int nflags, unsigned epoch);
 /* Exchange regions: a zeroed device block of its own (CUDA IPC maps whole
  * allocations), its 64-byte IPC handle, and the peer mapping of a handle
  * from another process of the node. */

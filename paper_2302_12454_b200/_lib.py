@@ -90,6 +90,11 @@ SIGNATURES = [
     ("ssqa_batch_shard_merge", C.c_int, [VP, VP]),
     ("ssqa_batch_shard_pass_to", C.c_int, [VP, C.POINTER(VP), C.POINTER(VP), C.c_int, C.c_uint]),
     ("ssqa_batch_shard_merge_from", C.c_int, [VP, VP, VP, C.c_int, C.c_uint]),
+    ("ssqa_batch_shard_direct_ok", C.c_int, [VP]),
+    ("ssqa_batch_sig4", C.c_int, [VP, C.POINTER(VP)]),
+    ("ssqa_batch_shard_pass_direct", C.c_int, [VP, C.POINTER(VP), C.POINTER(VP), C.POINTER(VP),
+                                               C.c_int, C.c_uint]),
+    ("ssqa_batch_shard_merge_direct", C.c_int, [VP, VP, C.c_longlong, VP, C.c_int, C.c_uint]),
     ("ssqa_exchange_alloc", C.c_int, [C.c_int, C.c_longlong, C.POINTER(VP)]),
     ("ssqa_exchange_free", C.c_int, [VP]),
     ("ssqa_ipc_handle", C.c_int, [VP, C.c_char_p]),

@@ -325,6 +325,28 @@ class Batch:
         f = (C.c_void_p * n)(*[C.c_void_p(x) for x in flags])
         check(lib().ssqa_batch_shard_pass_to(self._b, d, f, n, C.c_uint(epoch & 0xFFFFFFFF)))
 
+    def shard_direct_ok(self) -> bool:
+        return bool(lib().ssqa_batch_shard_direct_ok(self._b))
+
+    def sig4_ptr(self) -> int:
+        out = C.c_void_p()
+        check(lib().ssqa_batch_sig4(self._b, C.byref(out)))
+        return int(out.value)
+
+    def shard_pass_direct(self, peer_sig4: Sequence[int], peer_parts: Sequence[int],
+                          flags: Sequence[int], epoch: int):
+        """Shard pass with the exchange fused in (ssqa_batch_shard_pass_direct)."""
+        n = len(peer_sig4)
+        arr = lambda xs: (C.c_void_p * n)(*[C.c_void_p(x) for x in xs])
+        check(lib().ssqa_batch_shard_pass_direct(self._b, arr(peer_sig4), arr(peer_parts),
+                                                 arr(flags), n, C.c_uint(epoch & 0xFFFFFFFF)))
+
+    def shard_merge_direct(self, parts_ptr: int, part_stride: int, flags_ptr: int, nflags: int,
+                           epoch: int):
+        check(lib().ssqa_batch_shard_merge_direct(self._b, C.c_void_p(parts_ptr), part_stride,
+                                                  C.c_void_p(flags_ptr), nflags,
+                                                  C.c_uint(epoch & 0xFFFFFFFF)))
+
     def shard_merge_from(self, chunks_ptr: int, flags_ptr: int, nflags: int, epoch: int):
         """Wait for every shard's flag to reach epoch, then merge."""
         check(lib().ssqa_batch_shard_merge_from(self._b, C.c_void_p(chunks_ptr),

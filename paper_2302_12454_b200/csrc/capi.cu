@@ -911,6 +911,8 @@ int ssqa_batch_shard_begin(ssqa_batch b, int has_target, double target, int stop
 
 namespace {
 
+int shard_scan_advance(ssqa_batch b, bool upd, int dst);
+
 int shard_pass(ssqa_batch b, const PeerPush& pp) {
   if (b->cycle > b->p.sc) return set_err(SSQA_EINVAL, "run already complete");
   CU(cudaSetDevice(b->prob->device));
@@ -942,6 +944,12 @@ int shard_merge(ssqa_batch b, const void* chunks, const PeerWait& pw) {
   launch_shard_unpack(b->g, slot_ptr(b, dst), dst4, chunks, size_t(ssqa_batch_shard_bytes(b)),
                       b->nshards, b->g.npad / b->nshards, upd, b->d_E, pw, st);
   CHECK_LAUNCH();
+  return shard_scan_advance(b, upd, dst);
+}
+
+// after a merge: scan cycle c on the merged energies, advance the slot ring
+int shard_scan_advance(ssqa_batch b, bool upd, int dst) {
+  cudaStream_t st = b->prob->stream;
   ScanArgs sa{};
   sa.cycle = b->cycle;
   sa.sc = b->p.sc;
@@ -1007,6 +1015,66 @@ int ssqa_batch_shard_merge_from(ssqa_batch b, const void* chunks, const unsigned
   if (!b || !chunks || !flags) return set_err(SSQA_EINVAL, "null argument");
   if (nflags != b->nshards) return set_err(SSQA_EINVAL, "one flag per shard");
   return shard_merge(b, chunks, PeerWait{flags, epoch, nflags});
+}
+
+int ssqa_batch_shard_direct_ok(ssqa_batch b) {
+  return (b && b->engine == SSQA_ENGINE_TCGEN05 && b->prob->count == 1 && tc_shard_direct_ok(b))
+             ? 1 : 0;
+}
+
+int ssqa_batch_sig4(ssqa_batch b, void** dev_ptr_out) {
+  if (!b || !dev_ptr_out) return set_err(SSQA_EINVAL, "null argument");
+  if (!b->d_sig4) return set_err(SSQA_EUNSUP, "batch has no FP4 spin slots");
+  *dev_ptr_out = b->d_sig4;
+  return SSQA_OK;
+}
+
+int ssqa_batch_shard_pass_direct(ssqa_batch b, void* const* peer_sig4, void* const* peer_parts,
+                                 unsigned* const* flags, int npeer, unsigned epoch) {
+  if (!b || !peer_sig4 || !peer_parts || !flags) return set_err(SSQA_EINVAL, "null argument");
+  if (npeer < 1 || npeer > kMaxPeers) return set_err(SSQA_EINVAL, "1..8 peers");
+  if (b->cycle > b->p.sc) return set_err(SSQA_EINVAL, "run already complete");
+  if (!ssqa_batch_shard_direct_ok(b))
+    return set_err(SSQA_EUNSUP, "fused shard exchange needs FP4 operands and the table epilogue");
+  CU(cudaSetDevice(b->prob->device));
+  cudaStream_t st = b->prob->stream;
+  if (!b->d_push_ctr) {
+    int rc = dalloc(&b->d_push_ctr, 1);
+    if (rc) return rc;
+    CU(cudaMemsetAsync(b->d_push_ctr, 0, sizeof(unsigned), st));
+  }
+  long long delta[kMaxPeers];
+  unsigned long long* parts[kMaxPeers];
+  for (int d = 0; d < npeer; ++d) {
+    if (!peer_sig4[d] || !peer_parts[d] || !flags[d]) return set_err(SSQA_EINVAL, "null peer");
+    delta[d] = reinterpret_cast<const char*>(peer_sig4[d]) - reinterpret_cast<const char*>(b->d_sig4);
+    parts[d] = static_cast<unsigned long long*>(peer_parts[d]);
+  }
+  const int nrt = b->g.npad / 128 / b->nshards;
+  CU(cudaMemsetAsync(b->d_E, 0, size_t(b->g.ccols) * sizeof(long long), st));
+  int rc = tc_shard_pass_direct(b, b->shard * nrt, nrt, reinterpret_cast<unsigned long long*>(b->d_E),
+                                delta, parts, flags, npeer, epoch, b->d_push_ctr);
+  if (rc) return set_err(rc, tc_last_error());
+  b->launches += 1;
+  return SSQA_OK;
+}
+
+int ssqa_batch_shard_merge_direct(ssqa_batch b, const void* parts, long long part_stride,
+                                  const unsigned* flags, int nflags, unsigned epoch) {
+  if (!b || !parts || !flags) return set_err(SSQA_EINVAL, "null argument");
+  if (part_stride < (long long)b->g.ccols * 8 || part_stride % 8)
+    return set_err(SSQA_EINVAL, "partial rows need ccols * 8 bytes, 8-aligned");
+  if (nflags != b->nshards) return set_err(SSQA_EINVAL, "one flag per shard");
+  if (b->cycle > b->p.sc) return set_err(SSQA_EINVAL, "run already complete");
+  CU(cudaSetDevice(b->prob->device));
+  cudaStream_t st = b->prob->stream;
+  const bool upd = b->cycle < b->p.sc;
+  const int dst = upd ? pick_free(b) : b->cur;
+  launch_shard_merge_direct(b->g, slot_ptr(b, dst), b->d_sig4 + size_t(dst) * b->slot_elems / 2,
+                            parts, size_t(part_stride), b->nshards, upd, b->d_E,
+                            PeerWait{flags, epoch, nflags}, st);
+  CHECK_LAUNCH();
+  return shard_scan_advance(b, upd, dst);
 }
 
 int ssqa_exchange_alloc(int device, long long bytes, void** dev_ptr_out) {

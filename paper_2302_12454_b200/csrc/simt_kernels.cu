@@ -323,6 +323,61 @@ __global__ void k_shard_unpack(Geom g, int8_t* __restrict__ slot, uint8_t* __res
   }
 }
 
+// Fused exchange (tc_shard_pass_direct): the peers' passes already stored
+// their spin rows into this GPU's FP4 slot; once every shard's flag reads
+// `epoch`, sum the pushed energy partials [nshards][ccols] and refresh the
+// int8 slot (scan, best states) from the FP4 slot.
+__global__ void k_shard_merge_direct(Geom g, int8_t* __restrict__ slot,
+                                     const uint8_t* __restrict__ slot4,
+                                     const uint8_t* __restrict__ parts, size_t part_stride,
+                                     int nshards, int with_spins, long long* __restrict__ E,
+                                     PeerWait pw) {
+  if (threadIdx.x < pw.n) {
+    unsigned v;
+    do {
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(pw.flags + threadIdx.x)
+                   : "memory");
+    } while (int(v - pw.epoch) < 0);
+  }
+  __syncthreads();
+  if (with_spins) {
+    const size_t total = size_t(g.ccols) * (g.npad / 32);  // 32 rows = 16 bytes of nibbles
+    for (size_t x = blockIdx.x * size_t(blockDim.x) + threadIdx.x; x < total;
+         x += size_t(gridDim.x) * blockDim.x) {
+      const int4 a = __ldcg(reinterpret_cast<const int4*>(slot4) + x);
+      const uint32_t w[4] = {uint32_t(a.x), uint32_t(a.y), uint32_t(a.z), uint32_t(a.w)};
+      uint32_t o[8];
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          uint32_t b4 = 0;
+#pragma unroll
+          for (int y = 0; y < 4; ++y)  // nibble 4h + y of word q: bit 3 = negative
+            b4 |= (((w[q] >> (4 * (4 * h + y) + 3)) & 1u) ? 0xFFu : 0x01u) << (8 * y);
+          o[2 * q + h] = b4;
+        }
+      int4* dst = reinterpret_cast<int4*>(slot) + 2 * x;
+      dst[0] = make_int4(int(o[0]), int(o[1]), int(o[2]), int(o[3]));
+      dst[1] = make_int4(int(o[4]), int(o[5]), int(o[6]), int(o[7]));
+    }
+  }
+  for (int col = blockIdx.x * blockDim.x + threadIdx.x; col < g.ccols; col += gridDim.x * blockDim.x) {
+    long long e = 0;
+    for (int sh = 0; sh < nshards; ++sh)
+      e += __ldcg(reinterpret_cast<const long long*>(parts + size_t(sh) * part_stride) + col);
+    E[col] = e;
+  }
+}
+
+void launch_shard_merge_direct(const Geom& g, int8_t* slot, const uint8_t* slot4,
+                               const void* parts, size_t part_stride, int nshards,
+                               bool with_spins, long long* E, const PeerWait& pw,
+                               cudaStream_t st) {
+  k_shard_merge_direct<<<1184, 256, 0, st>>>(g, slot, slot4, static_cast<const uint8_t*>(parts),
+                                             part_stride, nshards, with_spins ? 1 : 0, E, pw);
+}
+
 void launch_shard_pack(const Geom& g, const int8_t* slot, int row0, int rows,
                        const unsigned long long* E, const PeerPush& pp, cudaStream_t st) {
   k_shard_pack<<<1184, 256, 0, st>>>(g, slot, row0, rows / 32, E, pp);

@@ -79,6 +79,13 @@ void launch_shard_pack(const Geom& g, const int8_t* slot, int row0, int rows,
 // FP4 slot variant of launch_shard_pack (tcgen05 FP4 / FP4-pair shard passes).
 void launch_shard_pack_fp4(const Geom& g, const uint8_t* slot4, int row0, int rows,
                            const unsigned long long* E, const PeerPush& pp, cudaStream_t st);
+// Fused exchange: wait for the peers' flags, sum the nshards int64 partial
+// rows (part_stride bytes apart) into E, expand the FP4 slot into the int8
+// slot (with_spins).
+void launch_shard_merge_direct(const Geom& g, int8_t* slot, const uint8_t* slot4,
+                               const void* parts, size_t part_stride, int nshards,
+                               bool with_spins, long long* E, const PeerWait& pw,
+                               cudaStream_t st);
 // slot4 (nullable): also write the FP4 image of the gathered spins.
 void launch_shard_unpack(const Geom& g, int8_t* slot, uint8_t* slot4, const void* all,
                          size_t chunk_bytes, int nshards, int rows_per_shard, bool with_spins,

@@ -99,6 +99,17 @@ struct TcParams {
   // entries per neighbour-sign combination
   int tab_lo1, tab_hi, tab_w;
   int pf_dist;  // J' L2 prefetch distance in K chunks (0: off)
+  // Shard passes with the exchange fused in (run_mode 2, npeer > 0; FP4 table
+  // epilogue): every spin word also goes to each peer GPU's FP4 slot at the
+  // same offset (peer_delta[d] = peer slot base - own slot base, bytes, over
+  // NVLink), and the last CTA of the pass pushes the energy partials to
+  // peer_E[d] and raises *peer_flag[d] = epoch (system-scope release).
+  int npeer;
+  long long peer_delta[8];
+  unsigned long long* peer_E[8];
+  unsigned* peer_flag[8];
+  unsigned epoch;
+  unsigned* push_ctr;
   int use_tab;  // fast mode: table epilogue (row splits) instead of update_fast2
   int mc_q;     // CL == 2: column tiles per cluster (= ntiles), sharing each J' tile
   long long* dbg;  // optional timeline (block 0): [role][rt_global][2] clock64 stamps
@@ -678,6 +689,8 @@ struct EpiRow {
   bool w_row;               // spin row exists (i < n)
   uint8_t* dst_w;           // FP4 word stores: byte of rows (warp row 0) + 8*(lane&3)
   uint32_t nib_live;        // FP4 word stores: nibble mask of the live rows of that word
+  int npeer;                // fused shard exchange: peers that get every spin word too
+  const long long* peer_delta;  // TcParams::peer_delta
 };
 
 // Table epilogue constants for one cycle.  With X = S + H' + noise * NR the
@@ -953,6 +966,12 @@ __device__ __forceinline__ void epi_chunks(const EpiRow& er, const UpdateConsts&
       } else {
         st_u32_if(reinterpret_cast<uint32_t*>(er.dst_w + (cw.x >> 1)), word,
                   (cw.y & 0x80000000u) && er.nib_live);
+        if (TAB && er.npeer) {
+          // fused shard exchange: the same word into every peer's slot
+          for (int d = 0; d < er.npeer; ++d)
+            st_u32_if(reinterpret_cast<uint32_t*>(er.dst_w + er.peer_delta[d] + (cw.x >> 1)), word,
+                      (cw.y & 0x80000000u) && er.nib_live);
+        }
       }
     }
     __syncwarp();
@@ -1611,6 +1630,8 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
             er.nib_live = nl >= 8 ? 0xffffffffu : ((1u << (4 * nl)) - 1u);
             er.dst_w = sig_dst + ((rt_lo + rt) * kBM + q * 32) / 2 + 4 * (lane & 3);
           }
+          er.npeer = P.npeer;
+          er.peer_delta = P.peer_delta;
 #define SSQA_EPI(B, S, F, T)                                                               \
   epi_chunks<B, S, F, F4, T>(er, uc, fc, tc, i2d, ctl, acc_ring, c_col, q_sum, trow, \
                              sub, kSubs, nchunk, nps, cnt0, il, lane)
@@ -1663,6 +1684,34 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
         // host all-gathers them with the shard's spin rows and scans
         for (int cl = ew * 32 + lane; cl < NT; cl += EPI * 32)
           atomicAdd(P.gE + col0 + cl, static_cast<unsigned long long>(cta_energy(cl)));
+        if (P.npeer) {
+          // fused exchange: this CTA's spin words (peer stores) and energy
+          // atomics are done; the last CTA of the pass pushes the summed
+          // partials to every peer and raises their flags
+          epi_bar<EPI>();
+          if (ew == 0 && lane == 0) {
+            __threadfence_system();
+            const unsigned done = atomicAdd(P.push_ctr, 1u);
+            __threadfence();
+            ctl->scan_me = done == gridDim.x - 1u;
+          }
+          epi_bar<EPI>();
+          if (ctl->scan_me) {
+            for (int col = ew * 32 + lane; col < g.ccols; col += EPI * 32) {
+              const unsigned long long v = __ldcg(P.gE + col);
+              for (int d = 0; d < P.npeer; ++d) P.peer_E[d][col] = v;
+            }
+            epi_bar<EPI>();
+            if (ew == 0 && lane == 0) {
+              __threadfence_system();
+              for (int d = 0; d < P.npeer; ++d)
+                asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(P.peer_flag[d]),
+                             "r"(P.epoch)
+                             : "memory");
+              *P.push_ctr = 0u;  // next pass
+            }
+          }
+        }
       }
       if (split && scan_mode && !drain) {
         // Row split: add this CTA's row partials to the column tile's pass
@@ -2000,7 +2049,7 @@ int launch(ssqa_batch_s* b, TcParams& P, bool f4) {
   // Table epilogue for row splits: their MMAs keep the tensor core busy, and
   // the FP64 units share its issue path; the FP64 epilogue is cheaper where
   // they are mostly free (C3: 1146 vs 1178 ms/step).  SSQA_TC_TAB=0/1 forces.
-  P.use_tab = (P.fast && P.tab_w > 0 && g.rs > 1) ? 1 : 0;
+  P.use_tab = (P.fast && P.tab_w > 0 && (g.rs > 1 || P.npeer)) ? 1 : 0;
   if (const char* t = getenv("SSQA_TC_TAB")) P.use_tab = (P.fast && P.tab_w > 0 && atoi(t)) ? 1 : 0;
   CUtensorMap maps[4];
   const uint64_t srows = uint64_t(b->nslots) * g.ccols;
@@ -2358,6 +2407,44 @@ int tc_shard_pass(ssqa_batch_s* b, int rt0, int nrt, unsigned long long* gE) {
   int rc = launch(b, P, tc_uses_fp4(b));
   if (rc) return rc;
   return SSQA_OK;
+}
+
+// The fused exchange needs FP4 operands and the table epilogue (its spin
+// words are what goes to the peers).
+bool tc_shard_direct_ok(ssqa_batch_s* b) {
+  if (!tc_uses_fp4(b)) return false;
+  TcParams P = base_params(b);
+  return P.fast && P.tab_w > 0 && !getenv("SSQA_TC_TAB");
+}
+
+int tc_shard_pass_direct(ssqa_batch_s* b, int rt0, int nrt, unsigned long long* gE,
+                         const long long* peer_delta, unsigned long long* const* peer_E,
+                         unsigned* const* peer_flag, int npeer, unsigned epoch,
+                         unsigned* push_ctr) {
+  if (!tc_shard_direct_ok(b)) {
+    g_tc_err = "fused shard exchange needs FP4 operands and the table epilogue";
+    return SSQA_EUNSUP;
+  }
+  TcParams P = base_params(b);
+  P.c_first = b->cycle;
+  P.c_last = b->cycle;
+  P.sc = b->p.sc;
+  P.run_mode = 2;
+  P.shard_rt0 = rt0;
+  P.shard_nrt = nrt;
+  P.gE = gE;
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, b->prob->device);
+  P.g.rs = std::max(1, std::min(nrt, sms / std::max(1, P.g.ntiles)));
+  P.npeer = npeer;
+  for (int d = 0; d < npeer; ++d) {
+    P.peer_delta[d] = peer_delta[d];
+    P.peer_E[d] = peer_E[d];
+    P.peer_flag[d] = peer_flag[d];
+  }
+  P.epoch = epoch;
+  P.push_ctr = push_ctr;
+  return launch(b, P, true);
 }
 
 const char* tc_last_error() { return g_tc_err.c_str(); }

@@ -24,6 +24,12 @@ int tc_sweep(ssqa_batch_s* b, double jperp, double i0);
 // partials added into gE[ccols] (zeroed by the caller); the ring is not
 // advanced (the caller merges all shards' rows first).
 int tc_shard_pass(ssqa_batch_s* b, int rt0, int nrt, unsigned long long* gE);
+// Shard pass with the exchange fused in (sweep_tc.cu, TcParams::npeer).
+bool tc_shard_direct_ok(ssqa_batch_s* b);
+int tc_shard_pass_direct(ssqa_batch_s* b, int rt0, int nrt, unsigned long long* gE,
+                         const long long* peer_delta, unsigned long long* const* peer_E,
+                         unsigned* const* peer_flag, int npeer, unsigned epoch,
+                         unsigned* push_ctr);
 const char* tc_last_error();
 // Non-empty after a kernel watchdog fired: who was stuck on which mbarrier.
 std::string tc_watchdog_message();

@@ -93,6 +93,21 @@ def shard_cycles_p2p(b, layout: P2PLayout, rank: int, bases: Sequence[int], cycl
     return e
 
 
+def shard_cycles_direct(b, layout: P2PLayout, rank: int, bases: Sequence[int],
+                        sig4: Sequence[int], cycles: int, epoch0: int = 0) -> int:
+    """The per-cycle exchange fused into the shard pass (exchange "direct"):
+    the pass's epilogue stores its spin words into every GPU's FP4 slot
+    (sig4[d]) and its last CTA pushes the energy partials into slot `rank` of
+    every region; the merge waits on its own flags."""
+    e = epoch0
+    for _ in range(cycles):
+        e += 1
+        parts, flags, mine, own_flags = layout.cycle_args(rank, e, bases)
+        b.shard_pass_direct(sig4, parts, flags, e)
+        b.shard_merge_direct(mine, layout.stride, own_flags, layout.nshards, e)
+    return e
+
+
 class ExchangeRegion:
     """A zeroed device block of its own (ssqa_exchange_alloc), IPC-shareable."""
 
@@ -136,9 +151,10 @@ def run_row_sharded(m: IsingModel, p: SsqaParams, seeds: Sequence[int],
     b = Batch(prob, p, len(seeds), opts.record_trace, _lib.ENGINE_TCGEN05)
     try:
         b.set_shard(rank, world)
-        if exchange == "p2p":
+        if exchange in ("p2p", "direct"):
             b.set_seeds(seeds)
-            return _run_p2p(b, p, seeds, target, opts, device, group, world, rank)
+            return _run_p2p(b, p, seeds, target, opts, device, group, world, rank,
+                            direct=exchange == "direct")
         buf = torch.empty(world * b.shard_bytes(), dtype=torch.uint8, device=f"cuda:{device}")
         stream = torch.cuda.ExternalStream(b.stream, device=f"cuda:{device}")
 
@@ -155,28 +171,51 @@ def run_row_sharded(m: IsingModel, p: SsqaParams, seeds: Sequence[int],
         prob.close()
 
 
-def _run_p2p(b, p, seeds, target, opts, device, group, world, rank):
+def _map_peers(local_ptr: int, handle: bytes, device: int, group, world: int, rank: int,
+               opened: list) -> List[int]:
+    """All-gather one IPC handle per rank; return every rank's pointer as
+    mapped in this process (its own pointer for this rank)."""
     import torch.distributed as dist
+    handles = [None] * world
+    if world > 1:
+        dist.all_gather_object(handles, handle, group=group)
+    out = []
+    for g in range(world):
+        if g == rank:
+            out.append(local_ptr)
+        else:
+            ptr = C.c_void_p()
+            _lib.check(_lib.lib().ssqa_ipc_open(handles[g], device, C.byref(ptr)))
+            opened.append(ptr)
+            out.append(int(ptr.value))
+    return out
+
+
+def _ipc_handle(ptr: int) -> bytes:
+    h = C.create_string_buffer(64)
+    _lib.check(_lib.lib().ssqa_ipc_handle(C.c_void_p(ptr), h))
+    return h.raw
+
+
+def _run_p2p(b, p, seeds, target, opts, device, group, world, rank, direct=False):
+    import torch.distributed as dist
+    if direct and not b.shard_direct_ok():
+        raise _lib.SsqaError("the fused exchange needs FP4 operands and the table epilogue")
     layout = P2PLayout(world, b.shard_bytes())
     region = ExchangeRegion(layout.total, device)
     opened = []
     try:
-        handles = [None] * world
-        if world > 1:
-            dist.all_gather_object(handles, region.handle(), group=group)
-        bases = []
-        for g in range(world):
-            if g == rank:
-                bases.append(region.base)
-            else:
-                ptr = C.c_void_p()
-                _lib.check(_lib.lib().ssqa_ipc_open(handles[g], device, C.byref(ptr)))
-                opened.append(ptr)
-                bases.append(int(ptr.value))
+        bases = _map_peers(region.base, region.handle(), device, group, world, rank, opened)
+        if direct:
+            mine4 = b.sig4_ptr()
+            sig4 = _map_peers(mine4, _ipc_handle(mine4), device, group, world, rank, opened)
         if world > 1:
             dist.barrier(group=group)  # every region is zeroed and mapped
         b.shard_begin(target, opts.stop_at_target)
-        shard_cycles_p2p(b, layout, rank, bases, p.sc + 1)
+        if direct:
+            shard_cycles_direct(b, layout, rank, bases, sig4, p.sc + 1)
+        else:
+            shard_cycles_p2p(b, layout, rank, bases, p.sc + 1)
         out = _finish(b, len(seeds), opts)
         if world > 1:
             dist.barrier(group=group)  # no peer still writes into this region
@@ -206,18 +245,26 @@ def run_emulated_shards(m: IsingModel, p: SsqaParams, seeds: Sequence[int], nsha
         nb = shards[0].shard_bytes()
         for b in shards:
             b.shard_begin(target, opts.stop_at_target)
-        if exchange == "p2p":
+        if exchange in ("p2p", "direct"):
             # one region per emulated GPU, all on this device
             layout = P2PLayout(nshards, nb)
             regions = [ExchangeRegion(layout.total, device) for _ in range(nshards)]
             try:
                 bases = [r.base for r in regions]
+                sig4 = [b.sig4_ptr() for b in shards] if exchange == "direct" else None
                 for c in range(p.sc + 1):
                     args = [layout.cycle_args(g, c + 1, bases) for g in range(nshards)]
                     for g, b in enumerate(shards):
-                        b.shard_pass_to(args[g][0], args[g][1], c + 1)
+                        if sig4:
+                            b.shard_pass_direct(sig4, args[g][0], args[g][1], c + 1)
+                        else:
+                            b.shard_pass_to(args[g][0], args[g][1], c + 1)
                     for g, b in enumerate(shards):
-                        b.shard_merge_from(args[g][2], args[g][3], nshards, c + 1)
+                        if sig4:
+                            b.shard_merge_direct(args[g][2], layout.stride, args[g][3], nshards,
+                                                 c + 1)
+                        else:
+                            b.shard_merge_from(args[g][2], args[g][3], nshards, c + 1)
                 return [_finish(b, len(seeds), opts) for b in shards]
             finally:
                 for r in regions:

@@ -656,11 +656,16 @@ def test_row_sharded_single_rank(orc):
         assert np.array_equal(bits(res[t].trace_energy), bits(o.trace))
 
 
+@pytest.mark.parametrize("exchange", ["p2p", "direct"])
 @pytest.mark.parametrize("nshards", [1, 2, 4])
-def test_row_shards_peer_push_match_oracle(orc, nshards):
-    """The peer-push exchange (pack kernel stores into every GPU's region +
-    flags, merge waits on its flags; ssqa_batch_shard_pass_to / _merge_from),
-    G regions on one GPU: every shard equals the oracle, incl. stop-at-target."""
+def test_row_shards_peer_push_match_oracle(orc, nshards, exchange):
+    """The exchanges without a collective library, G GPUs' regions on one GPU:
+    "p2p" -- the pack kernel stores into every GPU's region + flags, the merge
+    waits on its flags (ssqa_batch_shard_pass_to / _merge_from); "direct" --
+    the tcgen05 epilogue itself stores every spin word into every GPU's FP4
+    slot and its last CTA pushes the energy partials + flags
+    (ssqa_batch_shard_pass_direct / _merge_direct).  Every shard equals the
+    oracle, incl. stop-at-target; GI (FP4) and dense int[-8,7] (FP4 pairs)."""
     if not engine_ok(_lib.ENGINE_TCGEN05):
         pytest.skip("tcgen05 engine unavailable")
     from paper_2302_12454_b200.rowshard import run_emulated_shards
@@ -671,7 +676,7 @@ def test_row_shards_peer_push_match_oracle(orc, nshards):
         target = float(orc.ssqa_run(m.h, m.J, m.offset, p, seeds[0], None, False,
                                     False).best_energy) if stop else None
         runs = run_emulated_shards(m, to_sq(p), seeds, nshards, target,
-                                   sq.RunOptions(True, stop), exchange="p2p")
+                                   sq.RunOptions(True, stop), exchange=exchange)
         for t, sd in enumerate(seeds):
             o = orc.ssqa_run(m.h, m.J, m.offset, p, sd, target, True, stop)
             for g, res in enumerate(runs):
@@ -683,14 +688,16 @@ def test_row_shards_peer_push_match_oracle(orc, nshards):
                 assert np.array_equal(bits(r.trace_energy), bits(o.trace)), (nshards, g, t)
 
 
-def test_row_sharded_single_rank_peer_push(orc):
-    """run_row_sharded(exchange="p2p") on one rank: own region, no IPC."""
+@pytest.mark.parametrize("exchange", ["p2p", "direct"])
+def test_row_sharded_single_rank_peer_push(orc, exchange):
+    """run_row_sharded(exchange=...) on one rank: own region, no IPC."""
     if not engine_ok(_lib.ENGINE_TCGEN05):
         pytest.skip("tcgen05 engine unavailable")
     from paper_2302_12454_b200.rowshard import run_row_sharded
     m = sq.dense_ising(256, 0, 2)
     p = params(8, 30, tau=5)
-    res = run_row_sharded(m, to_sq(p), [3, 4], None, sq.RunOptions(True, False), exchange="p2p")
+    res = run_row_sharded(m, to_sq(p), [3, 4], None, sq.RunOptions(True, False),
+                          exchange=exchange)
     for t, sd in enumerate([3, 4]):
         o = orc.ssqa_run(m.h, m.J, m.offset, p, sd, None, True, False)
         assert res[t].best_energy == o.best_energy
