@@ -380,21 +380,6 @@ int ssqa_problem_create(int n, const double* h, const double* J, double offset, 
           pr->d_J4 = nullptr;
         }
       }
-      // FP6 image alongside (J'/2 in e2m3) for |J'| <= 15
-      if (e == cudaSuccess && !q.fp4_ok && q.max_abs_j <= 15) {
-        st[3] = 0;
-        e = cudaMemcpyAsync(d_stats + 3, st + 3, sizeof(int), cudaMemcpyHostToDevice, pr->stream);
-        if (e == cudaSuccess) e = pmalloc(&pr->d_J6, np2 / 4 * 3);
-        if (e == cudaSuccess) {
-          launch_qfp6(pr->d_J, np2, pr->d_J6, d_stats + 3, pr->stream);
-          e = cudaMemcpyAsync(st, d_stats, sizeof(st), cudaMemcpyDeviceToHost, pr->stream);
-        }
-        if (e == cudaSuccess) e = cudaStreamSynchronize(pr->stream);
-        if (e == cudaSuccess && st[3] && pr->d_J6) {
-          pool_free(pr->d_J6);
-          pr->d_J6 = nullptr;
-        }
-      }
       if (e == cudaSuccess) e = cudaStreamSynchronize(pr->stream);
     }
   }
@@ -528,7 +513,6 @@ int ssqa_problem_destroy(ssqa_problem pr) {
   dfree(pr->d_J);
   dfree(pr->d_H);
   dfree(pr->d_J4);
-  dfree(pr->d_J6);
   dfree(pr->d_offsets);
   if (pr->stream) cudaStreamDestroy(pr->stream);
   delete pr;

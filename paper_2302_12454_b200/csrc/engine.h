@@ -84,10 +84,6 @@ struct ssqa_problem_s {
   int8_t* d_J = nullptr;
   int32_t* d_H = nullptr;
   uint8_t* d_J4 = nullptr;  // FP4 couplings (q.fp4_ok) or the FP4 pair image (q.fp4x2_ok)
-  // FP6 image of J'/2 (e2m3, 16 couplings per 12 bytes, rows of npad*3/4
-  // bytes) when J' is not FP4-exact but |J'| <= 15: one kind::f8f6f4 MMA per
-  // K block instead of the pair's two kind::mxf4 MMAs, 0.75 B per coupling
-  uint8_t* d_J6 = nullptr;
 };
 
 struct ssqa_batch_s {

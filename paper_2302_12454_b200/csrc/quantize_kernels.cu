@@ -123,40 +123,7 @@ __global__ void k_qfp4x2(const int8_t* __restrict__ Jq, int npad, uint8_t* __res
   }
 }
 
-// FP6 image (engine.h Quantized::fp6_ok): J'/2 in e2m3 (exact for |J'| <= 15,
-// half-integers up to 7.5), 16 couplings per 12 bytes, coupling k of a group
-// at bits [6k, 6k + 6) little-endian -- the packed layout the TMA's 16U6
-// type expands into 16-byte-aligned groups for kind::f8f6f4.  One thread per
-// group; not_fp6 <- 1 if some |J'| > 15.
-__global__ void k_qfp6(const int8_t* __restrict__ Jq, size_t groups, uint8_t* __restrict__ J6,
-                       int* __restrict__ not_fp6) {
-  constexpr uint8_t kCode[16] = {0, 4, 8, 12, 16, 18, 20, 22, 24, 25, 26, 27, 28, 29, 30, 31};
-  for (size_t x = blockIdx.x * size_t(blockDim.x) + threadIdx.x; x < groups;
-       x += size_t(gridDim.x) * blockDim.x) {
-    const int8_t* src = Jq + 16 * x;
-    uint32_t w[3] = {0u, 0u, 0u};
-    for (int k = 0; k < 16; ++k) {
-      const int v = src[k];
-      int m = v < 0 ? -v : v;
-      if (m > 15) {
-        atomicOr(not_fp6, 1);
-        m = 0;
-      }
-      const uint32_t c = uint32_t(kCode[m]) | (v < 0 ? 32u : 0u);
-      const int bit = 6 * k;
-      w[bit >> 5] |= c << (bit & 31);
-      if ((bit & 31) > 26) w[(bit >> 5) + 1] |= c >> (32 - (bit & 31));
-    }
-    uint8_t* dst = J6 + 12 * x;
-    for (int b = 0; b < 12; ++b) dst[b] = uint8_t(w[b >> 2] >> (8 * (b & 3)));
-  }
-}
-
 }  // namespace
-
-void launch_qfp6(const int8_t* Jq, size_t elems, uint8_t* J6, int* not_fp6, cudaStream_t st) {
-  k_qfp6<<<1184, 256, 0, st>>>(Jq, elems / 16, J6, not_fp6);
-}
 
 void launch_qfp4x2(const int8_t* Jq, int npad, uint8_t* J4, int* not_split, cudaStream_t st) {
   k_qfp4x2<<<1184, 256, 0, st>>>(Jq, npad, J4, not_split);

@@ -23,8 +23,4 @@ void launch_qfp4(const int8_t* Jq, size_t elems, uint8_t* J4, int* not_fp4, cuda
 // not_split <- 1 if some |Jq| has no split (the image is then unusable).
 void launch_qfp4x2(const int8_t* Jq, int npad, uint8_t* J4, int* not_split, cudaStream_t st);
 
-// J6 <- FP6 (e2m3) image of Jq / 2, elems couplings (multiple of 16) packed
-// 16 per 12 bytes; not_fp6 <- 1 if some |Jq| > 15.
-void launch_qfp6(const int8_t* Jq, size_t elems, uint8_t* J6, int* not_fp6, cudaStream_t st);
-
 }  // namespace ssqa_engine

@@ -104,10 +104,6 @@ struct TcParams {
   // same offset (peer_delta[d] = peer slot base - own slot base, bytes, over
   // NVLink), and the last CTA of the pass pushes the energy partials to
   // peer_E[d] and raises *peer_flag[d] = epoch (system-scope release).
-  // FP6 operands (F4 kernels, ssqa_problem_s::d_J6): J'/2 in e2m3 through a
-  // 16U6 tensor map, spins e2m1 through a 16U4 map (both expanded by the TMA
-  // into 16-byte groups), tcgen05.mma kind::f8f6f4, f32 accumulators
-  int fp6;
   int npeer;
   long long peer_delta[8];
   unsigned long long* peer_E[8];
@@ -313,13 +309,6 @@ __host__ __device__ constexpr uint32_t idesc_i8(int M, int N) {
 }
 
 
-// kind::f8f6f4: D = f32 (c_format 1), A = e2m3 (format 3), B = e2m1 (format
-// 5), both K-major.
-__host__ __device__ constexpr uint32_t idesc_f8f6f4_e2m3_e2m1(int M, int N) {
-  return (1u << 4) | (3u << 7) | (5u << 10) | (uint32_t(N >> 3) << 17) |
-         (uint32_t(M >> 4) << 24);
-}
-
 // kind::mxf4 block-scaled MMA (A, B e2m1 packed, ue8m0 scales in TMEM).
 __host__ __device__ constexpr uint32_t idesc_mxf4(int M, int N) {
   return (1u << 7) | (1u << 10) | (uint32_t(N >> 3) << 17) | (1u << 23) |
@@ -359,23 +348,6 @@ __device__ __forceinline__ void mma_i8_w(uint32_t d_tmem, uint64_t a_desc, uint6
         "{\n\t.reg .pred p, e;\n\telect.sync _|e, 0xffffffff;\n\t"
         "setp.ne.b32 p, %4, 0;\n\t"
         "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
-        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
-}
-
-template <bool CTA2>
-__device__ __forceinline__ void mma_f8f6f4_w(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
-                                             uint32_t idesc, uint32_t accumulate) {
-  if (CTA2)
-    asm volatile(
-        "{\n\t.reg .pred p, e;\n\telect.sync _|e, 0xffffffff;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "@e tcgen05.mma.cta_group::2.kind::f8f6f4 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
-        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
-  else
-    asm volatile(
-        "{\n\t.reg .pred p, e;\n\telect.sync _|e, 0xffffffff;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "@e tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
         "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
 }
 
@@ -717,7 +689,6 @@ struct EpiRow {
   bool w_row;               // spin row exists (i < n)
   uint8_t* dst_w;           // FP4 word stores: byte of rows (warp row 0) + 8*(lane&3)
   uint32_t nib_live;        // FP4 word stores: nibble mask of the live rows of that word
-  float fs;                 // F4: field = fs * TMEM value (2 for FP6: the image holds J'/2)
   int npeer;                // fused shard exchange: peers that get every spin word too
   const long long* peer_delta;  // TcParams::peer_delta
 };
@@ -811,7 +782,7 @@ __device__ __forceinline__ void epi_chunks(const EpiRow& er, const UpdateConsts&
         const uint64_t cbase = (uint64_t(ct.y) << 32) | ct.x;
         const double a_old = ab[j * kBM];
         ao[j] = a_old;
-        const int S = F4 ? __float_as_int(fmaf(__int_as_float(v[j]), er.fs, 12582912.0f)) : v[j];
+        const int S = F4 ? __float_as_int(__int_as_float(v[j]) + 12582912.0f) : v[j];
         const int s2 = S + er.h2;
         if (SIGACC) {
           // sign of a finite, never -0.0 accumulator: s2 * (+-1) on the FMA pipe
@@ -885,7 +856,7 @@ __device__ __forceinline__ void epi_chunks(const EpiRow& er, const UpdateConsts&
         const uint32_t coff = ct.z;
         const uint32_t nb = ct.w;
         const double a_old = ab[j * kBM];
-        const int S = F4 ? __float_as_int(fmaf(__int_as_float(v[j]), er.fs, 12582912.0f)) : v[j];
+        const int S = F4 ? __float_as_int(__int_as_float(v[j]) + 12582912.0f) : v[j];
         const int s2 = S + er.h2;
         if (SIGACC) {
           ep[j] = s2 * ((__double2hiint(a_old) >> 30) | 1);
@@ -940,7 +911,7 @@ __device__ __forceinline__ void epi_chunks(const EpiRow& er, const UpdateConsts&
         // FP4: the fp32 accumulator holds a small exact integer (|S| < 2^22);
         // its bits after adding 1.5*2^23 are 0x4B400000 + S, and the bias is
         // folded into the per-row constants h1/h2 (EpiRow).
-        const int S = F4 ? __float_as_int(fmaf(__int_as_float(v[j]), er.fs, 12582912.0f)) : v[j];
+        const int S = F4 ? __float_as_int(__int_as_float(v[j]) + 12582912.0f) : v[j];
         const int s2 = S + er.h2;
         int sg;
         if (SIGACC) {
@@ -1125,7 +1096,6 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
   // FP4 pairs: a stage is K = 128 couplings -- one 128-byte J'' row holding
   // 64 bytes of A1 and 64 bytes of A2 nibbles -- against 64 bytes of spins
   const bool pair = F4 && P.pair != 0;
-  const bool fp6 = F4 && P.fp6 != 0;  // 128 couplings per stage, one f8f6f4 MMA per 32
   const int b_row = pair ? kBK / 2 : kBK;
   const Layout L = make_layout(NT, g.tpt, P.stages, P.nslot, kTileRow, b_row, CTA2 ? NT / 2 : NT,
                                P.use_tab ? (P.bidirectional ? 4 : 2) * P.tab_w * 8 : 0);
@@ -1180,7 +1150,7 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
                        : rt_base + int((long long)rt_span * (part + 1) / RS) - rt_lo;  // this CTA's
   // one stage = 128 bytes of K per row: 128 int8 or 256 e2m1 couplings/spins
   // (an FP4 row of npad = 128 is a partial chunk: TMA zero-fills the rest)
-  const int NKC = (F4 && !pair && !fp6) ? (g.npad + 2 * kBK - 1) / (2 * kBK) : g.npad / kBK;
+  const int NKC = (F4 && !pair) ? (g.npad + 2 * kBK - 1) / (2 * kBK) : g.npad / kBK;
   // multi-instance problems: this tile's trial anneals its own J', H', offset
   const int j_row0 = P.multi ? tile * g.npad : 0;
   const int nchunk = NT / kCW;
@@ -1192,7 +1162,7 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
   const int rgroup = (NRT + kMaxRowGroups - 1) / kMaxRowGroups;
   const int nrg = (NRT + rgroup - 1) / rgroup;
   // spin rows covered by one K chunk of the operand stream
-  const int kKRows = (F4 && !pair && !fp6) ? 2 * kBK : kBK;
+  const int kKRows = (F4 && !pair) ? 2 * kBK : kBK;
 
   // ---- one-time setup ----
   if (threadIdx.x == 0) {
@@ -1278,8 +1248,7 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
   tc_fence_after();
   const uint32_t tmem_base = ctl->tmem_base;
   constexpr int kMmaM = CTA2 ? 2 * kBM : kBM;
-  const uint32_t idesc = fp6 ? idesc_f8f6f4_e2m3_e2m1(kMmaM, NT)
-                             : (F4 ? idesc_mxf4(kMmaM, NT) : idesc_i8(kMmaM, NT));
+  const uint32_t idesc = F4 ? idesc_mxf4(kMmaM, NT) : idesc_i8(kMmaM, NT);
   const uint32_t sf_tmem = tmem_base + kSfCol;  // unit (2^0) block scales for FP4
   if (F4) {
     // every ue8m0 scale factor is 127 = 2^0: fill the whole scale region
@@ -1424,10 +1393,7 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
               const uint64_t bd = umma_desc_sw128(b0);
 #pragma unroll
               for (int k = 0; k < kBK / 32; ++k) {
-                if (fp6)
-                  mma_f8f6f4_w<CTA2>(d_tmem, ad + uint64_t(2 * k), bd + uint64_t(2 * k), idesc,
-                                     (kc | k) ? 1u : 0u);
-                else if (F4)
+                if (F4)
                   mma_mxf4_w<CTA2>(d_tmem, ad + uint64_t(2 * k), bd + uint64_t(2 * k), idesc,
                                    (kc | k) ? 1u : 0u, sf_tmem);
                 else
@@ -1665,7 +1631,6 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
             er.dst_w = sig_dst + ((rt_lo + rt) * kBM + q * 32) / 2 + 4 * (lane & 3);
           }
           er.npeer = P.npeer;
-          er.fs = P.fp6 ? 2.0f : 1.0f;
           er.peer_delta = P.peer_delta;
 #define SSQA_EPI(B, S, F, T)                                                               \
   epi_chunks<B, S, F, F4, T>(er, uc, fc, tc, i2d, ctl, acc_ring, c_col, q_sum, trow, \
@@ -1948,23 +1913,6 @@ bool make_map(CUtensorMap* m, void* base, CUtensorMapDataType dt, uint32_t esize
   return r == CUDA_SUCCESS;
 }
 
-// 2D map over packed sub-byte rows (16U6 / 16U4_ALIGN16B): `inner` elements
-// per row, `row_bytes` apart; the TMA expands every 16 elements into a
-// 16-byte group in shared memory (box_inner must be 128).
-bool make_map_packed(CUtensorMap* m, void* base, CUtensorMapDataType dt, uint64_t inner,
-                     uint64_t rows, uint64_t row_bytes, uint32_t box_rows) {
-  EncodeFn enc = get_encode();
-  if (!enc) return false;
-  cuuint64_t dims[2] = {inner, rows};
-  cuuint64_t strides[1] = {row_bytes};
-  cuuint32_t box[2] = {128, box_rows};
-  cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(m, dt, 2, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  return r == CUDA_SUCCESS;
-}
-
 // Operand stages and per-subgroup state-ring depth inside ~226 KB: prefer
 // deep accumulator rings (up to 3 slots per subgroup, so the loader runs
 // chunks ahead of the HBM latency), then as many operand stages (<= 4) as fit.
@@ -2107,25 +2055,17 @@ int launch(ssqa_batch_s* b, TcParams& P, bool f4) {
   const uint64_t srows = uint64_t(b->nslots) * g.ccols;
   // FP4 rows are npad/2 bytes (two e2m1 values per byte)
   const uint64_t row_bytes = f4 ? uint64_t(g.npad) / 2 : uint64_t(g.npad);
-  // FP6 (e2m3 J'/2, kind::f8f6f4) instead of the FP4 pair image when the
-  // problem has one and SSQA_TC_FP6=1
-  const char* env6 = getenv("SSQA_TC_FP6");
-  const bool fp6 = f4 && b->prob->d_J6 && b->prob->count == 1 && env6 && atoi(env6) == 1;
-  P.fp6 = fp6 ? 1 : 0;
-  void* Jsrc = fp6 ? static_cast<void*>(b->prob->d_J6)
-                   : (f4 ? static_cast<void*>(b->prob->d_J4) : static_cast<void*>(b->prob->d_J));
+  void* Jsrc = f4 ? static_cast<void*>(b->prob->d_J4) : static_cast<void*>(b->prob->d_J);
   // FP4 pair image: rows of npad bytes (two planes); spin stages of 64 bytes
-  const bool pair = f4 && b->prob->q.fp4x2_ok && !fp6;
+  const bool pair = f4 && b->prob->q.fp4x2_ok;
   P.pair = pair ? 1 : 0;
   const uint64_t j_row_bytes = pair ? uint64_t(g.npad) : row_bytes;
   const uint32_t b_row = pair ? kBK / 2 : kBK;
   void* Ssrc = f4 ? static_cast<void*>(b->d_sig4) : static_cast<void*>(b->d_sig);
   const uint32_t tile_row = f4 ? kBM / 2 : kBM;
   P.sig_base = static_cast<uint8_t*>(Ssrc);
-  if (!(fp6 ? make_map_packed(&maps[0], Jsrc, CU_TENSOR_MAP_DATA_TYPE_16U6_ALIGN16B, g.npad,
-                               g.npad, uint64_t(g.npad) / 4 * 3, kBM)
-             : make_map(&maps[0], Jsrc, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, j_row_bytes,
-                        uint64_t(g.npad) * b->prob->count, kBK, kBM, CU_TENSOR_MAP_SWIZZLE_128B)) ||
+  if (!make_map(&maps[0], Jsrc, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, j_row_bytes,
+                uint64_t(g.npad) * b->prob->count, kBK, kBM, CU_TENSOR_MAP_SWIZZLE_128B) ||
       !make_map(&maps[1], Ssrc, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, row_bytes, srows, b_row,
                 g.tile_cols, pair ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B) ||
       !make_map(&maps[2], Ssrc, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, row_bytes, srows, tile_row,
@@ -2179,11 +2119,8 @@ int launch(ssqa_batch_s* b, TcParams& P, bool f4) {
   Layout L;
   auto setup = [&](bool pairs) {
     const int b_cols = pairs ? g.tile_cols / 2 : g.tile_cols;
-    if (fp6 ? !make_map_packed(&maps[1], Ssrc, CU_TENSOR_MAP_DATA_TYPE_16U4_ALIGN16B, g.npad,
-                               srows, row_bytes, uint32_t(b_cols))
-            : !make_map(&maps[1], Ssrc, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, row_bytes, srows, b_row,
-                        uint32_t(b_cols),
-                        pair ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B))
+    if (!make_map(&maps[1], Ssrc, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, row_bytes, srows, b_row,
+                  uint32_t(b_cols), pair ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B))
       return false;
     const int tab_bytes = P.use_tab ? (P.bidirectional ? 4 : 2) * P.tab_w * 8 : 0;
     L = pick_layout(g.tile_cols, g.tpt, epi / 4, int(tile_row), int(b_row), b_cols, tab_bytes,

@@ -902,34 +902,6 @@ def test_fp4_pair_operands_match_oracle(orc, row_split, n, R, T, rs):
     assert sq.Problem(sq.IsingModel.from_arrays(h, J11 + J11.T, 1.5)).info()["fp4"] == 0
 
 
-@pytest.mark.parametrize("n,R,T,rs,jmax", [(300, 8, 5, 1, 12), (640, 12, 24, 4, 12),
-                                            (384, 6, 4, 1, 15), (1024, 8, 32, 4, 15)],
-                         ids=["tile", "split", "tile-15", "split-15"])
-def test_fp6_operands_match_oracle(orc, row_split, monkeypatch, n, R, T, rs, jmax):
-    """SSQA_TC_FP6=1: couplings |J'| <= 15 stream as one e2m3 image of J'/2
-    (16U6 tensor map, kind::f8f6f4 against e2m1 spins through a 16U4 map),
-    single CTAs and row splits (CTA pairs); up to 15 the pair image cannot go."""
-    if not engine_ok(_lib.ENGINE_TCGEN05):
-        pytest.skip("tcgen05 engine unavailable")
-    monkeypatch.setenv("SSQA_TC_FP6", "1")
-    if rs > 1:
-        row_split(rs)
-    rng = np.random.default_rng(n + jmax)
-    vals = np.arange(-jmax, jmax + 1)
-    J = np.triu(rng.choice(vals, (n, n)) / 4.0, 1)
-    h = rng.integers(-40, 41, n) / 4.0
-    m = sq.IsingModel.from_arrays(h, J + J.T, 1.5)
-    p = params(R, 30, tau=4, bidirectional=(rs == 1))
-    seeds = [int(s) for s in rng.integers(0, 2 ** 40, T)]
-    res = sq.ssqa_run_batch(m, to_sq(p), seeds, None, sq.RunOptions(True, False),
-                            engine=_lib.ENGINE_TCGEN05)
-    for t in sorted({0, T // 2, T - 1}):
-        o = orc.ssqa_run(m.h, m.J, m.offset, p, seeds[t], None, True, False)
-        assert (res[t].best_energy, res[t].best_replica) == (o.best_energy, o.best_replica), t
-        assert np.array_equal(res[t].best_state, o.best_state), t
-        assert np.array_equal(bits(res[t].trace_energy), bits(o.trace)), t
-
-
 @pytest.mark.gpu
 def test_pool_reuse_keeps_results_identical(orc):
     """Repeated public calls reuse the pool's blocks (csrc/devpool.h): a second
