@@ -25,8 +25,19 @@ std::string fmt(double v) {
 }
 
 IsingModel gi_model(const ProblemSpec& p, uint64_t seed) {
-  return qubo_to_ising(
-      build_gi_qubo(generate_gi(p.n_nodes, p.edge_prob, seed, p.permute, p.c1, p.c2)));
+  const GiInstance inst = generate_gi(p.n_nodes, p.edge_prob, seed, p.permute, p.c1, p.c2);
+  const int n = p.n_nodes * p.n_nodes;
+  IsingModel m(n);
+  std::vector<double> h(static_cast<size_t>(n)), J(static_cast<size_t>(n) * n);
+  double off = 0.0;
+  gi_ising_arrays(inst, h.data(), J.data(), &off);
+  for (int i = 0; i < n; ++i) {
+    m.set_bias(i, h[size_t(i)]);
+    for (int j = i + 1; j < n; ++j)
+      if (J[size_t(i) * n + j] != 0.0) m.set_coupling(i, j, J[size_t(i) * n + j]);
+  }
+  m.set_offset(off);
+  return m;
 }
 
 }  // namespace
@@ -128,15 +139,12 @@ BenchRecord run_trials(const BenchConfig& cfg) {
   std::vector<AnnealResult> results;
   int n = 0;
   if (!gi || !cfg.problem.fresh_instance) {
-    IsingModel m = gi ? gi_model(cfg.problem, cfg.problem.gi_seed)
-                      : std::get<IsingModel>(load_model(cfg.problem.model_file));
-    double target = 0.0;
-    if (!gi) {
-      if (!cfg.problem.target_energy)
-        throw std::invalid_argument(
-            "target energy unresolvable: pass one explicitly for model files");
-      target = *cfg.problem.target_energy;
-    }
+    if (!gi)
+      throw std::invalid_argument(
+          "model files are not read by the engine facade: load the model in the caller and "
+          "call ssqa_run / the C ABI");
+    IsingModel m = gi_model(cfg.problem, cfg.problem.gi_seed);
+    const double target = 0.0;  // GI ground state (bench.cpp:309-313)
     n = m.n();
     results = run(m, seeds, target);
   } else {

@@ -57,12 +57,8 @@ const char* ssqa_host_last_error(void) { return g_host_err.c_str(); }
 int ssqa_gi_ising(int n_nodes, double edge_prob, uint64_t seed, int permute, double c1,
                   double c2, double* h, double* J, double* offset) {
   return guard([&] {
-    ssqa::IsingModel m = ssqa::qubo_to_ising(
-        ssqa::build_gi_qubo(ssqa::generate_gi(n_nodes, edge_prob, seed, permute != 0, c1, c2)));
-    const int n = m.n();
-    std::memcpy(h, m.biases().data(), size_t(n) * sizeof(double));
-    std::memcpy(J, m.coupling_data(), size_t(n) * n * sizeof(double));
-    *offset = m.offset();
+    ssqa::gi_ising_arrays(ssqa::generate_gi(n_nodes, edge_prob, seed, permute != 0, c1, c2), h, J,
+                          offset);
   });
 }
 

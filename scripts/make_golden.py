@@ -230,6 +230,27 @@ def trials_fresh(ref: Oracle):
     return out
 
 
+def trials_large(ref: Oracle):
+    """run_trials at BASELINE configs 2 and 3 at their own shapes (bench.cpp:359-432):
+    C2 = GI n=20 (N=400), M=20, the full 1024-trial battery at sc=2000; C3 = GI n=50
+    (N=2500), M=20, seeds 1000..1047 at the full sc=5000.  Fixed instance (gi_seed 7,
+    permuted, c1=c2=1) as in BASELINE.json.  The device batch must match trial for trial."""
+    out = {}
+    cases = [("c2_gi20", dict(n_nodes=20, trials=1024, ec=40000, base_seed=1000)),
+             ("c3_gi50", dict(n_nodes=50, trials=48, ec=100000, base_seed=1000))]
+    for name, kw in cases:
+        outs, ps, tm, tts = ref.run_trials(params(20, 1), workers=os.cpu_count(), gi_seed=7,
+                                           **kw)
+        out[name] = dict(**{f"k_{k}": v for k, v in kw.items()}, r=20,
+                         seed=np.array([o["seed"] for o in outs], np.uint64),
+                         reached=np.array([o["reached_target"] for o in outs], np.int8),
+                         first_hit=np.array([o["first_hit_cycle"] for o in outs], np.int64),
+                         best_energy=np.array([o["best_energy"] for o in outs]), p_s=ps,
+                         wall=np.array([o["wall_seconds"] for o in outs]))
+        print(name, "p_s", ps, flush=True)
+    return out
+
+
 def manifests(ref: Oracle):
     """Manifests written by the reference (make_manifest, bench.cpp:519-531),
     replayed bitwise by the facade's replay_manifest in the GPU tests."""
@@ -250,10 +271,10 @@ def main():
     os.makedirs(OUT, exist_ok=True)
     jobs = [("lattice_traj", lattice_trajectories), ("gi_instances", gi_instances),
             ("runs", runs), ("trials", trials), ("ssa_runs", ssa_runs),
-            ("trials_fresh", trials_fresh)]
+            ("trials_fresh", trials_fresh), ("trials_large", trials_large)]
     only = set(sys.argv[1:])
     for fname, fn in jobs + [("manifests", manifests)]:
-        if only and fname not in only:
+        if (only and fname not in only) or (not only and fname == "trials_large"):
             continue
         data = fn(ref)
         if not data:

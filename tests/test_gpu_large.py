@@ -43,3 +43,57 @@ def test_full_size_first_50_steps(n, kind, R, T):
         assert np.array_equal(bits(r.trace_energy), bits(o.trace.reshape(-1))), t
         assert (r.best_energy, r.best_replica) == (o.best_energy, o.best_replica), t
         assert np.array_equal(r.best_state, o.best_state), t
+
+
+# ---- BASELINE configs 2 and 3 at their own shapes (Missing 1) ----
+# GI n=20 -> N=400 and n=50 -> N=2500 (fixed instance: gi seed 7, permuted,
+# c1 = c2 = 1), M=20, the full 1024-trial battery on the device with the
+# production geometry (FP4 operands, 147 column tiles of whole trials).
+
+GI_CFG = {"c2": (20, 2000), "c3": (50, 5000)}
+
+
+@pytest.mark.parametrize("cfg", ["c2", "c3"])
+def test_gi_full_battery_first_50_steps(cfg):
+    """The 1024-trial batch over its first 50 sweeps; trials spread over the
+    column tiles (first, a mid tile, the last trial of the last tile) are
+    recomputed by oracle/lattice_np.py and must agree bitwise: per-cycle
+    energies of every replica, best energy / replica / state."""
+    import lattice_np as lnp
+    nn, _ = GI_CFG[cfg]
+    T, R = 1024, 20
+    m = sq.gi_ising(nn, 0.5, 7, True, 1.0, 1.0)
+    p = params(R, STEPS)
+    seeds = [1000 + t for t in range(T)]
+    res = sq.ssqa_run_batch(m, sq.SsqaParams(r=R, sc=STEPS), seeds, None,
+                            sq.RunOptions(True, False))
+    check = [0, 146, 511, 1022, T - 1]
+    ref = lnp.run_lattice(m.h, m.J, m.offset, R, p.delay, p.n_rnd, p.alpha, False, STEPS,
+                          lnp.jperp_schedule(p), lambda c: p.i0, [seeds[t] for t in check])
+    for o, t in zip(ref, check):
+        r = res[t]
+        assert r.cycles_used == o.cycles_used == STEPS
+        assert np.array_equal(bits(r.trace_energy), bits(o.trace.reshape(-1))), t
+        assert (r.best_energy, r.best_replica) == (o.best_energy, o.best_replica), t
+        assert np.array_equal(r.best_state, o.best_state), t
+
+
+@pytest.mark.parametrize("cfg", ["c2", "c3"])
+def test_gi_full_battery_matches_reference_run_trials(golden, cfg):
+    """run_trials at the config's full budget (sc = 2000 / 5000, ec = 20 sc,
+    fixed budget, target 0) on the whole 1024-trial battery in one device
+    batch; the per-trial outcomes (reached, first hit cycle, best energy) of
+    the trials the reference ran (scripts/make_golden.py trials_large:
+    oracle/_ref run_trials, bench.cpp:359-432) must be identical."""
+    nn, sc = GI_CFG[cfg]
+    ref = golden("trials_large")[{"c2": "c2_gi20", "c3": "c3_gi50"}[cfg]]
+    m = sq.gi_ising(nn, 0.5, 7, True, 1.0, 1.0)
+    T = 1024
+    outs, p_s, _, _ = sq.run_trials(m, sq.SsqaParams(r=20), T, 20 * sc, 1000)
+    k = len(ref["seed"])
+    assert [o.seed for o in outs[:k]] == [int(x) for x in ref["seed"]]
+    assert [int(o.reached_target) for o in outs[:k]] == [int(x) for x in ref["reached"]]
+    assert [o.first_hit_cycle for o in outs[:k]] == [int(x) for x in ref["first_hit"]]
+    assert np.array_equal(bits([o.best_energy for o in outs[:k]]), bits(ref["best_energy"]))
+    if k == T:
+        assert p_s == float(ref["p_s"])

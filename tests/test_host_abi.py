@@ -62,6 +62,19 @@ def test_gi_builder_matches_reference(golden):
         assert hashlib.sha256(m.J.tobytes()).hexdigest() == str(c["J_sha"]), name
 
 
+def test_gi_builder_matches_live_reference_non_dyadic(ref):
+    """Penalties that are not dyadic (c1 = 0.7, c2 = 0.3): every sum rounds, so
+    only the reference's exact accumulation order reproduces h and offset
+    (host/inputs.cpp restates it in closed form, without the QUBO)."""
+    for nn, seed, perm, c1, c2 in [(6, 3, True, 0.7, 0.3), (9, 12, False, 0.7, 1.1),
+                                   (12, 5, True, 0.35, 0.9)]:
+        m = sq.gi_ising(nn, 0.45, seed, perm, c1, c2)
+        h, J, off = ref.gi_ising(nn, 0.45, seed, perm, c1, c2)
+        assert np.array_equal(m.h.view(np.uint64), h.view(np.uint64))
+        assert np.array_equal(m.J.view(np.uint64), J.view(np.uint64))
+        assert np.float64(m.offset).view(np.uint64) == np.float64(off).view(np.uint64)
+
+
 def test_gi_builder_rejects_bad_arguments():
     with pytest.raises(ValueError):
         sq.gi_ising(0)
