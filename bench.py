@@ -320,6 +320,12 @@ def run_rows(args, cfg):
 
     def step():
         b.shard_begin(target, False)
+        if p2p:
+            # every rank's previous step (its last merge reads the slots peers
+            # push into) and this step's repack are done before any pass 0
+            b.synchronize()
+            if dist:
+                dist.barrier()
         if direct:
             epoch[0] = shard_cycles_direct(b, layout, rank, bases, sig4, sc + 1, epoch[0])
         elif p2p:

@@ -200,6 +200,8 @@ long ssqa_batch_launch_count(ssqa_batch b);
 /* Device time of the last ssqa_batch_launch (CUDA events recorded on the
  * batch stream around everything the launch enqueued); waits for it. */
 int ssqa_batch_elapsed_ms(ssqa_batch b, double* ms);
+/* Block until everything queued on the batch stream has finished. */
+int ssqa_batch_synchronize(ssqa_batch b);
 /* Measurement hook: time `iters` back-to-back launches of the engine's field
  * contraction on the current state (CUDA events on the batch stream) and
  * return the mean duration of one launch.  State is not modified. */

@@ -9,7 +9,7 @@ from .api import (  # noqa: F401
     SsaParams, SsqaParams, TracePoint, TrialOutcome, TtsValue, compute_tts, dense_ising,
     gi_ising, i0_schedule, init_lattice, ising_energy, jperp_schedule, pool_stats, pool_trim, replica_energies,
     run_trials, run_trials_fresh, ssa_run, ssa_run_batch, ssqa_run, ssqa_run_batch, ssqa_sweep,
-    trial_instance_seeds,
+    trial_instance_seeds, tune,
 )
 from ._lib import (  # noqa: F401
     ENGINE_AUTO, ENGINE_SIMT, ENGINE_TCGEN05, SsqaError, SsqaInvalidArgument, lib,

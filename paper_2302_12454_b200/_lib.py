@@ -50,6 +50,9 @@ SIGNATURES = [
     ("ssqa_last_error", C.c_char_p, []),
     ("ssqa_version", C.c_char_p, []),
     ("ssqa_pool_trim", C.c_longlong, [C.c_int]),
+    ("ssqa_tune_set", C.c_int, [C.c_char_p, C.c_long]),
+    ("ssqa_tune_trace", C.c_int, [C.c_char_p]),
+    ("ssqa_tune_reset", None, []),
     ("ssqa_pool_stats", C.c_int, [C.c_int, C.POINTER(C.c_longlong), C.POINTER(C.c_longlong)]),
     ("ssqa_problem_create", C.c_int, [C.c_int, DP, DP, C.c_double, C.c_int, C.POINTER(VP)]),
     ("ssqa_problem_destroy", C.c_int, [VP]),
@@ -82,6 +85,7 @@ SIGNATURES = [
     ("ssqa_batch_fetch", C.c_int, [VP, C.POINTER(ResultC), I8P, DP]),
     ("ssqa_batch_launch_count", C.c_long, [VP]),
     ("ssqa_batch_elapsed_ms", C.c_int, [VP, DP]),
+    ("ssqa_batch_synchronize", C.c_int, [C.c_void_p]),
     ("ssqa_batch_profile_field", C.c_int, [VP, C.c_int, DP]),
     ("ssqa_batch_set_shard", C.c_int, [VP, C.c_int, C.c_int]),
     ("ssqa_batch_shard_bytes", C.c_long, [VP]),

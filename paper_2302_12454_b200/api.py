@@ -284,6 +284,10 @@ class Batch:
         check(lib().ssqa_batch_elapsed_ms(self._b, C.byref(out)))
         return out.value
 
+    def synchronize(self) -> None:
+        """Wait for everything queued on the batch stream."""
+        check(lib().ssqa_batch_synchronize(self._b))
+
     def profile_field(self, iters: int = 20) -> float:
         out = C.c_double()
         check(lib().ssqa_batch_profile_field(self._b, iters, C.byref(out)))
@@ -587,13 +591,16 @@ def run_trials_fresh(n_nodes: int, p, trials: int, ec: int, base_seed: int,
     models = [gi_ising(n_nodes, edge_prob, s, permute, c1, c2)
               for s in trial_instance_seeds(base_seed, trials)]
     prob = Problem.from_models(models, device)
-    if isinstance(p, SsaParams):
-        q = SsaParams(**{**p.__dict__, "sc": ec})
-        res = ssa_run_batch(models[0], q, seeds, 0.0, RunOptions(False, False), problem=prob)
-    else:
-        q = SsqaParams(**{**p.__dict__, "sc": ec // p.r})
-        res = ssqa_run_batch(models[0], q, seeds, 0.0, RunOptions(False, False), problem=prob)
-    prob.close()
+    try:
+        if isinstance(p, SsaParams):
+            q = SsaParams(**{**p.__dict__, "sc": ec})
+            res = ssa_run_batch(models[0], q, seeds, 0.0, RunOptions(False, False), problem=prob)
+        else:
+            q = SsqaParams(**{**p.__dict__, "sc": ec // p.r})
+            res = ssqa_run_batch(models[0], q, seeds, 0.0, RunOptions(False, False),
+                                 problem=prob)
+    finally:
+        prob.close()
     outs = [TrialOutcome(s, r.reached_target, r.first_hit_cycle, r.best_energy, r.wall_seconds)
             for s, r in zip(seeds, res)]
     p_s = sum(o.reached_target for o in outs) / trials
@@ -619,3 +626,17 @@ def run_trials(m: IsingModel, p, trials: int, ec: int, base_seed: int,
     p_s = sum(o.reached_target for o in outs) / trials
     t_mean = sum(o.wall_seconds for o in outs) / trials
     return outs, p_s, t_mean, compute_tts(p_s, max(t_mean, 1e-12), p_target)
+
+
+def tune(**overrides) -> None:
+    """Engine overrides for parity tests and tuning (include/ssqa_tune.h):
+    tune(tab=1), tune(fp4=0, rs=2), ...; tune() with no arguments resets all."""
+    L = lib()
+    if not overrides:
+        L.ssqa_tune_reset()
+        return
+    for k, v in overrides.items():
+        if k == "trace":
+            L.ssqa_tune_trace(v.encode() if v else None)
+        elif L.ssqa_tune_set(k.encode(), int(v)) != 0:
+            raise ValueError(f"unknown tune key {k!r}")

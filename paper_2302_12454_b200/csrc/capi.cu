@@ -16,8 +16,16 @@
 #include "quantize_kernels.cuh"
 #include "simt_kernels.cuh"
 #include "sweep_tc.h"
+#include "../../include/ssqa_tune.h"
 
 using namespace ssqa_engine;
+
+namespace ssqa_engine {
+TuneOverrides& tune() {
+  static TuneOverrides t;
+  return t;
+}
+}  // namespace ssqa_engine
 
 namespace {
 
@@ -140,8 +148,7 @@ Geom make_geom(int n, int npad, int R, int T, int sms, int engine, bool fp4, boo
     // 0.76 ms/sweep at 192 columns vs 0.84 at 256)
     const int cap = fp4 ? 240 : 192;
     int wide = std::max(1, std::min(T, cap / R));
-    if (const char* env = getenv("SSQA_TC_WIDE"))  // tuning override: trials per wide tile
-      wide = std::max(1, std::min(wide, atoi(env)));
+    if (tune().wide > 0) wide = std::max(1, std::min(wide, tune().wide));
     const int wtiles = (T + wide - 1) / wide;
     // worth it when the wide tiling still fills the SMs with >= 2 parts per tile
     if (nrt >= 16 && wide > tpt && wtiles * 2 <= sms) {
@@ -151,8 +158,8 @@ Geom make_geom(int n, int npad, int R, int T, int sms, int engine, bool fp4, boo
       // worth one idle SM per tile from 5 parts up
       if (rs >= 5 && (rs & 1) && nrt % 2 == 0) rs -= 1;
     }
-    if (const char* env = getenv("SSQA_TC_RS")) {  // test / tuning override
-      const int want = atoi(env);
+    {
+      const int want = tune().rs;  // test / tuning override
       if (want >= 1) {
         const int tiles = (T + tpt - 1) / tpt;
         rs = std::max(1, std::min({want, nrt, std::max(1, sms / tiles)}));
@@ -258,6 +265,34 @@ int init_state(ssqa_batch_s* b) {
 extern "C" {
 
 const char* ssqa_last_error(void) { return g_err.c_str(); }
+
+int ssqa_tune_set(const char* key, long value) {
+  if (!key) return set_err(SSQA_EINVAL, "ssqa_tune_set: null key");
+  TuneOverrides& t = tune();
+  const std::string k(key);
+  const int v = int(value);
+  if (k == "tab") t.tab = v;
+  else if (k == "fp4") t.fp4 = v;
+  else if (k == "rs") t.rs = v;
+  else if (k == "wide") t.wide = v;
+  else if (k == "epi") t.epi = v;
+  else if (k == "cta2") t.cta2 = v;
+  else if (k == "mc") t.mc = v;
+  else if (k == "stages") t.stages = v;
+  else if (k == "nps") t.nps = v;
+  else if (k == "exp") t.exp = v;
+  else if (k == "pf") t.pf = v;
+  else if (k == "i16") t.i16 = v;
+  else return set_err(SSQA_EINVAL, "ssqa_tune_set: unknown key '" + k + "'");
+  return SSQA_OK;
+}
+
+int ssqa_tune_trace(const char* path) {
+  tune().trace = path ? path : "";
+  return SSQA_OK;
+}
+
+void ssqa_tune_reset(void) { tune() = TuneOverrides(); }
 const char* ssqa_version(void) { return "ssqa-b200 0.1.0"; }
 
 int ssqa_params_validate(const ssqa_params_c* p, int n) { return validate(p, n); }
@@ -600,19 +635,30 @@ int create_batch(ssqa_problem pr, const ssqa_params_c* p, int trials, int record
     ssqa_batch_destroy(b);
     return rc;
   }
-  std::vector<double> jp(size_t(p->sc) + 1);
-  for (long c = 0; c <= p->sc; ++c) jp[size_t(c)] = jperp_at(c, *p);
-  CU(cudaMemcpy(b->d_jperp, jp.data(), jp.size() * sizeof(double), cudaMemcpyHostToDevice));
-  if (levels) {
-    std::vector<double> i0t(size_t(p->sc) + 1);
-    for (long c = 0; c <= p->sc; ++c) i0t[size_t(c)] = i0_at(b, c);
-    CU(cudaMemcpy(b->d_i0, i0t.data(), i0t.size() * sizeof(double), cudaMemcpyHostToDevice));
+  // any failure from here on releases the batch (and its pool blocks)
+  auto init = [&]() -> int {
+    std::vector<double> jp(size_t(p->sc) + 1);
+    for (long c = 0; c <= p->sc; ++c) jp[size_t(c)] = jperp_at(c, *p);
+    CU(cudaMemcpy(b->d_jperp, jp.data(), jp.size() * sizeof(double), cudaMemcpyHostToDevice));
+    if (levels) {
+      std::vector<double> i0t(size_t(p->sc) + 1);
+      for (long c = 0; c <= p->sc; ++c) i0t[size_t(c)] = i0_at(b, c);
+      CU(cudaMemcpy(b->d_i0, i0t.data(), i0t.size() * sizeof(double), cudaMemcpyHostToDevice));
+    }
+    CU(cudaMemset(b->d_sig, 0, b->slot_elems * b->nslots));
+    if (b->d_sig4) CU(cudaMemset(b->d_sig4, 0, b->slot_elems * b->nslots / 2));
+    CU(cudaMemset(b->d_acc, 0, b->slot_elems * sizeof(double)));
+    CU(cudaEventCreate(&b->ev0));
+    CU(cudaEventCreate(&b->ev1));
+    return SSQA_OK;
+  };
+  rc = init();
+  if (rc) {
+    const std::string keep = g_err;
+    ssqa_batch_destroy(b);
+    g_err = keep;
+    return rc;
   }
-  CU(cudaMemset(b->d_sig, 0, b->slot_elems * b->nslots));
-  if (b->d_sig4) CU(cudaMemset(b->d_sig4, 0, b->slot_elems * b->nslots / 2));
-  CU(cudaMemset(b->d_acc, 0, b->slot_elems * sizeof(double)));
-  CU(cudaEventCreate(&b->ev0));
-  CU(cudaEventCreate(&b->ev1));
   *out = b;
   return SSQA_OK;
 }
@@ -728,6 +774,13 @@ int ssqa_batch_elapsed_ms(ssqa_batch b, double* ms) {
   float f = 0.f;
   CU(cudaEventElapsedTime(&f, b->ev0, b->ev1));
   *ms = double(f);
+  return SSQA_OK;
+}
+
+int ssqa_batch_synchronize(ssqa_batch b) {
+  if (!b) return set_err(SSQA_EINVAL, "null batch");
+  CU(cudaSetDevice(b->prob->device));
+  CU(cudaStreamSynchronize(b->prob->stream));
   return SSQA_OK;
 }
 

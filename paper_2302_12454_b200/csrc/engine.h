@@ -22,6 +22,26 @@
 
 namespace ssqa_engine {
 
+// Process-wide engine overrides for the parity tests and tuning experiments
+// (include/ssqa_tune.h).  Defaults leave every choice to the engine; nothing
+// here is read from the environment.
+struct TuneOverrides {
+  int tab = -1;     // fast epilogue: 1 table, 0 FP64 (update_fast2), -1 engine's choice
+  int fp4 = -1;     // 0: force int8 operands
+  int rs = 0;       // > 0: row parts per column tile
+  int wide = 0;     // > 0: cap on trials per wide tile
+  int epi = 0;      // 12 / 16 epilogue warps (0: default)
+  int cta2 = -1;    // 0: no CTA pairs
+  int mc = 0;       // 1: J' multicast clusters
+  int stages = 0;   // > 0: operand stages (with nps)
+  int nps = 0;      // accumulator-ring slots per subgroup (with stages)
+  int exp = 0;      // ablation experiment bits (TcParams::exp_flags)
+  int pf = 0;       // J' L2 prefetch distance
+  int i16 = -1;     // 0: refuse the int16 (two-plane int8) coupling path
+  std::string trace;  // timeline dump path (block 0)
+};
+TuneOverrides& tune();
+
 struct Geom {
   int n = 0, npad = 0;     // spins, padded spins (multiple of 128)
   int R = 0, T = 0;        // replicas, trials

@@ -76,7 +76,7 @@ struct TcParams {
   double i0, n_rnd, alpha;
   int bidirectional;
   int fast, nr;                 // fast epilogue (host-checked) and n_rnd * 2^p
-  int exp_flags;                // ablation experiments (SSQA_TC_EXP): 1 no epilogue math, 2 no MMA,
+  int exp_flags;                // ablation experiments (tune "exp"): 1 no epilogue math, 2 no MMA,
                                 // 4 no operand TMA (MMAs on stale stages), 8 no J'
                                 // loads, 16 no spin loads (single CTAs only)
   double hi_clamp, lo_clamp;    // i0 - alpha, -i0 (formed on the host)
@@ -1945,15 +1945,40 @@ Layout pick_layout(int NT, int tpt, int nsubs, int tile_row, int b_row, int b_co
 // so more resident warps beat more registers per warp (C3: -5 %/sweep vs 12).
 constexpr int kDefaultEpi = 16;
 
+// A fused run with a row split (run_mode 1, g.rs > 1) spin-waits across the
+// CTAs of a column tile, so every CTA must be resident at once: those
+// launches are cooperative (the driver refuses a grid that cannot be
+// co-resident -- also next to other work on the device -- instead of letting
+// it deadlock) and checked against the occupancy first; the caller falls back
+// to rs = 1 on cudaErrorNotSupported.
 template <int EPI, bool F4>
 cudaError_t launch_variant(int grid, int smem, cudaStream_t st, const CUtensorMap* maps,
                            const TcParams& P) {
-  cudaError_t e = cudaFuncSetAttribute(k_sweep_tc<EPI, F4, 0>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  auto kern = k_sweep_tc<EPI, F4, 0>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  k_sweep_tc<EPI, F4, 0><<<grid, 32 * (4 + EPI), smem, st>>>(maps[0], maps[1], maps[2],
-                                                               maps[3], P);
-  return cudaSuccess;
+  const bool coop = P.run_mode == 1 && P.g.rs > 1;
+  if (coop) {
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * (4 + EPI), smem);
+    if (e != cudaSuccess) return e;
+    if (per_sm * sms < grid) return cudaErrorNotSupported;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(unsigned(grid));
+  cfg.blockDim = dim3(32 * (4 + EPI));
+  cfg.dynamicSmemBytes = size_t(smem);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = coop ? 1 : 0;
+  e = cudaLaunchKernelEx(&cfg, kern, maps[0], maps[1], maps[2], maps[3], P);
+  if (e == cudaErrorCooperativeLaunchTooLarge) return cudaErrorNotSupported;
+  return e;
 }
 
 // How many clusters of `csize` CTAs of the cluster variant fit at once.
@@ -2048,9 +2073,9 @@ int launch(ssqa_batch_s* b, TcParams& P, bool f4) {
   const Geom& g = P.g;  // the batch geometry (a shard pass may use its own row split)
   // Table epilogue for row splits: their MMAs keep the tensor core busy, and
   // the FP64 units share its issue path; the FP64 epilogue is cheaper where
-  // they are mostly free (C3: 1146 vs 1178 ms/step).  SSQA_TC_TAB=0/1 forces.
+  // they are mostly free (C3: 1146 vs 1178 ms/step).  Tune key "tab" forces.
   P.use_tab = (P.fast && P.tab_w > 0 && (g.rs > 1 || P.npeer)) ? 1 : 0;
-  if (const char* t = getenv("SSQA_TC_TAB")) P.use_tab = (P.fast && P.tab_w > 0 && atoi(t)) ? 1 : 0;
+  if (tune().tab >= 0) P.use_tab = (P.fast && P.tab_w > 0 && tune().tab) ? 1 : 0;
   CUtensorMap maps[4];
   const uint64_t srows = uint64_t(b->nslots) * g.ccols;
   // FP4 rows are npad/2 bytes (two e2m1 values per byte)
@@ -2100,21 +2125,19 @@ int launch(ssqa_batch_s* b, TcParams& P, bool f4) {
     P.g_rows = reinterpret_cast<int*>(base + size_t(2) * g.ccols * 8 + size_t(g.ntiles) * 8);
     P.g_arrive = reinterpret_cast<unsigned*>(P.g_rows + size_t(g.ntiles) * nrt_all);
   }
-  const char* env_epi = getenv("SSQA_TC_EPI");
-  const int epi = env_epi ? (atoi(env_epi) == 12 ? 12 : 16) : kDefaultEpi;
+  const int epi = tune().epi ? (tune().epi == 12 ? 12 : 16) : kDefaultEpi;
   // CTA pairs (M = 256 MMAs, each CTA streams half of the spin columns): the
   // fused run's row split with an even number of parts per column tile and
-  // of row tiles; SSQA_TC_CTA2=0 turns them off
+  // of row tiles; tune key "cta2" 0 turns them off
   bool cta2 = P.run_mode == 1 && g.rs > 1 && g.rs % 2 == 0 && (g.npad / kBM) % 2 == 0 &&
               epi == 16;
-  if (const char* e2 = getenv("SSQA_TC_CTA2")) cta2 = cta2 && atoi(e2) != 0;
+  if (tune().cta2 >= 0) cta2 = cta2 && tune().cta2 != 0;
   // J' multicast clusters (all column tiles of a row part), opt-in with
-  // SSQA_TC_MC=1: they cut the L2 reads of J' by the tile count but not the
+  // tune key "mc": they cut the L2 reads of J' by the tile count but not the
   // bytes each SM takes in, which is what limits the MMAs (C5: 927 us/sweep
   // against 533 with CTA pairs, whose MMAs read half of B from the peer SM)
   bool mc = P.run_mode == 1 && g.rs > 1 && g.ntiles >= 2 && g.ntiles <= 8 && epi == 16;
-  const char* e3 = getenv("SSQA_TC_MC");
-  mc = mc && e3 && atoi(e3) != 0;
+  mc = mc && tune().mc != 0;
   if (mc) cta2 = false;
   Layout L;
   auto setup = [&](bool pairs) {
@@ -2125,9 +2148,8 @@ int launch(ssqa_batch_s* b, TcParams& P, bool f4) {
     const int tab_bytes = P.use_tab ? (P.bidirectional ? 4 : 2) * P.tab_w * 8 : 0;
     L = pick_layout(g.tile_cols, g.tpt, epi / 4, int(tile_row), int(b_row), b_cols, tab_bytes,
                     pair || g.rs > 1);
-    if (const char* st = getenv("SSQA_TC_STAGES")) {  // experiment overrides
-      const char* np = getenv("SSQA_TC_NPS");
-      L = make_layout(g.tile_cols, g.tpt, atoi(st), (np ? atoi(np) : 1) * (epi / 4),
+    if (tune().stages > 0) {  // experiment overrides
+      L = make_layout(g.tile_cols, g.tpt, tune().stages, std::max(1, tune().nps) * (epi / 4),
                       int(tile_row), int(b_row), b_cols, tab_bytes);
     }
     P.stages = L.stages;
@@ -2139,7 +2161,7 @@ int launch(ssqa_batch_s* b, TcParams& P, bool f4) {
     return SSQA_ECUDA;
   }
   int smem = int(L.total);
-  const char* trace_path = getenv("SSQA_TC_TRACE");
+  const char* trace_path = tune().trace.empty() ? nullptr : tune().trace.c_str();
   long long* dbg = nullptr;
   const int dbg_rts = 4096;
   if (trace_path) {
@@ -2185,12 +2207,22 @@ int launch(ssqa_batch_s* b, TcParams& P, bool f4) {
     }
   }
   if (mc || cta2) {
-  } else if (epi == 16)
-    e = f4 ? launch_variant<16, true>(grid, smem, b->prob->stream, maps, P)
-           : launch_variant<16, false>(grid, smem, b->prob->stream, maps, P);
-  else
-    e = f4 ? launch_variant<12, true>(grid, smem, b->prob->stream, maps, P)
-           : launch_variant<12, false>(grid, smem, b->prob->stream, maps, P);
+  } else {
+    auto single = [&]() {
+      return epi == 16 ? (f4 ? launch_variant<16, true>(grid, smem, b->prob->stream, maps, P)
+                             : launch_variant<16, false>(grid, smem, b->prob->stream, maps, P))
+                       : (f4 ? launch_variant<12, true>(grid, smem, b->prob->stream, maps, P)
+                             : launch_variant<12, false>(grid, smem, b->prob->stream, maps, P));
+    };
+    e = single();
+    if (e == cudaErrorNotSupported && P.g.rs > 1) {
+      // the row parts cannot all be resident: every CTA runs all rows of its tile
+      cudaGetLastError();
+      P.g.rs = 1;
+      grid = g.ntiles;
+      e = single();
+    }
+  }
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) {
     g_tc_err = std::string("k_sweep_tc launch: ") + cudaGetErrorString(e);
@@ -2279,9 +2311,9 @@ TcParams base_params(ssqa_batch_s* b) {
   P.hi_clamp = b->p.i0 - b->p.alpha;
   P.lo_clamp = -b->p.i0;
   P.fast = fast_ok(b, &P) ? 1 : 0;
-  if (const char* ex = getenv("SSQA_TC_EXP")) P.exp_flags = atoi(ex);
+  P.exp_flags = tune().exp;
   P.pf_dist = 0;  // measured: prefetching J' rows costs more L2 bandwidth than it saves (C4, C5)
-  if (const char* pf = getenv("SSQA_TC_PF")) P.pf_dist = atoi(pf);
+  if (tune().pf > 0) P.pf_dist = tune().pf;
   P.ring_cur = b->cur;
   for (int q = 0; q <= b->d; ++q) P.ring_phys[q] = b->phys[size_t(q)];
   P.best_e = b->d_best_e;
@@ -2310,16 +2342,15 @@ void advance_ring(ssqa_batch_s* b, long count) {
 
 // FP4 operands when every coupling is e2m1-exact, fields stay below 2^22
 // (exact fp32 accumulation and float->int conversion) and the tile leaves
-// room for the scale-factor columns; SSQA_TC_FP4=0 forces int8.
+// room for the scale-factor columns; tune key "fp4" 0 forces int8.
 void launch_pack_fp4(const int8_t* src, uint8_t* dst, size_t bytes, cudaStream_t st) {
   k_pack_fp4<<<1184, 256, 0, st>>>(src, dst, bytes);
 }
 
 bool tc_uses_fp4(const ssqa_batch_s* b) {
   const Quantized& q = b->prob->q;
-  const char* envf4 = getenv("SSQA_TC_FP4");
   return (q.fp4_ok || q.fp4x2_ok) && b->d_sig4 && double(q.max_abs_j) * q.n < double(1 << 22) &&
-         2 * b->g.tile_cols <= int(kSfCol) && !(envf4 && envf4[0] == '0');
+         2 * b->g.tile_cols <= int(kSfCol) && tune().fp4 != 0;
 }
 
 bool tc_supported(int npad, int r, int delay) {
@@ -2342,7 +2373,7 @@ int tc_run(ssqa_batch_s* b, const ScanArgs& sa) {
   P.target_tol = sa.target_tol;
   // FP4 operands when every coupling is e2m1-exact, fields stay below 2^22
   // (exact fp32 accumulation and float->int conversion) and the tile leaves
-  // room for the scale-factor columns; SSQA_TC_FP4=0 forces int8.
+  // room for the scale-factor columns; tune key "fp4" 0 forces int8.
   const bool f4 = tc_uses_fp4(b);
   if (f4) {
     const size_t bytes = size_t(b->nslots) * b->slot_elems / 2;
@@ -2414,7 +2445,7 @@ int tc_shard_pass(ssqa_batch_s* b, int rt0, int nrt, unsigned long long* gE) {
 bool tc_shard_direct_ok(ssqa_batch_s* b) {
   if (!tc_uses_fp4(b)) return false;
   TcParams P = base_params(b);
-  return P.fast && P.tab_w > 0 && !getenv("SSQA_TC_TAB");
+  return P.fast && P.tab_w > 0 && tune().tab < 0;
 }
 
 int tc_shard_pass_direct(ssqa_batch_s* b, int rt0, int nrt, unsigned long long* gE,

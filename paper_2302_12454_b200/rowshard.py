@@ -209,9 +209,12 @@ def _run_p2p(b, p, seeds, target, opts, device, group, world, rank, direct=False
         if direct:
             mine4 = b.sig4_ptr()
             sig4 = _map_peers(mine4, _ipc_handle(mine4), device, group, world, rank, opened)
-        if world > 1:
-            dist.barrier(group=group)  # every region is zeroed and mapped
+        # shard_begin repacks this GPU's FP4 slots; it must be complete on the
+        # device before any peer's pass 0 pushes spin words into them
         b.shard_begin(target, opts.stop_at_target)
+        b.synchronize()
+        if world > 1:
+            dist.barrier(group=group)  # every region is zeroed, mapped and begun
         if direct:
             shard_cycles_direct(b, layout, rank, bases, sig4, p.sc + 1)
         else:

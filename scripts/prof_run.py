@@ -5,6 +5,11 @@ sys.path.insert(0, ROOT)
 import bench
 import paper_2302_12454_b200 as sq
 from paper_2302_12454_b200 import _lib
+# dev tooling: SSQA_TC_<KEY>=v environment variables map onto engine overrides
+for k, v in os.environ.items():
+    if k.startswith("SSQA_TC_"):
+        key = k[len("SSQA_TC_"):].lower()
+        sq.tune(**{key: v if key == "trace" else int(v)})
 cfg = dict(bench.CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "c3"])
 eng = {"simt": _lib.ENGINE_SIMT, "tcgen05": _lib.ENGINE_TCGEN05}[sys.argv[2] if len(sys.argv) > 2 else "tcgen05"]
 sc = int(sys.argv[3]) if len(sys.argv) > 3 else 20

@@ -30,6 +30,14 @@ def _ensure_built():
 _ensure_built()
 
 
+@pytest.fixture(autouse=True)
+def _reset_engine_tune():
+    """Engine overrides (include/ssqa_tune.h) never leak from one test into the next."""
+    yield
+    import paper_2302_12454_b200 as sq
+    sq.tune()
+
+
 @pytest.fixture(scope="session")
 def orc():
     import oracle_py

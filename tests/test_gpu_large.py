@@ -97,3 +97,36 @@ def test_gi_full_battery_matches_reference_run_trials(golden, cfg):
     assert np.array_equal(bits([o.best_energy for o in outs[:k]]), bits(ref["best_energy"]))
     if k == T:
         assert p_s == float(ref["p_s"])
+
+
+@pytest.mark.parametrize("jval", [6.0, 12.0], ids=["fp4", "fp4pair"])
+def test_fp4_large_aligned_fields_exact(jval):
+    """FP4 operands accumulate in the tensor core's fp32 TMEM accumulator;
+    exactness needs every partial sum of the block-scaled MMA to be exact.
+    A ferromagnet (J' = 6: one e2m1 plane; J' = 12 = 6 + 6: the FP4 pair) at
+    N = 8192 aligns within a few sweeps, so the fields reach |S| = J' (N - 1)
+    = 49146 / 98292 (> 2^15, > 2^16).  The run must equal the forced-int8 run
+    (int32 accumulators) bitwise and oracle/lattice_np.py on two trials."""
+    import lattice_np as lnp
+    n, R, T, steps = 8192, 8, 4, 30
+    J = np.full((n, n), jval)
+    np.fill_diagonal(J, 0.0)
+    m = sq.IsingModel.from_arrays(np.zeros(n), J, 0.0)
+    p = sq.SsqaParams(r=R, sc=steps)
+    seeds = [77 + t for t in range(T)]
+    opts = sq.RunOptions(True, False)
+    fp4 = sq.ssqa_run_batch(m, p, seeds, None, opts)
+    sq.tune(fp4=0)
+    i8 = sq.ssqa_run_batch(m, p, seeds, None, opts)
+    sq.tune()
+    for a, b in zip(fp4, i8):
+        assert np.array_equal(bits(a.trace_energy), bits(b.trace_energy))
+        assert np.array_equal(a.best_state, b.best_state)
+    # the runs really reached the large-field regime: an aligned replica
+    assert min(r.best_energy for r in fp4) == -jval * n * (n - 1) / 2
+    q = params(R, steps)
+    ref = lnp.run_lattice(m.h, m.J, m.offset, R, q.delay, q.n_rnd, q.alpha, False, steps,
+                          lnp.jperp_schedule(q), lambda c: q.i0, [seeds[0], seeds[-1]])
+    for o, t in zip(ref, [0, T - 1]):
+        assert np.array_equal(bits(fp4[t].trace_energy), bits(o.trace.reshape(-1))), t
+        assert np.array_equal(fp4[t].best_state, o.best_state), t

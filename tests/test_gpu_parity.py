@@ -177,9 +177,9 @@ def engine_epi(request, monkeypatch):
     if not engine_ok(engine):
         pytest.skip("engine unavailable for this build")
     if epi == "table":
-        monkeypatch.setenv("SSQA_TC_TAB", "1")
+        sq.tune(tab=1)
     elif epi == "fp64":
-        monkeypatch.setenv("SSQA_TC_TAB", "0")
+        sq.tune(tab=0)
     return engine
 
 
@@ -207,7 +207,7 @@ def test_full_runs_match_oracle_many_trials(orc, engine_epi):
 def operands(request, monkeypatch):
     """tcgen05 operand format: the engine's choice (FP4, FP4 pair) or int8."""
     if request.param == "int8":
-        monkeypatch.setenv("SSQA_TC_FP4", "0")
+        sq.tune(fp4=0)
     return request.param
 
 
@@ -220,7 +220,7 @@ def test_dense_integer_model_matches_oracle(orc, monkeypatch, engine, ops):
     if not engine_ok(engine):
         pytest.skip("engine unavailable for this build")
     if ops == "int8":
-        monkeypatch.setenv("SSQA_TC_FP4", "0")
+        sq.tune(fp4=0)
     m = sq.dense_ising(200, 0, 3)
     p = params(8, 40, tau=5, bidirectional=True)
     seeds = [11, 12, 13]
@@ -519,7 +519,7 @@ def test_stop_at_target_many_tiles_drain(orc, engine):
 @pytest.fixture
 def row_split(monkeypatch):
     def force(rs):
-        monkeypatch.setenv("SSQA_TC_RS", str(rs))
+        sq.tune(rs=rs)
     return force
 
 
@@ -544,13 +544,13 @@ def test_row_split_runs_match_oracle(orc, row_split, monkeypatch, rs, operands, 
     if not engine_ok(_lib.ENGINE_TCGEN05):
         pytest.skip("tcgen05 engine unavailable")
     if operands == "int8":
-        monkeypatch.setenv("SSQA_TC_FP4", "0")
+        sq.tune(fp4=0)
     if cluster == "mc":
-        monkeypatch.setenv("SSQA_TC_MC", "1")
+        sq.tune(mc=1)
     if cluster == "single":
-        monkeypatch.setenv("SSQA_TC_CTA2", "0")
+        sq.tune(cta2=0)
     if epi == "fp64":
-        monkeypatch.setenv("SSQA_TC_TAB", "0")
+        sq.tune(tab=0)
     row_split(rs)
     cases = [(sq.gi_ising(20, 0.5, 7, True, 1.0, 1.0), params(20, 60), [41, 42, 43, 44, 45, 46]),
              (sq.dense_ising(400, 0, 5), params(6, 30, tau=4, bidirectional=True), [7, 8, 9])]
@@ -933,7 +933,7 @@ def test_fused_run_leaves_exact_lattice(orc, monkeypatch):
     sweeps (int8 operands keep the lattice; FP4 runs mark it stale)."""
     if not engine_ok(_lib.ENGINE_TCGEN05):
         pytest.skip("tcgen05 engine unavailable")
-    monkeypatch.setenv("SSQA_TC_FP4", "0")
+    sq.tune(fp4=0)
     m = sq.gi_ising(10, 0.5, 7, True, 1.0, 1.0)
     for p in (params(20, 130), params(6, 90, delay=2, bidirectional=True)):
         T = 5
