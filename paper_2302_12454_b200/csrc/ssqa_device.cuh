@@ -184,6 +184,123 @@ __device__ __forceinline__ double update_fast2(const FastConsts& c, const I2D& i
   return (s >= c.i0) ? c.hi_clamp : lo;
 }
 
+// ---- Issue-lean noise draw for the fused epilogue --------------------------
+// The epilogue is bound by instruction issue and by the ALU pipe (LOP3 /
+// SHF / ISETP / SEL), while the FMA pipe (IMAD) sits mostly idle.  This
+// restatement of raw(spin_counter(cycle, k, i)) >> 59 (rng.hpp:10-15, 36-38)
+// moves the 64-bit shifts onto the FMA pipe as multiplies by powers of two
+// held in registers (mul.hi by 2^s == >> (32 - s), mul.lo by 2^s == << s),
+// forms the counter sum with one wide multiply-add, and keeps three-input
+// XORs on the ALU.  `base` = key + spin_counter(cycle, k, 0) * golden +
+// golden (mix64's first add), so x0 = base + i * golden.
+//   p4 = 4, p32 = 32: opaque to ptxas (kept in registers) so it cannot turn
+//   the multiplies back into shifts.
+// Returns the top five bits of the draw.
+#ifndef SSQA_RNG_FMA
+#define SSQA_RNG_FMA 1  // 1: shifts as IMAD.HI / IMAD.SHL (FMA pipe); 0: funnel shifts (ALU)
+#endif
+__device__ __forceinline__ uint32_t noise_top5(uint64_t base, uint32_t i, uint32_t p4,
+                                               uint32_t p32) {
+  uint32_t lo, hi;
+  // x0 = base + i * golden (mod 2^64)
+  asm("{\n\t.reg .u64 w;\n\t"
+      "mad.wide.u32 w, %2, 0x7f4a7c15, %3;\n\t"
+      "mov.b64 {%0, %1}, w;\n\t"
+      "mad.lo.u32 %1, %2, 0x9e3779b9, %1;\n\t}"
+      : "=r"(lo), "=r"(hi)
+      : "r"(i), "l"(base));
+  uint32_t l1, h1;
+#if SSQA_RNG_FMA
+  // x ^= x >> 30
+  l1 = lo ^ __umulhi(lo, p4) ^ (hi * p4);
+  h1 = hi ^ __umulhi(hi, p4);
+#else
+  l1 = lo ^ __funnelshift_r(lo, hi, 30);
+  h1 = hi ^ (hi >> 30);
+#endif
+  // x *= 0xbf58476d1ce4e5b9
+  uint32_t l2, h2;
+  asm("{\n\t.reg .u64 w;\n\t"
+      "mul.wide.u32 w, %2, 0x1ce4e5b9;\n\t"
+      "mov.b64 {%0, %1}, w;\n\t"
+      "mad.lo.u32 %1, %2, 0xbf58476d, %1;\n\t"
+      "mad.lo.u32 %1, %3, 0x1ce4e5b9, %1;\n\t}"
+      : "=r"(l2), "=r"(h2)
+      : "r"(l1), "r"(h1));
+  uint32_t l3, h3;
+#if SSQA_RNG_FMA
+  // x ^= x >> 27
+  l3 = l2 ^ __umulhi(l2, p32) ^ (h2 * p32);
+  h3 = h2 ^ __umulhi(h2, p32);
+#else
+  l3 = l2 ^ __funnelshift_r(l2, h2, 27);
+  h3 = h2 ^ (h2 >> 27);
+#endif
+  // high word of x * 0x94d049bb133111eb; its top five bits are the draw's
+  // (the final x ^= x >> 31 leaves bits 63..59 unchanged)
+  const uint32_t top = __umulhi(l3, 0x133111ebu) + l3 * 0x94d049bbu + h3 * 0x133111ebu;
+  return __umulhi(top, p32);  // top >> 27
+}
+
+// noise_top5 for the issue-lean epilogue: the counter sum with the row's
+// i * golden pinned in registers (add / add-with-carry), the low-word shifts
+// as funnel shifts (ALU) and the high-word shifts as high products by 2^2 /
+// 2^5 (FMA pipe), the last product as one multiply-high-add.
+__device__ __forceinline__ uint32_t noise_top5_v4(uint64_t base, uint32_t iG_lo, uint32_t iG_hi,
+                                                  uint32_t p4, uint32_t p32) {
+  uint32_t lo, hi;
+  asm("add.cc.u32 %0, %2, %4;\n\taddc.u32 %1, %3, %5;"
+      : "=r"(lo), "=r"(hi)
+      : "r"(uint32_t(base)), "r"(uint32_t(base >> 32)), "r"(iG_lo), "r"(iG_hi));
+  const uint32_t l1 = lo ^ __funnelshift_r(lo, hi, 30);
+  const uint32_t h1 = hi ^ __umulhi(hi, p4);
+  uint32_t l2, h2;
+  asm("{\n\t.reg .u64 w;\n\t"
+      "mul.wide.u32 w, %2, 0x1ce4e5b9;\n\t"
+      "mov.b64 {%0, %1}, w;\n\t"
+      "mad.lo.u32 %1, %2, 0xbf58476d, %1;\n\t"
+      "mad.lo.u32 %1, %3, 0x1ce4e5b9, %1;\n\t}"
+      : "=r"(l2), "=r"(h2)
+      : "r"(l1), "r"(h1));
+  const uint32_t l3 = l2 ^ __funnelshift_r(l2, h2, 27);
+  const uint32_t h3 = h2 ^ __umulhi(h2, p32);
+  uint32_t top;
+  asm("mad.hi.u32 %0, %1, 0x133111eb, %2;"
+      : "=r"(top)
+      : "r"(l3), "r"(l3 * 0x94d049bbu + h3 * 0x133111ebu));
+  return top >> 27;
+}
+
+// Noise level of update_spins (annealer.cpp:277-278) scaled to the integer
+// field: nz_lut[t5] = 0 (t5 < 14), -NR (t5 < 23), +NR, NR = n_rnd * 2^p,
+// |NR| <= 127 -- one conflict-free shared byte load instead of two compares
+// and two selects (32 bytes span 8 banks; lanes of one word broadcast).
+__device__ __forceinline__ void fill_noise_lut(int8_t* lut, int nr, int t) {
+  if (t < 32) lut[t] = int8_t(t < 14 ? 0 : (t < 23 ? -nr : nr));
+}
+__device__ __forceinline__ int noise_lut(const int8_t* lut, uint32_t t5) {
+  int v;
+  asm volatile("ld.shared.s8 %0, [%1];" : "=r"(v) : "r"(uint32_t(__cvta_generic_to_shared(lut)) + t5));
+  return v;
+}
+
+// update_fast2 with the noise already in the integer field and the bias of
+// the magic-number conversion folded into it: xb = (S + H' + nz NR) ^ 2^31
+// (i.e. + 2^31 mod 2^32, added once per row on the host side of the loop).
+template <bool BIDIR>
+__device__ __forceinline__ double update_fast3(const FastConsts& c, const I2D& i2d, uint32_t xb,
+                                               int up, int dn, double acc) {
+  double input = __dsub_rn(__hiloint2double(int(i2d.magic_hi), int(xb)), i2d.magic);
+  input = __dadd_rn(input, __hiloint2double(int(c.jp_hi ^ (uint32_t(up) & 0x80000000u)),
+                                            int(c.jp_lo)));
+  if (BIDIR)
+    input = __dadd_rn(input, __hiloint2double(int(c.jp_hi ^ (uint32_t(dn) & 0x80000000u)),
+                                              int(c.jp_lo)));
+  const double s = __dadd_rn(acc, input);
+  const double lo = (s < c.lo_clamp) ? c.lo_clamp : s;
+  return (s >= c.i0) ? c.hi_clamp : lo;
+}
+
 // Exact double of an integer field scaled by 2^-p (|v| < 2^53).
 __device__ __forceinline__ double scaled(long long v, double scale) {
   return __dmul_rn(double(v), scale);

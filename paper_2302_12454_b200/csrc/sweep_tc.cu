@@ -48,6 +48,24 @@ constexpr int kCW = 8;  // columns per epilogue chunk (one tcgen05.ld .x8)
 // 1024 spin words built but not stored, 2048 no ballots (spin words from one lane).
 #define SSQA_ABL 0
 #endif
+#ifndef SSQA_EPI_V
+#define SSQA_EPI_V 1  // FP64 epilogue: 1 issue-lean noise draw (noise_top5 / noise_lut), 0 previous
+#endif
+#ifndef SSQA_CT_ICMP
+#define SSQA_CT_ICMP 0  // clamped-table path: clamp with integer compares (1) or DSETP (0)
+#endif
+#ifndef SSQA_CT_LUT
+#define SSQA_CT_LUT 0  // clamped-table path: noise from the byte table (1) or compares (0)
+#endif
+#ifndef SSQA_LAZY_NS_MMA
+#define SSQA_LAZY_NS_MMA 128   // MMA issuer waiting for a free accumulator buffer
+#endif
+#ifndef SSQA_LAZY_NS_PROD
+#define SSQA_LAZY_NS_PROD 32   // operand producer waiting for a free stage
+#endif
+#ifndef SSQA_LAZY_NS_LOAD
+#define SSQA_LAZY_NS_LOAD 128  // state loaders waiting for a free slot / tile buffer
+#endif
 #ifndef SSQA_ENERGY_RED
 #define SSQA_ENERGY_RED 1  // 1: shuffle transpose-reduce, 0: per-column redux.sync
 #endif
@@ -111,6 +129,7 @@ struct TcParams {
   unsigned epoch;
   unsigned* push_ctr;
   int use_tab;  // fast mode: table epilogue (row splits) instead of update_fast2
+  int rails_lo; // the clamp rails i0 - alpha and -i0 share their low word (every cycle)
   int mc_q;     // CL == 2: column tiles per cluster (= ntiles), sharing each J' tile
   long long* dbg;  // optional timeline (block 0): [role][rt_global][2] clock64 stamps
   int dbg_rts;     // capacity in row tiles
@@ -130,6 +149,23 @@ struct TcParams {
   unsigned* g_arrive;      // [ntiles] CTAs of the column tile done with their pass
   long long* g_scan;       // [ntiles] (s+1) | stop << 62 once pass s is scanned
 };
+
+// Shared bytes of the per-cycle table: TAB (use_tab 1) [combo][tab_w],
+// clamped table (use_tab 2) [tab_w + 2][combo].
+__host__ __device__ inline int tab_bytes_of(const TcParams& P) {
+  const int ncmb = P.bidirectional ? 4 : 2;
+  return P.use_tab == 1 ? ncmb * P.tab_w * 8 : (P.use_tab == 2 ? ncmb * (P.tab_w + 2) * 8 : 0);
+}
+
+// Bytes per column of one delayed-neighbour tile buffer: the TMA-loaded spin
+// rows (int8 128, FP4 64) or, for the clamped-table epilogue, the
+// neighbour-sign bytes (128 per plane, a second plane when bidirectional).
+__host__ __device__ inline int sig_tile_row(const TcParams& P, bool f4) {
+  // (plus half a TMA tile per buffer: one staging tile for the copier warp)
+  if (P.fast && P.g.rs == 1 && ((P.use_tab == 0 && P.rails_lo) || P.use_tab == 2))
+    return 128 * (P.bidirectional ? 2 : 1) + (f4 ? 32 : 64);
+  return f4 ? 64 : 128;
+}
 
 // gpu-scope release/acquire helpers for the row-split protocol
 __device__ __forceinline__ int ld_acquire_gpu(const int* p) {
@@ -232,6 +268,21 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     if (clock64() - t0 > 20000000000ll) watchdog_fire(a, parity);
 }
 
+// Waits of the control warps (MMA issuer, producers, loaders) that are
+// expected to be long: poll with a plain try_wait and back off with
+// nanosleep, so a waiting control warp does not take issue slots from the
+// epilogue warps of its scheduler (a suspend-hinted try_wait wakes on every
+// barrier event of the CTA and re-runs the poll loop).
+__device__ __forceinline__ void mbar_wait_lazy(uint64_t* bar, uint32_t parity, uint32_t ns) {
+  const uint32_t a = smem_u32(bar);
+  if (mbar_try(a, parity)) return;
+  const long long t0 = clock64();
+  while (!mbar_try(a, parity)) {
+    __nanosleep(ns);
+    if (clock64() - t0 > 20000000000ll) watchdog_fire(a, parity);
+  }
+}
+
 __device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint64_t* bar, void* dst,
                                             int x, int y) {
   asm volatile(
@@ -249,6 +300,43 @@ __device__ __forceinline__ void tma_load_2d_hint(const CUtensorMap* map, uint64_
       ".L2::cache_hint [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(x), "r"(y), "l"(policy)
       : "memory");
+}
+
+// 3D tile load (accumulator chunks: {rows 0..31, columns, 32-row blocks}).
+__device__ __forceinline__ void tma_load_3d_hint(const CUtensorMap* map, uint64_t* bar, void* dst,
+                                                 int x, int y, int z, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      ".L2::cache_hint [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(x), "r"(y), "r"(z),
+      "l"(policy)
+      : "memory");
+}
+
+// 3D tile store shared -> global (bulk group; commit / wait by the caller).
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* src, int x, int y,
+                                             int z) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+          reinterpret_cast<uint64_t>(map)),
+      "r"(smem_u32(src)), "r"(x), "r"(y), "r"(z)
+      : "memory");
+}
+
+// cp.async.bulk.wait_group N for a run-time N (all but the N most recent
+// bulk groups complete).
+__device__ __forceinline__ void bulk_wait_group(int n) {
+  switch (n) {
+    case 0: asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); break;
+    case 1: asm volatile("cp.async.bulk.wait_group 1;" ::: "memory"); break;
+    case 2: asm volatile("cp.async.bulk.wait_group 2;" ::: "memory"); break;
+    case 3: asm volatile("cp.async.bulk.wait_group 3;" ::: "memory"); break;
+    case 4: asm volatile("cp.async.bulk.wait_group 4;" ::: "memory"); break;
+    case 5: asm volatile("cp.async.bulk.wait_group 5;" ::: "memory"); break;
+    case 6: asm volatile("cp.async.bulk.wait_group 6;" ::: "memory"); break;
+    case 7: asm volatile("cp.async.bulk.wait_group 7;" ::: "memory"); break;
+    default: asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); break;
+  }
 }
 
 // L2 prefetch of a tensor tile (no smem, no barrier): pulls the J' rows a few
@@ -611,6 +699,17 @@ __device__ __forceinline__ void st_s8_if(int8_t* p, int v, bool pred) {
       "r"(v), "r"(int(pred)));
 }
 
+__device__ __forceinline__ int lds_s8(uint32_t a) {
+  int v;
+  asm volatile("ld.shared.s8 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ double lds_f64(uint32_t a) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+  return v;
+}
+
 struct TrialTab {
   double best_e;
   long first_hit, cycles_used;
@@ -631,12 +730,16 @@ struct SmemCtl {
   // issuer and state loader of the next pass wait on it (one phase per pass).
   uint64_t rready[kMaxRowGroups];
   uint64_t done;       // epilogue finished (TMEM may be released)
+  uint64_t stg;        // clamped-table path: staged delayed spin rows (TMA -> copier)
+  int8_t nz_lut[32];   // integer noise per top-five-bit draw (noise_lut)
+  uint8_t umask[kMaxCols / kCW];  // per chunk: bit j = column 8 ch + j updates this cycle
   uint32_t tmem_base;
   long last_pass;  // last cycle any role may start (stop-at-target drain)
   int scan_me;     // row split: this CTA scans the pass (last arrival)
   int scan_stop;   // row split: the column tile's trials have all stopped
-  // slot ring per role (producer, loader, epilogue): [0] = cur, [1 + q] = phys[q]
-  int ring[3][kMaxDelay + 2];
+  // slot ring per role (producer, loader, epilogue, neighbour-tile copier):
+  // [0] = cur, [1 + q] = phys[q]
+  int ring[4][kMaxDelay + 2];
 };
 
 __device__ __forceinline__ void ring_advance(int* r, long c, int d, int nslots) {
@@ -691,6 +794,19 @@ struct EpiRow {
   uint32_t nib_live;        // FP4 word stores: nibble mask of the live rows of that word
   int npeer;                // fused shard exchange: peers that get every spin word too
   const long long* peer_delta;  // TcParams::peer_delta
+  // issue-lean FP64 epilogue (noise_top5 / noise_lut / update_fast3)
+  uint32_t i_u32;           // global spin row i
+  uint32_t p4, p32;         // 4 and 32 in registers (noise_top5)
+  uint32_t h1x;             // h1 + noise-free bias + 2^31 (update_fast3)
+  const int8_t* nz_lut;     // SmemCtl::nz_lut
+  // clamped-table epilogue (use_tab 2)
+  int h1c;                  // h1 (+ FP4 bias) - (tab_lo1 - 1): table index before the clamp
+  int ct_max;               // tab_w + 1: last table row
+  uint32_t nb_shift;        // neighbour sign bit -> bit 3 (FP4: 4 (i & 1), int8: 4)
+  uint32_t ytab;            // shared address of the table
+  const CUtensorMap* tmAs;  // accumulator store map (box 32 rows x 8 columns)
+  int col0;                 // first global column of the tile
+  int zq;                   // 32-row block index of this warp's rows
 };
 
 // Table epilogue constants for one cycle.  With X = S + H' + noise * NR the
@@ -743,7 +859,7 @@ template <bool BIDIR, bool SIGACC, bool FAST, bool F4, bool TAB>
 __device__ __forceinline__ void epi_chunks(const EpiRow& er, const UpdateConsts& uc,
                                            const FastConsts& fc, const TabConsts& tc,
                                            const I2D& i2d, SmemCtl* ctl,
-                                           const double* acc_ring, const ColTab* c_col,
+                                           double* acc_ring, const ColTab* c_col,
                                            long long* q_sum, uint32_t trow, int sub,
                                            int nsubs, int nchunk, int nps, uint32_t cnt0, int il,
                                            int lane) {
@@ -768,7 +884,8 @@ __device__ __forceinline__ void epi_chunks(const EpiRow& er, const UpdateConsts&
       sidx = 0;
       ph ^= 1;
     }
-    const double* ab = acc_ring + size_t(slot) * kCW * kBM + il;
+    // slot layout [column][128 rows] (2D accumulator map)
+    double* ab = acc_ring + size_t(slot) * kCW * kBM + il;
     int ep[kCW];
     uint32_t ball[kCW];
     if (FAST && TAB) {
@@ -879,9 +996,16 @@ __device__ __forceinline__ void epi_chunks(const EpiRow& er, const UpdateConsts&
           up = int8_t(er.st_i[nb & 0xffffu]);
           if (BIDIR) dn = int8_t(er.st_i[(nb >> 16) & 0x7fffu]);
         }
+#if SSQA_EPI_V
+        const uint32_t t5 = noise_top5(cbase, er.i_u32, er.p4, er.p32);
+        const double nv = update_fast3<BIDIR>(fc, i2d, uint32_t(S) + er.h1x +
+                                                           uint32_t(noise_lut(er.nz_lut, t5)),
+                                              up, dn, a_old);
+#else
         const uint32_t top = (SSQA_ABL & 512) ? uint32_t(cbase) ^ er.iG_lo
                                               : mix64_top32_pre(add64_pair(cbase, er.iG_lo, er.iG_hi));
         const double nv = update_fast2<BIDIR>(fc, i2d, S + er.h1, top, up, dn, a_old);
+#endif
         const uint32_t neg = uint32_t(__double2hiint(nv)) >> 31;
         const bool w = (nb & 0x80000000u) && er.w_row;
         if (!(SSQA_ABL & 64))
@@ -1020,6 +1144,381 @@ __device__ __forceinline__ void epi_chunks(const EpiRow& er, const UpdateConsts&
   }
 }
 
+// ---- Lean epilogue of the clamped-table path (use_tab 2, no row split) ----
+// Everything per update is one of: the counter RNG (noise_top5), three
+// shared loads (column key, noise byte, neighbour-sign byte), the table
+// lookup of y = fl(X 2^-p + jperp u [+ jperp d]), one FP64 add and the
+// clamp, one shared store of the new accumulator and one ballot.  Per chunk:
+// the TMEM field load, the energy partials (kept in TMEM across the row
+// tiles of a pass when the tile is narrow enough), the spin words and one
+// TMA store of the warp's accumulator block.
+struct CtRow {
+  uint32_t i_u32, p4, p32;  // noise_top5 operands
+  uint32_t iG_lo, iG_hi;    // i * golden (pinned in registers)
+  int nr;                   // n_rnd * 2^p
+  long long i0_bits, hic_bits, loc_bits;  // integer clamp (see TabConsts)
+  unsigned long long lo_bits;
+  int h1c, h2, ct_max;      // clamped table index = clamp(S + h1c + noise, 0, ct_max)
+  uint32_t nbt;             // shared address of row il of neighbour-sign tile column 0
+  uint32_t ytab, lut;       // shared addresses of the table and the noise bytes
+  uint32_t e_tmem;          // TMEM address of this warp's energy partials (column 0)
+  int e_mode;               // 0: reduce every chunk, 1: first row tile (store), 2: middle
+                            // (load, add, store), 3: last (load, add, reduce)
+  uint8_t* dst_w;           // FP4 spin words (see EpiRow::dst_w)
+  uint32_t nib_live;
+  uint64_t cur_i;           // first pass: current spin slot at row i (FP4: byte i/2)
+  uint64_t dst_i;           // int8 spin slot at row i
+  uint32_t nib_shift;
+  bool w_row;
+  const CUtensorMap* tmAs;
+  int col0, zq;
+};
+
+// Neighbour-sign tiles of the clamped-table path: [column][128 rows] bytes,
+// up plane value 8 where sigma_{k+1}(c-d) < 0, then (bidirectional) the down
+// plane with value 16 -- the byte offsets of the table entry.
+constexpr int kCtTileRow = 128;
+
+__device__ __forceinline__ uint32_t lds_u8(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint64_t lds_u64(uint32_t a) {
+  uint64_t v;
+  asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void tmem_ld8_nw(uint32_t taddr, int32_t (&v)[8]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const int32_t (&v)[8]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+      : "memory");
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+
+// Sum each of the 8 column partials over the warp's 32 rows (shuffle
+// transpose-reduce) and add it to the lane quarter's column sums.
+__device__ __forceinline__ void reduce8_to_quarter(const int (&ep)[kCW], long long* q_sum, int cb,
+                                                   int lane) {
+  int a4[4], a2[2], a1;
+  const bool b16 = lane & 16, b8 = lane & 8, b4 = lane & 4;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int keep = b16 ? ep[k + 4] : ep[k];
+    const int send = b16 ? ep[k] : ep[k + 4];
+    a4[k] = keep + shfl_xor_i(send, 16);
+  }
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const int keep = b8 ? a4[k + 2] : a4[k];
+    const int send = b8 ? a4[k] : a4[k + 2];
+    a2[k] = keep + shfl_xor_i(send, 8);
+  }
+  {
+    const int keep = b4 ? a2[1] : a2[0];
+    const int send = b4 ? a2[0] : a2[1];
+    a1 = keep + shfl_xor_i(send, 4);
+  }
+  a1 += shfl_xor_i(a1, 2);
+  a1 += shfl_xor_i(a1, 1);
+  const int col = (b16 ? 4 : 0) + (b8 ? 2 : 0) + (b4 ? 1 : 0);
+  red_add_u32_if(reinterpret_cast<uint32_t*>(q_sum) + cb + col, uint32_t(a1), (lane & 3) == 0);
+}
+
+// One row tile of this warp's chunks.  `pend`: ring slot whose TMA store may
+// still be reading it (released one chunk later; -1 none).
+template <bool BIDIR, bool SIGACC, bool F4>
+__device__ __forceinline__ void epi_ct(const CtRow& r, const FastConsts& fc, SmemCtl* ctl,
+                                       double* acc_ring, const ColTab* c_col,
+                                       const uint8_t* c_umask, long long* q_sum, uint32_t trow,
+                                       int sub, int nsubs, int nchunk, int nps, uint32_t cnt0,
+                                       int q, int lane, int& pend) {
+  int sidx = int(cnt0 % uint32_t(nps));
+  uint32_t ph = (cnt0 / uint32_t(nps)) & 1;
+  const int wj = lane >> 2;
+  const uint32_t colt = smem_u32(c_col);
+  for (int ch = sub; ch < nchunk; ch += nsubs) {
+    const int cb = ch * kCW;
+    const int slot = sub * nps + sidx;
+    int32_t v[kCW], e[kCW];
+    tmem_ld8_nw(trow + uint32_t(cb), v);
+    if (r.e_mode >= 2) tmem_ld8_nw(r.e_tmem + uint32_t(cb), e);
+    else
+#pragma unroll
+      for (int j = 0; j < kCW; ++j) e[j] = 0;
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    mbar_wait(&ctl->afull[slot], ph);
+    if (++sidx == nps) {
+      sidx = 0;
+      ph ^= 1;
+    }
+    double* ab = acc_ring + size_t(slot) * kCW * kBM + q * (kCW * 32) + lane;
+    const uint32_t umask = c_umask[ch];
+    const uint32_t nbq = r.nbt + uint32_t(cb) * uint32_t(BIDIR ? 2 * kCtTileRow : kCtTileRow);
+    uint32_t ball[kCW];
+    // The eight updates of the chunk stage by stage (each stage a loop over
+    // the columns), so the independent chains interleave.
+    int S[kCW];
+#pragma unroll
+    for (int j = 0; j < kCW; ++j) S[j] = F4 ? __float_as_int(__int_as_float(v[j]) + 12582912.0f) : v[j];
+    // counter RNG: raw(spin_counter(c, k, i)) >> 59 (rng.hpp:10-15, 36-38)
+    uint32_t xl[kCW], xh[kCW];
+#pragma unroll
+    for (int j = 0; j < kCW; ++j) {
+      const uint64_t x0 = add64_pair(lds_u64(colt + uint32_t(cb + j) * uint32_t(sizeof(ColTab))),
+                                     r.iG_lo, r.iG_hi);
+      xl[j] = uint32_t(x0);
+      xh[j] = uint32_t(x0 >> 32);
+    }
+#pragma unroll
+    for (int j = 0; j < kCW; ++j) {  // x ^= x >> 30
+      const uint32_t l = xl[j] ^ __funnelshift_r(xl[j], xh[j], 30);
+      xh[j] ^= xh[j] >> 30;
+      xl[j] = l;
+    }
+#pragma unroll
+    for (int j = 0; j < kCW; ++j) {  // x *= 0xbf58476d1ce4e5b9
+      uint32_t l2, h2;
+      asm("{\n\t.reg .u64 w;\n\t"
+          "mul.wide.u32 w, %2, 0x1ce4e5b9;\n\t"
+          "mov.b64 {%0, %1}, w;\n\t"
+          "mad.lo.u32 %1, %2, 0xbf58476d, %1;\n\t"
+          "mad.lo.u32 %1, %3, 0x1ce4e5b9, %1;\n\t}"
+          : "=r"(l2), "=r"(h2)
+          : "r"(xl[j]), "r"(xh[j]));
+      xl[j] = l2;
+      xh[j] = h2;
+    }
+#pragma unroll
+    for (int j = 0; j < kCW; ++j) {  // x ^= x >> 27
+      const uint32_t l = xl[j] ^ __funnelshift_r(xl[j], xh[j], 27);
+      xh[j] ^= xh[j] >> 27;
+      xl[j] = l;
+    }
+    int xi[kCW];
+#pragma unroll
+    for (int j = 0; j < kCW; ++j) {
+      // high word of x * 0x94d049bb133111eb (its top five bits are the draw's)
+      uint32_t top;
+      asm("mad.hi.u32 %0, %1, 0x133111eb, %2;"
+          : "=r"(top)
+          : "r"(xl[j]), "r"(xl[j] * 0x94d049bbu + xh[j] * 0x133111ebu));
+#if SSQA_CT_LUT
+      const int nz = lds_s8(r.lut + (top >> 27));
+#else
+      const int nz = top < 0x70000000u ? 0 : (top < 0xB8000000u ? -r.nr : r.nr);
+#endif
+      xi[j] = min(max(S[j] + r.h1c + nz, 0), r.ct_max);
+    }
+#pragma unroll
+    for (int j = 0; j < kCW; ++j) {
+      const double a_old = ab[j * 32];
+      const int s2 = S[j] + r.h2;
+      if (SIGACC) {
+        e[j] += s2 * ((__double2hiint(a_old) >> 30) | 1);
+      } else {
+        const uint32_t coff = c_col[cb + j].off;
+        int sg;
+        if (F4) {
+          const uint32_t bc = ld_u8(reinterpret_cast<const uint8_t*>(r.cur_i + (coff >> 1)));
+          sg = ((bc >> r.nib_shift) & 8u) ? -1 : 1;
+        } else {
+          sg = ld_s8(reinterpret_cast<const int8_t*>(r.cur_i + coff));
+        }
+        e[j] += sg * s2;
+      }
+      // neighbour signs -> byte offset of the table entry (8: up < 0, 16: down < 0)
+      // sign bytes 0x80 / 0 -> offsets 8 (up) and 16 (down)
+      uint32_t cmbo = lds_u8(nbq + uint32_t(j) * (BIDIR ? 2u * kCtTileRow : uint32_t(kCtTileRow))) >> 4;
+      if (BIDIR) cmbo |= lds_u8(nbq + uint32_t(j) * 2u * kCtTileRow + kCtTileRow) >> 3;
+      const double y = lds_f64(r.ytab + (uint32_t(xi[j]) << (BIDIR ? 5 : 4)) + cmbo);
+      const double sd = __dadd_rn(a_old, y);
+#if SSQA_CT_ICMP
+      // clamp on the bit patterns (ALU instead of the FP64 pipe): i0 > 0 > -i0,
+      // no NaN, never -0.0
+      const long long sb = __double_as_longlong(sd);
+      const long long nb = sb >= r.i0_bits ? r.hic_bits
+                                           : (static_cast<unsigned long long>(sb) > r.lo_bits ? r.loc_bits : sb);
+      const double nv = __longlong_as_double(nb);
+#else
+      const double lo = (sd < fc.lo_clamp) ? fc.lo_clamp : sd;
+      const double nv = (sd >= fc.i0) ? fc.hi_clamp : lo;
+#endif
+      if ((umask >> j) & 1u) ab[j * 32] = nv;
+      if (F4) {
+        ball[j] = __ballot_sync(0xffffffffu, __double2hiint(nv) < 0);
+      } else {
+        const uint32_t coff = c_col[cb + j].off;
+        st_s8_if(reinterpret_cast<int8_t*>(r.dst_i + uint64_t(coff)),
+                 __double2hiint(nv) < 0 ? -1 : 1, ((umask >> j) & 1u) && r.w_row);
+      }
+    }
+    if (F4) {
+      // lane L stores the e2m1 nibbles of rows 8 (L & 3) .. + 7 of column cb + (L >> 2)
+      const uint32_t a0 = (wj & 1) ? ball[1] : ball[0], a1 = (wj & 1) ? ball[3] : ball[2];
+      const uint32_t a2 = (wj & 1) ? ball[5] : ball[4], a3 = (wj & 1) ? ball[7] : ball[6];
+      const uint32_t b0 = (wj & 2) ? a1 : a0, b1 = (wj & 2) ? a3 : a2;
+      const uint32_t mm = (wj & 4) ? b1 : b0;
+      const uint32_t word = nibbles_pm1((mm >> (8 * (lane & 3))) & 0xffu) & r.nib_live;
+      const uint32_t coffw = c_col[cb + wj].off;
+      st_u32_if(reinterpret_cast<uint32_t*>(r.dst_w + (coffw >> 1)), word,
+                ((umask >> wj) & 1u) && r.nib_live);
+    }
+    if (r.e_mode == 1 || r.e_mode == 2) tmem_st8(r.e_tmem + uint32_t(cb), e);
+    else reduce8_to_quarter(e, q_sum, cb, lane);
+    // the warp's [8 columns x 32 rows] block of new accumulators -> HBM
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncwarp();
+    if (lane == 0) {
+      tma_store_3d(r.tmAs, ab, 0, r.col0 + cb, r.zq);
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      if (nps > 1) {
+        // release the previous chunk's slot once its store has read it
+        asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        if (pend >= 0) mbar_arrive(&ctl->aempty[pend]);
+      } else {
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        mbar_arrive(&ctl->aempty[slot]);
+      }
+    }
+    pend = nps > 1 ? slot : -1;
+  }
+}
+
+// ---- Issue-lean FP64 epilogue (use_tab 0, no row split) ------------------
+// update_fast2's exact arithmetic (magic-number field, the reference's three
+// FP64 adds, the clamp) with the ALU work cut down -- the hot loop is bound by
+// instruction issue and the ALU pipe:
+//  * counter RNG with the 64-bit counter sum pinned, high-word shifts on the
+//    FMA pipe, and the noise level from a byte table (noise_lut);
+//  * the 2^31 bias of the magic conversion folded into the row constant;
+//  * neighbour signs from the copier warp's permuted sign tile: one signed
+//    byte load at a fixed offset whose bit 31 is the sign (no address math);
+//  * the energy sign from the accumulator's high word on the FMA pipe, the
+//    partials kept in TMEM across the row tiles (one warp reduction per pass);
+//  * the clamp with three selects (the rails share their low word).
+struct V4Row {
+  uint32_t iG_lo, iG_hi, p4, p32;
+  uint32_t h1x;              // h1 (+ FP4 bias) + 2^31
+  int h2;
+  uint32_t nbt;              // shared address of row il of sign-tile column 0
+  uint32_t lut;
+  uint32_t e_tmem;
+  int e_mode;                // as CtRow::e_mode
+  uint64_t acc_col;          // &acc[col0 * npad + i]
+  uint32_t col_stride32;     // npad * 8 bytes
+  uint8_t* dst_w;
+  uint32_t nib_live;
+  uint64_t cur_i, dst_i;
+  uint32_t nib_shift;
+  bool w_row;
+  uint32_t jp_hi, jp_lo, hic_hi, loc_hi, rail_lo;
+  uint64_t pol;
+};
+
+template <bool BIDIR, bool SIGACC, bool F4>
+__device__ __forceinline__ void epi_v4(const V4Row& r, const FastConsts& fc, const I2D& i2d,
+                                       SmemCtl* ctl, const double* acc_ring, const ColTab* c_col,
+                                       const uint8_t* c_umask, long long* q_sum, uint32_t trow,
+                                       int sub, int nsubs, int nchunk, int nps, uint32_t cnt0,
+                                       int il, int lane) {
+  int sidx = int(cnt0 % uint32_t(nps));
+  uint32_t ph = (cnt0 / uint32_t(nps)) & 1;
+  const int wj = lane >> 2;
+  const uint32_t colt = smem_u32(c_col);
+  constexpr uint32_t kRow = BIDIR ? 2u * kCtTileRow : uint32_t(kCtTileRow);
+  for (int ch = sub; ch < nchunk; ch += nsubs) {
+    const int cb = ch * kCW;
+    const int slot = sub * nps + sidx;
+    int32_t v[kCW], e[kCW];
+    tmem_ld8_nw(trow + uint32_t(cb), v);
+    if (r.e_mode >= 2) tmem_ld8_nw(r.e_tmem + uint32_t(cb), e);
+    else
+#pragma unroll
+      for (int j = 0; j < kCW; ++j) e[j] = 0;
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    mbar_wait(&ctl->afull[slot], ph);
+    if (++sidx == nps) {
+      sidx = 0;
+      ph ^= 1;
+    }
+    const double* ab = acc_ring + size_t(slot) * kCW * kBM + il;
+    const uint32_t umask = c_umask[ch];
+    const uint32_t nbq = r.nbt + uint32_t(cb) * kRow;
+    uint32_t ball[kCW];
+#pragma unroll
+    for (int j = 0; j < kCW; ++j) {
+      const uint64_t cbase = lds_u64(colt + uint32_t(cb + j) * uint32_t(sizeof(ColTab)));
+      const double a_old = ab[j * kBM];
+      const int S = F4 ? __float_as_int(__int_as_float(v[j]) + 12582912.0f) : v[j];
+      const int s2 = S + r.h2;
+      if (SIGACC) {
+        // sign(acc) = 2 (hi >> 31) + 1, high product on the FMA pipe
+        const int t = __mulhi(__double2hiint(a_old), 2);
+        e[j] += s2 * (2 * t + 1);
+      } else {
+        const uint32_t coff = c_col[cb + j].off;
+        int sg;
+        if (F4) {
+          const uint32_t bc = ld_u8(reinterpret_cast<const uint8_t*>(r.cur_i + (coff >> 1)));
+          sg = ((bc >> r.nib_shift) & 8u) ? -1 : 1;
+        } else {
+          sg = ld_s8(reinterpret_cast<const int8_t*>(r.cur_i + coff));
+        }
+        e[j] += sg * s2;
+      }
+      const uint32_t up = uint32_t(lds_s8(nbq + uint32_t(j) * kRow));
+      const uint32_t t5 = noise_top5_v4(cbase, r.iG_lo, r.iG_hi, r.p4, r.p32);
+      const uint32_t xb = uint32_t(S) + r.h1x + uint32_t(lds_s8(r.lut + t5));
+      double input = __dsub_rn(__hiloint2double(int(i2d.magic_hi), int(xb)), i2d.magic);
+      input = __dadd_rn(input, __hiloint2double(int(r.jp_hi ^ (up & 0x80000000u)), int(r.jp_lo)));
+      if (BIDIR) {
+        const uint32_t dn = uint32_t(lds_s8(nbq + uint32_t(j) * kRow + kCtTileRow));
+        input = __dadd_rn(input, __hiloint2double(int(r.jp_hi ^ (dn & 0x80000000u)), int(r.jp_lo)));
+      }
+      const double sd = __dadd_rn(a_old, input);
+      const bool p_lo = sd < fc.lo_clamp, p_hi = sd >= fc.i0;
+      const int nhi = p_hi ? int(r.hic_hi) : (p_lo ? int(r.loc_hi) : __double2hiint(sd));
+      const int nlo = (p_hi || p_lo) ? int(r.rail_lo) : __double2loint(sd);
+      const double nv = __hiloint2double(nhi, nlo);
+      uint64_t addr;
+      asm("mad.wide.u32 %0, %1, %2, %3;"
+          : "=l"(addr)
+          : "r"(uint32_t(cb + j)), "r"(r.col_stride32), "l"(r.acc_col));
+      st_f64_if(reinterpret_cast<double*>(addr), nv, (umask >> j) & 1u, r.pol);
+      if (F4) {
+        ball[j] = __ballot_sync(0xffffffffu, nhi < 0);
+      } else {
+        const uint32_t coff = c_col[cb + j].off;
+        st_s8_if(reinterpret_cast<int8_t*>(r.dst_i + uint64_t(coff)), nhi < 0 ? -1 : 1,
+                 ((umask >> j) & 1u) && r.w_row);
+      }
+    }
+    if (F4) {
+      const uint32_t a0 = (wj & 1) ? ball[1] : ball[0], a1 = (wj & 1) ? ball[3] : ball[2];
+      const uint32_t a2 = (wj & 1) ? ball[5] : ball[4], a3 = (wj & 1) ? ball[7] : ball[6];
+      const uint32_t b0 = (wj & 2) ? a1 : a0, b1 = (wj & 2) ? a3 : a2;
+      const uint32_t mm = (wj & 4) ? b1 : b0;
+      const uint32_t word = nibbles_pm1((mm >> (8 * (lane & 3))) & 0xffu) & r.nib_live;
+      const uint32_t coffw = c_col[cb + wj].off;
+      st_u32_if(reinterpret_cast<uint32_t*>(r.dst_w + (coffw >> 1)), word,
+                ((umask >> wj) & 1u) && r.nib_live);
+    }
+    if (r.e_mode == 1 || r.e_mode == 2) tmem_st8(r.e_tmem + uint32_t(cb), e);
+    else reduce8_to_quarter(e, q_sum, cb, lane);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&ctl->aempty[slot]);
+  }
+}
+
 // Best-state snapshots during the run copy the packed spin column (npad
 // bytes int8, npad/2 bytes FP4; 16-byte aligned) with vector loads/stores;
 // expand_best_state turns it into the int8 +-1 best_state once at the end.
@@ -1084,7 +1583,7 @@ template <int EPI, bool F4, int CL>
 __global__ void __launch_bounds__(32 * (4 + EPI), 1)
     k_sweep_tc(const __grid_constant__ CUtensorMap tmJ, const __grid_constant__ CUtensorMap tmS,
                const __grid_constant__ CUtensorMap tmSe, const __grid_constant__ CUtensorMap tmA,
-               const TcParams P) {
+               const __grid_constant__ CUtensorMap tmAs, const TcParams P) {
   constexpr bool CTA2 = CL == 1, MC = CL == 2;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-align by offsetting into the shared array itself, so every derived
@@ -1097,8 +1596,8 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
   // 64 bytes of A1 and 64 bytes of A2 nibbles -- against 64 bytes of spins
   const bool pair = F4 && P.pair != 0;
   const int b_row = pair ? kBK / 2 : kBK;
-  const Layout L = make_layout(NT, g.tpt, P.stages, P.nslot, kTileRow, b_row, CTA2 ? NT / 2 : NT,
-                               P.use_tab ? (P.bidirectional ? 4 : 2) * P.tab_w * 8 : 0);
+  const Layout L = make_layout(NT, g.tpt, P.stages, P.nslot, sig_tile_row(P, F4), b_row,
+                               CTA2 ? NT / 2 : NT, tab_bytes_of(P));
   const int stages = L.stages, nslot = L.nslot;
   uint8_t* sA = smem;
   uint8_t* sB = smem + size_t(stages) * L.a_bytes;
@@ -1163,6 +1662,16 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
   const int nrg = (NRT + rgroup - 1) / rgroup;
   // spin rows covered by one K chunk of the operand stream
   const int kKRows = (F4 && !pair) ? 2 * kBK : kBK;
+  // clamped-table epilogue (use_tab 2, never with a row split): neighbour-sign
+  // tiles built by the copier warp, energy partials kept in TMEM columns
+  // [2 NT, 3 NT) across the row tiles when they fit below the scale factors
+  // Fast epilogues without a row split take their neighbour signs from a
+  // permuted sign tile built by the copier warp (nbt_mode): the clamped table
+  // (use_tab 2, ct_mode) and the issue-lean FP64 epilogue (use_tab 0, epi_v4).
+  const bool nbt_mode = P.fast && !split && ((P.use_tab == 0 && P.rails_lo) || P.use_tab == 2);
+  const bool ct_mode = nbt_mode && P.use_tab == 2;
+  const uint32_t ct_tile_bytes = uint32_t(NT) * kCtTileRow * (P.bidirectional ? 2u : 1u);
+  const bool e_tmem = nbt_mode && 3 * NT <= (F4 ? int(kSfCol) : 512);
 
   // ---- one-time setup ----
   if (threadIdx.x == 0) {
@@ -1174,7 +1683,7 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
     for (int b = 0; b < 2; ++b) {
       mbar_init(&ctl->tfull[b], 1);
       mbar_init(&ctl->tempty[b], CTA2 ? 2 * EPI : EPI);  // pair: both CTAs' epilogues
-      mbar_init(&ctl->sfull[b], 1);
+      mbar_init(&ctl->sfull[b], nbt_mode ? 32u : 1u);  // copier warp: every lane arrives
       mbar_init(&ctl->sempty[b], EPI);
     }
     for (int s = 0; s < nslot; ++s) {
@@ -1184,13 +1693,15 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
     for (int b = 0; b < nrg; ++b)
       mbar_init(&ctl->rready[b], EPI * (min(NRT, (b + 1) * rgroup) - b * rgroup));
     mbar_init(&ctl->done, EPI);
+    mbar_init(&ctl->stg, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    for (int r = 0; r < 3; ++r) {
+    for (int r = 0; r < 4; ++r) {
       ctl->ring[r][0] = P.ring_cur;
       for (int q = 0; q <= P.d; ++q) ctl->ring[r][1 + q] = P.ring_phys[q];
     }
     ctl->last_pass = P.c_last;
   }
+  if (threadIdx.x < 32) fill_noise_lut(ctl->nz_lut, P.nr, int(threadIdx.x));
   if (warp == kWarpProducer && lane == 0) {
     prefetch_tmap(&tmJ);
     prefetch_tmap(&tmS);
@@ -1200,7 +1711,7 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
     prefetch_tmap(&tmA);
   }
   if (warp == kWarpMma) {
-    const uint32_t ncols = (F4 || 2 * acc_cols > 256) ? 512u : 256u;
+    const uint32_t ncols = (F4 || nbt_mode || 2 * acc_cols > 256) ? 512u : 256u;
     if (CTA2) {
       asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                        smem_u32(&ctl->tmem_base)),
@@ -1277,6 +1788,8 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
   // before it has decided to stop is drained by the epilogue without work.
   // rows_wait(s, b): group b of pass index s (= c - c_first) is complete.
   auto rows_wait = [&](long s, int b) { mbar_wait(&ctl->rready[b], uint32_t(s) & 1u); };
+  // the control warps' form (long waits, no issue-slot polling)
+  auto rows_wait_lazy = [&](long s, int b) { mbar_wait_lazy(&ctl->rready[b], uint32_t(s) & 1u, 256); };
   auto stop_at = [&](long c) { return c > *reinterpret_cast<volatile long*>(&ctl->last_pass); };
 
   if (warp == kWarpProducer) {
@@ -1289,7 +1802,7 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
         const long s = c - P.c_first;
         int waited = 0;
         if (s > 0) {
-          rows_wait(s - 1, 0);
+          rows_wait_lazy(s - 1, 0);
           waited = 1;
           if (stop_at(c)) break;
         }
@@ -1306,7 +1819,7 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
                 asm volatile("fence.proxy.async.global;" ::: "memory");
               } else {
                 const int need = min(nrg - 1, min(NRT - 1, ((kc + 1) * kKRows - 1) / kBM) / rgroup);
-                while (waited <= need) rows_wait(s - 1, waited++);
+                while (waited <= need) rows_wait_lazy(s - 1, waited++);
               }
             }
             const int st = it % stages;
@@ -1318,7 +1831,7 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
               if (pk >= NKC) pk -= NKC, ++prt;
               if (prt < NRT) tma_prefetch_2d(&tmJ, pk * kBK, j_row0 + (rt_lo + prt) * kBM);
             }
-            mbar_wait(&ctl->empty[st], ph ^ 1);
+            mbar_wait_lazy(&ctl->empty[st], ph ^ 1, SSQA_LAZY_NS_PROD);
             if (P.exp_flags & 4) {
               if (!CTA2 || leader) mbar_arrive(&ctl->full[st]);
             } else if (MC) {
@@ -1362,13 +1875,13 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
       for (long c = P.c_first; c <= P.c_last; ++c) {
         const long s = c - P.c_first;
         if (s > 0) {
-          rows_wait(s - 1, 0);
+          rows_wait_lazy(s - 1, 0);
           if (stop_at(c)) break;
         }
         for (int rt = 0; rt < NRT; ++rt, ++acc_it) {
           const int buf = acc_it & 1;
           const uint32_t aph = (acc_it >> 1) & 1;
-          mbar_wait(&ctl->tempty[buf], aph ^ 1);
+          mbar_wait_lazy(&ctl->tempty[buf], aph ^ 1, SSQA_LAZY_NS_MMA);
           tc_fence_after();
           DBG_STAMP(0, acc_it, 0);
           const uint32_t d_tmem = tmem_base + uint32_t(buf * acc_cols);
@@ -1412,9 +1925,9 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
       }
     }
     __syncwarp();
-    mbar_wait(&ctl->done, 0);
+    mbar_wait_lazy(&ctl->done, 0, 1000);
     tc_fence_after();
-    const uint32_t ncols = (F4 || 2 * acc_cols > 256) ? 512u : 256u;
+    const uint32_t ncols = (F4 || nbt_mode || 2 * acc_cols > 256) ? 512u : 256u;
     if (CTA2) {
       cluster_sync_all();  // both CTAs' epilogues are done with the pair's TMEM
       asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
@@ -1439,7 +1952,7 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
         const long s = c - P.c_first;
         int waited = 0;
         if (s > 0) {
-          rows_wait(s - 1, 0);
+          rows_wait_lazy(s - 1, 0);
           waited = 1;
           if (stop_at(c)) break;
         }
@@ -1448,8 +1961,8 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
           // accumulators (and, for delay 0, the neighbour spins) of these rows
           // were written by pass c-1
           if (s > 0)
-            while (waited <= rt / rgroup) rows_wait(s - 1, waited++);
-          if (sb2 == 0) {
+            while (waited <= rt / rgroup) rows_wait_lazy(s - 1, waited++);
+          if (sb2 == 0 && split) {  // (without a row split warp EPI+3 loads these tiles)
             const int sb = acc_it & 1;
             const uint32_t sph = (acc_it >> 1) & 1;
             mbar_wait(&ctl->sempty[sb], sph ^ 1);
@@ -1466,10 +1979,14 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
             const uint32_t cnt = acc_it * my_chunks + uint32_t(ch / nsubs);
             const int slot = sb2 * nps + int(cnt % uint32_t(nps));
             const uint32_t ph = (cnt / uint32_t(nps)) & 1;
-            mbar_wait(&ctl->aempty[slot], ph ^ 1);
+            mbar_wait_lazy(&ctl->aempty[slot], ph ^ 1, SSQA_LAZY_NS_LOAD);
             mbar_expect_tx(&ctl->afull[slot], kCW * kBM * 8);
-            tma_load_2d_hint(&tmA, &ctl->afull[slot], acc_ring + size_t(slot) * kCW * kBM,
-                             (rt_lo + rt) * kBM, col0 + ch * kCW, pol_first);
+            if (ct_mode)  // [row block][column][32 rows]: one dense block per epilogue warp
+              tma_load_3d_hint(&tmA, &ctl->afull[slot], acc_ring + size_t(slot) * kCW * kBM, 0,
+                               col0 + ch * kCW, (rt_lo + rt) * 4, pol_first);
+            else
+              tma_load_2d_hint(&tmA, &ctl->afull[slot], acc_ring + size_t(slot) * kCW * kBM,
+                               (rt_lo + rt) * kBM, col0 + ch * kCW, pol_first);
           }
           if (sb2 == 0) DBG_STAMP(1, acc_it, 1);
         }
@@ -1486,12 +2003,142 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
     // written a group of its row tiles in pass c, stamp them for the other
     // CTAs of the column tile (their producers load all rows of sigma) =====
     SSQA_CTL_REGS();
-    if (split && scan_mode && lane == 0) {
+    if (nbt_mode) {
+      // ===== neighbour-sign tiles of the clamped-table epilogue: for row tile
+      // rt, byte [column][row] = 8 where sigma_{k+1}(c-d) of that row is
+      // negative (up plane), 16 where sigma_{k-1}(c-d) is (down plane,
+      // bidirectional only), copied from the delayed spin slot with the
+      // neighbour permutation applied (column p holds its neighbour's signs) =====
+      int* ring = ctl->ring[3];
+      const bool bidir = P.bidirectional != 0;
+      const uint32_t rowstride = uint32_t(kCtTileRow) * (bidir ? 2u : 1u);
+      // staging for the TMA-loaded spin rows (one tile, behind the two sign buffers)
+      uint8_t* stg = sig_tiles + 2 * size_t(ct_tile_bytes);
+      uint32_t it2 = 0, sph = 0;
+      for (long c = P.c_first; c <= P.c_last; ++c) {
+        const long s = c - P.c_first;
+        int waited = 0;
+        if (s > 0) {
+          rows_wait_lazy(s - 1, 0);
+          waited = 1;
+          if (stop_at(c)) break;
+        }
+        const int ySrc = ring[1 + int(c % (P.d + 1))] * g.ccols + col0;
+        for (int rt = 0; rt < NRT; ++rt, ++it2) {
+          if (s > 0)
+            while (waited <= rt / rgroup) rows_wait_lazy(s - 1, waited++);
+          if (lane == 0) {
+            mbar_expect_tx(&ctl->stg, uint32_t(NT) * kTileRow);
+            tma_load_2d(&tmSe, &ctl->stg, stg, (rt_lo + rt) * kTileRow, ySrc);
+          }
+          const int buf = int(it2 & 1u);
+          mbar_wait_lazy(&ctl->sempty[buf], ((it2 >> 1) & 1u) ^ 1u, SSQA_LAZY_NS_LOAD);
+          mbar_wait(&ctl->stg, sph);
+          sph ^= 1u;
+          uint8_t* dst = sig_tiles + size_t(buf) * ct_tile_bytes;
+          if (P.exp_flags & 32) {
+            // timing ablation: stale neighbour signs (no copy)
+          } else if (F4) {
+            // 64 bytes (128 rows) per column: 4 x 16 bytes, each -> 32 sign bytes
+            for (int u = lane; u < NT * 4; u += 32) {
+              const int pcol = u >> 2, part = u & 3;
+              const uint32_t nbr = c_col[pcol].nbr;
+              int su = int((nbr & 0xffffu) / uint32_t(kTileRow));
+              su = su < NT ? su : pcol;
+              const uint4 w = *reinterpret_cast<const uint4*>(stg + size_t(su) * kTileRow + part * 16);
+              const uint32_t wv[4] = {w.x, w.y, w.z, w.w};
+              uint32_t o[8];
+#pragma unroll
+              for (int k = 0; k < 4; ++k) {
+                const uint32_t t = wv[k] & 0x88888888u;
+                const uint32_t ev = (t << 4) & 0x80808080u, od = t & 0x80808080u;
+                o[2 * k] = __byte_perm(ev, od, 0x5140);
+                o[2 * k + 1] = __byte_perm(ev, od, 0x7362);
+              }
+              uint4* d = reinterpret_cast<uint4*>(dst + size_t(pcol) * rowstride + uint32_t(part) * 32u);
+              d[0] = make_uint4(o[0], o[1], o[2], o[3]);
+              d[1] = make_uint4(o[4], o[5], o[6], o[7]);
+              if (bidir) {
+                int sd = int(((nbr >> 16) & 0x7fffu) / uint32_t(kTileRow));
+                sd = sd < NT ? sd : pcol;
+                const uint4 w2 = *reinterpret_cast<const uint4*>(stg + size_t(sd) * kTileRow + part * 16);
+                const uint32_t wv2[4] = {w2.x, w2.y, w2.z, w2.w};
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                  const uint32_t t = wv2[k] & 0x88888888u;
+                  const uint32_t ev = (t << 4) & 0x80808080u, od = t & 0x80808080u;
+                  o[2 * k] = __byte_perm(ev, od, 0x5140);
+                  o[2 * k + 1] = __byte_perm(ev, od, 0x7362);
+                }
+                uint4* d2 = reinterpret_cast<uint4*>(dst + size_t(pcol) * rowstride + kCtTileRow +
+                                                     uint32_t(part) * 32u);
+                d2[0] = make_uint4(o[0], o[1], o[2], o[3]);
+                d2[1] = make_uint4(o[4], o[5], o[6], o[7]);
+              }
+            }
+          } else {
+            // int8 +-1 rows: 128 bytes per column, 8 x 16 bytes
+            for (int u = lane; u < NT * 8; u += 32) {
+              const int pcol = u >> 3, part = u & 7;
+              const uint32_t nbr = c_col[pcol].nbr;
+              int su = int((nbr & 0xffffu) / uint32_t(kTileRow));
+              su = su < NT ? su : pcol;
+              const uint4 w = *reinterpret_cast<const uint4*>(stg + size_t(su) * kTileRow + part * 16);
+              uint4* d = reinterpret_cast<uint4*>(dst + size_t(pcol) * rowstride + uint32_t(part) * 16u);
+              *d = make_uint4(w.x & 0x80808080u, w.y & 0x80808080u, w.z & 0x80808080u,
+                              w.w & 0x80808080u);
+              if (bidir) {
+                int sd = int(((nbr >> 16) & 0x7fffu) / uint32_t(kTileRow));
+                sd = sd < NT ? sd : pcol;
+                const uint4 w2 = *reinterpret_cast<const uint4*>(stg + size_t(sd) * kTileRow + part * 16);
+                uint4* d2 = reinterpret_cast<uint4*>(dst + size_t(pcol) * rowstride + kCtTileRow +
+                                                     uint32_t(part) * 16u);
+                *d2 = make_uint4(w2.x & 0x80808080u, w2.y & 0x80808080u, w2.z & 0x80808080u,
+                                 w2.w & 0x80808080u);
+              }
+            }
+          }
+          __syncwarp();  // the staging tile is read before the next TMA overwrites it
+          mbar_arrive(&ctl->sfull[buf]);  // every lane (count 32): its stores are done
+        }
+        __syncwarp();
+        if (lane == 0 && c < P.sc) ring_advance(ring, c, P.d, P.nslots);
+        __syncwarp();
+      }
+    } else if (!split) {
+      // ===== delayed-neighbour spin tiles (TMA), on their own warp so they never
+      // queue behind the accumulator loads of an epilogue subgroup =====
+      if (lane == 0) {
+        int* ring = ctl->ring[3];
+        uint32_t it2 = 0;
+        for (long c = P.c_first; c <= P.c_last; ++c) {
+          const long s = c - P.c_first;
+          int waited = 0;
+          if (s > 0) {
+            rows_wait_lazy(s - 1, 0);
+            waited = 1;
+            if (stop_at(c)) break;
+          }
+          const int ySrc = ring[1 + int(c % (P.d + 1))] * g.ccols + col0;
+          for (int rt = 0; rt < NRT; ++rt, ++it2) {
+            if (s > 0)
+              while (waited <= rt / rgroup) rows_wait_lazy(s - 1, waited++);
+            const int sb = int(it2 & 1u);
+            mbar_wait_lazy(&ctl->sempty[sb], ((it2 >> 1) & 1u) ^ 1u, SSQA_LAZY_NS_LOAD);
+            mbar_expect_tx(&ctl->sfull[sb], uint32_t(NT) * kTileRow);
+            tma_load_2d(&tmSe, &ctl->sfull[sb], sig_tiles + size_t(sb) * NT * kTileRow,
+                        (rt_lo + rt) * kTileRow, ySrc);
+          }
+          if (c < P.sc) ring_advance(ring, c, P.d, P.nslots);
+        }
+      }
+      __syncwarp();
+    } else if (split && scan_mode && lane == 0) {
       for (long c = P.c_first; c <= P.c_last; ++c) {
         const long s = c - P.c_first;
         if (s > 0 && stop_at(c)) break;
         for (int b = 0; b < nrg; ++b) {
-          rows_wait(s, b);
+          rows_wait_lazy(s, b);
           __threadfence();
           const int r1 = min(NRT, (b + 1) * rgroup);
           for (int r = b * rgroup; r < r1; ++r)
@@ -1509,13 +2156,31 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
     const int sub = ew >> 2;
     constexpr int kSubs = EPI / 4;
     int* ring = ctl->ring[2];
+    int ct_pend = -1;    // clamped-table path: ring slot still read by a TMA store
     bool drain = false;  // every trial of the tile has stopped: consume only
     for (long c = P.c_first; c <= P.c_last; ++c) {
       if (stop_at(c)) break;
       const bool do_update = c < P.sc;
       const int cur = ring[0];
       const int dst = do_update ? ring_free(cur, ring + 1, P.d, P.nslots) : cur;
-      if (!drain && P.fast && P.use_tab) {
+      if (!drain && P.fast && P.use_tab == 2) {
+        // clamped table (use_tab 2): row x = 0 .. tab_w + 1 holds X = tab_lo1 - 1 + x,
+        // entry [x][combo] = fl(fl(X 2^-p + jperp u) [+ jperp d]) with the
+        // reference's own operations (annealer.cpp:276-284); rows 0 and tab_w + 1
+        // are decided fields (low / high) and stand for every field beyond them
+        const double jp = P.run_mode ? P.jperp_tab[c] : P.jperp_fixed;
+        const double jpos = __dmul_rn(jp, 1.0), jneg = __dmul_rn(jp, -1.0);
+        const I2D i2 = make_i2d(P.shift_p);
+        const int ncmb = P.bidirectional ? 4 : 2;
+        for (int e = ew * 32 + lane; e < ncmb * (P.tab_w + 2); e += EPI * 32) {
+          const int x = e / ncmb, cmb = e - x * ncmb;
+          double in = scaled_i32(P.tab_lo1 - 1 + x, i2);
+          in = __dadd_rn(in, (cmb & 1) ? jneg : jpos);
+          if (P.bidirectional) in = __dadd_rn(in, (cmb & 2) ? jneg : jpos);
+          ytab[e] = in;
+        }
+      }
+      if (!drain && P.fast && P.use_tab == 1) {
         // this cycle's table of fl(fl(X 2^-p + jperp u) [+ jperp d]) (TabConsts),
         // with the reference's own operations (annealer.cpp:276-284)
         const double jp = P.run_mode ? P.jperp_tab[c] : P.jperp_fixed;
@@ -1531,14 +2196,21 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
         }
       }
       if (!drain) {
-        for (int cl = ew * 32 + lane; cl < NT; cl += EPI * 32) {
-          const int k = c_kt[cl] & 0xffff, tl = c_kt[cl] >> 16;
-          // key + spin_counter(c, k, 0) * golden, plus mix64's initial += golden
-          c_col[cl].base = c_key[cl] + spin_counter(uint64_t(c), uint32_t(k), 0) * kGolden + kGolden;
-          const uint32_t live = uint32_t(c_flag[cl] & 1);
-          const uint32_t upd = live && do_update && (!P.run_mode || trials[tl].active);
-          c_col[cl].nbr = (c_col[cl].nbr & 0x7fffffffu) | (upd << 31);
-          for (int qq = 0; qq < 4; ++qq) c_E[qq * NT + cl] = 0;
+        for (int c0 = ew * 32; c0 < NT; c0 += EPI * 32) {
+          const int cl = c0 + lane;
+          uint32_t upd = 0;
+          if (cl < NT) {
+            const int k = c_kt[cl] & 0xffff, tl = c_kt[cl] >> 16;
+            // key + spin_counter(c, k, 0) * golden, plus mix64's initial += golden
+            c_col[cl].base = c_key[cl] + spin_counter(uint64_t(c), uint32_t(k), 0) * kGolden + kGolden;
+            const uint32_t live = uint32_t(c_flag[cl] & 1);
+            upd = live && do_update && (!P.run_mode || trials[tl].active);
+            c_col[cl].nbr = (c_col[cl].nbr & 0x7fffffffu) | (upd << 31);
+            for (int qq = 0; qq < 4; ++qq) c_E[qq * NT + cl] = 0;
+          }
+          // per-chunk update masks (bit j: column 8 ch + j updates)
+          const uint32_t bal = __ballot_sync(0xffffffffu, upd != 0u);
+          if (lane < 4 && c0 + 8 * lane < NT) ctl->umask[c0 / 8 + lane] = uint8_t(bal >> (8 * lane));
         }
       }
       long long* q_sum = c_E + q * NT;
@@ -1632,13 +2304,108 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
           }
           er.npeer = P.npeer;
           er.peer_delta = P.peer_delta;
+          er.i_u32 = uint32_t(i);
+          asm volatile("mov.b32 %0, %1;" : "=r"(er.p4) : "r"(4u));
+          asm volatile("mov.b32 %0, %1;" : "=r"(er.p32) : "r"(32u));
+          er.h1x = uint32_t(er.h1) + 0x80000000u;
+          er.nz_lut = ctl->nz_lut;
+          er.h1c = er.h1 - (P.tab_lo1 - 1);
+          er.ct_max = P.tab_w + 1;
+          er.nb_shift = F4 ? er.nib_shift : 4u;
+          er.ytab = smem_u32(ytab);
+          er.tmAs = &tmAs;
+          er.col0 = col0;
+          er.zq = (rt_lo + rt) * 4 + q;
 #define SSQA_EPI(B, S, F, T)                                                               \
   epi_chunks<B, S, F, F4, T>(er, uc, fc, tc, i2d, ctl, acc_ring, c_col, q_sum, trow, \
                              sub, kSubs, nchunk, nps, cnt0, il, lane)
-#define SSQA_EPI_FAST(B, S)        \
-  if (P.use_tab) SSQA_EPI(B, S, true, true); \
+#define SSQA_EPI_FAST(B, S)                  \
+  if (P.use_tab == 1) SSQA_EPI(B, S, true, true); \
   else SSQA_EPI(B, S, true, false)
-          if (fast && sig_from_acc) {
+          if (ct_mode) {
+            CtRow cr;
+            cr.i_u32 = er.i_u32;
+            cr.iG_lo = er.iG_lo;
+            cr.iG_hi = er.iG_hi;
+            cr.nr = P.nr;
+            cr.i0_bits = tc.i0_bits;
+            cr.hic_bits = tc.hic_bits;
+            cr.loc_bits = tc.loc_bits;
+            cr.lo_bits = tc.lo_bits;
+            cr.p4 = er.p4;
+            cr.p32 = er.p32;
+            cr.h1c = er.h1 - (P.tab_lo1 - 1);
+            cr.h2 = er.h2;
+            cr.ct_max = P.tab_w + 1;
+            cr.nbt = smem_u32(sig_tiles) + uint32_t(buf) * ct_tile_bytes + uint32_t(il);
+            cr.ytab = smem_u32(ytab);
+            cr.lut = smem_u32(ctl->nz_lut);
+            cr.e_tmem = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(2 * acc_cols);
+            cr.e_mode = (!e_tmem || NRT == 1) ? 0 : (rt == 0 ? 1 : (rt == NRT - 1 ? 3 : 2));
+            cr.dst_w = er.dst_w;
+            cr.nib_live = er.nib_live;
+            cr.cur_i = er.cur_i;
+            cr.dst_i = er.dst_i;
+            cr.nib_shift = er.nib_shift;
+            cr.w_row = row_live;
+            cr.tmAs = &tmAs;
+            cr.col0 = col0;
+            cr.zq = (rt_lo + rt) * 4 + q;
+#define SSQA_CT(B, S)                                                                        \
+  epi_ct<B, S, F4>(cr, fc, ctl, acc_ring, c_col, ctl->umask, q_sum, trow, sub, kSubs, nchunk, \
+                   nps, cnt0, q, lane, ct_pend)
+            if (sig_from_acc) {
+              if (bidir) SSQA_CT(true, true);
+              else SSQA_CT(false, true);
+            } else {
+              if (bidir) SSQA_CT(true, false);
+              else SSQA_CT(false, false);
+            }
+#undef SSQA_CT
+            // the last chunk's slot, once its store has read it
+            if (lane == 0) {
+              asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+              if (ct_pend >= 0) mbar_arrive(&ctl->aempty[ct_pend]);
+            }
+            ct_pend = -1;
+          } else if (nbt_mode) {
+            V4Row vr;
+            vr.iG_lo = er.iG_lo;
+            vr.iG_hi = er.iG_hi;
+            vr.p4 = er.p4;
+            vr.p32 = er.p32;
+            vr.h1x = er.h1x;
+            vr.h2 = er.h2;
+            vr.nbt = smem_u32(sig_tiles) + uint32_t(buf) * ct_tile_bytes + uint32_t(il);
+            vr.lut = smem_u32(ctl->nz_lut);
+            vr.e_tmem = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(2 * acc_cols);
+            vr.e_mode = (!e_tmem || NRT == 1) ? 0 : (rt == 0 ? 1 : (rt == NRT - 1 ? 3 : 2));
+            vr.acc_col = reinterpret_cast<uint64_t>(P.acc + size_t(col0) * g.npad + i);
+            vr.col_stride32 = uint32_t(g.npad) * 8u;
+            vr.dst_w = er.dst_w;
+            vr.nib_live = er.nib_live;
+            vr.cur_i = er.cur_i;
+            vr.dst_i = er.dst_i;
+            vr.nib_shift = er.nib_shift;
+            vr.w_row = row_live;
+            vr.jp_hi = fc.jp_hi;
+            vr.jp_lo = fc.jp_lo;
+            vr.hic_hi = uint32_t(__double2hiint(fc.hi_clamp));
+            vr.loc_hi = uint32_t(__double2hiint(fc.lo_clamp));
+            vr.rail_lo = uint32_t(__double2loint(fc.hi_clamp));  // == loc's (fast_ok)
+            vr.pol = pol_first;
+#define SSQA_V4(B, S)                                                                       \
+  epi_v4<B, S, F4>(vr, fc, i2d, ctl, acc_ring, c_col, ctl->umask, q_sum, trow, sub, kSubs, \
+                   nchunk, nps, cnt0, il, lane)
+            if (sig_from_acc) {
+              if (bidir) SSQA_V4(true, true);
+              else SSQA_V4(false, true);
+            } else {
+              if (bidir) SSQA_V4(true, false);
+              else SSQA_V4(false, false);
+            }
+#undef SSQA_V4
+          } else if (fast && sig_from_acc) {
             if (bidir) SSQA_EPI_FAST(true, true);
             else SSQA_EPI_FAST(false, true);
           } else if (fast) {
@@ -1655,6 +2422,7 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
 #undef SSQA_EPI
         }
         tc_fence_before();
+        const bool ct_now = ct_mode && !drain && !(P.exp_flags & 1);
         // this warp's spin rows and accumulators of row tile rt are in global
         // memory: make them visible to the TMA (async proxy) reads of pass c+1
         asm volatile("fence.proxy.async.global;" ::: "memory");
@@ -1664,7 +2432,22 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
           if (CTA2 && !leader) mbar_arrive_cluster(mapa_rank(smem_u32(&ctl->tempty[buf]), 0));
           else mbar_arrive(&ctl->tempty[buf]);
           mbar_arrive(&ctl->sempty[buf]);
-          mbar_arrive(&ctl->rready[rt / rgroup]);
+          if (ct_now) {
+            // The accumulators of a row tile go out as TMA stores; it is
+            // published ("rows ready") once they are complete -- one row tile
+            // later, so no warp waits on the store it has just issued (the
+            // readers are the next pass's loads, a whole pass away).
+            if (rt == NRT - 1) {
+              asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+              if (rt > 0) mbar_arrive(&ctl->rready[(rt - 1) / rgroup]);
+              mbar_arrive(&ctl->rready[rt / rgroup]);
+            } else if (rt > 0) {
+              bulk_wait_group(chunks_of(sub));  // the previous row tile's stores
+              mbar_arrive(&ctl->rready[(rt - 1) / rgroup]);
+            }
+          } else {
+            mbar_arrive(&ctl->rready[rt / rgroup]);
+          }
         }
       }
       epi_bar<EPI>();
@@ -1913,6 +2696,24 @@ bool make_map(CUtensorMap* m, void* base, CUtensorMapDataType dt, uint32_t esize
   return r == CUDA_SUCCESS;
 }
 
+// Accumulators f64 [ccols][npad] as a 3D tensor {32 rows, ccols columns,
+// npad/32 row blocks} (strides 8 B, npad*8 B, 256 B): a box {32, 8, nq}
+// lands in shared memory as [row block][column][32 rows], so each epilogue
+// warp's rows of a chunk are one dense 2 KB block (load nq = 4, per-warp
+// store nq = 1).
+bool make_acc_map(CUtensorMap* m, void* base, uint64_t npad, uint64_t ccols, uint32_t nq) {
+  EncodeFn enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[3] = {32, ccols, npad / 32};
+  cuuint64_t strides[2] = {npad * 8, 256};
+  cuuint32_t box[3] = {32, uint32_t(kCW), nq};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 // Operand stages and per-subgroup state-ring depth inside ~226 KB: prefer
 // deep accumulator rings (up to 3 slots per subgroup, so the loader runs
 // chunks ahead of the HBM latency), then as many operand stages (<= 4) as fit.
@@ -1940,6 +2741,12 @@ Layout pick_layout(int NT, int tpt, int nsubs, int tile_row, int b_row, int b_co
     }
   return make_layout(NT, tpt, 2, nsubs, tile_row, b_row, b_cols, tab_bytes);
 }
+
+// Fast epilogue without a row split: 2 clamped table, 0 FP64 (update_fast2).
+#ifndef SSQA_NOSPLIT_EPI
+#define SSQA_NOSPLIT_EPI 0
+#endif
+constexpr int kDefaultNoSplitEpi = SSQA_NOSPLIT_EPI;
 
 // 16 epilogue warps (4 per scheduler): the update chain is latency-bound,
 // so more resident warps beat more registers per warp (C3: -5 %/sweep vs 12).
@@ -1976,7 +2783,7 @@ cudaError_t launch_variant(int grid, int smem, cudaStream_t st, const CUtensorMa
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
   cfg.numAttrs = coop ? 1 : 0;
-  e = cudaLaunchKernelEx(&cfg, kern, maps[0], maps[1], maps[2], maps[3], P);
+  e = cudaLaunchKernelEx(&cfg, kern, maps[0], maps[1], maps[2], maps[3], maps[4], P);
   if (e == cudaErrorCooperativeLaunchTooLarge) return cudaErrorNotSupported;
   return e;
 }
@@ -2034,7 +2841,7 @@ cudaError_t launch_variant_pair(int grid, int smem, cudaStream_t st, const CUten
   e = cudaOccupancyMaxActiveClusters(&clusters, kern, &cfg);
   if (e != cudaSuccess) return e;
   if (csize * clusters < grid) return cudaErrorNotSupported;
-  return cudaLaunchKernelEx(&cfg, kern, maps[0], maps[1], maps[2], maps[3], P);
+  return cudaLaunchKernelEx(&cfg, kern, maps[0], maps[1], maps[2], maps[3], maps[4], P);
 }
 
 // int8 spin slot -> FP4 (e2m1) slot: +1 -> 0x2, -1 -> 0xA, 0 -> 0x0.
@@ -2074,9 +2881,22 @@ int launch(ssqa_batch_s* b, TcParams& P, bool f4) {
   // Table epilogue for row splits: their MMAs keep the tensor core busy, and
   // the FP64 units share its issue path; the FP64 epilogue is cheaper where
   // they are mostly free (C3: 1146 vs 1178 ms/step).  Tune key "tab" forces.
-  P.use_tab = (P.fast && P.tab_w > 0 && (g.rs > 1 || P.npeer)) ? 1 : 0;
-  if (tune().tab >= 0) P.use_tab = (P.fast && P.tab_w > 0 && tune().tab) ? 1 : 0;
-  CUtensorMap maps[4];
+  // clamped-table epilogue elsewhere (two FP64 adds fewer than update_fast2).
+  // Tune key "tab": 0 FP64 epilogue, 1 table epilogue, 2 clamped table.
+  const bool tab_ok = P.fast && P.tab_w > 0;
+  P.use_tab = tab_ok ? ((g.rs > 1 || P.npeer) ? 1 : kDefaultNoSplitEpi) : 0;
+  if (tune().tab >= 0) P.use_tab = tab_ok ? std::min(2, tune().tab) : 0;
+  if (P.fast && g.rs == 1 && (P.use_tab == 2 || (P.use_tab == 0 && P.rails_lo))) {
+    // the sign tiles of the copier warp must fit next to the smallest pipeline
+    const bool pr = f4 && b->prob->q.fp4x2_ok;
+    const Layout Lmin = make_layout(g.tile_cols, g.tpt, 2, 4, sig_tile_row(P, f4),
+                                    pr ? kBK / 2 : kBK, g.tile_cols, tab_bytes_of(P));
+    if (Lmin.total > 226u * 1024u) {
+      P.use_tab = 0;
+      P.rails_lo = 0;  // plain FP64 epilogue, spin tiles by TMA
+    }
+  }
+  CUtensorMap maps[5];
   const uint64_t srows = uint64_t(b->nslots) * g.ccols;
   // FP4 rows are npad/2 bytes (two e2m1 values per byte)
   const uint64_t row_bytes = f4 ? uint64_t(g.npad) / 2 : uint64_t(g.npad);
@@ -2095,8 +2915,13 @@ int launch(ssqa_batch_s* b, TcParams& P, bool f4) {
                 g.tile_cols, pair ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B) ||
       !make_map(&maps[2], Ssrc, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, row_bytes, srows, tile_row,
                 g.tile_cols, CU_TENSOR_MAP_SWIZZLE_NONE) ||
-      !make_map(&maps[3], b->d_acc, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, g.npad, g.ccols, kBM,
-                kCW, CU_TENSOR_MAP_SWIZZLE_NONE)) {
+      !(P.fast && P.use_tab == 2 && g.rs == 1
+            ? make_acc_map(&maps[3], b->d_acc, g.npad, g.ccols, 4) &&
+                  make_acc_map(&maps[4], b->d_acc, g.npad, g.ccols, 1)
+            : make_map(&maps[3], b->d_acc, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, g.npad, g.ccols,
+                       kBM, kCW, CU_TENSOR_MAP_SWIZZLE_NONE) &&
+                  make_map(&maps[4], b->d_acc, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, g.npad,
+                           g.ccols, kBM, kCW, CU_TENSOR_MAP_SWIZZLE_NONE))) {
     g_tc_err = "cuTensorMapEncodeTiled failed";
     return SSQA_ECUDA;
   }
@@ -2125,7 +2950,10 @@ int launch(ssqa_batch_s* b, TcParams& P, bool f4) {
     P.g_rows = reinterpret_cast<int*>(base + size_t(2) * g.ccols * 8 + size_t(g.ntiles) * 8);
     P.g_arrive = reinterpret_cast<unsigned*>(P.g_rows + size_t(g.ntiles) * nrt_all);
   }
-  const int epi = tune().epi ? (tune().epi == 12 ? 12 : 16) : kDefaultEpi;
+  // 12 epilogue warps (160 registers each) for the issue-lean epilogue without
+  // a row split (C3: 213.9 vs 216.9 us/sweep with 16), 16 elsewhere (CTA pairs)
+  const bool lean = P.fast && g.rs == 1 && (P.use_tab == 2 || (P.use_tab == 0 && P.rails_lo));
+  const int epi = tune().epi ? (tune().epi == 12 ? 12 : 16) : (lean ? 12 : kDefaultEpi);
   // CTA pairs (M = 256 MMAs, each CTA streams half of the spin columns): the
   // fused run's row split with an even number of parts per column tile and
   // of row tiles; tune key "cta2" 0 turns them off
@@ -2145,12 +2973,12 @@ int launch(ssqa_batch_s* b, TcParams& P, bool f4) {
     if (!make_map(&maps[1], Ssrc, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, row_bytes, srows, b_row,
                   uint32_t(b_cols), pair ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B))
       return false;
-    const int tab_bytes = P.use_tab ? (P.bidirectional ? 4 : 2) * P.tab_w * 8 : 0;
-    L = pick_layout(g.tile_cols, g.tpt, epi / 4, int(tile_row), int(b_row), b_cols, tab_bytes,
+    const int tab_bytes = tab_bytes_of(P);
+    L = pick_layout(g.tile_cols, g.tpt, epi / 4, sig_tile_row(P, f4), int(b_row), b_cols, tab_bytes,
                     pair || g.rs > 1);
     if (tune().stages > 0) {  // experiment overrides
       L = make_layout(g.tile_cols, g.tpt, tune().stages, std::max(1, tune().nps) * (epi / 4),
-                      int(tile_row), int(b_row), b_cols, tab_bytes);
+                      sig_tile_row(P, f4), int(b_row), b_cols, tab_bytes);
     }
     P.stages = L.stages;
     P.nslot = L.nslot;
@@ -2219,6 +3047,7 @@ int launch(ssqa_batch_s* b, TcParams& P, bool f4) {
       // the row parts cannot all be resident: every CTA runs all rows of its tile
       cudaGetLastError();
       P.g.rs = 1;
+      if (P.use_tab == 2) P.use_tab = 0;  // layout and maps were set up for the split
       grid = g.ntiles;
       e = single();
     }
@@ -2256,7 +3085,8 @@ bool fast_ok(const ssqa_batch_s* b, TcParams* P) {
   for (double v : b->ssa_levels)
     if (!std::isfinite(v) || !std::isfinite(v - p.alpha)) return false;
   const double x = std::ldexp(p.n_rnd, q.p);
-  if (x != std::floor(x) || std::fabs(x) >= double(1 << 28)) return false;
+  // the noise joins the integer field through a byte table (noise_lut)
+  if (x != std::floor(x) || std::fabs(x) > 127.0) return false;
   const double row_max = double(q.max_abs_j) * q.n + 2.0 * q.max_abs_h;
   if (row_max + std::fabs(x) >= double(1u << 30)) return false;
   if (double(q.npad) / 4.0 * row_max >= 2147483647.0) return false;
@@ -2272,6 +3102,14 @@ bool fast_ok(const ssqa_batch_s* b, TcParams* P) {
     jpmax = std::max(std::fabs(p.jperp_min), std::fabs(p.jperp_max));
   }
   P->nr = int(x);
+  // the issue-lean epilogue selects the clamp rails' low word once
+  auto lo_word = [](double v) { uint64_t b; std::memcpy(&b, &v, 8); return uint32_t(b); };
+  P->rails_lo = 1;
+  if (b->ssa) {
+    for (double v : b->ssa_levels) P->rails_lo &= lo_word(v - p.alpha) == lo_word(-v);
+  } else {
+    P->rails_lo = lo_word(p.i0 - p.alpha) == lo_word(-p.i0);
+  }
   // table epilogue when i0 > 0 and the undecided band fits (else tab_w = 0)
   P->tab_w = 0;
   bool pos = i0max > 0.0;
