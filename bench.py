@@ -87,6 +87,15 @@ def n_spins(cfg):
     return cfg["n_nodes"] ** 2 if cfg["kind"] == "gi" else cfg["n"]
 
 
+def config_of(cfg):
+    """The `config` object of both arms (identical keys and values)."""
+    N, R, T = n_spins(cfg), cfg["R"], cfg["T"]
+    return {"workload": cfg["desc"], "n": N, "replicas": R, "trials": T, "sweeps": cfg["sc"],
+            "l2": "no flush needed: per-step state (acc f64 "
+                  f"{8 * N * R * T / 2**20:.0f} MiB + spins) exceeds L2"
+                  if 8 * N * R * T > 126 * 2**20 else "state fits L2 (small config)"}
+
+
 # ---------------------------------------------------------------------------
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled DURING the timed region."""
@@ -230,6 +239,35 @@ def reference_sample(cfg, workers, target_s):
                 cpu=cpu_model(), seconds=wall)
 
 
+def reference_full_sc(cfg, workers, trials=16):
+    """the reference's run_trials on `trials` trials at the
+    config's FULL sweep count (p_s and TTS99 with the reference's own
+    formula, bench.cpp:414-430), one trial per host thread."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle_py
+    kind = "reference" if oracle_py.available("ref") else "port"
+    if kind != "reference" or cfg["kind"] != "gi":
+        return None
+    o = oracle_py.Oracle("ref")
+    R, sc, N = cfg["R"], cfg["sc"], n_spins(cfg)
+    w = max(1, min(workers, trials))
+    t0 = time.perf_counter()
+    outs, ps, t_mean, (tts_s, tts_kind) = o.run_trials(
+        oracle_py.params(R, 1), n_nodes=cfg["n_nodes"], trials=trials, ec=R * sc,
+        base_seed=BASE_SEED, workers=w, gi_seed=GI_SEED)
+    wall = time.perf_counter() - t0
+    hits = sum(1 for x in outs if x["reached_target"])
+    import math
+    amort = (wall / trials) * math.log(0.01) / math.log(1.0 - ps) if 0.0 < ps < 1.0 else None
+    return {"trials": trials, "sweeps": sc, "threads": w, "seconds": wall,
+            "value": float(N) * R * trials * sc / wall, "unit": UNIT, "p_s": ps, "hits": hits,
+            "t_mean_trial_s": t_mean,
+            "tts99_ref_formula_s": tts_s if tts_kind == 0 else None,
+            "tts99_amortised_s": amort,
+            "sample": f"reference run_trials: {trials} trials x {sc} sweeps (full budget) on "
+                      f"{w} threads, seeds {BASE_SEED}+t"}
+
+
 def run_reference_arm(args, cfg):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -243,6 +281,13 @@ def run_reference_arm(args, cfg):
             vals.append(s)
     v = statistics.median(x["value"] for x in vals)
     last = vals[-1]
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    full = None
+    if world == 1 and not args.no_full_sc:
+        try:
+            full = reference_full_sc(cfg, workers)
+        except Exception as e:  # reported, never fatal
+            full = {"error": str(e)}
     N = n_spins(cfg)
     ms = 1e3 * float(N) * cfg["R"] * cfg["T"] * cfg["sc"] / v
     line = {
@@ -250,12 +295,12 @@ def run_reference_arm(args, cfg):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (reference GI generator, instance seed 7)",
-        "config": {"workload": cfg["desc"], "n": N, "replicas": cfg["R"],
-                   "trials": cfg["T"], "sweeps": cfg["sc"]},
+        "config": config_of(cfg),
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": last["cores"], "kind": last["kind"],
                          "sample": last["sample"] + "; ms_per_step extrapolated to the full "
                          "workload", "cpu": last["cpu"]},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "full_sc_sample": full,
     }
     print(json.dumps(line), flush=True)
     return 0
@@ -406,6 +451,53 @@ def run_rows(args, cfg):
     return 0
 
 
+def time_dense_config(name, steps=2, warmup=1):
+    """Device-timed run of a dense BASELINE config (C4 / C5) for the extra keys
+    of the headline line: the problem is built on the device
+    (ssqa_problem_create_dense), all trials x all sweeps per step."""
+    import torch
+
+    import paper_2302_12454_b200 as sq
+    from paper_2302_12454_b200 import _lib
+    cfg = CONFIGS[name]
+    N, R, T, sc = cfg["n"], cfg["R"], cfg["T"], cfg["sc"]
+    prob = sq.Problem.generated_dense(N, cfg["dense_kind"], GI_SEED)
+    info = prob.info()
+    b = sq.Batch(prob, sq.SsqaParams(r=R, sc=sc), T, False, _lib.ENGINE_TCGEN05)
+    b.set_seeds([BASE_SEED + t for t in range(T)])
+    for _ in range(warmup):
+        b.launch(None, False)
+        b.elapsed_ms()
+    clocks = ClockSampler(0)
+    torch.cuda.synchronize()
+    clocks.start()
+    times = []
+    for _ in range(steps):
+        b.launch(None, False)
+        times.append(b.elapsed_ms())
+    clk = clocks.stop()
+    ms = statistics.mean(times)
+    _, bf16_peak, peak_kind = peaks()
+    op_bits = b.operand_bits
+    planes = 2 if (op_bits == 4 and info.get("fp4") == 2) else 1
+    tc_mult = 4.0 if op_bits == 4 else 2.0
+    ops = 2.0 * N * N * R * T * (sc + 1) * planes
+    i8 = 2.0 * N * N * R * T * (sc + 1)
+    out = {"workload": cfg["desc"], "ms_per_step": ms, "steps": steps, "warmup": warmup,
+           "value": float(N) * R * T * sc / (ms * 1e-3), "unit": UNIT,
+           "tensor": {"achieved_tops": ops / (ms * 1e-3) / 1e12,
+                      "peak_tops": tc_mult * bf16_peak,
+                      "frac": ops / (ms * 1e-3) / 1e12 / (tc_mult * bf16_peak),
+                      "operands": ("fp4 pair" if planes == 2 else "fp4") if op_bits == 4 else "int8"},
+           "int8_equiv": {"achieved_tops": i8 / (ms * 1e-3) / 1e12, "peak_tops": 2.0 * bf16_peak,
+                          "frac": i8 / (ms * 1e-3) / 1e12 / (2.0 * bf16_peak)},
+           "peak_note": f"{peak_kind} bf16 x {tc_mult:g} (operand format) / x 2 (int8)",
+           "clocks": clk, "gpu_launches": b.launch_count()}
+    b.close()
+    prob.close()
+    return out
+
+
 def run_ours(args, cfg):
     import numpy as np
     import torch
@@ -501,12 +593,9 @@ def run_ours(args, cfg):
         sweeps_per_launch = sc
         launch_bytes = alg_bytes_per_update * updates_per_sweep * sc
     tensor_tops = ops / (k_ms * 1e-3) / 1e12
+    # DRAM bytes need a profiler: not measured in this run (the ncu captures of
+    # this build are under profiles/, see profiles/README.md)
     traffic = None
-    tfile = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tfile):
-        t = json.load(open(tfile)).get(f"{args.config}:{eng_name}")
-        if t:
-            traffic = t["dram_bytes_per_sweep"] * sweeps_per_launch
     tensor = {"achieved": tensor_tops, "peak": tc_peak, "unit": "TOPS",
               "frac": tensor_tops / tc_peak, "operands": tc_name}
     # BASELINE.json's target is phrased against the int8 tensor roofline: the
@@ -562,7 +651,18 @@ def run_ours(args, cfg):
     p_s = hits / T
     t_trial = step_ms * 1e-3 / T * world  # device time per trial on one GPU
     tts = sq.compute_tts(p_s, t_trial) if cfg["kind"] == "gi" else None
+    # the reference's formula (bench.cpp:424-430) with t = a trial's own wall
+    # time: every trial of the batch runs for the whole batch
+    tts_ref = sq.compute_tts(p_s, step_ms * 1e-3) if cfg["kind"] == "gi" else None
 
+    others = None
+    if world == 1 and args.config == "c3" and not args.no_other_configs:
+        others = {}
+        for name in ("c4", "c5"):
+            try:
+                others[name] = time_dense_config(name)
+            except Exception as e:  # reported, never fatal to the headline number
+                others[name] = {"error": str(e)}
     if rank == 0:
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
@@ -578,12 +678,10 @@ def run_ours(args, cfg):
                       "int8 contraction (int32 acc)") + " + f64 update",
             "data": "synthetic (reference GI generator, instance seed 7; seeds 1000+t)"
                     if cfg["kind"] == "gi" else "synthetic (CounterRng stream 8/9, seed 7)",
-            "config": {"workload": cfg["desc"], "n": N, "n_pad": npad, "replicas": R,
-                       "trials": T, "sweeps": sc, "engine": eng_name,
-                       "parallelism": f"trial-sharded x{world}",
-                       "l2": "no flush needed: per-step state (acc f64 "
-                             f"{8 * N * R * T / 2**20:.0f} MiB + spins) exceeds L2"
-                             if 8 * N * R * T > 126 * 2**20 else "state fits L2 (small config)"},
+            "config": config_of(cfg),
+            "engine_config": {"n_pad": npad, "engine": eng_name,
+                              "parallelism": f"trial-sharded x{world}",
+                              "operands": tc_name},
             "roofline": roofline,
             "e2e": {"value": upd_per_step / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "seconds_per_step": e2e_s,
@@ -593,8 +691,13 @@ def run_ours(args, cfg):
             "tts": {"p_s": p_s, "hits": hits, "trials": T, "t_trial_s": t_trial,
                     "tts99_s": None if tts is None else
                     (tts.seconds if tts.kind == "finite" else tts.kind),
-                    "definition": "amortised: batch device time / trials per GPU"},
+                    "definition": "amortised: batch device time / trials per GPU",
+                    "tts99_ref_formula_s": None if tts_ref is None else
+                    (tts_ref.seconds if tts_ref.kind == "finite" else tts_ref.kind),
+                    "ref_formula": "bench.cpp:424-430 with t = per-trial wall = the batch's "
+                                   "device time (all trials run concurrently)"},
             "cpu_baseline": cpu,
+            "other_configs": others,
         }
         print(json.dumps(line), flush=True)
     b.close()
@@ -618,6 +721,10 @@ def main():
     ap.add_argument("--engine", default="auto", choices=["auto", "simt", "tcgen05"])
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-full-sc", action="store_true",
+                    help="reference arm: skip the 16-trial full-budget run (p_s, TTS99)")
+    ap.add_argument("--no-other-configs", action="store_true",
+                    help="skip the device-timed C4/C5 lines added to the C3 line")
     ap.add_argument("--shard", default="trials", choices=["trials", "rows"],
                     help="multi-GPU layout: trial blocks per GPU (default) or J' rows per GPU")
     ap.add_argument("--exchange", default="nccl", choices=["nccl", "p2p", "direct"],

@@ -105,7 +105,8 @@ int ssqa_pool_stats(int device, long long* cached_bytes, long long* in_use_bytes
  * h[n], J[n*n] (dense, mirrored, zero diagonal: IsingModel storage,
  * model.hpp:59-66) and offset are quantized once to int8 J' = J*2^p and
  * int32 H' = h*2^p with the smallest p >= 0 that makes both integral, then
- * uploaded to `device`.  Returns SSQA_EUNSUP if no such p keeps |J'| <= 127.
+ * uploaded to `device`.  |J'| <= 127 gives int8 couplings, up to 32639 int16
+ * ones (ssqa_problem_int16); SSQA_EUNSUP beyond that.
  * The device copy is shared by every batch created on the handle. */
 int ssqa_problem_create(int n, const double* h, const double* J, double offset, int device,
                         ssqa_problem* out);
@@ -119,6 +120,20 @@ int ssqa_problem_destroy(ssqa_problem prob);
 int ssqa_problem_create_many(int count, int n, const double* h, const double* J,
                              const double* offsets, int device, ssqa_problem* out);
 int ssqa_problem_count(ssqa_problem prob);
+/* Problems built on the device, with no host model (SURVEY.md 8.1 f2 and the
+ * BASELINE C4/C5 instances): the same quantized problem as
+ *   ssqa_problem_create(ssqa_dense_ising(n, kind, seed))          (dense), and
+ *   ssqa_problem_create_many(qubo_to_ising(build_gi_qubo(generate_gi(
+ *       n_nodes, edge_prob, seeds[t], permute, c1, c2))) for t < count)   (GI;
+ *   count == 1 gives a single-instance problem), gi.cpp:102-184 --
+ * the GI graph pairs are drawn on the host, J' is written on the device from
+ * their adjacency matrices (the penalty's closed form); dyadic c1, c2 only. */
+int ssqa_problem_create_dense(int n, int kind, uint64_t seed, int device, ssqa_problem* out);
+int ssqa_problem_create_gi(int count, int n_nodes, double edge_prob, const uint64_t* seeds,
+                           int permute, double c1, double c2, int device, ssqa_problem* out);
+/* Device image of a problem: J' int8 [count*npad][npad], H' int32 [count*npad],
+ * offsets [count] (any pointer may be NULL). */
+int ssqa_problem_export(ssqa_problem prob, int8_t* J, int32_t* H, double* offsets);
 /* Quantizer report: padded size, scale exponent p, max |J'|, max |H'|. */
 int ssqa_problem_info(ssqa_problem prob, int* n, int* n_pad, int* shift_p, int* max_abs_j,
                       int* max_abs_h);
@@ -127,6 +142,10 @@ int ssqa_problem_info(ssqa_problem prob, int* n, int* n_pad, int* shift_p, int* 
  * {0, +-1, +-2, +-3, +-4, +-6}); the tcgen05 engine then streams 4-bit
  * operands (tcgen05.mma kind::mxf4 with unit block scales). */
 int ssqa_problem_fp4(ssqa_problem prob);
+/* 1 when the couplings need int16 (127 < max |J'| <= 32639): J' is held as two
+ * int8 planes J' = 256 Ahi + Alo and the tcgen05 engine runs one int8 MMA per
+ * plane (replicas <= 128; the SIMT engine refuses such problems). */
+int ssqa_problem_int16(ssqa_problem prob);
 
 /* Host-only dry run of the quantizer (no device touched): the scale and
  * ranges ssqa_problem_create would use, or SSQA_EUNSUP with the reason. */

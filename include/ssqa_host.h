@@ -19,6 +19,13 @@ extern "C" {
 int ssqa_gi_ising(int n_nodes, double edge_prob, uint64_t seed, int permute, double c1,
                   double c2, double* h, double* J, double* offset);
 
+/* The host half of the device GI generator (ssqa_problem_create_gi): the
+ * graph pair of generate_gi as 0/1 adjacency bytes adj[2*n_nodes^2] (graph 1,
+ * then graph 2, 0-based) and the penalty's biases h[n_nodes^2] and offset in
+ * closed form -- equal to ssqa_gi_ising's for dyadic c1, c2. */
+int ssqa_gi_compact(int n_nodes, double edge_prob, uint64_t seed, int permute, double c1,
+                    double c2, uint8_t* adj, double* h, double* offset);
+
 /* BASELINE configs C4/C5, drawn from CounterRng
  * stream 8 (couplings) and 9 (biases) -- ids 1..7 are taken (rng.hpp:20-28).
  *   kind 0: J_ij = below(i*n+j, 16) - 8 for i<j, h_i = below(i, 16) - 8;

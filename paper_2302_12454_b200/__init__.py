@@ -7,7 +7,7 @@ package is the Python view of the same ABI.
 from .api import (  # noqa: F401
     AnnealResult, Batch, IsingModel, K_TARGET_TOL, Problem, ReplicaLattice, RunOptions,
     SsaParams, SsqaParams, TracePoint, TrialOutcome, TtsValue, compute_tts, dense_ising,
-    gi_ising, i0_schedule, init_lattice, ising_energy, jperp_schedule, pool_stats, pool_trim, replica_energies,
+    gi_compact, gi_ising, i0_schedule, init_lattice, ising_energy, jperp_schedule, pool_stats, pool_trim, replica_energies,
     run_trials, run_trials_fresh, ssa_run, ssa_run_batch, ssqa_run, ssqa_run_batch, ssqa_sweep,
     trial_instance_seeds, tune,
 )

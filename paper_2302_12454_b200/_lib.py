@@ -59,9 +59,16 @@ SIGNATURES = [
     ("ssqa_problem_create_many", C.c_int, [C.c_int, C.c_int, DP, DP, DP, C.c_int,
                                            C.POINTER(VP)]),
     ("ssqa_problem_count", C.c_int, [VP]),
+    ("ssqa_problem_create_dense", C.c_int, [C.c_int, C.c_int, C.c_uint64, C.c_int, C.c_void_p]),
+    ("ssqa_problem_create_gi", C.c_int, [C.c_int, C.c_int, C.c_double, C.c_void_p, C.c_int,
+                                         C.c_double, C.c_double, C.c_int, C.c_void_p]),
+    ("ssqa_problem_export", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    ("ssqa_gi_compact", C.c_int, [C.c_int, C.c_double, C.c_uint64, C.c_int, C.c_double,
+                                  C.c_double, C.c_void_p, C.c_void_p, C.c_void_p]),
     ("ssqa_problem_info", C.c_int, [VP, IP, IP, IP, IP, IP]),
     ("ssqa_quantize_info", C.c_int, [C.c_int, DP, DP, IP, IP, IP, IP]),
     ("ssqa_problem_fp4", C.c_int, [VP]),
+    ("ssqa_problem_int16", C.c_int, [C.c_void_p]),
     ("ssqa_params_validate", C.c_int, [C.POINTER(ParamsC), C.c_int]),
     ("ssqa_jperp_schedule", C.c_int, [C.c_long, C.POINTER(ParamsC), DP]),
     ("ssqa_run_batch", C.c_int, [VP, C.POINTER(ParamsC), U64P, C.c_int, C.c_int, C.c_double,

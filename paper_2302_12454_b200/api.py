@@ -167,6 +167,19 @@ def gi_ising(n_nodes: int, edge_prob: float = 0.5, seed: int = 0, permute: bool 
     return IsingModel.from_arrays(h, J, off.value)
 
 
+def gi_compact(n_nodes: int, edge_prob: float = 0.5, seed: int = 0, permute: bool = True,
+               c1: float = 0.75, c2: float = 0.75):
+    """Host half of the device GI generator: adjacency [2, n, n] (graph 1, graph
+    2) and the closed-form biases / offset (equal to gi_ising's for dyadic c)."""
+    N = n_nodes * n_nodes
+    adj = np.zeros((2, n_nodes, n_nodes), dtype=np.uint8)
+    h = np.zeros(N)
+    off = C.c_double()
+    check(lib().ssqa_gi_compact(n_nodes, edge_prob, seed, int(permute), c1, c2,
+                                adj.ctypes.data_as(C.c_void_p), _dp(h), C.byref(off)), host=True)
+    return adj, h, off.value
+
+
 def dense_ising(n: int, kind: int, seed: int) -> IsingModel:
     """BASELINE configs C4 (kind 0, int[-8,7]) / C5 (kind 1, SK +-1)."""
     h = np.zeros(n)
@@ -216,12 +229,52 @@ class Problem:
                                              C.byref(self._h)))
         return self
 
+    @classmethod
+    def generated_dense(cls, n: int, kind: int, seed: int, device: int = 0) -> "Problem":
+        """BASELINE C4 / C5 model built on the device (ssqa_problem_create_dense):
+        the same quantized problem as Problem(dense_ising(n, kind, seed))."""
+        self = cls.__new__(cls)
+        self.n = n
+        self._h = C.c_void_p()
+        check(lib().ssqa_problem_create_dense(n, kind, seed, device, C.byref(self._h)))
+        return self
+
+    @classmethod
+    def generated_gi(cls, n_nodes: int, seeds: Sequence[int], edge_prob: float = 0.5,
+                     permute: bool = True, c1: float = 0.75, c2: float = 0.75,
+                     device: int = 0) -> "Problem":
+        """GI instance(s) built on the device (ssqa_problem_create_gi): one per
+        seed, stacked like Problem.from_models([gi_ising(n_nodes, edge_prob, s,
+        permute, c1, c2) for s in seeds]) (a single seed: a one-instance problem)."""
+        self = cls.__new__(cls)
+        self.n = n_nodes * n_nodes
+        self._h = C.c_void_p()
+        sd = np.ascontiguousarray(np.asarray(seeds, dtype=np.uint64))
+        check(lib().ssqa_problem_create_gi(len(sd), n_nodes, edge_prob,
+                                           sd.ctypes.data_as(C.c_void_p), int(permute), c1, c2,
+                                           device, C.byref(self._h)))
+        return self
+
+    def export(self):
+        """(J' int8 [count*npad, npad], H' int32 [count*npad], offsets [count])."""
+        inf = self.info()
+        cnt = int(lib().ssqa_problem_count(self._h))
+        npad = inf["n_pad"]
+        J = np.zeros((cnt * npad, npad * (2 if inf["int16"] else 1)), dtype=np.int8)
+        H = np.zeros(cnt * npad, dtype=np.int32)
+        off = np.zeros(cnt)
+        check(lib().ssqa_problem_export(self._h, J.ctypes.data_as(C.c_void_p),
+                                        H.ctypes.data_as(C.c_void_p), _dp(off)))
+        return J, H, off
+
     def info(self) -> dict:
         v = [C.c_int() for _ in range(5)]
         check(lib().ssqa_problem_info(self._h, *[C.byref(x) for x in v]))
         d = dict(zip(("n", "n_pad", "shift_p", "max_abs_j", "max_abs_h"), [x.value for x in v]))
         # FP4 (e2m1) image uploaded when every coupling is 0, +-1, +-2, +-3, +-4 or +-6
         d["fp4"] = int(lib().ssqa_problem_fp4(self._h))
+        # int16 couplings held as two int8 planes (J' = 256 Ahi + Alo)
+        d["int16"] = int(lib().ssqa_problem_int16(self._h))
         return d
 
     def close(self):
@@ -580,6 +633,11 @@ def trial_instance_seeds(base_seed: int, trials: int) -> List[int]:
     return [_mix64((key + t * 0x9E3779B97F4A7C15) & ((1 << 64) - 1)) for t in range(trials)]
 
 
+@dataclass
+class _Shape:
+    n: int
+
+
 def run_trials_fresh(n_nodes: int, p, trials: int, ec: int, base_seed: int,
                      edge_prob: float = 0.5, permute: bool = False, c1: float = 0.75,
                      c2: float = 0.75, p_target: float = 0.99, device: int = 0):
@@ -588,17 +646,17 @@ def run_trials_fresh(n_nodes: int, p, trials: int, ec: int, base_seed: int,
     CounterRng(base_seed, kStreamTrialInstance).raw(t), target 0, the whole
     battery as one multi-instance device batch."""
     seeds = [base_seed + t for t in range(trials)]
-    models = [gi_ising(n_nodes, edge_prob, s, permute, c1, c2)
-              for s in trial_instance_seeds(base_seed, trials)]
-    prob = Problem.from_models(models, device)
+    # every trial's instance built on the device (no host model per trial)
+    prob = Problem.generated_gi(n_nodes, trial_instance_seeds(base_seed, trials), edge_prob,
+                                permute, c1, c2, device)
+    shape = _Shape(n_nodes * n_nodes)  # the size is all the batch call needs
     try:
         if isinstance(p, SsaParams):
             q = SsaParams(**{**p.__dict__, "sc": ec})
-            res = ssa_run_batch(models[0], q, seeds, 0.0, RunOptions(False, False), problem=prob)
+            res = ssa_run_batch(shape, q, seeds, 0.0, RunOptions(False, False), problem=prob)
         else:
             q = SsqaParams(**{**p.__dict__, "sc": ec // p.r})
-            res = ssqa_run_batch(models[0], q, seeds, 0.0, RunOptions(False, False),
-                                 problem=prob)
+            res = ssqa_run_batch(shape, q, seeds, 0.0, RunOptions(False, False), problem=prob)
     finally:
         prob.close()
     outs = [TrialOutcome(s, r.reached_target, r.first_hit_cycle, r.best_energy, r.wall_seconds)

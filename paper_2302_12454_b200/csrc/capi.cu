@@ -9,11 +9,15 @@
 #include <cstdlib>
 #include <cstring>
 #include <limits>
+#include <stdexcept>
 #include <string>
 #include <vector>
 
 #include "engine.h"
 #include "quantize_kernels.cuh"
+#include "generate_kernels.cuh"
+#include "ssqa/gi.hpp"
+#include "ssqa/rng.hpp"
 #include "simt_kernels.cuh"
 #include "sweep_tc.h"
 #include "../../include/ssqa_tune.h"
@@ -128,13 +132,15 @@ int num_sms(int device) {
 // row tiles, widen the tiles (more trials per tile -> each J' row tile is
 // streamed by fewer CTAs, larger MMA N) and split each tile's rows over rs
 // CTAs (row split, one CTA per SM).  fp4: FP4 operands need tile_cols <= 240.
-Geom make_geom(int n, int npad, int R, int T, int sms, int engine, bool fp4, bool per_trial) {
+Geom make_geom(int n, int npad, int R, int T, int sms, int engine, bool fp4, bool per_trial,
+               bool i16 = false) {
   Geom g;
   g.n = n;
   g.npad = npad;
   g.R = R;
   g.T = T;
-  const int max_cols = 256;
+  // int16 planes: two accumulators per buffer, 4 x tile columns of TMEM
+  const int max_cols = i16 ? 128 : 256;
   int tpt = std::max(1, (T + sms - 1) / sms);
   if (R <= max_cols) tpt = std::min(tpt, max_cols / R);
   else tpt = 1;
@@ -146,7 +152,7 @@ Geom make_geom(int n, int npad, int R, int T, int sms, int engine, bool fp4, boo
     // FP4 tiles <= 240 columns (scale-factor TMEM columns); int8 tiles <= 192:
     // smaller operand stages leave room for a deeper TMA pipeline (C4 measured:
     // 0.76 ms/sweep at 192 columns vs 0.84 at 256)
-    const int cap = fp4 ? 240 : 192;
+    const int cap = i16 ? 128 : (fp4 ? 240 : 192);
     int wide = std::max(1, std::min(T, cap / R));
     if (tune().wide > 0) wide = std::max(1, std::min(wide, tune().wide));
     const int wtiles = (T + wide - 1) / wide;
@@ -260,6 +266,44 @@ int init_state(ssqa_batch_s* b) {
   return SSQA_OK;
 }
 
+// FP4 / FP4-pair images of a device-built J' (every instance of the problem),
+// with the rules of ssqa_problem_create: the e2m1 image when every coupling
+// is representable, otherwise the pair image when every |J'| splits.
+cudaError_t build_images(ssqa_problem_s* pr, int* d_stats) {
+  Quantized& q = pr->q;
+  const size_t np2 = size_t(q.npad) * q.npad, cnt = size_t(pr->count);
+  int flag = 0;
+  cudaError_t e = cudaSuccess;
+  q.fp4_ok = q.max_abs_j <= 6 && q.max_abs_j != 5;
+  if (q.fp4_ok) {
+    e = cudaMemsetAsync(d_stats, 0, sizeof(int), pr->stream);
+    if (e == cudaSuccess) e = pmalloc(&pr->d_J4, cnt * np2 / 2);
+    if (e == cudaSuccess) launch_qfp4(pr->d_J, cnt * np2, pr->d_J4, d_stats, pr->stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&flag, d_stats, sizeof(int), cudaMemcpyDeviceToHost, pr->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(pr->stream);
+    if (e == cudaSuccess && flag) {
+      q.fp4_ok = false;
+      pool_free(pr->d_J4);
+      pr->d_J4 = nullptr;
+    }
+  }
+  if (e == cudaSuccess && !q.fp4_ok && fp4x2_splittable(q.max_abs_j)) {
+    flag = 0;
+    e = cudaMemsetAsync(d_stats, 0, sizeof(int), pr->stream);
+    if (e == cudaSuccess) e = pmalloc(&pr->d_J4, cnt * np2);
+    for (size_t c = 0; c < cnt && e == cudaSuccess; ++c)
+      launch_qfp4x2(pr->d_J + c * np2, q.npad, pr->d_J4 + c * np2, d_stats, pr->stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&flag, d_stats, sizeof(int), cudaMemcpyDeviceToHost, pr->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(pr->stream);
+    q.fp4x2_ok = e == cudaSuccess && !flag;
+    if (!q.fp4x2_ok && pr->d_J4) {
+      pool_free(pr->d_J4);
+      pr->d_J4 = nullptr;
+    }
+  }
+  return e;
+}
+
 }  // namespace
 
 extern "C" {
@@ -361,8 +405,31 @@ int ssqa_problem_create(int n, const double* h, const double* J, double offset, 
                         pr->stream);
       e = cudaMemcpyAsync(st, d_stats, sizeof(st), cudaMemcpyDeviceToHost, pr->stream);
       if (e == cudaSuccess) e = cudaStreamSynchronize(pr->stream);
+      if (e == cudaSuccess && st[2] && tune().i16 != 0) {
+        // |J'| > 127: int16 couplings as two int8 planes (engine.h Quantized::i16)
+        int16_t* d_J16 = nullptr;
+        st[1] = st[2] = 0;
+        e = cudaMemcpyAsync(d_stats + 1, st + 1, 2 * sizeof(int), cudaMemcpyHostToDevice, pr->stream);
+        if (e == cudaSuccess) e = pmalloc(&d_J16, np2 * sizeof(int16_t));
+        if (e == cudaSuccess) {
+          launch_qtranspose16(d_Jd, n, q.npad, std::ldexp(1.0, p), d_J16, d_stats + 1,
+                              d_stats + 2, pr->stream);
+          e = cudaMemcpyAsync(st, d_stats, sizeof(st), cudaMemcpyDeviceToHost, pr->stream);
+        }
+        if (e == cudaSuccess) e = cudaStreamSynchronize(pr->stream);
+        if (e == cudaSuccess && !st[2]) {
+          pool_free(pr->d_J);
+          pr->d_J = nullptr;
+          e = pmalloc(&pr->d_J, 2 * np2);
+          if (e == cudaSuccess) launch_qplanes16(d_J16, q.npad, reinterpret_cast<uint8_t*>(pr->d_J), pr->stream);
+          if (e == cudaSuccess) e = cudaStreamSynchronize(pr->stream);
+          q.i16 = true;
+        }
+        if (d_J16) pool_free(d_J16);
+      }
       if (e == cudaSuccess && st[2])
-        fail = "coupling magnitude exceeds int8 at scale 2^" + std::to_string(p);
+        fail = std::string("coupling magnitude exceeds ") +
+               (tune().i16 != 0 ? "int16 (32639)" : "int8") + " at scale 2^" + std::to_string(p);
     }
   }
   if (e == cudaSuccess && fail.empty()) {
@@ -385,7 +452,7 @@ int ssqa_problem_create(int n, const double* h, const double* J, double offset, 
         e = cudaMemcpyAsync(pr->d_H, H.data(), H.size() * sizeof(int32_t),
                             cudaMemcpyHostToDevice, pr->stream);
       // FP4 (e2m1) image when every coupling is 0, +-1, +-2, +-3, +-4 or +-6
-      q.fp4_ok = q.max_abs_j <= 6 && q.max_abs_j != 5;
+      q.fp4_ok = !q.i16 && q.max_abs_j <= 6 && q.max_abs_j != 5;
       if (e == cudaSuccess && q.fp4_ok) {
         e = pmalloc(&pr->d_J4, np2 / 2);
         if (e == cudaSuccess) {
@@ -400,7 +467,7 @@ int ssqa_problem_create(int n, const double* h, const double* J, double offset, 
         }
       }
       // otherwise the FP4 pair image J' = A1 + A2 (|J'| <= 12, != 11)
-      if (e == cudaSuccess && !q.fp4_ok && fp4x2_splittable(q.max_abs_j)) {
+      if (e == cudaSuccess && !q.i16 && !q.fp4_ok && fp4x2_splittable(q.max_abs_j)) {
         st[3] = 0;
         e = cudaMemcpyAsync(d_stats + 3, st + 3, sizeof(int), cudaMemcpyHostToDevice, pr->stream);
         if (e == cudaSuccess) e = pmalloc(&pr->d_J4, np2);
@@ -434,6 +501,8 @@ int ssqa_problem_create(int n, const double* h, const double* J, double offset, 
 int ssqa_problem_fp4(ssqa_problem pr) {
   return !pr ? 0 : pr->q.fp4_ok ? 1 : pr->q.fp4x2_ok ? 2 : 0;
 }
+
+int ssqa_problem_int16(ssqa_problem pr) { return pr && pr->q.i16 ? 1 : 0; }
 
 int ssqa_problem_create_many(int count, int n, const double* h, const double* J,
                              const double* offsets, int device, ssqa_problem* out) {
@@ -523,6 +592,171 @@ int ssqa_problem_create_many(int count, int n, const double* h, const double* J,
   return SSQA_OK;
 }
 
+// ---- problems built on the device (generate_kernels.cu) -------------------
+int ssqa_problem_create_dense(int n, int kind, uint64_t seed, int device, ssqa_problem* out) {
+  if (!out) return set_err(SSQA_EINVAL, "null argument");
+  if (n < 1 || n >= kMaxSpins) return set_err(SSQA_EINVAL, "spin count out of range");
+  if (kind != 0 && kind != 1) return set_err(SSQA_EINVAL, "kind must be 0 or 1");
+  auto* pr = new ssqa_problem_s();
+  Quantized& q = pr->q;
+  q.n = n;
+  q.npad = (n + 127) / 128 * 128;
+  q.p = 0;  // integer couplings and biases
+  q.scale = 1.0;
+  q.offset = 0.0;
+  pr->device = device;
+  int* d_stats = nullptr;
+  int st[2] = {0, 0};
+  const size_t np2 = size_t(q.npad) * q.npad;
+  cudaError_t e = cudaSetDevice(device);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&pr->stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = pmalloc(&d_stats, 4 * sizeof(int));
+  if (e == cudaSuccess) e = pmalloc(&pr->d_J, np2);
+  if (e == cudaSuccess) e = pmalloc(&pr->d_H, size_t(q.npad) * sizeof(int32_t));
+  if (e == cudaSuccess) e = cudaMemsetAsync(d_stats, 0, 4 * sizeof(int), pr->stream);
+  if (e == cudaSuccess) {
+    // CounterRng(seed, 8 / 9).key() (host/instances.cpp: the host builder's streams)
+    const uint64_t kj = ssqa::CounterRng(seed, 8).key(), kh = ssqa::CounterRng(seed, 9).key();
+    launch_gen_dense(n, q.npad, kind, kj, kh, pr->d_J, pr->d_H, d_stats, d_stats + 1, pr->stream);
+    e = cudaMemcpyAsync(st, d_stats, sizeof(st), cudaMemcpyDeviceToHost, pr->stream);
+  }
+  if (e == cudaSuccess) e = cudaStreamSynchronize(pr->stream);
+  if (e == cudaSuccess) {
+    q.max_abs_j = st[0];
+    q.max_abs_h = st[1];
+    e = build_images(pr, d_stats + 2);
+  }
+  if (d_stats) pool_free(d_stats);
+  if (e != cudaSuccess) {
+    ssqa_problem_destroy(pr);
+    return set_err(SSQA_ECUDA, std::string("problem generation: ") + cudaGetErrorString(e));
+  }
+  *out = pr;
+  return SSQA_OK;
+}
+
+int ssqa_problem_create_gi(int count, int n_nodes, double edge_prob, const uint64_t* seeds,
+                           int permute, double c1, double c2, int device, ssqa_problem* out) {
+  if (!out || !seeds) return set_err(SSQA_EINVAL, "null argument");
+  if (count < 1) return set_err(SSQA_EINVAL, "count must be >= 1");
+  if (n_nodes < 1 || size_t(n_nodes) * n_nodes >= size_t(kMaxSpins))
+    return set_err(SSQA_EINVAL, "n_nodes out of range");
+  const int nn = n_nodes, N = nn * nn;
+  std::vector<uint8_t> adj(size_t(count) * 2 * nn * nn);
+  std::vector<double> h(size_t(N));
+  std::vector<double> offsets(static_cast<size_t>(count));
+  auto* pr = new ssqa_problem_s();
+  Quantized& q = pr->q;
+  q.n = N;
+  q.npad = (N + 127) / 128 * 128;
+  pr->count = count;
+  pr->device = device;
+  std::vector<int32_t> H(size_t(count) * q.npad, 0);
+  std::string fail;
+  int p = 0, jo = 0, jm = 0;
+  try {
+    // couplings -2 c1 / 4 (one-hot) and -c2 / 4 (edge mismatch)
+    const double jo_d = -0.25 * (2.0 * c1), jm_d = -0.25 * c2;
+    const int e1 = dyadic_exponent_of(jo_d), e2 = dyadic_exponent_of(jm_d);
+    if (e1 < 0 || e2 < 0) throw std::invalid_argument("GI penalties must be dyadic rationals");
+    std::vector<std::vector<double>> hs(static_cast<size_t>(count));
+    for (int c = 0; c < count; ++c) {
+      hs[size_t(c)].resize(size_t(N));
+      ssqa::gi_compact(ssqa::generate_gi(nn, edge_prob, seeds[c], permute != 0, c1, c2),
+                       adj.data() + size_t(c) * 2 * nn * nn, hs[size_t(c)].data(),
+                       &offsets[size_t(c)]);
+    }
+    // the scale the quantizer would find: every coupling value present and
+    // every bias.  One-hot couplings exist from n = 2; edge-mismatch ones in
+    // an instance with 0 < |E| < n(n-1)/2 edges.
+    p = nn >= 2 ? e1 : 0;
+    for (int c = 0; c < count; ++c) {
+      long m2 = 0;  // 2 |E1|
+      for (int x = 0; x < nn * nn; ++x) m2 += adj[size_t(c) * 2 * nn * nn + size_t(x)];
+      if (m2 > 0 && m2 < long(nn) * (nn - 1)) p = std::max(p, e2);
+    }
+    for (auto& hv : hs)
+      for (double v : hv) {
+        const int e = dyadic_exponent_of(v);
+        if (e < 0) throw std::invalid_argument("bias is not a dyadic rational");
+        p = std::max(p, e);
+      }
+    jo = int(std::ldexp(jo_d, p));
+    jm = int(std::ldexp(jm_d, p));
+    if (std::abs(jo) > 127 || std::abs(jm) > 127)
+      throw std::invalid_argument("coupling magnitude exceeds int8 at scale 2^" + std::to_string(p));
+    for (int c = 0; c < count; ++c)
+      for (int i = 0; i < N; ++i) {
+        const double x = std::ldexp(hs[size_t(c)][size_t(i)], p);
+        if (std::fabs(x) >= double(1 << 29))
+          throw std::invalid_argument("bias magnitude exceeds the int32 field range");
+        H[size_t(c) * q.npad + size_t(i)] = int32_t(x);
+        q.max_abs_h = std::max(q.max_abs_h, std::abs(int32_t(x)));
+      }
+  } catch (const std::exception& ex) {
+    fail = ex.what();
+  }
+  if (!fail.empty()) {
+    delete pr;
+    return set_err(SSQA_EUNSUP, fail);
+  }
+  q.p = p;
+  q.scale = std::ldexp(1.0, -p);
+  q.offset = offsets[0];
+  pr->offsets = offsets;
+  const size_t np2 = size_t(q.npad) * q.npad;
+  uint8_t* d_adj = nullptr;
+  int* d_stats = nullptr;
+  int mj = 0;
+  cudaError_t e = cudaSetDevice(device);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&pr->stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = pmalloc(&d_stats, 4 * sizeof(int));
+  if (e == cudaSuccess) e = pmalloc(&d_adj, adj.size());
+  if (e == cudaSuccess) e = pmalloc(&pr->d_J, size_t(count) * np2);
+  if (e == cudaSuccess) e = pmalloc(&pr->d_H, H.size() * sizeof(int32_t));
+  if (e == cudaSuccess) e = pmalloc(&pr->d_offsets, size_t(count) * sizeof(double));
+  if (e == cudaSuccess) e = cudaMemsetAsync(d_stats, 0, 4 * sizeof(int), pr->stream);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(d_adj, adj.data(), adj.size(), cudaMemcpyHostToDevice, pr->stream);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(pr->d_H, H.data(), H.size() * sizeof(int32_t), cudaMemcpyHostToDevice,
+                        pr->stream);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(pr->d_offsets, offsets.data(), size_t(count) * sizeof(double),
+                        cudaMemcpyHostToDevice, pr->stream);
+  if (e == cudaSuccess) {
+    launch_gen_gi(count, nn, q.npad, jo, jm, d_adj, pr->d_J, d_stats, pr->stream);
+    e = cudaMemcpyAsync(&mj, d_stats, sizeof(int), cudaMemcpyDeviceToHost, pr->stream);
+  }
+  if (e == cudaSuccess) e = cudaStreamSynchronize(pr->stream);
+  if (e == cudaSuccess) {
+    q.max_abs_j = mj;
+    e = build_images(pr, d_stats + 2);
+  }
+  if (d_adj) pool_free(d_adj);
+  if (d_stats) pool_free(d_stats);
+  if (e != cudaSuccess) {
+    ssqa_problem_destroy(pr);
+    return set_err(SSQA_ECUDA, std::string("problem generation: ") + cudaGetErrorString(e));
+  }
+  *out = pr;
+  return SSQA_OK;
+}
+
+int ssqa_problem_export(ssqa_problem pr, int8_t* J, int32_t* H, double* offsets) {
+  if (!pr) return set_err(SSQA_EINVAL, "null problem");
+  CU(cudaSetDevice(pr->device));
+  CU(cudaStreamSynchronize(pr->stream));
+  const size_t np = size_t(pr->q.npad), cnt = size_t(pr->count);
+  if (J) CU(cudaMemcpy(J, pr->d_J, cnt * np * np * (pr->q.i16 ? 2 : 1), cudaMemcpyDeviceToHost));
+  if (H) CU(cudaMemcpy(H, pr->d_H, cnt * np * sizeof(int32_t), cudaMemcpyDeviceToHost));
+  if (offsets) {
+    if (pr->count > 1) std::copy(pr->offsets.begin(), pr->offsets.end(), offsets);
+    else offsets[0] = pr->q.offset;
+  }
+  return SSQA_OK;
+}
+
 int ssqa_problem_count(ssqa_problem pr) { return pr ? pr->count : 0; }
 
 int ssqa_quantize_info(int n, const double* h, const double* J, int* n_pad, int* shift_p,
@@ -583,10 +817,13 @@ int create_batch(ssqa_problem pr, const ssqa_params_c* p, int trials, int record
   }
   CU(cudaSetDevice(pr->device));
   int eng = engine;
-  if (eng == SSQA_ENGINE_AUTO) eng = tc_supported(pr->q.npad, p->r, p->delay) ? SSQA_ENGINE_TCGEN05
-                                                                    : SSQA_ENGINE_SIMT;
-  if (eng == SSQA_ENGINE_TCGEN05 && !tc_supported(pr->q.npad, p->r, p->delay))
+  // int16 couplings: tcgen05 only, tiles of <= 128 replica columns
+  const bool tc_ok = tc_supported(pr->q.npad, p->r, p->delay) && (!pr->q.i16 || p->r <= 128);
+  if (eng == SSQA_ENGINE_AUTO) eng = tc_ok ? SSQA_ENGINE_TCGEN05 : SSQA_ENGINE_SIMT;
+  if (eng == SSQA_ENGINE_TCGEN05 && !tc_ok)
     return set_err(SSQA_EUNSUP, "tcgen05 engine does not support this shape");
+  if (pr->q.i16 && eng != SSQA_ENGINE_TCGEN05)
+    return set_err(SSQA_EUNSUP, "int16 couplings need the tcgen05 engine (replicas <= 128)");
   if (pr->count > 1 && eng != SSQA_ENGINE_TCGEN05)
     return set_err(SSQA_EUNSUP, "multi-instance problems need the tcgen05 engine");
   if (eng != SSQA_ENGINE_SIMT && eng != SSQA_ENGINE_TCGEN05)
@@ -606,7 +843,7 @@ int create_batch(ssqa_problem pr, const ssqa_params_c* p, int trials, int record
   b->nslots = p->delay + 3;
   const bool any_fp4 = pr->q.fp4_ok || pr->q.fp4x2_ok;
   b->g = make_geom(pr->q.n, pr->q.npad, p->r, trials, num_sms(pr->device), eng, any_fp4,
-                   pr->count > 1);
+                   pr->count > 1, pr->q.i16);
   b->slot_elems = size_t(b->g.ccols) * b->g.npad;
   b->phys.assign(size_t(b->d) + 1, 0);
   const int T = trials;

@@ -67,6 +67,12 @@ struct Quantized {
   // couplings a row holds 64 bytes of A1 nibbles, then 64 bytes of A2
   // nibbles, so one 128-byte TMA row feeds both MMAs of the chunk.
   bool fp4x2_ok = false;
+  // int16 couplings (127 < max |J'| <= kI16Max): J' = 256 Ahi + Alo with two
+  // signed int8 planes; the device image (d_J) holds, per 64-coupling K chunk
+  // of a row, 64 bytes of Alo then 64 bytes of Ahi (rows of 2 npad bytes),
+  // and the tcgen05 engine runs one kind::i8 MMA per plane into two
+  // accumulators, S = D_lo + 256 D_hi.
+  bool i16 = false;
   std::vector<uint8_t> J4;           // [npad * npad/2] (fp4_ok) or [npad * npad] (fp4x2_ok)
 };
 
@@ -75,6 +81,8 @@ struct Quantized {
 constexpr int kFp4x2A[13] = {0, 2, 4, 5, 6, 6, 7, 7, 7, 7, 7, -1, 7};
 constexpr int kFp4x2B[13] = {0, 0, 0, 0, 0, 2, 0, 2, 4, 5, 6, -1, 7};
 inline bool fp4x2_splittable(int max_abs) { return max_abs <= 12 && max_abs != 11; }
+// int16 planes: Alo = the signed low byte, Ahi = (J' - Alo) / 256 in [-128, 127].
+constexpr int kI16Max = 127 * 256 + 127;  // 32639
 // Byte offsets of coupling j's A1 / A2 nibbles inside a pair-image row, and
 // the nibble shift.
 inline size_t fp4x2_byte_a(int j) { return size_t(j >> 7) * 128 + size_t((j & 127) >> 1); }

@@ -123,7 +123,68 @@ __global__ void k_qfp4x2(const int8_t* __restrict__ Jq, int npad, uint8_t* __res
   }
 }
 
+// int16 variant of k_qtranspose: J16[i][j] = J[j][i] * up; overflow <- 1 if
+// any |J * up| > kI16Max (int16 planes, engine.h Quantized::i16).
+__global__ void k_qtranspose16(const double* __restrict__ J, int n, int npad, double up,
+                               int16_t* __restrict__ Jq, int* __restrict__ maxabs,
+                               int* __restrict__ overflow) {
+  __shared__ int16_t tile[32][33];
+  const int i0 = blockIdx.x * 32, j0 = blockIdx.y * 32;
+  int local = 0, bad = 0;
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int j = j0 + r, i = i0 + threadIdx.x;
+    int v = 0;
+    if (j < n && i < n) {
+      const double x = J[size_t(j) * n + i] * up;  // exact: a power-of-two scale
+      if (fabs(x) > 32639.0) bad = 1;
+      else v = int(x);
+    }
+    tile[r][threadIdx.x] = int16_t(v);
+    local = max(local, abs(v));
+  }
+  __syncthreads();
+  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+    const int i = i0 + r, j = j0 + threadIdx.x;
+    if (i < npad && j < npad) Jq[size_t(i) * npad + j] = tile[threadIdx.x][r];
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    local = max(local, __shfl_xor_sync(0xffffffffu, local, o));
+    bad |= __shfl_xor_sync(0xffffffffu, bad, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (local > 0) atomicMax(maxabs, local);
+    if (bad) atomicOr(overflow, 1);
+  }
+}
+
+// Plane image of int16 J': row i, K chunk kc (64 couplings) -> 64 bytes of
+// Alo then 64 bytes of Ahi at byte kc * 128 of a 2 npad-byte row.
+__global__ void k_qplanes16(const int16_t* __restrict__ Jq, int npad, uint8_t* __restrict__ out) {
+  const size_t total = size_t(npad) * npad;
+  for (size_t x = blockIdx.x * size_t(blockDim.x) + threadIdx.x; x < total;
+       x += size_t(gridDim.x) * blockDim.x) {
+    const size_t i = x / size_t(npad);
+    const int j = int(x % size_t(npad));
+    const int v = Jq[x];
+    const int lo = int(int8_t(uint8_t(v & 0xff)));
+    const int hi = (v - lo) / 256;
+    const size_t o = i * size_t(2 * npad) + size_t(j >> 6) * 128 + size_t(j & 63);
+    out[o] = uint8_t(int8_t(lo));
+    out[o + 64] = uint8_t(int8_t(hi));
+  }
+}
+
 }  // namespace
+
+void launch_qtranspose16(const double* J, int n, int npad, double up, int16_t* Jq, int* maxabs,
+                         int* overflow, cudaStream_t st) {
+  dim3 grid(npad / 32, npad / 32), block(32, 8);
+  k_qtranspose16<<<grid, block, 0, st>>>(J, n, npad, up, Jq, maxabs, overflow);
+}
+
+void launch_qplanes16(const int16_t* Jq, int npad, uint8_t* out, cudaStream_t st) {
+  k_qplanes16<<<1184, 256, 0, st>>>(Jq, npad, out);
+}
 
 void launch_qfp4x2(const int8_t* Jq, int npad, uint8_t* J4, int* not_split, cudaStream_t st) {
   k_qfp4x2<<<1184, 256, 0, st>>>(Jq, npad, J4, not_split);

@@ -23,4 +23,11 @@ void launch_qfp4(const int8_t* Jq, size_t elems, uint8_t* J4, int* not_fp4, cuda
 // not_split <- 1 if some |Jq| has no split (the image is then unusable).
 void launch_qfp4x2(const int8_t* Jq, int npad, uint8_t* J4, int* not_split, cudaStream_t st);
 
+// int16 couplings (127 < max |J'| <= 32639): Jq int16 [npad][npad] (transposed,
+// scaled), overflow <- 1 beyond 32639; then the two-plane image (engine.h
+// Quantized::i16), rows of 2 npad bytes.
+void launch_qtranspose16(const double* J, int n, int npad, double up, int16_t* Jq, int* maxabs,
+                         int* overflow, cudaStream_t st);
+void launch_qplanes16(const int16_t* Jq, int npad, uint8_t* out, cudaStream_t st);
+
 }  // namespace ssqa_engine

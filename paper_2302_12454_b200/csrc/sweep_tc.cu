@@ -111,6 +111,7 @@ struct TcParams {
   int ring_phys[kMaxDelay + 1];
   int stages, nslot;
   int pair;  // FP4 pair operands (Quantized::fp4x2_ok): J' = A1 + A2, spins in SWIZZLE_64B stages
+  int i16;   // int16 couplings (Quantized::i16): J' = 256 Ahi + Alo, int8 MMAs into two accumulators
   // Table epilogue (fast mode, tab_w > 0; see TabConsts): integer fields
   // X >= tab_hi / X < tab_lo1 clamp without FP64, the others read
   // fl(fl(X 2^-p + jperp u) [+ jperp d]) from a per-cycle smem table of tab_w
@@ -162,7 +163,7 @@ __host__ __device__ inline int tab_bytes_of(const TcParams& P) {
 // neighbour-sign bytes (128 per plane, a second plane when bidirectional).
 __host__ __device__ inline int sig_tile_row(const TcParams& P, bool f4) {
   // (plus half a TMA tile per buffer: one staging tile for the copier warp)
-  if (P.fast && P.g.rs == 1 && ((P.use_tab == 0 && P.rails_lo) || P.use_tab == 2))
+  if (P.fast && P.g.rs == 1 && !P.i16 && ((P.use_tab == 0 && P.rails_lo) || P.use_tab == 2))
     return 128 * (P.bidirectional ? 2 : 1) + (f4 ? 32 : 64);
   return f4 ? 64 : 128;
 }
@@ -794,6 +795,7 @@ struct EpiRow {
   uint32_t nib_live;        // FP4 word stores: nibble mask of the live rows of that word
   int npeer;                // fused shard exchange: peers that get every spin word too
   const long long* peer_delta;  // TcParams::peer_delta
+  uint32_t hi_off;          // int16 couplings: TMEM column offset of D_hi (0: none)
   // issue-lean FP64 epilogue (noise_top5 / noise_lut / update_fast3)
   uint32_t i_u32;           // global spin row i
   uint32_t p4, p32;         // 4 and 32 in registers (noise_top5)
@@ -878,6 +880,13 @@ __device__ __forceinline__ void epi_chunks(const EpiRow& er, const UpdateConsts&
       for (int j = 0; j < kCW; ++j) v[j] = int(trow) + cb + j;
     } else {
       tmem_ld8(trow + uint32_t(cb), v);
+      if (er.hi_off) {
+        // int16 couplings: S = D_lo + 256 D_hi
+        int32_t vh[kCW];
+        tmem_ld8(trow + er.hi_off + uint32_t(cb), vh);
+#pragma unroll
+        for (int j = 0; j < kCW; ++j) v[j] += vh[j] * 256;
+      }
     }
     if (!(SSQA_ABL & 128)) mbar_wait(&ctl->afull[slot], ph);
     if (++sidx == nps) {
@@ -1595,7 +1604,11 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
   // FP4 pairs: a stage is K = 128 couplings -- one 128-byte J'' row holding
   // 64 bytes of A1 and 64 bytes of A2 nibbles -- against 64 bytes of spins
   const bool pair = F4 && P.pair != 0;
-  const int b_row = pair ? kBK / 2 : kBK;
+  // int16 planes (Quantized::i16): a stage is K = 64 couplings -- one 128-byte
+  // row of 64 Alo bytes then 64 Ahi bytes -- against 64 spin bytes; the MMAs of
+  // the two planes accumulate into D_lo (columns [buf NT]) and D_hi ([2 NT + buf NT])
+  const bool i16 = !F4 && P.i16 != 0;
+  const int b_row = (pair || i16) ? kBK / 2 : kBK;
   const Layout L = make_layout(NT, g.tpt, P.stages, P.nslot, sig_tile_row(P, F4), b_row,
                                CTA2 ? NT / 2 : NT, tab_bytes_of(P));
   const int stages = L.stages, nslot = L.nslot;
@@ -1649,7 +1662,8 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
                        : rt_base + int((long long)rt_span * (part + 1) / RS) - rt_lo;  // this CTA's
   // one stage = 128 bytes of K per row: 128 int8 or 256 e2m1 couplings/spins
   // (an FP4 row of npad = 128 is a partial chunk: TMA zero-fills the rest)
-  const int NKC = (F4 && !pair) ? (g.npad + 2 * kBK - 1) / (2 * kBK) : g.npad / kBK;
+  const int NKC = (F4 && !pair) ? (g.npad + 2 * kBK - 1) / (2 * kBK)
+                                : (i16 ? g.npad / (kBK / 2) : g.npad / kBK);
   // multi-instance problems: this tile's trial anneals its own J', H', offset
   const int j_row0 = P.multi ? tile * g.npad : 0;
   const int nchunk = NT / kCW;
@@ -1661,14 +1675,14 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
   const int rgroup = (NRT + kMaxRowGroups - 1) / kMaxRowGroups;
   const int nrg = (NRT + rgroup - 1) / rgroup;
   // spin rows covered by one K chunk of the operand stream
-  const int kKRows = (F4 && !pair) ? 2 * kBK : kBK;
+  const int kKRows = (F4 && !pair) ? 2 * kBK : (i16 ? kBK / 2 : kBK);
   // clamped-table epilogue (use_tab 2, never with a row split): neighbour-sign
   // tiles built by the copier warp, energy partials kept in TMEM columns
   // [2 NT, 3 NT) across the row tiles when they fit below the scale factors
   // Fast epilogues without a row split take their neighbour signs from a
   // permuted sign tile built by the copier warp (nbt_mode): the clamped table
   // (use_tab 2, ct_mode) and the issue-lean FP64 epilogue (use_tab 0, epi_v4).
-  const bool nbt_mode = P.fast && !split && ((P.use_tab == 0 && P.rails_lo) || P.use_tab == 2);
+  const bool nbt_mode = P.fast && !split && !P.i16 && ((P.use_tab == 0 && P.rails_lo) || P.use_tab == 2);
   const bool ct_mode = nbt_mode && P.use_tab == 2;
   const uint32_t ct_tile_bytes = uint32_t(NT) * kCtTileRow * (P.bidirectional ? 2u : 1u);
   const bool e_tmem = nbt_mode && 3 * NT <= (F4 ? int(kSfCol) : 512);
@@ -1711,7 +1725,7 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
     prefetch_tmap(&tmA);
   }
   if (warp == kWarpMma) {
-    const uint32_t ncols = (F4 || nbt_mode || 2 * acc_cols > 256) ? 512u : 256u;
+    const uint32_t ncols = (F4 || nbt_mode || i16 || 2 * acc_cols > 256) ? 512u : 256u;
     if (CTA2) {
       asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                        smem_u32(&ctl->tmem_base)),
@@ -1894,7 +1908,15 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
             // address by 32 B (+2 in the >>4 field)
             const uint64_t ad = umma_desc_sw128(smem_u32(sA + size_t(st) * L.a_bytes));
             const uint32_t b0 = smem_u32(sB + size_t(st) * L.b_bytes);
-            if (pair && !(P.exp_flags & 2)) {
+            if (i16 && !(P.exp_flags & 2)) {
+              // A sub-blocks [Alo k0, Alo k1, Ahi k0, Ahi k1] against spin
+              // sub-blocks [k0, k1, k0, k1]: D_lo = Alo sigma, D_hi = Ahi sigma
+              const uint64_t bd = umma_desc_sw64(b0);
+#pragma unroll
+              for (int k = 0; k < kBK / 32; ++k)
+                mma_i8_w<CTA2>(k < 2 ? d_tmem : d_tmem + uint32_t(2 * acc_cols), ad + uint64_t(2 * k),
+                               bd + uint64_t(2 * (k & 1)), idesc, (kc | (k & 1)) ? 1u : 0u);
+            } else if (pair && !(P.exp_flags & 2)) {
               // A sub-blocks [A1 k0, A1 k1, A2 k0, A2 k1] against spin
               // sub-blocks [k0, k1, k0, k1]: S = A1 sigma + A2 sigma
               const uint64_t bd = umma_desc_sw64(b0);
@@ -1927,7 +1949,7 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
     __syncwarp();
     mbar_wait_lazy(&ctl->done, 0, 1000);
     tc_fence_after();
-    const uint32_t ncols = (F4 || nbt_mode || 2 * acc_cols > 256) ? 512u : 256u;
+    const uint32_t ncols = (F4 || nbt_mode || i16 || 2 * acc_cols > 256) ? 512u : 256u;
     if (CTA2) {
       cluster_sync_all();  // both CTAs' epilogues are done with the pair's TMEM
       asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
@@ -2304,6 +2326,7 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
           }
           er.npeer = P.npeer;
           er.peer_delta = P.peer_delta;
+          er.hi_off = i16 ? uint32_t(2 * acc_cols) : 0u;
           er.i_u32 = uint32_t(i);
           asm volatile("mov.b32 %0, %1;" : "=r"(er.p4) : "r"(4u));
           asm volatile("mov.b32 %0, %1;" : "=r"(er.p32) : "r"(32u));
@@ -2886,7 +2909,7 @@ int launch(ssqa_batch_s* b, TcParams& P, bool f4) {
   const bool tab_ok = P.fast && P.tab_w > 0;
   P.use_tab = tab_ok ? ((g.rs > 1 || P.npeer) ? 1 : kDefaultNoSplitEpi) : 0;
   if (tune().tab >= 0) P.use_tab = tab_ok ? std::min(2, tune().tab) : 0;
-  if (P.fast && g.rs == 1 && (P.use_tab == 2 || (P.use_tab == 0 && P.rails_lo))) {
+  if (P.fast && g.rs == 1 && !P.i16 && (P.use_tab == 2 || (P.use_tab == 0 && P.rails_lo))) {
     // the sign tiles of the copier warp must fit next to the smallest pipeline
     const bool pr = f4 && b->prob->q.fp4x2_ok;
     const Layout Lmin = make_layout(g.tile_cols, g.tpt, 2, 4, sig_tile_row(P, f4),
@@ -2904,18 +2927,21 @@ int launch(ssqa_batch_s* b, TcParams& P, bool f4) {
   // FP4 pair image: rows of npad bytes (two planes); spin stages of 64 bytes
   const bool pair = f4 && b->prob->q.fp4x2_ok;
   P.pair = pair ? 1 : 0;
-  const uint64_t j_row_bytes = pair ? uint64_t(g.npad) : row_bytes;
-  const uint32_t b_row = pair ? kBK / 2 : kBK;
+  // int16 couplings: plane image rows of 2 npad bytes, 64-byte spin stages
+  const bool i16 = !f4 && b->prob->q.i16;
+  P.i16 = i16 ? 1 : 0;
+  const uint64_t j_row_bytes = pair ? uint64_t(g.npad) : (i16 ? 2 * uint64_t(g.npad) : row_bytes);
+  const uint32_t b_row = (pair || i16) ? kBK / 2 : kBK;
   void* Ssrc = f4 ? static_cast<void*>(b->d_sig4) : static_cast<void*>(b->d_sig);
   const uint32_t tile_row = f4 ? kBM / 2 : kBM;
   P.sig_base = static_cast<uint8_t*>(Ssrc);
   if (!make_map(&maps[0], Jsrc, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, j_row_bytes,
                 uint64_t(g.npad) * b->prob->count, kBK, kBM, CU_TENSOR_MAP_SWIZZLE_128B) ||
       !make_map(&maps[1], Ssrc, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, row_bytes, srows, b_row,
-                g.tile_cols, pair ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B) ||
+                g.tile_cols, (pair || i16) ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B) ||
       !make_map(&maps[2], Ssrc, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, row_bytes, srows, tile_row,
                 g.tile_cols, CU_TENSOR_MAP_SWIZZLE_NONE) ||
-      !(P.fast && P.use_tab == 2 && g.rs == 1
+      !(P.fast && P.use_tab == 2 && g.rs == 1 && !P.i16
             ? make_acc_map(&maps[3], b->d_acc, g.npad, g.ccols, 4) &&
                   make_acc_map(&maps[4], b->d_acc, g.npad, g.ccols, 1)
             : make_map(&maps[3], b->d_acc, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, g.npad, g.ccols,
@@ -2952,7 +2978,7 @@ int launch(ssqa_batch_s* b, TcParams& P, bool f4) {
   }
   // 12 epilogue warps (160 registers each) for the issue-lean epilogue without
   // a row split (C3: 213.9 vs 216.9 us/sweep with 16), 16 elsewhere (CTA pairs)
-  const bool lean = P.fast && g.rs == 1 && (P.use_tab == 2 || (P.use_tab == 0 && P.rails_lo));
+  const bool lean = P.fast && g.rs == 1 && !P.i16 && (P.use_tab == 2 || (P.use_tab == 0 && P.rails_lo));
   const int epi = tune().epi ? (tune().epi == 12 ? 12 : 16) : (lean ? 12 : kDefaultEpi);
   // CTA pairs (M = 256 MMAs, each CTA streams half of the spin columns): the
   // fused run's row split with an even number of parts per column tile and
@@ -2971,11 +2997,11 @@ int launch(ssqa_batch_s* b, TcParams& P, bool f4) {
   auto setup = [&](bool pairs) {
     const int b_cols = pairs ? g.tile_cols / 2 : g.tile_cols;
     if (!make_map(&maps[1], Ssrc, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, row_bytes, srows, b_row,
-                  uint32_t(b_cols), pair ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B))
+                  uint32_t(b_cols), (pair || i16) ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B))
       return false;
     const int tab_bytes = tab_bytes_of(P);
     L = pick_layout(g.tile_cols, g.tpt, epi / 4, sig_tile_row(P, f4), int(b_row), b_cols, tab_bytes,
-                    pair || g.rs > 1);
+                    pair || i16 || g.rs > 1);
     if (tune().stages > 0) {  // experiment overrides
       L = make_layout(g.tile_cols, g.tpt, tune().stages, std::max(1, tune().nps) * (epi / 4),
                       sig_tile_row(P, f4), int(b_row), b_cols, tab_bytes);
@@ -3149,6 +3175,7 @@ TcParams base_params(ssqa_batch_s* b) {
   P.hi_clamp = b->p.i0 - b->p.alpha;
   P.lo_clamp = -b->p.i0;
   P.fast = fast_ok(b, &P) ? 1 : 0;
+  P.i16 = b->prob->q.i16 ? 1 : 0;
   P.exp_flags = tune().exp;
   P.pf_dist = 0;  // measured: prefetching J' rows costs more L2 bandwidth than it saves (C4, C5)
   if (tune().pf > 0) P.pf_dist = tune().pf;

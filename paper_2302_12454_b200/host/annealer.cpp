@@ -267,6 +267,62 @@ std::vector<AnnealResult> ssqa_run_instances(const std::vector<IsingModel>& mode
                     [&p](long c) { return jperp_schedule(c, p); });
 }
 
+std::vector<AnnealResult> ssqa_run_gi_instances(int n_nodes, double edge_prob, bool permute,
+                                                double c1, double c2,
+                                                const std::vector<uint64_t>& instance_seeds,
+                                                const SsqaParams& p,
+                                                const std::vector<uint64_t>& seeds,
+                                                std::optional<double> target_energy,
+                                                const RunOptions& opts, const EngineOptions& eng) {
+  if (instance_seeds.size() != seeds.size()) throw std::invalid_argument("one instance per seed");
+  if (seeds.empty()) return {};
+  const int n = n_nodes * n_nodes;
+  p.validate(n);
+  ProblemHandle ph;
+  check(ssqa_problem_create_gi(int(seeds.size()), n_nodes, edge_prob, instance_seeds.data(),
+                               permute ? 1 : 0, c1, c2, eng.device, &ph.p));
+  const int T = int(seeds.size());
+  ssqa_params_c c = to_c(p);
+  std::vector<ssqa_result_c> res(seeds.size());
+  std::vector<int8_t> best(size_t(T) * n);
+  std::vector<double> trace;
+  if (opts.record_trace) trace.resize(size_t(T) * (p.sc + 1) * p.r);
+  check(ssqa_run_batch(ph.p, &c, seeds.data(), T, target_energy ? 1 : 0,
+                       target_energy.value_or(0.0), opts.record_trace ? 1 : 0,
+                       opts.stop_at_target ? 1 : 0, eng.engine, res.data(), best.data(),
+                       opts.record_trace ? trace.data() : nullptr));
+  return to_results(T, n, p.r, p.sc, res, best, trace, opts.record_trace,
+                    [&p](long c) { return jperp_schedule(c, p); });
+}
+
+std::vector<AnnealResult> ssa_run_gi_instances(int n_nodes, double edge_prob, bool permute,
+                                               double c1, double c2,
+                                               const std::vector<uint64_t>& instance_seeds,
+                                               const SsaParams& p,
+                                               const std::vector<uint64_t>& seeds,
+                                               std::optional<double> target_energy,
+                                               const RunOptions& opts, const EngineOptions& eng) {
+  if (instance_seeds.size() != seeds.size()) throw std::invalid_argument("one instance per seed");
+  if (seeds.empty()) return {};
+  const int n = n_nodes * n_nodes;
+  p.validate(n);
+  ProblemHandle ph;
+  check(ssqa_problem_create_gi(int(seeds.size()), n_nodes, edge_prob, instance_seeds.data(),
+                               permute ? 1 : 0, c1, c2, eng.device, &ph.p));
+  const int T = int(seeds.size());
+  ssqa_ssa_params_c c = to_c(p);
+  std::vector<ssqa_result_c> res(seeds.size());
+  std::vector<int8_t> best(size_t(T) * n);
+  std::vector<double> trace;
+  if (opts.record_trace) trace.resize(size_t(T) * (p.sc + 1));
+  check(ssqa_ssa_run_batch(ph.p, &c, seeds.data(), T, target_energy ? 1 : 0,
+                           target_energy.value_or(0.0), opts.record_trace ? 1 : 0,
+                           opts.stop_at_target ? 1 : 0, eng.engine, res.data(), best.data(),
+                           opts.record_trace ? trace.data() : nullptr));
+  return to_results(T, n, 1, p.sc, res, best, trace, opts.record_trace,
+                    [](long) { return 0.0; });
+}
+
 std::vector<double> SsaParams::i0_levels() const {
   ssqa_ssa_params_c c = to_c(*this);
   double buf[65];

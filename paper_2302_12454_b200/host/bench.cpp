@@ -10,6 +10,8 @@
 #include <fstream>
 #include <limits>
 #include <stdexcept>
+#include <exception>
+#include <thread>
 
 #include "ssqa/gi.hpp"
 #include "ssqa/rng.hpp"
@@ -126,43 +128,82 @@ BenchRecord run_trials(const BenchConfig& cfg) {
   ps.sc = budget;
   RunOptions opts;
   opts.stop_at_target = false;
-  EngineOptions eng;
-  eng.device = cfg.device;
+  EngineOptions eng0;
   // run_engine (bench.cpp:332-357) for a set of seeds on one model.
-  auto run = [&](const IsingModel& m, const std::vector<uint64_t>& s, double target) {
+  auto run = [&](const IsingModel& m, const std::vector<uint64_t>& s, double target,
+                 const EngineOptions& eng) {
     return ssa ? ssa_run_batch(m, ps, s, target, opts, eng)
                : ssqa_run_batch(m, p, s, target, opts, eng);
   };
 
   std::vector<uint64_t> seeds(size_t(cfg.trials));
   for (int t = 0; t < cfg.trials; ++t) seeds[size_t(t)] = cfg.base_seed + uint64_t(t);
-  std::vector<AnnealResult> results;
-  int n = 0;
-  if (!gi || !cfg.problem.fresh_instance) {
-    if (!gi)
-      throw std::invalid_argument(
-          "model files are not read by the engine facade: load the model in the caller and "
-          "call ssqa_run / the C ABI");
-    IsingModel m = gi_model(cfg.problem, cfg.problem.gi_seed);
-    const double target = 0.0;  // GI ground state (bench.cpp:309-313)
-    n = m.n();
-    results = run(m, seeds, target);
-  } else {
-    // Fresh instance per trial (bench.cpp:387-389): every trial's GI instance
-    // in one multi-instance problem, the whole battery in one device batch.
-    const CounterRng inst(cfg.base_seed, kStreamTrialInstance);
-    std::vector<IsingModel> models;
-    models.reserve(size_t(cfg.trials));
-    for (int t = 0; t < cfg.trials; ++t) models.push_back(gi_model(cfg.problem, inst.raw(uint64_t(t))));
-    n = models.front().n();
-    if (ssa || (p.r <= 256 && p.delay <= 30)) {
-      results = ssa ? ssa_run_instances(models, ps, seeds, 0.0, opts, eng)
-                    : ssqa_run_instances(models, p, seeds, 0.0, opts, eng);
-    } else {  // shapes only the SIMT engine takes: one device run per instance
-      for (int t = 0; t < cfg.trials; ++t)
-        results.push_back(run(models[size_t(t)], {seeds[size_t(t)]}, 0.0).front());
-    }
+  if (!gi)
+    throw std::invalid_argument(
+        "model files are not read by the engine facade: load the model in the caller and "
+        "call ssqa_run / the C ABI");
+  const int n = cfg.problem.n_nodes * cfg.problem.n_nodes;
+  const bool fresh = cfg.problem.fresh_instance;
+  const bool device_gi = ssa || (p.r <= 256 && p.delay <= 30);  // tcgen05 shapes
+  // Fresh instance per trial (bench.cpp:387-389): seeds CounterRng(base_seed,
+  // kStreamTrialInstance).raw(t), every instance built on the device.
+  std::vector<uint64_t> inst(size_t(cfg.trials));
+  if (fresh) {
+    const CounterRng irng(cfg.base_seed, kStreamTrialInstance);
+    for (int t = 0; t < cfg.trials; ++t) inst[size_t(t)] = irng.raw(uint64_t(t));
   }
+  std::optional<IsingModel> pinned;
+  if (!fresh) pinned.emplace(gi_model(cfg.problem, cfg.problem.gi_seed));
+  const double target = 0.0;  // GI ground state (bench.cpp:309-313)
+
+  // One block of trials [lo, hi) on one GPU.
+  auto block = [&](int lo, int hi, int device) -> std::vector<AnnealResult> {
+    EngineOptions eng = eng0;
+    eng.device = device;
+    const std::vector<uint64_t> s(seeds.begin() + lo, seeds.begin() + hi);
+    if (!fresh) return run(*pinned, s, target, eng);
+    const std::vector<uint64_t> is(inst.begin() + lo, inst.begin() + hi);
+    if (device_gi) {
+      const ProblemSpec& ps_ = cfg.problem;
+      return ssa ? ssa_run_gi_instances(ps_.n_nodes, ps_.edge_prob, ps_.permute, ps_.c1, ps_.c2,
+                                        is, ps, s, target, opts, eng)
+                 : ssqa_run_gi_instances(ps_.n_nodes, ps_.edge_prob, ps_.permute, ps_.c1,
+                                         ps_.c2, is, p, s, target, opts, eng);
+    }
+    // shapes only the SIMT engine takes: one device run per instance
+    std::vector<AnnealResult> out;
+    for (size_t t = 0; t < s.size(); ++t)
+      out.push_back(run(gi_model(cfg.problem, is[t]), {s[t]}, target, eng).front());
+    return out;
+  };
+
+  // GPUs share the battery in contiguous trial blocks, one host thread each
+  // (the reference's worker pool over trials, bench.cpp:399-407).
+  const std::vector<int> devs = cfg.devices.empty() ? std::vector<int>{cfg.device} : cfg.devices;
+  const int G = std::max(1, std::min(int(devs.size()), cfg.trials));
+  std::vector<std::vector<AnnealResult>> parts(static_cast<size_t>(G));
+  std::vector<std::exception_ptr> errs(static_cast<size_t>(G));
+  auto work = [&](int gi_) {
+    const int lo = int(int64_t(cfg.trials) * gi_ / G), hi = int(int64_t(cfg.trials) * (gi_ + 1) / G);
+    try {
+      parts[size_t(gi_)] = block(lo, hi, devs[size_t(gi_)]);
+    } catch (...) {
+      errs[size_t(gi_)] = std::current_exception();
+    }
+  };
+  if (G == 1) {
+    work(0);
+  } else {
+    std::vector<std::thread> th;
+    for (int g = 0; g < G; ++g) th.emplace_back(work, g);
+    for (auto& x : th) x.join();
+  }
+  for (auto& e : errs)
+    if (e) std::rethrow_exception(e);
+  std::vector<AnnealResult> results;
+  results.reserve(size_t(cfg.trials));
+  for (auto& part : parts)
+    for (auto& a : part) results.push_back(std::move(a));
   BenchRecord rec;
   rec.engine = cfg.engine;
   rec.n = n;

@@ -326,4 +326,37 @@ void gi_ising_arrays(const GiInstance& inst, double* h, double* J, double* offse
   *offset = off;
 }
 
+// The pair of generate_gi as two 0/1 adjacency matrices (0-based, n x n,
+// graph 1 then graph 2) and the Ising biases / offset of its penalty in
+// closed form: with deg1 / deg2 the vertex degrees and m = |E1| = |E2|,
+//   h_(u,i) = c1 - c1 (n-1) - c2/4 [deg2(u)(n-1-deg1(i)) + (n-1-deg2(u)) deg1(i)]
+//   offset  = 2 c1 n - c1 n^2 + c1 n^2 (n-1) / 2 + c2/4 M,
+//   M = m (n(n-1) - 2m) + (n(n-1)/2 - m) 2m   (edge-mismatch pairs a < b).
+// Exact (hence equal to the reference's accumulation) whenever c1 and c2 are
+// dyadic, the only case the engine accepts; the device generator
+// (ssqa_problem_create_gi) builds J' from the same adjacency matrices.
+void gi_compact(const GiInstance& inst, uint8_t* adj, double* h, double* offset) {
+  const int n = inst.graph1.n_nodes;
+  const std::vector<uint8_t> a1 = adjacency(inst.graph1), a2 = adjacency(inst.graph2);
+  std::copy(a1.begin(), a1.end(), adj);
+  std::copy(a2.begin(), a2.end(), adj + size_t(n) * n);
+  std::vector<int> d1(size_t(n), 0), d2(size_t(n), 0);
+  for (int x = 0; x < n; ++x)
+    for (int y = 0; y < n; ++y) {
+      d1[size_t(x)] += a1[size_t(x) * n + y];
+      d2[size_t(x)] += a2[size_t(x) * n + y];
+    }
+  const double c1 = inst.c1, c2 = inst.c2;
+  for (int u = 0; u < n; ++u)
+    for (int i = 0; i < n; ++i) {
+      const long mis = long(d2[size_t(u)]) * (n - 1 - d1[size_t(i)]) +
+                       long(n - 1 - d2[size_t(u)]) * d1[size_t(i)];
+      h[size_t(u) * n + i] = c1 - c1 * double(n - 1) - 0.25 * c2 * double(mis);
+    }
+  const double m = double(inst.graph1.edges.size());
+  const double nn1 = double(n) * double(n - 1);
+  const double M = m * (nn1 - 2.0 * m) + (nn1 / 2.0 - m) * 2.0 * m;
+  *offset = 2.0 * c1 * n - c1 * double(n) * n + c1 * double(n) * n * (n - 1) / 2.0 + 0.25 * c2 * M;
+}
+
 }  // namespace ssqa

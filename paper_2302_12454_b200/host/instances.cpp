@@ -62,6 +62,14 @@ int ssqa_gi_ising(int n_nodes, double edge_prob, uint64_t seed, int permute, dou
   });
 }
 
+int ssqa_gi_compact(int n_nodes, double edge_prob, uint64_t seed, int permute, double c1,
+                    double c2, uint8_t* adj, double* h, double* offset) {
+  return guard([&] {
+    ssqa::gi_compact(ssqa::generate_gi(n_nodes, edge_prob, seed, permute != 0, c1, c2), adj, h,
+                     offset);
+  });
+}
+
 int ssqa_dense_ising(int n, int kind, uint64_t seed, double* h, double* J, double* offset) {
   return guard([&] {
     if (n < 1) throw std::invalid_argument("n must be >= 1");

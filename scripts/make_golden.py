@@ -237,8 +237,13 @@ def trials_large(ref: Oracle):
     permuted, c1=c2=1) as in BASELINE.json.  The device batch must match trial for trial."""
     out = {}
     cases = [("c2_gi20", dict(n_nodes=20, trials=1024, ec=40000, base_seed=1000)),
-             ("c3_gi50", dict(n_nodes=50, trials=48, ec=100000, base_seed=1000))]
-    for name, kw in cases:
+             ("c3_gi50", dict(n_nodes=50, trials=48, ec=100000, base_seed=1000)),
+             # fresh instance per trial at the C3 size (bench.hpp:28, the reference
+             # default), permuted, c1 = c2 = 1: the device-built battery's pin
+             ("c3_fresh_gi50", dict(n_nodes=50, trials=16, ec=100000, base_seed=1000,
+                                    fresh_instance=True))]
+    only = [c for c in cases if os.environ.get("SSQA_GOLDEN_CASE", c[0]) == c[0]]
+    for name, kw in only:
         outs, ps, tm, tts = ref.run_trials(params(20, 1), workers=os.cpu_count(), gi_seed=7,
                                            **kw)
         out[name] = dict(**{f"k_{k}": v for k, v in kw.items()}, r=20,
@@ -248,6 +253,15 @@ def trials_large(ref: Oracle):
                          best_energy=np.array([o["best_energy"] for o in outs]), p_s=ps,
                          wall=np.array([o["wall_seconds"] for o in outs]))
         print(name, "p_s", ps, flush=True)
+    # keep the cases already in the committed file that were not regenerated
+    path = os.path.join(OUT, "trials_large.npz")
+    if os.path.exists(path):
+        z = np.load(path)
+        for key in z.files:
+            case, field = key.split("/", 1)
+            if case not in out:
+                out.setdefault(case + "#keep", {})[field] = z[key]
+        out = {k.replace("#keep", ""): v for k, v in out.items()}
     return out
 
 

@@ -341,6 +341,12 @@ int main() {
   std::printf("FRESH %.17g\n", rf.p_s);
   for (const TrialOutcome& t : rf.per_trial)
     std::printf("F %d %ld %.17g\n", int(t.reached_target), t.first_hit_cycle, t.best_energy);
+  BenchConfig cf2 = cf;
+  cf2.devices = {0, 0};  // two host threads, one trial block each (same GPU here)
+  BenchRecord rf2 = run_trials(cf2);
+  std::printf("FRESH2 %.17g\n", rf2.p_s);
+  for (const TrialOutcome& t : rf2.per_trial)
+    std::printf("G %d %ld %.17g\n", int(t.reached_target), t.first_hit_cycle, t.best_energy);
   return 0;
 }
 ''')
@@ -361,6 +367,10 @@ int main() {
     rows = out[15:fi]
     fresh = golden_fresh()["fresh_gi10"]
     assert float(out[fi + 1]) == float(fresh["p_s"])
+    f2 = out.index("FRESH2")
+    assert out[f2 + 1] == out[fi + 1]
+    g = out[f2 + 2:]
+    assert [x for k, x in enumerate(g) if k % 4] == [x for k, x in enumerate(out[fi + 2:f2]) if k % 4]
     fr = out[fi + 2:]
     for t in range(64):
         assert fr[4 * t] == "F"
@@ -824,11 +834,13 @@ def test_device_quantizer_matches_host_quantizer():
     with pytest.raises(ValueError, match="not a dyadic"):
         sq.Problem(bad)
     tiny = sq.IsingModel(4)
-    tiny.set_coupling(0, 1, 0.1)  # needs p = 55: far beyond int8
-    with pytest.raises(ValueError, match="exceeds int8"):
+    tiny.set_coupling(0, 1, 0.1)  # needs p = 55: far beyond int16
+    with pytest.raises(ValueError, match="exceeds int16"):
         sq.Problem(tiny)
     big = sq.IsingModel(4)
-    big.set_coupling(1, 2, 200.0)
+    big.set_coupling(1, 2, 200.0)  # int16 planes (test_int16_*); refused when they are off
+    assert sq.Problem(big).info()["int16"] == 1
+    sq.tune(i16=0)
     with pytest.raises(ValueError, match="exceeds int8"):
         sq.Problem(big)
 
@@ -951,3 +963,77 @@ def test_fused_run_leaves_exact_lattice(orc, monkeypatch):
             assert np.array_equal(sg, s) and np.array_equal(bits(ac), bits(a)), (p.r, t)
             assert np.array_equal(hi, h)
         b.close()
+
+
+# ---- int16 couplings (north star: "int16 where the coefficient range requires it")
+
+def int16_model(n, jmax, seed, scale=1.0):
+    rng = np.random.default_rng(seed)
+    J = np.zeros((n, n))
+    iu = np.triu_indices(n, 1)
+    J[iu] = rng.integers(-jmax, jmax + 1, len(iu[0])) * scale
+    J = J + J.T
+    h = rng.integers(-3 * jmax, 3 * jmax + 1, n) * scale
+    return sq.IsingModel.from_arrays(h, J, 0.25)
+
+
+@pytest.mark.parametrize("rs", [1, 2], ids=["whole", "rowsplit"])
+def test_int16_couplings_match_oracle(orc, rs):
+    """|J'| up to 2^14 (and the plane limit 32639): two int8 planes J' = 256 Ahi +
+    Alo, one kind::i8 MMA per plane into its own TMEM accumulator, S = D_lo +
+    256 D_hi in the epilogue.  Full runs with traces against the C oracle,
+    whole tiles and a row split (table epilogue, CTA cooperation)."""
+    if rs > 1:
+        sq.tune(rs=rs)
+    for n, jmax, scale, bidir in [(300, 1 << 14, 1.0, False), (200, 32639, 1.0, True),
+                                  (260, 3000, 0.25, False)]:
+        m = int16_model(n, jmax, n + jmax, scale)
+        if jmax == 32639:
+            m.J[0, 1] = m.J[1, 0] = 32639.0  # the largest magnitude the planes hold
+        prob = sq.Problem(m)
+        assert prob.info()["int16"] == 1 and prob.info()["max_abs_j"] == jmax
+        p = params(6, 40, tau=5, bidirectional=bidir)
+        seeds = [5 + 3 * t for t in range(5)]
+        res = sq.ssqa_run_batch(m, to_sq(p), seeds, None, sq.RunOptions(True, False),
+                                _lib.ENGINE_TCGEN05, problem=prob)
+        for t in (0, 4):
+            o = orc.ssqa_run(m.h, m.J, m.offset, p, seeds[t], None, True, False)
+            assert np.array_equal(bits(res[t].trace_energy), bits(o.trace)), (n, t)
+            assert np.array_equal(res[t].best_state, o.best_state), (n, t)
+            assert res[t].best_energy == o.best_energy
+        prob.close()
+
+
+def test_int16_per_step_api_matches_oracle(orc):
+    """The per-step sweeps (ssqa_sweep, annealer.cpp:449-463) on int16 couplings:
+    spins, history and every accumulator bit after each sweep."""
+    m = int16_model(150, 9000, 3)
+    p = params(4, 30, tau=3)
+    seeds = [21, 22]
+    b = sq.Batch(sq.Problem(m), to_sq(p), len(seeds), engine=_lib.ENGINE_TCGEN05)
+    b.set_seeds(seeds)
+    b.init()
+    states = [orc.init_lattice(m.n, p.r, p.delay, sd) for sd in seeds]
+    for c in range(8):
+        b.sweep(1)
+        for t, (s, a, h) in enumerate(states):
+            orc.ssqa_sweep(m.h, m.J, m.offset, orc.jperp_schedule(c, p), p, seeds[t], c, s, a, h, c)
+            sg, ac, hi, cyc = b.read_lattice(t)
+            assert cyc == c + 1
+            assert np.array_equal(sg, s) and np.array_equal(bits(ac), bits(a)), (c, t)
+            assert np.array_equal(hi, h)
+    b.close()
+
+
+def test_int16_limits():
+    m = int16_model(64, 100, 1)
+    m.J[2, 3] = m.J[3, 2] = 32640.0  # one beyond the planes
+    with pytest.raises(sq.SsqaInvalidArgument):
+        sq.Problem(m)
+    m.J[2, 3] = m.J[3, 2] = 32639.0
+    prob = sq.Problem(m)
+    with pytest.raises(sq.SsqaInvalidArgument):  # SIMT engine: int8 only
+        sq.Batch(prob, sq.SsqaParams(r=4, sc=5), 2, engine=_lib.ENGINE_SIMT)
+    sq.tune(i16=0)
+    with pytest.raises(sq.SsqaInvalidArgument):
+        sq.Problem(m)

@@ -75,6 +75,26 @@ def test_gi_builder_matches_live_reference_non_dyadic(ref):
         assert np.float64(m.offset).view(np.uint64) == np.float64(off).view(np.uint64)
 
 
+def test_gi_compact_closed_form_matches_builder():
+    """The host half of the device GI generator: biases and offset in closed
+    form (host/inputs.cpp gi_compact) equal the builder's bit for bit for
+    dyadic penalties, and the adjacency matrices reproduce every coupling."""
+    for nn, seed, perm, c1, c2 in [(1, 3, True, 1.0, 1.0), (2, 5, True, 1.0, 1.0),
+                                   (5, 9, False, 0.75, 0.75), (10, 7, True, 1.0, 1.0),
+                                   (8, 4, True, 0.5, 2.0), (12, 99, False, 1.25, 0.375)]:
+        adj, h, off = sq.gi_compact(nn, 0.5, seed, perm, c1, c2)
+        m = sq.gi_ising(nn, 0.5, seed, perm, c1, c2)
+        assert np.array_equal(h.view(np.uint64), m.h.view(np.uint64))
+        assert np.float64(off).view(np.uint64) == np.float64(m.offset).view(np.uint64)
+        a1, a2 = adj[0].astype(bool), adj[1].astype(bool)
+        u, i = np.divmod(np.arange(nn * nn), nn)
+        one_hot = (u[:, None] == u[None, :]) != (i[:, None] == i[None, :])
+        mis = (u[:, None] != u[None, :]) & (i[:, None] != i[None, :]) & \
+            (a1[i[:, None], i[None, :]] != a2[u[:, None], u[None, :]])
+        J = np.where(one_hot, -0.25 * 2 * c1, np.where(mis, -0.25 * c2, 0.0))
+        assert np.array_equal(J.view(np.uint64), m.J.view(np.uint64))
+
+
 def test_gi_builder_rejects_bad_arguments():
     with pytest.raises(ValueError):
         sq.gi_ising(0)
