@@ -51,6 +51,9 @@ constexpr int kCW = 8;  // columns per epilogue chunk (one tcgen05.ld .x8)
 #ifndef SSQA_EPI_V
 #define SSQA_EPI_V 1  // FP64 epilogue: 1 issue-lean noise draw (noise_top5 / noise_lut), 0 previous
 #endif
+#ifndef SSQA_CT_V4
+#define SSQA_CT_V4 1  // clamped table in the issue-lean epilogue (STG stores, 2D ring) vs epi_ct
+#endif
 #ifndef SSQA_CT_ICMP
 #define SSQA_CT_ICMP 0  // clamped-table path: clamp with integer compares (1) or DSETP (0)
 #endif
@@ -1431,9 +1434,12 @@ struct V4Row {
   bool w_row;
   uint32_t jp_hi, jp_lo, hic_hi, loc_hi, rail_lo;
   uint64_t pol;
+  int h1c, ct_max;           // TBL: clamped table index = clamp(S + h1c + noise, 0, ct_max)
+  uint32_t ytab;
+  int exp;                   // timing ablations (TcParams::exp_flags): 64 no accumulator stores
 };
 
-template <bool BIDIR, bool SIGACC, bool F4>
+template <bool BIDIR, bool SIGACC, bool F4, bool TBL = false>
 __device__ __forceinline__ void epi_v4(const V4Row& r, const FastConsts& fc, const I2D& i2d,
                                        SmemCtl* ctl, const double* acc_ring, const ColTab* c_col,
                                        const uint8_t* c_umask, long long* q_sum, uint32_t trow,
@@ -1486,12 +1492,22 @@ __device__ __forceinline__ void epi_v4(const V4Row& r, const FastConsts& fc, con
       }
       const uint32_t up = uint32_t(lds_s8(nbq + uint32_t(j) * kRow));
       const uint32_t t5 = noise_top5_v4(cbase, r.iG_lo, r.iG_hi, r.p4, r.p32);
-      const uint32_t xb = uint32_t(S) + r.h1x + uint32_t(lds_s8(r.lut + t5));
-      double input = __dsub_rn(__hiloint2double(int(i2d.magic_hi), int(xb)), i2d.magic);
-      input = __dadd_rn(input, __hiloint2double(int(r.jp_hi ^ (up & 0x80000000u)), int(r.jp_lo)));
-      if (BIDIR) {
-        const uint32_t dn = uint32_t(lds_s8(nbq + uint32_t(j) * kRow + kCtTileRow));
-        input = __dadd_rn(input, __hiloint2double(int(r.jp_hi ^ (dn & 0x80000000u)), int(r.jp_lo)));
+      double input;
+      if (TBL) {
+        // y = fl(X 2^-p + jperp u [+ jperp d]) from the per-cycle clamped table
+        // (use_tab 2 layout [row][combo], 8-byte entries)
+        const int xi = min(max(S + r.h1c + lds_s8(r.lut + t5), 0), r.ct_max);
+        uint32_t cmbo = (up >> 28) & 8u;
+        if (BIDIR) cmbo |= (uint32_t(lds_s8(nbq + uint32_t(j) * kRow + kCtTileRow)) >> 27) & 16u;
+        input = lds_f64(r.ytab + (uint32_t(xi) << (BIDIR ? 5 : 4)) + cmbo);
+      } else {
+        const uint32_t xb = uint32_t(S) + r.h1x + uint32_t(lds_s8(r.lut + t5));
+        input = __dsub_rn(__hiloint2double(int(i2d.magic_hi), int(xb)), i2d.magic);
+        input = __dadd_rn(input, __hiloint2double(int(r.jp_hi ^ (up & 0x80000000u)), int(r.jp_lo)));
+        if (BIDIR) {
+          const uint32_t dn = uint32_t(lds_s8(nbq + uint32_t(j) * kRow + kCtTileRow));
+          input = __dadd_rn(input, __hiloint2double(int(r.jp_hi ^ (dn & 0x80000000u)), int(r.jp_lo)));
+        }
       }
       const double sd = __dadd_rn(a_old, input);
       const bool p_lo = sd < fc.lo_clamp, p_hi = sd >= fc.i0;
@@ -1502,7 +1518,7 @@ __device__ __forceinline__ void epi_v4(const V4Row& r, const FastConsts& fc, con
       asm("mad.wide.u32 %0, %1, %2, %3;"
           : "=l"(addr)
           : "r"(uint32_t(cb + j)), "r"(r.col_stride32), "l"(r.acc_col));
-      st_f64_if(reinterpret_cast<double*>(addr), nv, (umask >> j) & 1u, r.pol);
+      st_f64_if(reinterpret_cast<double*>(addr), nv, ((umask >> j) & 1u) && !(r.exp & 64), r.pol);
       if (F4) {
         ball[j] = __ballot_sync(0xffffffffu, nhi < 0);
       } else {
@@ -2003,7 +2019,7 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
             const uint32_t ph = (cnt / uint32_t(nps)) & 1;
             mbar_wait_lazy(&ctl->aempty[slot], ph ^ 1, SSQA_LAZY_NS_LOAD);
             mbar_expect_tx(&ctl->afull[slot], kCW * kBM * 8);
-            if (ct_mode)  // [row block][column][32 rows]: one dense block per epilogue warp
+            if (ct_mode && !SSQA_CT_V4)  // [row block][column][32 rows]: one dense block per epilogue warp
               tma_load_3d_hint(&tmA, &ctl->afull[slot], acc_ring + size_t(slot) * kCW * kBM, 0,
                                col0 + ch * kCW, (rt_lo + rt) * 4, pol_first);
             else
@@ -2345,7 +2361,48 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
 #define SSQA_EPI_FAST(B, S)                  \
   if (P.use_tab == 1) SSQA_EPI(B, S, true, true); \
   else SSQA_EPI(B, S, true, false)
-          if (ct_mode) {
+          if (ct_mode && SSQA_CT_V4) {
+            V4Row vr;
+            vr.iG_lo = er.iG_lo;
+            vr.iG_hi = er.iG_hi;
+            vr.p4 = er.p4;
+            vr.p32 = er.p32;
+            vr.h1x = er.h1x;
+            vr.h2 = er.h2;
+            vr.h1c = er.h1 - (P.tab_lo1 - 1);
+            vr.ct_max = P.tab_w + 1;
+            vr.ytab = smem_u32(ytab);
+            vr.nbt = smem_u32(sig_tiles) + uint32_t(buf) * ct_tile_bytes + uint32_t(il);
+            vr.lut = smem_u32(ctl->nz_lut);
+            vr.e_tmem = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(2 * acc_cols);
+            vr.e_mode = (!e_tmem || NRT == 1) ? 0 : (rt == 0 ? 1 : (rt == NRT - 1 ? 3 : 2));
+            vr.acc_col = reinterpret_cast<uint64_t>(P.acc + size_t(col0) * g.npad + i);
+            vr.col_stride32 = uint32_t(g.npad) * 8u;
+            vr.dst_w = er.dst_w;
+            vr.nib_live = er.nib_live;
+            vr.cur_i = er.cur_i;
+            vr.dst_i = er.dst_i;
+            vr.nib_shift = er.nib_shift;
+            vr.w_row = row_live;
+            vr.jp_hi = fc.jp_hi;
+            vr.jp_lo = fc.jp_lo;
+            vr.hic_hi = uint32_t(__double2hiint(fc.hi_clamp));
+            vr.loc_hi = uint32_t(__double2hiint(fc.lo_clamp));
+            vr.rail_lo = uint32_t(__double2loint(fc.hi_clamp));
+            vr.pol = pol_first;
+            vr.exp = P.exp_flags;
+#define SSQA_V4T(B, S)                                                                            \
+  epi_v4<B, S, F4, true>(vr, fc, i2d, ctl, acc_ring, c_col, ctl->umask, q_sum, trow, sub, kSubs, \
+                         nchunk, nps, cnt0, il, lane)
+            if (sig_from_acc) {
+              if (bidir) SSQA_V4T(true, true);
+              else SSQA_V4T(false, true);
+            } else {
+              if (bidir) SSQA_V4T(true, false);
+              else SSQA_V4T(false, false);
+            }
+#undef SSQA_V4T
+          } else if (ct_mode) {
             CtRow cr;
             cr.i_u32 = er.i_u32;
             cr.iG_lo = er.iG_lo;
@@ -2417,6 +2474,7 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
             vr.loc_hi = uint32_t(__double2hiint(fc.lo_clamp));
             vr.rail_lo = uint32_t(__double2loint(fc.hi_clamp));  // == loc's (fast_ok)
             vr.pol = pol_first;
+            vr.exp = P.exp_flags;
 #define SSQA_V4(B, S)                                                                       \
   epi_v4<B, S, F4>(vr, fc, i2d, ctl, acc_ring, c_col, ctl->umask, q_sum, trow, sub, kSubs, \
                    nchunk, nps, cnt0, il, lane)
@@ -2445,7 +2503,7 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
 #undef SSQA_EPI
         }
         tc_fence_before();
-        const bool ct_now = ct_mode && !drain && !(P.exp_flags & 1);
+        const bool ct_now = ct_mode && !SSQA_CT_V4 && !drain && !(P.exp_flags & 1);
         // this warp's spin rows and accumulators of row tile rt are in global
         // memory: make them visible to the TMA (async proxy) reads of pass c+1
         asm volatile("fence.proxy.async.global;" ::: "memory");
@@ -2941,7 +2999,7 @@ int launch(ssqa_batch_s* b, TcParams& P, bool f4) {
                 g.tile_cols, (pair || i16) ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B) ||
       !make_map(&maps[2], Ssrc, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, row_bytes, srows, tile_row,
                 g.tile_cols, CU_TENSOR_MAP_SWIZZLE_NONE) ||
-      !(P.fast && P.use_tab == 2 && g.rs == 1 && !P.i16
+      !(P.fast && P.use_tab == 2 && g.rs == 1 && !P.i16 && !SSQA_CT_V4
             ? make_acc_map(&maps[3], b->d_acc, g.npad, g.ccols, 4) &&
                   make_acc_map(&maps[4], b->d_acc, g.npad, g.ccols, 1)
             : make_map(&maps[3], b->d_acc, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, g.npad, g.ccols,
