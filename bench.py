@@ -363,7 +363,12 @@ def run_rows(args, cfg):
         with torch.cuda.stream(stream):
             dist.all_gather_into_tensor(out, mine)
 
+    graph = None
+
     def step():
+        if graph is not None:
+            graph.replay_on_engine()
+            return b.elapsed_ms()
         b.shard_begin(target, False)
         if p2p:
             # every rank's previous step (its last merge reads the slots peers
@@ -381,6 +386,12 @@ def run_rows(args, cfg):
         return b.elapsed_ms()
 
     for _ in range(args.warmup):
+        step()
+    if args.graph and not p2p:
+        # the whole run (begin, sc+1 x (pass, all-gather, merge), end) as one
+        # CUDA graph: one host launch per step (rowshard.capture_run)
+        from paper_2302_12454_b200.rowshard import capture_run
+        graph = capture_run(b, buf, rank, world, sc + 1, all_gather, stream, target, False)
         step()
     clocks = ClockSampler(local)
     barrier()
@@ -422,7 +433,8 @@ def run_rows(args, cfg):
                        "parallelism": f"J rows x{world} (" + {
                            "nccl": "NCCL all-gather", "p2p": "pack kernel pushes to peers",
                            "direct": "exchange fused into the sweep kernel's stores"}[
-                           args.exchange] + " per cycle)",
+                           args.exchange] + " per cycle"
+                           + (", whole run as one CUDA graph" if graph is not None else "") + ")",
                        "l2": "no flush needed: per-step state exceeds L2"},
             "roofline": {"bound": "tensor", "achieved": tensor_tops, "peak": tc_peak,
                          "unit": "TOPS", "frac": tensor_tops / tc_peak, "traffic": None,
@@ -727,6 +739,8 @@ def main():
                     help="skip the device-timed C4/C5 lines added to the C3 line")
     ap.add_argument("--shard", default="trials", choices=["trials", "rows"],
                     help="multi-GPU layout: trial blocks per GPU (default) or J' rows per GPU")
+    ap.add_argument("--graph", action="store_true",
+                    help="--shard rows, nccl: capture each run as one CUDA graph")
     ap.add_argument("--exchange", default="nccl", choices=["nccl", "p2p", "direct"],
                     help="--shard rows: NCCL all-gather, pack-kernel peer push, or the push "
                          "fused into the sweep kernel (CUDA IPC peer memory over NVLink)")

@@ -47,6 +47,17 @@ int set_err(int code, const std::string& msg) {
       return set_err(SSQA_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e__)); \
   } while (0)
 
+// Batch timing events.  Inside a stream capture (rowshard.capture_run) a plain
+// record only orders the capture; the external form makes it a real record
+// node, so elapsed-time queries work after every graph replay.
+cudaError_t record_event(cudaEvent_t ev, cudaStream_t st) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaError_t e = cudaStreamIsCapturing(st, &cs);
+  if (e != cudaSuccess) return e;
+  return cs == cudaStreamCaptureStatusActive ? cudaEventRecordWithFlags(ev, st, cudaEventRecordExternal)
+                                             : cudaEventRecord(ev, st);
+}
+
 #define CHECK_LAUNCH()                                                                 \
   do {                                                                                 \
     cudaError_t e__ = cudaGetLastError();                                              \
@@ -1066,7 +1077,7 @@ int ssqa_batch_launch(ssqa_batch b, int has_target, double target, int stop_at_t
   CU(cudaSetDevice(b->prob->device));
   cudaStream_t st = b->prob->stream;
   b->launches = 0;
-  CU(cudaEventRecord(b->ev0, st));
+  CU(record_event(b->ev0, st));
   launch_reset_results(b->g.T, b->p.sc, b->d_best_e, b->d_best_k, b->d_reached,
                        b->d_first_hit, b->d_cycles_used, b->d_active, st);
   CHECK_LAUNCH();
@@ -1092,7 +1103,7 @@ int ssqa_batch_launch(ssqa_batch b, int has_target, double target, int stop_at_t
       if (rc) return rc;
     }
   }
-  CU(cudaEventRecord(b->ev1, st));
+  CU(record_event(b->ev1, st));
   return SSQA_OK;
 }
 
@@ -1178,7 +1189,7 @@ int ssqa_batch_shard_begin(ssqa_batch b, int has_target, double target, int stop
   CU(cudaSetDevice(b->prob->device));
   cudaStream_t st = b->prob->stream;
   b->launches = 0;
-  CU(cudaEventRecord(b->ev0, st));
+  CU(record_event(b->ev0, st));
   launch_reset_results(b->g.T, b->p.sc, b->d_best_e, b->d_best_k, b->d_reached,
                        b->d_first_hit, b->d_cycles_used, b->d_active, st);
   CHECK_LAUNCH();
@@ -1410,7 +1421,7 @@ int ssqa_ipc_close(void* dev_ptr) {
 int ssqa_batch_shard_end(ssqa_batch b) {
   if (!b) return set_err(SSQA_EINVAL, "null batch");
   CU(cudaSetDevice(b->prob->device));
-  CU(cudaEventRecord(b->ev1, b->prob->stream));
+  CU(record_event(b->ev1, b->prob->stream));
   b->cycle = b->p.sc;
   return SSQA_OK;
 }

@@ -136,9 +136,34 @@ def _finish(b: Batch, trials: int, opts: RunOptions) -> List[AnnealResult]:
     return _results(res, best, tr, trials)
 
 
+def capture_run(b: Batch, buf, rank: int, world: int, cycles: int, all_gather, stream,
+                target: Optional[float], stop_at_target: bool):
+    """The whole row-sharded run -- begin, `cycles` x (pass, NCCL all-gather,
+    merge), end -- captured once as a CUDA graph on the engine's stream
+    (every cycle's launches keep their own parameters as graph nodes), so a
+    run is ONE host launch instead of ~5 per cycle (the per-cycle host cost
+    that dominates at 8 GPUs, where a C4 cycle computes in ~70 us).  The
+    batch must have run once before (one-time allocations and symbol copies
+    cannot be captured).  Replay with graph.replay_on_engine() (on the
+    engine's stream); results via b.fetch()."""
+    import torch
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=stream):
+        b.shard_begin(target, stop_at_target)
+        shard_cycles(b, buf, rank, world, cycles, all_gather)
+        b.shard_end()
+
+    def replay():  # on the engine's stream, ordered with the batch's own calls
+        with torch.cuda.stream(stream):
+            g.replay()
+    g.replay_on_engine = replay
+    return g
+
+
 def run_row_sharded(m: IsingModel, p: SsqaParams, seeds: Sequence[int],
                     target: Optional[float] = None, opts: RunOptions = RunOptions(),
-                    device: int = 0, group=None, exchange: str = "nccl") -> List[AnnealResult]:
+                    device: int = 0, group=None, exchange: str = "nccl",
+                    graph: bool = False) -> List[AnnealResult]:
     """ssqa_run for every seed with J' rows sharded over the ranks of `group`
     (the default process group when torch.distributed is initialised, else a
     single shard); exchange "nccl" (all-gather) or "p2p" (peer push)."""
@@ -165,7 +190,16 @@ def run_row_sharded(m: IsingModel, p: SsqaParams, seeds: Sequence[int],
         b.set_seeds(seeds)
         b.shard_begin(target, opts.stop_at_target)
         shard_cycles(b, buf, rank, world, p.sc + 1, all_gather)
-        return _finish(b, len(seeds), opts)
+        if not graph:
+            return _finish(b, len(seeds), opts)
+        b.shard_end()
+        # graph mode: the same run again, captured and replayed
+        g = capture_run(b, buf, rank, world, p.sc + 1, all_gather, stream, target,
+                        opts.stop_at_target)
+        g.replay_on_engine()
+        b.synchronize()
+        res, best, tr = b.fetch(True, opts.record_trace)
+        return _results(res, best, tr, len(seeds))
     finally:
         b.close()
         prob.close()

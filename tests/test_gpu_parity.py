@@ -660,10 +660,14 @@ def test_row_sharded_single_rank(orc):
     m = sq.dense_ising(256, 0, 2)
     p = params(8, 30, tau=5)
     res = run_row_sharded(m, to_sq(p), [3, 4], None, sq.RunOptions(True, False))
+    # the same run captured as one CUDA graph (rowshard.capture_run) and replayed
+    gres = run_row_sharded(m, to_sq(p), [3, 4], None, sq.RunOptions(True, False), graph=True)
     for t, sd in enumerate([3, 4]):
         o = orc.ssqa_run(m.h, m.J, m.offset, p, sd, None, True, False)
-        assert res[t].best_energy == o.best_energy
-        assert np.array_equal(bits(res[t].trace_energy), bits(o.trace))
+        for r in (res[t], gres[t]):
+            assert r.best_energy == o.best_energy
+            assert np.array_equal(bits(r.trace_energy), bits(o.trace))
+            assert np.array_equal(r.best_state, o.best_state)
 
 
 @pytest.mark.parametrize("exchange", ["p2p", "direct"])
