@@ -131,6 +131,9 @@ int ssqa_problem_count(ssqa_problem prob);
 int ssqa_problem_create_dense(int n, int kind, uint64_t seed, int device, ssqa_problem* out);
 int ssqa_problem_create_gi(int count, int n_nodes, double edge_prob, const uint64_t* seeds,
                            int permute, double c1, double c2, int device, ssqa_problem* out);
+/* The all-zero n-spin problem (h = 0, J = 0, offset 0), made on the device:
+ * what init_lattice / lattice-only batches need without uploading a model. */
+int ssqa_problem_create_zero(int n, int device, ssqa_problem* out);
 /* Device image of a problem: J' int8 [count*npad][npad], H' int32 [count*npad],
  * offsets [count] (any pointer may be NULL). */
 int ssqa_problem_export(ssqa_problem prob, int8_t* J, int32_t* H, double* offsets);

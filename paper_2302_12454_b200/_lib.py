@@ -62,6 +62,7 @@ SIGNATURES = [
     ("ssqa_problem_create_dense", C.c_int, [C.c_int, C.c_int, C.c_uint64, C.c_int, C.c_void_p]),
     ("ssqa_problem_create_gi", C.c_int, [C.c_int, C.c_int, C.c_double, C.c_void_p, C.c_int,
                                          C.c_double, C.c_double, C.c_int, C.c_void_p]),
+    ("ssqa_problem_create_zero", C.c_int, [C.c_int, C.c_int, C.c_void_p]),
     ("ssqa_problem_export", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     ("ssqa_gi_compact", C.c_int, [C.c_int, C.c_double, C.c_uint64, C.c_int, C.c_double,
                                   C.c_double, C.c_void_p, C.c_void_p, C.c_void_p]),

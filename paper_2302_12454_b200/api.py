@@ -230,6 +230,15 @@ class Problem:
         return self
 
     @classmethod
+    def zero(cls, n: int, device: int = 0) -> "Problem":
+        """All-zero n-spin problem made on the device (ssqa_problem_create_zero)."""
+        self = cls.__new__(cls)
+        self.n = n
+        self._h = C.c_void_p()
+        check(lib().ssqa_problem_create_zero(n, device, C.byref(self._h)))
+        return self
+
+    @classmethod
     def generated_dense(cls, n: int, kind: int, seed: int, device: int = 0) -> "Problem":
         """BASELINE C4 / C5 model built on the device (ssqa_problem_create_dense):
         the same quantized problem as Problem(dense_ising(n, kind, seed))."""
@@ -537,7 +546,7 @@ class ReplicaLattice:
 def init_lattice(n: int, replicas: int, delay: int, seed: int,
                  engine: int = ENGINE_AUTO) -> ReplicaLattice:
     """annealer.cpp:432-447, evaluated by the device init kernel."""
-    prob = Problem(IsingModel(n))
+    prob = Problem.zero(n)
     p = SsqaParams(r=replicas, delay=delay, sc=1)
     b = Batch(prob, p, 1, engine=engine)
     b.set_seeds([seed])

@@ -754,6 +754,33 @@ int ssqa_problem_create_gi(int count, int n_nodes, double edge_prob, const uint6
   return SSQA_OK;
 }
 
+int ssqa_problem_create_zero(int n, int device, ssqa_problem* out) {
+  if (!out) return set_err(SSQA_EINVAL, "null argument");
+  if (n < 1 || n >= kMaxSpins) return set_err(SSQA_EINVAL, "spin count out of range");
+  auto* pr = new ssqa_problem_s();
+  Quantized& q = pr->q;
+  q.n = n;
+  q.npad = (n + 127) / 128 * 128;
+  q.fp4_ok = true;  // all-zero couplings are e2m1-exact
+  pr->device = device;
+  const size_t np2 = size_t(q.npad) * q.npad;
+  cudaError_t e = cudaSetDevice(device);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&pr->stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = pmalloc(&pr->d_J, np2);
+  if (e == cudaSuccess) e = pmalloc(&pr->d_J4, np2 / 2);
+  if (e == cudaSuccess) e = pmalloc(&pr->d_H, size_t(q.npad) * sizeof(int32_t));
+  if (e == cudaSuccess) e = cudaMemsetAsync(pr->d_J, 0, np2, pr->stream);
+  if (e == cudaSuccess) e = cudaMemsetAsync(pr->d_J4, 0, np2 / 2, pr->stream);
+  if (e == cudaSuccess) e = cudaMemsetAsync(pr->d_H, 0, size_t(q.npad) * sizeof(int32_t), pr->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(pr->stream);
+  if (e != cudaSuccess) {
+    ssqa_problem_destroy(pr);
+    return set_err(SSQA_ECUDA, std::string("problem allocation: ") + cudaGetErrorString(e));
+  }
+  *out = pr;
+  return SSQA_OK;
+}
+
 int ssqa_problem_export(ssqa_problem pr, int8_t* J, int32_t* H, double* offsets) {
   if (!pr) return set_err(SSQA_EINVAL, "null problem");
   CU(cudaSetDevice(pr->device));

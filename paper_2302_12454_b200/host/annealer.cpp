@@ -116,10 +116,11 @@ const std::vector<double>& ReplicaLattice::delayed_sigma() const {
 }
 
 ReplicaLattice init_lattice(int n, int replicas, int delay, uint64_t seed) {
-  // The device init kernel needs a problem handle; any n-spin model does.
-  IsingModel blank(n);
+  // The device init kernel needs a problem handle; an all-zero n-spin problem
+  // made on the device does (no host model, no upload).
+  if (n < 1) throw std::invalid_argument("init_lattice needs n >= 1");
   ProblemHandle ph;
-  upload(blank, 0, ph);
+  check(ssqa_problem_create_zero(n, 0, &ph.p));
   SsqaParams p;
   p.r = replicas;
   p.delay = delay;
