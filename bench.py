@@ -155,11 +155,18 @@ class ClockSampler:
 
 
 def peaks():
+    """(HBM GB/s, bf16 TF/s for the tensor roofline, label, bf16 burst TF/s).
+    The fused sweep kernel is ONE launch of the whole job (0.5-1.2 s at the
+    BASELINE configs): the measured SUSTAINED bf16 figure applies to a kernel
+    timed inside a long step (MEASURED_PEAKS.json; the burst one is kept
+    beside it).  HBM has a single measured copy bandwidth."""
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(path):
         d = json.load(open(path))
-        return d.get("hbm_gbs", 6650.0), d.get("bf16_tflops", 1590.0), "measured"
-    return 6650.0, 1590.0, "fallback"
+        burst = d.get("bf16_tflops", 1590.0)
+        return (d.get("hbm_gbs", 6650.0), d.get("bf16_tflops_sustained", burst),
+                "measured sustained", burst)
+    return 6650.0, 1590.0, "fallback", 1590.0
 
 
 def cpu_model():
@@ -405,7 +412,7 @@ def run_rows(args, cfg):
     clk = clocks.stop()
     step_ms = shard.max_over_ranks(statistics.mean(times), dist, "cuda")
     value = float(N) * R * T * sc / (step_ms * 1e-3)
-    hbm_peak, bf16_peak, peak_kind = peaks()
+    hbm_peak, bf16_peak, peak_kind, bf16_burst = peaks()
     tc_peak = 2.0 * bf16_peak
     ops_rank = 2.0 * N * (N / world) * R * T * (sc + 1)
     tensor_tops = ops_rank / (statistics.mean(times) * 1e-3) / 1e12
@@ -489,7 +496,7 @@ def time_dense_config(name, steps=2, warmup=1):
         times.append(b.elapsed_ms())
     clk = clocks.stop()
     ms = statistics.mean(times)
-    _, bf16_peak, peak_kind = peaks()
+    _, bf16_peak, peak_kind, bf16_burst = peaks()
     op_bits = b.operand_bits
     planes = 2 if (op_bits == 4 and info.get("fp4") == 2) else 1
     tc_mult = 4.0 if op_bits == 4 else 2.0
@@ -503,6 +510,7 @@ def time_dense_config(name, steps=2, warmup=1):
                       "operands": ("fp4 pair" if planes == 2 else "fp4") if op_bits == 4 else "int8"},
            "int8_equiv": {"achieved_tops": i8 / (ms * 1e-3) / 1e12, "peak_tops": 2.0 * bf16_peak,
                           "frac": i8 / (ms * 1e-3) / 1e12 / (2.0 * bf16_peak)},
+           "tensor_frac_vs_burst_peak": ops / (ms * 1e-3) / 1e12 / (tc_mult * bf16_burst),
            "peak_note": f"{peak_kind} bf16 x {tc_mult:g} (operand format) / x 2 (int8)",
            "clocks": clk, "gpu_launches": b.launch_count()}
     b.close()
@@ -576,7 +584,7 @@ def run_ours(args, cfg):
     # int8 ops (tensor bound) and 16 B of accumulator state (f64 read+write)
     # + 0.25 B of packed spins + N/(M*T) B of J streamed once per sweep
     # (HBM bound); the binding one is reported, the other kept beside it.
-    hbm_peak, bf16_peak, peak_kind = peaks()
+    hbm_peak, bf16_peak, peak_kind, bf16_burst = peaks()
     # dense tensor peak of the operand format the kernel streams: int8 = 2x
     # bf16, FP4 (kind::mxf4) = 4x bf16 on B200
     op_bits = b.operand_bits
@@ -609,7 +617,8 @@ def run_ours(args, cfg):
     # this build are under profiles/, see profiles/README.md)
     traffic = None
     tensor = {"achieved": tensor_tops, "peak": tc_peak, "unit": "TOPS",
-              "frac": tensor_tops / tc_peak, "operands": tc_name}
+              "frac": tensor_tops / tc_peak, "operands": tc_name,
+              "frac_vs_burst_peak": tensor_tops / (tc_mult * bf16_burst)}
     # BASELINE.json's target is phrased against the int8 tensor roofline: the
     # algorithmic 2N ops per update (one coupling plane) at the int8 dense peak
     # (2 x bf16), whatever operand format the kernel streams
