@@ -339,6 +339,7 @@ int ssqa_tune_set(const char* key, long value) {
   else if (k == "pf") t.pf = v;
   else if (k == "i16") t.i16 = v;
   else if (k == "rt") t.rt = v;
+  else if (k == "tskip") t.tskip = v;
   else return set_err(SSQA_EINVAL, "ssqa_tune_set: unknown key '" + k + "'");
   return SSQA_OK;
 }

@@ -40,6 +40,7 @@ struct TuneOverrides {
   int i16 = -1;     // 0: refuse the int16 (two-plane int8) coupling path
   int rt = -1;      // 0: no rail-tag epilogue (fused FP4 runs fall back to the FP64 epilogue)
   std::string trace;  // timeline dump path (block 0)
+  int tskip = 0;      // timeline: first row tile recorded
 };
 TuneOverrides& tune();
 

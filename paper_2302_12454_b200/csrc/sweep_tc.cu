@@ -143,6 +143,7 @@ struct TcParams {
   int mc_q;     // CL == 2: column tiles per cluster (= ntiles), sharing each J' tile
   long long* dbg;  // optional timeline (block 0): [role][rt_global][2] clock64 stamps
   int dbg_rts;     // capacity in row tiles
+  int dbg_skip;    // first row tile recorded (tune key "tskip")
   // per-trial results
   double* best_e;
   int* best_k;
@@ -1562,48 +1563,122 @@ __device__ __forceinline__ void epi_v4(const V4Row& r, const FastConsts& fc, con
 //                                       X 2^-p >= 2 i0 + m       -> high rail
 //   any acc in [-i0, i0):               X 2^-p >= 2 i0 + m -> high, < -2 i0 - m -> low
 // whatever the noise draw and the delayed neighbours are (RtThr carries these
-// bounds as integers with 1.0 of margin over every rounding).  Such an update
+// bounds as integers with some margin over every rounding).  Such an update
 // needs no RNG, no FP64 and no accumulator: two tag bits per (row, column) --
 // "on a rail" and "spin negative", eight columns of a row in one u16 -- stand
 // for the accumulator, and the f64 array in HBM is current only where the
 // rail bit is clear.  The undecided updates (C3: 100 % in odd early cycles,
-// ~50 % around cycle 200, 2-6 % past cycle 1000; scripts/decided_probe.py) run
-// the exact arithmetic of epi_v4 afterwards, each lane on its own columns of
-// the chunk: field staged in shared memory, accumulator (only when off the
-// rails) fetched by cp.async during the fast loop, neighbour signs from the
-// delayed FP4 slot.
-// Per-warp staging block of the rail-tag epilogue: fields [8][32] s32,
-// accumulators [8][32] f64, result words [32] u32, entry queue [256] u8.
-constexpr uint32_t kRtXs = 0, kRtAs = 1024, kRtRes = 3072, kRtQueue = 3200, kRtStage = 3584;
+// ~50 % around cycle 200, 2-6 % past cycle 1000, clustered in a few rows;
+// scripts/decided_probe.py) go through a per-warp queue in shared memory --
+// entry = biased field, tile column, row lane, old tag bits; an off-rail
+// accumulator follows by cp.async -- and are worked off 32 at a time by
+// whichever lanes: the exact arithmetic of epi_v4, then the new tag bits and
+// a negative spin are OR-ed into the words the fast path has already stored.
+constexpr uint32_t kRtCap = 320;                  // queue entries per warp (>= 31 + 32 * kCW)
+constexpr uint32_t kRtAcc = kRtCap * 8;           // byte offset of the staged accumulators
+constexpr uint32_t kRtStage = 2 * kRtCap * 8;     // shared bytes per epilogue warp
 struct RtThr {
   int hh, oh;      // X >= hh: high-rail acc stays high; X >= oh: any acc goes high
   int ll, hl, ol;  // X <= ll: low stays low; <= hl: high goes low; <= ol: any goes low
 };
 struct RtRow {
-  uint32_t iG_lo, iG_hi, p4, p32;
+  uint32_t iGb_lo, iGb_hi;  // (global row of warp row 0) * golden
+  uint32_t p4, p32;
   uint32_t h1x;           // h1 - FP4 bias + 2^31 (magic-number conversion of the slow path)
   int h1d;                // h1 - FP4 bias; rows past n: always decided (X = INT_MAX)
   int h2;                 // 2 h1 - FP4 bias (energy)
   uint32_t lut;
   uint32_t e_tmem;
   int e_mode;
-  uint64_t acc_col;       // &acc[col0 * npad + i]
+  uint64_t acc_w0;        // &acc[col0 * npad + i0w]   (i0w: global row of warp row 0)
   uint32_t col_stride32;  // npad * 8
-  uint8_t* dst_w;
+  uint8_t* dst_w;         // spin words of this lane: sig_dst + i0w / 2 + 4 * (lane & 3)
+  uint8_t* dst_w0;        // sig_dst + i0w / 2
   uint32_t nib_live;
   uint32_t jp_hi, jp_lo, hic_hi, loc_hi, rail_lo;
   uint64_t pol;
   RtThr thr;
   uint16_t* tag_row;      // &rt_tags[(col0 / 8) * npad + i]
+  uint16_t* tag_w0;       // &rt_tags[(col0 / 8) * npad + i0w]
   uint32_t npad;
   uint32_t nbt;           // shared: delayed FP4 spin tile [NT][64] of this row tile, byte of warp row 0
   uint32_t wst;           // shared: this warp's staging block (kRtStage bytes)
+  int exp;                // timing ablations: 256 no batches, 512 no accumulator prefetch, 1024 no queue
 };
 
-__device__ __forceinline__ uint32_t ldg_u16(const uint16_t* p) {
+__device__ __forceinline__ uint32_t ldg_u16_cg(const uint16_t* p) {
   uint32_t v;
-  asm volatile("ld.global.u16 %0, [%1];" : "=r"(v) : "l"(p));
+  asm volatile("ld.global.cg.u16 %0, [%1];" : "=r"(v) : "l"(p));
   return v;
+}
+
+// One batch of queued undecided updates: entries [head, head + n), n <= 32.
+template <bool BIDIR>
+__device__ __forceinline__ void rt_batch(const RtRow& r, const FastConsts& fc, const I2D& i2d,
+                                         uint32_t colt, uint32_t head, uint32_t n, int lane) {
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  __syncwarp();
+  if (uint32_t(lane) < n) {
+    uint32_t slot = head + uint32_t(lane);
+    slot = slot >= kRtCap ? slot - kRtCap : slot;
+    uint32_t xb0, meta;
+    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(xb0), "=r"(meta) : "r"(r.wst + slot * 8u));
+    const bool rl = (meta & 1u) != 0u, ng = (meta & 2u) != 0u;
+    const uint32_t rw = (meta >> 2) & 31u;   // row lane
+    const uint32_t cj = meta >> 8;           // tile column
+    const uint32_t ce = colt + cj * uint32_t(sizeof(ColTab));
+    const uint64_t cbase = lds_u64(ce);
+    uint32_t coff, nbr;
+    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(coff), "=r"(nbr) : "r"(ce + 8u));
+    // row * golden = (row 0 of the warp) * golden + rw * golden
+    uint32_t g_lo, g_hi;
+    asm("{\n\t.reg .u64 w;\n\tmul.wide.u32 w, %2, 0x7f4a7c15;\n\tmov.b64 {%0, %1}, w;\n\t"
+        "mad.lo.u32 %1, %2, 0x9e3779b9, %1;\n\t"
+        "add.cc.u32 %0, %0, %3;\n\taddc.u32 %1, %1, %4;\n\t}"
+        : "=r"(g_lo), "=r"(g_hi)
+        : "r"(rw), "r"(r.iGb_lo), "r"(r.iGb_hi));
+    // delayed neighbours: nbr holds their byte offsets into the spin tile
+    // (64 bytes per column); rows of a warp start at a multiple of 32
+    const uint32_t nb_r = r.nbt + (rw >> 1);
+    const uint32_t nb_sh = 28u - 4u * (rw & 1u);
+    const uint32_t bu = lds_u8(nb_r + (nbr & 0xffffu));
+    uint32_t bd = 0;
+    if (BIDIR) bd = lds_u8(nb_r + ((nbr >> 16) & 0x7fffu));
+    const uint32_t t5 = noise_top5_v4(cbase, g_lo, g_hi, r.p4, r.p32);
+    const uint32_t xb = xb0 + uint32_t(lds_s8(r.lut + t5));
+    double input = __dsub_rn(__hiloint2double(int(i2d.magic_hi), int(xb)), i2d.magic);
+    input = __dadd_rn(input, __hiloint2double(int(r.jp_hi ^ ((bu << nb_sh) & 0x80000000u)),
+                                              int(r.jp_lo)));
+    if (BIDIR)
+      input = __dadd_rn(input, __hiloint2double(int(r.jp_hi ^ ((bd << nb_sh) & 0x80000000u)),
+                                                int(r.jp_lo)));
+    const double a_old = rl ? __hiloint2double(int(ng ? r.loc_hi : r.hic_hi), int(r.rail_lo))
+                            : lds_f64(r.wst + kRtAcc + slot * 8u);
+    const double sd = __dadd_rn(a_old, input);
+    const bool p_lo = sd < fc.lo_clamp, p_hi = sd >= fc.i0;
+    const bool clamped = p_hi || p_lo;
+    const int nhi = p_hi ? int(r.hic_hi) : (p_lo ? int(r.loc_hi) : __double2hiint(sd));
+    const int nlo = clamped ? int(r.rail_lo) : __double2loint(sd);
+    if (!clamped) {
+      uint64_t addr;
+      asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(addr) : "r"(cj), "r"(r.col_stride32), "l"(r.acc_w0));
+      st_f64_if(reinterpret_cast<double*>(addr + rw * 8u), __hiloint2double(nhi, nlo), true, r.pol);
+    }
+    const uint32_t bits = (clamped ? 1u : 0u) | (nhi < 0 ? 2u : 0u);
+    if (bits) {
+      // tag: u16 [chunk][row]; two rows share the u32 the OR goes to
+      const uint16_t* tw = r.tag_w0 + size_t(cj >> 3) * r.npad + (rw & ~1u);
+      asm volatile("red.global.or.b32 [%0], %1;" ::"l"(tw),
+                   "r"(bits << (2u * (cj & 7u) + 16u * (rw & 1u)))
+                   : "memory");
+    }
+    if (nhi < 0) {
+      // spin: e2m1 -1 = 0xA over the +1 = 0x2 the fast path stored
+      asm volatile("red.global.or.b32 [%0], %1;" ::"l"(r.dst_w0 + (coff >> 1) + (rw >> 3) * 4u),
+                   "r"(8u << (4u * (rw & 7u)))
+                   : "memory");
+    }
+  }
 }
 
 template <bool BIDIR>
@@ -1613,7 +1688,9 @@ __device__ __forceinline__ void epi_rt(const RtRow& r, const FastConsts& fc, con
                                        int nchunk, int lane, uint32_t& tag_next) {
   const int wj = lane >> 2;
   const uint32_t colt = smem_u32(c_col);
+  const uint32_t lt = (1u << lane) - 1u;
   uint32_t tcur = tag_next;
+  uint32_t head = 0, qn = 0;  // queue: entries [head, head + qn) mod kRtCap (warp-uniform)
   for (int ch = sub; ch < nchunk; ch += nsubs) {
     const int cb = ch * kCW;
     int32_t v[kCW], e[kCW];
@@ -1624,151 +1701,59 @@ __device__ __forceinline__ void epi_rt(const RtRow& r, const FastConsts& fc, con
       for (int j = 0; j < kCW; ++j) e[j] = 0;
     const uint32_t told = tcur;
     // tags of this warp's next chunk: same row tile, else the first chunk of
-    // the next row tile (rows + 128; past the last tile the load stays inside
-    // the array or is skipped by the caller's bound)
+    // the next row tile (rows + 128; unused past the last tile, the array has slack)
     {
       const int chn = ch + nsubs;
       const uint16_t* tp = chn < nchunk ? r.tag_row + size_t(chn) * r.npad
                                         : r.tag_row + size_t(sub) * r.npad + kBM;
-      tcur = ldg_u16(tp);
+      tcur = ldg_u16_cg(tp);
     }
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
     const uint32_t umask = c_umask[ch];
-    uint32_t tnew = told, mund = 0;
+    uint32_t tnew = told;
+    const uint32_t meta0 = (uint32_t(cb) << 8) | (uint32_t(lane) << 2);
 #pragma unroll
     for (int j = 0; j < kCW; ++j) {
       const int Sb = __float_as_int(__int_as_float(v[j]) + 12582912.0f);
       const int X = Sb + r.h1d;
       const int s2 = Sb + r.h2;
-      const bool rl = (told & (1u << (2 * j))) != 0u;
-      const bool ng = (told & (2u << (2 * j))) != 0u;
+      const uint32_t st2 = (told >> (2 * j)) & 3u;
+      const bool rl = (st2 & 1u) != 0u;
+      const bool ng = (st2 & 2u) != 0u;
       e[j] += ng ? -s2 : s2;
-      const int thi = (rl && !ng) ? r.thr.hh : r.thr.oh;
+      const int thi = st2 == 1u ? r.thr.hh : r.thr.oh;
       const int tlo = rl ? (ng ? r.thr.ll : r.thr.hl) : r.thr.ol;
       const bool dhi = X >= thi, dlo = X <= tlo;
       if ((umask >> j) & 1u) {  // warp-uniform: the column updates this cycle
-        tnew &= ~(3u << (2 * j));
-        if (dhi) tnew |= 1u << (2 * j);
-        if (dlo) tnew |= 3u << (2 * j);
-        if (!(dhi || dlo)) {
-          mund |= 1u << j;
-          asm volatile("st.shared.u32 [%0], %1;" ::"r"(r.wst + kRtXs + uint32_t(j) * 128u + uint32_t(lane) * 4u), "r"(Sb) : "memory");
-          if (!rl) {
-            uint64_t addr;
-            asm("mad.wide.u32 %0, %1, %2, %3;"
-                : "=l"(addr)
-                : "r"(uint32_t(cb + j)), "r"(r.col_stride32), "l"(r.acc_col));
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(r.wst + kRtAs + uint32_t(j) * 256u + uint32_t(lane) * 8u),
-                         "l"(addr)
-                         : "memory");
-          }
+        // decided: rail bit, sign of the rail; undecided: 0 until its batch
+        tnew = (tnew & ~(3u << (2 * j))) | (dhi ? (1u << (2 * j)) : 0u) | (dlo ? (3u << (2 * j)) : 0u);
+        const bool und = !(dhi || dlo);
+        const uint32_t bj = __ballot_sync(0xffffffffu, und);
+        if (bj && !(r.exp & 1024)) {  // warp-uniform
+          uint32_t pos = head + qn + uint32_t(__popc(bj & lt));
+          pos = pos >= kRtCap ? pos - kRtCap : pos;
+          const uint32_t sa = r.wst + pos * 8u;
+          uint64_t ga;
+          asm("mad.wide.u32 %0, %1, %2, %3;"
+              : "=l"(ga)
+              : "r"(uint32_t(cb + j)), "r"(r.col_stride32), "l"(r.acc_w0 + uint64_t(lane) * 8u));
+          asm volatile(
+              "{\n\t.reg .pred pu, pa;\n\t"
+              "setp.ne.b32 pu, %0, 0;\n\t"
+              "setp.ne.b32 pa, %1, 0;\n\t"
+              "@pu st.shared.v2.u32 [%2], {%3, %4};\n\t"
+              "@pa cp.async.ca.shared.global [%5], [%6], 8;\n\t}" ::"r"(int(und)),
+              "r"(int(und && !rl && !(r.exp & 512))), "r"(sa), "r"(uint32_t(Sb) + r.h1x),
+              "r"(meta0 + (uint32_t(j) << 8) + st2), "r"(sa + kRtAcc), "l"(ga)
+              : "memory");
+          qn += uint32_t(__popc(bj));
         }
       }
-    }
-    // ---- undecided updates: exact arithmetic, compacted across the warp.
-    // They cluster in a few rows (a frustrated spin is undecided in most of
-    // its replicas), so each one is handed to any lane: up to four rows as
-    // (row slot, column) = (lane / 8, lane % 8), otherwise through a byte
-    // queue of (column << 5 | row lane) entries.  The row's constants come by
-    // shuffle, its staged field / accumulator from shared memory, and the
-    // new tag bits go back through an OR into the row's result word.
-    const uint32_t rb = __ballot_sync(0xffffffffu, mund != 0u);
-    if (rb) {
-      asm volatile("cp.async.wait_all;" ::: "memory");
-      asm volatile("st.shared.u32 [%0], %1;" ::"r"(r.wst + kRtRes + uint32_t(lane) * 4u), "r"(0u) : "memory");
-      const int nrows = __popc(rb);
-      int total = 0;
-      if (nrows > 4) {
-        // queue: per column, the undecided lanes take consecutive entries
-#pragma unroll
-        for (int j = 0; j < kCW; ++j) {
-          const bool mine = (mund >> j) & 1u;
-          const uint32_t bj = __ballot_sync(0xffffffffu, mine);
-          const uint32_t pos = uint32_t(total) + uint32_t(__popc(bj & ((1u << lane) - 1u)));
-          if (mine)
-            asm volatile("st.shared.u8 [%0], %1;" ::"r"(r.wst + kRtQueue + pos),
-                         "r"(uint32_t(j << 5) | uint32_t(lane))
-                         : "memory");
-          total += __popc(bj);
-        }
-      }
-      __syncwarp();
-      const int niter = nrows > 4 ? (total + 31) >> 5 : 1;
-      for (int itq = 0; itq < niter; ++itq) {
-        uint32_t rr, jj;
-        bool act;
-        if (nrows > 4) {
-          const int qi = itq * 32 + lane;
-          act = qi < total;
-          const uint32_t en = act ? lds_u8(r.wst + kRtQueue + uint32_t(qi)) : 0u;
-          rr = en & 31u;
-          jj = en >> 5;
-        } else {
-          // rows = the set bits of rb in order; slot lane / 8 takes the
-          // (lane / 8)-th of them
-          uint32_t m = rb;
-          const int slot = lane >> 3;
-          if (slot >= 1) m &= m - 1u;
-          if (slot >= 2) m &= m - 1u;
-          if (slot >= 3) m &= m - 1u;
-          rr = m ? uint32_t(__ffs(int(m)) - 1) : 0u;
-          jj = uint32_t(lane) & 7u;
-          const uint32_t mr = __shfl_sync(0xffffffffu, mund, int(rr));
-          act = slot < nrows && ((mr >> jj) & 1u);
-        }
-        const uint32_t t_r = __shfl_sync(0xffffffffu, told, int(rr));
-        const uint32_t h1x_r = __shfl_sync(0xffffffffu, r.h1x, int(rr));
-        const uint32_t iGl_r = __shfl_sync(0xffffffffu, r.iG_lo, int(rr));
-        const uint32_t iGh_r = __shfl_sync(0xffffffffu, r.iG_hi, int(rr));
-        if (act) {
-          const uint32_t sh = 2u * jj;
-          const bool rl = ((t_r >> sh) & 1u) != 0u, ng = ((t_r >> sh) & 2u) != 0u;
-          const uint32_t cj = uint32_t(cb) + jj;
-          const uint32_t ce = colt + cj * uint32_t(sizeof(ColTab));
-          const uint64_t cbase = lds_u64(ce);
-          uint32_t nbr;
-          asm volatile("ld.shared.u32 %0, [%1];" : "=r"(nbr) : "r"(ce + 12u));
-          // delayed neighbours: nbr holds their byte offsets into the spin tile
-          // (64 bytes per column); rows of a warp start at a multiple of 32
-          const uint32_t nb_r = r.nbt + (rr >> 1);
-          const uint32_t nb_sh = 28u - 4u * (rr & 1u);
-          const uint32_t bu = lds_u8(nb_r + (nbr & 0xffffu));
-          uint32_t bd = 0;
-          if (BIDIR) bd = lds_u8(nb_r + ((nbr >> 16) & 0x7fffu));
-          int Sb;
-          asm volatile("ld.shared.s32 %0, [%1];" : "=r"(Sb) : "r"(r.wst + kRtXs + jj * 128u + rr * 4u));
-          const uint32_t t5 = noise_top5_v4(cbase, iGl_r, iGh_r, r.p4, r.p32);
-          const uint32_t xb = uint32_t(Sb) + h1x_r + uint32_t(lds_s8(r.lut + t5));
-          double input = __dsub_rn(__hiloint2double(int(i2d.magic_hi), int(xb)), i2d.magic);
-          input = __dadd_rn(input, __hiloint2double(int(r.jp_hi ^ ((bu << nb_sh) & 0x80000000u)),
-                                                    int(r.jp_lo)));
-          if (BIDIR)
-            input = __dadd_rn(input, __hiloint2double(int(r.jp_hi ^ ((bd << nb_sh) & 0x80000000u)),
-                                                      int(r.jp_lo)));
-          const double a_old = rl ? __hiloint2double(int(ng ? r.loc_hi : r.hic_hi), int(r.rail_lo))
-                                  : lds_f64(r.wst + kRtAs + jj * 256u + rr * 8u);
-          const double sd = __dadd_rn(a_old, input);
-          const bool p_lo = sd < fc.lo_clamp, p_hi = sd >= fc.i0;
-          const int nhi = p_hi ? int(r.hic_hi) : (p_lo ? int(r.loc_hi) : __double2hiint(sd));
-          const int nlo = (p_hi || p_lo) ? int(r.rail_lo) : __double2loint(sd);
-          if (!(p_hi || p_lo)) {
-            uint64_t addr;
-            asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(addr) : "r"(cj), "r"(r.col_stride32), "l"(r.acc_col));
-            addr += uint64_t(int64_t(int(rr) - lane) * 8);
-            st_f64_if(reinterpret_cast<double*>(addr), __hiloint2double(nhi, nlo), true, r.pol);
-          }
-          const uint32_t bits = (((p_hi || p_lo) ? 1u : 0u) | (nhi < 0 ? 2u : 0u)) << sh;
-          asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(r.wst + kRtRes + rr * 4u), "r"(bits) : "memory");
-        }
-      }
-      __syncwarp();
-      uint32_t got;
-      asm volatile("ld.shared.u32 %0, [%1];" : "=r"(got) : "r"(r.wst + kRtRes + uint32_t(lane) * 4u) : "memory");
-      tnew |= got;
     }
     if (umask) {
       asm volatile("st.global.u16 [%0], %1;" ::"l"(r.tag_row + size_t(ch) * r.npad),
-                   "h"(static_cast<unsigned short>(tnew)));
+                   "h"(static_cast<unsigned short>(tnew))
+                   : "memory");
     }
     {
       uint32_t ball[kCW];
@@ -1780,12 +1765,23 @@ __device__ __forceinline__ void epi_rt(const RtRow& r, const FastConsts& fc, con
       const uint32_t mm = (wj & 4) ? b1 : b0;
       const uint32_t word = nibbles_pm1((mm >> (8 * (lane & 3))) & 0xffu) & r.nib_live;
       const uint32_t coffw = c_col[cb + wj].off;
-      st_u32_if(reinterpret_cast<uint32_t*>(r.dst_w + (coffw >> 1)), word,
-                ((umask >> wj) & 1u) && r.nib_live);
+      asm volatile(
+          "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t"
+          "@q st.global.u32 [%0], %1;\n\t}" ::"l"(r.dst_w + (coffw >> 1)),
+          "r"(word), "r"(int(((umask >> wj) & 1u) && r.nib_live))
+          : "memory");
     }
     if (r.e_mode == 1 || r.e_mode == 2) tmem_st8(r.e_tmem + uint32_t(cb), e);
     else reduce8_to_quarter(e, q_sum, cb, lane);
+    // work off the full batches
+    while (qn >= 32u) {
+      if (!(r.exp & 256)) rt_batch<BIDIR>(r, fc, i2d, colt, head, 32u, lane);
+      head += 32u;
+      head = head >= kRtCap ? head - kRtCap : head;
+      qn -= 32u;
+    }
   }
+  if (qn && !(r.exp & 256)) rt_batch<BIDIR>(r, fc, i2d, colt, head, qn, lane);
   tag_next = tcur;
 }
 
@@ -1830,8 +1826,9 @@ __device__ __forceinline__ void expand_best_state(const TcParams& P, int trial, 
 // ready, -).  Block 0, lane 0 only; no cost when P.dbg is null.
 #define DBG_STAMP(role, rtg, which)                                                    \
   do {                                                                                 \
-    if (P.dbg && blockIdx.x == 0 && lane == 0 && int(rtg) < P.dbg_rts)                 \
-      P.dbg[(size_t(role) * P.dbg_rts + (rtg)) * 2 + (which)] = clock64();            \
+    if (P.dbg && blockIdx.x == 0 && lane == 0 && int(rtg) >= P.dbg_skip &&            \
+        int(rtg) - P.dbg_skip < P.dbg_rts)                                             \
+      P.dbg[(size_t(role) * P.dbg_rts + ((rtg) - P.dbg_skip)) * 2 + (which)] = clock64(); \
   } while (0)
 
 // Registers per thread after setmaxnreg: control warpgroup / epilogue
@@ -2562,7 +2559,7 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
         // rail-tag epilogue: tags of this warp's first chunk (the later ones
         // are prefetched chunk by chunk)
         if (rt_mode && rt == 0)
-          rt_tag = ldg_u16(P.rt_tags + (size_t(col0 / kCW) + size_t(sub)) * g.npad + i);
+          rt_tag = ldg_u16_cg(P.rt_tags + (size_t(col0 / kCW) + size_t(sub)) * g.npad + i);
         mbar_wait(&ctl->sfull[buf], aph);
         mbar_wait(&ctl->tfull[buf], aph);
         tc_fence_after();
@@ -2638,8 +2635,10 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
           if constexpr (F4) {
             if (rt_mode) {
               RtRow rr;
-              rr.iG_lo = er.iG_lo;
-              rr.iG_hi = er.iG_hi;
+              const int i0w = (rt_lo + rt) * kBM + q * 32;  // global row of warp row 0
+              const uint64_t iGb = uint64_t(i0w) * kGolden;
+              rr.iGb_lo = uint32_t(iGb);
+              rr.iGb_hi = uint32_t(iGb >> 32);
               rr.p4 = er.p4;
               rr.p32 = er.p32;
               rr.h1x = er.h1x;
@@ -2648,9 +2647,10 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
               rr.lut = smem_u32(ctl->nz_lut);
               rr.e_tmem = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(2 * acc_cols);
               rr.e_mode = (!e_tmem || NRT == 1) ? 0 : (rt == 0 ? 1 : (rt == NRT - 1 ? 3 : 2));
-              rr.acc_col = reinterpret_cast<uint64_t>(P.acc + size_t(col0) * g.npad + i);
+              rr.acc_w0 = reinterpret_cast<uint64_t>(P.acc + size_t(col0) * g.npad + i0w);
               rr.col_stride32 = uint32_t(g.npad) * 8u;
               rr.dst_w = er.dst_w;
+              rr.dst_w0 = sig_dst + i0w / 2;
               rr.nib_live = er.nib_live;
               rr.jp_hi = fc.jp_hi;
               rr.jp_lo = fc.jp_lo;
@@ -2659,11 +2659,13 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
               rr.rail_lo = uint32_t(__double2loint(fc.hi_clamp));  // == loc's (fast_ok)
               rr.pol = pol_first;
               rr.thr = rthr;
-              rr.tag_row = P.rt_tags + size_t(col0 / kCW) * g.npad + i;
+              rr.tag_w0 = P.rt_tags + size_t(col0 / kCW) * g.npad + i0w;
+              rr.tag_row = rr.tag_w0 + lane;
               rr.npad = uint32_t(g.npad);
               rr.nbt = smem_u32(stile) + uint32_t(q) * 16u;
               // per-warp staging inside the (unused) accumulator ring
               rr.wst = smem_u32(acc_ring) + uint32_t(ew) * kRtStage;
+              rr.exp = P.exp_flags;
               if (bidir) epi_rt<true>(rr, fc, i2d, c_col, ctl->umask, q_sum, trow, sub, kSubs, nchunk,
                                       lane, rt_tag);
               else epi_rt<false>(rr, fc, i2d, c_col, ctl->umask, q_sum, trow, sub, kSubs, nchunk,
@@ -3298,7 +3300,7 @@ int launch(ssqa_batch_s* b, TcParams& P, bool f4) {
   P.rt = 0;
   if (f4 && P.run_mode == 1 && P.fast && g.rs == 1 && !P.i16 && P.use_tab == 0 && P.rails_lo &&
       !P.i0_tab && !P.npeer && !std::signbit(P.hi_clamp) && P.hi_clamp < P.i0 && g.ccols % kCW == 0 &&
-      P.exp_flags == 0 && tune().rt != 0) {
+      (P.exp_flags & ~0x700) == 0 && tune().rt > 0) {
     const size_t bytes = size_t(g.ccols / kCW) * g.npad * 2 + 512;
     if (b->rt_bytes < bytes) {
       if (b->d_rt_tags) {
@@ -3442,6 +3444,7 @@ int launch(ssqa_batch_s* b, TcParams& P, bool f4) {
     cudaMemsetAsync(dbg, 0, sizeof(long long) * 4 * dbg_rts * 2, b->prob->stream);
     P.dbg = dbg;
     P.dbg_rts = dbg_rts;
+    P.dbg_skip = tune().tskip;
   }
   cudaError_t e;
   // one persistent CTA per (column tile, row part); every CTA must be

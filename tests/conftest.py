@@ -32,9 +32,14 @@ _ensure_built()
 
 @pytest.fixture(autouse=True)
 def _reset_engine_tune():
-    """Engine overrides (include/ssqa_tune.h) never leak from one test into the next."""
-    yield
+    """Engine overrides (include/ssqa_tune.h) never leak from one test into the next.
+    SSQA_TEST_TUNE="key=v,key=v" runs every test on top of those overrides (e.g.
+    the whole GPU suite through an opt-in engine path)."""
     import paper_2302_12454_b200 as sq
+    base = os.environ.get("SSQA_TEST_TUNE", "")
+    if base:
+        sq.tune(**{k: int(v) for k, v in (kv.split("=") for kv in base.split(","))})
+    yield
     sq.tune()
 
 
