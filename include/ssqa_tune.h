@@ -13,7 +13,7 @@
  *   "epi" 12 or 16 epilogue warps              "cta2"   0 disables CTA pairs
  *   "mc" 1 J' multicast clusters               "stages" / "nps" smem ring shape
  *   "exp" ablation bits                        "pf"     J' L2 prefetch distance
- *   "i16" 0 refuses the int16 two-plane path    "rt"     0 no rail-tag epilogue
+ *   "i16" 0 refuses the int16 two-plane path    "tskip"  timeline: first row tile recorded
  */
 #ifndef SSQA_TUNE_H
 #define SSQA_TUNE_H

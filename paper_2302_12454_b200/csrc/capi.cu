@@ -338,7 +338,6 @@ int ssqa_tune_set(const char* key, long value) {
   else if (k == "exp") t.exp = v;
   else if (k == "pf") t.pf = v;
   else if (k == "i16") t.i16 = v;
-  else if (k == "rt") t.rt = v;
   else if (k == "tskip") t.tskip = v;
   else return set_err(SSQA_EINVAL, "ssqa_tune_set: unknown key '" + k + "'");
   return SSQA_OK;
@@ -1024,7 +1023,7 @@ int ssqa_batch_destroy(ssqa_batch b) {
   if (!b) return SSQA_OK;
   cudaSetDevice(b->prob->device);
   cudaStreamSynchronize(b->prob->stream);
-  for (void* ptr : {(void*)b->d_sig, (void*)b->d_sig4, (void*)b->d_acc, (void*)b->d_seeds, (void*)b->d_jperp, (void*)b->d_i0, b->d_split, b->d_rt_tags,
+  for (void* ptr : {(void*)b->d_sig, (void*)b->d_sig4, (void*)b->d_acc, (void*)b->d_seeds, (void*)b->d_jperp, (void*)b->d_i0, b->d_split,
                     (void*)b->d_S, (void*)b->d_E, (void*)b->d_best_e, (void*)b->d_best_k,
                     (void*)b->d_reached, (void*)b->d_first_hit, (void*)b->d_cycles_used,
                     (void*)b->d_active, (void*)b->d_best_state, (void*)b->d_best_packed,

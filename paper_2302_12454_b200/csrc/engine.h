@@ -38,7 +38,6 @@ struct TuneOverrides {
   int exp = 0;      // ablation experiment bits (TcParams::exp_flags)
   int pf = 0;       // J' L2 prefetch distance
   int i16 = -1;     // 0: refuse the int16 (two-plane int8) coupling path
-  int rt = -1;      // 0: no rail-tag epilogue (fused FP4 runs fall back to the FP64 epilogue)
   std::string trace;  // timeline dump path (block 0)
   int tskip = 0;      // timeline: first row tile recorded
 };
@@ -142,9 +141,6 @@ struct ssqa_batch_s {
   //   pass stamps, arrive [ntiles] pass arrivals, scan [ntiles] scan stamps
   void* d_split = nullptr;
   size_t split_bytes = 0;
-  // rail-tag epilogue (sweep_tc.cu epi_rt): u16 tags [ccols / 8][npad] (+ slack)
-  void* d_rt_tags = nullptr;
-  size_t rt_bytes = 0;
   // GPU row shard (ssqa_batch_set_shard): this batch updates row tiles
   // [shard * nrt / nshards, (shard + 1) * nrt / nshards) of every column
   int shard = 0, nshards = 1;

@@ -134,12 +134,6 @@ struct TcParams {
   unsigned* push_ctr;
   int use_tab;  // fast mode: table epilogue (row splits) instead of update_fast2
   int rails_lo; // the clamp rails i0 - alpha and -i0 share their low word (every cycle)
-  // Rail-tag epilogue (epi_rt; fused FP4 runs without a row split): per
-  // (row, column) two tag bits -- accumulator sits on a clamp rail, spin is
-  // negative -- in rt_tags [ccols / 8][npad] (u16: eight columns of one row);
-  // the f64 accumulator in HBM is current only where the rail bit is clear.
-  int rt;
-  uint16_t* rt_tags;
   int mc_q;     // CL == 2: column tiles per cluster (= ntiles), sharing each J' tile
   long long* dbg;  // optional timeline (block 0): [role][rt_global][2] clock64 stamps
   int dbg_rts;     // capacity in row tiles
@@ -173,7 +167,6 @@ __host__ __device__ inline int tab_bytes_of(const TcParams& P) {
 // neighbour-sign bytes (128 per plane, a second plane when bidirectional).
 __host__ __device__ inline int sig_tile_row(const TcParams& P, bool f4) {
   // (plus half a TMA tile per buffer: one staging tile for the copier warp)
-  if (P.rt) return f4 ? 64 : 128;  // rail-tag epilogue: the plain TMA-loaded spin rows
   if (P.fast && P.g.rs == 1 && !P.i16 && ((P.use_tab == 0 && P.rails_lo) || P.use_tab == 2))
     return 128 * (P.bidirectional ? 2 : 1) + (f4 ? 32 : 64);
   return f4 ? 64 : 128;
@@ -1552,239 +1545,6 @@ __device__ __forceinline__ void epi_v4(const V4Row& r, const FastConsts& fc, con
   }
 }
 
-// ---- Rail-tag epilogue (fused FP4 runs without a row split) ---------------
-// Most updates of a run are decided by the integer field alone.  With
-// X = S + H' the scaled field, in = X 2^-p + n_rnd nz + jperp u [+ jperp d]
-// and |n_rnd nz + jperp (u [+ d])| <= m = n_rnd + nb |jperp|, the reference's
-// update (annealer.cpp:269-295) gives
-//   acc on the high rail (i0 - alpha):  X 2^-p >= alpha + m      -> stays high
-//                                       X 2^-p <  -(2 i0 - alpha) - m -> low rail
-//   acc on the low rail (-i0):          X 2^-p <  -m             -> stays low
-//                                       X 2^-p >= 2 i0 + m       -> high rail
-//   any acc in [-i0, i0):               X 2^-p >= 2 i0 + m -> high, < -2 i0 - m -> low
-// whatever the noise draw and the delayed neighbours are (RtThr carries these
-// bounds as integers with some margin over every rounding).  Such an update
-// needs no RNG, no FP64 and no accumulator: two tag bits per (row, column) --
-// "on a rail" and "spin negative", eight columns of a row in one u16 -- stand
-// for the accumulator, and the f64 array in HBM is current only where the
-// rail bit is clear.  The undecided updates (C3: 100 % in odd early cycles,
-// ~50 % around cycle 200, 2-6 % past cycle 1000, clustered in a few rows;
-// scripts/decided_probe.py) go through a per-warp queue in shared memory --
-// entry = biased field, tile column, row lane, old tag bits; an off-rail
-// accumulator follows by cp.async -- and are worked off 32 at a time by
-// whichever lanes: the exact arithmetic of epi_v4, then the new tag bits and
-// a negative spin are OR-ed into the words the fast path has already stored.
-constexpr uint32_t kRtCap = 320;                  // queue entries per warp (>= 31 + 32 * kCW)
-constexpr uint32_t kRtAcc = kRtCap * 8;           // byte offset of the staged accumulators
-constexpr uint32_t kRtStage = 2 * kRtCap * 8;     // shared bytes per epilogue warp
-struct RtThr {
-  int hh, oh;      // X >= hh: high-rail acc stays high; X >= oh: any acc goes high
-  int ll, hl, ol;  // X <= ll: low stays low; <= hl: high goes low; <= ol: any goes low
-};
-struct RtRow {
-  uint32_t iGb_lo, iGb_hi;  // (global row of warp row 0) * golden
-  uint32_t p4, p32;
-  uint32_t h1x;           // h1 - FP4 bias + 2^31 (magic-number conversion of the slow path)
-  int h1d;                // h1 - FP4 bias; rows past n: always decided (X = INT_MAX)
-  int h2;                 // 2 h1 - FP4 bias (energy)
-  uint32_t lut;
-  uint32_t e_tmem;
-  int e_mode;
-  uint64_t acc_w0;        // &acc[col0 * npad + i0w]   (i0w: global row of warp row 0)
-  uint32_t col_stride32;  // npad * 8
-  uint8_t* dst_w;         // spin words of this lane: sig_dst + i0w / 2 + 4 * (lane & 3)
-  uint8_t* dst_w0;        // sig_dst + i0w / 2
-  uint32_t nib_live;
-  uint32_t jp_hi, jp_lo, hic_hi, loc_hi, rail_lo;
-  uint64_t pol;
-  RtThr thr;
-  uint16_t* tag_row;      // &rt_tags[(col0 / 8) * npad + i]
-  uint16_t* tag_w0;       // &rt_tags[(col0 / 8) * npad + i0w]
-  uint32_t npad;
-  uint32_t nbt;           // shared: delayed FP4 spin tile [NT][64] of this row tile, byte of warp row 0
-  uint32_t wst;           // shared: this warp's staging block (kRtStage bytes)
-  int exp;                // timing ablations: 256 no batches, 512 no accumulator prefetch, 1024 no queue
-};
-
-__device__ __forceinline__ uint32_t ldg_u16_cg(const uint16_t* p) {
-  uint32_t v;
-  asm volatile("ld.global.cg.u16 %0, [%1];" : "=r"(v) : "l"(p));
-  return v;
-}
-
-// One batch of queued undecided updates: entries [head, head + n), n <= 32.
-template <bool BIDIR>
-__device__ __forceinline__ void rt_batch(const RtRow& r, const FastConsts& fc, const I2D& i2d,
-                                         uint32_t colt, uint32_t head, uint32_t n, int lane) {
-  asm volatile("cp.async.wait_all;" ::: "memory");
-  __syncwarp();
-  if (uint32_t(lane) < n) {
-    uint32_t slot = head + uint32_t(lane);
-    slot = slot >= kRtCap ? slot - kRtCap : slot;
-    uint32_t xb0, meta;
-    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(xb0), "=r"(meta) : "r"(r.wst + slot * 8u));
-    const bool rl = (meta & 1u) != 0u, ng = (meta & 2u) != 0u;
-    const uint32_t rw = (meta >> 2) & 31u;   // row lane
-    const uint32_t cj = meta >> 8;           // tile column
-    const uint32_t ce = colt + cj * uint32_t(sizeof(ColTab));
-    const uint64_t cbase = lds_u64(ce);
-    uint32_t coff, nbr;
-    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(coff), "=r"(nbr) : "r"(ce + 8u));
-    // row * golden = (row 0 of the warp) * golden + rw * golden
-    uint32_t g_lo, g_hi;
-    asm("{\n\t.reg .u64 w;\n\tmul.wide.u32 w, %2, 0x7f4a7c15;\n\tmov.b64 {%0, %1}, w;\n\t"
-        "mad.lo.u32 %1, %2, 0x9e3779b9, %1;\n\t"
-        "add.cc.u32 %0, %0, %3;\n\taddc.u32 %1, %1, %4;\n\t}"
-        : "=r"(g_lo), "=r"(g_hi)
-        : "r"(rw), "r"(r.iGb_lo), "r"(r.iGb_hi));
-    // delayed neighbours: nbr holds their byte offsets into the spin tile
-    // (64 bytes per column); rows of a warp start at a multiple of 32
-    const uint32_t nb_r = r.nbt + (rw >> 1);
-    const uint32_t nb_sh = 28u - 4u * (rw & 1u);
-    const uint32_t bu = lds_u8(nb_r + (nbr & 0xffffu));
-    uint32_t bd = 0;
-    if (BIDIR) bd = lds_u8(nb_r + ((nbr >> 16) & 0x7fffu));
-    const uint32_t t5 = noise_top5_v4(cbase, g_lo, g_hi, r.p4, r.p32);
-    const uint32_t xb = xb0 + uint32_t(lds_s8(r.lut + t5));
-    double input = __dsub_rn(__hiloint2double(int(i2d.magic_hi), int(xb)), i2d.magic);
-    input = __dadd_rn(input, __hiloint2double(int(r.jp_hi ^ ((bu << nb_sh) & 0x80000000u)),
-                                              int(r.jp_lo)));
-    if (BIDIR)
-      input = __dadd_rn(input, __hiloint2double(int(r.jp_hi ^ ((bd << nb_sh) & 0x80000000u)),
-                                                int(r.jp_lo)));
-    const double a_old = rl ? __hiloint2double(int(ng ? r.loc_hi : r.hic_hi), int(r.rail_lo))
-                            : lds_f64(r.wst + kRtAcc + slot * 8u);
-    const double sd = __dadd_rn(a_old, input);
-    const bool p_lo = sd < fc.lo_clamp, p_hi = sd >= fc.i0;
-    const bool clamped = p_hi || p_lo;
-    const int nhi = p_hi ? int(r.hic_hi) : (p_lo ? int(r.loc_hi) : __double2hiint(sd));
-    const int nlo = clamped ? int(r.rail_lo) : __double2loint(sd);
-    if (!clamped) {
-      uint64_t addr;
-      asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(addr) : "r"(cj), "r"(r.col_stride32), "l"(r.acc_w0));
-      st_f64_if(reinterpret_cast<double*>(addr + rw * 8u), __hiloint2double(nhi, nlo), true, r.pol);
-    }
-    const uint32_t bits = (clamped ? 1u : 0u) | (nhi < 0 ? 2u : 0u);
-    if (bits) {
-      // tag: u16 [chunk][row]; two rows share the u32 the OR goes to
-      const uint16_t* tw = r.tag_w0 + size_t(cj >> 3) * r.npad + (rw & ~1u);
-      asm volatile("red.global.or.b32 [%0], %1;" ::"l"(tw),
-                   "r"(bits << (2u * (cj & 7u) + 16u * (rw & 1u)))
-                   : "memory");
-    }
-    if (nhi < 0) {
-      // spin: e2m1 -1 = 0xA over the +1 = 0x2 the fast path stored
-      asm volatile("red.global.or.b32 [%0], %1;" ::"l"(r.dst_w0 + (coff >> 1) + (rw >> 3) * 4u),
-                   "r"(8u << (4u * (rw & 7u)))
-                   : "memory");
-    }
-  }
-}
-
-template <bool BIDIR>
-__device__ __forceinline__ void epi_rt(const RtRow& r, const FastConsts& fc, const I2D& i2d,
-                                       const ColTab* c_col, const uint8_t* c_umask,
-                                       long long* q_sum, uint32_t trow, int sub, int nsubs,
-                                       int nchunk, int lane, uint32_t& tag_next) {
-  const int wj = lane >> 2;
-  const uint32_t colt = smem_u32(c_col);
-  const uint32_t lt = (1u << lane) - 1u;
-  uint32_t tcur = tag_next;
-  uint32_t head = 0, qn = 0;  // queue: entries [head, head + qn) mod kRtCap (warp-uniform)
-  for (int ch = sub; ch < nchunk; ch += nsubs) {
-    const int cb = ch * kCW;
-    int32_t v[kCW], e[kCW];
-    tmem_ld8_nw(trow + uint32_t(cb), v);
-    if (r.e_mode >= 2) tmem_ld8_nw(r.e_tmem + uint32_t(cb), e);
-    else
-#pragma unroll
-      for (int j = 0; j < kCW; ++j) e[j] = 0;
-    const uint32_t told = tcur;
-    // tags of this warp's next chunk: same row tile, else the first chunk of
-    // the next row tile (rows + 128; unused past the last tile, the array has slack)
-    {
-      const int chn = ch + nsubs;
-      const uint16_t* tp = chn < nchunk ? r.tag_row + size_t(chn) * r.npad
-                                        : r.tag_row + size_t(sub) * r.npad + kBM;
-      tcur = ldg_u16_cg(tp);
-    }
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-    const uint32_t umask = c_umask[ch];
-    uint32_t tnew = told;
-    const uint32_t meta0 = (uint32_t(cb) << 8) | (uint32_t(lane) << 2);
-#pragma unroll
-    for (int j = 0; j < kCW; ++j) {
-      const int Sb = __float_as_int(__int_as_float(v[j]) + 12582912.0f);
-      const int X = Sb + r.h1d;
-      const int s2 = Sb + r.h2;
-      const uint32_t st2 = (told >> (2 * j)) & 3u;
-      const bool rl = (st2 & 1u) != 0u;
-      const bool ng = (st2 & 2u) != 0u;
-      e[j] += ng ? -s2 : s2;
-      const int thi = st2 == 1u ? r.thr.hh : r.thr.oh;
-      const int tlo = rl ? (ng ? r.thr.ll : r.thr.hl) : r.thr.ol;
-      const bool dhi = X >= thi, dlo = X <= tlo;
-      if ((umask >> j) & 1u) {  // warp-uniform: the column updates this cycle
-        // decided: rail bit, sign of the rail; undecided: 0 until its batch
-        tnew = (tnew & ~(3u << (2 * j))) | (dhi ? (1u << (2 * j)) : 0u) | (dlo ? (3u << (2 * j)) : 0u);
-        const bool und = !(dhi || dlo);
-        const uint32_t bj = __ballot_sync(0xffffffffu, und);
-        if (bj && !(r.exp & 1024)) {  // warp-uniform
-          uint32_t pos = head + qn + uint32_t(__popc(bj & lt));
-          pos = pos >= kRtCap ? pos - kRtCap : pos;
-          const uint32_t sa = r.wst + pos * 8u;
-          uint64_t ga;
-          asm("mad.wide.u32 %0, %1, %2, %3;"
-              : "=l"(ga)
-              : "r"(uint32_t(cb + j)), "r"(r.col_stride32), "l"(r.acc_w0 + uint64_t(lane) * 8u));
-          asm volatile(
-              "{\n\t.reg .pred pu, pa;\n\t"
-              "setp.ne.b32 pu, %0, 0;\n\t"
-              "setp.ne.b32 pa, %1, 0;\n\t"
-              "@pu st.shared.v2.u32 [%2], {%3, %4};\n\t"
-              "@pa cp.async.ca.shared.global [%5], [%6], 8;\n\t}" ::"r"(int(und)),
-              "r"(int(und && !rl && !(r.exp & 512))), "r"(sa), "r"(uint32_t(Sb) + r.h1x),
-              "r"(meta0 + (uint32_t(j) << 8) + st2), "r"(sa + kRtAcc), "l"(ga)
-              : "memory");
-          qn += uint32_t(__popc(bj));
-        }
-      }
-    }
-    if (umask) {
-      asm volatile("st.global.u16 [%0], %1;" ::"l"(r.tag_row + size_t(ch) * r.npad),
-                   "h"(static_cast<unsigned short>(tnew))
-                   : "memory");
-    }
-    {
-      uint32_t ball[kCW];
-#pragma unroll
-      for (int j = 0; j < kCW; ++j) ball[j] = ballot_nz(tnew & (2u << (2 * j)));
-      const uint32_t a0 = (wj & 1) ? ball[1] : ball[0], a1 = (wj & 1) ? ball[3] : ball[2];
-      const uint32_t a2 = (wj & 1) ? ball[5] : ball[4], a3 = (wj & 1) ? ball[7] : ball[6];
-      const uint32_t b0 = (wj & 2) ? a1 : a0, b1 = (wj & 2) ? a3 : a2;
-      const uint32_t mm = (wj & 4) ? b1 : b0;
-      const uint32_t word = nibbles_pm1((mm >> (8 * (lane & 3))) & 0xffu) & r.nib_live;
-      const uint32_t coffw = c_col[cb + wj].off;
-      asm volatile(
-          "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t"
-          "@q st.global.u32 [%0], %1;\n\t}" ::"l"(r.dst_w + (coffw >> 1)),
-          "r"(word), "r"(int(((umask >> wj) & 1u) && r.nib_live))
-          : "memory");
-    }
-    if (r.e_mode == 1 || r.e_mode == 2) tmem_st8(r.e_tmem + uint32_t(cb), e);
-    else reduce8_to_quarter(e, q_sum, cb, lane);
-    // work off the full batches
-    while (qn >= 32u) {
-      if (!(r.exp & 256)) rt_batch<BIDIR>(r, fc, i2d, colt, head, 32u, lane);
-      head += 32u;
-      head = head >= kRtCap ? head - kRtCap : head;
-      qn -= 32u;
-    }
-  }
-  if (qn && !(r.exp & 256)) rt_batch<BIDIR>(r, fc, i2d, colt, head, qn, lane);
-  tag_next = tcur;
-}
-
 // Best-state snapshots during the run copy the packed spin column (npad
 // bytes int8, npad/2 bytes FP4; 16-byte aligned) with vector loads/stores;
 // expand_best_state turns it into the int8 +-1 best_state once at the end.
@@ -1942,8 +1702,6 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
   // (use_tab 2, ct_mode) and the issue-lean FP64 epilogue (use_tab 0, epi_v4).
   const bool nbt_mode = P.fast && !split && !P.i16 && ((P.use_tab == 0 && P.rails_lo) || P.use_tab == 2);
   const bool ct_mode = nbt_mode && P.use_tab == 2;
-  // rail-tag epilogue (epi_rt): no accumulator ring, no sign tiles
-  const bool rt_mode = F4 && nbt_mode && P.rt != 0;
   const uint32_t ct_tile_bytes = uint32_t(NT) * kCtTileRow * (P.bidirectional ? 2u : 1u);
   const bool e_tmem = nbt_mode && 3 * NT <= (F4 ? int(kSfCol) : 512);
 
@@ -1957,7 +1715,7 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
     for (int b = 0; b < 2; ++b) {
       mbar_init(&ctl->tfull[b], 1);
       mbar_init(&ctl->tempty[b], CTA2 ? 2 * EPI : EPI);  // pair: both CTAs' epilogues
-      mbar_init(&ctl->sfull[b], (nbt_mode && !rt_mode) ? 32u : 1u);  // copier warp: every lane arrives
+      mbar_init(&ctl->sfull[b], nbt_mode ? 32u : 1u);  // copier warp: every lane arrives
       mbar_init(&ctl->sempty[b], EPI);
     }
     for (int s = 0; s < nslot; ++s) {
@@ -2257,7 +2015,7 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
           // subgroup's own ring (slots [sub*nps, sub*nps + nps)): each slot is
           // consumed, in order, by a single subgroup, so no consumer can ever
           // wait on a slot barrier two phases ahead (parity aliasing).
-          for (int ch = sb2; ch < nchunk && !(SSQA_ABL & 128) && !rt_mode; ch += nsubs) {
+          for (int ch = sb2; ch < nchunk && !(SSQA_ABL & 128); ch += nsubs) {
             const uint32_t cnt = acc_it * my_chunks + uint32_t(ch / nsubs);
             const int slot = sb2 * nps + int(cnt % uint32_t(nps));
             const uint32_t ph = (cnt / uint32_t(nps)) & 1;
@@ -2285,7 +2043,7 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
     // written a group of its row tiles in pass c, stamp them for the other
     // CTAs of the column tile (their producers load all rows of sigma) =====
     SSQA_CTL_REGS();
-    if (nbt_mode && !rt_mode) {
+    if (nbt_mode) {
       // ===== neighbour-sign tiles of the clamped-table epilogue: for row tile
       // rt, byte [column][row] = 8 where sigma_{k+1}(c-d) of that row is
       // negative (up plane), 16 where sigma_{k-1}(c-d) is (down plane,
@@ -2439,7 +2197,6 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
     constexpr int kSubs = EPI / 4;
     int* ring = ctl->ring[2];
     int ct_pend = -1;    // clamped-table path: ring slot still read by a TMA store
-    uint32_t rt_tag = 0;  // rail-tag path: prefetched tags of the warp's next chunk
     bool drain = false;  // every trial of the tile has stopped: consume only
     for (long c = P.c_first; c <= P.c_last; ++c) {
       if (stop_at(c)) break;
@@ -2511,25 +2268,6 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
       fc.i0 = i0c;
       fc.hi_clamp = (P.run_mode && P.i0_tab) ? __dsub_rn(i0c, P.alpha) : P.hi_clamp;
       fc.lo_clamp = -i0c;
-      RtThr rthr{};
-      if (rt_mode) {
-        // integer bounds of the decided fields (see epi_rt), 1.0 of margin
-        const double m = P.n_rnd + (bidir ? 2.0 : 1.0) * fabs(jperp) + 1.0;
-        const double s2p = ldexp(1.0, P.shift_p);
-        auto at_least = [&](double v) {  // X 2^-p >= v  <=>  X >= ceil(v 2^p)
-          const double x = ceil(v * s2p);
-          return x < 1.0e9 ? int(x) : 0x7fffffff;
-        };
-        auto at_most = [&](double v) {  // X 2^-p <= v  <=>  X <= floor(v 2^p)
-          const double x = floor(v * s2p);
-          return x > -1.0e9 ? int(x) : int(0x80000000u);
-        };
-        rthr.hh = at_least((i0c - fc.hi_clamp) + m);
-        rthr.oh = at_least(2.0 * i0c + m);
-        rthr.ll = at_most(-m);
-        rthr.hl = at_most(-(i0c + fc.hi_clamp) - m);
-        rthr.ol = at_most(-2.0 * i0c - m);
-      }
       TabConsts tc;
       tc.lo1 = P.tab_lo1;
       tc.hi = P.tab_hi;
@@ -2556,18 +2294,12 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
         const uint32_t trow = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(buf * acc_cols);
         const uint8_t* stile = sig_tiles + size_t(buf) * NT * kTileRow;
         if (warp == 0) DBG_STAMP(2, acc_it, 0);
-        // rail-tag epilogue: tags of this warp's first chunk (the later ones
-        // are prefetched chunk by chunk)
-        if (rt_mode && rt == 0)
-          rt_tag = ldg_u16_cg(P.rt_tags + (size_t(col0 / kCW) + size_t(sub)) * g.npad + i);
         mbar_wait(&ctl->sfull[buf], aph);
         mbar_wait(&ctl->tfull[buf], aph);
         tc_fence_after();
         if (warp == 0) DBG_STAMP(3, acc_it, 0);
         const uint32_t cnt0 = acc_it * uint32_t(chunks_of(sub));
-        if (rt_mode && (drain || (P.exp_flags & 1))) {
-          // nothing staged per chunk in rail-tag mode
-        } else if (drain || (P.exp_flags & 1)) {
+        if (drain || (P.exp_flags & 1)) {
           // consume the chunks without the update arithmetic (drain, or the
           // ablation of the update math)
           uint32_t cnt = cnt0;
@@ -2631,50 +2363,7 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
 #define SSQA_EPI_FAST(B, S)                  \
   if (P.use_tab == 1) SSQA_EPI(B, S, true, true); \
   else SSQA_EPI(B, S, true, false)
-          bool rt_done = false;
-          if constexpr (F4) {
-            if (rt_mode) {
-              RtRow rr;
-              const int i0w = (rt_lo + rt) * kBM + q * 32;  // global row of warp row 0
-              const uint64_t iGb = uint64_t(i0w) * kGolden;
-              rr.iGb_lo = uint32_t(iGb);
-              rr.iGb_hi = uint32_t(iGb >> 32);
-              rr.p4 = er.p4;
-              rr.p32 = er.p32;
-              rr.h1x = er.h1x;
-              rr.h1d = row_live ? er.h1 : 0x7fffffff - 0x4B400000;
-              rr.h2 = er.h2;
-              rr.lut = smem_u32(ctl->nz_lut);
-              rr.e_tmem = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(2 * acc_cols);
-              rr.e_mode = (!e_tmem || NRT == 1) ? 0 : (rt == 0 ? 1 : (rt == NRT - 1 ? 3 : 2));
-              rr.acc_w0 = reinterpret_cast<uint64_t>(P.acc + size_t(col0) * g.npad + i0w);
-              rr.col_stride32 = uint32_t(g.npad) * 8u;
-              rr.dst_w = er.dst_w;
-              rr.dst_w0 = sig_dst + i0w / 2;
-              rr.nib_live = er.nib_live;
-              rr.jp_hi = fc.jp_hi;
-              rr.jp_lo = fc.jp_lo;
-              rr.hic_hi = uint32_t(__double2hiint(fc.hi_clamp));
-              rr.loc_hi = uint32_t(__double2hiint(fc.lo_clamp));
-              rr.rail_lo = uint32_t(__double2loint(fc.hi_clamp));  // == loc's (fast_ok)
-              rr.pol = pol_first;
-              rr.thr = rthr;
-              rr.tag_w0 = P.rt_tags + size_t(col0 / kCW) * g.npad + i0w;
-              rr.tag_row = rr.tag_w0 + lane;
-              rr.npad = uint32_t(g.npad);
-              rr.nbt = smem_u32(stile) + uint32_t(q) * 16u;
-              // per-warp staging inside the (unused) accumulator ring
-              rr.wst = smem_u32(acc_ring) + uint32_t(ew) * kRtStage;
-              rr.exp = P.exp_flags;
-              if (bidir) epi_rt<true>(rr, fc, i2d, c_col, ctl->umask, q_sum, trow, sub, kSubs, nchunk,
-                                      lane, rt_tag);
-              else epi_rt<false>(rr, fc, i2d, c_col, ctl->umask, q_sum, trow, sub, kSubs, nchunk,
-                                 lane, rt_tag);
-              rt_done = true;
-            }
-          }
-          if (rt_done) {
-          } else if (ct_mode && SSQA_CT_V4) {
+          if (ct_mode && SSQA_CT_V4) {
             V4Row vr;
             vr.iG_lo = er.iG_lo;
             vr.iG_hi = er.iG_hi;
@@ -3238,20 +2927,6 @@ cudaError_t launch_variant_pair(int grid, int smem, cudaStream_t st, const CUten
   return cudaLaunchKernelEx(&cfg, kern, maps[0], maps[1], maps[2], maps[3], maps[4], P);
 }
 
-// Rail-tag epilogue: tags of a lattice whose accumulators are all current
-// in HBM -- no rail bits, sign bits from the int8 spin slot [ccols][npad].
-__global__ void k_rt_init(const int8_t* __restrict__ sig, uint16_t* __restrict__ tags, int npad,
-                          size_t n16) {
-  const size_t e = blockIdx.x * size_t(blockDim.x) + threadIdx.x;
-  if (e >= n16) return;
-  const size_t cg = e / size_t(npad), i = e % size_t(npad);
-  uint32_t t = 0;
-#pragma unroll
-  for (int j = 0; j < kCW; ++j)
-    if (sig[(cg * kCW + j) * size_t(npad) + i] < 0) t |= 2u << (2 * j);
-  tags[e] = uint16_t(t);
-}
-
 // int8 spin slot -> FP4 (e2m1) slot: +1 -> 0x2, -1 -> 0xA, 0 -> 0x0.
 __global__ void k_pack_fp4(const int8_t* __restrict__ src, uint8_t* __restrict__ dst,
                            size_t nbytes) {
@@ -3294,33 +2969,6 @@ int launch(ssqa_batch_s* b, TcParams& P, bool f4) {
   const bool tab_ok = P.fast && P.tab_w > 0;
   P.use_tab = tab_ok ? ((g.rs > 1 || P.npeer) ? 1 : kDefaultNoSplitEpi) : 0;
   if (tune().tab >= 0) P.use_tab = tab_ok ? std::min(2, tune().tab) : 0;
-  // Rail-tag epilogue (epi_rt): fused FP4 runs from a fresh lattice (every
-  // accumulator in [-i0, i0)), no row split, constant i0, non-negative high
-  // rail (its sign is the spin).  Tune key "rt" 0 turns it off.
-  P.rt = 0;
-  if (f4 && P.run_mode == 1 && P.fast && g.rs == 1 && !P.i16 && P.use_tab == 0 && P.rails_lo &&
-      !P.i0_tab && !P.npeer && !std::signbit(P.hi_clamp) && P.hi_clamp < P.i0 && g.ccols % kCW == 0 &&
-      (P.exp_flags & ~0x700) == 0 && tune().rt > 0) {
-    const size_t bytes = size_t(g.ccols / kCW) * g.npad * 2 + 512;
-    if (b->rt_bytes < bytes) {
-      if (b->d_rt_tags) {
-        cudaStreamSynchronize(b->prob->stream);
-        pool_free(b->d_rt_tags);
-      }
-      b->d_rt_tags = nullptr;
-      b->rt_bytes = 0;
-      if (pmalloc(&b->d_rt_tags, bytes) == cudaSuccess) b->rt_bytes = bytes;
-    }
-    if (b->d_rt_tags) {
-      P.rt = 1;
-      P.rt_tags = static_cast<uint16_t*>(b->d_rt_tags);
-      // tags of the lattice as it stands: nothing on a rail, signs of sigma(cycle)
-      const size_t n16 = size_t(g.ccols / kCW) * g.npad;
-      k_rt_init<<<unsigned((n16 + 255) / 256), 256, 0, b->prob->stream>>>(
-          b->d_sig + size_t(b->cur) * b->slot_elems, P.rt_tags, g.npad, n16);
-      b->launches += 1;
-    }
-  }
   if (P.fast && g.rs == 1 && !P.i16 && (P.use_tab == 2 || (P.use_tab == 0 && P.rails_lo))) {
     // the sign tiles of the copier warp must fit next to the smallest pipeline
     const bool pr = f4 && b->prob->q.fp4x2_ok;
@@ -3414,16 +3062,7 @@ int launch(ssqa_batch_s* b, TcParams& P, bool f4) {
     const int tab_bytes = tab_bytes_of(P);
     L = pick_layout(g.tile_cols, g.tpt, epi / 4, sig_tile_row(P, f4), int(b_row), b_cols, tab_bytes,
                     pair || i16 || g.rs > 1);
-    if (P.rt) {
-      // no accumulator ring: its region holds the epilogue warps' staging
-      // (kRtStage bytes each); the rest goes to operand stages
-      const int nsl = ((epi * int(kRtStage) + kCW * kBM * 8 - 1) / (kCW * kBM * 8) + epi / 4 - 1) / (epi / 4) * (epi / 4);
-      for (int stg = 4; stg >= 2; --stg) {
-        L = make_layout(g.tile_cols, g.tpt, stg, nsl, sig_tile_row(P, f4), int(b_row), b_cols, tab_bytes);
-        if (L.total <= 226u * 1024u) break;
-      }
-    }
-    if (tune().stages > 0 && !P.rt) {  // experiment overrides
+    if (tune().stages > 0) {  // experiment overrides
       L = make_layout(g.tile_cols, g.tpt, tune().stages, std::max(1, tune().nps) * (epi / 4),
                       sig_tile_row(P, f4), int(b_row), b_cols, tab_bytes);
     }
