@@ -117,11 +117,19 @@ class AnnealResult:
     cycles_used: int = 0
     trace_energy: np.ndarray = field(default_factory=lambda: np.zeros(0))
     wall_seconds: float = 0.0
+    # per-cycle jperp of the recorded cycles (SSA: zeros), set with trace_energy
+    trace_jperp: np.ndarray = field(default_factory=lambda: np.zeros(0), repr=False)
 
     @property
     def trace(self) -> List[TracePoint]:
-        """TracePoint list in the reference order (cycle-major, replica-minor)."""
-        raise NotImplementedError("use trace_energy (+ jperp_schedule) for bulk traces")
+        """AnnealResult::trace (annealer.cpp:343): one TracePoint per replica and
+        scanned cycle, cycle-major, replica-minor, with the cycle's jperp."""
+        ncyc = len(self.trace_jperp)
+        if ncyc == 0:
+            return []
+        r = len(self.trace_energy) // ncyc
+        return [TracePoint(c, k, float(self.trace_energy[c * r + k]), float(self.trace_jperp[c]))
+                for c in range(ncyc) for k in range(r)]
 
 
 class IsingModel:
@@ -463,16 +471,24 @@ class Batch:
             pass
 
 
-def _results(res, best, tr, trials) -> List[AnnealResult]:
+def _results(res, best, tr, trials, p=None) -> List[AnnealResult]:
+    """p: the run's parameters; SsqaParams give the trace its jperp column
+    (jperp_schedule of each recorded cycle), SSA traces carry jperp = 0."""
     out = []
+    jp = None
+    if tr is not None:
+        ncyc = tr.shape[1]
+        jp = (np.array([jperp_schedule(c, p) for c in range(ncyc)])
+              if isinstance(p, SsqaParams) else np.zeros(ncyc))
     for t in range(trials):
         r = res[t]
-        te = np.zeros(0)
+        te = tj = np.zeros(0)
         if tr is not None:
             te = tr[t, : r.cycles_used + 1].reshape(-1).copy()
+            tj = jp[: r.cycles_used + 1].copy()
         out.append(AnnealResult(r.best_energy, best[t].copy() if best is not None else None,
                                 r.best_replica, bool(r.reached_target), r.first_hit_cycle,
-                                r.cycles_used, te, r.wall_seconds))
+                                r.cycles_used, te, r.wall_seconds, tj))
     return out
 
 
@@ -488,7 +504,7 @@ def ssqa_run_batch(m: IsingModel, p: SsqaParams, seeds: Sequence[int],
         b.set_seeds(seeds)
         b.launch(target_energy, opts.stop_at_target)
         res, best, tr = b.fetch(True, opts.record_trace)
-        return _results(res, best, tr, len(seeds))
+        return _results(res, best, tr, len(seeds), p)
     finally:
         b.close()
 
@@ -511,7 +527,7 @@ def ssa_run_batch(m: IsingModel, p: SsaParams, seeds: Sequence[int],
         b.set_seeds(seeds)
         b.launch(target_energy, opts.stop_at_target)
         res, best, tr = b.fetch(True, opts.record_trace)
-        return _results(res, best, tr, len(seeds))
+        return _results(res, best, tr, len(seeds), p)
     finally:
         b.close()
 

@@ -130,10 +130,10 @@ class ExchangeRegion:
             self.ptr = C.c_void_p()
 
 
-def _finish(b: Batch, trials: int, opts: RunOptions) -> List[AnnealResult]:
+def _finish(b: Batch, trials: int, opts: RunOptions, p=None) -> List[AnnealResult]:
     b.shard_end()
     res, best, tr = b.fetch(True, opts.record_trace)
-    return _results(res, best, tr, trials)
+    return _results(res, best, tr, trials, p)
 
 
 def capture_run(b: Batch, buf, rank: int, world: int, cycles: int, all_gather, stream,
@@ -191,7 +191,7 @@ def run_row_sharded(m: IsingModel, p: SsqaParams, seeds: Sequence[int],
         b.shard_begin(target, opts.stop_at_target)
         shard_cycles(b, buf, rank, world, p.sc + 1, all_gather)
         if not graph:
-            return _finish(b, len(seeds), opts)
+            return _finish(b, len(seeds), opts, p)
         b.shard_end()
         # graph mode: the same run again, captured and replayed
         g = capture_run(b, buf, rank, world, p.sc + 1, all_gather, stream, target,
@@ -199,7 +199,7 @@ def run_row_sharded(m: IsingModel, p: SsqaParams, seeds: Sequence[int],
         g.replay_on_engine()
         b.synchronize()
         res, best, tr = b.fetch(True, opts.record_trace)
-        return _results(res, best, tr, len(seeds))
+        return _results(res, best, tr, len(seeds), p)
     finally:
         b.close()
         prob.close()
@@ -253,7 +253,7 @@ def _run_p2p(b, p, seeds, target, opts, device, group, world, rank, direct=False
             shard_cycles_direct(b, layout, rank, bases, sig4, p.sc + 1)
         else:
             shard_cycles_p2p(b, layout, rank, bases, p.sc + 1)
-        out = _finish(b, len(seeds), opts)
+        out = _finish(b, len(seeds), opts, p)
         if world > 1:
             dist.barrier(group=group)  # no peer still writes into this region
         return out
@@ -302,7 +302,7 @@ def run_emulated_shards(m: IsingModel, p: SsqaParams, seeds: Sequence[int], nsha
                                                  c + 1)
                         else:
                             b.shard_merge_from(args[g][2], args[g][3], nshards, c + 1)
-                return [_finish(b, len(seeds), opts) for b in shards]
+                return [_finish(b, len(seeds), opts, p) for b in shards]
             finally:
                 for r in regions:
                     r.close()
@@ -312,7 +312,7 @@ def run_emulated_shards(m: IsingModel, p: SsqaParams, seeds: Sequence[int], nsha
                 b.shard_pass(buf[g * nb:].data_ptr())
             for b in shards:
                 b.shard_merge(buf.data_ptr())
-        return [_finish(b, len(seeds), opts) for b in shards]
+        return [_finish(b, len(seeds), opts, p) for b in shards]
     finally:
         for b in shards:
             b.close()

@@ -201,6 +201,16 @@ def test_full_runs_match_oracle_many_trials(orc, engine_epi):
                                        o.first_hit_cycle, o.cycles_used), t
             assert np.array_equal(r.best_state, o.best_state)
             assert np.array_equal(bits(r.trace_energy), bits(o.trace))
+        # AnnealResult::trace (annealer.cpp:343): one TracePoint per replica and
+        # scanned cycle, cycle-major, with the cycle's jperp (annealer.cpp:349)
+        o = orc.ssqa_run(m.h, m.J, m.offset, p, seeds[0], 0.0, True, False)
+        tp = res[0].trace
+        assert len(tp) == (o.cycles_used + 1) * R
+        assert [(x.cycle, x.replica) for x in tp] == [(c, k) for c in range(o.cycles_used + 1)
+                                                      for k in range(R)]
+        assert np.array_equal(bits([x.energy for x in tp]), bits(o.trace))
+        assert np.array_equal(bits([x.jperp for x in tp]),
+                              bits([orc.jperp_schedule(x.cycle, p) for x in tp]))
 
 
 @pytest.fixture(params=["auto", "int8"])

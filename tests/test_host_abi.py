@@ -206,3 +206,26 @@ def test_compute_tts():
     assert v.kind == "finite" and v.seconds == pytest.approx(2.0 * np.log(0.01) / np.log(0.5))
     with pytest.raises(ValueError):
         sq.compute_tts(0.5, 0.0)
+
+
+def test_anneal_result_trace_points():
+    """AnnealResult.trace: TracePoint{cycle, replica, energy, jperp} per replica
+    and scanned cycle in the reference's order (annealer.cpp:343), built from the
+    bulk energy trace and the jperp staircase (annealer.cpp:375-380)."""
+    from paper_2302_12454_b200 import api
+    p = sq.SsqaParams(r=3, sc=250)
+    res = [type("R", (), dict(best_energy=1.0, best_replica=2, reached_target=0,
+                              first_hit_cycle=-1, cycles_used=205, wall_seconds=0.0))()]
+    tr = np.arange(1 * 251 * 3, dtype=np.float64).reshape(1, 251, 3)
+    out = api._results(res, None, tr, 1, p)[0]
+    tp = out.trace
+    assert len(tp) == 206 * 3
+    assert (tp[0].cycle, tp[0].replica, tp[0].energy, tp[0].jperp) == (0, 0, 0.0, 0.0)
+    x = tp[205 * 3 + 2]
+    assert (x.cycle, x.replica, x.energy) == (205, 2, float(205 * 3 + 2))
+    assert x.jperp == sq.jperp_schedule(205, p) == 0.0 + 2 * (0.5 - 0.0) / 3
+    assert tp[100 * 3].jperp == sq.jperp_schedule(100, p)
+    # no trace recorded -> empty list; SSA traces carry jperp = 0
+    assert api._results(res, None, None, 1, p)[0].trace == []
+    s = api._results(res, None, tr[:, :, :1], 1, sq.SsaParams(sc=250))[0].trace
+    assert len(s) == 206 and all(q.jperp == 0.0 and q.replica == 0 for q in s)
