@@ -51,15 +51,6 @@ constexpr int kCW = 8;  // columns per epilogue chunk (one tcgen05.ld .x8)
 #ifndef SSQA_EPI_V
 #define SSQA_EPI_V 1  // FP64 epilogue: 1 issue-lean noise draw (noise_top5 / noise_lut), 0 previous
 #endif
-#ifndef SSQA_CT_V4
-#define SSQA_CT_V4 1  // clamped table in the issue-lean epilogue (STG stores, 2D ring) vs epi_ct
-#endif
-#ifndef SSQA_CT_ICMP
-#define SSQA_CT_ICMP 0  // clamped-table path: clamp with integer compares (1) or DSETP (0)
-#endif
-#ifndef SSQA_CT_LUT
-#define SSQA_CT_LUT 0  // clamped-table path: noise from the byte table (1) or compares (0)
-#endif
 #ifndef SSQA_LAZY_NS_MMA
 #define SSQA_LAZY_NS_MMA 128   // MMA issuer waiting for a free accumulator buffer
 #endif
@@ -308,44 +299,6 @@ __device__ __forceinline__ void tma_load_2d_hint(const CUtensorMap* map, uint64_
 }
 
 // 3D tile load (accumulator chunks: {rows 0..31, columns, 32-row blocks}).
-__device__ __forceinline__ void tma_load_3d_hint(const CUtensorMap* map, uint64_t* bar, void* dst,
-                                                 int x, int y, int z, uint64_t policy) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-      ".L2::cache_hint [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(x), "r"(y), "r"(z),
-      "l"(policy)
-      : "memory");
-}
-
-// 3D tile store shared -> global (bulk group; commit / wait by the caller).
-__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* src, int x, int y,
-                                             int z) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
-          reinterpret_cast<uint64_t>(map)),
-      "r"(smem_u32(src)), "r"(x), "r"(y), "r"(z)
-      : "memory");
-}
-
-// cp.async.bulk.wait_group N for a run-time N (all but the N most recent
-// bulk groups complete).
-__device__ __forceinline__ void bulk_wait_group(int n) {
-  switch (n) {
-    case 0: asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); break;
-    case 1: asm volatile("cp.async.bulk.wait_group 1;" ::: "memory"); break;
-    case 2: asm volatile("cp.async.bulk.wait_group 2;" ::: "memory"); break;
-    case 3: asm volatile("cp.async.bulk.wait_group 3;" ::: "memory"); break;
-    case 4: asm volatile("cp.async.bulk.wait_group 4;" ::: "memory"); break;
-    case 5: asm volatile("cp.async.bulk.wait_group 5;" ::: "memory"); break;
-    case 6: asm volatile("cp.async.bulk.wait_group 6;" ::: "memory"); break;
-    case 7: asm volatile("cp.async.bulk.wait_group 7;" ::: "memory"); break;
-    default: asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); break;
-  }
-}
-
-// L2 prefetch of a tensor tile (no smem, no barrier): pulls the J' rows a few
-// stages ahead of the TMA loads, so those hit L2 when J' streams from HBM.
 __device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* map, int x, int y) {
   asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(
                    reinterpret_cast<uint64_t>(map)),
@@ -805,14 +758,6 @@ struct EpiRow {
   uint32_t p4, p32;         // 4 and 32 in registers (noise_top5)
   uint32_t h1x;             // h1 + noise-free bias + 2^31 (update_fast3)
   const int8_t* nz_lut;     // SmemCtl::nz_lut
-  // clamped-table epilogue (use_tab 2)
-  int h1c;                  // h1 (+ FP4 bias) - (tab_lo1 - 1): table index before the clamp
-  int ct_max;               // tab_w + 1: last table row
-  uint32_t nb_shift;        // neighbour sign bit -> bit 3 (FP4: 4 (i & 1), int8: 4)
-  uint32_t ytab;            // shared address of the table
-  const CUtensorMap* tmAs;  // accumulator store map (box 32 rows x 8 columns)
-  int col0;                 // first global column of the tile
-  int zq;                   // 32-row block index of this warp's rows
 };
 
 // Table epilogue constants for one cycle.  With X = S + H' + noise * NR the
@@ -1157,36 +1102,6 @@ __device__ __forceinline__ void epi_chunks(const EpiRow& er, const UpdateConsts&
   }
 }
 
-// ---- Lean epilogue of the clamped-table path (use_tab 2, no row split) ----
-// Everything per update is one of: the counter RNG (noise_top5), three
-// shared loads (column key, noise byte, neighbour-sign byte), the table
-// lookup of y = fl(X 2^-p + jperp u [+ jperp d]), one FP64 add and the
-// clamp, one shared store of the new accumulator and one ballot.  Per chunk:
-// the TMEM field load, the energy partials (kept in TMEM across the row
-// tiles of a pass when the tile is narrow enough), the spin words and one
-// TMA store of the warp's accumulator block.
-struct CtRow {
-  uint32_t i_u32, p4, p32;  // noise_top5 operands
-  uint32_t iG_lo, iG_hi;    // i * golden (pinned in registers)
-  int nr;                   // n_rnd * 2^p
-  long long i0_bits, hic_bits, loc_bits;  // integer clamp (see TabConsts)
-  unsigned long long lo_bits;
-  int h1c, h2, ct_max;      // clamped table index = clamp(S + h1c + noise, 0, ct_max)
-  uint32_t nbt;             // shared address of row il of neighbour-sign tile column 0
-  uint32_t ytab, lut;       // shared addresses of the table and the noise bytes
-  uint32_t e_tmem;          // TMEM address of this warp's energy partials (column 0)
-  int e_mode;               // 0: reduce every chunk, 1: first row tile (store), 2: middle
-                            // (load, add, store), 3: last (load, add, reduce)
-  uint8_t* dst_w;           // FP4 spin words (see EpiRow::dst_w)
-  uint32_t nib_live;
-  uint64_t cur_i;           // first pass: current spin slot at row i (FP4: byte i/2)
-  uint64_t dst_i;           // int8 spin slot at row i
-  uint32_t nib_shift;
-  bool w_row;
-  const CUtensorMap* tmAs;
-  int col0, zq;
-};
-
 // Neighbour-sign tiles of the clamped-table path: [column][128 rows] bytes,
 // up plane value 8 where sigma_{k+1}(c-d) < 0, then (bidirectional) the down
 // plane with value 16 -- the byte offsets of the table entry.
@@ -1246,166 +1161,6 @@ __device__ __forceinline__ void reduce8_to_quarter(const int (&ep)[kCW], long lo
   red_add_u32_if(reinterpret_cast<uint32_t*>(q_sum) + cb + col, uint32_t(a1), (lane & 3) == 0);
 }
 
-// One row tile of this warp's chunks.  `pend`: ring slot whose TMA store may
-// still be reading it (released one chunk later; -1 none).
-template <bool BIDIR, bool SIGACC, bool F4>
-__device__ __forceinline__ void epi_ct(const CtRow& r, const FastConsts& fc, SmemCtl* ctl,
-                                       double* acc_ring, const ColTab* c_col,
-                                       const uint8_t* c_umask, long long* q_sum, uint32_t trow,
-                                       int sub, int nsubs, int nchunk, int nps, uint32_t cnt0,
-                                       int q, int lane, int& pend) {
-  int sidx = int(cnt0 % uint32_t(nps));
-  uint32_t ph = (cnt0 / uint32_t(nps)) & 1;
-  const int wj = lane >> 2;
-  const uint32_t colt = smem_u32(c_col);
-  for (int ch = sub; ch < nchunk; ch += nsubs) {
-    const int cb = ch * kCW;
-    const int slot = sub * nps + sidx;
-    int32_t v[kCW], e[kCW];
-    tmem_ld8_nw(trow + uint32_t(cb), v);
-    if (r.e_mode >= 2) tmem_ld8_nw(r.e_tmem + uint32_t(cb), e);
-    else
-#pragma unroll
-      for (int j = 0; j < kCW; ++j) e[j] = 0;
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-    mbar_wait(&ctl->afull[slot], ph);
-    if (++sidx == nps) {
-      sidx = 0;
-      ph ^= 1;
-    }
-    double* ab = acc_ring + size_t(slot) * kCW * kBM + q * (kCW * 32) + lane;
-    const uint32_t umask = c_umask[ch];
-    const uint32_t nbq = r.nbt + uint32_t(cb) * uint32_t(BIDIR ? 2 * kCtTileRow : kCtTileRow);
-    uint32_t ball[kCW];
-    // The eight updates of the chunk stage by stage (each stage a loop over
-    // the columns), so the independent chains interleave.
-    int S[kCW];
-#pragma unroll
-    for (int j = 0; j < kCW; ++j) S[j] = F4 ? __float_as_int(__int_as_float(v[j]) + 12582912.0f) : v[j];
-    // counter RNG: raw(spin_counter(c, k, i)) >> 59 (rng.hpp:10-15, 36-38)
-    uint32_t xl[kCW], xh[kCW];
-#pragma unroll
-    for (int j = 0; j < kCW; ++j) {
-      const uint64_t x0 = add64_pair(lds_u64(colt + uint32_t(cb + j) * uint32_t(sizeof(ColTab))),
-                                     r.iG_lo, r.iG_hi);
-      xl[j] = uint32_t(x0);
-      xh[j] = uint32_t(x0 >> 32);
-    }
-#pragma unroll
-    for (int j = 0; j < kCW; ++j) {  // x ^= x >> 30
-      const uint32_t l = xl[j] ^ __funnelshift_r(xl[j], xh[j], 30);
-      xh[j] ^= xh[j] >> 30;
-      xl[j] = l;
-    }
-#pragma unroll
-    for (int j = 0; j < kCW; ++j) {  // x *= 0xbf58476d1ce4e5b9
-      uint32_t l2, h2;
-      asm("{\n\t.reg .u64 w;\n\t"
-          "mul.wide.u32 w, %2, 0x1ce4e5b9;\n\t"
-          "mov.b64 {%0, %1}, w;\n\t"
-          "mad.lo.u32 %1, %2, 0xbf58476d, %1;\n\t"
-          "mad.lo.u32 %1, %3, 0x1ce4e5b9, %1;\n\t}"
-          : "=r"(l2), "=r"(h2)
-          : "r"(xl[j]), "r"(xh[j]));
-      xl[j] = l2;
-      xh[j] = h2;
-    }
-#pragma unroll
-    for (int j = 0; j < kCW; ++j) {  // x ^= x >> 27
-      const uint32_t l = xl[j] ^ __funnelshift_r(xl[j], xh[j], 27);
-      xh[j] ^= xh[j] >> 27;
-      xl[j] = l;
-    }
-    int xi[kCW];
-#pragma unroll
-    for (int j = 0; j < kCW; ++j) {
-      // high word of x * 0x94d049bb133111eb (its top five bits are the draw's)
-      uint32_t top;
-      asm("mad.hi.u32 %0, %1, 0x133111eb, %2;"
-          : "=r"(top)
-          : "r"(xl[j]), "r"(xl[j] * 0x94d049bbu + xh[j] * 0x133111ebu));
-#if SSQA_CT_LUT
-      const int nz = lds_s8(r.lut + (top >> 27));
-#else
-      const int nz = top < 0x70000000u ? 0 : (top < 0xB8000000u ? -r.nr : r.nr);
-#endif
-      xi[j] = min(max(S[j] + r.h1c + nz, 0), r.ct_max);
-    }
-#pragma unroll
-    for (int j = 0; j < kCW; ++j) {
-      const double a_old = ab[j * 32];
-      const int s2 = S[j] + r.h2;
-      if (SIGACC) {
-        e[j] += s2 * ((__double2hiint(a_old) >> 30) | 1);
-      } else {
-        const uint32_t coff = c_col[cb + j].off;
-        int sg;
-        if (F4) {
-          const uint32_t bc = ld_u8(reinterpret_cast<const uint8_t*>(r.cur_i + (coff >> 1)));
-          sg = ((bc >> r.nib_shift) & 8u) ? -1 : 1;
-        } else {
-          sg = ld_s8(reinterpret_cast<const int8_t*>(r.cur_i + coff));
-        }
-        e[j] += sg * s2;
-      }
-      // neighbour signs -> byte offset of the table entry (8: up < 0, 16: down < 0)
-      // sign bytes 0x80 / 0 -> offsets 8 (up) and 16 (down)
-      uint32_t cmbo = lds_u8(nbq + uint32_t(j) * (BIDIR ? 2u * kCtTileRow : uint32_t(kCtTileRow))) >> 4;
-      if (BIDIR) cmbo |= lds_u8(nbq + uint32_t(j) * 2u * kCtTileRow + kCtTileRow) >> 3;
-      const double y = lds_f64(r.ytab + (uint32_t(xi[j]) << (BIDIR ? 5 : 4)) + cmbo);
-      const double sd = __dadd_rn(a_old, y);
-#if SSQA_CT_ICMP
-      // clamp on the bit patterns (ALU instead of the FP64 pipe): i0 > 0 > -i0,
-      // no NaN, never -0.0
-      const long long sb = __double_as_longlong(sd);
-      const long long nb = sb >= r.i0_bits ? r.hic_bits
-                                           : (static_cast<unsigned long long>(sb) > r.lo_bits ? r.loc_bits : sb);
-      const double nv = __longlong_as_double(nb);
-#else
-      const double lo = (sd < fc.lo_clamp) ? fc.lo_clamp : sd;
-      const double nv = (sd >= fc.i0) ? fc.hi_clamp : lo;
-#endif
-      if ((umask >> j) & 1u) ab[j * 32] = nv;
-      if (F4) {
-        ball[j] = __ballot_sync(0xffffffffu, __double2hiint(nv) < 0);
-      } else {
-        const uint32_t coff = c_col[cb + j].off;
-        st_s8_if(reinterpret_cast<int8_t*>(r.dst_i + uint64_t(coff)),
-                 __double2hiint(nv) < 0 ? -1 : 1, ((umask >> j) & 1u) && r.w_row);
-      }
-    }
-    if (F4) {
-      // lane L stores the e2m1 nibbles of rows 8 (L & 3) .. + 7 of column cb + (L >> 2)
-      const uint32_t a0 = (wj & 1) ? ball[1] : ball[0], a1 = (wj & 1) ? ball[3] : ball[2];
-      const uint32_t a2 = (wj & 1) ? ball[5] : ball[4], a3 = (wj & 1) ? ball[7] : ball[6];
-      const uint32_t b0 = (wj & 2) ? a1 : a0, b1 = (wj & 2) ? a3 : a2;
-      const uint32_t mm = (wj & 4) ? b1 : b0;
-      const uint32_t word = nibbles_pm1((mm >> (8 * (lane & 3))) & 0xffu) & r.nib_live;
-      const uint32_t coffw = c_col[cb + wj].off;
-      st_u32_if(reinterpret_cast<uint32_t*>(r.dst_w + (coffw >> 1)), word,
-                ((umask >> wj) & 1u) && r.nib_live);
-    }
-    if (r.e_mode == 1 || r.e_mode == 2) tmem_st8(r.e_tmem + uint32_t(cb), e);
-    else reduce8_to_quarter(e, q_sum, cb, lane);
-    // the warp's [8 columns x 32 rows] block of new accumulators -> HBM
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    __syncwarp();
-    if (lane == 0) {
-      tma_store_3d(r.tmAs, ab, 0, r.col0 + cb, r.zq);
-      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-      if (nps > 1) {
-        // release the previous chunk's slot once its store has read it
-        asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-        if (pend >= 0) mbar_arrive(&ctl->aempty[pend]);
-      } else {
-        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-        mbar_arrive(&ctl->aempty[slot]);
-      }
-    }
-    pend = nps > 1 ? slot : -1;
-  }
-}
-
 // ---- Issue-lean FP64 epilogue (use_tab 0, no row split) ------------------
 // update_fast2's exact arithmetic (magic-number field, the reference's three
 // FP64 adds, the clamp) with the ALU work cut down -- the hot loop is bound by
@@ -1425,7 +1180,8 @@ struct V4Row {
   uint32_t nbt;              // shared address of row il of sign-tile column 0
   uint32_t lut;
   uint32_t e_tmem;
-  int e_mode;                // as CtRow::e_mode
+  int e_mode;                // energy partials in TMEM: 0 reduce every chunk, 1 first row tile
+                             // (store), 2 middle (load, add, store), 3 last (load, add, reduce)
   uint64_t acc_col;          // &acc[col0 * npad + i]
   uint32_t col_stride32;     // npad * 8 bytes
   uint8_t* dst_w;
@@ -1610,7 +1366,7 @@ template <int EPI, bool F4, int CL>
 __global__ void __launch_bounds__(32 * (4 + EPI), 1)
     k_sweep_tc(const __grid_constant__ CUtensorMap tmJ, const __grid_constant__ CUtensorMap tmS,
                const __grid_constant__ CUtensorMap tmSe, const __grid_constant__ CUtensorMap tmA,
-               const __grid_constant__ CUtensorMap tmAs, const TcParams P) {
+               const TcParams P) {
   constexpr bool CTA2 = CL == 1, MC = CL == 2;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-align by offsetting into the shared array itself, so every derived
@@ -2021,12 +1777,8 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
             const uint32_t ph = (cnt / uint32_t(nps)) & 1;
             mbar_wait_lazy(&ctl->aempty[slot], ph ^ 1, SSQA_LAZY_NS_LOAD);
             mbar_expect_tx(&ctl->afull[slot], kCW * kBM * 8);
-            if (ct_mode && !SSQA_CT_V4)  // [row block][column][32 rows]: one dense block per epilogue warp
-              tma_load_3d_hint(&tmA, &ctl->afull[slot], acc_ring + size_t(slot) * kCW * kBM, 0,
-                               col0 + ch * kCW, (rt_lo + rt) * 4, pol_first);
-            else
-              tma_load_2d_hint(&tmA, &ctl->afull[slot], acc_ring + size_t(slot) * kCW * kBM,
-                               (rt_lo + rt) * kBM, col0 + ch * kCW, pol_first);
+            tma_load_2d_hint(&tmA, &ctl->afull[slot], acc_ring + size_t(slot) * kCW * kBM,
+                             (rt_lo + rt) * kBM, col0 + ch * kCW, pol_first);
           }
           if (sb2 == 0) DBG_STAMP(1, acc_it, 1);
         }
@@ -2196,7 +1948,6 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
     const int sub = ew >> 2;
     constexpr int kSubs = EPI / 4;
     int* ring = ctl->ring[2];
-    int ct_pend = -1;    // clamped-table path: ring slot still read by a TMA store
     bool drain = false;  // every trial of the tile has stopped: consume only
     for (long c = P.c_first; c <= P.c_last; ++c) {
       if (stop_at(c)) break;
@@ -2350,20 +2101,13 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
           asm volatile("mov.b32 %0, %1;" : "=r"(er.p32) : "r"(32u));
           er.h1x = uint32_t(er.h1) + 0x80000000u;
           er.nz_lut = ctl->nz_lut;
-          er.h1c = er.h1 - (P.tab_lo1 - 1);
-          er.ct_max = P.tab_w + 1;
-          er.nb_shift = F4 ? er.nib_shift : 4u;
-          er.ytab = smem_u32(ytab);
-          er.tmAs = &tmAs;
-          er.col0 = col0;
-          er.zq = (rt_lo + rt) * 4 + q;
 #define SSQA_EPI(B, S, F, T)                                                               \
   epi_chunks<B, S, F, F4, T>(er, uc, fc, tc, i2d, ctl, acc_ring, c_col, q_sum, trow, \
                              sub, kSubs, nchunk, nps, cnt0, il, lane)
 #define SSQA_EPI_FAST(B, S)                  \
   if (P.use_tab == 1) SSQA_EPI(B, S, true, true); \
   else SSQA_EPI(B, S, true, false)
-          if (ct_mode && SSQA_CT_V4) {
+          if (ct_mode) {
             V4Row vr;
             vr.iG_lo = er.iG_lo;
             vr.iG_hi = er.iG_hi;
@@ -2404,52 +2148,6 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
               else SSQA_V4T(false, false);
             }
 #undef SSQA_V4T
-          } else if (ct_mode) {
-            CtRow cr;
-            cr.i_u32 = er.i_u32;
-            cr.iG_lo = er.iG_lo;
-            cr.iG_hi = er.iG_hi;
-            cr.nr = P.nr;
-            cr.i0_bits = tc.i0_bits;
-            cr.hic_bits = tc.hic_bits;
-            cr.loc_bits = tc.loc_bits;
-            cr.lo_bits = tc.lo_bits;
-            cr.p4 = er.p4;
-            cr.p32 = er.p32;
-            cr.h1c = er.h1 - (P.tab_lo1 - 1);
-            cr.h2 = er.h2;
-            cr.ct_max = P.tab_w + 1;
-            cr.nbt = smem_u32(sig_tiles) + uint32_t(buf) * ct_tile_bytes + uint32_t(il);
-            cr.ytab = smem_u32(ytab);
-            cr.lut = smem_u32(ctl->nz_lut);
-            cr.e_tmem = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(2 * acc_cols);
-            cr.e_mode = (!e_tmem || NRT == 1) ? 0 : (rt == 0 ? 1 : (rt == NRT - 1 ? 3 : 2));
-            cr.dst_w = er.dst_w;
-            cr.nib_live = er.nib_live;
-            cr.cur_i = er.cur_i;
-            cr.dst_i = er.dst_i;
-            cr.nib_shift = er.nib_shift;
-            cr.w_row = row_live;
-            cr.tmAs = &tmAs;
-            cr.col0 = col0;
-            cr.zq = (rt_lo + rt) * 4 + q;
-#define SSQA_CT(B, S)                                                                        \
-  epi_ct<B, S, F4>(cr, fc, ctl, acc_ring, c_col, ctl->umask, q_sum, trow, sub, kSubs, nchunk, \
-                   nps, cnt0, q, lane, ct_pend)
-            if (sig_from_acc) {
-              if (bidir) SSQA_CT(true, true);
-              else SSQA_CT(false, true);
-            } else {
-              if (bidir) SSQA_CT(true, false);
-              else SSQA_CT(false, false);
-            }
-#undef SSQA_CT
-            // the last chunk's slot, once its store has read it
-            if (lane == 0) {
-              asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-              if (ct_pend >= 0) mbar_arrive(&ctl->aempty[ct_pend]);
-            }
-            ct_pend = -1;
           } else if (nbt_mode) {
             V4Row vr;
             vr.iG_lo = er.iG_lo;
@@ -2505,7 +2203,6 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
 #undef SSQA_EPI
         }
         tc_fence_before();
-        const bool ct_now = ct_mode && !SSQA_CT_V4 && !drain && !(P.exp_flags & 1);
         // this warp's spin rows and accumulators of row tile rt are in global
         // memory: make them visible to the TMA (async proxy) reads of pass c+1
         asm volatile("fence.proxy.async.global;" ::: "memory");
@@ -2515,22 +2212,7 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
           if (CTA2 && !leader) mbar_arrive_cluster(mapa_rank(smem_u32(&ctl->tempty[buf]), 0));
           else mbar_arrive(&ctl->tempty[buf]);
           mbar_arrive(&ctl->sempty[buf]);
-          if (ct_now) {
-            // The accumulators of a row tile go out as TMA stores; it is
-            // published ("rows ready") once they are complete -- one row tile
-            // later, so no warp waits on the store it has just issued (the
-            // readers are the next pass's loads, a whole pass away).
-            if (rt == NRT - 1) {
-              asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-              if (rt > 0) mbar_arrive(&ctl->rready[(rt - 1) / rgroup]);
-              mbar_arrive(&ctl->rready[rt / rgroup]);
-            } else if (rt > 0) {
-              bulk_wait_group(chunks_of(sub));  // the previous row tile's stores
-              mbar_arrive(&ctl->rready[(rt - 1) / rgroup]);
-            }
-          } else {
-            mbar_arrive(&ctl->rready[rt / rgroup]);
-          }
+          mbar_arrive(&ctl->rready[rt / rgroup]);
         }
       }
       epi_bar<EPI>();
@@ -2779,24 +2461,6 @@ bool make_map(CUtensorMap* m, void* base, CUtensorMapDataType dt, uint32_t esize
   return r == CUDA_SUCCESS;
 }
 
-// Accumulators f64 [ccols][npad] as a 3D tensor {32 rows, ccols columns,
-// npad/32 row blocks} (strides 8 B, npad*8 B, 256 B): a box {32, 8, nq}
-// lands in shared memory as [row block][column][32 rows], so each epilogue
-// warp's rows of a chunk are one dense 2 KB block (load nq = 4, per-warp
-// store nq = 1).
-bool make_acc_map(CUtensorMap* m, void* base, uint64_t npad, uint64_t ccols, uint32_t nq) {
-  EncodeFn enc = get_encode();
-  if (!enc) return false;
-  cuuint64_t dims[3] = {32, ccols, npad / 32};
-  cuuint64_t strides[2] = {npad * 8, 256};
-  cuuint32_t box[3] = {32, uint32_t(kCW), nq};
-  cuuint32_t estr[3] = {1, 1, 1};
-  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides, box, estr,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  return r == CUDA_SUCCESS;
-}
-
 // Operand stages and per-subgroup state-ring depth inside ~226 KB: prefer
 // deep accumulator rings (up to 3 slots per subgroup, so the loader runs
 // chunks ahead of the HBM latency), then as many operand stages (<= 4) as fit.
@@ -2866,7 +2530,7 @@ cudaError_t launch_variant(int grid, int smem, cudaStream_t st, const CUtensorMa
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
   cfg.numAttrs = coop ? 1 : 0;
-  e = cudaLaunchKernelEx(&cfg, kern, maps[0], maps[1], maps[2], maps[3], maps[4], P);
+  e = cudaLaunchKernelEx(&cfg, kern, maps[0], maps[1], maps[2], maps[3], P);
   if (e == cudaErrorCooperativeLaunchTooLarge) return cudaErrorNotSupported;
   return e;
 }
@@ -2924,7 +2588,7 @@ cudaError_t launch_variant_pair(int grid, int smem, cudaStream_t st, const CUten
   e = cudaOccupancyMaxActiveClusters(&clusters, kern, &cfg);
   if (e != cudaSuccess) return e;
   if (csize * clusters < grid) return cudaErrorNotSupported;
-  return cudaLaunchKernelEx(&cfg, kern, maps[0], maps[1], maps[2], maps[3], maps[4], P);
+  return cudaLaunchKernelEx(&cfg, kern, maps[0], maps[1], maps[2], maps[3], P);
 }
 
 // int8 spin slot -> FP4 (e2m1) slot: +1 -> 0x2, -1 -> 0xA, 0 -> 0x0.
@@ -2979,7 +2643,7 @@ int launch(ssqa_batch_s* b, TcParams& P, bool f4) {
       P.rails_lo = 0;  // plain FP64 epilogue, spin tiles by TMA
     }
   }
-  CUtensorMap maps[5];
+  CUtensorMap maps[4];
   const uint64_t srows = uint64_t(b->nslots) * g.ccols;
   // FP4 rows are npad/2 bytes (two e2m1 values per byte)
   const uint64_t row_bytes = f4 ? uint64_t(g.npad) / 2 : uint64_t(g.npad);
@@ -3001,13 +2665,8 @@ int launch(ssqa_batch_s* b, TcParams& P, bool f4) {
                 g.tile_cols, (pair || i16) ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B) ||
       !make_map(&maps[2], Ssrc, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, row_bytes, srows, tile_row,
                 g.tile_cols, CU_TENSOR_MAP_SWIZZLE_NONE) ||
-      !(P.fast && P.use_tab == 2 && g.rs == 1 && !P.i16 && !SSQA_CT_V4
-            ? make_acc_map(&maps[3], b->d_acc, g.npad, g.ccols, 4) &&
-                  make_acc_map(&maps[4], b->d_acc, g.npad, g.ccols, 1)
-            : make_map(&maps[3], b->d_acc, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, g.npad, g.ccols,
-                       kBM, kCW, CU_TENSOR_MAP_SWIZZLE_NONE) &&
-                  make_map(&maps[4], b->d_acc, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, g.npad,
-                           g.ccols, kBM, kCW, CU_TENSOR_MAP_SWIZZLE_NONE))) {
+      !make_map(&maps[3], b->d_acc, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, g.npad, g.ccols, kBM, kCW,
+                CU_TENSOR_MAP_SWIZZLE_NONE)) {
     g_tc_err = "cuTensorMapEncodeTiled failed";
     return SSQA_ECUDA;
   }

@@ -165,13 +165,15 @@ def test_run_trials_matches_reference_kat(golden, engine):
     assert tts.kind == "finite" and t_mean > 0
 
 
-EPILOGUES = [("simt", "auto"), ("tcgen05", "auto"), ("tcgen05", "table"), ("tcgen05", "fp64")]
+EPILOGUES = [("simt", "auto"), ("tcgen05", "auto"), ("tcgen05", "table"), ("tcgen05", "fp64"),
+             ("tcgen05", "ctable")]
 
 
 @pytest.fixture(params=EPILOGUES, ids=["-".join(e) for e in EPILOGUES])
 def engine_epi(request, monkeypatch):
     """Engine and tcgen05 fast epilogue: the engine's choice, the table path
-    (integer clamps + per-cycle smem table) or the FP64 path (update_fast2)."""
+    (integer clamps + per-cycle smem table), the FP64 path (update_fast2) or the
+    clamped table of the issue-lean epilogue."""
     eng, epi = request.param
     engine = ENGINES[0] if eng == "simt" else ENGINES[1]
     if not engine_ok(engine):
@@ -180,6 +182,8 @@ def engine_epi(request, monkeypatch):
         sq.tune(tab=1)
     elif epi == "fp64":
         sq.tune(tab=0)
+    elif epi == "ctable":  # clamped table inside the issue-lean epilogue (epi_v4 TBL)
+        sq.tune(tab=2)
     return engine
 
 
