@@ -45,6 +45,44 @@ def test_full_size_first_50_steps(n, kind, R, T):
         assert np.array_equal(r.best_state, o.best_state), t
 
 
+DENSE = {"c4": (8192, 0, 32, 256, 2000), "c5": (32768, 1, 16, 64, 1000)}
+
+
+@pytest.mark.parametrize("cfg", ["c4", "c5"])
+def test_dense_full_budget_matches_golden(golden, cfg):
+    """C4 / C5 at their full sweep budgets (2000 / 1000 sweeps, production
+    geometry: wide tiles, row split, CTA pairs, table epilogue): the first and
+    the last trial's whole energy trace, best energy / replica and best state
+    equal the outcomes scripts/make_golden_dense.py computed with
+    oracle/lattice_np.py (tests/golden/dense_full.npz, SHA-256 of the float64
+    trace and int8 state bytes)."""
+    import hashlib
+    cases = golden("dense_full")
+    if cfg not in cases:
+        pytest.skip(f"no {cfg} case in tests/golden/dense_full.npz")
+    g = cases[cfg]
+    n, kind, R, T, sc = DENSE[cfg]
+    assert [int(x) for x in g["k"]] == [n, kind, R, T, sc]
+    prob = sq.Problem.generated_dense(n, kind, 7)  # built on the device, as bench.py does
+    try:
+        seeds = [1000 + t for t in range(T)]
+        res = sq.ssqa_run_batch(sq.api._Shape(n), sq.SsqaParams(r=R, sc=sc), seeds, None,
+                                sq.RunOptions(True, False), problem=prob)
+    finally:
+        prob.close()
+    sha = lambda a: hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+    for j, t in enumerate(int(x) for x in g["trial"]):
+        r = res[t]
+        assert r.cycles_used == int(g["cycles_used"][j]) == sc
+        tr = r.trace_energy.reshape(sc + 1, R)
+        peek = [int(c) for c in g["peek_cycle"]]
+        assert np.array_equal(bits(tr[peek]), bits(g["peek_energy"][j])), (cfg, t)
+        assert sha(r.trace_energy.astype(np.float64)) == str(g["trace_sha"][j]), (cfg, t)
+        assert (r.best_energy, r.best_replica) == (float(g["best_energy"][j]),
+                                                   int(g["best_replica"][j])), (cfg, t)
+        assert sha(r.best_state.astype(np.int8)) == str(g["state_sha"][j]), (cfg, t)
+
+
 # ---- BASELINE configs 2 and 3 at their own shapes (VERDICT r1, Missing 1) ----
 # GI n=20 -> N=400 and n=50 -> N=2500 (fixed instance: gi seed 7, permuted,
 # c1 = c2 = 1), M=20, the full 1024-trial battery on the device with the
