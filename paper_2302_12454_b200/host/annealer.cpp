@@ -4,6 +4,9 @@
 // into the reference's exceptions (annealer.cpp:25-30, 365-373).
 #include "ssqa/annealer.hpp"
 
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -241,6 +244,176 @@ std::vector<AnnealResult> ssqa_run_batch(const IsingModel& m, const SsqaParams& 
 AnnealResult ssqa_run(const IsingModel& m, const SsqaParams& p, uint64_t seed,
                       std::optional<double> target_energy, const RunOptions& opts) {
   return ssqa_run_batch(m, p, {seed}, target_energy, opts).front();
+}
+
+// ---- J' row shards over several GPUs, driven from one host thread ----------
+// (the Python driver is paper_2302_12454_b200/rowshard.py.)
+// NCCL is bound at run time (dlopen of libnccl.so.2): the engine library has
+// no link-time dependency on it and single-GPU callers never load it.
+namespace {
+
+struct Nccl {
+  using Comm = void*;
+  int (*CommInitAll)(Comm*, int, const int*) = nullptr;
+  int (*CommDestroy)(Comm) = nullptr;
+  int (*AllGather)(const void*, void*, size_t, int, Comm, cudaStream_t) = nullptr;
+  int (*GroupStart)() = nullptr;
+  int (*GroupEnd)() = nullptr;
+  const char* (*GetErrorString)(int) = nullptr;
+  static constexpr int kUint8 = 1;  // ncclUint8
+
+  static Nccl& get() {
+    static Nccl n = [] {
+      Nccl x;
+      void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+      if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+      if (!h) throw std::runtime_error(std::string("NCCL not found: ") + dlerror());
+      auto sym = [&](const char* name) {
+        void* p = dlsym(h, name);
+        if (!p) throw std::runtime_error(std::string("NCCL symbol missing: ") + name);
+        return p;
+      };
+      x.CommInitAll = reinterpret_cast<decltype(x.CommInitAll)>(sym("ncclCommInitAll"));
+      x.CommDestroy = reinterpret_cast<decltype(x.CommDestroy)>(sym("ncclCommDestroy"));
+      x.AllGather = reinterpret_cast<decltype(x.AllGather)>(sym("ncclAllGather"));
+      x.GroupStart = reinterpret_cast<decltype(x.GroupStart)>(sym("ncclGroupStart"));
+      x.GroupEnd = reinterpret_cast<decltype(x.GroupEnd)>(sym("ncclGroupEnd"));
+      x.GetErrorString = reinterpret_cast<decltype(x.GetErrorString)>(sym("ncclGetErrorString"));
+      return x;
+    }();
+    return n;
+  }
+  void ok(int rc) const {
+    if (rc != 0) throw std::runtime_error(std::string("NCCL: ") + GetErrorString(rc));
+  }
+};
+
+void cuda_ok(cudaError_t e) {
+  if (e != cudaSuccess) throw std::runtime_error(std::string("CUDA: ") + cudaGetErrorString(e));
+}
+
+}  // namespace
+
+std::vector<AnnealResult> ssqa_run_row_sharded(const IsingModel& m, const SsqaParams& p,
+                                               const std::vector<uint64_t>& seeds,
+                                               const std::vector<int>& devices,
+                                               std::optional<double> target_energy,
+                                               const RunOptions& opts, RowShardExchange exchange) {
+  p.validate(m.n());
+  if (seeds.empty()) return {};
+  if (devices.empty()) throw std::invalid_argument("ssqa_run_row_sharded: no devices");
+  const int G = int(devices.size()), T = int(seeds.size());
+  struct Shard {
+    ProblemHandle ph;
+    BatchHandle bh;
+    void* buf = nullptr;  // two halves (cycle parity) of G chunks in shard order
+    cudaEvent_t packed[2] = {nullptr, nullptr};  // this shard's chunk of that parity is written
+    cudaStream_t stream = nullptr;
+    int device = 0;
+    ~Shard() {
+      cudaSetDevice(device);
+      for (cudaEvent_t e : packed)
+        if (e) cudaEventDestroy(e);
+      if (buf) cudaFree(buf);
+    }
+  };
+  std::vector<Shard> sh(static_cast<size_t>(G));
+  const ssqa_params_c c = to_c(p);
+  size_t nb = 0;
+  for (int g = 0; g < G; ++g) {
+    Shard& s = sh[size_t(g)];
+    s.device = devices[size_t(g)];
+    upload(m, s.device, s.ph);
+    check(ssqa_batch_create(s.ph.p, &c, T, opts.record_trace ? 1 : 0, SSQA_ENGINE_TCGEN05,
+                            &s.bh.b));
+    check(ssqa_batch_set_shard(s.bh.b, g, G));
+    check(ssqa_batch_set_seeds(s.bh.b, seeds.data()));
+    nb = size_t(ssqa_batch_shard_bytes(s.bh.b));
+    s.stream = static_cast<cudaStream_t>(ssqa_batch_stream(s.bh.b));
+    cuda_ok(cudaSetDevice(s.device));
+    cuda_ok(cudaMalloc(&s.buf, 2 * nb * size_t(G)));
+    for (cudaEvent_t& e : s.packed) cuda_ok(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  // NCCL needs distinct devices; a device listed twice (several shards on one
+  // GPU, e.g. to check the sharding on a single-GPU box) takes the copy
+  // exchange below, which is also what `exchange` = kPeerCopy asks for
+  bool distinct = true;
+  for (int g = 0; g < G; ++g)
+    for (int h = 0; h < g; ++h) distinct = distinct && devices[size_t(g)] != devices[size_t(h)];
+  const bool use_nccl = G > 1 && distinct && exchange == RowShardExchange::kNccl;
+  std::vector<Nccl::Comm> comms(static_cast<size_t>(G), nullptr);
+  const Nccl* nccl = nullptr;
+  if (use_nccl) {
+    nccl = &Nccl::get();
+    nccl->ok(nccl->CommInitAll(comms.data(), G, devices.data()));
+  }
+  auto destroy_comms = [&] {
+    if (nccl)
+      for (Nccl::Comm cm : comms)
+        if (cm) nccl->CommDestroy(cm);
+  };
+  try {
+    for (Shard& s : sh)
+      check(ssqa_batch_shard_begin(s.bh.b, target_energy ? 1 : 0, target_energy.value_or(0.0),
+                                   opts.stop_at_target ? 1 : 0));
+    for (long cyc = 0; cyc <= p.sc; ++cyc) {
+      // Chunks alternate between two halves by cycle parity: a GPU rewrites
+      // its chunk of a half two cycles later, after its merge of the cycle
+      // in between, which needed every peer's next chunk -- sent only after
+      // that peer had merged (and so read or received) this one.
+      const int par = int(cyc & 1);
+      auto half = [&](Shard& s) { return static_cast<char*>(s.buf) + size_t(par) * nb * size_t(G); };
+      // pass: each GPU updates its rows and packs them into its own chunk
+      for (int g = 0; g < G; ++g) {
+        Shard& s = sh[size_t(g)];
+        check(ssqa_batch_shard_pass(s.bh.b, half(s) + size_t(g) * nb));
+        if (G > 1 && !use_nccl) {
+          cuda_ok(cudaSetDevice(s.device));
+          cuda_ok(cudaEventRecord(s.packed[par], s.stream));
+        }
+      }
+      if (use_nccl) {
+        // in-place all-gather of the chunks, ordered on each engine stream
+        nccl->ok(nccl->GroupStart());
+        for (int g = 0; g < G; ++g) {
+          Shard& s = sh[size_t(g)];
+          nccl->ok(nccl->AllGather(half(s) + size_t(g) * nb, half(s), nb, Nccl::kUint8,
+                                   comms[size_t(g)], s.stream));
+        }
+        nccl->ok(nccl->GroupEnd());
+      } else if (G > 1) {
+        // copy exchange: every GPU pulls the peers' chunks on its own stream
+        // once they are packed (cudaMemcpyPeerAsync over NVLink)
+        for (int g = 0; g < G; ++g) {
+          Shard& d = sh[size_t(g)];
+          cuda_ok(cudaSetDevice(d.device));
+          for (int h = 0; h < G; ++h) {
+            if (h == g) continue;
+            Shard& src = sh[size_t(h)];
+            cuda_ok(cudaStreamWaitEvent(d.stream, src.packed[par], 0));
+            cuda_ok(cudaMemcpyPeerAsync(half(d) + size_t(h) * nb, d.device,
+                                        half(src) + size_t(h) * nb, src.device, nb, d.stream));
+          }
+        }
+      }
+      for (Shard& s : sh) check(ssqa_batch_shard_merge(s.bh.b, half(s)));
+    }
+    for (Shard& s : sh) check(ssqa_batch_shard_end(s.bh.b));
+  } catch (...) {
+    destroy_comms();
+    throw;
+  }
+  // identical results on every GPU: read shard 0's
+  std::vector<ssqa_result_c> res(seeds.size());
+  std::vector<int8_t> best(size_t(T) * m.n());
+  std::vector<double> trace;
+  if (opts.record_trace) trace.resize(size_t(T) * (p.sc + 1) * p.r);
+  for (size_t g = 1; g < sh.size(); ++g) check(ssqa_batch_synchronize(sh[g].bh.b));
+  check(ssqa_batch_fetch(sh[0].bh.b, res.data(), best.data(),
+                         opts.record_trace ? trace.data() : nullptr));
+  destroy_comms();
+  return to_results(T, m.n(), p.r, p.sc, res, best, trace, opts.record_trace,
+                    [&p](long cy) { return jperp_schedule(cy, p); });
 }
 
 std::vector<AnnealResult> ssqa_run_instances(const std::vector<IsingModel>& models,

@@ -21,4 +21,7 @@ for c in c3 c4 c5; do
   sw=20; [ $c != c3 ] && sw=6
   timeout 300 python scripts/prof_run.py $c tcgen05 $sw > gpurun_out/pre_${TAG}_$c.log 2>&1 && \
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_sweep -s 1 -c 1 -o gpurun_out/prof_${TAG}_$c python scripts/prof_run.py $c tcgen05 $sw > gpurun_out/ncu_${TAG}_$c.log 2>&1; echo "ncu $c rc=$?"
+  # the text summary travels back; the report itself (~20 MB) does not fit gpurun_out's 64 MiB
+  python scripts/ncu_summary.py gpurun_out/prof_${TAG}_$c.ncu-rep gpurun_out/ncu_k_sweep_tc_${c}_$TAG.txt > /dev/null 2>&1
+  rm -f gpurun_out/prof_${TAG}_$c.ncu-rep
 done

@@ -361,6 +361,27 @@ int main() {
   std::printf("FRESH2 %.17g\n", rf2.p_s);
   for (const TrialOutcome& t : rf2.per_trial)
     std::printf("G %d %ld %.17g\n", int(t.reached_target), t.first_hit_cycle, t.best_energy);
+  // J' row shards driven from C++ (ssqa_run_row_sharded): one shard, and two
+  // shards on this GPU (a repeated device takes the copy exchange) against the
+  // unsharded batch -- energies of every cycle, best states, first hits
+  IsingModel m2 = qubo_to_ising(build_gi_qubo(generate_gi(16, 0.5, 5, true, 1.0, 1.0)));
+  SsqaParams p2; p2.r = 6; p2.sc = 80;
+  std::vector<uint64_t> sd = {11, 12, 13};
+  std::vector<AnnealResult> whole = ssqa_run_batch(m2, p2, sd, 0.0, o);
+  int rows_ok = 0;
+  for (const std::vector<int>& devs : {std::vector<int>{0}, std::vector<int>{0, 0}}) {
+    std::vector<AnnealResult> sh = ssqa_run_row_sharded(m2, p2, sd, devs, 0.0, o);
+    bool same = sh.size() == whole.size();
+    for (size_t t = 0; same && t < sh.size(); ++t) {
+      same = sh[t].best_energy == whole[t].best_energy && sh[t].best_replica == whole[t].best_replica &&
+             sh[t].first_hit_cycle == whole[t].first_hit_cycle && sh[t].best_state == whole[t].best_state &&
+             sh[t].trace.size() == whole[t].trace.size();
+      for (size_t k = 0; same && k < sh[t].trace.size(); ++k)
+        same = sh[t].trace[k].energy == whole[t].trace[k].energy;
+    }
+    rows_ok += same ? 1 : 0;
+  }
+  std::printf("ROWS %d\n", rows_ok);
   return 0;
 }
 ''')
@@ -383,6 +404,9 @@ int main() {
     assert float(out[fi + 1]) == float(fresh["p_s"])
     f2 = out.index("FRESH2")
     assert out[f2 + 1] == out[fi + 1]
+    ri = out.index("ROWS")
+    assert out[ri + 1] == "2"  # one shard and two emulated shards equal the unsharded batch
+    out = out[:ri]
     g = out[f2 + 2:]
     assert [x for k, x in enumerate(g) if k % 4] == [x for k, x in enumerate(out[fi + 2:f2]) if k % 4]
     fr = out[fi + 2:]
