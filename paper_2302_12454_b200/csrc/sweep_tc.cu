@@ -60,10 +60,6 @@ constexpr int kCW = 8;  // columns per epilogue chunk (one tcgen05.ld .x8)
 #ifndef SSQA_LAZY_NS_LOAD
 #define SSQA_LAZY_NS_LOAD 128  // state loaders waiting for a free slot / tile buffer
 #endif
-#ifndef SSQA_SKIP_SAME
-#define SSQA_SKIP_SAME 1  // fast epilogues: no store for an accumulator that keeps its value
-                          // (most sit on a clamp rail; C3: 219.5 -> 212 us/sweep)
-#endif
 #ifndef SSQA_ENERGY_RED
 #define SSQA_ENERGY_RED 1  // 1: shuffle transpose-reduce, 0: per-column redux.sync
 #endif
@@ -910,11 +906,9 @@ __device__ __forceinline__ void epi_chunks(const EpiRow& er, const UpdateConsts&
         }
         const uint32_t neg = uint32_t(static_cast<unsigned long long>(res) >> 63);
         const bool w = (cw.y & 0x80000000u) && er.w_row;
-        // an unchanged accumulator (it stays on its rail) needs no store
-        const bool wa = w && !(SSQA_SKIP_SAME && res == __double_as_longlong(ao[j]));
         if (!(SSQA_ABL & 64))
           st_f64_if(reinterpret_cast<double*>(er.acc_i + uint64_t(cw.x) * 8u),
-                    __longlong_as_double(res), wa, er.pol_stream);
+                    __longlong_as_double(res), w, er.pol_stream);
         if (SSQA_ABL & 32) {
         } else if (kWordSt) {
           ball[j] = (SSQA_ABL & 2048) ? neg : ballot_neg(neg);
@@ -972,10 +966,8 @@ __device__ __forceinline__ void epi_chunks(const EpiRow& er, const UpdateConsts&
 #endif
         const uint32_t neg = uint32_t(__double2hiint(nv)) >> 31;
         const bool w = (nb & 0x80000000u) && er.w_row;
-        const bool wa = w && !(SSQA_SKIP_SAME &&
-                               __double_as_longlong(nv) == __double_as_longlong(a_old));
         if (!(SSQA_ABL & 64))
-          st_f64_if(reinterpret_cast<double*>(er.acc_i + uint64_t(coff) * 8u), nv, wa, er.pol_stream);
+          st_f64_if(reinterpret_cast<double*>(er.acc_i + uint64_t(coff) * 8u), nv, w, er.pol_stream);
         if (SSQA_ABL & 32) {
         } else if (kWordSt) {
           ball[j] = (SSQA_ABL & 2048) ? neg : ballot_neg(neg);
@@ -1283,9 +1275,7 @@ __device__ __forceinline__ void epi_v4(const V4Row& r, const FastConsts& fc, con
       asm("mad.wide.u32 %0, %1, %2, %3;"
           : "=l"(addr)
           : "r"(uint32_t(cb + j)), "r"(r.col_stride32), "l"(r.acc_col));
-      // an unchanged accumulator (it stays on its rail) needs no store
-      const bool same = SSQA_SKIP_SAME && nhi == __double2hiint(a_old) && nlo == __double2loint(a_old);
-      st_f64_if(reinterpret_cast<double*>(addr), nv, ((umask >> j) & 1u) && !(r.exp & 64) && !same, r.pol);
+      st_f64_if(reinterpret_cast<double*>(addr), nv, ((umask >> j) & 1u) && !(r.exp & 64), r.pol);
       if (F4) {
         ball[j] = __ballot_sync(0xffffffffu, nhi < 0);
       } else {
