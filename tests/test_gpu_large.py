@@ -137,6 +137,24 @@ def test_gi_full_battery_matches_reference_run_trials(golden, cfg):
         assert p_s == float(ref["p_s"])
 
 
+@pytest.mark.parametrize("T", [512, 256, 128], ids=["g2", "g4", "g8"])
+def test_c3_rank_block_shapes_match_reference(golden, T):
+    """Trial sharding over G = 2 / 4 / 8 GPUs hands each rank a block of 512 /
+    256 / 128 trials of the C3 battery (shard.py; seeds stay base + global
+    index).  Rank 0's block at each of those sizes -- its own geometry: fewer,
+    narrower column tiles, a row split at 128 trials -- at the full budget must
+    give the reference's per-trial outcomes (tests/golden/trials_large.npz,
+    seeds 1000..1047)."""
+    ref = golden("trials_large")["c3_gi50"]
+    m = sq.gi_ising(50, 0.5, 7, True, 1.0, 1.0)
+    outs, _, _, _ = sq.run_trials(m, sq.SsqaParams(r=20), T, 20 * 5000, 1000)
+    k = len(ref["seed"])
+    assert [o.seed for o in outs[:k]] == [int(x) for x in ref["seed"]]
+    assert [int(o.reached_target) for o in outs[:k]] == [int(x) for x in ref["reached"]]
+    assert [o.first_hit_cycle for o in outs[:k]] == [int(x) for x in ref["first_hit"]]
+    assert np.array_equal(bits([o.best_energy for o in outs[:k]]), bits(ref["best_energy"]))
+
+
 @pytest.mark.parametrize("jval", [6.0, 12.0], ids=["fp4", "fp4pair"])
 def test_fp4_large_aligned_fields_exact(jval):
     """FP4 operands accumulate in the tensor core's fp32 TMEM accumulator;
