@@ -143,6 +143,10 @@ int num_sms(int device) {
 // row tiles, widen the tiles (more trials per tile -> each J' row tile is
 // streamed by fewer CTAs, larger MMA N) and split each tile's rows over rs
 // CTAs (row split, one CTA per SM).  fp4: FP4 operands need tile_cols <= 240.
+// CTA pairs pay where the operand feed binds (C4: 64 row tiles, C5: 256);
+// at C3's 20 row tiles they cost ~15 % (scripts/geom_sweep.py).
+constexpr int kPairMinRowTiles = 64;
+
 Geom make_geom(int n, int npad, int R, int T, int sms, int engine, bool fp4, bool per_trial,
                bool i16 = false) {
   Geom g;
@@ -167,13 +171,39 @@ Geom make_geom(int n, int npad, int R, int T, int sms, int engine, bool fp4, boo
     int wide = std::max(1, std::min(T, cap / R));
     if (tune().wide > 0) wide = std::max(1, std::min(wide, tune().wide));
     const int wtiles = (T + wide - 1) / wide;
-    // worth it when the wide tiling still fills the SMs with >= 2 parts per tile
-    if (nrt >= 16 && wide > tpt && wtiles * 2 <= sms) {
+    if (nrt >= 16 && nrt < kPairMinRowTiles && tune().wide <= 0) {
+      // Mid-size problems (C3's N = 2500 with a short battery, e.g. one GPU's
+      // block of a trial-sharded run): epilogue-bound, so pick the (trials per
+      // tile, row parts) that minimise the busiest CTA's sweep -- measured on
+      // C3 blocks of 128 / 256 / 512 trials (scripts/geom_sweep.py), in units
+      // of one epilogue column of one row tile:
+      //   whole tiles   nrt * (cols + 40 k) * 1.05            (FP64 epilogue)
+      //   row split     ceil(nrt / rs) * (cols + 122 k) + 159 (table epilogue,
+      //                 cross-CTA stamps once per pass),  k = npad / 2560
+      const double k = double(npad) / 2560.0;
+      double best = 1e300;
+      int best_tpt = tpt, best_rs = 1;
+      for (int w = 1; w <= std::max(1, std::min(T, cap / R)); ++w) {
+        const int tiles = (T + w - 1) / w;
+        if (tiles > sms) continue;
+        const int te = (T + tiles - 1) / tiles;
+        const int cols = (te * R + 15) / 16 * 16;
+        const double whole = nrt * (cols + 40.0 * k) * 1.05;
+        if (whole < best) best = whole, best_tpt = te, best_rs = 1;
+        for (int r2 = 2; r2 <= std::min(nrt, sms / tiles); ++r2) {
+          const double split = double((nrt + r2 - 1) / r2) * (cols + 122.0 * k) + 159.0;
+          if (split < best) best = split, best_tpt = te, best_rs = r2;
+        }
+      }
+      tpt = best_tpt;
+      rs = best_rs;
+    } else if (nrt >= 16 && wide > tpt && wtiles * 2 <= sms) {
+      // worth it when the wide tiling still fills the SMs with >= 2 parts per tile
       tpt = (T + wtiles - 1) / wtiles;  // as even as the tile count allows
       rs = std::min(nrt, sms / wtiles);
       // an even part count lets the parts run as CTA pairs (M = 256 MMAs);
       // worth one idle SM per tile from 5 parts up
-      if (rs >= 5 && (rs & 1) && nrt % 2 == 0) rs -= 1;
+      if (rs >= 5 && (rs & 1) && nrt % 2 == 0 && nrt >= kPairMinRowTiles) rs -= 1;
     }
     {
       const int want = tune().rs;  // test / tuning override

@@ -2704,7 +2704,11 @@ int launch(ssqa_batch_s* b, TcParams& P, bool f4) {
   // of row tiles; tune key "cta2" 0 turns them off
   bool cta2 = P.run_mode == 1 && g.rs > 1 && g.rs % 2 == 0 && (g.npad / kBM) % 2 == 0 &&
               epi == 16;
+  // ... and from 64 row tiles up: below, the MMAs are not what binds and the
+  // pair's cross-CTA handshakes cost ~15 % (C3 blocks, scripts/geom_sweep.py);
+  // tune key "cta2" 1 pairs whenever the shape allows
   if (tune().cta2 >= 0) cta2 = cta2 && tune().cta2 != 0;
+  else cta2 = cta2 && g.npad / kBM >= 64;
   // J' multicast clusters (all column tiles of a row part), opt-in with
   // tune key "mc": they cut the L2 reads of J' by the tile count but not the
   // bytes each SM takes in, which is what limits the MMAs (C5: 927 us/sweep

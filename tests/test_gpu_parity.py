@@ -597,6 +597,8 @@ def test_row_split_runs_match_oracle(orc, row_split, monkeypatch, rs, operands, 
         sq.tune(mc=1)
     if cluster == "single":
         sq.tune(cta2=0)
+    if cluster == "pairs":  # small shapes pair only on request
+        sq.tune(cta2=1)
     if epi == "fp64":
         sq.tune(tab=0)
     row_split(rs)
