@@ -2071,6 +2071,32 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(&ctl->aempty[slot]);
           }
+        } else if ((rt_lo + rt) * kBM + q * 32 >= g.n) {
+          // every row of this warp is padding (n is not a multiple of 128:
+          // C2's last row tile has 16 live rows): nothing to update or store,
+          // zero energy; hand the staged chunks back and keep the energy
+          // partials in TMEM consistent (first tile: zero; last: reduce)
+          const uint32_t e_tm = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(2 * acc_cols);
+          const int e_mode = (!nbt_mode || !e_tmem || NRT == 1)
+                                 ? 0 : (rt == 0 ? 1 : (rt == NRT - 1 ? 3 : 2));
+          uint32_t cnt = cnt0;
+          for (int ch = sub; ch < nchunk; ch += kSubs, ++cnt) {
+            const int slot = sub * nps + int(cnt % uint32_t(nps));
+            mbar_wait(&ctl->afull[slot], (cnt / uint32_t(nps)) & 1);
+            if (e_mode == 1) {
+              int32_t z[kCW];
+#pragma unroll
+              for (int j = 0; j < kCW; ++j) z[j] = 0;
+              tmem_st8(e_tm + uint32_t(ch * kCW), z);
+            } else if (e_mode == 3) {
+              int32_t e[kCW];
+              tmem_ld8_nw(e_tm + uint32_t(ch * kCW), e);
+              asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+              reduce8_to_quarter(e, q_sum, ch * kCW, lane);
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&ctl->aempty[slot]);
+          }
         } else {
           const int h1 = row_live ? P.H[j_row0 + i] : 0;
           const int h2 = 2 * h1;
