@@ -155,6 +155,35 @@ def test_c3_rank_block_shapes_match_reference(golden, T):
     assert np.array_equal(bits([o.best_energy for o in outs[:k]]), bits(ref["best_energy"]))
 
 
+@pytest.mark.parametrize("n,R,T", [(2048, 20, 1), (2048, 7, 5), (2100, 1, 17), (2560, 20, 40),
+                                   (4000, 12, 9), (2048, 33, 3)])
+def test_mid_size_geometry_search_matches_numpy(n, R, T):
+    """Problems of 16-63 row tiles take the column tiling from make_geom's
+    search (trials per tile x row parts by a cost model): odd batteries --
+    one trial, one replica, widths that do not divide the tile cap, sizes
+    with padding rows -- over 40 sweeps against oracle/lattice_np.py, every
+    trial, every replica's energy of every cycle."""
+    import lattice_np as lnp
+    rng = np.random.default_rng(n + R + T)
+    J = np.zeros((n, n))
+    iu = np.triu_indices(n, 1)
+    J[iu] = rng.integers(-2, 3, len(iu[0])) * 0.5
+    J = J + J.T
+    h = rng.integers(-6, 7, n) * 0.5
+    m = sq.IsingModel.from_arrays(h, J, 0.5)
+    steps = 40
+    p = params(R, steps)
+    seeds = [31 + 7 * t for t in range(T)]
+    res = sq.ssqa_run_batch(m, sq.SsqaParams(r=R, sc=steps), seeds, None,
+                            sq.RunOptions(True, False))
+    ref = lnp.run_lattice(m.h, m.J, m.offset, R, p.delay, p.n_rnd, p.alpha, False, steps,
+                          lnp.jperp_schedule(p), lambda c: p.i0, seeds)
+    for t, (r, o) in enumerate(zip(res, ref)):
+        assert np.array_equal(bits(r.trace_energy), bits(o.trace.reshape(-1))), t
+        assert (r.best_energy, r.best_replica) == (o.best_energy, o.best_replica), t
+        assert np.array_equal(r.best_state, o.best_state), t
+
+
 @pytest.mark.parametrize("jval", [6.0, 12.0], ids=["fp4", "fp4pair"])
 def test_fp4_large_aligned_fields_exact(jval):
     """FP4 operands accumulate in the tensor core's fp32 TMEM accumulator;
