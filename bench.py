@@ -16,6 +16,9 @@ value : replica-spin updates/s = N*M*T*sc / step time, device-timed with CUDA
 e2e   : same metric through the public C-ABI call ssqa_run_batch with HOST
         buffers (quantize + upload of the model, seeds and schedule, the run,
         download of per-trial results and best states) inside the timed region.
+roofline.traffic : DRAM bytes (read + write) of one launch of this workload,
+        measured in the run by one ncu metric pass over a child process
+        (scripts/prof_run.py), outside every timed region; null without ncu.
 --impl reference : the reference's own C++ run_trials (oracle/_ref, built from
         /root/reference by oracle/Makefile) on the host cores, rank 0 only.
 
@@ -613,9 +616,13 @@ def run_ours(args, cfg):
         sweeps_per_launch = sc
         launch_bytes = alg_bytes_per_update * updates_per_sweep * sc
     tensor_tops = ops / (k_ms * 1e-3) / 1e12
-    # DRAM bytes need a profiler: not measured in this run (the ncu captures of
-    # this build are under profiles/, see profiles/README.md)
+    # DRAM bytes of one launch: measured in this run, outside every timed
+    # region, by one ncu metric pass over a separate process that runs this
+    # workload's launch (scripts/prof_run.py); null where ncu is unavailable
     traffic = None
+    traffic_note = "not measured (--no-traffic, N > 1, SIMT engine or no ncu)"
+    if (rank == 0 and world == 1 and b.engine != _lib.ENGINE_SIMT and not args.no_traffic):
+        traffic, traffic_note = measure_traffic(args.config, sc)
     tensor = {"achieved": tensor_tops, "peak": tc_peak, "unit": "TOPS",
               "frac": tensor_tops / tc_peak, "operands": tc_name,
               "frac_vs_burst_peak": tensor_tops / (tc_mult * bf16_burst)}
@@ -633,19 +640,22 @@ def run_ours(args, cfg):
         hbm = {"achieved": achieved, "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak}
         # report the binding roofline (the larger fraction), the other beside it
         if hbm["frac"] >= tensor["frac"]:
-            roofline = {"bound": "hbm", **hbm, "traffic": traffic, "kernel": kname,
-                        "kernel_ms": k_ms, "alg_bytes_per_update": alg_bytes_per_update,
+            roofline = {"bound": "hbm", **hbm, "traffic": traffic, "traffic_note": traffic_note,
+                        "kernel": kname, "kernel_ms": k_ms,
+                        "alg_bytes_per_update": alg_bytes_per_update,
                         "tensor": tensor, "peak_note": peak_note}
         else:
             roofline = {"bound": "tensor", **{k: tensor[k] for k in ("achieved", "peak", "unit",
                                                                       "frac")},
-                        "traffic": traffic, "kernel": kname, "kernel_ms": k_ms,
+                        "traffic": traffic, "traffic_note": traffic_note, "kernel": kname,
+                        "kernel_ms": k_ms,
                         "operands": tc_name, "alg_bytes_per_update": alg_bytes_per_update,
                         "int8_equiv": tensor["int8_equiv"], "hbm": hbm, "peak_note": peak_note}
     else:
         roofline = {"bound": "tensor", **{k: tensor[k] for k in ("achieved", "peak", "unit",
                                                                   "frac")},
-                    "traffic": traffic, "kernel": kname, "kernel_ms": k_ms,
+                    "traffic": traffic, "traffic_note": traffic_note, "kernel": kname,
+                    "kernel_ms": k_ms,
                     "operands": tc_name, "peak_note": peak_note, "int8_equiv": tensor["int8_equiv"]}
 
     # ---- e2e through the public C-ABI call with host buffers ----
@@ -732,6 +742,48 @@ def cfg_name(args):
     return args.config
 
 
+def measure_traffic(config: str, sc: int):
+    """dram__bytes_read.sum + dram__bytes_write.sum of ONE launch of the fused
+    kernel on this config's workload: `ncu --metrics ... --clock-control none`
+    over a child process (scripts/prof_run.py: two launches, the second one
+    captured).  Nothing here is timed or reported as throughput.  Returns
+    (bytes or None, note)."""
+    import csv as _csv
+    import shutil
+    import subprocess
+    import tempfile
+    ncu = shutil.which("ncu") or ("/usr/local/cuda/bin/ncu"
+                                  if os.path.exists("/usr/local/cuda/bin/ncu") else None)
+    script = os.path.join(ROOT, "scripts", "prof_run.py")
+    if not ncu or not os.path.exists(script):
+        return None, "not measured: ncu or scripts/prof_run.py not found"
+    try:
+        with tempfile.TemporaryDirectory() as td:
+            log = os.path.join(td, "t.csv")
+            cmd = [ncu, "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum",
+                   "--clock-control", "none", "-k", "regex:k_sweep", "-s", "1", "-c", "1", "--csv",
+                   "--log-file", log, sys.executable, script, config, "tcgen05", str(sc)]
+            r = subprocess.run(cmd, capture_output=True, text=True, timeout=240)
+            if r.returncode != 0 or not os.path.exists(log):
+                return None, f"not measured: ncu exited {r.returncode}"
+            tot = 0.0
+            seen = 0
+            for row in _csv.reader(open(log)):
+                if len(row) > 3 and row[-3] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+                    v = float(row[-1].replace(",", ""))
+                    unit = row[-2].lower()
+                    scale = {"byte": 1.0, "kbyte": 1e3, "mbyte": 1e6, "gbyte": 1e9, "tbyte": 1e12}
+                    tot += v * scale.get(unit, 1.0)
+                    seen += 1
+            if seen != 2:
+                return None, "not measured: ncu log without the DRAM metrics"
+            return tot, ("dram__bytes_read.sum + dram__bytes_write.sum of one launch (this "
+                         "workload, separate process under ncu --clock-control none, in this run, "
+                         "outside the timed regions)")
+    except Exception as e:  # noqa: BLE001 -- the bench line must not depend on the profiler
+        return None, f"not measured: {type(e).__name__}"
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -744,6 +796,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-full-sc", action="store_true",
                     help="reference arm: skip the 16-trial full-budget run (p_s, TTS99)")
+    ap.add_argument("--no-traffic", action="store_true",
+                    help="skip the ncu metric pass that measures roofline.traffic")
     ap.add_argument("--no-other-configs", action="store_true",
                     help="skip the device-timed C4/C5 lines added to the C3 line")
     ap.add_argument("--shard", default="trials", choices=["trials", "rows"],
