@@ -11,8 +11,7 @@
  *   "tab" 1 table epilogue / 0 FP64 epilogue   "fp4"    0 forces int8 operands
  *   "rs" row parts per column tile             "wide"   trials per wide tile cap
  *   "epi" 12 or 16 epilogue warps              "cta2"   0 disables CTA pairs
- *   "mc" 1 J' multicast clusters               "stages" / "nps" smem ring shape
- *   "exp" ablation bits                        "pf"     J' L2 prefetch distance
+ *   "stages" / "nps" smem ring shape           "exp"    ablation bits
  *   "i16" 0 refuses the int16 two-plane path    "tskip"  timeline: first row tile recorded
  */
 #ifndef SSQA_TUNE_H

@@ -362,11 +362,9 @@ int ssqa_tune_set(const char* key, long value) {
   else if (k == "wide") t.wide = v;
   else if (k == "epi") t.epi = v;
   else if (k == "cta2") t.cta2 = v;
-  else if (k == "mc") t.mc = v;
   else if (k == "stages") t.stages = v;
   else if (k == "nps") t.nps = v;
   else if (k == "exp") t.exp = v;
-  else if (k == "pf") t.pf = v;
   else if (k == "i16") t.i16 = v;
   else if (k == "tskip") t.tskip = v;
   else return set_err(SSQA_EINVAL, "ssqa_tune_set: unknown key '" + k + "'");

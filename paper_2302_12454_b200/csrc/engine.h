@@ -32,11 +32,9 @@ struct TuneOverrides {
   int wide = 0;     // > 0: cap on trials per wide tile
   int epi = 0;      // 12 / 16 epilogue warps (0: default)
   int cta2 = -1;    // 0: no CTA pairs
-  int mc = 0;       // 1: J' multicast clusters
   int stages = 0;   // > 0: operand stages (with nps)
   int nps = 0;      // accumulator-ring slots per subgroup (with stages)
   int exp = 0;      // ablation experiment bits (TcParams::exp_flags)
-  int pf = 0;       // J' L2 prefetch distance
   int i16 = -1;     // 0: refuse the int16 (two-plane int8) coupling path
   std::string trace;  // timeline dump path (block 0)
   int tskip = 0;      // timeline: first row tile recorded

@@ -111,7 +111,6 @@ struct TcParams {
   // fl(fl(X 2^-p + jperp u) [+ jperp d]) from a per-cycle smem table of tab_w
   // entries per neighbour-sign combination
   int tab_lo1, tab_hi, tab_w;
-  int pf_dist;  // J' L2 prefetch distance in K chunks (0: off)
   // Shard passes with the exchange fused in (run_mode 2, npeer > 0; FP4 table
   // epilogue): every spin word also goes to each peer GPU's FP4 slot at the
   // same offset (peer_delta[d] = peer slot base - own slot base, bytes, over
@@ -125,7 +124,6 @@ struct TcParams {
   unsigned* push_ctr;
   int use_tab;  // fast mode: table epilogue (row splits) instead of update_fast2
   int rails_lo; // the clamp rails i0 - alpha and -i0 share their low word (every cycle)
-  int mc_q;     // CL == 2: column tiles per cluster (= ntiles), sharing each J' tile
   long long* dbg;  // optional timeline (block 0): [role][rt_global][2] clock64 stamps
   int dbg_rts;     // capacity in row tiles
   int dbg_skip;    // first row tile recorded (tune key "tskip")
@@ -299,13 +297,6 @@ __device__ __forceinline__ void tma_load_2d_hint(const CUtensorMap* map, uint64_
 }
 
 // 3D tile load (accumulator chunks: {rows 0..31, columns, 32-row blocks}).
-__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* map, int x, int y) {
-  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(
-                   reinterpret_cast<uint64_t>(map)),
-               "r"(x), "r"(y)
-               : "memory");
-}
-
 __device__ __forceinline__ uint64_t policy_evict_first() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
@@ -436,26 +427,6 @@ __device__ __forceinline__ void mma_commit_w(uint64_t* bar) {
 }
 
 // J' tile multicast to the CTAs of `mask` (same smem offset and barrier in each)
-__device__ __forceinline__ void tma_load_2d_mc(const CUtensorMap* map, uint64_t* bar, void* dst,
-                                               int x, int y, uint16_t mask, uint64_t policy) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
-      ".multicast::cluster.L2::cache_hint [%0], [%1, {%4, %5}], [%2], %3, %6;" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "h"(mask), "r"(x), "r"(y),
-      "l"(policy)
-      : "memory");
-}
-
-// Commit arriving on the barrier at the same offset in every CTA of `mask`.
-__device__ __forceinline__ void mma_commit_mc(uint64_t* bar, uint16_t mask) {
-  asm volatile(
-      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
-      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
-      " [%0], %1;\n\t}" ::"r"(smem_u32(bar)),
-      "h"(mask)
-      : "memory");
-}
-
 __device__ __forceinline__ uint32_t cluster_rank() {
   uint32_t r;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
@@ -1360,14 +1331,13 @@ static_assert((16 * EpiRegs<16>::value + 4 * kCtlRegs) * 32 <= 20 * 32 * 96, "EP
 // EPI operand TMA producer, EPI+1 TMEM allocator + MMA issuer, EPI+2 state
 // loader (TMA of accumulator chunks and delayed-spin tiles).
 // CL: cluster mode -- 0 none; 1 CTA pairs (clusters of 2 row parts sharing
-// M = 256 MMAs); 2 J' multicast (clusters of the column tiles of one row part:
-// the leader loads each J' tile once and multicasts it to every CTA).
+// M = 256 MMAs).
 template <int EPI, bool F4, int CL>
 __global__ void __launch_bounds__(32 * (4 + EPI), 1)
     k_sweep_tc(const __grid_constant__ CUtensorMap tmJ, const __grid_constant__ CUtensorMap tmS,
                const __grid_constant__ CUtensorMap tmSe, const __grid_constant__ CUtensorMap tmA,
                const TcParams P) {
-  constexpr bool CTA2 = CL == 1, MC = CL == 2;
+  constexpr bool CTA2 = CL == 1;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-align by offsetting into the shared array itself, so every derived
   // pointer keeps the shared address space (no generic loads)
@@ -1411,9 +1381,8 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
   // a column tile share its columns and own contiguous ranges of row tiles.
   const int RS = g.rs;
   const bool split = RS > 1;
-  // MC: blockIdx = part * ntiles + tile, one cluster per row part
-  const int tile = MC ? int(blockIdx.x) % P.mc_q : int(blockIdx.x) / RS;
-  const int part = MC ? int(blockIdx.x) / P.mc_q : int(blockIdx.x) % RS;
+  const int tile = int(blockIdx.x) / RS;
+  const int part = int(blockIdx.x) % RS;
   const int col0 = tile * NT;
   const int ntl = max(0, min(g.tpt, g.T - tile * g.tpt));
   const int NRT_all = g.npad / kBM;
@@ -1425,9 +1394,8 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
   // the leader is rank 0); pair p owns row tiles [2 u_lo, 2 u_hi), rank 0 the
   // first half and rank 1 the second -- equal counts, as one M = 256 MMA
   // covers a row tile of each.
-  const uint32_t crank = CTA2 ? uint32_t(part & 1) : (MC ? uint32_t(tile) : 0u);
+  const uint32_t crank = CTA2 ? uint32_t(part & 1) : 0u;
   const bool leader = crank == 0;
-  const uint16_t mc_all = uint16_t((1u << (MC ? P.mc_q : 1)) - 1u);
   const int u_lo = int((long long)(rt_span / 2) * (part / 2) / (RS / 2 > 0 ? RS / 2 : 1));
   const int u_hi = int((long long)(rt_span / 2) * (part / 2 + 1) / (RS / 2 > 0 ? RS / 2 : 1));
   const int rt_lo = CTA2 ? rt_base + 2 * u_lo + int(crank) * (u_hi - u_lo)
@@ -1465,8 +1433,7 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < stages; ++s) {
       mbar_init(&ctl->full[s], 1);
-      // MC: the leader reuses a stage once every CTA of the cluster is done with it
-      mbar_init(&ctl->empty[s], (MC && leader) ? uint32_t(P.mc_q) : 1u);
+      mbar_init(&ctl->empty[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&ctl->tfull[b], 1);
@@ -1612,23 +1579,9 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
             }
             const int st = it % stages;
             const uint32_t ph = (it / stages) & 1;
-            if (P.pf_dist > 0) {
-              // J' tile pf_dist chunks ahead (the next row tile's first chunks
-              // near the end of this one)
-              int pk = kc + P.pf_dist, prt = rt;
-              if (pk >= NKC) pk -= NKC, ++prt;
-              if (prt < NRT) tma_prefetch_2d(&tmJ, pk * kBK, j_row0 + (rt_lo + prt) * kBM);
-            }
             mbar_wait_lazy(&ctl->empty[st], ph ^ 1, SSQA_LAZY_NS_PROD);
             if (P.exp_flags & 4) {
               if (!CTA2 || leader) mbar_arrive(&ctl->full[st]);
-            } else if (MC) {
-              // the leader's J' tile lands in every CTA of the cluster
-              mbar_expect_tx(&ctl->full[st], L.a_bytes + L.b_bytes);
-              if (leader)
-                tma_load_2d_mc(&tmJ, &ctl->full[st], sA + size_t(st) * L.a_bytes, kc * kBK,
-                               j_row0 + (rt_lo + rt) * kBM, mc_all, pol_keep);
-              tma_load_2d(&tmS, &ctl->full[st], sB + size_t(st) * L.b_bytes, kc * b_row, yS);
             } else if (CTA2) {
               // both CTAs' tiles complete on the leader's barrier: its own J'
               // rows and half of the spin columns from each CTA
@@ -1710,10 +1663,7 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
                                  (kc | k) ? 1u : 0u);
               }
             }
-            if (MC)  // free the stage here and at the leader, which refills it
-              mma_commit_mc(&ctl->empty[st], uint16_t(leader ? 1u : (1u | (1u << crank))));
-            else
-              mma_commit_w<CTA2>(&ctl->empty[st]);
+            mma_commit_w<CTA2>(&ctl->empty[st]);
           }
           mma_commit_w<CTA2>(&ctl->tfull[buf]);
           DBG_STAMP(0, acc_it, 1);
@@ -1729,7 +1679,6 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
       asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
                    "r"(ncols));
     } else {
-      if (MC) cluster_sync_all();
       asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
                    "r"(ncols));
     }
@@ -2408,14 +2357,13 @@ __global__ void __launch_bounds__(32 * (4 + EPI), 1)
           else
             for (int t = 0; t < ntl; ++t) any |= trials[t].active;
           // nothing left to anneal: the other roles may already be in pass
-          // c+1 -- let it run (drained) and stop everyone after it.  MC: the
-          // cluster shares every J' stage, so its CTAs run all passes (drained)
-          if (!any && c < P.c_last && !MC) ctl->last_pass = c + 1;
+          // c+1 -- let it run (drained) and stop everyone after it
+          if (!any && c < P.c_last) ctl->last_pass = c + 1;
         }
       }
       epi_bar<EPI>();
       if (scan_mode && !drain &&
-          (MC || c + 1 == *reinterpret_cast<volatile long*>(&ctl->last_pass)) &&
+          c + 1 == *reinterpret_cast<volatile long*>(&ctl->last_pass) &&
           c + 1 <= P.c_last) {
         int any = 0;
         if (split) any = !ctl->scan_stop;
@@ -2561,41 +2509,14 @@ cudaError_t launch_variant(int grid, int smem, cudaStream_t st, const CUtensorMa
   return e;
 }
 
-// How many clusters of `csize` CTAs of the cluster variant fit at once.
-template <bool F4, int CL>
-int max_clusters(int smem, int csize) {
-  auto kern = k_sweep_tc<16, F4, CL>;
-  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
-      cudaSuccess)
-    return 0;
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(unsigned(csize));
-  cfg.blockDim = dim3(32 * (4 + 16));
-  cfg.dynamicSmemBytes = size_t(smem);
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = unsigned(csize);
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  int clusters = 0;
-  if (cudaOccupancyMaxActiveClusters(&clusters, kern, &cfg) != cudaSuccess) {
-    cudaGetLastError();
-    return 0;
-  }
-  return clusters;
-}
-
-// Cluster variants: CTA pairs (CL 1, clusters of 2) and J' multicast (CL 2,
-// clusters of mc_q).  Every CTA must be resident at once (the row split
-// synchronises across CTAs), so the launch is refused (cudaErrorNotSupported)
-// unless all grid / csize clusters fit on the device.
+// CTA pairs (CL 1, clusters of 2).  Every CTA must be resident at once (the
+// row split synchronises across CTAs), so the launch is refused
+// (cudaErrorNotSupported) unless all grid / 2 clusters fit on the device.
 template <bool F4, int CL>
 cudaError_t launch_variant_pair(int grid, int smem, cudaStream_t st, const CUtensorMap* maps,
                                 const TcParams& P) {
   auto kern = k_sweep_tc<16, F4, CL>;
-  const int csize = CL == 1 ? 2 : P.mc_q;
+  constexpr int csize = 2;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
@@ -2735,13 +2656,6 @@ int launch(ssqa_batch_s* b, TcParams& P, bool f4) {
   // tune key "cta2" 1 pairs whenever the shape allows
   if (tune().cta2 >= 0) cta2 = cta2 && tune().cta2 != 0;
   else cta2 = cta2 && g.npad / kBM >= 64;
-  // J' multicast clusters (all column tiles of a row part), opt-in with
-  // tune key "mc": they cut the L2 reads of J' by the tile count but not the
-  // bytes each SM takes in, which is what limits the MMAs (C5: 927 us/sweep
-  // against 533 with CTA pairs, whose MMAs read half of B from the peer SM)
-  bool mc = P.run_mode == 1 && g.rs > 1 && g.ntiles >= 2 && g.ntiles <= 8 && epi == 16;
-  mc = mc && tune().mc != 0;
-  if (mc) cta2 = false;
   Layout L;
   auto setup = [&](bool pairs) {
     const int b_cols = pairs ? g.tile_cols / 2 : g.tile_cols;
@@ -2778,29 +2692,7 @@ int launch(ssqa_batch_s* b, TcParams& P, bool f4) {
   // one persistent CTA per (column tile, row part); every CTA must be
   // resident (the row split synchronises across CTAs): grid <= SM count
   int grid = g.ntiles * g.rs;
-  if (mc) {
-    // as many row parts as clusters fit at once (a cluster of ntiles CTAs must
-    // sit inside one GPC)
-    P.mc_q = g.ntiles;
-    const int fit = f4 ? max_clusters<true, 2>(smem, P.mc_q) : max_clusters<false, 2>(smem, P.mc_q);
-    if (fit >= 2) {
-      const int rs0 = P.g.rs;
-      P.g.rs = std::min(P.g.rs, fit);  // g aliases P.g
-      grid = g.ntiles * g.rs;
-      e = f4 ? launch_variant_pair<true, 2>(grid, smem, b->prob->stream, maps, P)
-             : launch_variant_pair<false, 2>(grid, smem, b->prob->stream, maps, P);
-      if (e == cudaErrorNotSupported) {
-        cudaGetLastError();
-        mc = false;
-        P.g.rs = rs0;
-        grid = g.ntiles * g.rs;
-      }
-    } else {
-      mc = false;
-    }
-  }
-  if (mc) {
-  } else if (cta2) {
+  if (cta2) {
     e = f4 ? launch_variant_pair<true, 1>(grid, smem, b->prob->stream, maps, P)
            : launch_variant_pair<false, 1>(grid, smem, b->prob->stream, maps, P);
     if (e == cudaErrorNotSupported) {  // the pairs do not all fit at once: single CTAs
@@ -2810,8 +2702,7 @@ int launch(ssqa_batch_s* b, TcParams& P, bool f4) {
       smem = int(L.total);
     }
   }
-  if (mc || cta2) {
-  } else {
+  if (!cta2) {
     auto single = [&]() {
       return epi == 16 ? (f4 ? launch_variant<16, true>(grid, smem, b->prob->stream, maps, P)
                              : launch_variant<16, false>(grid, smem, b->prob->stream, maps, P))
@@ -2927,8 +2818,6 @@ TcParams base_params(ssqa_batch_s* b) {
   P.fast = fast_ok(b, &P) ? 1 : 0;
   P.i16 = b->prob->q.i16 ? 1 : 0;
   P.exp_flags = tune().exp;
-  P.pf_dist = 0;  // measured: prefetching J' rows costs more L2 bandwidth than it saves (C4, C5)
-  if (tune().pf > 0) P.pf_dist = tune().pf;
   P.ring_cur = b->cur;
   for (int q = 0; q <= b->d; ++q) P.ring_phys[q] = b->phys[size_t(q)];
   P.best_e = b->d_best_e;

@@ -578,7 +578,7 @@ def _row_split_cases():
     out = []
     for rs in (2, 3, 4):
         for ops in ("auto", "int8"):
-            for cl in ("mc", "pairs", "single"):
+            for cl in ("pairs", "single"):
                 if not (rs == 3 and cl == "pairs"):
                     out.append((rs, ops, cl, "auto"))
         if rs % 2 == 0:
@@ -593,8 +593,6 @@ def test_row_split_runs_match_oracle(orc, row_split, monkeypatch, rs, operands, 
         pytest.skip("tcgen05 engine unavailable")
     if operands == "int8":
         sq.tune(fp4=0)
-    if cluster == "mc":
-        sq.tune(mc=1)
     if cluster == "single":
         sq.tune(cta2=0)
     if cluster == "pairs":  # small shapes pair only on request
