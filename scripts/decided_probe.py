@@ -76,10 +76,18 @@ def main():
             up[:n] = und
             ch = up.reshape(npad // 32, 32, (T * r) // 4, 4)  # 32 rows x 4 cols
             c8 = up.reshape(npad // 32, 32, (T * r) // 4, 4).any(axis=(1, 3))
+            # transposed blocking: one row x the 20 replicas of a trial, and one
+            # row x 32 consecutive columns (what a warp would hold if the lanes
+            # were replicas instead of rows)
+            tr20 = und.reshape(n, T, r).any(axis=2).mean()
+            w32 = und[:, : (T * r) // 32 * 32].reshape(n, -1, 32).any(axis=2).mean() \
+                if T * r >= 32 else float("nan")
             print(f"cycle {cycle:5d} jperp {jperp:.3f} undecided {und.mean():.4f} "
                   f"blind-undecided {(~blind).mean():.4f} on-rail {(on_hi | on_lo).mean():.4f} "
                   f"32x4 chunks with any {c8.mean():.3f}  max per 32x4 chunk "
                   f"{ch.sum(axis=(1, 3)).max()}", flush=True)
+            print(f"      row x {r} replicas of a trial with any {tr20:.3f}   row x 32 columns with "
+                  f"any {w32:.3f}", flush=True)
         hcur = hist[cycle % (delay + 1)]
         for t in range(T):
             cols = slice(t * r, (t + 1) * r)
