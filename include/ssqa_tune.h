@@ -13,6 +13,7 @@
  *   "epi" 12 or 16 epilogue warps              "cta2"   0 disables CTA pairs
  *   "stages" / "nps" smem ring shape           "exp"    ablation bits
  *   "i16" 0 refuses the int16 two-plane path    "tskip"  timeline: first row tile recorded
+ *   "nccl1" 1: ssqa_run_row_sharded goes through NCCL even with one device
  */
 #ifndef SSQA_TUNE_H
 #define SSQA_TUNE_H

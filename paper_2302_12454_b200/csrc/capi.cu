@@ -366,6 +366,7 @@ int ssqa_tune_set(const char* key, long value) {
   else if (k == "nps") t.nps = v;
   else if (k == "exp") t.exp = v;
   else if (k == "i16") t.i16 = v;
+  else if (k == "nccl1") t.nccl1 = v;
   else if (k == "tskip") t.tskip = v;
   else return set_err(SSQA_EINVAL, "ssqa_tune_set: unknown key '" + k + "'");
   return SSQA_OK;

@@ -36,6 +36,7 @@ struct TuneOverrides {
   int nps = 0;      // accumulator-ring slots per subgroup (with stages)
   int exp = 0;      // ablation experiment bits (TcParams::exp_flags)
   int i16 = -1;     // 0: refuse the int16 (two-plane int8) coupling path
+  int nccl1 = 0;    // 1: the C++ row-shard driver uses NCCL even for a single device (tests)
   std::string trace;  // timeline dump path (block 0)
   int tskip = 0;      // timeline: first row tile recorded
 };

@@ -12,6 +12,7 @@
 #include <string>
 
 #include "ssqa_cuda.h"
+#include "engine.h"
 
 namespace ssqa {
 
@@ -340,7 +341,8 @@ std::vector<AnnealResult> ssqa_run_row_sharded(const IsingModel& m, const SsqaPa
   bool distinct = true;
   for (int g = 0; g < G; ++g)
     for (int h = 0; h < g; ++h) distinct = distinct && devices[size_t(g)] != devices[size_t(h)];
-  const bool use_nccl = G > 1 && distinct && exchange == RowShardExchange::kNccl;
+  const bool use_nccl = (G > 1 || ssqa_engine::tune().nccl1 > 0) && distinct &&
+                        exchange == RowShardExchange::kNccl;
   std::vector<Nccl::Comm> comms(static_cast<size_t>(G), nullptr);
   const Nccl* nccl = nullptr;
   if (use_nccl) {
