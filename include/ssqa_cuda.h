@@ -155,6 +155,14 @@ int ssqa_problem_int16(ssqa_problem prob);
 int ssqa_quantize_info(int n, const double* h, const double* J, int* n_pad, int* shift_p,
                        int* max_abs_j, int* max_abs_h);
 
+/* Host-only dry run of the column tiling (no device touched): how a batch of
+ * `trials` x `replicas` columns over n spins would be laid out on `sms` SMs
+ * by the tcgen05 engine with 4- or 8-bit operands -- columns per tile, column
+ * tiles, trials per tile and row parts per tile (1: whole tiles; > 1: each
+ * tile's rows split over that many CTAs). */
+int ssqa_plan_geometry(int n, int replicas, int trials, int sms, int operand_bits,
+                       int* tile_cols, int* tiles, int* trials_per_tile, int* row_parts);
+
 /* ---- Validation: SsqaParams::validate (annealer.cpp:365-373) ---------- */
 int ssqa_params_validate(const ssqa_params_c* p, int n);
 /* jperp_schedule (annealer.cpp:375-380); SSQA_EINVAL for cycle < 0. */

@@ -68,6 +68,7 @@ SIGNATURES = [
                                   C.c_double, C.c_void_p, C.c_void_p, C.c_void_p]),
     ("ssqa_problem_info", C.c_int, [VP, IP, IP, IP, IP, IP]),
     ("ssqa_quantize_info", C.c_int, [C.c_int, DP, DP, IP, IP, IP, IP]),
+    ("ssqa_plan_geometry", C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, IP, IP, IP, IP]),
     ("ssqa_problem_fp4", C.c_int, [VP]),
     ("ssqa_problem_int16", C.c_int, [C.c_void_p]),
     ("ssqa_params_validate", C.c_int, [C.POINTER(ParamsC), C.c_int]),

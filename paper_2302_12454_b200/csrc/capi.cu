@@ -842,6 +842,21 @@ int ssqa_quantize_info(int n, const double* h, const double* J, int* n_pad, int*
   return SSQA_OK;
 }
 
+int ssqa_plan_geometry(int n, int replicas, int trials, int sms, int operand_bits,
+                       int* tile_cols, int* tiles, int* trials_per_tile, int* row_parts) {
+  if (n < 1 || n >= kMaxSpins) return set_err(SSQA_EINVAL, "spin count out of range");
+  if (replicas < 1 || trials < 1 || sms < 1) return set_err(SSQA_EINVAL, "bad batch shape");
+  if (operand_bits != 4 && operand_bits != 8) return set_err(SSQA_EINVAL, "operand bits: 4 or 8");
+  const int npad = (n + 127) / 128 * 128;
+  const Geom g = make_geom(n, npad, replicas, trials, sms, SSQA_ENGINE_TCGEN05, operand_bits == 4,
+                           false);
+  if (tile_cols) *tile_cols = g.tile_cols;
+  if (tiles) *tiles = g.ntiles;
+  if (trials_per_tile) *trials_per_tile = g.tpt;
+  if (row_parts) *row_parts = g.rs;
+  return SSQA_OK;
+}
+
 int ssqa_problem_destroy(ssqa_problem pr) {
   if (!pr) return SSQA_OK;
   cudaSetDevice(pr->device);

@@ -229,3 +229,30 @@ def test_anneal_result_trace_points():
     assert api._results(res, None, None, 1, p)[0].trace == []
     s = api._results(res, None, tr[:, :, :1], 1, sq.SsaParams(sc=250))[0].trace
     assert len(s) == 206 and all(q.jperp == 0.0 and q.replica == 0 for q in s)
+
+
+def test_column_tiling_plans():
+    """make_geom through ssqa_plan_geometry (host only): the BASELINE configs'
+    layouts on 148 SMs, and the searched layouts of the C3 rank blocks (512 /
+    256 / 128 trials: whole tiles, then row splits that fill the SMs)."""
+    import ctypes as C
+    L = _lib.lib()
+
+    def plan(n, r, t, bits, sms=148):
+        o = [C.c_int() for _ in range(4)]
+        _lib.check(L.ssqa_plan_geometry(n, r, t, sms, bits, *[C.byref(x) for x in o]), host=True)
+        return tuple(x.value for x in o)  # tile_cols, tiles, trials per tile, row parts
+
+    assert plan(100, 20, 100, 4) == (32, 100, 1, 1)          # C1
+    assert plan(400, 20, 1024, 4) == (144, 147, 7, 1)        # C2
+    assert plan(2500, 20, 1024, 4) == (144, 147, 7, 1)       # C3: whole tiles, 147 of 148 SMs
+    assert plan(8192, 32, 256, 4) == (224, 37, 7, 4)         # C4: 37 x 4 = 148 CTAs (pairs)
+    assert plan(32768, 16, 64, 4) == (208, 5, 13, 28)        # C5: 5 x 28 = 140 CTAs (pairs)
+    cols, tiles, tpt, rs = plan(2500, 20, 512, 4)
+    assert rs == 1 and tpt == 4 and tiles == 128
+    for t in (256, 128, 64):
+        cols, tiles, tpt, rs = plan(2500, 20, t, 4)
+        assert rs > 1 and tiles * rs <= 148 and tiles * tpt >= t and cols <= 240
+        assert tiles * rs >= 120                              # the split fills the SMs
+    with pytest.raises(ValueError):
+        plan(2500, 20, 128, 5)
