@@ -513,6 +513,30 @@ def test_ssa_many_trials_match_oracle(orc, engine):
             assert np.array_equal(bits(r.trace_energy), bits(o.trace))
 
 
+def test_ssa_mid_size_geometry_matches_oracle(orc):
+    """SSA batches (one replica per trial) on a 2048-spin model: make_geom's
+    search packs many trials per column tile and splits the rows over the SMs;
+    traces, hits and best states of a few trials against the C oracle."""
+    n = 2048
+    rng = np.random.default_rng(11)
+    J = np.zeros((n, n))
+    iu = np.triu_indices(n, 1)
+    J[iu] = rng.integers(-1, 2, len(iu[0])) * 0.5
+    J = J + J.T
+    m = sq.IsingModel.from_arrays(rng.integers(-4, 5, n) * 0.5, J, 0.0)
+    for T, sc, kw in [(300, 30, dict(tau=5)), (37, 24, dict(tau=3, beta=0.6, i0_max=60.0))]:
+        p = ssa_params(sc, **kw)
+        seeds = list(range(50, 50 + T))
+        res = sq.ssa_run_batch(m, to_sq_ssa(p), seeds, None, sq.RunOptions(True, False),
+                               engine=_lib.ENGINE_TCGEN05)
+        for t in (0, T // 2, T - 1):
+            o = orc.ssa_run(m.h, m.J, m.offset, p, seeds[t], None, True, False)
+            r = res[t]
+            assert (r.best_energy, r.cycles_used) == (o.best_energy, o.cycles_used), (T, t)
+            assert np.array_equal(r.best_state, o.best_state)
+            assert np.array_equal(bits(r.trace_energy), bits(o.trace))
+
+
 def test_ssa_batch_sweeps_follow_the_ladder(orc, engine):
     """Per-step API on an SSA batch: ssqa_batch_sweep uses i0_schedule(cycle)."""
     m = sq.gi_ising(10, 0.5, 7, True, 1.0, 1.0)
