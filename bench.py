@@ -752,6 +752,11 @@ def measure_traffic(config: str, sc: int):
     import shutil
     import subprocess
     import tempfile
+    # never nest profilers: when this process already runs under one (the
+    # launch-list pass runs bench.py under ncu), injection variables are set
+    if any(k in os.environ for k in ("CUDA_INJECTION64_PATH", "CUDA_INJECTION32_PATH",
+                                     "NV_COMPUTE_PROFILER_PERFWORKS_DIR", "NVTX_INJECTION64_PATH")):
+        return None, "not measured: this run is itself under a profiler"
     ncu = shutil.which("ncu") or ("/usr/local/cuda/bin/ncu"
                                   if os.path.exists("/usr/local/cuda/bin/ncu") else None)
     script = os.path.join(ROOT, "scripts", "prof_run.py")
